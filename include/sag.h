@@ -1,0 +1,219 @@
+/*
+ * sag.h -- C-ABI of the B200-native (sm_100a) solve-phase hot path of the
+ * monolithic SA-AMG / additive-Vanka Stokes solver (arXiv 2306.06795,
+ * reference implementation "stokesamg").
+ *
+ * Every entry point replaces one reference interface; the citation is given
+ * as <reference file>:<line> relative to the reference's proj/core tree.
+ * Setup objects (hierarchy, patterns) still come from the reference's own
+ * host C++ (build_case / build_monolithic_hierarchy); this library takes the
+ * resulting CSR arrays and runs everything from factor_patches down on the GPU.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Every `const double*` / `double*` vector
+ *    argument may be a HOST pointer (pageable or pinned; copied in/out inside
+ *    the call) or a DEVICE pointer of this context's GPU (used in place).
+ *  - Every function returns a status (SAG_OK = 0). The codes map 1:1 onto the
+ *    reference's exception classes (errors.hpp:8-58); sag_last_error() gives
+ *    the message of the calling thread's last failure.
+ *  - Calls on one context are serialised on its CUDA stream; results are
+ *    complete when a call with host output returns, or after sag_synchronize.
+ *  - There is no CPU fallback: without a usable sm_100 device sag_create fails.
+ */
+#ifndef SAG_H
+#define SAG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.hpp:8-58) ------------------------------------ */
+enum sag_status {
+  SAG_OK = 0,
+  SAG_ERROR = 1,               /* stokesamg::Error                         */
+  SAG_DIMENSION_MISMATCH = 2,  /* stokesamg::DimensionMismatch              */
+  SAG_SINGULAR_MATRIX = 3,     /* stokesamg::SingularMatrix                 */
+  SAG_SINGULAR_PATCH = 4,      /* stokesamg::SingularPatch                  */
+  SAG_CONFIG_ERROR = 5,        /* stokesamg::ConfigError                    */
+  SAG_SOLVER_STAGNATION = 6,   /* stokesamg::SolverStagnation               */
+  SAG_CUDA_ERROR = 100,        /* device / driver failure (no reference analogue) */
+  SAG_INVALID_ARGUMENT = 101   /* null handle / pointer                     */
+};
+
+typedef struct sag_ctx sag_ctx;         /* device, stream, workspaces            */
+typedef struct sag_matrix sag_matrix;   /* CSR on device (sparse.hpp:11-28)     */
+typedef struct sag_patches sag_patches; /* Vanka patch sets (vanka.hpp:11-15)   */
+typedef struct sag_vanka sag_vanka;     /* factorization (vanka.hpp:23-40)      */
+typedef struct sag_dc sag_dc;           /* DCPreconditioner (preconditioner.hpp:77-100) */
+
+/* Thread-local message of the last failing call on this thread. */
+const char* sag_last_error(void);
+
+/* ---- context ------------------------------------------------------------ */
+/* Creates a context on CUDA device `device` (fails with SAG_CUDA_ERROR if it
+ * is not an sm_100 part). No reference analogue (the reference is host-only). */
+int sag_create(int device, sag_ctx** out);
+int sag_destroy(sag_ctx* ctx);
+int sag_synchronize(sag_ctx* ctx);
+/* Device buffers for callers that keep vectors resident (bench, pipelines). */
+int sag_alloc(sag_ctx* ctx, size_t bytes, void** dptr);
+int sag_free(sag_ctx* ctx, void* dptr);
+/* cudaMemcpyDefault semantics, ordered on the context stream, synchronous. */
+int sag_memcpy(sag_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* Number of kernels this library launched on ctx since creation. */
+int sag_launch_count(sag_ctx* ctx, long long* out);
+/* CUDA stream of the context (cudaStream_t), for event timing by callers. */
+int sag_stream(sag_ctx* ctx, void** stream);
+
+/* ---- sparse (sparse.hpp:11-28, :42, :64-65) ------------------------------ */
+/* Uploads a canonical CSR matrix (sorted, duplicate-free rows; int32 indices,
+ * fp64 values). Replaces stokesamg::SparseMatrix (sparse.hpp:11-28). */
+int sag_matrix_create(sag_ctx* ctx, int nrows, int ncols, long long nnz, const int* row_offsets,
+                      const int* col_indices, const double* values, sag_matrix** out);
+int sag_matrix_destroy(sag_matrix* m);
+int sag_matrix_shape(const sag_matrix* m, int* nrows, int* ncols, long long* nnz);
+/* y = m x. Replaces spmv (sparse.hpp:42; sparse.cpp:78-91). */
+int sag_spmv(sag_ctx* ctx, const sag_matrix* m, const double* x, double* y);
+/* Replaces norm2 / dot (sparse.hpp:64-65; sparse.cpp:217-227). Deterministic
+ * fixed-order two-stage reductions. */
+int sag_norm2(sag_ctx* ctx, int n, const double* v, double* out);
+int sag_dot(sag_ctx* ctx, int n, const double* a, const double* b, double* out);
+
+/* ---- Vanka (vanka.hpp:11-55) --------------------------------------------- */
+/* Replaces build_patches (vanka.hpp:20-21; vanka.cpp:11-42): one patch per
+ * pressure row, or per consecutive row triple when sv_triples != 0. */
+int sag_build_patches(sag_ctx* ctx, const sag_matrix* k, int n_x, int n_y, int n_p,
+                      int sv_triples, sag_patches** out);
+/* Explicit patch lists (the reference tests build hand-made VankaPatch sets,
+ * tests/test_vanka.cpp:98-113). Arrays are host or device, CSR-like. */
+int sag_patches_create(sag_ctx* ctx, int npatch, const int* pressure_ptr,
+                       const int* pressure_idx, const int* velocity_ptr,
+                       const int* velocity_idx, const int* nx, sag_patches** out);
+int sag_patches_destroy(sag_patches* p);
+/* info = [npatch, total pressure entries, total velocity entries, max nv, max np] */
+int sag_patches_info(const sag_patches* p, long long* info);
+/* Copies the patch lists out (host or device arrays sized from info). */
+int sag_patches_export(sag_ctx* ctx, const sag_patches* p, int* pressure_ptr,
+                       int* pressure_idx, int* velocity_ptr, int* velocity_idx, int* nx);
+
+/* Replaces factor_patches (vanka.hpp:42-43; vanka.cpp:64-149): batched
+ * block-LU on the device. Fails with SAG_SINGULAR_PATCH like the reference. */
+int sag_factor_patches(sag_ctx* ctx, const sag_matrix* k, const sag_patches* p, int n_u,
+                       sag_vanka** out);
+int sag_vanka_destroy(sag_vanka* f);
+/* stats = [a_factor_bytes, aux_bytes, dense_inverse_bytes (vanka.hpp:36-39),
+ *          device bytes of the apply representation, npatch, n, n_slots]      */
+int sag_vanka_stats(const sag_vanka* f, long long* stats);
+/* Factor payload in the reference's layout (vanka.hpp:31-33), concatenated in
+ * patch order: u_hat (nv x np), b_hat (np x nv), s_inv (np x np), row-major;
+ * weights (length n). Any pointer may be NULL. For parity tests. */
+int sag_vanka_export(sag_ctx* ctx, const sag_vanka* f, double* u_hat, double* b_hat,
+                     double* s_inv, double* weights);
+/* delta = sum_i V_i^T W K_i^-1 V_i r. Replaces apply_vanka (vanka.hpp:47;
+ * vanka.cpp:151-184). */
+int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta);
+
+/* Replaces vanka_relax (vanka.hpp:49-55; vanka.cpp:186-209). */
+enum sag_relax_mode { SAG_RELAX_KRYLOV_WRAPPED = 0, SAG_RELAX_STATIONARY = 1 };
+int sag_vanka_relax(sag_ctx* ctx, const sag_matrix* k, const sag_vanka* f, double* x,
+                    const double* b, int mode, int sweeps, double omega);
+
+/* ---- Krylov (krylov.hpp:17-35) ------------------------------------------- */
+typedef struct {
+  double tol;       /* relative to ||b|| (krylov.hpp:18) */
+  int max_iters;
+  int restart;
+  double breakdown; /* happy-breakdown threshold (krylov.hpp:21) */
+} sag_fgmres_options;
+
+typedef struct {
+  int converged;
+  int iterations;
+  double final_relative_residual;
+  int history_len; /* = iterations + 1 (krylov.hpp:26) */
+} sag_krylov_report;
+
+/* Preconditioner selector for sag_fgmres (the reference passes a
+ * LinearOperator, krylov.hpp:12). */
+enum sag_prec_kind {
+  SAG_PREC_IDENTITY = 0, /* identity_operator (krylov.cpp:13-15) */
+  SAG_PREC_VANKA = 1,    /* prec = const sag_vanka*: apply_vanka  */
+  SAG_PREC_JACOBI = 2,   /* prec = const sag_matrix*: z = D^-1 r (amg.cpp:266-269) */
+  SAG_PREC_DC = 3        /* prec = const sag_dc*: DCPreconditioner::apply */
+};
+/* Replaces fgmres(matrix_operator(a), b, x, prec, opt) (krylov.hpp:33-35;
+ * krylov.cpp:17-121). x holds the guess on entry. history may be NULL. */
+int sag_fgmres(sag_ctx* ctx, const sag_matrix* a, const double* b, double* x, int prec_kind,
+               const void* prec, const sag_fgmres_options* opt, sag_krylov_report* rep,
+               double* history, int history_cap);
+
+/* ---- preconditioner (preconditioner.hpp:19-148) --------------------------- */
+enum sag_variant { SAG_DC_ALL = 0, SAG_DC_LO = 1, SAG_DC_HO = 2 };
+
+typedef struct { /* SolverConfig, preconditioner.hpp:19-36 */
+  int variant;
+  double eta_u, eta_p, omega0;
+  int nu1, nu2, gamma, restart;
+  double tol;
+  int max_iters;
+  int enclosed_flow;
+} sag_solver_config;
+
+/* Fills the reference defaults (preconditioner.hpp:20-33). */
+int sag_solver_config_default(sag_solver_config* cfg);
+/* Replaces SolverConfig::check (preconditioner.cpp:30-38). */
+int sag_solver_config_check(const sag_solver_config* cfg);
+
+/* One level of the low-order monolithic hierarchy (amg.hpp:85-90): K and the
+ * prolongator to the next level (NULL on the coarsest). */
+typedef struct {
+  const sag_matrix* k;
+  const sag_matrix* p;
+  int n_x, n_y, n_p;
+} sag_level_desc;
+
+/* Replaces the DCPreconditioner constructor (preconditioner.cpp:90-105) and
+ * MonolithicSolver's (preconditioner.cpp:40-55): Vanka factors for K0 and every
+ * non-coarsest level, R = P^T, coarse dense LU (with the enclosed-flow pin
+ * 1e-12 * norm_inf(K of level 0), preconditioner.cpp:49-53), all on device.
+ * TH injection transfer (transfer.cpp:97-125) when sv == 0. For sv != 0 the
+ * fine patches are element triples with stationary relaxation, and the
+ * transfer needs sag_dc_set_sv_transfer before the first apply. */
+int sag_dc_create(sag_ctx* ctx, const sag_matrix* k0, int n_x0, int n_y0, int n_p0, int sv,
+                  int nlevels, const sag_level_desc* levels, const sag_solver_config* cfg,
+                  sag_dc** out);
+int sag_dc_destroy(sag_dc* d);
+/* set_parameters (preconditioner.hpp:87) */
+int sag_dc_set_parameters(sag_dc* d, double eta_u, double eta_p, double omega0);
+/* SV transfer (transfer.cpp:18-53, :82-95): duplication map P^p (n_p0 x n_p1),
+ * M_mix (n_p1 x n_p0), Mcg (n_p1 x n_p1) and its scalar SA hierarchy
+ * (amg.hpp:68-76): nsl matrices, nsl-1 prolongators. Mass projection solved by
+ * device FGMRES(20) to 1e-12 with one scalar V(2,2) cycle as preconditioner. */
+int sag_dc_set_sv_transfer(sag_dc* d, const sag_matrix* p_dup, const sag_matrix* m_mix,
+                           int nsl, const sag_matrix* const* scalar_levels,
+                           const sag_matrix* const* scalar_prolongators);
+/* Replaces DCPreconditioner::apply (preconditioner.cpp:114-153). */
+int sag_dc_apply(sag_ctx* ctx, sag_dc* d, const double* r, double* z);
+/* Replaces MonolithicSolver::vcycle (preconditioner.cpp:83-88) on the
+ * low-order hierarchy, skip_finest_relax = 0. */
+int sag_dc_vcycle(sag_ctx* ctx, sag_dc* d, const double* b, double* x, int nu1, int nu2);
+/* counters = [fine_relax_units, level1_relax_units] (preconditioner.hpp:46-48) */
+int sag_dc_counters(const sag_dc* d, long long* counters);
+/* levels info: out = [nlevels, n0, n_levels rows..]; bytes of device factors */
+int sag_dc_info(const sag_dc* d, long long* out, int cap);
+
+/* Replaces solve_stokes (preconditioner.hpp:147-148; preconditioner.cpp:229-259):
+ * outer FGMRES on K0 with the DC preconditioner and the enclosed-flow pressure
+ * projection. Solver settings are read from cfg (restart, tol, max_iters,
+ * enclosed_flow). x is overwritten (zero initial guess). */
+int sag_solve_stokes(sag_ctx* ctx, sag_dc* d, const double* rhs, double* x,
+                     const sag_solver_config* cfg, sag_krylov_report* rep, double* history,
+                     int history_cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAG_H */

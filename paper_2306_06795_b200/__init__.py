@@ -1,0 +1,621 @@
+"""B200-native solve phase of the monolithic SA-AMG / additive-Vanka Stokes
+solver (arXiv 2306.06795; reference implementation ``stokesamg``).
+
+Python mirror of the reference's C++ solver API for the hot path, on top of
+the C-ABI in ``include/sag.h`` (``libsag.so``, hand-written sm_100a kernels).
+Names, argument meaning and error classes follow the reference:
+
+===============================  ==============================================
+reference (proj/core)            here
+===============================  ==============================================
+SparseMatrix (sparse.hpp:11-28)  :class:`SparseMatrix` (device CSR)
+spmv (sparse.hpp:42)             :func:`spmv`
+norm2 / dot (sparse.hpp:64-65)   :func:`norm2`, :func:`dot`
+build_patches (vanka.hpp:20-21)  :func:`build_patches`
+factor_patches (vanka.hpp:42)    :func:`factor_patches`
+apply_vanka (vanka.hpp:47)       :func:`apply_vanka`
+vanka_relax (vanka.hpp:53-55)    :func:`vanka_relax`
+fgmres (krylov.hpp:33-35)        :func:`fgmres`
+SolverConfig (precond.hpp:19)    :class:`SolverConfig`
+DCPreconditioner (:77-100)       :class:`DCPreconditioner`
+solve_stokes (:147-148)          :func:`solve_stokes`
+errors.hpp:8-58                  :class:`Error` and subclasses
+===============================  ==============================================
+
+There is no CPU fallback: importing works anywhere, but every operation needs
+``libsag.so`` and an sm_100 GPU and raises otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsag.so")
+
+__all__ = [
+    "Error", "DimensionMismatch", "SingularMatrix", "SingularPatch", "ConfigError",
+    "SolverStagnation", "CudaError", "Context", "SparseMatrix", "Patches",
+    "VankaFactorization", "spmv", "norm2", "dot", "build_patches", "factor_patches",
+    "apply_vanka", "vanka_relax", "RelaxMode", "FgmresOptions", "KrylovReport", "fgmres",
+    "SolverConfig", "Variant", "DCPreconditioner", "solve_stokes", "default_context", "lib",
+]
+
+
+# ----------------------------------------------------------------- errors --
+class Error(RuntimeError):
+    """stokesamg::Error (errors.hpp:8-10)."""
+
+
+class DimensionMismatch(Error):
+    pass
+
+
+class SingularMatrix(Error):
+    pass
+
+
+class SingularPatch(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class SolverStagnation(Error):
+    pass
+
+
+class CudaError(Error):
+    """Device/driver failure (no reference analogue)."""
+
+
+_ERRORS = {1: Error, 2: DimensionMismatch, 3: SingularMatrix, 4: SingularPatch,
+           5: ConfigError, 6: SolverStagnation, 100: CudaError, 101: Error}
+
+i32p = C.POINTER(C.c_int)
+f64p = C.POINTER(C.c_double)
+i64p = C.POINTER(C.c_longlong)
+vp = C.c_void_p
+
+
+class sag_fgmres_options(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iters", C.c_int), ("restart", C.c_int),
+                ("breakdown", C.c_double)]
+
+
+class sag_krylov_report(C.Structure):
+    _fields_ = [("converged", C.c_int), ("iterations", C.c_int),
+                ("final_relative_residual", C.c_double), ("history_len", C.c_int)]
+
+
+class sag_solver_config(C.Structure):
+    _fields_ = [("variant", C.c_int), ("eta_u", C.c_double), ("eta_p", C.c_double),
+                ("omega0", C.c_double), ("nu1", C.c_int), ("nu2", C.c_int), ("gamma", C.c_int),
+                ("restart", C.c_int), ("tol", C.c_double), ("max_iters", C.c_int),
+                ("enclosed_flow", C.c_int)]
+
+
+class sag_level_desc(C.Structure):
+    _fields_ = [("k", vp), ("p", vp), ("n_x", C.c_int), ("n_y", C.c_int), ("n_p", C.c_int)]
+
+
+#: every entry point declared in include/sag.h, with its ctypes signature
+SIGNATURES = {
+    "sag_last_error": (C.c_char_p, []),
+    "sag_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "sag_destroy": (C.c_int, [vp]),
+    "sag_synchronize": (C.c_int, [vp]),
+    "sag_alloc": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
+    "sag_free": (C.c_int, [vp, vp]),
+    "sag_memcpy": (C.c_int, [vp, vp, vp, C.c_size_t]),
+    "sag_launch_count": (C.c_int, [vp, i64p]),
+    "sag_stream": (C.c_int, [vp, C.POINTER(vp)]),
+    "sag_matrix_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_longlong, vp, vp, vp, C.POINTER(vp)]),
+    "sag_matrix_destroy": (C.c_int, [vp]),
+    "sag_matrix_shape": (C.c_int, [vp, i32p, i32p, i64p]),
+    "sag_spmv": (C.c_int, [vp, vp, vp, vp]),
+    "sag_norm2": (C.c_int, [vp, C.c_int, vp, f64p]),
+    "sag_dot": (C.c_int, [vp, C.c_int, vp, vp, f64p]),
+    "sag_build_patches": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "sag_patches_create": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, C.POINTER(vp)]),
+    "sag_patches_destroy": (C.c_int, [vp]),
+    "sag_patches_info": (C.c_int, [vp, i64p]),
+    "sag_patches_export": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+    "sag_factor_patches": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(vp)]),
+    "sag_vanka_destroy": (C.c_int, [vp]),
+    "sag_vanka_stats": (C.c_int, [vp, i64p]),
+    "sag_vanka_export": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    "sag_apply_vanka": (C.c_int, [vp, vp, vp, vp]),
+    "sag_vanka_relax": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_double]),
+    "sag_fgmres": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, C.POINTER(sag_fgmres_options),
+                             C.POINTER(sag_krylov_report), vp, C.c_int]),
+    "sag_solver_config_default": (C.c_int, [C.POINTER(sag_solver_config)]),
+    "sag_solver_config_check": (C.c_int, [C.POINTER(sag_solver_config)]),
+    "sag_dc_create": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                C.POINTER(sag_level_desc), C.POINTER(sag_solver_config),
+                                C.POINTER(vp)]),
+    "sag_dc_destroy": (C.c_int, [vp]),
+    "sag_dc_set_parameters": (C.c_int, [vp, C.c_double, C.c_double, C.c_double]),
+    "sag_dc_set_sv_transfer": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]),
+    "sag_dc_apply": (C.c_int, [vp, vp, vp, vp]),
+    "sag_dc_vcycle": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int]),
+    "sag_dc_counters": (C.c_int, [vp, i64p]),
+    "sag_dc_info": (C.c_int, [vp, i64p, C.c_int]),
+    "sag_solve_stokes": (C.c_int, [vp, vp, vp, vp, C.POINTER(sag_solver_config),
+                                   C.POINTER(sag_krylov_report), vp, C.c_int]),
+}
+
+_lib = None
+
+
+def lib():
+    """Loads libsag.so (fails loudly: there is no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise CudaError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                            "(no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().sag_last_error().decode(errors="replace")
+        raise _ERRORS.get(rc, Error)(msg)
+
+
+# --------------------------------------------------------------- vectors --
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _vec_in(x, n: int):
+    """(pointer, keepalive) for a host (numpy) or device (torch CUDA) vector."""
+    if _is_torch(x):
+        if not x.is_cuda:
+            x = x.detach().cpu().numpy()
+        else:
+            assert x.dtype.is_floating_point and x.element_size() == 8 and x.is_contiguous()
+            if x.numel() != n:
+                raise DimensionMismatch(f"vector length {x.numel()} != {n}")
+            return C.c_void_p(x.data_ptr()), x
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if a.size != n:
+        raise DimensionMismatch(f"vector length {a.size} != {n}")
+    return C.c_void_p(a.ctypes.data), a
+
+
+def _vec_out(out, n: int, like=None):
+    if out is None:
+        if like is not None and _is_torch(like) and like.is_cuda:
+            import torch
+            out = torch.empty(n, dtype=torch.float64, device=like.device)
+        else:
+            out = np.empty(n, dtype=np.float64)
+    if _is_torch(out):
+        return C.c_void_p(out.data_ptr()), out
+    if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != n:
+        raise DimensionMismatch("output must be a contiguous float64 vector of length %d" % n)
+    return C.c_void_p(out.ctypes.data), out
+
+
+def _ints(a):
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return C.c_void_p(a.ctypes.data), a
+
+
+# --------------------------------------------------------------- context --
+class Context:
+    """One CUDA device + stream + workspaces (no reference analogue)."""
+
+    def __init__(self, device: int = 0):
+        h = vp()
+        _check(lib().sag_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sag_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(lib().sag_synchronize(self.h))
+
+    def launch_count(self) -> int:
+        v = C.c_longlong()
+        _check(lib().sag_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    def stream_ptr(self) -> int:
+        s = vp()
+        _check(lib().sag_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(int(os.environ.get("SAG_DEVICE", "0")))
+    return _default_ctx
+
+
+# ---------------------------------------------------------------- sparse --
+class SparseMatrix:
+    """Device CSR (sparse.hpp:11-28): canonical rows, int32 indices, fp64."""
+
+    def __init__(self, nrows, ncols, row_offsets, col_indices, values, ctx: Context = None):
+        self.ctx = ctx or default_context()
+        rp, self._rp = _ints(row_offsets)
+        ci, self._ci = _ints(col_indices)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        h = vp()
+        _check(lib().sag_matrix_create(self.ctx.h, int(nrows), int(ncols), int(self._rp[-1]),
+                                       rp, ci, C.c_void_p(v.ctypes.data), C.byref(h)))
+        self.h = h
+        self.nrows, self.ncols, self.nnz = int(nrows), int(ncols), int(self._rp[-1])
+        del self._rp, self._ci
+
+    @classmethod
+    def from_csr(cls, m, ctx: Context = None) -> "SparseMatrix":
+        """From any object with nrows/ncols/rp/ci/v (oracle.Csr) or a scipy matrix."""
+        if hasattr(m, "rp"):
+            return cls(m.nrows, m.ncols, m.rp, m.ci, m.v, ctx)
+        m = m.tocsr()
+        m.sort_indices()
+        return cls(m.shape[0], m.shape[1], m.indptr, m.indices, m.data, ctx)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().sag_matrix_destroy(self.h)
+        except Exception:
+            pass
+
+
+def spmv(m: SparseMatrix, x, out=None):
+    """y = m x (sparse.cpp:78-91)."""
+    xp, xk = _vec_in(x, m.ncols)
+    yp, y = _vec_out(out, m.nrows, like=x)
+    _check(lib().sag_spmv(m.ctx.h, m.h, xp, yp))
+    return y
+
+
+def norm2(v, ctx: Context = None) -> float:
+    ctx = ctx or default_context()
+    n = v.numel() if _is_torch(v) else len(v)
+    p, k = _vec_in(v, n)
+    out = C.c_double()
+    _check(lib().sag_norm2(ctx.h, n, p, C.byref(out)))
+    return out.value
+
+
+def dot(a, b, ctx: Context = None) -> float:
+    ctx = ctx or default_context()
+    n = a.numel() if _is_torch(a) else len(a)
+    pa, ka = _vec_in(a, n)
+    pb, kb = _vec_in(b, n)
+    out = C.c_double()
+    _check(lib().sag_dot(ctx.h, n, pa, pb, C.byref(out)))
+    return out.value
+
+
+# ----------------------------------------------------------------- vanka --
+@dataclass
+class PatchLists:
+    pressure_ptr: np.ndarray
+    pressure: np.ndarray
+    velocity_ptr: np.ndarray
+    velocity: np.ndarray
+    nx: np.ndarray
+
+
+class Patches:
+    """Vanka patch sets (vanka.hpp:11-15) on the device."""
+
+    def __init__(self, h, ctx: Context):
+        self.h, self.ctx = h, ctx
+        info = np.zeros(5, dtype=np.int64)
+        _check(lib().sag_patches_info(h, info.ctypes.data_as(i64p)))
+        self.npatch, self.total_pressure, self.total_velocity, self.max_nv, self.max_np = (
+            int(v) for v in info)
+
+    @classmethod
+    def from_lists(cls, pressure_ptr, pressure, velocity_ptr, velocity, nx,
+                   ctx: Context = None) -> "Patches":
+        ctx = ctx or default_context()
+        arrs = [_ints(a) for a in (pressure_ptr, pressure, velocity_ptr, velocity, nx)]
+        h = vp()
+        _check(lib().sag_patches_create(ctx.h, len(arrs[4][1]), *[a[0] for a in arrs],
+                                        C.byref(h)))
+        return cls(h, ctx)
+
+    def export(self) -> PatchLists:
+        pp = np.empty(self.npatch + 1, dtype=np.int32)
+        vpp = np.empty(self.npatch + 1, dtype=np.int32)
+        pi = np.empty(max(self.total_pressure, 1), dtype=np.int32)
+        vi = np.empty(max(self.total_velocity, 1), dtype=np.int32)
+        nx = np.empty(max(self.npatch, 1), dtype=np.int32)
+        _check(lib().sag_patches_export(self.ctx.h, self.h, *[C.c_void_p(a.ctypes.data)
+                                                               for a in (pp, pi, vpp, vi, nx)]))
+        return PatchLists(pp, pi[:self.total_pressure], vpp, vi[:self.total_velocity],
+                          nx[:self.npatch])
+
+    def __del__(self):
+        try:
+            lib().sag_patches_destroy(self.h)
+        except Exception:
+            pass
+
+
+def build_patches(k: SparseMatrix, n_x: int, n_y: int, n_p: int,
+                  sv_triples: bool = False) -> Patches:
+    """build_patches (vanka.cpp:11-42)."""
+    h = vp()
+    _check(lib().sag_build_patches(k.ctx.h, k.h, n_x, n_y, n_p, int(sv_triples), C.byref(h)))
+    return Patches(h, k.ctx)
+
+
+class VankaFactorization:
+    """factor_patches result (vanka.hpp:23-40), device resident."""
+
+    def __init__(self, h, ctx: Context, k: SparseMatrix):
+        self.h, self.ctx, self.k = h, ctx, k
+        s = np.zeros(7, dtype=np.int64)
+        _check(lib().sag_vanka_stats(h, s.ctypes.data_as(i64p)))
+        (self.a_factor_bytes, self.aux_bytes, self.dense_inverse_bytes, self.device_bytes,
+         self.npatch, self.n, self.nslots) = (int(v) for v in s)
+
+    def export(self, patches: PatchLists):
+        nv = np.diff(patches.velocity_ptr).astype(np.int64)
+        npp = np.diff(patches.pressure_ptr).astype(np.int64)
+        aux = int((nv * npp).sum())
+        ss = int((npp * npp).sum())
+        u = np.empty(max(aux, 1))
+        b = np.empty(max(aux, 1))
+        s = np.empty(max(ss, 1))
+        w = np.empty(self.n)
+        _check(lib().sag_vanka_export(self.ctx.h, self.h, *[C.c_void_p(a.ctypes.data)
+                                                             for a in (u, b, s, w)]))
+        return dict(uhat=u[:aux], bhat=b[:aux], sinv=s[:ss], weights=w)
+
+    def __del__(self):
+        try:
+            lib().sag_vanka_destroy(self.h)
+        except Exception:
+            pass
+
+
+def factor_patches(k: SparseMatrix, patches: Patches, n_u: int) -> VankaFactorization:
+    """factor_patches (vanka.cpp:64-149): batched block LU on the device."""
+    h = vp()
+    _check(lib().sag_factor_patches(k.ctx.h, k.h, patches.h, int(n_u), C.byref(h)))
+    return VankaFactorization(h, k.ctx, k)
+
+
+def apply_vanka(f: VankaFactorization, r, out=None):
+    """delta = sum_i V_i^T W K_i^-1 V_i r (vanka.cpp:151-184)."""
+    rp, rk = _vec_in(r, f.n)
+    dp, d = _vec_out(out, f.n, like=r)
+    _check(lib().sag_apply_vanka(f.ctx.h, f.h, rp, dp))
+    return d
+
+
+class RelaxMode:
+    KrylovWrapped = 0
+    Stationary = 1
+
+
+def vanka_relax(k: SparseMatrix, f: VankaFactorization, x, b, mode: int, sweeps: int,
+                omega: float = 1.0):
+    """vanka_relax (vanka.cpp:186-209); x is updated in place and returned."""
+    if not _is_torch(x):
+        if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous):
+            raise TypeError("x must be a contiguous float64 numpy array (updated in place)")
+    xp, xk = _vec_out(x, k.nrows)
+    bp, bk = _vec_in(b, k.nrows)
+    _check(lib().sag_vanka_relax(k.ctx.h, k.h, f.h, xp, bp, int(mode), int(sweeps),
+                                 float(omega)))
+    return x
+
+
+# ---------------------------------------------------------------- krylov --
+@dataclass
+class FgmresOptions:
+    """krylov.hpp:17-22"""
+    tol: float = 1e-8
+    max_iters: int = 500
+    restart: int = 20
+    breakdown: float = 1e-30
+
+
+@dataclass
+class KrylovReport:
+    """krylov.hpp:24-29"""
+    converged: bool = False
+    iterations: int = 0
+    residual_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    final_relative_residual: float = 0.0
+
+
+def fgmres(a: SparseMatrix, b, x, prec=None, opt: FgmresOptions = None) -> KrylovReport:
+    """fgmres(matrix_operator(a), b, x, prec, opt) (krylov.cpp:17-121). ``prec``
+    is None (identity), a VankaFactorization, a SparseMatrix (Jacobi on its
+    diagonal) or a DCPreconditioner. x (guess) is updated in place."""
+    opt = opt or FgmresOptions()
+    if prec is None:
+        kind, ph = 0, None
+    elif isinstance(prec, VankaFactorization):
+        kind, ph = 1, prec.h
+    elif isinstance(prec, SparseMatrix):
+        kind, ph = 2, prec.h
+    elif isinstance(prec, DCPreconditioner):
+        kind, ph = 3, prec.h
+    else:
+        raise ConfigError("unsupported preconditioner object")
+    bp, bk = _vec_in(b, a.nrows)
+    xp, xk = _vec_out(x, a.nrows)
+    rep = sag_krylov_report()
+    cap = opt.max_iters + 2
+    hist = np.zeros(cap)
+    o = sag_fgmres_options(opt.tol, opt.max_iters, opt.restart, opt.breakdown)
+    _check(lib().sag_fgmres(a.ctx.h, a.h, bp, xp, kind, ph, C.byref(o), C.byref(rep),
+                            C.c_void_p(hist.ctypes.data), cap))
+    return KrylovReport(bool(rep.converged), rep.iterations,
+                        hist[:min(rep.iterations + 1, cap)].copy(), rep.final_relative_residual)
+
+
+# -------------------------------------------------------- preconditioner --
+class Variant:
+    DCall = 0
+    DCLO = 1
+    DCHO = 2
+
+
+@dataclass
+class SolverConfig:
+    """preconditioner.hpp:19-36 (reference defaults)."""
+    variant: int = Variant.DCall
+    eta_u: float = 1.0
+    eta_p: float = 1.0
+    omega0: float = 1.0
+    nu1: int = 2
+    nu2: int = 2
+    gamma: int = 1
+    restart: int = 20
+    tol: float = 1e-10
+    max_iters: int = 200
+    enclosed_flow: bool = False
+
+    def to_c(self) -> sag_solver_config:
+        return sag_solver_config(int(self.variant), float(self.eta_u), float(self.eta_p),
+                                 float(self.omega0), int(self.nu1), int(self.nu2),
+                                 int(self.gamma), int(self.restart), float(self.tol),
+                                 int(self.max_iters), int(bool(self.enclosed_flow)))
+
+    def check(self):
+        c = self.to_c()
+        _check(lib().sag_solver_config_check(C.byref(c)))
+
+
+class DCPreconditioner:
+    """DCPreconditioner (preconditioner.hpp:77-100) on a host-built hierarchy.
+
+    ``k0``: SparseMatrix of the high-order system with block sizes ``nxyz0``;
+    ``levels``: [(K_l SparseMatrix, P_l SparseMatrix | None, (n_x, n_y, n_p))]
+    of the low-order monolithic hierarchy (amg.hpp:85-93, as produced by the
+    reference's build_monolithic_hierarchy)."""
+
+    def __init__(self, k0: SparseMatrix, nxyz0: Sequence[int], levels, cfg: SolverConfig,
+                 sv: bool = False):
+        self.ctx = k0.ctx
+        self.k0 = k0
+        self.levels = levels  # keep the device matrices alive
+        self.cfg = cfg
+        descs = (sag_level_desc * len(levels))()
+        for i, (k, p, (nx, ny, npp)) in enumerate(levels):
+            descs[i] = sag_level_desc(k.h.value if k is not None else None,
+                                      p.h.value if p is not None else None, nx, ny, npp)
+        h = vp()
+        c = cfg.to_c()
+        _check(lib().sag_dc_create(self.ctx.h, k0.h, int(nxyz0[0]), int(nxyz0[1]),
+                                   int(nxyz0[2]), int(sv), len(levels), descs, C.byref(c),
+                                   C.byref(h)))
+        self.h = h
+        self.n = k0.nrows
+        self.n_p = int(nxyz0[2])
+        self.sv = sv
+
+    def set_sv_transfer(self, p_dup: SparseMatrix, m_mix: SparseMatrix, scalar_levels,
+                        scalar_prolongators):
+        self._sv_keep = (p_dup, m_mix, scalar_levels, scalar_prolongators)
+        L = (vp * len(scalar_levels))(*[m.h.value for m in scalar_levels])
+        P = (vp * max(len(scalar_prolongators), 1))(*[m.h.value for m in scalar_prolongators])
+        _check(lib().sag_dc_set_sv_transfer(self.h, p_dup.h, m_mix.h, len(scalar_levels), L, P))
+
+    def set_parameters(self, eta_u: float, eta_p: float, omega0: float):
+        _check(lib().sag_dc_set_parameters(self.h, eta_u, eta_p, omega0))
+        self.cfg.eta_u, self.cfg.eta_p, self.cfg.omega0 = eta_u, eta_p, omega0
+
+    def apply(self, r, out=None):
+        rp, rk = _vec_in(r, self.n)
+        zp, z = _vec_out(out, self.n, like=r)
+        _check(lib().sag_dc_apply(self.ctx.h, self.h, rp, zp))
+        return z
+
+    def vcycle(self, b, nu1: int, nu2: int, out=None):
+        n1 = self.levels[0][0].nrows
+        bp, bk = _vec_in(b, n1)
+        xp, x = _vec_out(out, n1, like=b)
+        _check(lib().sag_dc_vcycle(self.ctx.h, self.h, bp, xp, nu1, nu2))
+        return x
+
+    @property
+    def fine_relax_units(self) -> int:
+        return self._counters()[0]
+
+    @property
+    def level1_relax_units(self) -> int:
+        return self._counters()[1]
+
+    def _counters(self):
+        v = np.zeros(2, dtype=np.int64)
+        _check(lib().sag_dc_counters(self.h, v.ctypes.data_as(i64p)))
+        return int(v[0]), int(v[1])
+
+    def info(self):
+        v = np.zeros(32, dtype=np.int64)
+        _check(lib().sag_dc_info(self.h, v.ctypes.data_as(i64p), 32))
+        nl = int(v[0])
+        return dict(nlevels=nl, n0=int(v[1]), level_rows=[int(x) for x in v[2:2 + nl]],
+                    factor_bytes=int(v[2 + nl]), graph_launches=int(v[3 + nl]))
+
+    def size(self):
+        return self.n
+
+    def pressure_size(self):
+        return self.n_p
+
+    def __del__(self):
+        try:
+            lib().sag_dc_destroy(self.h)
+        except Exception:
+            pass
+
+
+def solve_stokes(k0: SparseMatrix, rhs, prec: DCPreconditioner, cfg: SolverConfig, x=None):
+    """solve_stokes (preconditioner.cpp:229-259): returns (x, KrylovReport)."""
+    if k0 is not prec.k0:
+        raise ConfigError("solve_stokes: k0 must be the preconditioner's high-order operator")
+    bp, bk = _vec_in(rhs, prec.n)
+    xp, xo = _vec_out(x, prec.n, like=rhs)
+    rep = sag_krylov_report()
+    cap = cfg.max_iters + 2
+    hist = np.zeros(cap)
+    c = cfg.to_c()
+    _check(lib().sag_solve_stokes(prec.ctx.h, prec.h, bp, xp, C.byref(c), C.byref(rep),
+                                  C.c_void_p(hist.ctypes.data), cap))
+    return xo, KrylovReport(bool(rep.converged), rep.iterations,
+                            hist[:min(rep.history_len, cap)].copy(),
+                            rep.final_relative_residual)

@@ -1,0 +1,191 @@
+// Internal C++ objects behind the C-ABI handles, device-side scalar state of
+// the Krylov solvers, and the host-side launchers shared by the .cu files.
+#pragma once
+
+#include <memory>
+
+#include "common.cuh"
+
+struct sag_ctx {
+  sag::Ctx c;
+};
+
+namespace sag {
+
+// CSR on device (sparse.hpp:11-28). `group` = lanes per row used by SpMV.
+struct Matrix {
+  Ctx* ctx = nullptr;
+  int nrows = 0, ncols = 0;
+  long long nnz = 0;
+  DevBuf<int> rp, ci;
+  DevBuf<double> v;
+  int group = 8;
+  double norm_inf = -1.0;  // cached (sparse.cpp:229-237)
+};
+
+// Vanka patch sets (vanka.hpp:11-15), CSR-like on device.
+struct Patches {
+  int npatch = 0;
+  long long tot_p = 0, tot_v = 0;
+  int max_nv = 0, max_np = 0, max_dim = 0;  // max_dim = max over patches of max(nx, ny)
+  DevBuf<int> pptr, pidx, vptr, vidx, nx;
+};
+
+// Device factorization (vanka.hpp:23-40) in the apply representation: one
+// 16-byte-aligned blob per patch
+//   header {int nx, ny, np, slot_base}
+//   A_x^-1 (nx*nx, column-major) | A_y^-1 (ny*ny, column-major)
+//   U_hat  (np rows of nv: [a*nv+i] = u_hat(i,a))
+//   B_hat  (np rows of nv: [a*nv+j] = b_hat(a,j))
+//   S^-1   (np*np row-major)
+//   velocity dofs (nv int32) | pressure dofs (np int32) | pad to 16 B
+// plus the PoU weights and the dof -> slot map of the atomic-free
+// owner-computes scatter: each dof sums its patch contributions in ascending
+// patch order, the order of vanka.cpp:176-181.
+struct Vanka {
+  int n = 0, npatch = 0;
+  DevBuf<unsigned char> blob;
+  DevBuf<long long> off;  // npatch + 1, bytes
+  int slot_bytes = 0;     // max blob bytes
+  int max_dim = 0, max_nv = 0, max_np = 0;
+  long long nslots = 0;
+  DevBuf<double> out;     // per-patch local results (nslots)
+  DevBuf<double> w;       // PoU weights (n)
+  DevBuf<int> dof_ptr;    // n + 1
+  DevBuf<int> dof_slot;   // nslots
+  long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
+  long long blob_bytes = 0;
+};
+
+// Krylov scalar state in device memory (one per FGMRES instance); mirrors the
+// host scalars of krylov.cpp:17-121.
+struct KState {
+  double ref, tol, bd;
+  double beta, rnorm, wnorm;
+  int m, stop, breakdown, jeff, iterations, hist_len, hist_cap, converged;
+  // followed by h[(m+1)*m], cs[m], sn[m], g[m+1], y[m], hist[hist_cap]
+};
+__host__ __device__ inline size_t kstate_bytes(int m, int hist_cap) {
+  return sizeof(KState) +
+         sizeof(double) * ((size_t)(m + 1) * m + m + m + (m + 1) + m + hist_cap);
+}
+__host__ __device__ inline double* ks_h(KState* s) { return reinterpret_cast<double*>(s + 1); }
+__host__ __device__ inline double* ks_cs(KState* s) { return ks_h(s) + (size_t)(s->m + 1) * s->m; }
+__host__ __device__ inline double* ks_sn(KState* s) { return ks_cs(s) + s->m; }
+__host__ __device__ inline double* ks_g(KState* s) { return ks_sn(s) + s->m; }
+__host__ __device__ inline double* ks_y(KState* s) { return ks_g(s) + s->m + 1; }
+__host__ __device__ inline double* ks_hist(KState* s) { return ks_y(s) + s->m; }
+
+// What the last block of a reducing kernel does with the total.
+enum FinKind {
+  FIN_NONE = 0,
+  FIN_STORE,      // *out = tot
+  FIN_SQRT,       // *out = sqrt(tot)
+  FIN_MEAN,       // *out = tot / i
+  FIN_REF,        // st->ref = sqrt(tot) > 0 ? sqrt(tot) : 1           (krylov.cpp:23-24)
+  FIN_BETA,       // (re)start: beta = rnorm = sqrt(tot); g = beta e_0;   (krylov.cpp:44-53)
+  FIN_H,          // h[i*m+j] = tot                                       (krylov.cpp:64-65)
+  FIN_ARNOLDI,    // wnorm = sqrt(tot); Givens; residual estimate        (krylov.cpp:68-100)
+  FIN_FINAL,      // *out = sqrt(tot) / st->ref                           (krylov.cpp:116-118)
+};
+struct Fin {
+  int kind = FIN_NONE;
+  KState* st = nullptr;
+  int i = 0, j = 0;
+  double* out = nullptr;
+  double tol = 0.0;  // FIN_BETA with bit 4: (re)initialise st (m = j, tol, bd = 1e-30)
+};
+
+__device__ void apply_fin(const Fin& f, double tot);
+
+// SpMV epilogues: y_i from the row sum s_i
+enum class Epi {
+  Store,      // y = s
+  Resid,      // y = b - s
+  ResidEta,   // y = eta_(u|p) * (b - s)     (residual + apply_eta_weighting, transfer.cpp:127-135)
+  Add,        // y += s                      (x += P xc, preconditioner.cpp:75-76)
+  StoreDot,   // y = s, reduce y * dotv      (w = A z_j fused with h_0j, krylov.cpp:61-64)
+  ResidSsq,   // y = b - s, reduce y^2       (residual + norm2, krylov.cpp:44-46)
+};
+
+struct SpmvArgs {
+  const double* b = nullptr;
+  const double* dotv = nullptr;
+  double eta_u = 1.0, eta_p = 1.0;
+  int n_u = 0;
+  Fin fin;
+  const int* gate = nullptr;  // skip the whole launch when *gate != 0
+};
+
+void launch_spmv(Ctx& c, const Matrix& m, const double* x, double* y, Epi e,
+                 const SpmvArgs& a = SpmvArgs());
+void compute_norm_inf(Ctx& c, Matrix& m);
+
+// deterministic BLAS-1 (reductions finish through Fin)
+void launch_dot(Ctx& c, int n, const double* a, const double* b, const Fin& fin,
+                const int* gate = nullptr);
+void launch_ssq(Ctx& c, int n, const double* a, const Fin& fin, const int* gate = nullptr);
+void launch_sum(Ctx& c, int n, const double* a, const Fin& fin);
+// y = x / *s (skipped when *gate or *gate2)
+void launch_div(Ctx& c, int n, const double* x, const double* s, double* y, const int* gate,
+                const int* gate2 = nullptr);
+// w -= (*h) * vprev; reduce w . vnext (vprev may be null)        (krylov.cpp:63-67)
+void launch_mgs(Ctx& c, int n, double* w, const double* vprev, const double* h,
+                const double* vnext, const Fin& fin, const int* gate);
+// w -= (*h) * v; reduce w . w
+void launch_mgs_last(Ctx& c, int n, double* w, const double* v, const double* h, const Fin& fin,
+                     const int* gate);
+// y = back-substitution of the jeff x jeff Hessenberg system (krylov.cpp:102-107)
+void launch_backsub(Ctx& c, KState* st);
+// x += sum_{i<jeff} y_i Z_i   (krylov.cpp:108-110 then vanka.cpp:208);
+// store = true: x = sum (x was zero)
+void launch_update(Ctx& c, int n, double* x, const double* Z, size_t zstride, KState* st,
+                   bool store = false);
+// z = dinv * r
+void launch_mul(Ctx& c, int n, const double* a, const double* b, double* y);
+// dinv_i = 1 / a_ii; returns false (via *bad) if a diagonal entry is missing/zero
+void launch_inv_diag(Ctx& c, const Matrix& m, double* dinv, int* bad);
+// KState (re)initialisation for a new solve: ref/tol/bd/m/iterations
+void launch_kinit(Ctx& c, KState* st, int m, double tol, double bd, int hist_cap,
+                  bool keep_ref);
+void launch_copy(Ctx& c, int n, const double* x, double* y);
+void launch_zero(Ctx& c, int n, double* y);
+// y = x with the pressure block shifted by -(*mean)   (preconditioner.cpp:235-240)
+void launch_project(Ctx& c, int n, int n_u, const double* x, const double* mean, double* y);
+// y = eta_u * x (i < n_u), eta_p * x (i >= n_u)   (transfer.cpp:127-135)
+void launch_eta(Ctx& c, int n, int n_u, double eta_u, double eta_p, const double* x, double* y);
+// x += y
+void launch_add(Ctx& c, int n, double* x, const double* y);
+// x += omega * d
+void launch_axpy(Ctx& c, int n, double* x, double omega, const double* d);
+
+// Vanka: delta = apply_vanka(r) (vanka.cpp:151-184). With `div`, r is read as
+// r / *div (v_0 = r / ||r||, krylov.cpp:47). With `xadd`, the gather adds
+// omega*delta into xadd instead of storing delta (vanka.cpp:195).
+void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta,
+                 const int* gate = nullptr);
+void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega);
+std::unique_ptr<Patches> build_patches_dev(Ctx& c, const Matrix& k, int n_x, int n_y, int n_p,
+                                           bool sv_triples);
+std::unique_ptr<Patches> patches_from_lists(Ctx& c, int npatch, const int* pptr,
+                                            const int* pidx, const int* vptr, const int* vidx,
+                                            const int* nx);
+std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches& p);
+// the reference's factor layout, for parity tests (vanka.hpp:31-33)
+void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* sinv,
+                  double* weights);
+
+// transpose on device (sparse.cpp:93-111): rows of the result in ascending order
+std::unique_ptr<Matrix> transpose_dev(Ctx& c, const Matrix& a);
+
+}  // namespace sag
+
+struct sag_matrix {
+  sag::Matrix m;
+};
+struct sag_patches {
+  sag::Patches p;
+};
+struct sag_vanka {
+  sag::Vanka f;
+};

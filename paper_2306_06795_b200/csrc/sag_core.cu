@@ -1,0 +1,796 @@
+// libsag core: context, CSR upload/validation, SpMV with fused epilogues,
+// deterministic BLAS-1 reductions, Krylov scalar finishers, transpose, and the
+// C-ABI for those pieces (include/sag.h).
+//
+// Reference behaviour restated here:
+//   spmv            sparse.cpp:78-91   (row sums; here G lanes per row + shuffle tree)
+//   norm2 / dot     sparse.cpp:217-227 (here fixed-order two-stage reductions)
+//   norm_inf        sparse.cpp:229-237
+//   transpose       sparse.cpp:93-111  (rows of P^T in ascending order)
+//   FGMRES scalars  krylov.cpp:42-110  (finishers below)
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "internal.cuh"
+
+namespace sag {
+
+// ------------------------------------------------------------ finishers --
+
+__device__ void apply_fin(const Fin& f, double tot) {
+  KState* st = f.st;
+  switch (f.kind) {
+    case FIN_STORE:
+      *f.out = tot;
+      break;
+    case FIN_SQRT:
+      *f.out = sqrt(tot);
+      break;
+    case FIN_MEAN:
+      *f.out = tot / (double)f.i;
+      break;
+    case FIN_REF: {
+      const double b = sqrt(tot);
+      st->ref = b > 0.0 ? b : 1.0;
+      break;
+    }
+    case FIN_BETA: {
+      // f.i bit0: also set ref (inner solve: ||b|| == ||r|| for x0 = 0)
+      // f.i bit1: push the residual to the history
+      const double beta = sqrt(tot);
+      if (f.i & 4) {
+        st->m = f.j;
+        st->tol = f.tol;
+        st->bd = 1e-30;
+        st->iterations = 0;
+        st->converged = 0;
+        st->hist_len = 0;
+        st->hist_cap = 0;
+      }
+      if (f.i & 1) st->ref = beta > 0.0 ? beta : 1.0;
+      st->beta = beta;
+      st->rnorm = beta;
+      double* g = ks_g(st);
+      g[0] = beta;
+      for (int i = 1; i <= st->m; ++i) g[i] = 0.0;
+      st->jeff = 0;
+      st->breakdown = 0;
+      st->stop = (beta / st->ref <= st->tol) ? 1 : 0;
+      if (st->stop) st->converged = 1;
+      if (f.i & 2) {
+        if (st->hist_len < st->hist_cap) ks_hist(st)[st->hist_len] = beta;
+        st->hist_len++;
+      }
+      break;
+    }
+    case FIN_H:
+      ks_h(st)[(size_t)f.i * st->m + f.j] = tot;
+      break;
+    case FIN_ARNOLDI: {
+      const int m = st->m, j = f.j;
+      double* h = ks_h(st);
+      double* cs = ks_cs(st);
+      double* sn = ks_sn(st);
+      double* g = ks_g(st);
+      const double wnorm = sqrt(tot);
+      st->wnorm = wnorm;
+      h[(size_t)(j + 1) * m + j] = wnorm;
+      const int bd = wnorm < st->bd;
+      st->breakdown = bd;
+      for (int i = 0; i < j; ++i) {
+        const double a = h[(size_t)i * m + j], b = h[(size_t)(i + 1) * m + j];
+        const double t = cs[i] * a + sn[i] * b;
+        h[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * b;
+        h[(size_t)i * m + j] = t;
+      }
+      const double a = h[(size_t)j * m + j], b = h[(size_t)(j + 1) * m + j];
+      const double denom = hypot(a, b);
+      if (denom > 0.0) {
+        cs[j] = a / denom;
+        sn[j] = b / denom;
+      } else {
+        cs[j] = 1.0;
+        sn[j] = 0.0;
+      }
+      h[(size_t)j * m + j] = cs[j] * a + sn[j] * b;
+      h[(size_t)(j + 1) * m + j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      st->iterations++;
+      const double rn = fabs(g[j + 1]);
+      st->rnorm = rn;
+      if (st->hist_len < st->hist_cap) ks_hist(st)[st->hist_len] = rn;
+      st->hist_len++;
+      st->jeff = j + 1;
+      const int conv = rn / st->ref <= st->tol;
+      if (conv) st->converged = 1;
+      if (conv || bd) st->stop = 1;
+      break;
+    }
+    case FIN_FINAL: {
+      const double fr = sqrt(tot) / st->ref;
+      *f.out = fr;
+      if (fr <= st->tol) st->converged = 1;
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+// Block partial -> last block sums partials in order -> finisher.
+__device__ __forceinline__ void reduce_finish(double red, const Fin& fin, double* partials,
+                                              unsigned* ticket) {
+  __shared__ double sh[32];
+  const double bs = block_sum(red, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = bs;
+  if (last_block(ticket)) {
+    const double tot = sum_partials(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      apply_fin(fin, tot);
+      *ticket = 0u;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ SpMV --
+// G lanes per row; the warp iterates over groups of rows with a warp-uniform
+// trip count so the segmented shuffle tree is always executed by full warps.
+template <int G, Epi E>
+__global__ void __launch_bounds__(256) spmv_kernel(int nrows, const int* __restrict__ rp,
+                                                   const int* __restrict__ ci,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   double* __restrict__ y, SpmvArgs a,
+                                                   double* partials, unsigned* ticket) {
+  if (a.gate && *a.gate) return;
+  constexpr bool kRed = (E == Epi::StoreDot || E == Epi::ResidSsq);
+  constexpr int RPW = 32 / G;  // rows per warp per step
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (G - 1);
+  const int grp = lane / G;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  double red = 0.0;
+  for (int base = warp * RPW; base < nrows; base += nwarps * RPW) {
+    const int row = base + grp;
+    double s = 0.0;
+    if (row < nrows) {
+      const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
+#pragma unroll 4
+      for (int k = beg + sub; k < end; k += G) s = fma(__ldg(val + k), __ldg(x + __ldg(ci + k)), s);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+    if (sub == 0 && row < nrows) {
+      if constexpr (E == Epi::Store) {
+        y[row] = s;
+      } else if constexpr (E == Epi::Resid) {
+        y[row] = a.b[row] - s;
+      } else if constexpr (E == Epi::ResidEta) {
+        y[row] = (row < a.n_u ? a.eta_u : a.eta_p) * (a.b[row] - s);
+      } else if constexpr (E == Epi::Add) {
+        y[row] = y[row] + s;
+      } else if constexpr (E == Epi::StoreDot) {
+        y[row] = s;
+        red = fma(s, a.dotv[row], red);
+      } else if constexpr (E == Epi::ResidSsq) {
+        const double r = a.b[row] - s;
+        y[row] = r;
+        red = fma(r, r, red);
+      }
+    }
+  }
+  if constexpr (kRed) reduce_finish(red, a.fin, partials, ticket);
+}
+
+template <int G>
+static void spmv_dispatch_e(Ctx& c, const Matrix& m, const double* x, double* y, Epi e,
+                            const SpmvArgs& a) {
+  const int rows_per_block = 256 / G;
+  long long need = (m.nrows + rows_per_block - 1) / rows_per_block;
+  const bool red = (e == Epi::StoreDot || e == Epi::ResidSsq);
+  const long long cap = red ? kMaxRedGrid : (long long)c.num_sms * 16;
+  int grid = (int)std::max(1LL, std::min(need, cap));
+  auto* rp = m.rp.p;
+  auto* ci = m.ci.p;
+  auto* v = m.v.p;
+  switch (e) {
+#define CASE(EE)                                                                              \
+  case Epi::EE:                                                                               \
+    spmv_kernel<G, Epi::EE><<<grid, 256, 0, c.stream>>>(m.nrows, rp, ci, v, x, y, a,          \
+                                                        c.partials.p, c.ticket.p);            \
+    break;
+    CASE(Store)
+    CASE(Resid)
+    CASE(ResidEta)
+    CASE(Add)
+    CASE(StoreDot)
+    CASE(ResidSsq)
+#undef CASE
+  }
+  SAG_LAUNCHED(c);
+}
+
+void launch_spmv(Ctx& c, const Matrix& m, const double* x, double* y, Epi e, const SpmvArgs& a) {
+  if (m.nrows == 0) return;
+  switch (m.group) {
+    case 2: spmv_dispatch_e<2>(c, m, x, y, e, a); break;
+    case 4: spmv_dispatch_e<4>(c, m, x, y, e, a); break;
+    case 8: spmv_dispatch_e<8>(c, m, x, y, e, a); break;
+    case 16: spmv_dispatch_e<16>(c, m, x, y, e, a); break;
+    default: spmv_dispatch_e<32>(c, m, x, y, e, a); break;
+  }
+}
+
+// --------------------------------------------------------------- BLAS-1 --
+
+__global__ void __launch_bounds__(kRedBlock) dot_kernel(int n, const double* __restrict__ a,
+                                                        const double* __restrict__ b, Fin fin,
+                                                        const int* gate, double* partials,
+                                                        unsigned* ticket) {
+  if (gate && *gate) return;
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    s = fma(a[i], b[i], s);
+  reduce_finish(s, fin, partials, ticket);
+}
+
+__global__ void __launch_bounds__(kRedBlock) sum_kernel(int n, const double* __restrict__ a,
+                                                        Fin fin, double* partials,
+                                                        unsigned* ticket) {
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    s += a[i];
+  reduce_finish(s, fin, partials, ticket);
+}
+
+__global__ void div_kernel(int n, const double* __restrict__ x, const double* s,
+                           double* __restrict__ y, const int* gate, const int* gate2) {
+  if ((gate && *gate) || (gate2 && *gate2)) return;
+  const double d = *s;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = x[i] / d;
+}
+
+__global__ void __launch_bounds__(kRedBlock) mgs_kernel(int n, double* __restrict__ w,
+                                                        const double* __restrict__ vprev,
+                                                        const double* h,
+                                                        const double* __restrict__ vnext,
+                                                        Fin fin, const int* gate,
+                                                        double* partials, unsigned* ticket) {
+  if (gate && *gate) return;
+  const double hh = vprev ? *h : 0.0;
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double wi = w[i];
+    if (vprev) {
+      wi = fma(-hh, vprev[i], wi);
+      w[i] = wi;
+    }
+    s = fma(wi, vnext[i], s);
+  }
+  reduce_finish(s, fin, partials, ticket);
+}
+
+__global__ void __launch_bounds__(kRedBlock) mgs_last_kernel(int n, double* __restrict__ w,
+                                                             const double* __restrict__ v,
+                                                             const double* h, Fin fin,
+                                                             const int* gate, double* partials,
+                                                             unsigned* ticket) {
+  if (gate && *gate) return;
+  const double hh = *h;
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double wi = fma(-hh, v[i], w[i]);
+    w[i] = wi;
+    s = fma(wi, wi, s);
+  }
+  reduce_finish(s, fin, partials, ticket);
+}
+
+// krylov.cpp:102-107, one thread (j <= restart)
+__global__ void backsub_kernel(KState* st) {
+  const int j = st->jeff, m = st->m;
+  const double* h = ks_h(st);
+  const double* g = ks_g(st);
+  double* y = ks_y(st);
+  for (int i = j - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int k = i + 1; k < j; ++k) s -= h[(size_t)i * m + k] * y[k];
+    y[i] = s / h[(size_t)i * m + i];
+  }
+}
+
+// krylov.cpp:108-110 (+ vanka.cpp:208 for relaxation): x += sum_i y_i Z_i
+__global__ void update_kernel(int n, double* __restrict__ x, const double* __restrict__ Z,
+                              size_t zs, const KState* st, int store) {
+  const int j = st->jeff;
+  if (j == 0 && !store) return;
+  const double* y = ks_y(const_cast<KState*>(st));
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    double corr = 0.0;
+    for (int i = 0; i < j; ++i) corr = fma(y[i], Z[(size_t)i * zs + k], corr);
+    x[k] = store ? corr : x[k] + corr;
+  }
+}
+
+__global__ void mul_kernel(int n, const double* __restrict__ a, const double* __restrict__ b,
+                           double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = a[i] * b[i];
+}
+
+// inv_diagonal (sparse.cpp:208-215)
+__global__ void inv_diag_kernel(int n, const int* rp, const int* ci, const double* v,
+                                double* dinv, int* bad) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double d = 0.0;
+    for (int k = rp[r]; k < rp[r + 1]; ++k)
+      if (ci[k] == r) d = v[k];
+    if (d == 0.0) atomicOr(bad, 1);
+    dinv[r] = 1.0 / d;
+  }
+}
+
+__global__ void kinit_kernel(KState* st, int m, double tol, double bd, int hist_cap,
+                             int keep_ref) {
+  if (!keep_ref) st->ref = 1.0;
+  st->tol = tol;
+  st->bd = bd;
+  st->m = m;
+  st->stop = 0;
+  st->breakdown = 0;
+  st->jeff = 0;
+  st->iterations = 0;
+  st->hist_len = 0;
+  st->hist_cap = hist_cap;
+  st->converged = 0;
+  st->beta = 0.0;
+  st->rnorm = 0.0;
+}
+
+__global__ void copy_kernel(int n, const double* __restrict__ x, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+__global__ void zero_kernel(int n, double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = 0.0;
+}
+__global__ void project_kernel(int n, int n_u, const double* __restrict__ x, const double* mean,
+                               double* __restrict__ y) {
+  const double mu = *mean;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = i < n_u ? x[i] : x[i] - mu;
+}
+__global__ void eta_kernel(int n, int n_u, double eu, double ep, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = (i < n_u ? eu : ep) * x[i];
+}
+__global__ void add_kernel(int n, double* __restrict__ x, const double* __restrict__ y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = x[i] + y[i];
+}
+__global__ void axpy_kernel(int n, double* __restrict__ x, double omega,
+                            const double* __restrict__ d) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = x[i] + omega * d[i];
+}
+
+static int ew_grid(Ctx& c, long long n) {
+  long long g = (n + 255) / 256;
+  return (int)std::max(1LL, std::min(g, (long long)c.num_sms * 16));
+}
+
+void launch_dot(Ctx& c, int n, const double* a, const double* b, const Fin& fin,
+                const int* gate) {
+  dot_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, a, b, fin, gate, c.partials.p,
+                                                      c.ticket.p);
+  SAG_LAUNCHED(c);
+}
+void launch_ssq(Ctx& c, int n, const double* a, const Fin& fin, const int* gate) {
+  dot_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, a, a, fin, gate, c.partials.p,
+                                                      c.ticket.p);
+  SAG_LAUNCHED(c);
+}
+void launch_sum(Ctx& c, int n, const double* a, const Fin& fin) {
+  sum_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, a, fin, c.partials.p, c.ticket.p);
+  SAG_LAUNCHED(c);
+}
+void launch_div(Ctx& c, int n, const double* x, const double* s, double* y, const int* gate,
+                const int* gate2) {
+  div_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, s, y, gate, gate2);
+  SAG_LAUNCHED(c);
+}
+void launch_mgs(Ctx& c, int n, double* w, const double* vprev, const double* h,
+                const double* vnext, const Fin& fin, const int* gate) {
+  mgs_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, w, vprev, h, vnext, fin, gate,
+                                                      c.partials.p, c.ticket.p);
+  SAG_LAUNCHED(c);
+}
+void launch_mgs_last(Ctx& c, int n, double* w, const double* v, const double* h, const Fin& fin,
+                     const int* gate) {
+  mgs_last_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, w, v, h, fin, gate, c.partials.p,
+                                                           c.ticket.p);
+  SAG_LAUNCHED(c);
+}
+void launch_backsub(Ctx& c, KState* st) {
+  backsub_kernel<<<1, 1, 0, c.stream>>>(st);
+  SAG_LAUNCHED(c);
+}
+void launch_update(Ctx& c, int n, double* x, const double* Z, size_t zstride, KState* st,
+                   bool store) {
+  update_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, Z, zstride, st, store ? 1 : 0);
+  SAG_LAUNCHED(c);
+}
+void launch_mul(Ctx& c, int n, const double* a, const double* b, double* y) {
+  mul_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, a, b, y);
+  SAG_LAUNCHED(c);
+}
+void launch_inv_diag(Ctx& c, const Matrix& m, double* dinv, int* bad) {
+  inv_diag_kernel<<<ew_grid(c, m.nrows), 256, 0, c.stream>>>(m.nrows, m.rp.p, m.ci.p, m.v.p, dinv,
+                                                             bad);
+  SAG_LAUNCHED(c);
+}
+void launch_kinit(Ctx& c, KState* st, int m, double tol, double bd, int hist_cap,
+                  bool keep_ref) {
+  kinit_kernel<<<1, 1, 0, c.stream>>>(st, m, tol, bd, hist_cap, keep_ref ? 1 : 0);
+  SAG_LAUNCHED(c);
+}
+void launch_copy(Ctx& c, int n, const double* x, double* y) {
+  copy_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, y);
+  SAG_LAUNCHED(c);
+}
+void launch_zero(Ctx& c, int n, double* y) {
+  zero_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, y);
+  SAG_LAUNCHED(c);
+}
+void launch_project(Ctx& c, int n, int n_u, const double* x, const double* mean, double* y) {
+  project_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, n_u, x, mean, y);
+  SAG_LAUNCHED(c);
+}
+void launch_eta(Ctx& c, int n, int n_u, double eta_u, double eta_p, const double* x, double* y) {
+  eta_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, n_u, eta_u, eta_p, x, y);
+  SAG_LAUNCHED(c);
+}
+void launch_add(Ctx& c, int n, double* x, const double* y) {
+  add_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, y);
+  SAG_LAUNCHED(c);
+}
+void launch_axpy(Ctx& c, int n, double* x, double omega, const double* d) {
+  axpy_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, omega, d);
+  SAG_LAUNCHED(c);
+}
+
+// ---------------------------------------------------- matrix validation --
+
+__global__ void validate_csr_kernel(int nrows, int ncols, long long nnz, const int* rp,
+                                    const int* ci, int* bad) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const int b = rp[r], e = rp[r + 1];
+    if (b > e || b < 0 || (long long)e > nnz) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    for (int k = b; k < e; ++k) {
+      const int c = ci[k];
+      if (c < 0 || c >= ncols) atomicOr(bad, 2);
+      if (k > b && c <= ci[k - 1]) atomicOr(bad, 4);
+    }
+  }
+}
+
+__global__ void norm_inf_kernel(int nrows, const int* rp, const double* v, double* out) {
+  __shared__ double sh[32];
+  double best = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = rp[r]; k < rp[r + 1]; ++k) s += fabs(v[k]);
+    best = fmax(best, s);
+  }
+  // max-reduce in one block (gridDim.x == 1)
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) b = fmax(b, sh[i]);
+    *out = b;
+  }
+}
+
+void compute_norm_inf(Ctx& c, Matrix& m) {
+  if (m.norm_inf >= 0.0) return;
+  norm_inf_kernel<<<1, 1024, 0, c.stream>>>(m.nrows, m.rp.p, m.v.p, c.scal.p);
+  SAG_LAUNCHED(c);
+  SAG_CUDA(cudaMemcpyAsync(&m.norm_inf, c.scal.p, sizeof(double), cudaMemcpyDeviceToHost,
+                           c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+// ------------------------------------------------------------ transpose --
+
+__global__ void row_of_kernel(int nrows, const int* rp, int* row_of) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x)
+    for (int k = rp[r]; k < rp[r + 1]; ++k) row_of[k] = r;
+}
+__global__ void iota_kernel(long long n, int* a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = (int)i;
+}
+__global__ void count_kernel(long long n, const int* key, int* cnt) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    atomicAdd(cnt + key[i], 1);
+}
+__global__ void permute_kernel(long long n, const int* perm, const int* row_of, const double* v,
+                               int* ciT, double* vT) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int o = perm[q];
+    ciT[q] = row_of[o];
+    vT[q] = v[o];
+  }
+}
+
+static int pick_group(long long nnz, int nrows) {
+  if (const char* e = getenv("SAG_SPMV_GROUP")) return atoi(e);
+  const double avg = nrows > 0 ? (double)nnz / nrows : 0.0;
+  if (avg <= 3.0) return 2;
+  if (avg <= 8.0) return 4;
+  if (avg <= 24.0) return 8;
+  if (avg <= 48.0) return 16;
+  return 32;
+}
+
+std::unique_ptr<Matrix> transpose_dev(Ctx& c, const Matrix& a) {
+  auto t = std::make_unique<Matrix>();
+  t->ctx = &c;
+  t->nrows = a.ncols;
+  t->ncols = a.nrows;
+  t->nnz = a.nnz;
+  t->rp.alloc(a.ncols + 1);
+  t->ci.alloc(a.nnz);
+  t->v.alloc(a.nnz);
+  const long long n = a.nnz;
+  DevBuf<int> row_of(n), idx(n), keys_out(n), perm(n), cnt(a.ncols + 1);
+  const int g = ew_grid(c, n);
+  row_of_kernel<<<ew_grid(c, a.nrows), 256, 0, c.stream>>>(a.nrows, a.rp.p, row_of.p);
+  SAG_LAUNCHED(c);
+  iota_kernel<<<g, 256, 0, c.stream>>>(n, idx.p);
+  SAG_LAUNCHED(c);
+  SAG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (a.ncols + 1), c.stream));
+  count_kernel<<<g, 256, 0, c.stream>>>(n, a.ci.p, cnt.p);
+  SAG_LAUNCHED(c);
+  size_t tmp = 0, tmp2 = 0;
+  SAG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.p, t->rp.p, a.ncols + 1, c.stream));
+  SAG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, a.ci.p, keys_out.p, idx.p, perm.p,
+                                           (int)n, 0, 32, c.stream));
+  DevBuf<unsigned char> ws(std::max(tmp, tmp2));
+  SAG_CUDA(cub::DeviceScan::ExclusiveSum(ws.p, tmp, cnt.p, t->rp.p, a.ncols + 1, c.stream));
+  SAG_CUDA(cub::DeviceRadixSort::SortPairs(ws.p, tmp2, a.ci.p, keys_out.p, idx.p, perm.p,
+                                           (int)n, 0, 32, c.stream));
+  permute_kernel<<<g, 256, 0, c.stream>>>(n, perm.p, row_of.p, a.v.p, t->ci.p, t->v.p);
+  SAG_LAUNCHED(c);
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  t->group = pick_group(t->nnz, t->nrows);
+  return t;
+}
+
+std::unique_ptr<Matrix> matrix_upload(Ctx& c, int nrows, int ncols, long long nnz,
+                                      const int* rp, const int* ci, const double* v) {
+  SAG_REQUIRE(nrows >= 0 && ncols >= 0 && nnz >= 0, SAG_DIMENSION_MISMATCH,
+              "sag_matrix_create: negative size");
+  SAG_REQUIRE(nnz < (1LL << 31), SAG_DIMENSION_MISMATCH, "sag_matrix_create: nnz exceeds int32");
+  SAG_REQUIRE(rp && (nnz == 0 || (ci && v)), SAG_INVALID_ARGUMENT, "sag_matrix_create: null array");
+  auto m = std::make_unique<Matrix>();
+  m->ctx = &c;
+  m->nrows = nrows;
+  m->ncols = ncols;
+  m->nnz = nnz;
+  m->rp.alloc(nrows + 1);
+  m->ci.alloc(nnz);
+  m->v.alloc(nnz);
+  SAG_CUDA(cudaMemcpyAsync(m->rp.p, rp, sizeof(int) * (nrows + 1), cudaMemcpyDefault, c.stream));
+  if (nnz) {
+    SAG_CUDA(cudaMemcpyAsync(m->ci.p, ci, sizeof(int) * nnz, cudaMemcpyDefault, c.stream));
+    SAG_CUDA(cudaMemcpyAsync(m->v.p, v, sizeof(double) * nnz, cudaMemcpyDefault, c.stream));
+  }
+  int* bad = reinterpret_cast<int*>(c.scal.p);
+  SAG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+  validate_csr_kernel<<<ew_grid(c, nrows), 256, 0, c.stream>>>(nrows, ncols, nnz, m->rp.p,
+                                                               m->ci.p, bad);
+  SAG_LAUNCHED(c);
+  int hb = 0, first = 0, last = 0;
+  SAG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaMemcpyAsync(&first, m->rp.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaMemcpyAsync(&last, m->rp.p + nrows, sizeof(int), cudaMemcpyDeviceToHost,
+                           c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  SAG_REQUIRE(first == 0 && last == nnz, SAG_DIMENSION_MISMATCH,
+              "sag_matrix_create: row_offsets do not span [0, nnz]");
+  SAG_REQUIRE(!(hb & 1), SAG_DIMENSION_MISMATCH, "sag_matrix_create: row_offsets not monotone");
+  SAG_REQUIRE(!(hb & 2), SAG_DIMENSION_MISMATCH, "sag_matrix_create: column index out of range");
+  SAG_REQUIRE(!(hb & 4), SAG_ERROR,
+              "sag_matrix_create: rows must be canonical (strictly increasing columns)");
+  m->group = pick_group(nnz, nrows);
+  return m;
+}
+
+}  // namespace sag
+
+// =================================================================== C-ABI
+
+using sag::Ctx;
+
+namespace {
+thread_local std::string g_last_error;
+}
+namespace sag {
+void set_last_error(const std::string& s) { g_last_error = s; }
+}  // namespace sag
+using sag::guard;
+#define NOTNULL SAG_NOTNULL
+
+extern "C" {
+
+const char* sag_last_error(void) { return g_last_error.c_str(); }
+
+int sag_create(int device, sag_ctx** out) {
+  return guard([&] {
+    NOTNULL(out);
+    *out = nullptr;
+    int ndev = 0;
+    SAG_CUDA(cudaGetDeviceCount(&ndev));
+    SAG_REQUIRE(device >= 0 && device < ndev, SAG_CUDA_ERROR, "sag_create: no such CUDA device");
+    cudaDeviceProp prop;
+    SAG_CUDA(cudaGetDeviceProperties(&prop, device));
+    SAG_REQUIRE(prop.major == 10, SAG_CUDA_ERROR,
+                std::string("sag_create: libsag is built for sm_100a, device is ") + prop.name);
+    SAG_CUDA(cudaSetDevice(device));
+    auto* h = new sag_ctx;
+    h->c.device = device;
+    h->c.num_sms = prop.multiProcessorCount;
+    SAG_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+    h->c.partials.alloc(sag::kMaxRedGrid * 2);
+    h->c.ticket.alloc(64);
+    SAG_CUDA(cudaMemset(h->c.ticket.p, 0, sizeof(unsigned) * 64));
+    h->c.scal.alloc(64);
+    *out = h;
+  });
+}
+
+int sag_destroy(sag_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+  });
+}
+
+int sag_synchronize(sag_ctx* ctx) {
+  return guard([&] {
+    NOTNULL(ctx);
+    SAG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sag_alloc(sag_ctx* ctx, size_t bytes, void** dptr) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(dptr);
+    SAG_CUDA(cudaSetDevice(ctx->c.device));
+    SAG_CUDA(cudaMalloc(dptr, bytes ? bytes : 1));
+  });
+}
+
+int sag_free(sag_ctx* ctx, void* dptr) {
+  return guard([&] {
+    NOTNULL(ctx);
+    SAG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    SAG_CUDA(cudaFree(dptr));
+  });
+}
+
+int sag_memcpy(sag_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  return guard([&] {
+    NOTNULL(ctx);
+    SAG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->c.stream));
+    SAG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sag_launch_count(sag_ctx* ctx, long long* out) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(out);
+    *out = ctx->c.launches;
+  });
+}
+
+int sag_stream(sag_ctx* ctx, void** stream) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(stream);
+    *stream = (void*)ctx->c.stream;
+  });
+}
+
+int sag_matrix_create(sag_ctx* ctx, int nrows, int ncols, long long nnz, const int* row_offsets,
+                      const int* col_indices, const double* values, sag_matrix** out) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(out);
+    *out = nullptr;
+    auto m = sag::matrix_upload(ctx->c, nrows, ncols, nnz, row_offsets, col_indices, values);
+    auto* h = new sag_matrix;
+    h->m = std::move(*m);
+    *out = h;
+  });
+}
+
+int sag_matrix_destroy(sag_matrix* m) {
+  return guard([&] { delete m; });
+}
+
+int sag_matrix_shape(const sag_matrix* m, int* nrows, int* ncols, long long* nnz) {
+  return guard([&] {
+    NOTNULL(m);
+    if (nrows) *nrows = m->m.nrows;
+    if (ncols) *ncols = m->m.ncols;
+    if (nnz) *nnz = m->m.nnz;
+  });
+}
+
+int sag_spmv(sag_ctx* ctx, const sag_matrix* m, const double* x, double* y) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(m);
+    auto& c = ctx->c;
+    sag::InVec xi(c, x, m->m.ncols, 0);
+    sag::OutVec yo(c, y, m->m.nrows, 1, false);
+    sag::launch_spmv(c, m->m, xi.d, yo.d, sag::Epi::Store);
+    yo.finish();
+  });
+}
+
+int sag_norm2(sag_ctx* ctx, int n, const double* v, double* out) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(out);
+    auto& c = ctx->c;
+    sag::InVec vi(c, v, n, 0);
+    sag::Fin f;
+    f.kind = sag::FIN_SQRT;
+    f.out = c.scal.p;
+    sag::launch_ssq(c, n, vi.d, f);
+    SAG_CUDA(cudaMemcpyAsync(out, c.scal.p, sizeof(double), cudaMemcpyDefault, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sag_dot(sag_ctx* ctx, int n, const double* a, const double* b, double* out) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(out);
+    auto& c = ctx->c;
+    sag::InVec ai(c, a, n, 0);
+    sag::InVec bi(c, b, n, 1);
+    sag::Fin f;
+    f.kind = sag::FIN_STORE;
+    f.out = c.scal.p;
+    sag::launch_dot(c, n, ai.d, bi.d, f);
+    SAG_CUDA(cudaMemcpyAsync(out, c.scal.p, sizeof(double), cudaMemcpyDefault, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

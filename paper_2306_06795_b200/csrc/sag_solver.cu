@@ -1,0 +1,1141 @@
+// libsag solver module: device-resident FGMRES (krylov.cpp:17-121),
+// Krylov-wrapped / stationary Vanka relaxation (vanka.cpp:186-209), coarse
+// dense solve, the monolithic V-cycle (preconditioner.cpp:40-88), the
+// defect-correction preconditioner (preconditioner.cpp:90-153) and
+// solve_stokes (preconditioner.cpp:229-259), plus their C-ABI.
+//
+// All vectors and all Krylov scalars (Hessenberg matrix, Givens rotations,
+// residual estimates) stay on the device; a preconditioner application is a
+// fixed sequence of kernel launches with no host synchronisation (captured
+// once into a CUDA graph). The outer solve reads one small status record per
+// Arnoldi step to decide convergence, as krylov.cpp:95-97 does.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace sag {
+
+// ================================================================ Krylov ==
+
+struct Krylov {
+  int n = 0, m = 0, hist_cap = 0;
+  DevBuf<double> V, Z, w, r;
+  DevBuf<unsigned char> stbuf;
+  KState* st = nullptr;
+  void init(int n_, int m_, int hist_cap_) {
+    n = n_;
+    m = std::max(m_, 1);
+    hist_cap = hist_cap_;
+    V.alloc((size_t)(m + 1) * n);
+    Z.alloc((size_t)m * n);
+    w.alloc(n);
+    r.alloc(n);
+    stbuf.alloc(kstate_bytes(m, hist_cap));
+    SAG_CUDA(cudaMemset(stbuf.p, 0, stbuf.n));
+    st = reinterpret_cast<KState*>(stbuf.p);
+  }
+  double* v(int i) { return V.p + (size_t)i * n; }
+  double* z(int i) { return Z.p + (size_t)i * n; }
+  // device address of h[i*mm + j] for restart length mm (address arithmetic only)
+  double* h(int mm, int i, int j) { return ks_h(st) + (size_t)i * mm + j; }
+  const int* stop() { return &st->stop; }
+  const int* breakdown() { return &st->breakdown; }
+  const double* beta() { return &st->beta; }
+  const double* wnorm() { return &st->wnorm; }
+};
+
+// Arnoldi step j with z_j already in K.z(j) (krylov.cpp:61-100):
+//   w = A z_j fused with h_0j = (w, v_0)
+//   MGS: w -= h_(i-1)j v_(i-1) fused with h_ij = (w, v_i), i = 1..j
+//   w -= h_jj v_j fused with ||w||^2 -> Givens + residual estimate (finisher)
+//   v_(j+1) = w / ||w|| unless breakdown
+static void arnoldi_step(Ctx& c, const Matrix& A, Krylov& K, int mm, int j, const int* gate) {
+  const int n = K.n;
+  {
+    SpmvArgs a;
+    a.dotv = K.v(0);
+    a.gate = gate;
+    a.fin.kind = FIN_H;
+    a.fin.st = K.st;
+    a.fin.i = 0;
+    a.fin.j = j;
+    launch_spmv(c, A, K.z(j), K.w.p, Epi::StoreDot, a);
+  }
+  for (int i = 1; i <= j; ++i) {
+    Fin f;
+    f.kind = FIN_H;
+    f.st = K.st;
+    f.i = i;
+    f.j = j;
+    launch_mgs(c, n, K.w.p, K.v(i - 1), K.h(mm, i - 1, j), K.v(i), f, gate);
+  }
+  Fin f;
+  f.kind = FIN_ARNOLDI;
+  f.st = K.st;
+  f.j = j;
+  launch_mgs_last(c, n, K.w.p, K.v(j), K.h(mm, j, j), f, gate);
+  launch_div(c, n, K.w.p, K.wnorm(), K.v(j + 1), gate, K.breakdown());
+}
+
+// vanka_relax, KrylovWrapped (vanka.cpp:199-208): x += FGMRES_nu(K, b - K x;
+// M = apply_vanka, tol 0, restart = max_iters = nu, zero inner guess).
+// x_zero: x is known to be zero, so r = b and x = corr (the reference's
+// spmv of a zero vector is exactly zero).
+static void relax_kw(Ctx& c, const Matrix& K, const Vanka& f, Krylov& kr, double* x,
+                     const double* b, int nu, bool x_zero) {
+  if (nu <= 0) {
+    if (x_zero) launch_zero(c, K.nrows, x);
+    return;
+  }
+  const int n = K.nrows;
+  Fin fb;
+  fb.kind = FIN_BETA;
+  fb.st = kr.st;
+  fb.i = 1 | 4;  // ref = ||r|| (b of the inner solve), full (re)init with m = nu
+  fb.j = nu;
+  fb.tol = 0.0;
+  const double* r;
+  if (x_zero) {
+    launch_ssq(c, n, b, fb);
+    r = b;
+  } else {
+    SpmvArgs a;
+    a.b = b;
+    a.fin = fb;
+    launch_spmv(c, K, x, kr.r.p, Epi::ResidSsq, a);
+    r = kr.r.p;
+  }
+  launch_div(c, n, r, kr.beta(), kr.v(0), kr.stop());
+  for (int j = 0; j < nu; ++j) {
+    vanka_apply(c, f, kr.v(j), kr.z(j), kr.stop());
+    arnoldi_step(c, K, kr, nu, j, kr.stop());
+  }
+  launch_backsub(c, kr.st);
+  launch_update(c, n, x, kr.Z.p, (size_t)n, kr.st, x_zero);
+}
+
+// vanka_relax, Stationary (vanka.cpp:190-197): x += omega * vanka(b - K x).
+static void relax_stationary(Ctx& c, const Matrix& K, const Vanka& f, double* rbuf, double* x,
+                             const double* b, int sweeps, double omega, bool x_zero) {
+  if (x_zero) launch_zero(c, K.nrows, x);
+  for (int s = 0; s < sweeps; ++s) {
+    const double* r = b;
+    if (!(s == 0 && x_zero)) {
+      SpmvArgs a;
+      a.b = b;
+      launch_spmv(c, K, x, rbuf, Epi::Resid, a);
+      r = rbuf;
+    }
+    vanka_apply_stationary(c, f, r, x, omega);
+  }
+}
+
+struct KHeader {
+  double ref, tol, bd, beta, rnorm, wnorm;
+  int m, stop, breakdown, jeff, iterations, hist_len, hist_cap, converged;
+};
+static_assert(sizeof(KHeader) == sizeof(KState), "KState layout");
+
+static KHeader read_header(Ctx& c, KState* st) {
+  KHeader h;
+  SAG_CUDA(cudaMemcpyAsync(&h, st, sizeof(KHeader), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  return h;
+}
+
+struct FgmresOut {
+  int converged = 0, iterations = 0;
+  double final_rel = 0.0;
+  std::vector<double> hist;
+};
+
+using DevOp = std::function<void(const double* in, double* out)>;
+
+// fgmres (krylov.cpp:17-121) with A = K, right preconditioner `prec`, x in/out
+// on device. One host synchronisation per Arnoldi step.
+static FgmresOut fgmres_dev(Ctx& c, const Matrix& A, const double* b, double* x, const DevOp& prec,
+                            double tol, int max_iters, int restart, double bd, Krylov& K) {
+  const int n = A.nrows;
+  SAG_REQUIRE(restart >= 1 && K.m >= restart && K.n == n, SAG_CONFIG_ERROR,
+              "fgmres: workspace does not match restart / size");
+  launch_kinit(c, K.st, restart, tol, bd, K.hist_cap, false);
+  {
+    Fin f;
+    f.kind = FIN_REF;
+    f.st = K.st;
+    launch_ssq(c, n, b, f);  // bnorm, ref (krylov.cpp:23-24)
+  }
+  FgmresOut out;
+  // initial residual (krylov.cpp:26-35): history[0]
+  {
+    SpmvArgs a;
+    a.b = b;
+    a.fin.kind = FIN_BETA;
+    a.fin.st = K.st;
+    a.fin.i = 2;
+    launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
+  }
+  KHeader hd = read_header(c, K.st);
+  int iters = 0;
+  bool converged = hd.stop != 0;
+  while (!converged && iters < max_iters) {
+    // (re)start from the true residual (krylov.cpp:43-53)
+    SpmvArgs a;
+    a.b = b;
+    a.fin.kind = FIN_BETA;
+    a.fin.st = K.st;
+    a.fin.i = 0;
+    launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
+    hd = read_header(c, K.st);
+    if (hd.stop) {
+      converged = true;
+      break;
+    }
+    launch_div(c, n, K.r.p, K.beta(), K.v(0), K.stop());
+    for (int j = 0; j < restart && iters < max_iters; ++j) {
+      prec(K.v(j), K.z(j));
+      arnoldi_step(c, A, K, restart, j, K.stop());
+      hd = read_header(c, K.st);
+      iters = hd.iterations;
+      if (hd.stop) break;
+    }
+    launch_backsub(c, K.st);
+    launch_update(c, n, x, K.Z.p, (size_t)n, K.st, false);
+    hd = read_header(c, K.st);
+    if (hd.converged) converged = true;
+  }
+  // final true residual (krylov.cpp:116-119)
+  {
+    SpmvArgs a;
+    a.b = b;
+    a.fin.kind = FIN_FINAL;
+    a.fin.st = K.st;
+    a.fin.out = c.scal.p;
+    launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
+  }
+  hd = read_header(c, K.st);
+  SAG_CUDA(cudaMemcpyAsync(&out.final_rel, c.scal.p, sizeof(double), cudaMemcpyDeviceToHost,
+                           c.stream));
+  out.iterations = hd.iterations;
+  out.converged = hd.converged;
+  const int hl = std::min(hd.hist_len, K.hist_cap);
+  out.hist.resize(hl);
+  if (hl)
+    SAG_CUDA(cudaMemcpyAsync(out.hist.data(), ks_h(K.st) + (size_t)(restart + 1) * restart +
+                                                  restart + restart + (restart + 1) + restart,
+                             sizeof(double) * hl, cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  return out;
+}
+
+// ========================================================== coarse solve ==
+// MonolithicSolver coarse level (preconditioner.cpp:47-54, :60-63): dense LU
+// with partial pivoting of to_dense(K_L) (+ enclosed-flow pin), factorised on
+// the device with the reference's elimination order. The solve applies the
+// explicit inverse (columns = dense_lu_solve(lu, e_c)) as one coalesced dense
+// mat-vec; SAG_COARSE=lu selects a row-oriented triangular solve instead.
+
+__global__ void dense_scatter_kernel(int n, const int* rp, const int* ci, const double* v,
+                                     double* A) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    for (int k = rp[r]; k < rp[r + 1]; ++k) A[(size_t)r * n + ci[k]] += v[k];
+}
+
+__global__ void pin_kernel(double* A, int n, int row, double pin) {
+  A[(size_t)row * n + row] += pin;
+}
+
+// sparse.cpp:310-341 by one CTA on a row-major matrix in global memory.
+__global__ void __launch_bounds__(1024) dense_lu_kernel(int n, double* A, int* piv, int* err) {
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  __shared__ int sp;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x;
+  for (int i = tid; i < n; i += nt) piv[i] = i;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    double bv = -1.0;
+    int bi = n;
+    for (int i = k + 1 + tid; i < n; i += nt) {
+      const double v = fabs(A[(size_t)i * n + k]);
+      if (v > bv) {
+        bv = v;
+        bi = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      sv[wid] = bv;
+      si[wid] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double b = -1.0;
+      int bidx = n;
+      for (int w = 0; w < (nt >> 5); ++w)
+        if (sv[w] > b || (sv[w] == b && si[w] < bidx)) {
+          b = sv[w];
+          bidx = si[w];
+        }
+      const double akk = fabs(A[(size_t)k * n + k]);
+      int p = (b > akk) ? bidx : k;
+      const double best = (b > akk) ? b : akk;
+      if (best == 0.0) {
+        *err = 1;
+        p = -1;
+      }
+      sp = p;
+    }
+    __syncthreads();
+    const int p = sp;
+    if (p < 0) return;
+    if (p != k) {
+      for (int j = tid; j < n; j += nt) {
+        const double t = A[(size_t)k * n + j];
+        A[(size_t)k * n + j] = A[(size_t)p * n + j];
+        A[(size_t)p * n + j] = t;
+      }
+      if (tid == 0) {
+        const int t = piv[k];
+        piv[k] = piv[p];
+        piv[p] = t;
+      }
+    }
+    __syncthreads();
+    const double inv = __ddiv_rn(1.0, A[(size_t)k * n + k]);
+    for (int i = k + 1 + tid; i < n; i += nt) A[(size_t)i * n + k] = __dmul_rn(A[(size_t)i * n + k], inv);
+    __syncthreads();
+    const int m = n - k - 1;
+    for (long long e = tid; e < (long long)m * m; e += nt) {
+      const int i = k + 1 + (int)(e / m), j = k + 1 + (int)(e % m);
+      const double mult = A[(size_t)i * n + k];
+      if (mult != 0.0) A[(size_t)i * n + j] = __dsub_rn(A[(size_t)i * n + j], __dmul_rn(mult, A[(size_t)k * n + j]));
+    }
+    __syncthreads();
+  }
+}
+
+// inverse columns: thread c solves e_c with the reference's substitution order
+__global__ void dense_inv_kernel(int n, const double* LU, const int* piv, double* X,
+                                 double* Ainv) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double* x = X + (size_t)c * n;
+  for (int i = 0; i < n; ++i) x[i] = piv[i] == c ? 1.0 : 0.0;
+  for (int i = 1; i < n; ++i) {
+    double acc = x[i];
+    for (int j = 0; j < i; ++j) acc = __dsub_rn(acc, __dmul_rn(LU[(size_t)i * n + j], x[j]));
+    x[i] = acc;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double acc = x[i];
+    for (int j = i + 1; j < n; ++j) acc = __dsub_rn(acc, __dmul_rn(LU[(size_t)i * n + j], x[j]));
+    x[i] = __ddiv_rn(acc, LU[(size_t)i * n + i]);
+  }
+  for (int i = 0; i < n; ++i) Ainv[(size_t)i * n + c] = x[i];
+}
+
+// x = Ainv b, one warp per row
+__global__ void dense_matvec_kernel(int n, const double* __restrict__ A,
+                                    const double* __restrict__ b, double* __restrict__ x) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const double* row = A + (size_t)warp * n;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32) s = fma(row[j], b[j], s);
+  s = warp_sum(s);
+  if (lane == 0) x[warp] = s;
+}
+
+// dense_lu_solve (sparse.cpp:343-369) by one warp: row-oriented sweeps, the
+// per-row dot products as warp trees.
+__global__ void dense_lu_solve_kernel(int n, const double* __restrict__ LU,
+                                      const int* __restrict__ piv, const double* __restrict__ b,
+                                      double* __restrict__ x) {
+  const int lane = threadIdx.x;
+  for (int i = lane; i < n; i += 32) x[i] = b[piv[i]];
+  __syncwarp();
+  for (int i = 1; i < n; ++i) {
+    double s = 0.0;
+    for (int j = lane; j < i; j += 32) s = fma(LU[(size_t)i * n + j], x[j], s);
+    s = warp_sum(s);
+    if (lane == 0) x[i] = x[i] - s;
+    __syncwarp();
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int j = i + 1 + lane; j < n; j += 32) s = fma(LU[(size_t)i * n + j], x[j], s);
+    s = warp_sum(s);
+    if (lane == 0) x[i] = (x[i] - s) / LU[(size_t)i * n + i];
+    __syncwarp();
+  }
+}
+
+struct Coarse {
+  int n = 0;
+  bool use_inv = true;
+  DevBuf<double> lu, inv;
+  DevBuf<int> piv;
+  void setup(Ctx& c, const Matrix& K, int pin_row, double pin) {
+    n = K.nrows;
+    SAG_REQUIRE(n == K.ncols && n > 0, SAG_DIMENSION_MISMATCH, "coarse level must be square");
+    SAG_REQUIRE(n <= 8192, SAG_ERROR, "coarse level too large for the dense solve");
+    if (const char* e = getenv("SAG_COARSE")) use_inv = std::strcmp(e, "lu") != 0;
+    lu.alloc((size_t)n * n);
+    piv.alloc(n);
+    SAG_CUDA(cudaMemsetAsync(lu.p, 0, sizeof(double) * n * n, c.stream));
+    dense_scatter_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(n, K.rp.p, K.ci.p, K.v.p, lu.p);
+    SAG_LAUNCHED(c);
+    if (pin_row >= 0) {
+      pin_kernel<<<1, 1, 0, c.stream>>>(lu.p, n, pin_row, pin);
+      SAG_LAUNCHED(c);
+    }
+    DevBuf<int> err(1);
+    SAG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
+    dense_lu_kernel<<<1, 1024, 0, c.stream>>>(n, lu.p, piv.p, err.p);
+    SAG_LAUNCHED(c);
+    int herr = 0;
+    SAG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    if (herr) throw Error(SAG_SINGULAR_MATRIX, "dense_lu_factor: singular pivot column (coarse level)");
+    if (use_inv) {
+      inv.alloc((size_t)n * n);
+      DevBuf<double> X((size_t)n * n);
+      dense_inv_kernel<<<(n + 63) / 64, 64, 0, c.stream>>>(n, lu.p, piv.p, X.p, inv.p);
+      SAG_LAUNCHED(c);
+      SAG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+  }
+  void solve(Ctx& c, const double* b, double* x) {
+    if (use_inv) {
+      dense_matvec_kernel<<<(n * 32 + 255) / 256, 256, 0, c.stream>>>(n, inv.p, b, x);
+    } else {
+      dense_lu_solve_kernel<<<1, 32, 0, c.stream>>>(n, lu.p, piv.p, b, x);
+    }
+    SAG_LAUNCHED(c);
+  }
+};
+
+// ==================================================== monolithic solver ==
+
+struct Level {
+  const Matrix* K = nullptr;
+  const Matrix* P = nullptr;
+  std::unique_ptr<Matrix> R;  // P^T, built once (the reference rebuilds it per call, :72)
+  int n_x = 0, n_y = 0, n_p = 0, n = 0;
+  std::unique_ptr<Vanka> vanka;
+  Krylov kry;
+  DevBuf<double> b, x, r;
+};
+
+// SV transfer pieces (transfer.cpp:18-53): duplication P^p, mixed mass M_mix,
+// Mcg with its scalar SA hierarchy (amg.cpp:231-296).
+struct SvTransfer {
+  const Matrix* pdup = nullptr;
+  const Matrix* mmix = nullptr;
+  std::vector<const Matrix*> A;  // scalar levels
+  std::vector<const Matrix*> P;
+  std::vector<std::unique_ptr<Matrix>> R;
+  std::vector<DevBuf<double>> dinv, sb, sx, sr;
+  std::vector<Krylov> kr;        // Jacobi-FGMRES(2) smoothing workspaces
+  Coarse coarse;
+  Krylov outer;                  // FGMRES(20) on Mcg
+  DevBuf<double> rhs, pcg;
+  std::vector<int> iterations;
+};
+
+struct Dc {
+  Ctx* ctx = nullptr;
+  const Matrix* K0 = nullptr;
+  int n_x0 = 0, n_y0 = 0, n_p0 = 0, n0 = 0;
+  bool sv = false;
+  sag_solver_config cfg{};
+  std::unique_ptr<Vanka> fine;
+  Krylov fine_kry;
+  DevBuf<double> fine_r;
+  std::vector<Level> lv;
+  Coarse coarse;
+  std::unique_ptr<SvTransfer> svt;
+  long long fine_units = 0, l1_units = 0;
+  // outer solve workspace
+  Krylov outer;
+  DevBuf<double> din, dout;
+  DevBuf<double> gam_rc, gam_e;  // gamma > 1 accumulators
+  // CUDA graph of apply(din -> dout)
+  cudaGraphExec_t graph = nullptr;
+  bool graph_ok = false;
+  long long graph_launches = 0;
+  ~Dc() {
+    if (graph) cudaGraphExecDestroy(graph);
+  }
+};
+
+// MonolithicSolver::cycle_level (preconditioner.cpp:57-81) on lv[l]:
+// input lv[l].b, output lv[l].x (from a zero guess).
+static void cycle_level(Ctx& c, Dc& d, int l, int nu1, int nu2, bool skip_finest) {
+  Level& L = d.lv[l];
+  const int nl = (int)d.lv.size();
+  if (l == nl - 1) {
+    d.coarse.solve(c, L.b.p, L.x.p);
+    return;
+  }
+  const bool relax_here = !(l == 0 && skip_finest);
+  const bool pre = relax_here && nu1 > 0;
+  if (pre)
+    relax_kw(c, *L.K, *L.vanka, L.kry, L.x.p, L.b.p, nu1, true);
+  else
+    launch_zero(c, L.n, L.x.p);
+  Level& C = d.lv[l + 1];
+  if (pre) {
+    SpmvArgs a;
+    a.b = L.b.p;
+    launch_spmv(c, *L.K, L.x.p, L.r.p, Epi::Resid, a);
+    launch_spmv(c, *L.R, L.r.p, C.b.p, Epi::Store);
+  } else {
+    launch_spmv(c, *L.R, L.b.p, C.b.p, Epi::Store);
+  }
+  cycle_level(c, d, l + 1, nu1, nu2, skip_finest);
+  launch_spmv(c, *L.P, C.x.p, L.x.p, Epi::Add);
+  if (relax_here && nu2 > 0) relax_kw(c, *L.K, *L.vanka, L.kry, L.x.p, L.b.p, nu2, false);
+}
+
+// ---- SV restriction: p_cg = Mcg^-1 (M_mix p_dg) (transfer.cpp:18-37) ------
+
+// scalar_vcycle (amg.cpp:258-296) on level l of the Mcg hierarchy: FGMRES(2)
+// Jacobi smoothing from the current x, R = P^T, dense coarse solve.
+static void scalar_level(Ctx& c, SvTransfer& t, int l, const double* b, double* x);
+
+static void jacobi_fgmres2(Ctx& c, SvTransfer& t, int l, const double* b, double* x, bool x_zero) {
+  // fgmres(matrix_operator(a), b, x, jacobi, {tol 0, max 2, restart 2}) with x in/out:
+  // bnorm = ||b|| is the reference (krylov.cpp:23-24), the residual b - a x.
+  const Matrix& A = *t.A[l];
+  Krylov& K = t.kr[l];
+  const int n = A.nrows;
+  {
+    Fin f;
+    f.kind = FIN_REF;
+    f.st = K.st;
+    launch_ssq(c, n, b, f);
+  }
+  Fin fb;
+  fb.kind = FIN_BETA;
+  fb.st = K.st;
+  fb.i = 4;  // init m = 2, tol = 0 (ref kept from FIN_REF)
+  fb.j = 2;
+  fb.tol = 0.0;
+  const double* r;
+  if (x_zero) {
+    launch_ssq(c, n, b, fb);
+    r = b;
+  } else {
+    SpmvArgs a;
+    a.b = b;
+    a.fin = fb;
+    launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
+    r = K.r.p;
+  }
+  launch_div(c, n, r, K.beta(), K.v(0), K.stop());
+  for (int j = 0; j < 2; ++j) {
+    launch_mul(c, n, t.dinv[l].p, K.v(j), K.z(j));
+    arnoldi_step(c, A, K, 2, j, K.stop());
+  }
+  launch_backsub(c, K.st);
+  launch_update(c, n, x, K.Z.p, (size_t)n, K.st, x_zero);
+}
+
+static void scalar_level(Ctx& c, SvTransfer& t, int l, const double* b, double* x) {
+  const int nl = (int)t.A.size();
+  if (l == nl - 1) {
+    t.coarse.solve(c, b, x);
+    return;
+  }
+  const Matrix& A = *t.A[l];
+  jacobi_fgmres2(c, t, l, b, x, true);
+  SpmvArgs a;
+  a.b = b;
+  launch_spmv(c, A, x, t.sr[l].p, Epi::Resid, a);
+  launch_spmv(c, *t.R[l], t.sr[l].p, t.sb[l + 1].p, Epi::Store);
+  scalar_level(c, t, l + 1, t.sb[l + 1].p, t.sx[l + 1].p);
+  launch_spmv(c, *t.P[l], t.sx[l + 1].p, x, Epi::Add);
+  jacobi_fgmres2(c, t, l, b, x, false);
+}
+
+static void sv_restrict(Ctx& c, Dc& d, const double* p_dg, double* p_cg) {
+  SvTransfer& t = *d.svt;
+  launch_spmv(c, *t.mmix, p_dg, t.rhs.p, Epi::Store);
+  launch_zero(c, t.mmix->nrows, p_cg);
+  DevOp prec = [&](const double* in, double* out) { scalar_level(c, t, 0, in, out); };
+  FgmresOut o = fgmres_dev(c, *t.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, 20, 1e-30, t.outer);
+  if (!o.converged)
+    throw Error(SAG_SOLVER_STAGNATION,
+                "SvPressureRestrict: mass projection did not reach tolerance in 200 iterations");
+  t.iterations.push_back(o.iterations);
+}
+
+// DCPreconditioner::apply (preconditioner.cpp:114-153), r -> z on device.
+static void dc_apply_dev(Ctx& c, Dc& d, const double* r, double* z) {
+  const sag_solver_config& cf = d.cfg;
+  const bool relax_fine = cf.variant != SAG_DC_LO;
+  const bool pre = relax_fine && cf.nu1 > 0;
+  double* x = z;
+  if (pre) {
+    if (d.sv)
+      relax_stationary(c, *d.K0, *d.fine, d.fine_r.p, x, r, cf.nu1, cf.omega0, true);
+    else
+      relax_kw(c, *d.K0, *d.fine, d.fine_kry, x, r, cf.nu1, true);
+    d.fine_units += cf.nu1;
+  } else {
+    launch_zero(c, d.n0, x);
+  }
+  Level& L0 = d.lv[0];
+  const int n_u0 = d.n_x0 + d.n_y0;
+  // r1 = r - K0 x, eta weighting (transfer.cpp:127-135), TH restriction = copy
+  double* rw = d.sv ? d.fine_r.p : L0.b.p;
+  {
+    SpmvArgs a;
+    a.b = r;
+    a.eta_u = cf.eta_u;
+    a.eta_p = cf.eta_p;
+    a.n_u = n_u0;
+    if (pre)
+      launch_spmv(c, *d.K0, x, rw, Epi::ResidEta, a);
+    else
+      launch_eta(c, d.n0, n_u0, cf.eta_u, cf.eta_p, r, rw);  // r1 = r (preconditioner.cpp:128-129)
+  }
+  const int n_u1 = L0.n_x + L0.n_y;
+  if (d.sv) {
+    // velocity injection + pressure mass projection (transfer.cpp:112-125)
+    launch_copy(c, n_u1, rw, L0.b.p);
+    sv_restrict(c, d, rw + n_u0, L0.b.p + n_u1);
+  }
+  const bool skip_finest = cf.variant == SAG_DC_HO;
+  const int nl = (int)d.lv.size();
+  if (cf.gamma <= 1) {
+    cycle_level(c, d, 0, cf.nu1, cf.nu2, skip_finest);
+  } else {
+    // e accumulates gamma V-cycles (preconditioner.cpp:131-145)
+    DevBuf<double>& rc = d.gam_rc;
+    DevBuf<double>& e = d.gam_e;
+    launch_copy(c, L0.n, L0.b.p, rc.p);
+    launch_zero(c, L0.n, e.p);
+    for (int g = 0; g < cf.gamma; ++g) {
+      if (g > 0) {
+        SpmvArgs a;
+        a.b = rc.p;
+        launch_spmv(c, *L0.K, e.p, L0.b.p, Epi::Resid, a);
+      } else {
+        launch_copy(c, L0.n, rc.p, L0.b.p);
+      }
+      cycle_level(c, d, 0, cf.nu1, cf.nu2, skip_finest);
+      launch_add(c, L0.n, e.p, L0.x.p);
+    }
+    launch_copy(c, L0.n, e.p, L0.x.p);
+  }
+  if (nl > 1 && !skip_finest) d.l1_units += (long long)cf.gamma * (cf.nu1 + cf.nu2);
+  // prolong (transfer.cpp:97-110) and x += up
+  if (!d.sv) {
+    launch_add(c, d.n0, x, L0.x.p);
+  } else {
+    launch_add(c, n_u0, x, L0.x.p);
+    SpmvArgs a;
+    launch_spmv(c, *d.svt->pdup, L0.x.p + n_u1, x + n_u0, Epi::Add, a);
+  }
+  if (relax_fine && cf.nu2 > 0) {
+    if (d.sv)
+      relax_stationary(c, *d.K0, *d.fine, d.fine_r.p, x, r, cf.nu2, cf.omega0, false);
+    else
+      relax_kw(c, *d.K0, *d.fine, d.fine_kry, x, r, cf.nu2, false);
+    d.fine_units += cf.nu2;
+  }
+}
+
+static void check_config(const sag_solver_config& c) {
+  // SolverConfig::check (preconditioner.cpp:30-38)
+  SAG_REQUIRE(c.eta_u > 0.0 && c.eta_p > 0.0, SAG_CONFIG_ERROR, "eta_u and eta_p must be positive");
+  SAG_REQUIRE(c.omega0 > 0.0 && c.omega0 < 2.0, SAG_CONFIG_ERROR, "omega0 must lie in (0, 2)");
+  SAG_REQUIRE(c.nu1 >= 0 && c.nu2 >= 0, SAG_CONFIG_ERROR, "nu1 and nu2 must be non-negative");
+  SAG_REQUIRE(c.gamma >= 1, SAG_CONFIG_ERROR, "gamma must be at least 1");
+  SAG_REQUIRE(c.restart >= 1, SAG_CONFIG_ERROR, "restart must be at least 1");
+  SAG_REQUIRE(c.tol > 0.0, SAG_CONFIG_ERROR, "tol must be positive");
+  SAG_REQUIRE(c.max_iters >= 1, SAG_CONFIG_ERROR, "max_iters must be at least 1");
+  SAG_REQUIRE(c.variant >= 0 && c.variant <= 2, SAG_CONFIG_ERROR, "unknown solver variant");
+}
+
+// DC apply as a CUDA graph over the fixed buffers din -> dout (SV excluded:
+// its mass projection synchronises with the host for convergence).
+static void dc_apply_graph(Ctx& c, Dc& d) {
+  const bool use_graph = !d.sv && !(getenv("SAG_NO_GRAPH") && atoi(getenv("SAG_NO_GRAPH")));
+  if (!use_graph) {
+    dc_apply_dev(c, d, d.din.p, d.dout.p);
+    return;
+  }
+  if (!d.graph_ok) {
+    const long long fu = d.fine_units, lu = d.l1_units, la = c.launches;
+    cudaGraph_t g;
+    SAG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      dc_apply_dev(c, d, d.din.p, d.dout.p);
+    } catch (...) {
+      cudaStreamEndCapture(c.stream, &g);
+      throw;
+    }
+    SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
+    if (d.graph) cudaGraphExecDestroy(d.graph);
+    SAG_CUDA(cudaGraphInstantiate(&d.graph, g, 0));
+    cudaGraphDestroy(g);
+    d.graph_ok = true;
+    d.fine_units = fu;
+    d.l1_units = lu;
+    d.graph_launches = c.launches - la;
+    c.launches = la;
+  }
+  SAG_CUDA(cudaGraphLaunch(d.graph, c.stream));
+  c.launches += d.graph_launches;
+  const sag_solver_config& cf = d.cfg;
+  if (cf.variant != SAG_DC_LO) d.fine_units += cf.nu1 + cf.nu2;
+  if (cf.variant != SAG_DC_HO && d.lv.size() > 1)
+    d.l1_units += (long long)cf.gamma * (cf.nu1 + cf.nu2);
+}
+
+}  // namespace sag
+
+// =================================================================== C-ABI
+using namespace sag;
+
+struct sag_dc {
+  Dc d;
+};
+
+namespace {
+
+void dc_setup(Ctx& c, Dc& d, const Matrix* k0, int n_x0, int n_y0, int n_p0, int sv, int nlevels,
+              const sag_level_desc* levels, const sag_solver_config& cfg) {
+  check_config(cfg);
+  SAG_REQUIRE(nlevels >= 1, SAG_DIMENSION_MISMATCH, "sag_dc_create: empty hierarchy");
+  SAG_REQUIRE(k0->nrows == k0->ncols && k0->nrows == n_x0 + n_y0 + n_p0, SAG_DIMENSION_MISMATCH,
+              "sag_dc_create: K0 does not match its block sizes");
+  d.ctx = &c;
+  d.K0 = k0;
+  d.n_x0 = n_x0;
+  d.n_y0 = n_y0;
+  d.n_p0 = n_p0;
+  d.n0 = k0->nrows;
+  d.sv = sv != 0;
+  d.cfg = cfg;
+  const int mrelax = std::max(std::max(cfg.nu1, cfg.nu2), 1);
+  // fine-level Vanka (preconditioner.cpp:95-97)
+  {
+    auto p = build_patches_dev(c, *k0, n_x0, n_y0, n_p0, d.sv);
+    d.fine = factor_patches_dev(c, *k0, *p);
+  }
+  if (!d.sv) d.fine_kry.init(d.n0, mrelax, 0);
+  d.fine_r.alloc(d.n0);
+  // low-order hierarchy (preconditioner.cpp:40-55)
+  d.lv.resize(nlevels);
+  for (int l = 0; l < nlevels; ++l) {
+    Level& L = d.lv[l];
+    SAG_NOTNULL(levels[l].k);
+    L.K = &levels[l].k->m;
+    L.n_x = levels[l].n_x;
+    L.n_y = levels[l].n_y;
+    L.n_p = levels[l].n_p;
+    L.n = L.K->nrows;
+    SAG_REQUIRE(L.K->ncols == L.n && L.n == L.n_x + L.n_y + L.n_p, SAG_DIMENSION_MISMATCH,
+                "sag_dc_create: level " + std::to_string(l) + " does not match its block sizes");
+    L.b.alloc(L.n);
+    L.x.alloc(L.n);
+    if (l + 1 < nlevels) {
+      SAG_REQUIRE(levels[l].p != nullptr, SAG_DIMENSION_MISMATCH,
+                  "sag_dc_create: missing prolongator on level " + std::to_string(l));
+      L.P = &levels[l].p->m;
+      SAG_REQUIRE(L.P->nrows == L.n && L.P->ncols == levels[l + 1].k->m.nrows,
+                  SAG_DIMENSION_MISMATCH, "sag_dc_create: prolongator shape mismatch");
+      auto p = build_patches_dev(c, *L.K, L.n_x, L.n_y, L.n_p, false);
+      L.vanka = factor_patches_dev(c, *L.K, *p);
+      L.R = transpose_dev(c, *L.P);
+      L.kry.init(L.n, mrelax, 0);
+      L.r.alloc(L.n);
+    }
+  }
+  Level& B = d.lv.back();
+  int pin_row = -1;
+  double pin = 0.0;
+  if (cfg.enclosed_flow) {
+    Matrix& K1 = const_cast<Matrix&>(*d.lv[0].K);
+    compute_norm_inf(c, K1);
+    pin_row = B.n_x + B.n_y;
+    pin = 1e-12 * K1.norm_inf;  // preconditioner.cpp:49-53 (norm of the FINEST level)
+  }
+  d.coarse.setup(c, *B.K, pin_row, pin);
+  if (!d.sv) {
+    SAG_REQUIRE(d.lv[0].n == d.n0 && d.lv[0].n_x + d.lv[0].n_y == n_x0 + n_y0,
+                SAG_DIMENSION_MISMATCH,
+                "DCPreconditioner: transfer does not match the low-order system");
+  } else {
+    SAG_REQUIRE(d.lv[0].n_x + d.lv[0].n_y == n_x0 + n_y0, SAG_DIMENSION_MISMATCH,
+                "DCPreconditioner: transfer does not match the low-order system");
+  }
+  if (cfg.gamma > 1) {
+    d.gam_rc.alloc(d.lv[0].n);
+    d.gam_e.alloc(d.lv[0].n);
+  }
+  d.din.alloc(d.n0);
+  d.dout.alloc(d.n0);
+}
+
+void require_ready(Dc& d) {
+  SAG_REQUIRE(!d.sv || d.svt, SAG_CONFIG_ERROR,
+              "SV preconditioner needs sag_dc_set_sv_transfer before use");
+}
+
+}  // namespace
+
+extern "C" {
+
+int sag_solver_config_default(sag_solver_config* cfg) {
+  return guard([&] {
+    SAG_NOTNULL(cfg);
+    // preconditioner.hpp:20-33
+    cfg->variant = SAG_DC_ALL;
+    cfg->eta_u = 1.0;
+    cfg->eta_p = 1.0;
+    cfg->omega0 = 1.0;
+    cfg->nu1 = 2;
+    cfg->nu2 = 2;
+    cfg->gamma = 1;
+    cfg->restart = 20;
+    cfg->tol = 1e-10;
+    cfg->max_iters = 200;
+    cfg->enclosed_flow = 0;
+  });
+}
+
+int sag_solver_config_check(const sag_solver_config* cfg) {
+  return guard([&] {
+    SAG_NOTNULL(cfg);
+    check_config(*cfg);
+  });
+}
+
+int sag_vanka_relax(sag_ctx* ctx, const sag_matrix* k, const sag_vanka* f, double* x,
+                    const double* b, int mode, int sweeps, double omega) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(k);
+    SAG_NOTNULL(f);
+    auto& c = ctx->c;
+    const int n = k->m.nrows;
+    SAG_REQUIRE(f->f.n == n, SAG_DIMENSION_MISMATCH, "vanka_relax: factorization size mismatch");
+    InVec bi(c, b, n, 0);
+    OutVec xo(c, x, n, 1, true);
+    if (sweeps > 0) {
+      if (mode == SAG_RELAX_STATIONARY) {
+        DevBuf<double> rbuf(n);
+        relax_stationary(c, k->m, f->f, rbuf.p, xo.d, bi.d, sweeps, omega, false);
+      } else {
+        Krylov kr;
+        kr.init(n, sweeps, 0);
+        relax_kw(c, k->m, f->f, kr, xo.d, bi.d, sweeps, false);
+        SAG_CUDA(cudaStreamSynchronize(c.stream));
+      }
+    }
+    xo.finish();
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sag_fgmres(sag_ctx* ctx, const sag_matrix* a, const double* b, double* x, int prec_kind,
+               const void* prec, const sag_fgmres_options* opt, sag_krylov_report* rep,
+               double* history, int history_cap) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(a);
+    SAG_NOTNULL(opt);
+    auto& c = ctx->c;
+    const Matrix& A = a->m;
+    const int n = A.nrows;
+    SAG_REQUIRE(A.ncols == n, SAG_DIMENSION_MISMATCH, "fgmres: operator must be square");
+    SAG_REQUIRE(opt->restart >= 1 && opt->max_iters >= 0, SAG_CONFIG_ERROR,
+                "fgmres: restart must be >= 1");
+    InVec bi(c, b, n, 0);
+    OutVec xo(c, x, n, 1, true);
+    DevBuf<double> dinv;
+    DevOp op;
+    switch (prec_kind) {
+      case SAG_PREC_IDENTITY:
+        op = [&](const double* in, double* out) { launch_copy(c, n, in, out); };
+        break;
+      case SAG_PREC_VANKA: {
+        SAG_NOTNULL(prec);
+        const Vanka& f = static_cast<const sag_vanka*>(prec)->f;
+        SAG_REQUIRE(f.n == n, SAG_DIMENSION_MISMATCH, "fgmres: preconditioner size mismatch");
+        op = [&c, &f](const double* in, double* out) { vanka_apply(c, f, in, out); };
+        break;
+      }
+      case SAG_PREC_JACOBI: {
+        SAG_NOTNULL(prec);
+        const Matrix& D = static_cast<const sag_matrix*>(prec)->m;
+        SAG_REQUIRE(D.nrows == n, SAG_DIMENSION_MISMATCH, "fgmres: preconditioner size mismatch");
+        dinv.alloc(n);
+        int* bad = reinterpret_cast<int*>(c.scal.p + 8);
+        SAG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+        launch_inv_diag(c, D, dinv.p, bad);
+        int hb = 0;
+        SAG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        SAG_CUDA(cudaStreamSynchronize(c.stream));
+        SAG_REQUIRE(!hb, SAG_ERROR, "inv_diagonal: zero diagonal");
+        op = [&](const double* in, double* out) { launch_mul(c, n, dinv.p, in, out); };
+        break;
+      }
+      case SAG_PREC_DC: {
+        SAG_NOTNULL(prec);
+        Dc& d = const_cast<sag_dc*>(static_cast<const sag_dc*>(prec))->d;
+        require_ready(d);
+        SAG_REQUIRE(d.n0 == n, SAG_DIMENSION_MISMATCH, "fgmres: preconditioner size mismatch");
+        op = [&c, &d](const double* in, double* out) { dc_apply_dev(c, d, in, out); };
+        break;
+      }
+      default:
+        throw Error(SAG_CONFIG_ERROR, "fgmres: unknown preconditioner kind");
+    }
+    Krylov K;
+    K.init(n, opt->restart, std::max(history_cap, 1));
+    sag_krylov_report r{};
+    if (opt->max_iters == 0) {
+      // zero iterations: only the initial / final residual (krylov.cpp:26-35, :116)
+    }
+    FgmresOut o = fgmres_dev(c, A, bi.d, xo.d, op, opt->tol, opt->max_iters, opt->restart,
+                             opt->breakdown, K);
+    xo.finish();
+    r.converged = o.converged;
+    r.iterations = o.iterations;
+    r.final_relative_residual = o.final_rel;
+    r.history_len = o.iterations + 1;
+    if (rep) *rep = r;
+    if (history)
+      for (int i = 0; i < history_cap && i < (int)o.hist.size(); ++i) history[i] = o.hist[i];
+  });
+}
+
+int sag_dc_create(sag_ctx* ctx, const sag_matrix* k0, int n_x0, int n_y0, int n_p0, int sv,
+                  int nlevels, const sag_level_desc* levels, const sag_solver_config* cfg,
+                  sag_dc** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(k0);
+    SAG_NOTNULL(levels);
+    SAG_NOTNULL(cfg);
+    SAG_NOTNULL(out);
+    *out = nullptr;
+    auto h = std::make_unique<sag_dc>();
+    dc_setup(ctx->c, h->d, &k0->m, n_x0, n_y0, n_p0, sv, nlevels, levels, *cfg);
+    *out = h.release();
+  });
+}
+
+int sag_dc_destroy(sag_dc* d) {
+  return guard([&] { delete d; });
+}
+
+int sag_dc_set_parameters(sag_dc* h, double eta_u, double eta_p, double omega0) {
+  return guard([&] {
+    SAG_NOTNULL(h);
+    sag_solver_config c = h->d.cfg;
+    c.eta_u = eta_u;
+    c.eta_p = eta_p;
+    c.omega0 = omega0;
+    check_config(c);
+    h->d.cfg = c;
+    h->d.graph_ok = false;
+  });
+}
+
+int sag_dc_set_sv_transfer(sag_dc* h, const sag_matrix* p_dup, const sag_matrix* m_mix, int nsl,
+                           const sag_matrix* const* scalar_levels,
+                           const sag_matrix* const* scalar_prolongators) {
+  return guard([&] {
+    SAG_NOTNULL(h);
+    SAG_NOTNULL(p_dup);
+    SAG_NOTNULL(m_mix);
+    SAG_NOTNULL(scalar_levels);
+    Dc& d = h->d;
+    SAG_REQUIRE(d.sv, SAG_CONFIG_ERROR, "sag_dc_set_sv_transfer: preconditioner is not SV");
+    Ctx& c = *d.ctx;
+    auto t = std::make_unique<SvTransfer>();
+    t->pdup = &p_dup->m;
+    t->mmix = &m_mix->m;
+    const int n_p1 = d.lv[0].n_p;
+    SAG_REQUIRE(t->pdup->nrows == d.n_p0 && t->pdup->ncols == n_p1 && t->mmix->nrows == n_p1 &&
+                    t->mmix->ncols == d.n_p0,
+                SAG_DIMENSION_MISMATCH, "sag_dc_set_sv_transfer: transfer shapes mismatch");
+    SAG_REQUIRE(nsl >= 1, SAG_DIMENSION_MISMATCH, "sag_dc_set_sv_transfer: empty hierarchy");
+    for (int l = 0; l < nsl; ++l) t->A.push_back(&scalar_levels[l]->m);
+    SAG_REQUIRE(t->A[0]->nrows == n_p1, SAG_DIMENSION_MISMATCH,
+                "sag_dc_set_sv_transfer: Mcg size mismatch");
+    t->kr.resize(nsl);
+    t->dinv.resize(nsl);
+    t->sb.resize(nsl);
+    t->sx.resize(nsl);
+    t->sr.resize(nsl);
+    for (int l = 0; l < nsl; ++l) {
+      const int n = t->A[l]->nrows;
+      t->sb[l].alloc(n);
+      t->sx[l].alloc(n);
+      if (l + 1 < nsl) {
+        SAG_NOTNULL(scalar_prolongators);
+        t->P.push_back(&scalar_prolongators[l]->m);
+        t->R.push_back(transpose_dev(c, *t->P.back()));
+        t->kr[l].init(n, 2, 0);
+        t->dinv[l].alloc(n);
+        t->sr[l].alloc(n);
+        int* bad = reinterpret_cast<int*>(c.scal.p + 8);
+        SAG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+        launch_inv_diag(c, *t->A[l], t->dinv[l].p, bad);
+        int hb = 0;
+        SAG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        SAG_CUDA(cudaStreamSynchronize(c.stream));
+        SAG_REQUIRE(!hb, SAG_ERROR, "inv_diagonal: zero diagonal in the Mcg hierarchy");
+      }
+    }
+    t->coarse.setup(c, *t->A.back(), -1, 0.0);
+    t->outer.init(n_p1, 20, 202);
+    t->rhs.alloc(n_p1);
+    d.svt = std::move(t);
+  });
+}
+
+int sag_dc_apply(sag_ctx* ctx, sag_dc* h, const double* r, double* z) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(h);
+    auto& c = ctx->c;
+    Dc& d = h->d;
+    require_ready(d);
+    InVec ri(c, r, d.n0, 0);
+    OutVec zo(c, z, d.n0, 1, false);
+    launch_copy(c, d.n0, ri.d, d.din.p);
+    dc_apply_graph(c, d);
+    launch_copy(c, d.n0, d.dout.p, zo.d);
+    zo.finish();
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sag_dc_vcycle(sag_ctx* ctx, sag_dc* h, const double* b, double* x, int nu1, int nu2) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(h);
+    auto& c = ctx->c;
+    Dc& d = h->d;
+    const int n = d.lv[0].n;
+    InVec bi(c, b, n, 0);
+    OutVec xo(c, x, n, 1, false);
+    launch_copy(c, n, bi.d, d.lv[0].b.p);
+    SAG_REQUIRE(nu1 <= d.lv[0].kry.m && nu2 <= d.lv[0].kry.m, SAG_CONFIG_ERROR,
+                "vcycle: nu exceeds the configured relaxation workspace");
+    cycle_level(c, d, 0, nu1, nu2, false);
+    launch_copy(c, n, d.lv[0].x.p, xo.d);
+    xo.finish();
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sag_dc_counters(const sag_dc* h, long long* counters) {
+  return guard([&] {
+    SAG_NOTNULL(h);
+    SAG_NOTNULL(counters);
+    counters[0] = h->d.fine_units;
+    counters[1] = h->d.l1_units;
+  });
+}
+
+int sag_dc_info(const sag_dc* h, long long* out, int cap) {
+  return guard([&] {
+    SAG_NOTNULL(h);
+    SAG_NOTNULL(out);
+    const Dc& d = h->d;
+    std::vector<long long> v;
+    v.push_back((long long)d.lv.size());
+    v.push_back(d.n0);
+    for (const auto& L : d.lv) v.push_back(L.n);
+    long long fb = d.fine ? d.fine->blob_bytes : 0;
+    for (const auto& L : d.lv)
+      if (L.vanka) fb += L.vanka->blob_bytes;
+    v.push_back(fb);
+    v.push_back(d.graph_launches);
+    for (int i = 0; i < cap && i < (int)v.size(); ++i) out[i] = v[i];
+  });
+}
+
+int sag_solve_stokes(sag_ctx* ctx, sag_dc* h, const double* rhs, double* x,
+                     const sag_solver_config* cfg, sag_krylov_report* rep, double* history,
+                     int history_cap) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(h);
+    SAG_NOTNULL(cfg);
+    check_config(*cfg);
+    auto& c = ctx->c;
+    Dc& d = h->d;
+    require_ready(d);
+    const int n = d.n0;
+    const int n_u = d.n_x0 + d.n_y0, n_p = d.n_p0;
+    InVec bi(c, rhs, n, 0);
+    OutVec xo(c, x, n, 1, false);
+    launch_zero(c, n, xo.d);
+    const int hist_cap = cfg->max_iters + 2;
+    if (d.outer.n != n || d.outer.m < cfg->restart || d.outer.hist_cap < hist_cap)
+      d.outer.init(n, cfg->restart, hist_cap);
+    double* mean_r = c.scal.p + 1;
+    double* mean_z = c.scal.p + 2;
+    const bool enclosed = cfg->enclosed_flow != 0;
+    // apply_prec (preconditioner.cpp:241-250)
+    DevOp prec = [&](const double* v, double* z) {
+      if (enclosed) {
+        Fin f;
+        f.kind = FIN_MEAN;
+        f.i = n_p;
+        f.out = mean_r;
+        launch_sum(c, n_p, v + n_u, f);
+        launch_project(c, n, n_u, v, mean_r, d.din.p);
+      } else {
+        launch_copy(c, n, v, d.din.p);
+      }
+      dc_apply_graph(c, d);
+      if (enclosed) {
+        Fin f;
+        f.kind = FIN_MEAN;
+        f.i = n_p;
+        f.out = mean_z;
+        launch_sum(c, n_p, d.dout.p + n_u, f);
+        launch_project(c, n, n_u, d.dout.p, mean_z, z);
+      } else {
+        launch_copy(c, n, d.dout.p, z);
+      }
+    };
+    FgmresOut o = fgmres_dev(c, *d.K0, bi.d, xo.d, prec, cfg->tol, cfg->max_iters, cfg->restart,
+                             1e-30, d.outer);
+    xo.finish();
+    if (rep) {
+      rep->converged = o.converged;
+      rep->iterations = o.iterations;
+      rep->final_relative_residual = o.final_rel;
+      rep->history_len = (int)o.hist.size();
+    }
+    if (history)
+      for (int i = 0; i < history_cap && i < (int)o.hist.size(); ++i) history[i] = o.hist[i];
+  });
+}
+
+}  // extern "C"

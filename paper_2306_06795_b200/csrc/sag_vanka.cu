@@ -1,0 +1,958 @@
+// libsag Vanka module (vanka.hpp:11-55 / vanka.cpp:11-209 of the reference):
+//   build_patches    -> patch_count_kernel / patch_fill_kernel
+//   factor_patches   -> factor_kernel: warp-per-patch block LU in shared memory
+//   apply_vanka      -> vanka_patch_kernel (cp.async.bulk-staged factor blobs,
+//                       warp-per-patch dense solves) + vanka_gather_kernel
+//                       (atomic-free owner-computes scatter-add)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace sag {
+
+// ======================================================== build_patches ==
+
+// vanka.cpp:20-38: patch i seeds pressure rows n_u + i*group + g; its
+// velocity set is the sorted union of the seed rows' columns c < n_u.
+__device__ __forceinline__ int merge_unique(const int* rp, const int* ci, int row0, int group,
+                                            int n_u, int* dst) {
+  int pos[3], end[3];
+  for (int g = 0; g < group; ++g) {
+    pos[g] = rp[row0 + g];
+    end[g] = rp[row0 + g + 1];
+  }
+  int cnt = 0, last = -1;
+  while (true) {
+    int best = 0x7fffffff, bg = -1;
+    for (int g = 0; g < group; ++g) {
+      if (pos[g] < end[g]) {
+        const int c = ci[pos[g]];
+        if (c < n_u && c < best) {
+          best = c;
+          bg = g;
+        }
+      }
+    }
+    if (bg < 0) break;
+    ++pos[bg];
+    if (best != last) {
+      if (dst) dst[cnt] = best;
+      ++cnt;
+      last = best;
+    }
+  }
+  return cnt;
+}
+
+__global__ void patch_count_kernel(int npatch, int group, int n_u, int n_x, const int* rp,
+                                   const int* ci, int* cnt_v, int* cnt_x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npatch; i += gridDim.x * blockDim.x) {
+    const int row0 = n_u + i * group;
+    int nv, nx = 0;
+    if (group == 1) {
+      nv = 0;
+      for (int q = rp[row0]; q < rp[row0 + 1]; ++q) {
+        const int c = ci[q];
+        nv += c < n_u;
+        nx += c < n_x;
+      }
+    } else {
+      nv = merge_unique(rp, ci, row0, group, n_u, nullptr);
+    }
+    cnt_v[i] = nv;
+    cnt_x[i] = nx;  // group 3: recomputed in fill
+  }
+}
+
+__global__ void patch_fill_kernel(int npatch, int group, int n_u, int n_x, const int* rp,
+                                  const int* ci, const int* vptr, int* vidx, int* pptr,
+                                  int* pidx, int* nx_out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npatch; i += gridDim.x * blockDim.x) {
+    const int row0 = n_u + i * group;
+    int* dst = vidx + vptr[i];
+    int nv;
+    if (group == 1) {
+      nv = 0;
+      for (int q = rp[row0]; q < rp[row0 + 1]; ++q)
+        if (ci[q] < n_u) dst[nv++] = ci[q];
+    } else {
+      nv = merge_unique(rp, ci, row0, group, n_u, dst);
+    }
+    int nx = 0;
+    while (nx < nv && dst[nx] < n_x) ++nx;  // lower_bound(n_x), vanka.cpp:36-38
+    nx_out[i] = nx;
+    for (int g = 0; g < group; ++g) pidx[i * group + g] = row0 + g;
+    pptr[i] = i * group;
+    if (i == npatch - 1) pptr[npatch] = npatch * group;
+  }
+}
+
+static void patch_maxima(Patches& p, const std::vector<int>& vptr, const std::vector<int>& pptr,
+                         const std::vector<int>& nx) {
+  p.max_nv = p.max_np = p.max_dim = 0;
+  for (int i = 0; i < p.npatch; ++i) {
+    const int nv = vptr[i + 1] - vptr[i], np = pptr[i + 1] - pptr[i];
+    p.max_nv = std::max(p.max_nv, nv);
+    p.max_np = std::max(p.max_np, np);
+    p.max_dim = std::max(p.max_dim, std::max(nx[i], nv - nx[i]));
+  }
+  p.tot_v = p.npatch ? vptr[p.npatch] : 0;
+  p.tot_p = p.npatch ? pptr[p.npatch] : 0;
+}
+
+std::unique_ptr<Patches> build_patches_dev(Ctx& c, const Matrix& k, int n_x, int n_y, int n_p,
+                                           bool sv_triples) {
+  const int n_u = n_x + n_y;
+  SAG_REQUIRE(n_x >= 0 && n_y >= 0 && n_p >= 0 && k.nrows == n_u + n_p && k.ncols == k.nrows,
+              SAG_DIMENSION_MISMATCH, "build_patches: block sizes do not match K");
+  SAG_REQUIRE(!sv_triples || n_p % 3 == 0, SAG_DIMENSION_MISMATCH,
+              "build_patches: triple seeding needs a multiple-of-3 pressure count");
+  const int group = sv_triples ? 3 : 1;
+  auto p = std::make_unique<Patches>();
+  const int np = n_p / group;
+  p->npatch = np;
+  p->pptr.alloc(np + 1);
+  p->pidx.alloc(n_p);
+  p->vptr.alloc(np + 1);
+  p->nx.alloc(np);
+  if (np == 0) {
+    SAG_CUDA(cudaMemsetAsync(p->pptr.p, 0, sizeof(int), c.stream));
+    SAG_CUDA(cudaMemsetAsync(p->vptr.p, 0, sizeof(int), c.stream));
+    p->vidx.alloc(1);
+    return p;
+  }
+  DevBuf<int> cv(np), cx(np);
+  const int grid = std::max(1, std::min((np + 255) / 256, c.num_sms * 16));
+  patch_count_kernel<<<grid, 256, 0, c.stream>>>(np, group, n_u, n_x, k.rp.p, k.ci.p, cv.p, cx.p);
+  SAG_LAUNCHED(c);
+  std::vector<int> hv(np);
+  SAG_CUDA(cudaMemcpyAsync(hv.data(), cv.p, sizeof(int) * np, cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  std::vector<int> vptr(np + 1, 0);
+  long long acc = 0;
+  for (int i = 0; i < np; ++i) {
+    if (hv[i] == 0)
+      throw Error(SAG_SINGULAR_PATCH, "build_patches: pressure row " + std::to_string(i * group) +
+                                          " couples to no velocity DoFs");
+    acc += hv[i];
+    SAG_REQUIRE(acc < (1LL << 31), SAG_DIMENSION_MISMATCH, "build_patches: too many entries");
+    vptr[i + 1] = (int)acc;
+  }
+  SAG_CUDA(cudaMemcpyAsync(p->vptr.p, vptr.data(), sizeof(int) * (np + 1), cudaMemcpyHostToDevice,
+                           c.stream));
+  p->vidx.alloc(acc);
+  patch_fill_kernel<<<grid, 256, 0, c.stream>>>(np, group, n_u, n_x, k.rp.p, k.ci.p, p->vptr.p,
+                                                p->vidx.p, p->pptr.p, p->pidx.p, p->nx.p);
+  SAG_LAUNCHED(c);
+  std::vector<int> hnx(np), pptr(np + 1);
+  for (int i = 0; i <= np; ++i) pptr[i] = i * group;
+  SAG_CUDA(cudaMemcpyAsync(hnx.data(), p->nx.p, sizeof(int) * np, cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  patch_maxima(*p, vptr, pptr, hnx);
+  return p;
+}
+
+std::unique_ptr<Patches> patches_from_lists(Ctx& c, int npatch, const int* pptr_in,
+                                            const int* pidx_in, const int* vptr_in,
+                                            const int* vidx_in, const int* nx_in) {
+  SAG_REQUIRE(npatch >= 0, SAG_DIMENSION_MISMATCH, "sag_patches_create: negative count");
+  std::vector<int> pptr(npatch + 1), vptr(npatch + 1), nx(std::max(npatch, 1));
+  SAG_CUDA(cudaMemcpy(pptr.data(), pptr_in, sizeof(int) * (npatch + 1), cudaMemcpyDefault));
+  SAG_CUDA(cudaMemcpy(vptr.data(), vptr_in, sizeof(int) * (npatch + 1), cudaMemcpyDefault));
+  if (npatch) SAG_CUDA(cudaMemcpy(nx.data(), nx_in, sizeof(int) * npatch, cudaMemcpyDefault));
+  const int tp = pptr[npatch], tv = vptr[npatch];
+  std::vector<int> pidx(std::max(tp, 1)), vidx(std::max(tv, 1));
+  if (tp) SAG_CUDA(cudaMemcpy(pidx.data(), pidx_in, sizeof(int) * tp, cudaMemcpyDefault));
+  if (tv) SAG_CUDA(cudaMemcpy(vidx.data(), vidx_in, sizeof(int) * tv, cudaMemcpyDefault));
+  for (int i = 0; i < npatch; ++i) {
+    const int nv = vptr[i + 1] - vptr[i];
+    SAG_REQUIRE(nv > 0 && pptr[i + 1] > pptr[i] && nx[i] >= 0 && nx[i] <= nv,
+                SAG_DIMENSION_MISMATCH, "sag_patches_create: malformed patch " + std::to_string(i));
+    for (int q = vptr[i] + 1; q < vptr[i + 1]; ++q)
+      SAG_REQUIRE(vidx[q] > vidx[q - 1], SAG_ERROR,
+                  "sag_patches_create: velocity lists must be sorted and unique");
+  }
+  auto p = std::make_unique<Patches>();
+  p->npatch = npatch;
+  p->pptr.alloc(npatch + 1);
+  p->vptr.alloc(npatch + 1);
+  p->nx.alloc(std::max(npatch, 1));
+  p->pidx.alloc(std::max(tp, 1));
+  p->vidx.alloc(std::max(tv, 1));
+  SAG_CUDA(cudaMemcpy(p->pptr.p, pptr.data(), sizeof(int) * (npatch + 1), cudaMemcpyHostToDevice));
+  SAG_CUDA(cudaMemcpy(p->vptr.p, vptr.data(), sizeof(int) * (npatch + 1), cudaMemcpyHostToDevice));
+  SAG_CUDA(cudaMemcpy(p->nx.p, nx.data(), sizeof(int) * nx.size(), cudaMemcpyHostToDevice));
+  SAG_CUDA(cudaMemcpy(p->pidx.p, pidx.data(), sizeof(int) * pidx.size(), cudaMemcpyHostToDevice));
+  SAG_CUDA(cudaMemcpy(p->vidx.p, vidx.data(), sizeof(int) * vidx.size(), cudaMemcpyHostToDevice));
+  patch_maxima(*p, vptr, pptr, nx);
+  return p;
+}
+
+// ======================================================= factor_patches ==
+// Arithmetic restates vanka.cpp:64-149 and sparse.cpp:310-361 with explicit
+// round-to-nearest operations (no FMA contraction), so u_hat, b_hat and s_inv
+// are bitwise those of the reference. The apply representation additionally
+// stores A_x^-1 and A_y^-1, whose columns are dense_lu_solve(lu, e_c).
+
+__device__ __forceinline__ int bsearch_idx(const int* a, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return (lo < n && a[lo] == key) ? lo : -1;
+}
+
+// sparse.cpp:310-341 by one warp on a row-major n x n matrix in shared memory.
+__device__ bool warp_lu(double* A, int n, int ld, int* piv, int lane) {
+  for (int i = lane; i < n; i += 32) piv[i] = i;
+  __syncwarp();
+  for (int k = 0; k < n; ++k) {
+    double bv = -1.0;
+    int bi = n;
+    for (int i = k + 1 + lane; i < n; i += 32) {
+      const double v = fabs(A[i * ld + k]);
+      if (v > bv) {
+        bv = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    const double akk = fabs(A[k * ld + k]);
+    const int p = (bv > akk) ? bi : k;
+    const double best = (bv > akk) ? bv : akk;
+    if (best == 0.0) return false;
+    if (p != k) {
+      for (int j = lane; j < n; j += 32) {
+        const double t = A[k * ld + j];
+        A[k * ld + j] = A[p * ld + j];
+        A[p * ld + j] = t;
+      }
+      if (lane == 0) {
+        const int t = piv[k];
+        piv[k] = piv[p];
+        piv[p] = t;
+      }
+    }
+    __syncwarp();
+    const double inv = __ddiv_rn(1.0, A[k * ld + k]);
+    for (int i = k + 1 + lane; i < n; i += 32) A[i * ld + k] = __dmul_rn(A[i * ld + k], inv);
+    __syncwarp();
+    for (int j = k + 1 + lane; j < n; j += 32) {
+      const double akj = A[k * ld + j];
+      for (int i = k + 1; i < n; ++i) {
+        const double m = A[i * ld + k];
+        if (m != 0.0) A[i * ld + j] = __dsub_rn(A[i * ld + j], __dmul_rn(m, akj));
+      }
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// sparse.cpp:343-361, one right-hand side per lane (x: this lane's scratch).
+__device__ __forceinline__ void lu_solve_lane(const double* LU, int n, int ld, double* x) {
+  for (int i = 1; i < n; ++i) {
+    double acc = x[i];
+    for (int j = 0; j < i; ++j) acc = __dsub_rn(acc, __dmul_rn(LU[i * ld + j], x[j]));
+    x[i] = acc;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double acc = x[i];
+    for (int j = i + 1; j < n; ++j) acc = __dsub_rn(acc, __dmul_rn(LU[i * ld + j], x[j]));
+    x[i] = __ddiv_rn(acc, LU[i * ld + i]);
+  }
+}
+
+struct FactorLayout {
+  int D, NV, NP;  // max dim, max nv, max np
+  int bytes;      // per warp
+  __host__ __device__ FactorLayout(int d, int nv, int np) : D(d), NV(nv), NP(np) {
+    size_t dbl = 2 * (size_t)D * D + 2 * (size_t)NP * NV + (size_t)NP * NP + 32 * (size_t)D;
+    size_t ints = (size_t)NV + 2 * (size_t)D + NP;
+    bytes = (int)(((dbl * 8 + ints * 4) + 15) / 16 * 16);
+  }
+};
+
+__global__ void __launch_bounds__(256) factor_kernel(
+    int npatch, int D, int NV, int NP, int wbytes, const int* __restrict__ rp,
+    const int* __restrict__ ci, const double* __restrict__ kv, const int* __restrict__ pptr,
+    const int* __restrict__ pidx, const int* __restrict__ vptr, const int* __restrict__ vidx,
+    const int* __restrict__ nxs, const long long* __restrict__ off, const int* __restrict__ sbase,
+    unsigned char* __restrict__ blob, int* err) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* base = smem + (size_t)wib * wbytes;
+  double* Ax = reinterpret_cast<double*>(base);
+  double* Ay = Ax + (size_t)D * D;
+  double* Bm = Ay + (size_t)D * D;   // NP x NV  [a*NV + m]
+  double* Um = Bm + (size_t)NP * NV; // NV x NP  [m*NP + a] (u_hat row-major)
+  double* Sm = Um + (size_t)NV * NP; // NP x NP
+  double* W = Sm + (size_t)NP * NP;  // 32 lanes x D
+  int* sv = reinterpret_cast<int*>(W + 32 * (size_t)D);
+  int* pivx = sv + NV;
+  int* pivy = pivx + D;
+  int* spiv = pivy + D;
+  double* xw = W + (size_t)lane * D;
+
+  const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int k = gw; k < npatch; k += nw) {
+    const int v0 = vptr[k], nv = vptr[k + 1] - v0;
+    const int p0 = pptr[k], np = pptr[k + 1] - p0;
+    const int nx = nxs[k], ny = nv - nx;
+    for (int i = lane; i < nv; i += 32) sv[i] = vidx[v0 + i];
+    for (int i = lane; i < D * D; i += 32) {
+      Ax[i] = 0.0;
+      Ay[i] = 0.0;
+    }
+    for (int i = lane; i < NP * NV; i += 32) Bm[i] = 0.0;
+    __syncwarp();
+    // gather_dense (vanka.cpp:47-60): A_x, A_y, B
+    for (int r = lane; r < nx; r += 32) {
+      const int row = sv[r];
+      for (int q = rp[row]; q < rp[row + 1]; ++q) {
+        const int pos = bsearch_idx(sv, nx, ci[q]);
+        if (pos >= 0) Ax[r * D + pos] = kv[q];
+      }
+    }
+    for (int r = lane; r < ny; r += 32) {
+      const int row = sv[nx + r];
+      for (int q = rp[row]; q < rp[row + 1]; ++q) {
+        const int pos = bsearch_idx(sv + nx, ny, ci[q]);
+        if (pos >= 0) Ay[r * D + pos] = kv[q];
+      }
+    }
+    for (int a = 0; a < np; ++a) {
+      const int row = pidx[p0 + a];
+      for (int q = rp[row] + lane; q < rp[row + 1]; q += 32) {
+        const int pos = bsearch_idx(sv, nv, ci[q]);
+        if (pos >= 0) Bm[a * NV + pos] = kv[q];
+      }
+    }
+    __syncwarp();
+    bool ok = true;
+    if (nx > 0) ok = warp_lu(Ax, nx, D, pivx, lane);
+    if (ok && ny > 0) ok = warp_lu(Ay, ny, D, pivy, lane);
+    if (!ok) {
+      if (lane == 0) atomicMin(err, k);
+      continue;
+    }
+    unsigned char* bl = blob + off[k];
+    double* gAx = reinterpret_cast<double*>(bl + 16);
+    double* gAy = gAx + (size_t)nx * nx;
+    double* gU = gAy + (size_t)ny * ny;
+    double* gB = gU + (size_t)np * nv;
+    double* gS = gB + (size_t)np * nv;
+    int* gidx = reinterpret_cast<int*>(gS + (size_t)np * np);
+    // per component: RHS t < n are unit vectors (inverse columns), t = n + j
+    // are -B(j, comp)^T (u_hat columns, vanka.cpp:99-111)
+    for (int comp = 0; comp < 2; ++comp) {
+      const int n = comp == 0 ? nx : ny;
+      const int c0 = comp == 0 ? 0 : nx;
+      const double* LU = comp == 0 ? Ax : Ay;
+      const int* pv = comp == 0 ? pivx : pivy;
+      double* gA = comp == 0 ? gAx : gAy;
+      if (n == 0) continue;
+      for (int t0 = 0; t0 < n + np; t0 += 32) {
+        const int t = t0 + lane;
+        if (t < n + np) {
+          for (int i = 0; i < n; ++i) {
+            const int src = pv[i];
+            xw[i] = (t < n) ? (src == t ? 1.0 : 0.0) : -Bm[(t - n) * NV + c0 + src];
+          }
+          lu_solve_lane(LU, n, D, xw);
+          if (t < n) {
+            for (int i = 0; i < n; ++i) gA[(size_t)t * n + i] = xw[i];
+          } else {
+            for (int i = 0; i < n; ++i) Um[(c0 + i) * NP + (t - n)] = xw[i];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // S = B u_hat (vanka.cpp:112-119)
+    for (int e = lane; e < np * np; e += 32) {
+      const int a = e / np, cc = e % np;
+      double acc = 0.0;
+      for (int m = 0; m < nv; ++m) acc = __dadd_rn(acc, __dmul_rn(Bm[a * NV + m], Um[m * NP + cc]));
+      Sm[a * np + cc] = acc;
+    }
+    __syncwarp();
+    if (!warp_lu(Sm, np, np, spiv, lane)) {
+      if (lane == 0) atomicMin(err, k);
+      continue;
+    }
+    // S^-1 columns from unit vectors (vanka.cpp:126-132), into gS row-major
+    if (lane < np) {
+      for (int i = 0; i < np; ++i) xw[i] = spiv[i] == lane ? 1.0 : 0.0;
+      lu_solve_lane(Sm, np, np, xw);
+      for (int i = 0; i < np; ++i) gS[i * np + lane] = xw[i];
+    }
+    __syncwarp();
+    // b_hat = S^-1 u_hat^T (vanka.cpp:133-140); stored [a*nv + j]
+    for (int e = lane; e < np * nv; e += 32) {
+      const int a = e / nv, j = e % nv;
+      double acc = 0.0;
+      for (int m = 0; m < np; ++m) acc = __dadd_rn(acc, __dmul_rn(gS[a * np + m], Um[j * NP + m]));
+      gB[(size_t)a * nv + j] = acc;
+    }
+    // u_hat stored [a*nv + i]
+    for (int e = lane; e < np * nv; e += 32) {
+      const int a = e / nv, i = e % nv;
+      gU[(size_t)a * nv + i] = Um[i * NP + a];
+    }
+    for (int i = lane; i < nv; i += 32) gidx[i] = sv[i];
+    for (int a = lane; a < np; a += 32) gidx[nv + a] = pidx[p0 + a];
+    if (lane == 0) {
+      int* hdr = reinterpret_cast<int*>(bl);
+      hdr[0] = nx;
+      hdr[1] = ny;
+      hdr[2] = np;
+      hdr[3] = sbase[k];
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void slot_keys_kernel(int npatch, const int* pptr, const int* pidx, const int* vptr,
+                                 const int* vidx, const int* sbase, int* keys) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < npatch; k += gridDim.x * blockDim.x) {
+    int s = sbase[k];
+    for (int q = vptr[k]; q < vptr[k + 1]; ++q) keys[s++] = vidx[q];
+    for (int q = pptr[k]; q < pptr[k + 1]; ++q) keys[s++] = pidx[q];
+  }
+}
+
+__global__ void count_int_kernel(long long n, const int* key, int* cnt) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    atomicAdd(cnt + key[i], 1);
+}
+
+__global__ void iota_int_kernel(long long n, int* a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = (int)i;
+}
+
+// vanka.cpp:67-73: w_d = 1 / #patches containing d (0 if none)
+__global__ void weights_kernel(int n, const int* dof_ptr, double* w) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const int m = dof_ptr[d + 1] - dof_ptr[d];
+    w[d] = m > 0 ? 1.0 / (double)m : 0.0;
+  }
+}
+
+static int grid_for(Ctx& c, long long n) {
+  return (int)std::max(1LL, std::min((n + 255) / 256, (long long)c.num_sms * 16));
+}
+
+std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches& p) {
+  SAG_REQUIRE(k.nrows == k.ncols, SAG_DIMENSION_MISMATCH, "factor_patches: K must be square");
+  SAG_REQUIRE(p.max_np <= 4, SAG_ERROR, "factor_patches: at most 4 pressure seeds per patch");
+  SAG_REQUIRE(p.max_dim <= 128, SAG_ERROR,
+              "factor_patches: velocity blocks larger than 128 per component are not supported");
+  auto f = std::make_unique<Vanka>();
+  const int np_ = p.npatch;
+  f->n = k.nrows;
+  f->npatch = np_;
+  f->max_dim = p.max_dim;
+  f->max_nv = p.max_nv;
+  f->max_np = p.max_np;
+  // host bookkeeping: blob offsets, slot bases, storage accounting (vanka.cpp:142-144)
+  std::vector<int> vptr(np_ + 1), pptr(np_ + 1), nx(std::max(np_, 1));
+  SAG_CUDA(cudaMemcpyAsync(vptr.data(), p.vptr.p, sizeof(int) * (np_ + 1), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaMemcpyAsync(pptr.data(), p.pptr.p, sizeof(int) * (np_ + 1), cudaMemcpyDeviceToHost, c.stream));
+  if (np_) SAG_CUDA(cudaMemcpyAsync(nx.data(), p.nx.p, sizeof(int) * np_, cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  std::vector<long long> off(np_ + 1, 0);
+  std::vector<int> sbase(std::max(np_, 1), 0);
+  long long slots = 0;
+  int maxbytes = 16;
+  for (int i = 0; i < np_; ++i) {
+    const long long nv = vptr[i + 1] - vptr[i], npp = pptr[i + 1] - pptr[i];
+    const long long x = nx[i], y = nv - x;
+    long long bytes = 16 + 8 * (x * x + y * y + 2 * nv * npp + npp * npp) + 4 * (nv + npp);
+    bytes = (bytes + 15) / 16 * 16;
+    off[i + 1] = off[i] + bytes;
+    maxbytes = std::max<long long>(maxbytes, bytes);
+    sbase[i] = (int)slots;
+    slots += nv + npp;
+    SAG_REQUIRE(slots < (1LL << 31), SAG_DIMENSION_MISMATCH, "factor_patches: too many slots");
+    f->a_factor_bytes += 8 * (x * x + y * y);
+    f->aux_bytes += 8 * (2 * nv * npp + npp * npp);
+    f->dense_inverse_bytes += 8 * (nv + npp) * (nv + npp);
+  }
+  f->slot_bytes = maxbytes;
+  f->nslots = slots;
+  f->blob_bytes = off[np_];
+  f->blob.alloc(std::max<long long>(off[np_], 16));
+  f->off.alloc(np_ + 1);
+  SAG_CUDA(cudaMemcpyAsync(f->off.p, off.data(), sizeof(long long) * (np_ + 1), cudaMemcpyHostToDevice, c.stream));
+  DevBuf<int> dsbase(std::max(np_, 1));
+  SAG_CUDA(cudaMemcpyAsync(dsbase.p, sbase.data(), sizeof(int) * sbase.size(), cudaMemcpyHostToDevice, c.stream));
+
+  // dof -> slot map (stable sort of slot ids by dof) and PoU weights
+  const int n = k.nrows;
+  f->out.alloc(std::max<long long>(slots, 1));
+  f->w.alloc(std::max(n, 1));
+  f->dof_ptr.alloc(n + 1);
+  f->dof_slot.alloc(std::max<long long>(slots, 1));
+  if (slots > 0) {
+    DevBuf<int> keys(slots), keys_sorted(slots), ids(slots), cnt(n + 1);
+    slot_keys_kernel<<<grid_for(c, np_), 256, 0, c.stream>>>(np_, p.pptr.p, p.pidx.p, p.vptr.p,
+                                                             p.vidx.p, dsbase.p, keys.p);
+    SAG_LAUNCHED(c);
+    iota_int_kernel<<<grid_for(c, slots), 256, 0, c.stream>>>(slots, ids.p);
+    SAG_LAUNCHED(c);
+    SAG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (n + 1), c.stream));
+    count_int_kernel<<<grid_for(c, slots), 256, 0, c.stream>>>(slots, keys.p, cnt.p);
+    SAG_LAUNCHED(c);
+    size_t t1 = 0, t2 = 0;
+    SAG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, cnt.p, f->dof_ptr.p, n + 1, c.stream));
+    SAG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t2, keys.p, keys_sorted.p, ids.p,
+                                             f->dof_slot.p, (int)slots, 0, 32, c.stream));
+    DevBuf<unsigned char> ws(std::max(t1, t2));
+    SAG_CUDA(cub::DeviceScan::ExclusiveSum(ws.p, t1, cnt.p, f->dof_ptr.p, n + 1, c.stream));
+    SAG_CUDA(cub::DeviceRadixSort::SortPairs(ws.p, t2, keys.p, keys_sorted.p, ids.p,
+                                             f->dof_slot.p, (int)slots, 0, 32, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  } else {
+    SAG_CUDA(cudaMemsetAsync(f->dof_ptr.p, 0, sizeof(int) * (n + 1), c.stream));
+  }
+  weights_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, f->dof_ptr.p, f->w.p);
+  SAG_LAUNCHED(c);
+
+  // batched factorization
+  if (np_ > 0) {
+    FactorLayout L(std::max(p.max_dim, 1), std::max(p.max_nv, 1), std::max(p.max_np, 1));
+    int warps = std::max(1, std::min(8, (200 * 1024) / L.bytes));
+    SAG_REQUIRE((size_t)L.bytes <= 220 * 1024, SAG_ERROR,
+                "factor_patches: patch too large for shared-memory factorization");
+    const int smem = warps * L.bytes;
+    SAG_CUDA(cudaFuncSetAttribute(factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    DevBuf<int> err(1);
+    const int big = 0x7fffffff;
+    SAG_CUDA(cudaMemcpyAsync(err.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    const int blocks = std::max(1, std::min((np_ + warps - 1) / warps, c.num_sms * 8));
+    factor_kernel<<<blocks, warps * 32, smem, c.stream>>>(
+        np_, L.D, L.NV, L.NP, L.bytes, k.rp.p, k.ci.p, k.v.p, p.pptr.p, p.pidx.p, p.vptr.p,
+        p.vidx.p, p.nx.p, f->off.p, dsbase.p, f->blob.p, err.p);
+    SAG_LAUNCHED(c);
+    int herr = big;
+    SAG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    if (herr != big)
+      throw Error(SAG_SINGULAR_PATCH,
+                  "factor_patches: singular velocity or Schur block in patch " + std::to_string(herr));
+  }
+  return f;
+}
+
+// ========================================================== apply_vanka ==
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+// One 1-D bulk copy global -> shared, completion signalled on `bar`.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Warp-per-patch additive Vanka: each warp streams its patches' factor blobs
+// through an NSTAGE-deep shared-memory ring filled by cp.async.bulk (TMA
+// engine), gathers r at the patch dofs, solves with the block factors
+// (t = A^-1 b_u; x_p = S^-1 b_p + B_hat b_u; x_u = t + U_hat x_p,
+// vanka.cpp:161-181) and writes the unweighted local result to its slots.
+template <int R>
+__global__ void __launch_bounds__(256) vanka_patch_kernel(
+    int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
+    int slot_bytes, int nstage, int sb_len, const double* __restrict__ r,
+    double* __restrict__ out, const int* gate) {
+  if (gate && *gate) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* ring = smem + (size_t)wib * nstage * slot_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)warps * nstage * slot_bytes) +
+                   (size_t)wib * nstage;
+  double* sb = reinterpret_cast<double*>(smem + (size_t)warps * nstage * slot_bytes +
+                                         (size_t)warps * nstage * 8) +
+               (size_t)wib * sb_len;
+  const int first = blockIdx.x * warps + wib;
+  const int stride = gridDim.x * warps;
+  if (lane == 0) {
+    for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < nstage; ++s) {
+      const int kk = first + s * stride;
+      if (kk < npatch)
+        bulk_load(ring + (size_t)s * slot_bytes, blob + off[kk], (unsigned)(off[kk + 1] - off[kk]),
+                  bars + s);
+    }
+  }
+  __syncwarp();
+  int it = 0;
+  for (int k = first; k < npatch; k += stride, ++it) {
+    const int stage = it % nstage;
+    const unsigned parity = (unsigned)((it / nstage) & 1);
+    mbar_wait(bars + stage, parity);
+    const unsigned char* B = ring + (size_t)stage * slot_bytes;
+    const int4 hdr = *reinterpret_cast<const int4*>(B);
+    const int nx = hdr.x, ny = hdr.y, np = hdr.z, sbase = hdr.w;
+    const int nv = nx + ny;
+    const double* Ax = reinterpret_cast<const double*>(B + 16);
+    const double* Ay = Ax + nx * nx;
+    const double* U = Ay + ny * ny;
+    const double* Bh = U + np * nv;
+    const double* Si = Bh + np * nv;
+    const int* idx = reinterpret_cast<const int*>(Si + np * np);
+    for (int i = lane; i < nv + np; i += 32) sb[i] = __ldg(r + idx[i]);
+    __syncwarp();
+    // t = A^-1 b_u per component (vanka.cpp:164-166)
+    double tx[R], ty[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) tx[q] = ty[q] = 0.0;
+    const int nmax = nx > ny ? nx : ny;
+    for (int j = 0; j < nmax; ++j) {
+      const double bx = sb[j];
+      const double by = sb[nx + j];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        if (j < nx && i < nx) tx[q] = fma(Ax[j * nx + i], bx, tx[q]);
+        if (j < ny && i < ny) ty[q] = fma(Ay[j * ny + i], by, ty[q]);
+      }
+    }
+    // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
+    double xp[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      xp[a] = 0.0;
+      if (a < np) {
+        double part = 0.0;
+        for (int m = lane; m < nv; m += 32) part = fma(Bh[a * nv + m], sb[m], part);
+        part = warp_sum(part);
+        double sp = 0.0;
+        for (int j = 0; j < np; ++j) sp = fma(Si[a * np + j], sb[nv + j], sp);
+        xp[a] = sp + part;
+        if (lane == 0) out[sbase + nv + a] = xp[a];
+      }
+    }
+    // x_u = t + U_hat x_p (vanka.cpp:176-180)
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int i = lane + 32 * q;
+      if (i < nx) {
+        double v = tx[q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          if (a < np) v = fma(U[a * nv + i], xp[a], v);
+        out[sbase + i] = v;
+      }
+      if (i < ny) {
+        double v = ty[q];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          if (a < np) v = fma(U[a * nv + nx + i], xp[a], v);
+        out[sbase + nx + i] = v;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const int kn = k + nstage * stride;
+      if (kn < npatch) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_load(ring + (size_t)stage * slot_bytes, blob + off[kn],
+                  (unsigned)(off[kn + 1] - off[kn]), bars + stage);
+      }
+    }
+  }
+}
+
+// Owner-computes scatter-add: delta_d = sum over d's slots (ascending patch
+// order) of w_d * x_slot (vanka.cpp:179-181); with xadd: x_d += omega*delta_d
+// (vanka.cpp:195).
+__global__ void vanka_gather_kernel(int n, const int* __restrict__ dof_ptr,
+                                    const int* __restrict__ dof_slot,
+                                    const double* __restrict__ out, const double* __restrict__ w,
+                                    double* __restrict__ delta, double* __restrict__ xadd,
+                                    double omega, const int* gate) {
+  if (gate && *gate) return;
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const double wd = w[d];
+    double acc = 0.0;
+    for (int s = dof_ptr[d]; s < dof_ptr[d + 1]; ++s)
+      acc = __dadd_rn(acc, __dmul_rn(wd, __ldcg(out + dof_slot[s])));
+    if (xadd)
+      xadd[d] = xadd[d] + omega * acc;
+    else
+      delta[d] = acc;
+  }
+}
+
+struct ApplyCfg {
+  int warps, nstage, sb_len, smem, blocks;
+};
+
+template <int R>
+static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
+  static thread_local int configured_smem[4] = {0, 0, 0, 0};
+  ApplyCfg a;
+  a.nstage = 2;
+  a.sb_len = f.max_nv + f.max_np + f.max_dim + 2;
+  a.sb_len = (a.sb_len + 1) / 2 * 2;
+  const int per_warp = a.nstage * f.slot_bytes + a.nstage * 8 + a.sb_len * 8;
+  a.warps = std::max(1, std::min(8, (112 * 1024) / per_warp));
+  if (a.warps * per_warp > 112 * 1024) a.warps = std::max(1, (220 * 1024) / per_warp);
+  a.smem = a.warps * per_warp;
+  SAG_REQUIRE(a.smem <= 227 * 1024, SAG_ERROR, "apply_vanka: patch blobs too large for staging");
+  if (configured_smem[R - 1] < a.smem) {
+    SAG_CUDA(cudaFuncSetAttribute(vanka_patch_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  a.smem));
+    configured_smem[R - 1] = a.smem;
+  }
+  int occ = 0;
+  SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vanka_patch_kernel<R>, a.warps * 32,
+                                                         a.smem));
+  occ = std::max(occ, 1);
+  const long long need = (f.npatch + a.warps - 1) / a.warps;
+  a.blocks = (int)std::max(1LL, std::min<long long>(need, (long long)occ * c.num_sms));
+  return a;
+}
+
+template <int R>
+static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gate) {
+  const ApplyCfg a = apply_cfg<R>(c, f);
+  vanka_patch_kernel<R><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
+      f.npatch, f.blob.p, f.off.p, f.slot_bytes, a.nstage, a.sb_len, r, f.out.p, gate);
+  SAG_LAUNCHED(c);
+}
+
+static void launch_patch_any(Ctx& c, const Vanka& f, const double* r, const int* gate) {
+  if (f.npatch == 0) return;
+  const int R = (f.max_dim + 31) / 32;
+  switch (R) {
+    case 1: launch_patch<1>(c, f, r, gate); break;
+    case 2: launch_patch<2>(c, f, r, gate); break;
+    case 3: launch_patch<3>(c, f, r, gate); break;
+    default: launch_patch<4>(c, f, r, gate); break;
+  }
+}
+
+void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta, const int* gate) {
+  launch_patch_any(c, f, r, gate);
+  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(f.n, f.dof_ptr.p, f.dof_slot.p,
+                                                              f.out.p, f.w.p, delta, nullptr, 1.0,
+                                                              gate);
+  SAG_LAUNCHED(c);
+}
+
+void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega) {
+  launch_patch_any(c, f, r, nullptr);
+  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(f.n, f.dof_ptr.p, f.dof_slot.p,
+                                                              f.out.p, f.w.p, nullptr, x, omega,
+                                                              nullptr);
+  SAG_LAUNCHED(c);
+}
+
+// The reference's factor layout (vanka.hpp:31-33), unpacked on the host for
+// parity tests.
+void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* sinv,
+                  double* weights) {
+  std::vector<unsigned char> blob(f.blob_bytes);
+  std::vector<long long> off(f.npatch + 1);
+  SAG_CUDA(cudaMemcpyAsync(blob.data(), f.blob.p, f.blob_bytes, cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaMemcpyAsync(off.data(), f.off.p, sizeof(long long) * (f.npatch + 1),
+                           cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  size_t ou = 0, os = 0;
+  for (int k = 0; k < f.npatch; ++k) {
+    const unsigned char* B = blob.data() + off[k];
+    const int* hdr = reinterpret_cast<const int*>(B);
+    const int nx = hdr[0], ny = hdr[1], np = hdr[2], nv = nx + ny;
+    const double* Ax = reinterpret_cast<const double*>(B + 16);
+    const double* U = Ax + nx * nx + ny * ny;
+    const double* Bh = U + np * nv;
+    const double* Si = Bh + np * nv;
+    for (int i = 0; i < nv; ++i)
+      for (int a = 0; a < np; ++a) {
+        if (uhat) uhat[ou + (size_t)i * np + a] = U[a * nv + i];
+        if (bhat) bhat[ou + (size_t)a * nv + i] = Bh[a * nv + i];
+      }
+    if (sinv)
+      for (int e = 0; e < np * np; ++e) sinv[os + e] = Si[e];
+    ou += (size_t)nv * np;
+    os += (size_t)np * np;
+  }
+  if (weights) SAG_CUDA(cudaMemcpy(weights, f.w.p, sizeof(double) * f.n, cudaMemcpyDefault));
+}
+
+}  // namespace sag
+
+// =================================================================== C-ABI
+using namespace sag;
+
+extern "C" {
+
+int sag_build_patches(sag_ctx* ctx, const sag_matrix* k, int n_x, int n_y, int n_p,
+                      int sv_triples, sag_patches** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(k);
+    SAG_NOTNULL(out);
+    *out = nullptr;
+    auto p = build_patches_dev(ctx->c, k->m, n_x, n_y, n_p, sv_triples != 0);
+    auto* h = new sag_patches;
+    h->p = std::move(*p);
+    *out = h;
+  });
+}
+
+int sag_patches_create(sag_ctx* ctx, int npatch, const int* pressure_ptr, const int* pressure_idx,
+                       const int* velocity_ptr, const int* velocity_idx, const int* nx,
+                       sag_patches** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(out);
+    SAG_NOTNULL(pressure_ptr);
+    SAG_NOTNULL(velocity_ptr);
+    *out = nullptr;
+    auto p = patches_from_lists(ctx->c, npatch, pressure_ptr, pressure_idx, velocity_ptr,
+                                velocity_idx, nx);
+    auto* h = new sag_patches;
+    h->p = std::move(*p);
+    *out = h;
+  });
+}
+
+int sag_patches_destroy(sag_patches* p) {
+  return guard([&] { delete p; });
+}
+
+int sag_patches_info(const sag_patches* p, long long* info) {
+  return guard([&] {
+    SAG_NOTNULL(p);
+    SAG_NOTNULL(info);
+    info[0] = p->p.npatch;
+    info[1] = p->p.tot_p;
+    info[2] = p->p.tot_v;
+    info[3] = p->p.max_nv;
+    info[4] = p->p.max_np;
+  });
+}
+
+int sag_patches_export(sag_ctx* ctx, const sag_patches* p, int* pptr, int* pidx, int* vptr,
+                       int* vidx, int* nx) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(p);
+    const auto& q = p->p;
+    auto& c = ctx->c;
+    if (pptr) SAG_CUDA(cudaMemcpyAsync(pptr, q.pptr.p, sizeof(int) * (q.npatch + 1), cudaMemcpyDefault, c.stream));
+    if (vptr) SAG_CUDA(cudaMemcpyAsync(vptr, q.vptr.p, sizeof(int) * (q.npatch + 1), cudaMemcpyDefault, c.stream));
+    if (pidx && q.tot_p) SAG_CUDA(cudaMemcpyAsync(pidx, q.pidx.p, sizeof(int) * q.tot_p, cudaMemcpyDefault, c.stream));
+    if (vidx && q.tot_v) SAG_CUDA(cudaMemcpyAsync(vidx, q.vidx.p, sizeof(int) * q.tot_v, cudaMemcpyDefault, c.stream));
+    if (nx && q.npatch) SAG_CUDA(cudaMemcpyAsync(nx, q.nx.p, sizeof(int) * q.npatch, cudaMemcpyDefault, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sag_factor_patches(sag_ctx* ctx, const sag_matrix* k, const sag_patches* p, int n_u,
+                       sag_vanka** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(k);
+    SAG_NOTNULL(p);
+    SAG_NOTNULL(out);
+    (void)n_u;  // vanka.cpp:147: unused by the reference as well
+    *out = nullptr;
+    auto f = factor_patches_dev(ctx->c, k->m, p->p);
+    auto* h = new sag_vanka;
+    h->f = std::move(*f);
+    *out = h;
+  });
+}
+
+int sag_vanka_destroy(sag_vanka* f) {
+  return guard([&] { delete f; });
+}
+
+int sag_vanka_stats(const sag_vanka* f, long long* s) {
+  return guard([&] {
+    SAG_NOTNULL(f);
+    SAG_NOTNULL(s);
+    const auto& v = f->f;
+    s[0] = v.a_factor_bytes;
+    s[1] = v.aux_bytes;
+    s[2] = v.dense_inverse_bytes;
+    s[3] = v.blob_bytes;
+    s[4] = v.npatch;
+    s[5] = v.n;
+    s[6] = v.nslots;
+  });
+}
+
+int sag_vanka_export(sag_ctx* ctx, const sag_vanka* f, double* u_hat, double* b_hat,
+                     double* s_inv, double* weights) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    vanka_export(ctx->c, f->f, u_hat, b_hat, s_inv, weights);
+  });
+}
+
+int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    auto& c = ctx->c;
+    InVec ri(c, r, f->f.n, 0);
+    OutVec d(c, delta, f->f.n, 1, false);
+    vanka_apply(c, f->f, ri.d, d.d);
+    d.finish();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,358 @@
+// Drop-in adapter: reference C++ solver API on top of libsag's C-ABI, and the
+// host-application entry points (sagh_*) the Python harness uses to obtain
+// reference-built cases (build_case, assemble_saddle_matrix,
+// build_monolithic_hierarchy -- the setup north_star keeps in the reference's
+// host C++).
+#include "stokesamg_gpu.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "stokesamg/experiments.hpp"
+
+namespace stokesamg::gpu {
+
+void check(int s) {
+  if (s == SAG_OK) return;
+  const std::string msg = sag_last_error();
+  switch (s) {
+    case SAG_DIMENSION_MISMATCH: throw DimensionMismatch(msg);
+    case SAG_SINGULAR_MATRIX: throw SingularMatrix(msg);
+    case SAG_SINGULAR_PATCH: throw SingularPatch(msg);
+    case SAG_CONFIG_ERROR: throw ConfigError(msg);
+    case SAG_SOLVER_STAGNATION: throw SolverStagnation(msg);
+    default: throw Error(msg);
+  }
+}
+
+Device::Device(int ordinal) { check(sag_create(ordinal, &ctx_)); }
+Device::~Device() { sag_destroy(ctx_); }
+
+DeviceMatrix::DeviceMatrix(Device& dev, const SparseMatrix& m) : nrows_(m.nrows), ncols_(m.ncols) {
+  check(sag_matrix_create(dev.handle(), m.nrows, m.ncols, m.nnz(), m.row_offsets.data(),
+                          m.col_indices.data(), m.values.data(), &h_));
+}
+DeviceMatrix::~DeviceMatrix() { sag_matrix_destroy(h_); }
+
+std::vector<double> spmv(Device& dev, const DeviceMatrix& m, const std::vector<double>& x) {
+  if (static_cast<int>(x.size()) != m.ncols())
+    throw DimensionMismatch("spmv: vector length does not match column count");
+  std::vector<double> y(m.nrows());
+  check(sag_spmv(dev.handle(), m.handle(), x.data(), y.data()));
+  return y;
+}
+
+VankaFactorization::VankaFactorization(Device& dev, const DeviceMatrix& k, int n_x, int n_y,
+                                       int n_p, bool sv_triples) {
+  sag_patches* p = nullptr;
+  check(sag_build_patches(dev.handle(), k.handle(), n_x, n_y, n_p, sv_triples ? 1 : 0, &p));
+  const int rc = sag_factor_patches(dev.handle(), k.handle(), p, n_x + n_y, &f_);
+  sag_patches_destroy(p);
+  check(rc);
+  long long s[7];
+  check(sag_vanka_stats(f_, s));
+  a_factor_bytes = s[0];
+  aux_bytes = s[1];
+  dense_inverse_bytes = s[2];
+}
+VankaFactorization::~VankaFactorization() { sag_vanka_destroy(f_); }
+
+std::vector<double> apply_vanka(Device& dev, const VankaFactorization& f,
+                                const std::vector<double>& r) {
+  std::vector<double> d(r.size());
+  check(sag_apply_vanka(dev.handle(), f.handle(), r.data(), d.data()));
+  return d;
+}
+
+static sag_solver_config to_c(const SolverConfig& c) {
+  sag_solver_config s;
+  s.variant = c.variant == Variant::DCLO ? SAG_DC_LO : c.variant == Variant::DCHO ? SAG_DC_HO
+                                                                                   : SAG_DC_ALL;
+  s.eta_u = c.eta_u;
+  s.eta_p = c.eta_p;
+  s.omega0 = c.omega0;
+  s.nu1 = c.nu1;
+  s.nu2 = c.nu2;
+  s.gamma = c.gamma;
+  s.restart = c.restart;
+  s.tol = c.tol;
+  s.max_iters = c.max_iters;
+  s.enclosed_flow = c.enclosed_flow ? 1 : 0;
+  return s;
+}
+
+DCPreconditioner::DCPreconditioner(Device& dev, const SaddleSystem& sys0, const SaddleSystem& sys1,
+                                   TransferPair transfer, SolverConfig cfg)
+    : dev_(dev), cfg_(std::move(cfg)) {
+  if (cfg_.validate) cfg_.check();
+  if (cfg_.variant != Variant::DCall && cfg_.variant != Variant::DCLO &&
+      cfg_.variant != Variant::DCHO)
+    throw ConfigError("gpu::DCPreconditioner: variant must be a DC variant");
+  k0_ = assemble_saddle_matrix(sys0);
+  n_p0_ = sys0.n_p;
+  if (transfer.n_u0 != sys0.n_u() || transfer.n_p0 != n_p0_)
+    throw DimensionMismatch("DCPreconditioner: transfer does not match the high-order system");
+  h_ = build_monolithic_hierarchy(sys1, cfg_.amg);
+  const bool sv = sys0.disc == Discretization::SV;
+  mats_.push_back(std::make_unique<DeviceMatrix>(dev, k0_));
+  const sag_matrix* k0h = mats_.back()->handle();
+  std::vector<sag_level_desc> lv(h_.num_levels());
+  for (int l = 0; l < h_.num_levels(); ++l) {
+    const auto& L = h_.levels[l];
+    mats_.push_back(std::make_unique<DeviceMatrix>(dev, L.k));
+    lv[l].k = mats_.back()->handle();
+    lv[l].p = nullptr;
+    if (l + 1 < h_.num_levels()) {
+      mats_.push_back(std::make_unique<DeviceMatrix>(dev, L.p));
+      lv[l].p = mats_.back()->handle();
+    }
+    lv[l].n_x = L.n_x;
+    lv[l].n_y = L.n_y;
+    lv[l].n_p = L.n_p;
+  }
+  const sag_solver_config c = to_c(cfg_);
+  check(sag_dc_create(dev.handle(), k0h, sys0.n_x, sys0.n_y, sys0.n_p, sv ? 1 : 0,
+                      h_.num_levels(), lv.data(), &c, &dc_));
+  if (sv) {
+    // SvPressureRestrict's own hierarchy (transfer.cpp:18-23), rebuilt by the
+    // reference's build_scalar_hierarchy with the default AmgConfig
+    ScalarHierarchy sh = build_scalar_hierarchy(sys0.Mp_cg, AmgConfig{});
+    mats_.push_back(std::make_unique<DeviceMatrix>(dev, transfer.p0_pressure));
+    const sag_matrix* pdup = mats_.back()->handle();
+    mats_.push_back(std::make_unique<DeviceMatrix>(dev, sys0.M_mix));
+    const sag_matrix* mmix = mats_.back()->handle();
+    std::vector<const sag_matrix*> A, P;
+    for (const auto& m : sh.matrices) {
+      mats_.push_back(std::make_unique<DeviceMatrix>(dev, m));
+      A.push_back(mats_.back()->handle());
+    }
+    for (const auto& m : sh.prolongators) {
+      mats_.push_back(std::make_unique<DeviceMatrix>(dev, m));
+      P.push_back(mats_.back()->handle());
+    }
+    check(sag_dc_set_sv_transfer(dc_, pdup, mmix, static_cast<int>(A.size()), A.data(),
+                                 P.data()));
+  }
+}
+
+DCPreconditioner::~DCPreconditioner() { sag_dc_destroy(dc_); }
+
+std::vector<double> DCPreconditioner::apply(const std::vector<double>& r) const {
+  if (static_cast<int>(r.size()) != size())
+    throw DimensionMismatch("DCPreconditioner::apply: size mismatch");
+  std::vector<double> z(r.size());
+  check(sag_dc_apply(dev_.handle(), dc_, r.data(), z.data()));
+  long long cnt[2];
+  check(sag_dc_counters(dc_, cnt));
+  fine_relax_units = cnt[0];
+  level1_relax_units = cnt[1];
+  return z;
+}
+
+void DCPreconditioner::set_parameters(double eta_u, double eta_p, double omega0) {
+  cfg_.eta_u = eta_u;
+  cfg_.eta_p = eta_p;
+  cfg_.omega0 = omega0;
+  if (cfg_.validate) cfg_.check();
+  check(sag_dc_set_parameters(dc_, eta_u, eta_p, omega0));
+}
+
+SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
+                         const DCPreconditioner& prec, const SolverConfig& cfg) {
+  if (cfg.validate) cfg.check();
+  if (k0.nrows != prec.size() || static_cast<int>(rhs.size()) != prec.size())
+    throw DimensionMismatch("solve_stokes: size mismatch");
+  SolveResult res;
+  res.x.assign(rhs.size(), 0.0);
+  const sag_solver_config c = to_c(cfg);
+  sag_krylov_report rep{};
+  std::vector<double> hist(cfg.max_iters + 2);
+  check(sag_solve_stokes(prec.device().handle(), prec.handle(), rhs.data(), res.x.data(), &c,
+                         &rep, hist.data(), static_cast<int>(hist.size())));
+  res.report.converged = rep.converged != 0;
+  res.report.iterations = rep.iterations;
+  res.report.final_relative_residual = rep.final_relative_residual;
+  res.report.residual_history.assign(hist.begin(),
+                                     hist.begin() + std::min<int>(rep.history_len, hist.size()));
+  return res;
+}
+
+}  // namespace stokesamg::gpu
+
+// ======================================================================
+// Host-application entry points for the Python harness (bench.py): the
+// reference's setup produces the inputs of the GPU path.
+// ======================================================================
+using namespace stokesamg;
+
+namespace {
+thread_local std::string g_err;
+
+struct HostCase {
+  AssembledCase c;
+  SparseMatrix k0;
+  MonolithicHierarchy h;
+  ScalarHierarchy sh;  // SV only
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+const SparseMatrix* pick(const HostCase& hc, int which) {
+  if (which == 0) return &hc.k0;
+  if (which >= 1 && which < 1000) {
+    const int l = (which - 1) / 2;
+    if (l >= hc.h.num_levels()) return nullptr;
+    if ((which - 1) % 2 == 0) return &hc.h.levels[l].k;
+    return l + 1 < hc.h.num_levels() ? &hc.h.levels[l].p : nullptr;
+  }
+  if (which == 1000) return &hc.c.transfer.p0_pressure;
+  if (which == 1001) return &hc.c.sys0.M_mix;
+  const int s = (which - 1002) / 2;
+  if ((which - 1002) % 2 == 0) return s < hc.sh.levels() ? &hc.sh.matrices[s] : nullptr;
+  return s + 1 < hc.sh.levels() ? &hc.sh.prolongators[s] : nullptr;
+}
+
+// f = (sin(k1 x), cos(k2 y)) body force, all-Dirichlet zero (BASELINE config 4)
+AssembledCase mesh_case(const char* path, double k1, double k2) {
+  ProblemData prob = zero_problem();
+  prob.force = [k1, k2](double x, double y) {
+    return std::array<double, 2>{std::sin(k1 * x), std::cos(k2 * y)};
+  };
+  prob.check_compatibility = false;
+  AssembledCase c;
+  c.enclosed = true;
+  c.mesh = read_mesh(path);
+  for (auto& be : c.mesh.boundary_edges) be.tag = BoundaryTag::DirichletZero;
+  c.sys0 = assemble_taylor_hood(c.mesh, prob);
+  auto [mf, qmap] = quadrisect(c.mesh);
+  c.sys1 = assemble_iso(c.mesh, mf, qmap, prob);
+  c.transfer = build_th_transfer(c.sys0, c.sys1);
+  return c;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sagh_last_error() { return g_err.c_str(); }
+
+// problem/sv/mesh_kind/n as ExperimentSpec (experiments.hpp:24-38); mesh_kind
+// "file" reads mesh_path; "file_forced" builds BASELINE config 4 from
+// mesh_path with force wavenumbers (k1, k2). coarse_size <= 0 keeps the
+// reference default (amg.hpp:58).
+void* sagh_case_build(const char* problem, int sv, const char* mesh_kind, int n,
+                      const char* mesh_path, int coarse_size, double k1, double k2) {
+  HostCase* out = nullptr;
+  guarded([&] {
+    auto hc = std::make_unique<HostCase>();
+    if (std::string(mesh_kind) == "file_forced") {
+      hc->c = mesh_case(mesh_path, k1, k2);
+    } else {
+      ExperimentSpec s;
+      s.problem = problem;
+      s.disc = sv ? Discretization::SV : Discretization::TH;
+      s.mesh.kind = mesh_kind;
+      s.mesh.n = n;
+      if (mesh_path) s.mesh.path = mesh_path;
+      hc->c = build_case(s, 0);
+    }
+    AmgConfig amg;
+    if (coarse_size > 0) amg.coarse_size = coarse_size;
+    hc->k0 = assemble_saddle_matrix(hc->c.sys0);
+    hc->h = build_monolithic_hierarchy(hc->c.sys1, amg);
+    if (hc->c.sys0.disc == Discretization::SV)
+      hc->sh = build_scalar_hierarchy(hc->c.sys0.Mp_cg, AmgConfig{});
+    out = hc.release();
+  });
+  return out;
+}
+
+void sagh_case_free(void* h) { delete static_cast<HostCase*>(h); }
+
+// out = [n_x0, n_y0, n_p0, nlevels, enclosed, sv, scalar levels]
+int sagh_case_info(void* h, long long* out) {
+  const auto& hc = *static_cast<HostCase*>(h);
+  out[0] = hc.c.sys0.n_x;
+  out[1] = hc.c.sys0.n_y;
+  out[2] = hc.c.sys0.n_p;
+  out[3] = hc.h.num_levels();
+  out[4] = hc.c.enclosed ? 1 : 0;
+  out[5] = hc.c.sys0.disc == Discretization::SV ? 1 : 0;
+  out[6] = hc.sh.levels();
+  return 0;
+}
+
+int sagh_case_level(void* h, int l, int* nxyz) {
+  const auto& lev = static_cast<HostCase*>(h)->h.levels.at(l);
+  nxyz[0] = lev.n_x;
+  nxyz[1] = lev.n_y;
+  nxyz[2] = lev.n_p;
+  return 0;
+}
+
+int sagh_case_matrix_shape(void* h, int which, int* nr, int* nc, long long* nnz) {
+  const SparseMatrix* m = pick(*static_cast<HostCase*>(h), which);
+  if (!m) {
+    g_err = "sagh_case_matrix_shape: no such matrix";
+    return 2;
+  }
+  *nr = m->nrows;
+  *nc = m->ncols;
+  *nnz = m->nnz();
+  return 0;
+}
+
+int sagh_case_matrix_copy(void* h, int which, int* rp, int* ci, double* v) {
+  const SparseMatrix* m = pick(*static_cast<HostCase*>(h), which);
+  if (!m) {
+    g_err = "sagh_case_matrix_copy: no such matrix";
+    return 2;
+  }
+  std::memcpy(rp, m->row_offsets.data(), sizeof(int) * (m->nrows + 1));
+  std::memcpy(ci, m->col_indices.data(), sizeof(int) * m->nnz());
+  std::memcpy(v, m->values.data(), sizeof(double) * m->nnz());
+  return 0;
+}
+
+int sagh_case_rhs(void* h, double* rhs) {
+  const auto& r = static_cast<HostCase*>(h)->c.sys0.rhs;
+  std::memcpy(rhs, r.data(), sizeof(double) * r.size());
+  return 0;
+}
+
+// Drop-in end to end through the C++ adapter: gpu::DCPreconditioner +
+// gpu::solve_stokes on this case. rep = [converged, iterations], res = final
+// relative residual.
+int sagh_case_solve(void* h, int device, int nu, int restart, double tol, int max_iters,
+                    double eta_u, double eta_p, double omega0, double* x, int* rep, double* res) {
+  return guarded([&] {
+    auto& hc = *static_cast<HostCase*>(h);
+    gpu::Device dev(device);
+    SolverConfig cfg;
+    cfg.nu1 = cfg.nu2 = nu;
+    cfg.restart = restart;
+    cfg.tol = tol;
+    cfg.max_iters = max_iters;
+    cfg.eta_u = eta_u;
+    cfg.eta_p = eta_p;
+    cfg.omega0 = omega0;
+    cfg.enclosed_flow = hc.c.enclosed;
+    gpu::DCPreconditioner prec(dev, hc.c.sys0, hc.c.sys1, hc.c.transfer, cfg);
+    SolveResult r = gpu::solve_stokes(prec.k0(), hc.c.sys0.rhs, prec, cfg);
+    std::memcpy(x, r.x.data(), sizeof(double) * r.x.size());
+    rep[0] = r.report.converged ? 1 : 0;
+    rep[1] = r.report.iterations;
+    *res = r.report.final_relative_residual;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,110 @@
+// stokesamg_gpu.hpp -- drop-in GPU solve phase for the reference C++ API
+// (stokesamg, proj/core/include/stokesamg). A stokesamg user keeps building
+// meshes, systems and hierarchies with the reference library and swaps
+//
+//     stokesamg::DCPreconditioner  ->  stokesamg::gpu::DCPreconditioner
+//     stokesamg::solve_stokes      ->  stokesamg::gpu::solve_stokes
+//
+// Everything from factor_patches down (Vanka factorization and sweeps, SpMV,
+// V-cycle transfers, FGMRES vector work) then runs in libsag's sm_100a
+// kernels through the C-ABI in include/sag.h. Errors surface as the
+// reference's own exception classes (errors.hpp:8-58).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "sag.h"
+#include "stokesamg/errors.hpp"
+#include "stokesamg/preconditioner.hpp"
+
+namespace stokesamg::gpu {
+
+// Throws the stokesamg exception matching a libsag status code.
+void check(int status);
+
+// One CUDA device + stream (sag_ctx).
+class Device {
+ public:
+  explicit Device(int ordinal = 0);
+  ~Device();
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+  sag_ctx* handle() const { return ctx_; }
+
+ private:
+  sag_ctx* ctx_ = nullptr;
+};
+
+// Device copy of a stokesamg::SparseMatrix (sparse.hpp:11-28).
+class DeviceMatrix {
+ public:
+  DeviceMatrix(Device& dev, const SparseMatrix& m);
+  ~DeviceMatrix();
+  DeviceMatrix(const DeviceMatrix&) = delete;
+  DeviceMatrix& operator=(const DeviceMatrix&) = delete;
+  sag_matrix* handle() const { return h_; }
+  int nrows() const { return nrows_; }
+  int ncols() const { return ncols_; }
+
+ private:
+  sag_matrix* h_ = nullptr;
+  int nrows_ = 0, ncols_ = 0;
+};
+
+// spmv (sparse.hpp:42) on the device.
+std::vector<double> spmv(Device& dev, const DeviceMatrix& m, const std::vector<double>& x);
+
+// factor_patches (vanka.hpp:42-43) on the device; apply_vanka (vanka.hpp:47).
+class VankaFactorization {
+ public:
+  VankaFactorization(Device& dev, const DeviceMatrix& k, int n_x, int n_y, int n_p,
+                     bool sv_triples = false);
+  ~VankaFactorization();
+  VankaFactorization(const VankaFactorization&) = delete;
+  VankaFactorization& operator=(const VankaFactorization&) = delete;
+  sag_vanka* handle() const { return f_; }
+  size_t a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
+
+ private:
+  sag_vanka* f_ = nullptr;
+};
+std::vector<double> apply_vanka(Device& dev, const VankaFactorization& f,
+                                const std::vector<double>& r);
+
+// DCPreconditioner (preconditioner.hpp:77-100) with the same constructor
+// arguments as the reference. The low-order hierarchy is built by the
+// reference's build_monolithic_hierarchy on the host (setup, discrete and
+// rounding-sensitive: SURVEY.md H1), then uploaded once.
+class DCPreconditioner : public StokesPreconditioner {
+ public:
+  DCPreconditioner(Device& dev, const SaddleSystem& sys0, const SaddleSystem& sys1,
+                   TransferPair transfer, SolverConfig cfg);
+  ~DCPreconditioner() override;
+
+  std::vector<double> apply(const std::vector<double>& r) const override;
+  int size() const override { return k0_.nrows; }
+  int pressure_size() const override { return n_p0_; }
+  void set_parameters(double eta_u, double eta_p, double omega0);
+  const SolverConfig& config() const { return cfg_; }
+  const SparseMatrix& k0() const { return k0_; }
+  const MonolithicHierarchy& hierarchy() const { return h_; }
+  sag_dc* handle() const { return dc_; }
+  Device& device() const { return dev_; }
+
+ private:
+  Device& dev_;
+  SolverConfig cfg_;
+  SparseMatrix k0_;
+  int n_p0_ = 0;
+  MonolithicHierarchy h_;
+  std::vector<std::unique_ptr<DeviceMatrix>> mats_;
+  sag_dc* dc_ = nullptr;
+};
+
+// solve_stokes (preconditioner.hpp:147-148): the outer FGMRES with all
+// vectors resident on the device.
+SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
+                         const DCPreconditioner& prec, const SolverConfig& cfg);
+
+}  // namespace stokesamg::gpu

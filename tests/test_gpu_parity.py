@@ -1,0 +1,223 @@
+"""GPU parity of the sm_100a path against the reference (oracle/_ref) and the
+C restatement (oracle/), through the C-ABI (include/sag.h).
+
+Tolerances (north_star): Vanka apply and SpMV agree to 1e-12 relative,
+measured normwise ||y_gpu - y_ref||_inf / ||y_ref||_inf; FGMRES iteration
+counts agree within +-1 and both final relative residuals are <= rtol.
+Integer work (patch sets) and the stored factor payload (u_hat, b_hat, s_inv,
+weights: same elimination order, explicit round-to-nearest ops) are bitwise.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import ref_case
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def rel_inf(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    s = np.abs(b).max()
+    return np.abs(a - b).max() / (s if s > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2306_06795_b200 as S
+    return S
+
+
+@pytest.mark.parametrize("n", [8, 64])
+def test_spmv_all_levels(S, n):
+    c, d, k0, levels, _ = ref_case(n)
+    mats = [k0] + [l[0] for l in levels] + [l[1] for l in levels if l[1] is not None]
+    for m in mats:
+        x = O.splitmix64_uniform(m.ncols)
+        ref = O.RefMat.from_csr(m).spmv(x)
+        got = S.spmv(S.SparseMatrix.from_csr(m), x)
+        assert rel_inf(got, ref) <= TOL
+        # restatement is bitwise the reference
+        assert np.array_equal(O.Oracle.spmv(m, x), ref)
+
+
+def test_spmv_hand_product(S):
+    # tests/test_sparse.cpp:37-45
+    m = O.RefMat.from_triplets(3, 3, [0, 0, 1, 1, 2, 2], [0, 1, 1, 2, 0, 2],
+                               [1, 2, 3, 4, 5, 6]).csr()
+    y = S.spmv(S.SparseMatrix.from_csr(m), np.array([1.0, 2.0, 3.0]))
+    assert np.array_equal(y, [5.0, 18.0, 23.0])
+
+
+@pytest.mark.parametrize("n", [8, 64])
+def test_build_patches_exact(S, n):
+    c, d, k0, levels, _ = ref_case(n)
+    for k, nxyz in [(k0, d.nxyz0)] + [(l[0], l[2]) for l in levels[:-1]]:
+        ref = O.ref_build_patches(O.RefMat.from_csr(k), *nxyz)
+        got = S.build_patches(S.SparseMatrix.from_csr(k), *nxyz).export()
+        assert np.array_equal(got.pressure_ptr, ref.pptr)
+        assert np.array_equal(got.pressure, ref.pidx)
+        assert np.array_equal(got.velocity_ptr, ref.vptr)
+        assert np.array_equal(got.velocity, ref.vidx)
+        assert np.array_equal(got.nx, ref.nx)
+
+
+def test_build_patches_sv_triples(S):
+    c, d, k0, levels, _ = ref_case(4, sv=True, cfg=dict(omega0=0.78, eta_p=2.68))
+    ref = O.ref_build_patches(O.RefMat.from_csr(k0), *d.nxyz0, sv_triples=True)
+    got = S.build_patches(S.SparseMatrix.from_csr(k0), *d.nxyz0, sv_triples=True).export()
+    assert np.array_equal(got.velocity_ptr, ref.vptr)
+    assert np.array_equal(got.velocity, ref.vidx)
+    assert np.array_equal(got.pressure, ref.pidx)
+    assert np.array_equal(got.nx, ref.nx)
+    assert int(np.diff(ref.vptr).max() + 3) == 15  # tests/test_vanka.cpp:81-96
+
+
+@pytest.mark.parametrize("n", [8, 64])
+def test_factor_payload_bitwise(S, n):
+    c, d, k0, levels, _ = ref_case(n)
+    for k, nxyz in [(k0, d.nxyz0)] + [(l[0], l[2]) for l in levels[:-1]]:
+        rk = O.RefMat.from_csr(k)
+        rv = O.RefVanka.build(rk, *nxyz)
+        want = rv.factors()
+        K = S.SparseMatrix.from_csr(k)
+        p = S.build_patches(K, *nxyz)
+        f = S.factor_patches(K, p, nxyz[0] + nxyz[1])
+        got = f.export(p.export())
+        for key in ("uhat", "bhat", "sinv", "weights"):
+            assert np.array_equal(got[key], want[key]), key
+        assert f.a_factor_bytes == want["a_factor_bytes"]
+        assert f.aux_bytes == want["aux_bytes"]
+        assert f.dense_inverse_bytes == want["dense_inverse_bytes"]
+
+
+@pytest.mark.parametrize("n", [8, 64])
+def test_apply_vanka_parity(S, n):
+    c, d, k0, levels, _ = ref_case(n)
+    for k, nxyz in [(k0, d.nxyz0)] + [(l[0], l[2]) for l in levels[:-1]]:
+        rv = O.RefVanka.build(O.RefMat.from_csr(k), *nxyz)
+        K = S.SparseMatrix.from_csr(k)
+        f = S.factor_patches(K, S.build_patches(K, *nxyz), nxyz[0] + nxyz[1])
+        r = O.splitmix64_uniform(k.nrows)
+        assert rel_inf(S.apply_vanka(f, r), rv.apply(r)) <= TOL
+        z = S.apply_vanka(f, np.zeros(k.nrows))
+        assert np.all(z == 0.0)  # tests/test_vanka.cpp:264-271
+
+
+def test_apply_vanka_sv(S):
+    c, d, k0, levels, _ = ref_case(8, sv=True, cfg=dict(omega0=0.78, eta_p=2.68))
+    rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0, sv_triples=True)
+    K = S.SparseMatrix.from_csr(k0)
+    f = S.factor_patches(K, S.build_patches(K, *d.nxyz0, sv_triples=True),
+                         d.nxyz0[0] + d.nxyz0[1])
+    r = O.splitmix64_uniform(k0.nrows)
+    assert rel_inf(S.apply_vanka(f, r), rv.apply(r)) <= TOL
+
+
+def test_hand_factored_patch(S):
+    # tests/test_vanka.cpp:98-113
+    k = O.RefMat.from_triplets(3, 3, [0, 0, 1, 2], [0, 2, 1, 0], [1, 1, 1, 1]).csr()
+    K = S.SparseMatrix.from_csr(k)
+    p = S.Patches.from_lists([0, 1], [2], [0, 2], [0, 1], [1])
+    f = S.factor_patches(K, p, 2)
+    assert f.export(p.export())["sinv"][0] == -1.0
+    assert np.allclose(S.apply_vanka(f, np.array([1.0, 0.0, 1.0])), [1.0, 0.0, 0.0])
+
+
+def test_block_lu_random_patches(S):
+    # tests/test_vanka.cpp:115-155: block-LU patch solve == dense solve, 200 trials
+    rng = np.random.default_rng(42)
+    worst = 0.0
+    for _ in range(200):
+        ax = 0.3 * rng.uniform(-1, 1, (5, 5))
+        ay = 0.3 * rng.uniform(-1, 1, (5, 5))
+        A = np.zeros((12, 12))
+        A[:5, :5] = 0.5 * (ax + ax.T) + 4 * np.eye(5)
+        A[5:10, 5:10] = 0.5 * (ay + ay.T) + 4 * np.eye(5)
+        B = rng.uniform(-1, 1, (2, 10))
+        A[10:, :10] = B
+        A[:10, 10:] = B.T
+        r, cc = np.nonzero(A)
+        k = O.RefMat.from_triplets(12, 12, r, cc, A[r, cc]).csr()
+        K = S.SparseMatrix.from_csr(k)
+        p = S.Patches.from_lists([0, 2], [10, 11], [0, 10], list(range(10)), [5])
+        f = S.factor_patches(K, p, 10)
+        b = rng.uniform(-1, 1, 12)
+        x = S.apply_vanka(f, b)
+        ref = np.linalg.solve(A, b)
+        worst = max(worst, float(np.max(np.abs(x - ref) / np.maximum(1.0, np.abs(ref)))))
+    assert worst <= 1e-10
+
+
+def test_singular_patch_raises(S):
+    k = O.RefMat.from_triplets(3, 3, [0, 1, 2], [2, 1, 0], [1.0, 1.0, 1.0]).csr()
+    K = S.SparseMatrix.from_csr(k)
+    p = S.Patches.from_lists([0, 1], [2], [0, 2], [0, 1], [1])
+    with pytest.raises(S.SingularPatch):
+        S.factor_patches(K, p, 2)
+
+
+@pytest.mark.parametrize("mode,sweeps,omega", [(0, 1, 1.0), (0, 2, 1.0), (1, 3, 0.78)])
+def test_vanka_relax_parity(S, mode, sweeps, omega):
+    c, d, k0, levels, _ = ref_case(32)
+    rk = O.RefMat.from_csr(k0)
+    rv = O.RefVanka.build(rk, *d.nxyz0)
+    K = S.SparseMatrix.from_csr(k0)
+    f = S.factor_patches(K, S.build_patches(K, *d.nxyz0), d.nxyz0[0] + d.nxyz0[1])
+    x0 = np.sin(0.1 * np.arange(k0.nrows))
+    b = O.splitmix64_uniform(k0.nrows)
+    want = rv.relax(x0, b, mode, sweeps, omega)
+    got = S.vanka_relax(K, f, x0.copy(), b, mode, sweeps, omega)
+    assert rel_inf(got, want) <= 1e-11
+
+
+def test_relax_fixed_point(S):
+    # tests/test_vanka.cpp:214-233: b = K x => relaxation leaves x unchanged
+    c, d, k0, levels, _ = ref_case(8)
+    K = S.SparseMatrix.from_csr(k0)
+    f = S.factor_patches(K, S.build_patches(K, *d.nxyz0), d.nxyz0[0] + d.nxyz0[1])
+    x = np.sin(0.1 * np.arange(k0.nrows))
+    b = O.RefMat.from_csr(k0).spmv(x)
+    x1 = S.vanka_relax(K, f, x.copy(), b, 0, 2)
+    assert np.allclose(x1, x, rtol=1e-12, atol=1e-12)
+    x2 = S.vanka_relax(K, f, x.copy(), b, 1, 3, 0.0)
+    assert np.array_equal(x2, x)
+
+
+def _device_dc(S, k0, nxyz0, levels, conf, sv=False):
+    K0 = S.SparseMatrix.from_csr(k0)
+    lv = [(S.SparseMatrix.from_csr(k), S.SparseMatrix.from_csr(p) if p is not None else None,
+           nxyz) for k, p, nxyz in levels]
+    cfg = S.SolverConfig(nu1=conf["nu1"], nu2=conf["nu2"], restart=conf["restart"],
+                         tol=conf["tol"], max_iters=conf["max_iters"],
+                         enclosed_flow=conf["enclosed_flow"], eta_u=conf.get("eta_u", 1.0),
+                         eta_p=conf.get("eta_p", 1.0), omega0=conf.get("omega0", 1.0))
+    return K0, S.DCPreconditioner(K0, nxyz0, lv, cfg, sv=sv), cfg
+
+
+@pytest.mark.parametrize("n", [8, 32, 64])
+def test_dc_apply_parity(S, n):
+    c, d, k0, levels, conf = ref_case(n)
+    K0, dc, cfg = _device_dc(S, k0, d.nxyz0, levels, conf)
+    r = O.splitmix64_uniform(k0.nrows)
+    want = d.apply(r)
+    got = dc.apply(r)
+    assert rel_inf(got, want) <= 1e-9
+
+
+@pytest.mark.parametrize("n,its", [(32, 20), (64, 24)])
+def test_solve_stokes_cavity(S, n, its):
+    c, d, k0, levels, conf = ref_case(n)
+    K0, dc, cfg = _device_dc(S, k0, d.nxyz0, levels, conf)
+    rhs = c.rhs()
+    x_ref, rep_ref = d.solve(rhs)
+    assert rep_ref["iterations"] == its
+    x, rep = S.solve_stokes(K0, rhs, dc, cfg)
+    assert rep.converged
+    assert abs(rep.iterations - rep_ref["iterations"]) <= 1
+    assert rep.final_relative_residual <= cfg.tol
+    assert len(rep.residual_history) == rep.iterations + 1
+    assert rel_inf(x, x_ref) <= 1e-6
