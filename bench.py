@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 solve-phase hot path (BASELINE.json metric:
+"Vanka sweep + SpMV GDOF/s (frac. of HBM roofline); FGMRES solve s vs CPU").
+
+A step = one additive Vanka sweep (apply_vanka, vanka.cpp:151-184) plus one
+CSR SpMV (sparse.cpp:78-91) on the high-order operator K0 of BASELINE config 2
+(TH P2/P1 lid-driven cavity, 512x512 structured mesh), input x_i ~ U[-1,1)
+from splitmix64. value = total K0 DoFs processed per second
+by all ranks (GDOF/s). Inputs (K0 0.48 GB + Vanka factors 1.4 GB) exceed the
+126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
+  python bench.py --impl reference      # the reference's CPU path, host cores
+
+Multi-GPU (torchrun): every rank runs an independent replica of the config on
+its own GPU (weak scaling; the row-partitioned halo path is future work, see
+DESIGN.md). Times are CUDA events on libsag's stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    1: dict(workload="th_cavity_64x64", problem="cavity", sv=False, n=64),
+    2: dict(workload="th_cavity_512x512", problem="cavity", sv=False, n=512),
+    3: dict(workload="sv_cavity_256x256_barycentric", problem="cavity", sv=True, n=256,
+            omega0=0.78, eta_p=2.68),
+}
+METRIC = "Vanka sweep + SpMV GDOF/s (frac. of HBM roofline); FGMRES solve s vs CPU"
+
+
+def splitmix64_uniform(n, seed=0x5EED):
+    with np.errstate(over="ignore"):
+        z = (np.uint64(seed) ^ np.arange(n, dtype=np.uint64)) + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return ((z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53) * 2.0 - 1.0
+
+
+def peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={dev}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                      text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.15)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def dist_max(v, ws):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def spmv_bytes(nrows, ncols, nnz):
+    # 12 nnz + 4 (n_r + 1) + 8 n_c + 8 n_r
+    return 12 * nnz + 4 * (nrows + 1) + 8 * ncols + 8 * nrows
+
+
+def vanka_bytes(f, tot_idx, n):
+    # factors (a_factor + aux) + patch index lists + 24 n
+    return f.a_factor_bytes + f.aux_bytes + 4 * tot_idx + 24 * n
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_steps(k0csr, nxyz, steps, threads, budget_s=None):
+    """The reference's own spmv + apply_vanka (oracle/_ref) on `threads` host
+    threads, each running whole steps. Returns (steps_done, wall_s)."""
+    import oracle as O
+    rk = O.RefMat.from_csr(O.Csr(k0csr.nrows, k0csr.ncols, k0csr.rp, k0csr.ci, k0csr.v))
+    rv = O.RefVanka.build(rk, *nxyz)
+    x = splitmix64_uniform(k0csr.nrows)
+    rk.spmv(x)
+    rv.apply(x)  # warm
+    done = [0] * threads
+    t0 = time.perf_counter()
+    deadline = t0 + budget_s if budget_s else None
+
+    def worker(i):
+        todo = steps // threads + (1 if i < steps % threads else 0)
+        for _ in range(todo):
+            if deadline and time.perf_counter() > deadline and done[i] > 0:
+                break
+            rv.apply(x)
+            rk.spmv(x)
+            done[i] += 1
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(threads)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return sum(done), time.perf_counter() - t0
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    import oracle as O
+    cfg = CONFIGS[args.config]
+    t0 = time.perf_counter()
+    case = O.RefCase.build(cfg["problem"], cfg["sv"], "structured", cfg["n"])
+    k0 = case.k0().csr()
+    setup_s = time.perf_counter() - t0
+    threads = os.cpu_count() or 1
+    if args.warmup:
+        cpu_steps(k0, (case.n_x0, case.n_y0, case.n_p0), min(args.warmup, threads), threads)
+    done, wall = cpu_steps(k0, (case.n_x0, case.n_y0, case.n_p0), args.steps, threads)
+    val = done * k0.nrows / wall / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GDOF/s", "n_gpus": ws,
+        "steps": done, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(done, 1) * threads,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference build_case, splitmix64 input)",
+        "config": {"workload": cfg["workload"], "k0_rows": k0.nrows, "k0_nnz": k0.nnz},
+        "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": threads, "kind": "reference",
+                         "sample": f"{done} whole steps (apply_vanka + spmv on K0), "
+                                   f"{threads} threads x independent steps"},
+        "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "setup_s": setup_s,
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, ws, rank, local):
+    import torch
+
+    import paper_2306_06795_b200 as S
+    from paper_2306_06795_b200.cases import HostCase
+
+    cfg = CONFIGS[args.config]
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    t0 = time.perf_counter()
+    case = HostCase(cfg["problem"], cfg["sv"], "structured", cfg["n"])
+    k0 = case.k0()
+    host_setup_s = time.perf_counter() - t0
+    ctx = S.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+    t1 = time.perf_counter()
+    K0 = S.SparseMatrix.from_csr(k0, ctx)
+    patches = S.build_patches(K0, *case.nxyz0, sv_triples=case.sv)
+    f = S.factor_patches(K0, patches, case.n_x0 + case.n_y0)
+    ctx.synchronize()
+    factor_s = time.perf_counter() - t1
+    n = k0.nrows
+    tot_idx = patches.total_velocity + patches.total_pressure
+    x_host = splitmix64_uniform(n)
+    x = torch.from_numpy(x_host).to(dev)
+    delta = torch.empty(n, dtype=torch.float64, device=dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    lib = S.lib()
+
+    def step():
+        S.apply_vanka(f, x, out=delta)
+        S.spmv(K0, x, out=y)
+
+    def timed(fn, k):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / 1e3
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    ctx.synchronize()
+    clocks = ClockSampler(local)
+    barrier(ws)
+    ctx.synchronize()
+    launches0 = ctx.launch_count()
+    t_steps = timed(step, args.steps)
+    launches = ctx.launch_count() - launches0
+    ctx.synchronize()
+    barrier(ws)
+    t_steps = dist_max(t_steps, ws)
+
+    # per-kernel breakdown (same stream, CUDA events)
+    xp, dp = S.C.c_void_p(x.data_ptr()), S.C.c_void_p(delta.data_ptr())
+    kper = max(args.steps // 2, 10)
+    t_patch = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 1)), kper) / kper
+    t_gather = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 2)), kper) / kper
+    t_vanka = timed(lambda: S.apply_vanka(f, x, out=delta), kper) / kper
+    t_spmv = timed(lambda: S.spmv(K0, x, out=y), kper) / kper
+    clk = clocks.stop()
+
+    # e2e: the same step through the C-ABI with pinned HOST buffers
+    xh = torch.from_numpy(x_host).pin_memory().numpy()
+    dh = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    yh = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    for _ in range(2):
+        S.apply_vanka(f, xh, out=dh)
+        S.spmv(K0, xh, out=yh)
+    barrier(ws)
+    ke = max(args.steps // 4, 5)
+    te0 = time.perf_counter()
+    for _ in range(ke):
+        S.apply_vanka(f, xh, out=dh)
+        S.spmv(K0, xh, out=yh)
+    t_e2e = dist_max((time.perf_counter() - te0) / ke, ws)
+
+    peak, peak_kind = peak_hbm()
+    b_v = vanka_bytes(f, tot_idx, n)
+    b_s = spmv_bytes(n, n, k0.nnz)
+    ms_step = 1e3 * t_steps / args.steps
+    value = ws * n / (t_steps / args.steps) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference build_case cavity + splitmix64 x (SURVEY 8(d))",
+        "config": {"workload": cfg["workload"], "k0_rows": n, "k0_nnz": k0.nnz,
+                   "patches": f.npatch, "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                   "l2": "inputs (K0 + factors ~1.9 GB) exceed L2; no flush"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "vanka sweep (patch + gather)",
+                     "achieved": b_v / t_vanka / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": b_v / t_vanka / 1e9 / peak, "traffic": None,
+                     "algorithmic_bytes": b_v, "peak_kind": peak_kind},
+        "kernels": {
+            "vanka_sweep_us": 1e6 * t_vanka, "vanka_patch_us": 1e6 * t_patch,
+            "vanka_gather_us": 1e6 * t_gather, "spmv_us": 1e6 * t_spmv,
+            "vanka_gdofs": n / t_vanka / 1e9, "spmv_gdofs": n / t_spmv / 1e9,
+            "spmv_bytes": b_s, "spmv_gbs": b_s / t_spmv / 1e9,
+            "spmv_frac": b_s / t_spmv / 1e9 / peak,
+            "vanka_device_bytes": f.device_bytes,
+        },
+        "e2e": {"value": ws * n / t_e2e / 1e9, "unit": "GDOF/s",
+                "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n},
+        "setup": {"host_reference_setup_s": host_setup_s, "gpu_patch_factor_s": factor_s},
+    }
+    if clk:
+        out["clocks"] = clk
+
+    if not args.no_solve:
+        scfg = S.SolverConfig(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
+                              enclosed_flow=case.enclosed, eta_u=cfg.get("eta_u", 1.0),
+                              eta_p=cfg.get("eta_p", 1.0), omega0=cfg.get("omega0", 1.0))
+        K0s, dc, _ = case.device(scfg, ctx)
+        rhs = case.rhs()
+        S.solve_stokes(K0s, rhs, dc, scfg)  # warm (graph capture)
+        barrier(ws)
+        ts = time.perf_counter()
+        xs, rep = S.solve_stokes(K0s, rhs, dc, scfg)
+        t_solve = dist_max(time.perf_counter() - ts, ws)
+        out["solve"] = {"gpu_s": t_solve, "iterations": rep.iterations,
+                        "final_relative_residual": rep.final_relative_residual,
+                        "converged": rep.converged,
+                        "reference_cpu_s_1core": {1: 1.21, 2: 152.9, 3: 178.0}.get(args.config),
+                        "reference_cpu_note": "BASELINE.md 2 (1 core, measured at survey time)",
+                        "dc_info": dc.info()}
+
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        done, wall = cpu_steps(k0, case.nxyz0, 4 * threads, threads, budget_s=20.0)
+        cpuv = done * n / wall / 1e9
+        out["cpu_baseline"] = {"value": cpuv, "unit": "GDOF/s", "cores": threads,
+                               "kind": "reference",
+                               "sample": f"{done} whole steps (apply_vanka + spmv on K0) of the "
+                                         f"reference build (oracle/_ref), {threads} threads"}
+    if rank == 0:
+        print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -116,6 +116,12 @@ int sag_vanka_export(sag_ctx* ctx, const sag_vanka* f, double* u_hat, double* b_
  * vanka.cpp:151-184). */
 int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta);
 
+/* One stage of sag_apply_vanka, for per-kernel timing (device pointers):
+ * stage 1 = patch kernel (local solves into the slot buffer),
+ * stage 2 = owner-computes gather (slots -> delta). */
+int sag_apply_vanka_stage(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta,
+                          int stage);
+
 /* Replaces vanka_relax (vanka.hpp:49-55; vanka.cpp:186-209). */
 enum sag_relax_mode { SAG_RELAX_KRYLOV_WRAPPED = 0, SAG_RELAX_STATIONARY = 1 };
 int sag_vanka_relax(sag_ctx* ctx, const sag_matrix* k, const sag_vanka* f, double* x,

@@ -193,7 +193,7 @@ class Oracle:
     @staticmethod
     def build_patches(k: Csr, n_x, n_y, n_p, sv_triples=False):
         p = or_patches()
-        _ocheck(olib().or_build_patches(C.byref(_ocsr(k)), n_x, n_y, n_p, int(sv_triples),
+        _ocheck(olib().or_build_patches(C.byref(_ocsr(k)), int(n_x), int(n_y), int(n_p), int(sv_triples),
                                         C.byref(p)))
         out = _patches_to_np(p)
         olib().or_patches_free(C.byref(p))
@@ -233,7 +233,7 @@ class OracleVanka:
         self._k = k
         self._patches = patches
         self.f = or_vanka()
-        _ocheck(olib().or_factor_patches(C.byref(_ocsr(k)), C.byref(patches.to_c()), n_u,
+        _ocheck(olib().or_factor_patches(C.byref(_ocsr(k)), C.byref(patches.to_c()), int(n_u),
                                          C.byref(self.f)))
         self.n = k.nrows
 
@@ -253,7 +253,7 @@ class OracleVanka:
         x = np.array(x, dtype=np.float64)
         b = np.ascontiguousarray(b, dtype=np.float64)
         _ocheck(olib().or_vanka_relax(C.byref(_ocsr(self._k)), C.byref(self.f), dp(x), dp(b),
-                                      int(mode), int(sweeps), float(omega)))
+                                      int(mode), int(sweeps), C.c_double(omega)))
         return x
 
     def factors(self):
@@ -287,7 +287,7 @@ class OracleDC:
                       cfg.get("max_iters", 500), int(cfg.get("enclosed_flow", True)))
         self.d = or_dc()
         self.n = k0.nrows
-        _ocheck(olib().or_dc_setup(C.byref(self.d), C.byref(_ocsr(k0)), *nxyz0, int(sv), L,
+        _ocheck(olib().or_dc_setup(C.byref(self.d), C.byref(_ocsr(k0)), *[int(v) for v in nxyz0], int(sv), L,
                                    ks, ps, ip(nxyz), C.byref(c)))
 
     def __del__(self):

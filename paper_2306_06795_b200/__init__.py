@@ -132,6 +132,7 @@ SIGNATURES = {
     "sag_vanka_stats": (C.c_int, [vp, i64p]),
     "sag_vanka_export": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "sag_apply_vanka": (C.c_int, [vp, vp, vp, vp]),
+    "sag_apply_vanka_stage": (C.c_int, [vp, vp, vp, vp, C.c_int]),
     "sag_vanka_relax": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_double]),
     "sag_fgmres": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, C.POINTER(sag_fgmres_options),
                              C.POINTER(sag_krylov_report), vp, C.c_int]),

@@ -1,0 +1,150 @@
+"""Reference-built inputs of the GPU path (the host application side).
+
+The reference keeps mesh generation, FEM assembly and the SA hierarchy setup in
+its own host C++ (north_star; the setup is discrete and
+rounding-sensitive). ``libsag_stokesamg.so`` links the reference library
+(compiled from its sources by hostapp/Makefile) and exposes
+build_case + assemble_saddle_matrix + build_monolithic_hierarchy as ``sagh_*``
+entry points; this module turns their output into device matrices for the
+Python mirror of the solver API.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import DCPreconditioner, SolverConfig, SparseMatrix, Context, HERE
+
+_HLIB = os.path.join(HERE, "libsag_stokesamg.so")
+_h = None
+
+
+def hlib():
+    global _h
+    if _h is None:
+        if not os.path.exists(_HLIB):
+            raise RuntimeError(f"{_HLIB} missing: run __graft_entry__.build()")
+        L = C.CDLL(_HLIB)
+        L.sagh_case_build.restype = C.c_void_p
+        L.sagh_case_build.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_int, C.c_char_p,
+                                      C.c_int, C.c_double, C.c_double]
+        L.sagh_case_free.argtypes = [C.c_void_p]
+        L.sagh_last_error.restype = C.c_char_p
+        L.sagh_case_info.argtypes = [C.c_void_p, C.c_void_p]
+        L.sagh_case_level.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.sagh_case_matrix_shape.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                             C.c_void_p]
+        L.sagh_case_matrix_copy.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]
+        L.sagh_case_rhs.argtypes = [C.c_void_p, C.c_void_p]
+        L.sagh_case_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                      C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]
+        _h = L
+    return _h
+
+
+@dataclass
+class Csr:
+    nrows: int
+    ncols: int
+    rp: np.ndarray
+    ci: np.ndarray
+    v: np.ndarray
+
+    @property
+    def nnz(self):
+        return int(self.rp[-1])
+
+
+class HostCase:
+    """build_case (experiments.cpp:215-235) + K0 + low-order hierarchy."""
+
+    def __init__(self, problem="cavity", sv=False, mesh_kind="structured", n=64, mesh_path=None,
+                 coarse_size=0, k1=0.0, k2=0.0):
+        h = hlib().sagh_case_build(problem.encode(), int(sv), mesh_kind.encode(), int(n),
+                                   mesh_path.encode() if mesh_path else None, int(coarse_size),
+                                   float(k1), float(k2))
+        if not h:
+            raise RuntimeError("sagh_case_build: " + hlib().sagh_last_error().decode())
+        self.h = C.c_void_p(h)
+        info = np.zeros(7, dtype=np.int64)
+        hlib().sagh_case_info(self.h, info.ctypes.data)
+        (self.n_x0, self.n_y0, self.n_p0, self.nlevels, enc, sv_, self.n_scalar) = (
+            int(v) for v in info)
+        self.enclosed, self.sv = bool(enc), bool(sv_)
+        self.n0 = self.n_x0 + self.n_y0 + self.n_p0
+        self.nxyz0 = (self.n_x0, self.n_y0, self.n_p0)
+
+    def __del__(self):
+        try:
+            hlib().sagh_case_free(self.h)
+        except Exception:
+            pass
+
+    def matrix(self, which: int) -> Csr:
+        nr, nc, nnz = C.c_int(), C.c_int(), C.c_longlong()
+        rc = hlib().sagh_case_matrix_shape(self.h, which, C.byref(nr), C.byref(nc), C.byref(nnz))
+        if rc:
+            raise RuntimeError(hlib().sagh_last_error().decode())
+        rp = np.empty(nr.value + 1, dtype=np.int32)
+        ci = np.empty(nnz.value, dtype=np.int32)
+        v = np.empty(nnz.value)
+        hlib().sagh_case_matrix_copy(self.h, which, rp.ctypes.data, ci.ctypes.data, v.ctypes.data)
+        return Csr(nr.value, nc.value, rp, ci, v)
+
+    def k0(self) -> Csr:
+        return self.matrix(0)
+
+    def level(self, l):
+        nxyz = np.zeros(3, dtype=np.int32)
+        hlib().sagh_case_level(self.h, l, nxyz.ctypes.data)
+        k = self.matrix(1 + 2 * l)
+        p = self.matrix(2 + 2 * l) if l + 1 < self.nlevels else None
+        return k, p, tuple(int(v) for v in nxyz)
+
+    def levels(self):
+        return [self.level(l) for l in range(self.nlevels)]
+
+    def rhs(self):
+        r = np.empty(self.n0)
+        hlib().sagh_case_rhs(self.h, r.ctypes.data)
+        return r
+
+    def device(self, cfg: SolverConfig, ctx: Context = None, keep_host=False):
+        """(K0, DCPreconditioner, host levels) uploaded through the C-ABI."""
+        k0 = self.k0()
+        K0 = SparseMatrix.from_csr(k0, ctx)
+        lv = []
+        host = []
+        for k, p, nxyz in self.levels():
+            lv.append((SparseMatrix.from_csr(k, ctx),
+                       SparseMatrix.from_csr(p, ctx) if p is not None else None, nxyz))
+            if keep_host:
+                host.append((k, p, nxyz))
+        dc = DCPreconditioner(K0, self.nxyz0, lv, cfg, sv=self.sv)
+        if self.sv:
+            pd = SparseMatrix.from_csr(self.matrix(1000), ctx)
+            mm = SparseMatrix.from_csr(self.matrix(1001), ctx)
+            A = [SparseMatrix.from_csr(self.matrix(1002 + 2 * s), ctx)
+                 for s in range(self.n_scalar)]
+            P = [SparseMatrix.from_csr(self.matrix(1003 + 2 * s), ctx)
+                 for s in range(self.n_scalar - 1)]
+            dc.set_sv_transfer(pd, mm, A, P)
+        return K0, dc, (k0, host)
+
+    def solve_dropin(self, device=0, nu=1, restart=30, tol=1e-8, max_iters=500, eta_u=1.0,
+                     eta_p=1.0, omega0=1.0):
+        """The C++ drop-in (gpu::DCPreconditioner + gpu::solve_stokes) end to end."""
+        x = np.empty(self.n0)
+        rep = np.zeros(2, dtype=np.int32)
+        res = C.c_double()
+        rc = hlib().sagh_case_solve(self.h, device, nu, restart, tol, max_iters, eta_u, eta_p,
+                                    omega0, x.ctypes.data, rep.ctypes.data, C.byref(res))
+        if rc:
+            raise RuntimeError(hlib().sagh_last_error().decode())
+        return x, dict(converged=bool(rep[0]), iterations=int(rep[1]),
+                       final_relative_residual=res.value)

@@ -164,6 +164,7 @@ void launch_axpy(Ctx& c, int n, double* x, double omega, const double* d);
 // omega*delta into xadd instead of storing delta (vanka.cpp:195).
 void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta,
                  const int* gate = nullptr);
+void vanka_apply_stage(Ctx& c, const Vanka& f, const double* r, double* delta, int stage);
 void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega);
 std::unique_ptr<Patches> build_patches_dev(Ctx& c, const Matrix& k, int n_x, int n_y, int n_p,
                                            bool sv_triples);

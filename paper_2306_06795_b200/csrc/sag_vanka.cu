@@ -789,6 +789,17 @@ void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta, const i
   SAG_LAUNCHED(c);
 }
 
+void vanka_apply_stage(Ctx& c, const Vanka& f, const double* r, double* delta, int stage) {
+  if (stage == 1) {
+    launch_patch_any(c, f, r, nullptr);
+  } else {
+    vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(f.n, f.dof_ptr.p, f.dof_slot.p,
+                                                                f.out.p, f.w.p, delta, nullptr,
+                                                                1.0, nullptr);
+    SAG_LAUNCHED(c);
+  }
+}
+
 void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega) {
   launch_patch_any(c, f, r, nullptr);
   vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(f.n, f.dof_ptr.p, f.dof_slot.p,
@@ -952,6 +963,18 @@ int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* d
     OutVec d(c, delta, f->f.n, 1, false);
     vanka_apply(c, f->f, ri.d, d.d);
     d.finish();
+  });
+}
+
+int sag_apply_vanka_stage(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta,
+                          int stage) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    SAG_REQUIRE(stage == 1 || stage == 2, SAG_CONFIG_ERROR, "stage must be 1 or 2");
+    SAG_REQUIRE(is_device_ptr(r) && is_device_ptr(delta), SAG_INVALID_ARGUMENT,
+                "sag_apply_vanka_stage takes device pointers");
+    vanka_apply_stage(ctx->c, f->f, r, delta, stage);
   });
 }
 
