@@ -21,7 +21,14 @@ struct Matrix {
   DevBuf<double> v;
   int group = 8;
   double norm_inf = -1.0;  // cached (sparse.cpp:229-237)
+  // row chunks of the streaming SpMV: chunk c covers rows [chunk_row[c],
+  // chunk_row[c+1]) with at most kChunkNnz entries (0 chunks: vector kernel)
+  DevBuf<int> chunk_row;
+  int nchunks = 0;
 };
+constexpr int kChunkNnz = 4096;
+constexpr int kChunkRows = 512;
+void build_chunks(Ctx& c, Matrix& m);
 
 // Vanka patch sets (vanka.hpp:11-15), CSR-like on device.
 struct Patches {
@@ -55,6 +62,7 @@ struct Vanka {
   DevBuf<int> dof_slot;   // nslots
   long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
   long long blob_bytes = 0;
+  bool sym = false;  // A^-1 blocks stored as packed symmetrised upper triangles
 };
 
 // Krylov scalar state in device memory (one per FGMRES instance); mirrors the
@@ -171,7 +179,7 @@ std::unique_ptr<Patches> build_patches_dev(Ctx& c, const Matrix& k, int n_x, int
 std::unique_ptr<Patches> patches_from_lists(Ctx& c, int npatch, const int* pptr,
                                             const int* pidx, const int* vptr, const int* vidx,
                                             const int* nx);
-std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches& p);
+std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches& p, int n_u);
 // the reference's factor layout, for parity tests (vanka.hpp:31-33)
 void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* sinv,
                   double* weights);

@@ -215,8 +215,119 @@ static void spmv_dispatch_e(Ctx& c, const Matrix& m, const double* x, double* y,
   SAG_LAUNCHED(c);
 }
 
+// Streaming CSR SpMV: a CTA takes a chunk of consecutive rows holding at most
+// kChunkNnz entries, streams the chunk's values/columns fully coalesced
+// (evict-first: K is read once per product, x stays in L2) while gathering x,
+// keeps the products in shared memory, then one thread per row sums its
+// products in column order -- the reference's order (sparse.cpp:85-88), so
+// with the product rounded before the sum the result is bitwise the
+// reference's. Only two dependent memory round trips per chunk, ~16
+// independent loads in flight per thread.
+template <Epi E>
+__global__ void __launch_bounds__(256) spmv_stream_kernel(
+    int nchunks, const int* __restrict__ chunk_row, const int* __restrict__ rp,
+    const int* __restrict__ ci, const double* __restrict__ val, const double* __restrict__ x,
+    double* __restrict__ y, SpmvArgs a, double* partials, unsigned* ticket) {
+  if (a.gate && *a.gate) return;
+  constexpr bool kRed = (E == Epi::StoreDot || E == Epi::ResidSsq);
+  __shared__ double prod[kChunkNnz];
+  __shared__ int srp[kChunkRows + 1];
+  double red = 0.0;
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int r0 = chunk_row[ch], nr = chunk_row[ch + 1] - r0;
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) srp[i] = rp[r0 + i];
+    __syncthreads();
+    const int k0 = srp[0], k1 = srp[nr];
+#pragma unroll 4
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x)
+      prod[k - k0] = __dmul_rn(__ldcs(val + k), __ldg(x + __ldcs(ci + k)));
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+      double s = 0.0;
+      const int e = srp[i + 1] - k0;
+      for (int k = srp[i] - k0; k < e; ++k) s = __dadd_rn(s, prod[k]);
+      const int row = r0 + i;
+      if constexpr (E == Epi::Store) {
+        y[row] = s;
+      } else if constexpr (E == Epi::Resid) {
+        y[row] = a.b[row] - s;
+      } else if constexpr (E == Epi::ResidEta) {
+        y[row] = (row < a.n_u ? a.eta_u : a.eta_p) * (a.b[row] - s);
+      } else if constexpr (E == Epi::Add) {
+        y[row] = y[row] + s;
+      } else if constexpr (E == Epi::StoreDot) {
+        y[row] = s;
+        red = fma(s, a.dotv[row], red);
+      } else if constexpr (E == Epi::ResidSsq) {
+        const double r = a.b[row] - s;
+        y[row] = r;
+        red = fma(r, r, red);
+      }
+    }
+    __syncthreads();
+  }
+  if constexpr (kRed) reduce_finish(red, a.fin, partials, ticket);
+}
+
+static void spmv_stream(Ctx& c, const Matrix& m, const double* x, double* y, Epi e,
+                        const SpmvArgs& a) {
+  const char* env_ctas = getenv("SAG_SPMV_CTAS");
+  const int ctas_per_sm = env_ctas ? atoi(env_ctas) : 6;
+  const int grid = std::max(1, std::min(m.nchunks, std::min(c.num_sms * ctas_per_sm, kMaxRedGrid)));
+  switch (e) {
+#define CASE(EE)                                                                               \
+  case Epi::EE:                                                                                \
+    spmv_stream_kernel<Epi::EE><<<grid, 256, 0, c.stream>>>(m.nchunks, m.chunk_row.p, m.rp.p,  \
+                                                            m.ci.p, m.v.p, x, y, a,            \
+                                                            c.partials.p, c.ticket.p);         \
+    break;
+    CASE(Store)
+    CASE(Resid)
+    CASE(ResidEta)
+    CASE(Add)
+    CASE(StoreDot)
+    CASE(ResidSsq)
+#undef CASE
+  }
+  SAG_LAUNCHED(c);
+}
+
+// Greedy row chunks of <= kChunkNnz entries and <= kChunkRows rows; a row
+// longer than a chunk leaves the matrix on the G-lanes-per-row kernel.
+void build_chunks(Ctx& c, Matrix& m) {
+  m.nchunks = 0;
+  if (m.nrows == 0) return;
+  // opt-in for now: measured slower than the G-lanes kernel on K0 (175 vs 142 us)
+  const char* e = getenv("SAG_SPMV_STREAM");
+  if (!e || atoi(e) == 0) return;
+  std::vector<int> rp(m.nrows + 1);
+  SAG_CUDA(cudaMemcpyAsync(rp.data(), m.rp.p, sizeof(int) * (m.nrows + 1), cudaMemcpyDeviceToHost,
+                           c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  std::vector<int> ch{0};
+  int r0 = 0;
+  for (int r = 0; r < m.nrows; ++r) {
+    const int len = rp[r + 1] - rp[r];
+    if (len > kChunkNnz) return;
+    if (rp[r + 1] - rp[r0] > kChunkNnz || r - r0 >= kChunkRows) {
+      ch.push_back(r);
+      r0 = r;
+    }
+  }
+  ch.push_back(m.nrows);
+  m.chunk_row.alloc(ch.size());
+  SAG_CUDA(cudaMemcpyAsync(m.chunk_row.p, ch.data(), sizeof(int) * ch.size(),
+                           cudaMemcpyHostToDevice, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  m.nchunks = (int)ch.size() - 1;
+}
+
 void launch_spmv(Ctx& c, const Matrix& m, const double* x, double* y, Epi e, const SpmvArgs& a) {
   if (m.nrows == 0) return;
+  if (m.nchunks > 0) {
+    spmv_stream(c, m, x, y, e, a);
+    return;
+  }
   switch (m.group) {
     case 2: spmv_dispatch_e<2>(c, m, x, y, e, a); break;
     case 4: spmv_dispatch_e<4>(c, m, x, y, e, a); break;
@@ -580,6 +691,7 @@ std::unique_ptr<Matrix> transpose_dev(Ctx& c, const Matrix& a) {
   SAG_LAUNCHED(c);
   SAG_CUDA(cudaStreamSynchronize(c.stream));
   t->group = pick_group(t->nnz, t->nrows);
+  build_chunks(c, *t);
   return t;
 }
 
@@ -620,6 +732,7 @@ std::unique_ptr<Matrix> matrix_upload(Ctx& c, int nrows, int ncols, long long nn
   SAG_REQUIRE(!(hb & 4), SAG_ERROR,
               "sag_matrix_create: rows must be canonical (strictly increasing columns)");
   m->group = pick_group(nnz, nrows);
+  build_chunks(c, *m);
   return m;
 }
 

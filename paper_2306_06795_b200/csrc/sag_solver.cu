@@ -737,7 +737,7 @@ void dc_setup(Ctx& c, Dc& d, const Matrix* k0, int n_x0, int n_y0, int n_p0, int
   // fine-level Vanka (preconditioner.cpp:95-97)
   {
     auto p = build_patches_dev(c, *k0, n_x0, n_y0, n_p0, d.sv);
-    d.fine = factor_patches_dev(c, *k0, *p);
+    d.fine = factor_patches_dev(c, *k0, *p, n_x0 + n_y0);
   }
   if (!d.sv) d.fine_kry.init(d.n0, mrelax, 0);
   d.fine_r.alloc(d.n0);
@@ -762,7 +762,7 @@ void dc_setup(Ctx& c, Dc& d, const Matrix* k0, int n_x0, int n_y0, int n_p0, int
       SAG_REQUIRE(L.P->nrows == L.n && L.P->ncols == levels[l + 1].k->m.nrows,
                   SAG_DIMENSION_MISMATCH, "sag_dc_create: prolongator shape mismatch");
       auto p = build_patches_dev(c, *L.K, L.n_x, L.n_y, L.n_p, false);
-      L.vanka = factor_patches_dev(c, *L.K, *p);
+      L.vanka = factor_patches_dev(c, *L.K, *p, L.n_x + L.n_y);
       L.R = transpose_dev(c, *L.P);
       L.kry.init(L.n, mrelax, 0);
       L.r.alloc(L.n);

@@ -279,18 +279,26 @@ __device__ __forceinline__ void lu_solve_lane(const double* LU, int n, int ld, d
   }
 }
 
+// Entries stored for one A^-1 block of order n: full column-major, or the
+// symmetrised upper triangle packed column by column (column j = rows 0..j at
+// offset j(j+1)/2) when the level's velocity block is symmetric.
+__host__ __device__ __forceinline__ long long ainv_len(long long n, bool sym) {
+  return sym ? n * (n + 1) / 2 : n * n;
+}
+
 struct FactorLayout {
   int D, NV, NP;  // max dim, max nv, max np
   int bytes;      // per warp
   __host__ __device__ FactorLayout(int d, int nv, int np) : D(d), NV(nv), NP(np) {
-    size_t dbl = 2 * (size_t)D * D + 2 * (size_t)NP * NV + (size_t)NP * NP + 32 * (size_t)D;
+    size_t dbl = 3 * (size_t)D * D + 2 * (size_t)NP * NV + (size_t)NP * NP +
+                 (size_t)(32 + NP) * (size_t)(D > NP ? D : NP);
     size_t ints = (size_t)NV + 2 * (size_t)D + NP;
     bytes = (int)(((dbl * 8 + ints * 4) + 15) / 16 * 16);
   }
 };
 
 __global__ void __launch_bounds__(256) factor_kernel(
-    int npatch, int D, int NV, int NP, int wbytes, const int* __restrict__ rp,
+    int npatch, int D, int NV, int NP, int wbytes, int sym, const int* __restrict__ rp,
     const int* __restrict__ ci, const double* __restrict__ kv, const int* __restrict__ pptr,
     const int* __restrict__ pidx, const int* __restrict__ vptr, const int* __restrict__ vidx,
     const int* __restrict__ nxs, const long long* __restrict__ off, const int* __restrict__ sbase,
@@ -298,17 +306,19 @@ __global__ void __launch_bounds__(256) factor_kernel(
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned char* base = smem + (size_t)wib * wbytes;
+  const int DX = D > NP ? D : NP;
   double* Ax = reinterpret_cast<double*>(base);
   double* Ay = Ax + (size_t)D * D;
-  double* Bm = Ay + (size_t)D * D;   // NP x NV  [a*NV + m]
-  double* Um = Bm + (size_t)NP * NV; // NV x NP  [m*NP + a] (u_hat row-major)
-  double* Sm = Um + (size_t)NV * NP; // NP x NP
-  double* W = Sm + (size_t)NP * NP;  // 32 lanes x D
-  int* sv = reinterpret_cast<int*>(W + 32 * (size_t)D);
+  double* Winv = Ay + (size_t)D * D;  // D x D inverse columns [c*D + i]
+  double* Bm = Winv + (size_t)D * D;  // NP x NV  [a*NV + m]
+  double* Um = Bm + (size_t)NP * NV;  // NV x NP  [m*NP + a] (u_hat row-major)
+  double* Sm = Um + (size_t)NV * NP;  // NP x NP
+  double* W = Sm + (size_t)NP * NP;   // (32 + NP) lanes x DX solve scratch
+  int* sv = reinterpret_cast<int*>(W + (size_t)(32 + NP) * DX);
   int* pivx = sv + NV;
   int* pivy = pivx + D;
   int* spiv = pivy + D;
-  double* xw = W + (size_t)lane * D;
+  double* xw = W + (size_t)lane * DX;
 
   const int gw = blockIdx.x * (blockDim.x >> 5) + wib;
   const int nw = gridDim.x * (blockDim.x >> 5);
@@ -355,13 +365,14 @@ __global__ void __launch_bounds__(256) factor_kernel(
     }
     unsigned char* bl = blob + off[k];
     double* gAx = reinterpret_cast<double*>(bl + 16);
-    double* gAy = gAx + (size_t)nx * nx;
-    double* gU = gAy + (size_t)ny * ny;
+    double* gAy = gAx + ainv_len(nx, sym);
+    double* gU = gAy + ainv_len(ny, sym);
     double* gB = gU + (size_t)np * nv;
     double* gS = gB + (size_t)np * nv;
     int* gidx = reinterpret_cast<int*>(gS + (size_t)np * np);
-    // per component: RHS t < n are unit vectors (inverse columns), t = n + j
-    // are -B(j, comp)^T (u_hat columns, vanka.cpp:99-111)
+    // per component: RHS t < n are unit vectors (inverse columns, each one
+    // dense_lu_solve(lu, e_t)), t = n + j are -B(j, comp)^T (u_hat columns,
+    // vanka.cpp:99-111)
     for (int comp = 0; comp < 2; ++comp) {
       const int n = comp == 0 ? nx : ny;
       const int c0 = comp == 0 ? 0 : nx;
@@ -372,20 +383,27 @@ __global__ void __launch_bounds__(256) factor_kernel(
       for (int t0 = 0; t0 < n + np; t0 += 32) {
         const int t = t0 + lane;
         if (t < n + np) {
+          double* x = (t < n) ? Winv + (size_t)t * D : xw;
           for (int i = 0; i < n; ++i) {
             const int src = pv[i];
-            xw[i] = (t < n) ? (src == t ? 1.0 : 0.0) : -Bm[(t - n) * NV + c0 + src];
+            x[i] = (t < n) ? (src == t ? 1.0 : 0.0) : -Bm[(t - n) * NV + c0 + src];
           }
-          lu_solve_lane(LU, n, D, xw);
-          if (t < n) {
-            for (int i = 0; i < n; ++i) gA[(size_t)t * n + i] = xw[i];
-          } else {
-            for (int i = 0; i < n; ++i) Um[(c0 + i) * NP + (t - n)] = xw[i];
-          }
+          lu_solve_lane(LU, n, D, x);
+          if (t >= n)
+            for (int i = 0; i < n; ++i) Um[(c0 + i) * NP + (t - n)] = x[i];
         }
       }
+      __syncwarp();
+      if (sym) {
+        // symmetrised upper triangle, packed by columns
+        for (int c = 0; c < n; ++c)
+          for (int i = lane; i <= c; i += 32)
+            gA[(size_t)c * (c + 1) / 2 + i] = 0.5 * (Winv[(size_t)c * D + i] + Winv[(size_t)i * D + c]);
+      } else {
+        for (int e = lane; e < n * n; e += 32) gA[e] = Winv[(size_t)(e / n) * D + (e % n)];
+      }
+      __syncwarp();
     }
-    __syncwarp();
     // S = B u_hat (vanka.cpp:112-119)
     for (int e = lane; e < np * np; e += 32) {
       const int a = e / np, cc = e % np;
@@ -463,7 +481,50 @@ static int grid_for(Ctx& c, long long n) {
   return (int)std::max(1LL, std::min((n + 255) / 256, (long long)c.num_sms * 16));
 }
 
-std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches& p) {
+// Relative asymmetry of the velocity block K[0:n_u, 0:n_u]: max |a_ij - a_ji|
+// and max |a_ij| (as ordered uint64 bit patterns of non-negative doubles).
+__global__ void asym_kernel(int n_u, const int* rp, const int* ci, const double* v,
+                            unsigned long long* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_u; i += gridDim.x * blockDim.x) {
+    double dmax = 0.0, amax = 0.0;
+    for (int q = rp[i]; q < rp[i + 1]; ++q) {
+      const int j = ci[q];
+      if (j >= n_u) break;
+      amax = fmax(amax, fabs(v[q]));
+      if (j <= i) continue;
+      int lo = rp[j], hi = rp[j + 1];
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ci[mid] < i) lo = mid + 1; else hi = mid;
+      }
+      const double vt = (lo < rp[j + 1] && ci[lo] == i) ? v[lo] : 0.0;
+      dmax = fmax(dmax, fabs(v[q] - vt));
+    }
+    atomicMax(out, (unsigned long long)__double_as_longlong(dmax));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(amax));
+  }
+}
+
+// A^-1 is stored as its symmetrised upper triangle when the velocity block is
+// symmetric to 1e-12 relative (the reference's b_hat formula, vanka.cpp:133,
+// assumes symmetric A as well); SAG_VANKA_SYM=0/1 overrides.
+static bool velocity_block_symmetric(Ctx& c, const Matrix& k, int n_u) {
+  if (const char* e = getenv("SAG_VANKA_SYM")) return atoi(e) != 0;
+  if (n_u <= 0) return true;
+  DevBuf<unsigned long long> o(2);
+  SAG_CUDA(cudaMemsetAsync(o.p, 0, 16, c.stream));
+  asym_kernel<<<grid_for(c, n_u), 256, 0, c.stream>>>(n_u, k.rp.p, k.ci.p, k.v.p, o.p);
+  SAG_LAUNCHED(c);
+  unsigned long long h[2];
+  SAG_CUDA(cudaMemcpyAsync(h, o.p, 16, cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  double d, a;
+  std::memcpy(&d, &h[0], 8);
+  std::memcpy(&a, &h[1], 8);
+  return d <= 1e-12 * a;
+}
+
+std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches& p, int n_u) {
   SAG_REQUIRE(k.nrows == k.ncols, SAG_DIMENSION_MISMATCH, "factor_patches: K must be square");
   SAG_REQUIRE(p.max_np <= 4, SAG_ERROR, "factor_patches: at most 4 pressure seeds per patch");
   SAG_REQUIRE(p.max_dim <= 128, SAG_ERROR,
@@ -475,6 +536,8 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   f->max_dim = p.max_dim;
   f->max_nv = p.max_nv;
   f->max_np = p.max_np;
+  f->sym = velocity_block_symmetric(c, k, std::min(std::max(n_u, 0), k.nrows));
+  const bool sym = f->sym;
   // host bookkeeping: blob offsets, slot bases, storage accounting (vanka.cpp:142-144)
   std::vector<int> vptr(np_ + 1), pptr(np_ + 1), nx(std::max(np_, 1));
   SAG_CUDA(cudaMemcpyAsync(vptr.data(), p.vptr.p, sizeof(int) * (np_ + 1), cudaMemcpyDeviceToHost, c.stream));
@@ -488,7 +551,8 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   for (int i = 0; i < np_; ++i) {
     const long long nv = vptr[i + 1] - vptr[i], npp = pptr[i + 1] - pptr[i];
     const long long x = nx[i], y = nv - x;
-    long long bytes = 16 + 8 * (x * x + y * y + 2 * nv * npp + npp * npp) + 4 * (nv + npp);
+    long long bytes = 16 + 8 * (ainv_len(x, sym) + ainv_len(y, sym) + 2 * nv * npp + npp * npp) +
+                      4 * (nv + npp);
     bytes = (bytes + 15) / 16 * 16;
     off[i + 1] = off[i] + bytes;
     maxbytes = std::max<long long>(maxbytes, bytes);
@@ -552,7 +616,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     SAG_CUDA(cudaMemcpyAsync(err.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
     const int blocks = std::max(1, std::min((np_ + warps - 1) / warps, c.num_sms * 8));
     factor_kernel<<<blocks, warps * 32, smem, c.stream>>>(
-        np_, L.D, L.NV, L.NP, L.bytes, k.rp.p, k.ci.p, k.v.p, p.pptr.p, p.pidx.p, p.vptr.p,
+        np_, L.D, L.NV, L.NP, L.bytes, sym ? 1 : 0, k.rp.p, k.ci.p, k.v.p, p.pptr.p, p.pidx.p, p.vptr.p,
         p.vidx.p, p.nx.p, f->off.p, dsbase.p, f->blob.p, err.p);
     SAG_LAUNCHED(c);
     int herr = big;
@@ -606,50 +670,114 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // engine), gathers r at the patch dofs, solves with the block factors
 // (t = A^-1 b_u; x_p = S^-1 b_p + B_hat b_u; x_u = t + U_hat x_p,
 // vanka.cpp:161-181) and writes the unweighted local result to its slots.
-template <int R>
+// Blob pointers of one patch (layout in internal.cuh).
+struct PatchView {
+  int nx, ny, np, sbase, nv;
+  const double *Ax, *Ay, *U, *Bh, *Si;
+  const int* idx;
+};
+template <bool SYM>
+__device__ __forceinline__ PatchView patch_view(const unsigned char* B) {
+  PatchView v;
+  const int4 hdr = *reinterpret_cast<const int4*>(B);
+  v.nx = hdr.x;
+  v.ny = hdr.y;
+  v.np = hdr.z;
+  v.sbase = hdr.w;
+  v.nv = v.nx + v.ny;
+  v.Ax = reinterpret_cast<const double*>(B + 16);
+  v.Ay = v.Ax + (SYM ? v.nx * (v.nx + 1) / 2 : v.nx * v.nx);
+  v.U = v.Ay + (SYM ? v.ny * (v.ny + 1) / 2 : v.ny * v.ny);
+  v.Bh = v.U + v.np * v.nv;
+  v.Si = v.Bh + v.np * v.nv;
+  v.idx = reinterpret_cast<const int*>(v.Si + v.np * v.np);
+  return v;
+}
+
+// Warp-per-patch additive Vanka. Each warp streams its patches' factor blobs
+// through an NSTAGE-deep shared-memory ring filled by cp.async.bulk (TMA
+// engine, L2 evict-first: the factors are read once per sweep, r stays in L2),
+// solves with the block factors (t = A^-1 b_u; x_p = S^-1 b_p + B_hat b_u;
+// x_u = t + U_hat x_p, vanka.cpp:161-181) and writes the unweighted local
+// result to its slots. The gather of r for patch k+1 is issued before the
+// solve of patch k (double-buffered), hiding its L2 latency.
+// SYM: A^-1 blocks are packed symmetrised upper triangles; lane i reads
+// column j rows (i <= j) or column i rows (i > j): both conflict-free.
+template <int R, bool SYM>
 __global__ void __launch_bounds__(256) vanka_patch_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, int sb_len, const double* __restrict__ r,
     double* __restrict__ out, const int* gate) {
   if (gate && *gate) return;
+  constexpr int G = 2 * R + 1;  // gathered values per lane (nv + np <= 32 G)
   extern __shared__ __align__(128) unsigned char smem[];
   const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* ring = smem + (size_t)wib * nstage * slot_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)warps * nstage * slot_bytes) +
                    (size_t)wib * nstage;
-  double* sb = reinterpret_cast<double*>(smem + (size_t)warps * nstage * slot_bytes +
-                                         (size_t)warps * nstage * 8) +
-               (size_t)wib * sb_len;
+  double* sbuf = reinterpret_cast<double*>(smem + (size_t)warps * nstage * slot_bytes +
+                                           (size_t)warps * nstage * 8) +
+                 (size_t)wib * 2 * sb_len;
   const int first = blockIdx.x * warps + wib;
   const int stride = gridDim.x * warps;
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  auto issue = [&](int s, int kk) {
+    unsigned char* dst = ring + (size_t)s * slot_bytes;
+    const unsigned bytes = (unsigned)(off[kk + 1] - off[kk]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bars + s)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(blob + off[kk]), "r"(bytes), "r"(smem_u32(bars + s)), "l"(policy)
+        : "memory");
+  };
   if (lane == 0) {
     for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int s = 0; s < nstage; ++s) {
       const int kk = first + s * stride;
-      if (kk < npatch)
-        bulk_load(ring + (size_t)s * slot_bytes, blob + off[kk], (unsigned)(off[kk + 1] - off[kk]),
-                  bars + s);
+      if (kk < npatch) issue(s, kk);
     }
   }
   __syncwarp();
+  if (first < npatch) {
+    mbar_wait(bars, 0);
+    const PatchView v = patch_view<SYM>(ring);
+    for (int i = lane; i < v.nv + v.np; i += 32) sbuf[i] = __ldg(r + v.idx[i]);
+  }
+  __syncwarp();
+  int csl[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) csl[q] = (lane + 32 * q) * (lane + 32 * q + 1) / 2;
   int it = 0;
   for (int k = first; k < npatch; k += stride, ++it) {
     const int stage = it % nstage;
-    const unsigned parity = (unsigned)((it / nstage) & 1);
-    mbar_wait(bars + stage, parity);
-    const unsigned char* B = ring + (size_t)stage * slot_bytes;
-    const int4 hdr = *reinterpret_cast<const int4*>(B);
-    const int nx = hdr.x, ny = hdr.y, np = hdr.z, sbase = hdr.w;
-    const int nv = nx + ny;
-    const double* Ax = reinterpret_cast<const double*>(B + 16);
-    const double* Ay = Ax + nx * nx;
-    const double* U = Ay + ny * ny;
-    const double* Bh = U + np * nv;
-    const double* Si = Bh + np * nv;
-    const int* idx = reinterpret_cast<const int*>(Si + np * np);
-    for (int i = lane; i < nv + np; i += 32) sb[i] = __ldg(r + idx[i]);
-    __syncwarp();
+    const PatchView v = patch_view<SYM>(ring + (size_t)stage * slot_bytes);
+    const double* sb = sbuf + (it & 1) * sb_len;
+    // prefetch r at the next patch's dofs (its blob was issued nstage-1 solves ago)
+    const int kn = k + stride;
+    double g[G];
+    int gn = 0;
+    if (kn < npatch) {
+      const int sn = (it + 1) % nstage;
+      mbar_wait(bars + sn, (unsigned)(((it + 1) / nstage) & 1));
+      const PatchView w = patch_view<SYM>(ring + (size_t)sn * slot_bytes);
+      gn = w.nv + w.np;
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        const int i = lane + 32 * q;
+        g[q] = i < gn ? __ldg(r + w.idx[i]) : 0.0;
+      }
+    }
+    const int nx = v.nx, ny = v.ny, np = v.np, nv = v.nv, sbase = v.sbase;
+    const double* Ax = v.Ax;
+    const double* Ay = v.Ay;
+    const double* U = v.U;
+    const double* Bh = v.Bh;
+    const double* Si = v.Si;
     // t = A^-1 b_u per component (vanka.cpp:164-166)
     double tx[R], ty[R];
 #pragma unroll
@@ -658,11 +786,18 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
     for (int j = 0; j < nmax; ++j) {
       const double bx = sb[j];
       const double by = sb[nx + j];
+      const int csj = j * (j + 1) / 2;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int i = lane + 32 * q;
-        if (j < nx && i < nx) tx[q] = fma(Ax[j * nx + i], bx, tx[q]);
-        if (j < ny && i < ny) ty[q] = fma(Ay[j * ny + i], by, ty[q]);
+        if (SYM) {
+          const int a = i <= j ? csj + i : csl[q] + j;
+          if (j < nx && i < nx) tx[q] = fma(Ax[a], bx, tx[q]);
+          if (j < ny && i < ny) ty[q] = fma(Ay[a], by, ty[q]);
+        } else {
+          if (j < nx && i < nx) tx[q] = fma(Ax[j * nx + i], bx, tx[q]);
+          if (j < ny && i < ny) ty[q] = fma(Ay[j * ny + i], by, ty[q]);
+        }
       }
     }
     // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
@@ -699,13 +834,19 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
         out[sbase + nx + i] = v;
       }
     }
+    // publish the prefetched r values for the next patch
+    double* sbn = sbuf + ((it + 1) & 1) * sb_len;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int i = lane + 32 * q;
+      if (i < gn) sbn[i] = g[q];
+    }
     __syncwarp();
     if (lane == 0) {
-      const int kn = k + nstage * stride;
-      if (kn < npatch) {
+      const int kr = k + nstage * stride;
+      if (kr < npatch) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        bulk_load(ring + (size_t)stage * slot_bytes, blob + off[kn],
-                  (unsigned)(off[kn + 1] - off[kn]), bars + stage);
+        issue(stage, kr);
       }
     }
   }
@@ -736,49 +877,65 @@ struct ApplyCfg {
   int warps, nstage, sb_len, smem, blocks;
 };
 
-template <int R>
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// Launch shape: NSTAGE >= 3 blobs in flight per warp (one being solved, one
+// gathered, >= 1 landing), as many warps as shared memory allows (up to 8
+// per CTA, several CTAs per SM), a persistent grid of occupancy x #SMs.
+template <int R, bool SYM>
 static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
-  static thread_local int configured_smem[4] = {0, 0, 0, 0};
+  static thread_local int configured_smem[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
   ApplyCfg a;
-  a.nstage = 2;
+  a.nstage = std::max(3, env_int("SAG_VANKA_STAGES", 3));
   a.sb_len = f.max_nv + f.max_np + f.max_dim + 2;
   a.sb_len = (a.sb_len + 1) / 2 * 2;
-  const int per_warp = a.nstage * f.slot_bytes + a.nstage * 8 + a.sb_len * 8;
-  a.warps = std::max(1, std::min(8, (112 * 1024) / per_warp));
-  if (a.warps * per_warp > 112 * 1024) a.warps = std::max(1, (220 * 1024) / per_warp);
+  const int per_warp = a.nstage * f.slot_bytes + a.nstage * 8 + 2 * a.sb_len * 8;
+  const int cta_budget = env_int("SAG_VANKA_CTA_SMEM", 60000);
+  a.warps = std::max(1, std::min(env_int("SAG_VANKA_WARPS", 8), cta_budget / per_warp));
+  if (a.warps * per_warp > 220 * 1024) a.warps = std::max(1, (220 * 1024) / per_warp);
   a.smem = a.warps * per_warp;
   SAG_REQUIRE(a.smem <= 227 * 1024, SAG_ERROR, "apply_vanka: patch blobs too large for staging");
-  if (configured_smem[R - 1] < a.smem) {
-    SAG_CUDA(cudaFuncSetAttribute(vanka_patch_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  a.smem));
-    configured_smem[R - 1] = a.smem;
+  auto kern = vanka_patch_kernel<R, SYM>;
+  if (configured_smem[SYM][R - 1] < a.smem) {
+    SAG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem));
+    configured_smem[SYM][R - 1] = a.smem;
   }
   int occ = 0;
-  SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vanka_patch_kernel<R>, a.warps * 32,
-                                                         a.smem));
+  SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, a.warps * 32, a.smem));
   occ = std::max(occ, 1);
   const long long need = (f.npatch + a.warps - 1) / a.warps;
   a.blocks = (int)std::max(1LL, std::min<long long>(need, (long long)occ * c.num_sms));
   return a;
 }
 
-template <int R>
+template <int R, bool SYM>
 static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gate) {
-  const ApplyCfg a = apply_cfg<R>(c, f);
-  vanka_patch_kernel<R><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
+  const ApplyCfg a = apply_cfg<R, SYM>(c, f);
+  vanka_patch_kernel<R, SYM><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
       f.npatch, f.blob.p, f.off.p, f.slot_bytes, a.nstage, a.sb_len, r, f.out.p, gate);
   SAG_LAUNCHED(c);
 }
 
-static void launch_patch_any(Ctx& c, const Vanka& f, const double* r, const int* gate) {
-  if (f.npatch == 0) return;
+template <bool SYM>
+static void launch_patch_r(Ctx& c, const Vanka& f, const double* r, const int* gate) {
   const int R = (f.max_dim + 31) / 32;
   switch (R) {
-    case 1: launch_patch<1>(c, f, r, gate); break;
-    case 2: launch_patch<2>(c, f, r, gate); break;
-    case 3: launch_patch<3>(c, f, r, gate); break;
-    default: launch_patch<4>(c, f, r, gate); break;
+    case 1: launch_patch<1, SYM>(c, f, r, gate); break;
+    case 2: launch_patch<2, SYM>(c, f, r, gate); break;
+    case 3: launch_patch<3, SYM>(c, f, r, gate); break;
+    default: launch_patch<4, SYM>(c, f, r, gate); break;
   }
+}
+
+static void launch_patch_any(Ctx& c, const Vanka& f, const double* r, const int* gate) {
+  if (f.npatch == 0) return;
+  if (f.sym)
+    launch_patch_r<true>(c, f, r, gate);
+  else
+    launch_patch_r<false>(c, f, r, gate);
 }
 
 void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta, const int* gate) {
@@ -824,7 +981,7 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
     const int* hdr = reinterpret_cast<const int*>(B);
     const int nx = hdr[0], ny = hdr[1], np = hdr[2], nv = nx + ny;
     const double* Ax = reinterpret_cast<const double*>(B + 16);
-    const double* U = Ax + nx * nx + ny * ny;
+    const double* U = Ax + ainv_len(nx, f.sym) + ainv_len(ny, f.sym);
     const double* Bh = U + np * nv;
     const double* Si = Bh + np * nv;
     for (int i = 0; i < nv; ++i)
@@ -917,9 +1074,10 @@ int sag_factor_patches(sag_ctx* ctx, const sag_matrix* k, const sag_patches* p, 
     SAG_NOTNULL(k);
     SAG_NOTNULL(p);
     SAG_NOTNULL(out);
-    (void)n_u;  // vanka.cpp:147: unused by the reference as well
+    // vanka.cpp:147 leaves n_u unused; here it delimits the velocity block
+    // whose symmetry selects the packed A^-1 representation
     *out = nullptr;
-    auto f = factor_patches_dev(ctx->c, k->m, p->p);
+    auto f = factor_patches_dev(ctx->c, k->m, p->p, n_u);
     auto* h = new sag_vanka;
     h->f = std::move(*f);
     *out = h;

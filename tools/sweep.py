@@ -1,0 +1,88 @@
+#!/usr/bin/env python
+"""Launch-shape sweep for the Vanka patch kernel and the SpMV on one config
+(GPU). Prints one JSON line per variant: microseconds per launch (CUDA
+events over K launches on libsag's stream) and GB/s of algorithmic bytes."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2306_06795_b200 as S  # noqa: E402
+from paper_2306_06795_b200.cases import HostCase  # noqa: E402
+from bench import splitmix64_uniform, spmv_bytes, vanka_bytes  # noqa: E402
+
+
+def main():
+    n_mesh = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+    t0 = time.time()
+    case = HostCase("cavity", False, "structured", n_mesh)
+    k0 = case.k0()
+    ctx = S.Context(0)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+    n = k0.nrows
+    x = torch.from_numpy(splitmix64_uniform(n)).to(dev)
+    y = torch.empty_like(x)
+    print(json.dumps({"setup_s": time.time() - t0, "n": n, "nnz": k0.nnz}), flush=True)
+
+    def timed(fn, k=30):
+        for _ in range(3):
+            fn()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / k * 1e3  # us
+
+    bs = spmv_bytes(n, n, k0.nnz)
+    for stream_mode in ("1", "0"):
+        os.environ["SAG_SPMV_STREAM"] = stream_mode
+        K = S.SparseMatrix.from_csr(k0, ctx)
+        ctas = ["4", "6", "8"] if stream_mode == "1" else ["6"]
+        for c in ctas:
+            os.environ["SAG_SPMV_CTAS"] = c
+            us = timed(lambda: S.spmv(K, x, out=y))
+            print(json.dumps({"kernel": "spmv", "stream": stream_mode, "ctas": c, "us": us,
+                              "gbs": bs / us / 1e3}), flush=True)
+        del K
+    os.environ["SAG_SPMV_STREAM"] = "1"
+    os.environ.pop("SAG_SPMV_CTAS", None)
+    K = S.SparseMatrix.from_csr(k0, ctx)
+    ref_y = S.spmv(K, x).cpu().numpy() if False else None
+    lib = S.lib()
+    for sym in ("1", "0"):
+        os.environ["SAG_VANKA_SYM"] = sym
+        p = S.build_patches(K, *case.nxyz0)
+        f = S.factor_patches(K, p, case.n_x0 + case.n_y0)
+        bv = vanka_bytes(f, p.total_velocity + p.total_pressure, n)
+        xp, dp = S.C.c_void_p(x.data_ptr()), S.C.c_void_p(y.data_ptr())
+        for stages in ("3", "4", "5"):
+            for cta in ("60000", "75000", "112000", "150000", "220000"):
+                os.environ["SAG_VANKA_STAGES"] = stages
+                os.environ["SAG_VANKA_CTA_SMEM"] = cta
+                try:
+                    us_patch = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 1)))
+                    us_g = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 2)))
+                except S.Error as e:
+                    print(json.dumps({"sym": sym, "stages": stages, "cta": cta, "err": str(e)}))
+                    continue
+                print(json.dumps({"kernel": "vanka", "sym": sym, "stages": stages, "cta_smem": cta,
+                                  "patch_us": us_patch, "gather_us": us_g,
+                                  "sweep_us": us_patch + us_g,
+                                  "device_bytes": f.device_bytes,
+                                  "patch_dev_gbs": f.device_bytes / us_patch / 1e3,
+                                  "sweep_alg_gbs": bv / (us_patch + us_g) / 1e3}), flush=True)
+        del f, p
+
+
+if __name__ == "__main__":
+    main()
