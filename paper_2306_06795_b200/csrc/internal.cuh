@@ -38,6 +38,23 @@ struct Patches {
   DevBuf<int> pptr, pidx, vptr, vidx, nx;
 };
 
+// Thread-per-patch Vanka buckets: 32 patches of one shape (nx, ny, np); the
+// payload entry e of bucket lane l sits at D[dbl_off + 32 e + l] (A_x^-1
+// packed, A_y^-1 packed, U_hat, B_hat, S^-1) and I[int_off + 32 e + l]
+// (velocity then pressure dofs); local results at out[slot_off + 32 e + l].
+constexpr int kTppMaxDim = 20;
+__host__ __device__ inline int tpp_class(int d) {
+  return d <= 8 ? 8 : d <= 12 ? 12 : d <= 16 ? 16 : 20;
+}
+struct BucketHdr {
+  int nx, ny, np, count;
+  long long dbl_off, int_off;
+  int slot_off, nm;
+};
+struct TppClass {
+  int nm, b0, b1;
+};
+
 // Device factorization (vanka.hpp:23-40) in the apply representation: one
 // 16-byte-aligned blob per patch
 //   header {int nx, ny, np, slot_base}
@@ -63,6 +80,17 @@ struct Vanka {
   long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
   long long blob_bytes = 0;
   bool sym = false;  // A^-1 blocks stored as packed symmetrised upper triangles
+  // thread-per-patch layout (tpp): shape buckets of 32 patches, entries
+  // interleaved across the bucket (D: doubles, I: dof indices)
+  bool tpp = false;
+  DevBuf<double> D;
+  DevBuf<int> I;
+  DevBuf<struct BucketHdr> hdr;
+  int nbuckets = 0;
+  std::vector<struct TppClass> classes;
+  // per-patch payload bases and shapes (host copies, for export)
+  std::vector<long long> h_dbase, h_ibase;
+  std::vector<int> h_nx, h_nv, h_np;
 };
 
 // Krylov scalar state in device memory (one per FGMRES instance); mirrors the

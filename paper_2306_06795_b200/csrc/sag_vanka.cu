@@ -14,6 +14,11 @@
 
 namespace sag {
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 // ======================================================== build_patches ==
 
 // vanka.cpp:20-38: patch i seeds pressure rows n_u + i*group + g; its
@@ -297,12 +302,26 @@ struct FactorLayout {
   }
 };
 
+// Where factor_kernel writes a patch's payload: double entries at
+// D[dbase[k] + e*es], int entries at I[ibase[k] + e*es]; es = 1 for the blob
+// layout (plus a header at blob + hoff[k]), es = 32 for the interleaved
+// bucket layout of the thread-per-patch apply.
+struct FactorOut {
+  double* D = nullptr;
+  int* I = nullptr;
+  const long long* dbase = nullptr;
+  const long long* ibase = nullptr;
+  long long es = 1;
+  unsigned char* blob = nullptr;
+  const long long* hoff = nullptr;
+  const int* sbase = nullptr;
+};
+
 __global__ void __launch_bounds__(256) factor_kernel(
     int npatch, int D, int NV, int NP, int wbytes, int sym, const int* __restrict__ rp,
     const int* __restrict__ ci, const double* __restrict__ kv, const int* __restrict__ pptr,
     const int* __restrict__ pidx, const int* __restrict__ vptr, const int* __restrict__ vidx,
-    const int* __restrict__ nxs, const long long* __restrict__ off, const int* __restrict__ sbase,
-    unsigned char* __restrict__ blob, int* err) {
+    const int* __restrict__ nxs, FactorOut fo, int* err) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned char* base = smem + (size_t)wib * wbytes;
@@ -363,13 +382,15 @@ __global__ void __launch_bounds__(256) factor_kernel(
       if (lane == 0) atomicMin(err, k);
       continue;
     }
-    unsigned char* bl = blob + off[k];
-    double* gAx = reinterpret_cast<double*>(bl + 16);
-    double* gAy = gAx + ainv_len(nx, sym);
-    double* gU = gAy + ainv_len(ny, sym);
-    double* gB = gU + (size_t)np * nv;
-    double* gS = gB + (size_t)np * nv;
-    int* gidx = reinterpret_cast<int*>(gS + (size_t)np * np);
+    // payload entries e of this patch live at D[db + e*es] / I[ib + e*es]
+    const long long es = fo.es;
+    const long long db = fo.dbase[k], ib = fo.ibase[k];
+    double* gAx = fo.D + db;
+    double* gAy = gAx + ainv_len(nx, sym) * es;
+    double* gU = gAy + ainv_len(ny, sym) * es;
+    double* gB = gU + (long long)np * nv * es;
+    double* gS = gB + (long long)np * nv * es;
+    int* gidx = fo.I + ib;
     // per component: RHS t < n are unit vectors (inverse columns, each one
     // dense_lu_solve(lu, e_t)), t = n + j are -B(j, comp)^T (u_hat columns,
     // vanka.cpp:99-111)
@@ -398,12 +419,14 @@ __global__ void __launch_bounds__(256) factor_kernel(
         // symmetrised upper triangle, packed by columns
         for (int c = 0; c < n; ++c)
           for (int i = lane; i <= c; i += 32)
-            gA[(size_t)c * (c + 1) / 2 + i] = 0.5 * (Winv[(size_t)c * D + i] + Winv[(size_t)i * D + c]);
+            gA[((long long)c * (c + 1) / 2 + i) * es] =
+                0.5 * (Winv[(size_t)c * D + i] + Winv[(size_t)i * D + c]);
       } else {
-        for (int e = lane; e < n * n; e += 32) gA[e] = Winv[(size_t)(e / n) * D + (e % n)];
+        for (int e = lane; e < n * n; e += 32) gA[e * es] = Winv[(size_t)(e / n) * D + (e % n)];
       }
       __syncwarp();
     }
+    double* Sinv = Winv;  // the inverse columns are written out; reuse the space
     // S = B u_hat (vanka.cpp:112-119)
     for (int e = lane; e < np * np; e += 32) {
       const int a = e / np, cc = e % np;
@@ -416,45 +439,54 @@ __global__ void __launch_bounds__(256) factor_kernel(
       if (lane == 0) atomicMin(err, k);
       continue;
     }
-    // S^-1 columns from unit vectors (vanka.cpp:126-132), into gS row-major
+    // S^-1 columns from unit vectors (vanka.cpp:126-132), row-major
     if (lane < np) {
       for (int i = 0; i < np; ++i) xw[i] = spiv[i] == lane ? 1.0 : 0.0;
       lu_solve_lane(Sm, np, np, xw);
-      for (int i = 0; i < np; ++i) gS[i * np + lane] = xw[i];
+      for (int i = 0; i < np; ++i) Sinv[i * np + lane] = xw[i];
     }
     __syncwarp();
+    for (int e = lane; e < np * np; e += 32) gS[e * es] = Sinv[e];
     // b_hat = S^-1 u_hat^T (vanka.cpp:133-140); stored [a*nv + j]
     for (int e = lane; e < np * nv; e += 32) {
       const int a = e / nv, j = e % nv;
       double acc = 0.0;
-      for (int m = 0; m < np; ++m) acc = __dadd_rn(acc, __dmul_rn(gS[a * np + m], Um[j * NP + m]));
-      gB[(size_t)a * nv + j] = acc;
+      for (int m = 0; m < np; ++m) acc = __dadd_rn(acc, __dmul_rn(Sinv[a * np + m], Um[j * NP + m]));
+      gB[e * es] = acc;
     }
     // u_hat stored [a*nv + i]
     for (int e = lane; e < np * nv; e += 32) {
       const int a = e / nv, i = e % nv;
-      gU[(size_t)a * nv + i] = Um[i * NP + a];
+      gU[e * es] = Um[i * NP + a];
     }
-    for (int i = lane; i < nv; i += 32) gidx[i] = sv[i];
-    for (int a = lane; a < np; a += 32) gidx[nv + a] = pidx[p0 + a];
-    if (lane == 0) {
-      int* hdr = reinterpret_cast<int*>(bl);
+    for (int i = lane; i < nv; i += 32) gidx[i * es] = sv[i];
+    for (int a = lane; a < np; a += 32) gidx[(nv + a) * es] = pidx[p0 + a];
+    if (lane == 0 && fo.hoff) {
+      int* hdr = reinterpret_cast<int*>(fo.blob + fo.hoff[k]);
       hdr[0] = nx;
       hdr[1] = ny;
       hdr[2] = np;
-      hdr[3] = sbase[k];
+      hdr[3] = fo.sbase[k];
     }
     __syncwarp();
   }
 }
 
+// keys[slot] = dof of that slot: patch k's entry e sits at slot sbase[k] + e*es
+// (velocity entries first, then pressure, as the apply writes them)
 __global__ void slot_keys_kernel(int npatch, const int* pptr, const int* pidx, const int* vptr,
-                                 const int* vidx, const int* sbase, int* keys) {
+                                 const int* vidx, const int* sbase, int es, int* keys) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < npatch; k += gridDim.x * blockDim.x) {
     int s = sbase[k];
-    for (int q = vptr[k]; q < vptr[k + 1]; ++q) keys[s++] = vidx[q];
-    for (int q = pptr[k]; q < pptr[k + 1]; ++q) keys[s++] = pidx[q];
+    for (int q = vptr[k]; q < vptr[k + 1]; ++q, s += es) keys[s] = vidx[q];
+    for (int q = pptr[k]; q < pptr[k + 1]; ++q, s += es) keys[s] = pidx[q];
   }
+}
+
+__global__ void fill_int_kernel(long long n, int v, int* a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = v;
 }
 
 __global__ void count_int_kernel(long long n, const int* key, int* cnt) {
@@ -544,33 +576,113 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   SAG_CUDA(cudaMemcpyAsync(pptr.data(), p.pptr.p, sizeof(int) * (np_ + 1), cudaMemcpyDeviceToHost, c.stream));
   if (np_) SAG_CUDA(cudaMemcpyAsync(nx.data(), p.nx.p, sizeof(int) * np_, cudaMemcpyDeviceToHost, c.stream));
   SAG_CUDA(cudaStreamSynchronize(c.stream));
-  std::vector<long long> off(np_ + 1, 0);
-  std::vector<int> sbase(std::max(np_, 1), 0);
-  long long slots = 0;
-  int maxbytes = 16;
+  f->h_nx.resize(np_);
+  f->h_nv.resize(np_);
+  f->h_np.resize(np_);
   for (int i = 0; i < np_; ++i) {
     const long long nv = vptr[i + 1] - vptr[i], npp = pptr[i + 1] - pptr[i];
     const long long x = nx[i], y = nv - x;
-    long long bytes = 16 + 8 * (ainv_len(x, sym) + ainv_len(y, sym) + 2 * nv * npp + npp * npp) +
-                      4 * (nv + npp);
-    bytes = (bytes + 15) / 16 * 16;
-    off[i + 1] = off[i] + bytes;
-    maxbytes = std::max<long long>(maxbytes, bytes);
-    sbase[i] = (int)slots;
-    slots += nv + npp;
-    SAG_REQUIRE(slots < (1LL << 31), SAG_DIMENSION_MISMATCH, "factor_patches: too many slots");
+    f->h_nx[i] = (int)x;
+    f->h_nv[i] = (int)nv;
+    f->h_np[i] = (int)npp;
     f->a_factor_bytes += 8 * (x * x + y * y);
     f->aux_bytes += 8 * (2 * nv * npp + npp * npp);
     f->dense_inverse_bytes += 8 * (nv + npp) * (nv + npp);
   }
-  f->slot_bytes = maxbytes;
+  auto ndbl = [&](int i) {
+    const long long nv = f->h_nv[i], npp = f->h_np[i], x = f->h_nx[i], y = nv - x;
+    return ainv_len(x, sym) + ainv_len(y, sym) + 2 * nv * npp + npp * npp;
+  };
+  f->h_dbase.assign(np_, 0);
+  f->h_ibase.assign(np_, 0);
+  std::vector<int> sbase(std::max(np_, 1), 0);
+  long long slots = 0;
+  f->tpp = sym && p.max_dim <= kTppMaxDim && p.max_np <= 4 && np_ > 0 &&
+           env_int("SAG_VANKA_TPP", 1) != 0;
+  if (f->tpp) {
+    // thread-per-patch layout: patches sorted (stably) by shape, buckets of 32
+    // equal-shape patches, every payload entry interleaved across the bucket
+    std::vector<int> order(np_);
+    for (int i = 0; i < np_; ++i) order[i] = i;
+    auto key = [&](int i) {
+      const int x = f->h_nx[i], y = f->h_nv[i] - x;
+      const int nm = tpp_class(std::max(x, y));
+      return (((long long)nm * 256 + x) * 256 + y) * 8 + f->h_np[i];
+    };
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
+    std::vector<BucketHdr> hdr;
+    long long doff = 0, ioff = 0;
+    for (int s = 0; s < np_;) {
+      const int i0 = order[s];
+      int e = s + 1;
+      while (e < np_ && e - s < 32 && key(order[e]) == key(i0)) ++e;
+      BucketHdr h;
+      h.nx = f->h_nx[i0];
+      h.ny = f->h_nv[i0] - h.nx;
+      h.np = f->h_np[i0];
+      h.count = e - s;
+      h.dbl_off = doff;
+      h.int_off = ioff;
+      h.slot_off = (int)slots;
+      h.nm = tpp_class(std::max(h.nx, h.ny));
+      for (int q = s; q < e; ++q) {
+        const int i = order[q], lane = q - s;
+        f->h_dbase[i] = doff + lane;
+        f->h_ibase[i] = ioff + lane;
+        sbase[i] = (int)slots + lane;
+      }
+      doff += 32 * ndbl(i0);
+      ioff += 32LL * (f->h_nv[i0] + h.np);
+      slots += 32LL * (f->h_nv[i0] + h.np);
+      SAG_REQUIRE(slots < (1LL << 31), SAG_DIMENSION_MISMATCH, "factor_patches: too many slots");
+      hdr.push_back(h);
+      s = e;
+    }
+    f->nbuckets = (int)hdr.size();
+    for (int b = 0; b < f->nbuckets;) {
+      int e = b;
+      while (e < f->nbuckets && hdr[e].nm == hdr[b].nm) ++e;
+      f->classes.push_back({hdr[b].nm, b, e});
+      b = e;
+    }
+    f->hdr.alloc(hdr.size());
+    SAG_CUDA(cudaMemcpyAsync(f->hdr.p, hdr.data(), sizeof(BucketHdr) * hdr.size(),
+                             cudaMemcpyHostToDevice, c.stream));
+    f->D.alloc(std::max(doff, 1LL));
+    f->I.alloc(std::max(ioff, 1LL));
+    f->blob_bytes = 8 * doff + 4 * ioff;
+  } else {
+    std::vector<long long> off(np_ + 1, 0);
+    int maxbytes = 16;
+    for (int i = 0; i < np_; ++i) {
+      long long bytes = 16 + 8 * ndbl(i) + 4 * (f->h_nv[i] + f->h_np[i]);
+      bytes = (bytes + 15) / 16 * 16;
+      off[i + 1] = off[i] + bytes;
+      maxbytes = std::max<long long>(maxbytes, bytes);
+      f->h_dbase[i] = (off[i] + 16) / 8;
+      f->h_ibase[i] = (off[i] + 16 + 8 * ndbl(i)) / 4;
+      sbase[i] = (int)slots;
+      slots += f->h_nv[i] + f->h_np[i];
+      SAG_REQUIRE(slots < (1LL << 31), SAG_DIMENSION_MISMATCH, "factor_patches: too many slots");
+    }
+    f->slot_bytes = maxbytes;
+    f->blob_bytes = off[np_];
+    f->blob.alloc(std::max<long long>(off[np_], 16));
+    f->off.alloc(np_ + 1);
+    SAG_CUDA(cudaMemcpyAsync(f->off.p, off.data(), sizeof(long long) * (np_ + 1),
+                             cudaMemcpyHostToDevice, c.stream));
+  }
   f->nslots = slots;
-  f->blob_bytes = off[np_];
-  f->blob.alloc(std::max<long long>(off[np_], 16));
-  f->off.alloc(np_ + 1);
-  SAG_CUDA(cudaMemcpyAsync(f->off.p, off.data(), sizeof(long long) * (np_ + 1), cudaMemcpyHostToDevice, c.stream));
   DevBuf<int> dsbase(std::max(np_, 1));
+  DevBuf<long long> ddbase(std::max(np_, 1)), dibase(std::max(np_, 1));
   SAG_CUDA(cudaMemcpyAsync(dsbase.p, sbase.data(), sizeof(int) * sbase.size(), cudaMemcpyHostToDevice, c.stream));
+  if (np_) {
+    SAG_CUDA(cudaMemcpyAsync(ddbase.p, f->h_dbase.data(), sizeof(long long) * np_,
+                             cudaMemcpyHostToDevice, c.stream));
+    SAG_CUDA(cudaMemcpyAsync(dibase.p, f->h_ibase.data(), sizeof(long long) * np_,
+                             cudaMemcpyHostToDevice, c.stream));
+  }
+  const int es = f->tpp ? 32 : 1;
 
   // dof -> slot map (stable sort of slot ids by dof) and PoU weights
   const int n = k.nrows;
@@ -580,8 +692,10 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   f->dof_slot.alloc(std::max<long long>(slots, 1));
   if (slots > 0) {
     DevBuf<int> keys(slots), keys_sorted(slots), ids(slots), cnt(n + 1);
+    fill_int_kernel<<<grid_for(c, slots), 256, 0, c.stream>>>(slots, n, keys.p);  // padding -> n
+    SAG_LAUNCHED(c);
     slot_keys_kernel<<<grid_for(c, np_), 256, 0, c.stream>>>(np_, p.pptr.p, p.pidx.p, p.vptr.p,
-                                                             p.vidx.p, dsbase.p, keys.p);
+                                                             p.vidx.p, dsbase.p, es, keys.p);
     SAG_LAUNCHED(c);
     iota_int_kernel<<<grid_for(c, slots), 256, 0, c.stream>>>(slots, ids.p);
     SAG_LAUNCHED(c);
@@ -615,9 +729,23 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     const int big = 0x7fffffff;
     SAG_CUDA(cudaMemcpyAsync(err.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
     const int blocks = std::max(1, std::min((np_ + warps - 1) / warps, c.num_sms * 8));
+    FactorOut fo;
+    fo.es = es;
+    fo.dbase = ddbase.p;
+    fo.ibase = dibase.p;
+    fo.sbase = dsbase.p;
+    if (f->tpp) {
+      fo.D = f->D.p;
+      fo.I = f->I.p;
+    } else {
+      fo.D = reinterpret_cast<double*>(f->blob.p);
+      fo.I = reinterpret_cast<int*>(f->blob.p);
+      fo.blob = f->blob.p;
+      fo.hoff = f->off.p;
+    }
     factor_kernel<<<blocks, warps * 32, smem, c.stream>>>(
-        np_, L.D, L.NV, L.NP, L.bytes, sym ? 1 : 0, k.rp.p, k.ci.p, k.v.p, p.pptr.p, p.pidx.p, p.vptr.p,
-        p.vidx.p, p.nx.p, f->off.p, dsbase.p, f->blob.p, err.p);
+        np_, L.D, L.NV, L.NP, L.bytes, sym ? 1 : 0, k.rp.p, k.ci.p, k.v.p, p.pptr.p, p.pidx.p,
+        p.vptr.p, p.vidx.p, p.nx.p, fo, err.p);
     SAG_LAUNCHED(c);
     int herr = big;
     SAG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -873,14 +1001,133 @@ __global__ void vanka_gather_kernel(int n, const int* __restrict__ dof_ptr,
   }
 }
 
+// ------------------------------------------------ thread-per-patch apply --
+// One component of a patch solve with all operands in registers:
+// t = A^-1 b with A^-1 the packed symmetrised upper triangle (each stored
+// entry loaded once: t_i += a_ij b_j, t_j += a_ij b_i), then
+// x_u = t + U_hat x_p written to the patch's slots (vanka.cpp:164-180).
+template <int NM>
+__device__ __forceinline__ void tpp_component(const double* __restrict__ A, const double (&b)[NM],
+                                              int n, const double* __restrict__ U, int nv, int np,
+                                              const double (&xp)[4], double* __restrict__ o) {
+  double t[NM];
+#pragma unroll
+  for (int i = 0; i < NM; ++i) t[i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < NM; ++j) {
+    if (j < n) {
+#pragma unroll
+      for (int i = 0; i <= j; ++i) {
+        const double a = __ldg(A + 32 * (j * (j + 1) / 2 + i));
+        t[i] = fma(a, b[j], t[i]);
+        if (i != j) t[j] = fma(a, b[i], t[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    if (i < n) {
+      double v = t[i];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (a < np) v = fma(__ldg(U + 32 * (a * nv + i)), xp[a], v);
+      o[32 * i] = v;
+    }
+  }
+}
+
+// Thread-per-patch additive Vanka over shape buckets (layout in internal.cuh):
+// lane l of a warp solves patch l of its bucket. Every payload load is one
+// coalesced 256-byte warp access at an address known up front, so a warp
+// keeps a deep queue of loads in flight, and the instruction count is ~1/15
+// of the warp-per-patch kernel's.
+template <int NM>
+__global__ void __launch_bounds__(128) vanka_tpp_kernel(int b0, int b1,
+                                                        const BucketHdr* __restrict__ hdr,
+                                                        const double* __restrict__ D,
+                                                        const int* __restrict__ I,
+                                                        const double* __restrict__ r,
+                                                        double* __restrict__ out,
+                                                        const int* gate) {
+  if (gate && *gate) return;
+  const int lane = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int b = b0 + wg; b < b1; b += nw) {
+    const BucketHdr h = hdr[b];
+    if (lane >= h.count) continue;
+    const int nx = h.nx, ny = h.ny, np = h.np, nv = nx + ny;
+    const int* ix = I + h.int_off + lane;
+    const double* d = D + h.dbl_off + lane;
+    double* o = out + h.slot_off + lane;
+    // gather r at the patch dofs (vanka.cpp:161-162)
+    double bx[NM], by[NM], bp[4];
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+      bx[j] = j < nx ? __ldg(r + __ldg(ix + 32 * j)) : 0.0;
+      by[j] = j < ny ? __ldg(r + __ldg(ix + 32 * (nx + j))) : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) bp[a] = a < np ? __ldg(r + __ldg(ix + 32 * (nv + a))) : 0.0;
+    const double* Ax = d;
+    const double* Ay = Ax + 32 * (nx * (nx + 1) / 2);
+    const double* U = Ay + 32 * (ny * (ny + 1) / 2);
+    const double* Bh = U + 32 * (np * nv);
+    const double* Si = Bh + 32 * (np * nv);
+    // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
+    double xp[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      xp[a] = 0.0;
+      if (a < np) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < np) s = fma(__ldg(Si + 32 * (a * np + q)), bp[q], s);
+        const double* bh = Bh + 32 * (a * nv);
+#pragma unroll
+        for (int j = 0; j < NM; ++j) {
+          if (j < nx) s = fma(__ldg(bh + 32 * j), bx[j], s);
+          if (j < ny) s = fma(__ldg(bh + 32 * (nx + j)), by[j], s);
+        }
+        xp[a] = s;
+        o[32 * (nv + a)] = s;
+      }
+    }
+    tpp_component<NM>(Ax, bx, nx, U, nv, np, xp, o);
+    tpp_component<NM>(Ay, by, ny, U + 32 * nx, nv, np, xp, o + 32 * nx);
+  }
+}
+
+template <int NM>
+static void launch_tpp(Ctx& c, const Vanka& f, int b0, int b1, const double* r, const int* gate) {
+  static thread_local int occ = 0;
+  if (!occ) {
+    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vanka_tpp_kernel<NM>, 128, 0));
+    occ = std::max(occ, 1);
+  }
+  const long long warps_needed = b1 - b0;
+  const long long cap = (long long)occ * c.num_sms * 4;
+  const int warps = (int)std::max(1LL, std::min(warps_needed, cap));
+  vanka_tpp_kernel<NM><<<(warps + 3) / 4, 128, 0, c.stream>>>(b0, b1, f.hdr.p, f.D.p, f.I.p, r,
+                                                              f.out.p, gate);
+  SAG_LAUNCHED(c);
+}
+
+static void launch_tpp_all(Ctx& c, const Vanka& f, const double* r, const int* gate) {
+  for (const auto& cl : f.classes) {
+    switch (cl.nm) {
+      case 8: launch_tpp<8>(c, f, cl.b0, cl.b1, r, gate); break;
+      case 12: launch_tpp<12>(c, f, cl.b0, cl.b1, r, gate); break;
+      case 16: launch_tpp<16>(c, f, cl.b0, cl.b1, r, gate); break;
+      default: launch_tpp<20>(c, f, cl.b0, cl.b1, r, gate); break;
+    }
+  }
+}
+
 struct ApplyCfg {
   int warps, nstage, sb_len, smem, blocks;
 };
-
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
 
 // Launch shape: NSTAGE >= 3 blobs in flight per warp (one being solved, one
 // gathered, >= 1 landing), as many warps as shared memory allows (up to 8
@@ -932,7 +1179,9 @@ static void launch_patch_r(Ctx& c, const Vanka& f, const double* r, const int* g
 
 static void launch_patch_any(Ctx& c, const Vanka& f, const double* r, const int* gate) {
   if (f.npatch == 0) return;
-  if (f.sym)
+  if (f.tpp)
+    launch_tpp_all(c, f, r, gate);
+  else if (f.sym)
     launch_patch_r<true>(c, f, r, gate);
   else
     launch_patch_r<false>(c, f, r, gate);
@@ -969,28 +1218,30 @@ void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, 
 // parity tests.
 void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* sinv,
                   double* weights) {
-  std::vector<unsigned char> blob(f.blob_bytes);
-  std::vector<long long> off(f.npatch + 1);
-  SAG_CUDA(cudaMemcpyAsync(blob.data(), f.blob.p, f.blob_bytes, cudaMemcpyDeviceToHost, c.stream));
-  SAG_CUDA(cudaMemcpyAsync(off.data(), f.off.p, sizeof(long long) * (f.npatch + 1),
-                           cudaMemcpyDeviceToHost, c.stream));
+  std::vector<double> D;
+  if (f.tpp) {
+    D.resize(f.D.n);
+    SAG_CUDA(cudaMemcpyAsync(D.data(), f.D.p, sizeof(double) * f.D.n, cudaMemcpyDeviceToHost, c.stream));
+  } else {
+    D.resize((f.blob_bytes + 7) / 8);
+    SAG_CUDA(cudaMemcpyAsync(D.data(), f.blob.p, f.blob_bytes, cudaMemcpyDeviceToHost, c.stream));
+  }
   SAG_CUDA(cudaStreamSynchronize(c.stream));
+  const long long es = f.tpp ? 32 : 1;
   size_t ou = 0, os = 0;
   for (int k = 0; k < f.npatch; ++k) {
-    const unsigned char* B = blob.data() + off[k];
-    const int* hdr = reinterpret_cast<const int*>(B);
-    const int nx = hdr[0], ny = hdr[1], np = hdr[2], nv = nx + ny;
-    const double* Ax = reinterpret_cast<const double*>(B + 16);
-    const double* U = Ax + ainv_len(nx, f.sym) + ainv_len(ny, f.sym);
-    const double* Bh = U + np * nv;
-    const double* Si = Bh + np * nv;
+    const int nx = f.h_nx[k], nv = f.h_nv[k], ny = nv - nx, np = f.h_np[k];
+    const double* Ax = D.data() + f.h_dbase[k];
+    const double* U = Ax + (ainv_len(nx, f.sym) + ainv_len(ny, f.sym)) * es;
+    const double* Bh = U + (long long)np * nv * es;
+    const double* Si = Bh + (long long)np * nv * es;
     for (int i = 0; i < nv; ++i)
       for (int a = 0; a < np; ++a) {
-        if (uhat) uhat[ou + (size_t)i * np + a] = U[a * nv + i];
-        if (bhat) bhat[ou + (size_t)a * nv + i] = Bh[a * nv + i];
+        if (uhat) uhat[ou + (size_t)i * np + a] = U[(a * nv + i) * es];
+        if (bhat) bhat[ou + (size_t)a * nv + i] = Bh[(a * nv + i) * es];
       }
     if (sinv)
-      for (int e = 0; e < np * np; ++e) sinv[os + e] = Si[e];
+      for (int e = 0; e < np * np; ++e) sinv[os + e] = Si[e * es];
     ou += (size_t)nv * np;
     os += (size_t)np * np;
   }

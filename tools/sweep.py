@@ -59,14 +59,15 @@ def main():
     K = S.SparseMatrix.from_csr(k0, ctx)
     ref_y = S.spmv(K, x).cpu().numpy() if False else None
     lib = S.lib()
-    for sym in ("1", "0"):
+    for tpp, sym in (("1", "1"), ("0", "1")):
         os.environ["SAG_VANKA_SYM"] = sym
+        os.environ["SAG_VANKA_TPP"] = tpp
         p = S.build_patches(K, *case.nxyz0)
         f = S.factor_patches(K, p, case.n_x0 + case.n_y0)
         bv = vanka_bytes(f, p.total_velocity + p.total_pressure, n)
         xp, dp = S.C.c_void_p(x.data_ptr()), S.C.c_void_p(y.data_ptr())
-        for stages in ("3", "4", "5"):
-            for cta in ("60000", "75000", "112000", "150000", "220000"):
+        for stages in ("3",):
+            for cta in (("60000",) if tpp == "0" else ("0",)):
                 os.environ["SAG_VANKA_STAGES"] = stages
                 os.environ["SAG_VANKA_CTA_SMEM"] = cta
                 try:
@@ -75,7 +76,7 @@ def main():
                 except S.Error as e:
                     print(json.dumps({"sym": sym, "stages": stages, "cta": cta, "err": str(e)}))
                     continue
-                print(json.dumps({"kernel": "vanka", "sym": sym, "stages": stages, "cta_smem": cta,
+                print(json.dumps({"kernel": "vanka", "tpp": tpp, "sym": sym, "stages": stages, "cta_smem": cta,
                                   "patch_us": us_patch, "gather_us": us_g,
                                   "sweep_us": us_patch + us_g,
                                   "device_bytes": f.device_bytes,
