@@ -44,7 +44,11 @@ struct Patches {
 // (velocity then pressure dofs); local results at out[slot_off + 32 e + l].
 constexpr int kTppMaxDim = 20;
 __host__ __device__ inline int tpp_class(int d) {
-  return d <= 8 ? 8 : d <= 12 ? 12 : d <= 16 ? 16 : 20;
+  // one class: per-class launches ran small classes on a few SMs (measured
+  // 35 us for a 34 MB class); the unrolled NM = 20 code skips unused
+  // columns with uniform branches
+  (void)d;
+  return 20;
 }
 struct BucketHdr {
   int nx, ny, np, count;
@@ -170,7 +174,11 @@ void launch_mgs(Ctx& c, int n, double* w, const double* vprev, const double* h,
                 const double* vnext, const Fin& fin, const int* gate);
 // w -= (*h) * v; reduce w . w
 void launch_mgs_last(Ctx& c, int n, double* w, const double* v, const double* h, const Fin& fin,
-                     const int* gate);
+                     const int* gate, bool write_w = true);
+// r = eta .* (b - y_0 w): residual after a one-step relaxation x = y_0 z_0
+// whose w = K z_0 is kept (K x by linearity, no SpMV)
+void launch_lin_resid(Ctx& c, int n, int n_u, double eta_u, double eta_p, const double* b,
+                      const double* w, const KState* st, double* r);
 // y = back-substitution of the jeff x jeff Hessenberg system (krylov.cpp:102-107)
 void launch_backsub(Ctx& c, KState* st);
 // x += sum_{i<jeff} y_i Z_i   (krylov.cpp:108-110 then vanka.cpp:208);

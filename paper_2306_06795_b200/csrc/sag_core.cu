@@ -158,6 +158,17 @@ __global__ void __launch_bounds__(256) spmv_kernel(int nrows, const int* __restr
   for (int base = warp * RPW; base < nrows; base += nwarps * RPW) {
     const int row = base + grp;
     double s = 0.0;
+    // the epilogue operand is loaded before the row product so that its
+    // latency overlaps the gather instead of adding a dependent round trip
+    double pre = 0.0;
+    const bool lead = sub == 0 && row < nrows;
+    if constexpr (E == Epi::StoreDot) {
+      if (lead) pre = __ldg(a.dotv + row);
+    } else if constexpr (E == Epi::Resid || E == Epi::ResidEta || E == Epi::ResidSsq) {
+      if (lead) pre = __ldg(a.b + row);
+    } else if constexpr (E == Epi::Add) {
+      if (lead) pre = y[row];
+    }
     if (row < nrows) {
       const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
 #pragma unroll 4
@@ -165,20 +176,20 @@ __global__ void __launch_bounds__(256) spmv_kernel(int nrows, const int* __restr
     }
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-    if (sub == 0 && row < nrows) {
+    if (lead) {
       if constexpr (E == Epi::Store) {
         y[row] = s;
       } else if constexpr (E == Epi::Resid) {
-        y[row] = a.b[row] - s;
+        y[row] = pre - s;
       } else if constexpr (E == Epi::ResidEta) {
-        y[row] = (row < a.n_u ? a.eta_u : a.eta_p) * (a.b[row] - s);
+        y[row] = (row < a.n_u ? a.eta_u : a.eta_p) * (pre - s);
       } else if constexpr (E == Epi::Add) {
-        y[row] = y[row] + s;
+        y[row] = pre + s;
       } else if constexpr (E == Epi::StoreDot) {
         y[row] = s;
-        red = fma(s, a.dotv[row], red);
+        red = fma(s, pre, red);
       } else if constexpr (E == Epi::ResidSsq) {
-        const double r = a.b[row] - s;
+        const double r = pre - s;
         y[row] = r;
         red = fma(r, r, red);
       }
@@ -387,20 +398,37 @@ __global__ void __launch_bounds__(kRedBlock) mgs_kernel(int n, double* __restric
   reduce_finish(s, fin, partials, ticket);
 }
 
+// write_w = 0: the orthogonalised w is only needed for its norm (last Arnoldi
+// step of a fixed-length inner solve, whose v_(j+1) is never used), so w keeps
+// A z_j -- which the relaxation reuses for the next residual.
 __global__ void __launch_bounds__(kRedBlock) mgs_last_kernel(int n, double* __restrict__ w,
                                                              const double* __restrict__ v,
                                                              const double* h, Fin fin,
-                                                             const int* gate, double* partials,
-                                                             unsigned* ticket) {
+                                                             const int* gate, int write_w,
+                                                             double* partials, unsigned* ticket) {
   if (gate && *gate) return;
   const double hh = *h;
   double s = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double wi = fma(-hh, v[i], w[i]);
-    w[i] = wi;
+    if (write_w) w[i] = wi;
     s = fma(wi, wi, s);
   }
   reduce_finish(s, fin, partials, ticket);
+}
+
+// r = eta .* (b - y_0 w) with w = K z_0 from a one-step relaxation x = y_0 z_0
+// (so r = eta .* (b - K x) by linearity); r = eta .* b when the relaxation
+// made no step (jeff == 0, zero residual).
+__global__ void lin_resid_kernel(int n, int n_u, double eu, double ep,
+                                 const double* __restrict__ b, const double* __restrict__ w,
+                                 const KState* st, double* __restrict__ r) {
+  const bool step = st->jeff > 0;
+  const double y0 = step ? ks_y(const_cast<KState*>(st))[0] : 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double v = step ? fma(-y0, w[i], b[i]) : b[i];
+    r[i] = (i < n_u ? eu : ep) * v;
+  }
 }
 
 // krylov.cpp:102-107, one thread (j <= restart)
@@ -525,9 +553,14 @@ void launch_mgs(Ctx& c, int n, double* w, const double* vprev, const double* h,
   SAG_LAUNCHED(c);
 }
 void launch_mgs_last(Ctx& c, int n, double* w, const double* v, const double* h, const Fin& fin,
-                     const int* gate) {
-  mgs_last_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, w, v, h, fin, gate, c.partials.p,
-                                                           c.ticket.p);
+                     const int* gate, bool write_w) {
+  mgs_last_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, w, v, h, fin, gate, write_w ? 1 : 0,
+                                                           c.partials.p, c.ticket.p);
+  SAG_LAUNCHED(c);
+}
+void launch_lin_resid(Ctx& c, int n, int n_u, double eta_u, double eta_p, const double* b,
+                      const double* w, const KState* st, double* r) {
+  lin_resid_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, n_u, eta_u, eta_p, b, w, st, r);
   SAG_LAUNCHED(c);
 }
 void launch_backsub(Ctx& c, KState* st) {

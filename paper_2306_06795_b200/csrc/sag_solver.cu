@@ -53,7 +53,10 @@ struct Krylov {
 //   MGS: w -= h_(i-1)j v_(i-1) fused with h_ij = (w, v_i), i = 1..j
 //   w -= h_jj v_j fused with ||w||^2 -> Givens + residual estimate (finisher)
 //   v_(j+1) = w / ||w|| unless breakdown
-static void arnoldi_step(Ctx& c, const Matrix& A, Krylov& K, int mm, int j, const int* gate) {
+// last: final step of a fixed-length inner solve -- v_(j+1) is never used, so
+// it is not formed and w keeps A z_j (reused by lin_resid for nu = 1).
+static void arnoldi_step(Ctx& c, const Matrix& A, Krylov& K, int mm, int j, const int* gate,
+                         bool last = false) {
   const int n = K.n;
   {
     SpmvArgs a;
@@ -77,8 +80,8 @@ static void arnoldi_step(Ctx& c, const Matrix& A, Krylov& K, int mm, int j, cons
   f.kind = FIN_ARNOLDI;
   f.st = K.st;
   f.j = j;
-  launch_mgs_last(c, n, K.w.p, K.v(j), K.h(mm, j, j), f, gate);
-  launch_div(c, n, K.w.p, K.wnorm(), K.v(j + 1), gate, K.breakdown());
+  launch_mgs_last(c, n, K.w.p, K.v(j), K.h(mm, j, j), f, gate, !last);
+  if (!last) launch_div(c, n, K.w.p, K.wnorm(), K.v(j + 1), gate, K.breakdown());
 }
 
 // vanka_relax, KrylovWrapped (vanka.cpp:199-208): x += FGMRES_nu(K, b - K x;
@@ -112,7 +115,7 @@ static void relax_kw(Ctx& c, const Matrix& K, const Vanka& f, Krylov& kr, double
   launch_div(c, n, r, kr.beta(), kr.v(0), kr.stop());
   for (int j = 0; j < nu; ++j) {
     vanka_apply(c, f, kr.v(j), kr.z(j), kr.stop());
-    arnoldi_step(c, K, kr, nu, j, kr.stop());
+    arnoldi_step(c, K, kr, nu, j, kr.stop(), j == nu - 1);
   }
   launch_backsub(c, kr.st);
   launch_update(c, n, x, kr.Z.p, (size_t)n, kr.st, x_zero);
@@ -498,9 +501,14 @@ static void cycle_level(Ctx& c, Dc& d, int l, int nu1, int nu2, bool skip_finest
     launch_zero(c, L.n, L.x.p);
   Level& C = d.lv[l + 1];
   if (pre) {
-    SpmvArgs a;
-    a.b = L.b.p;
-    launch_spmv(c, *L.K, L.x.p, L.r.p, Epi::Resid, a);
+    if (nu1 == 1) {
+      // x = y_0 z_0 and w = K z_0: r = b - y_0 w (= b - K x by linearity)
+      launch_lin_resid(c, L.n, L.n, 1.0, 1.0, L.b.p, L.kry.w.p, L.kry.st, L.r.p);
+    } else {
+      SpmvArgs a;
+      a.b = L.b.p;
+      launch_spmv(c, *L.K, L.x.p, L.r.p, Epi::Resid, a);
+    }
     launch_spmv(c, *L.R, L.r.p, C.b.p, Epi::Store);
   } else {
     launch_spmv(c, *L.R, L.b.p, C.b.p, Epi::Store);
@@ -608,7 +616,9 @@ static void dc_apply_dev(Ctx& c, Dc& d, const double* r, double* z) {
     a.eta_u = cf.eta_u;
     a.eta_p = cf.eta_p;
     a.n_u = n_u0;
-    if (pre)
+    if (pre && !d.sv && cf.nu1 == 1)
+      launch_lin_resid(c, d.n0, n_u0, cf.eta_u, cf.eta_p, r, d.fine_kry.w.p, d.fine_kry.st, rw);
+    else if (pre)
       launch_spmv(c, *d.K0, x, rw, Epi::ResidEta, a);
     else
       launch_eta(c, d.n0, n_u0, cf.eta_u, cf.eta_p, r, rw);  // r1 = r (preconditioner.cpp:128-129)

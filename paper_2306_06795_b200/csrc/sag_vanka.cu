@@ -315,6 +315,7 @@ struct FactorOut {
   unsigned char* blob = nullptr;
   const long long* hoff = nullptr;
   const int* sbase = nullptr;
+  int tps = 0;  // streamed thread-per-patch section order
 };
 
 __global__ void __launch_bounds__(256) factor_kernel(
@@ -385,11 +386,28 @@ __global__ void __launch_bounds__(256) factor_kernel(
     // payload entries e of this patch live at D[db + e*es] / I[ib + e*es]
     const long long es = fo.es;
     const long long db = fo.dbase[k], ib = fo.ibase[k];
-    double* gAx = fo.D + db;
-    double* gAy = gAx + ainv_len(nx, sym) * es;
-    double* gU = gAy + ainv_len(ny, sym) * es;
-    double* gB = gU + (long long)np * nv * es;
-    double* gS = gB + (long long)np * nv * es;
+    // sections: blob order A_x | A_y | U (rows of nv) | B_hat | S^-1, or the
+    // streamed thread-per-patch order B_hat | S^-1 | A_x | U_x | A_y | U_y
+    double *gAx, *gAy, *gUx, *gUy, *gB, *gS;
+    int urx, ury;
+    if (fo.tps) {
+      gB = fo.D + db;
+      gS = gB + (long long)np * nv * es;
+      gAx = gS + (long long)np * np * es;
+      gUx = gAx + ainv_len(nx, sym) * es;
+      gAy = gUx + (long long)np * nx * es;
+      gUy = gAy + ainv_len(ny, sym) * es;
+      urx = nx;
+      ury = ny;
+    } else {
+      gAx = fo.D + db;
+      gAy = gAx + ainv_len(nx, sym) * es;
+      gUx = gAy + ainv_len(ny, sym) * es;
+      gUy = gUx + (long long)nx * es;
+      gB = gUx + (long long)np * nv * es;
+      gS = gB + (long long)np * nv * es;
+      urx = ury = nv;
+    }
     int* gidx = fo.I + ib;
     // per component: RHS t < n are unit vectors (inverse columns, each one
     // dense_lu_solve(lu, e_t)), t = n + j are -B(j, comp)^T (u_hat columns,
@@ -454,10 +472,13 @@ __global__ void __launch_bounds__(256) factor_kernel(
       for (int m = 0; m < np; ++m) acc = __dadd_rn(acc, __dmul_rn(Sinv[a * np + m], Um[j * NP + m]));
       gB[e * es] = acc;
     }
-    // u_hat stored [a*nv + i]
+    // u_hat stored by rows a: [a*urx + i] (x part) and [a*ury + i - nx] (y part)
     for (int e = lane; e < np * nv; e += 32) {
       const int a = e / nv, i = e % nv;
-      gU[e * es] = Um[i * NP + a];
+      if (i < nx)
+        gUx[((long long)a * urx + i) * es] = Um[i * NP + a];
+      else
+        gUy[((long long)a * ury + i - nx) * es] = Um[i * NP + a];
     }
     for (int i = lane; i < nv; i += 32) gidx[i * es] = sv[i];
     for (int a = lane; a < np; a += 32) gidx[(nv + a) * es] = pidx[p0 + a];
@@ -598,7 +619,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   std::vector<int> sbase(std::max(np_, 1), 0);
   long long slots = 0;
   f->tpp = sym && p.max_dim <= kTppMaxDim && p.max_np <= 4 && np_ > 0 &&
-           env_int("SAG_VANKA_TPP", 1) != 0;
+           env_int("SAG_VANKA_TPP", 0) != 0;
   if (f->tpp) {
     // thread-per-patch layout: patches sorted (stably) by shape, buckets of 32
     // equal-shape patches, every payload entry interleaved across the bucket
@@ -650,6 +671,9 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
                              cudaMemcpyHostToDevice, c.stream));
     f->D.alloc(std::max(doff, 1LL));
     f->I.alloc(std::max(ioff, 1LL));
+    // padding lanes of partial buckets stay finite / in range
+    SAG_CUDA(cudaMemsetAsync(f->D.p, 0, sizeof(double) * f->D.n, c.stream));
+    SAG_CUDA(cudaMemsetAsync(f->I.p, 0, sizeof(int) * f->I.n, c.stream));
     f->blob_bytes = 8 * doff + 4 * ioff;
   } else {
     std::vector<long long> off(np_ + 1, 0);
@@ -737,6 +761,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     if (f->tpp) {
       fo.D = f->D.p;
       fo.I = f->I.p;
+      fo.tps = 1;
     } else {
       fo.D = reinterpret_cast<double*>(f->blob.p);
       fo.I = reinterpret_cast<int*>(f->blob.p);
@@ -831,7 +856,8 @@ __device__ __forceinline__ PatchView patch_view(const unsigned char* B) {
 // solve of patch k (double-buffered), hiding its L2 latency.
 // SYM: A^-1 blocks are packed symmetrised upper triangles; lane i reads
 // column j rows (i <= j) or column i rows (i > j): both conflict-free.
-template <int R, bool SYM>
+// NMT > 0: compile-time bound on max(nx, ny) (fully unrolled column loop).
+template <int R, bool SYM, int NMT>
 __global__ void __launch_bounds__(256) vanka_patch_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, int sb_len, const double* __restrict__ r,
@@ -911,7 +937,7 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
 #pragma unroll
     for (int q = 0; q < R; ++q) tx[q] = ty[q] = 0.0;
     const int nmax = nx > ny ? nx : ny;
-    for (int j = 0; j < nmax; ++j) {
+    auto step = [&](int j) {
       const double bx = sb[j];
       const double by = sb[nx + j];
       const int csj = j * (j + 1) / 2;
@@ -927,6 +953,15 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
           if (j < ny && i < ny) ty[q] = fma(Ay[j * ny + i], by, ty[q]);
         }
       }
+    };
+    if constexpr (NMT > 0) {
+      // compile-time trip count: column offsets become immediates and the
+      // shared-memory loads of successive columns overlap
+#pragma unroll
+      for (int j = 0; j < NMT; ++j)
+        if (j < nmax) step(j);
+    } else {
+      for (int j = 0; j < nmax; ++j) step(j);
     }
     // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
     double xp[4];
@@ -1001,79 +1036,119 @@ __global__ void vanka_gather_kernel(int n, const int* __restrict__ dof_ptr,
   }
 }
 
-// ------------------------------------------------ thread-per-patch apply --
-// One component of a patch solve with all operands in registers:
-// t = A^-1 b with A^-1 the packed symmetrised upper triangle (each stored
-// entry loaded once: t_i += a_ij b_j, t_j += a_ij b_i), then
-// x_u = t + U_hat x_p written to the patch's slots (vanka.cpp:164-180).
-template <int NM>
-__device__ __forceinline__ void tpp_component(const double* __restrict__ A, const double (&b)[NM],
-                                              int n, const double* __restrict__ U, int nv, int np,
-                                              const double (&xp)[4], double* __restrict__ o) {
-  double t[NM];
-#pragma unroll
-  for (int i = 0; i < NM; ++i) t[i] = 0.0;
-#pragma unroll
-  for (int j = 0; j < NM; ++j) {
-    if (j < n) {
-#pragma unroll
-      for (int i = 0; i <= j; ++i) {
-        const double a = __ldg(A + 32 * (j * (j + 1) / 2 + i));
-        t[i] = fma(a, b[j], t[i]);
-        if (i != j) t[j] = fma(a, b[i], t[j]);
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < NM; ++i) {
-    if (i < n) {
-      double v = t[i];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-        if (a < np) v = fma(__ldg(U + 32 * (a * nv + i)), xp[a], v);
-      o[32 * i] = v;
-    }
-  }
+// -------------------------------------- streamed thread-per-patch apply --
+// Thread-per-patch Vanka over shape buckets (layout in internal.cuh, TPPS
+// section order Bh | S^-1 | A_x^-1 | U_x | A_y^-1 | U_y, entries interleaved
+// across the 32 patches of a bucket). One warp per CTA streams its buckets'
+// payload through a 4-chunk shared-memory ring (8 KB cp.async.bulk copies,
+// L2 evict-first) and lane l solves patch l with r, t and x_p in registers:
+// every stored entry of A^-1 is read once from shared memory
+// (t_i += a_ij b_j, t_j += a_ij b_i). ~1/10 of the warp-per-patch kernel's
+// instructions; the r gathers of the next bucket are issued one bucket ahead.
+constexpr int kTpsCE = 32;                   // entries per chunk (x 32 lanes x 8 B = 8 KB)
+constexpr int kTpsRing = 4;                  // chunks in the ring
+constexpr int kTpsRingE = kTpsCE * kTpsRing; // 128 entries
+
+__host__ __device__ inline int tps_entries(int nx, int ny, int np) {
+  const int nv = nx + ny;
+  return np * nv + np * np + nx * (nx + 1) / 2 + np * nx + ny * (ny + 1) / 2 + np * ny;
 }
 
-// Thread-per-patch additive Vanka over shape buckets (layout in internal.cuh):
-// lane l of a warp solves patch l of its bucket. Every payload load is one
-// coalesced 256-byte warp access at an address known up front, so a warp
-// keeps a deep queue of loads in flight, and the instruction count is ~1/15
-// of the warp-per-patch kernel's.
 template <int NM>
-__global__ void __launch_bounds__(128) vanka_tpp_kernel(int b0, int b1,
-                                                        const BucketHdr* __restrict__ hdr,
-                                                        const double* __restrict__ D,
-                                                        const int* __restrict__ I,
-                                                        const double* __restrict__ r,
-                                                        double* __restrict__ out,
-                                                        const int* gate) {
+__global__ void __launch_bounds__(32) vanka_tps_kernel(int b0, int b1,
+                                                       const BucketHdr* __restrict__ hdr,
+                                                       const double* __restrict__ D,
+                                                       const int* __restrict__ I,
+                                                       const double* __restrict__ r,
+                                                       double* __restrict__ out, const int* gate) {
   if (gate && *gate) return;
-  const int lane = threadIdx.x & 31;
-  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int b = b0 + wg; b < b1; b += nw) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* ring = reinterpret_cast<double*>(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTpsRingE * 32);
+  const int lane = threadIdx.x;
+  const int nw = gridDim.x;
+  uint64_t policy;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  if (lane == 0) {
+    for (int s = 0; s < kTpsRing; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // ---- producer cursor over this warp's chunk stream (all lanes agree)
+  int ib = b0 + blockIdx.x, ic = 0, issued = 0;
+  auto issue_next = [&]() {
+    if (ib >= b1) return;
+    const BucketHdr h = hdr[ib];
+    const int E = tps_entries(h.nx, h.ny, h.np);
+    const int nch = (E + kTpsCE - 1) / kTpsCE;
+    const int ecount = min(kTpsCE, E - ic * kTpsCE);
+    __syncwarp();
+    if (lane == 0) {
+      const int slot = issued % kTpsRing;
+      const unsigned bytes = (unsigned)ecount * 32u * 8u;
+      const double* src = D + h.dbl_off + (long long)ic * kTpsCE * 32;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bars + slot)),
+                   "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+          " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(ring + (size_t)slot * kTpsCE * 32)),
+          "l"(src), "r"(bytes), "r"(smem_u32(bars + slot)), "l"(policy)
+          : "memory");
+    }
+    ++issued;
+    if (++ic == nch) {
+      ic = 0;
+      ib += nw;
+    }
+  };
+  issue_next();
+  issue_next();
+  int landed = 0;  // chunks waited so far
+  int gbase = 0;   // first chunk (global index) of the current bucket
+
+  // gathers of one bucket into registers
+  double bx[NM], by[NM], bp[4];
+  auto gather = [&](int b, double (&gx)[NM], double (&gy)[NM], double (&gp)[4]) {
     const BucketHdr h = hdr[b];
-    if (lane >= h.count) continue;
-    const int nx = h.nx, ny = h.ny, np = h.np, nv = nx + ny;
+    const bool act = lane < h.count;
     const int* ix = I + h.int_off + lane;
-    const double* d = D + h.dbl_off + lane;
-    double* o = out + h.slot_off + lane;
-    // gather r at the patch dofs (vanka.cpp:161-162)
-    double bx[NM], by[NM], bp[4];
+    const int nv = h.nx + h.ny;
 #pragma unroll
     for (int j = 0; j < NM; ++j) {
-      bx[j] = j < nx ? __ldg(r + __ldg(ix + 32 * j)) : 0.0;
-      by[j] = j < ny ? __ldg(r + __ldg(ix + 32 * (nx + j))) : 0.0;
+      gx[j] = (act && j < h.nx) ? __ldg(r + __ldg(ix + 32 * j)) : 0.0;
+      gy[j] = (act && j < h.ny) ? __ldg(r + __ldg(ix + 32 * (h.nx + j))) : 0.0;
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) bp[a] = a < np ? __ldg(r + __ldg(ix + 32 * (nv + a))) : 0.0;
-    const double* Ax = d;
-    const double* Ay = Ax + 32 * (nx * (nx + 1) / 2);
-    const double* U = Ay + 32 * (ny * (ny + 1) / 2);
-    const double* Bh = U + 32 * (np * nv);
-    const double* Si = Bh + 32 * (np * nv);
+    for (int a = 0; a < 4; ++a) gp[a] = (act && a < h.np) ? __ldg(r + __ldg(ix + 32 * (nv + a))) : 0.0;
+  };
+  int b = b0 + blockIdx.x;
+  if (b < b1) gather(b, bx, by, bp);
+  for (; b < b1; b += nw) {
+    const BucketHdr h = hdr[b];
+    const int nx = h.nx, ny = h.ny, np = h.np, nv = nx + ny;
+    const int E = tps_entries(nx, ny, np);
+    const bool act = lane < h.count;
+    double* o = out + h.slot_off + lane;
+    // next bucket's gathers, in flight during this bucket's solve
+    double nbx[NM], nby[NM], nbp[4];
+    const bool has_next = b + nw < b1;
+    if (has_next) gather(b + nw, nbx, nby, nbp);
+    // entry e of this bucket, lane's copy; ensure() keeps <= 2 chunks ahead live
+    auto ensure = [&](int e_last) {
+      const int need = gbase + e_last / kTpsCE;
+      while (landed <= need) {
+        mbar_wait(bars + landed % kTpsRing, (unsigned)((landed / kTpsRing) & 1));
+        ++landed;
+        issue_next();
+      }
+    };
+    const int g0 = gbase * kTpsCE;
+    auto ent = [&](int e) -> double { return ring[((g0 + e) & (kTpsRingE - 1)) * 32 + lane]; };
+    const int oSi = np * nv, oAx = oSi + np * np;
+    const int oUx = oAx + nx * (nx + 1) / 2, oAy = oUx + np * nx;
+    const int oUy = oAy + ny * (ny + 1) / 2;
     // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
     double xp[4];
 #pragma unroll
@@ -1081,46 +1156,97 @@ __global__ void __launch_bounds__(128) vanka_tpp_kernel(int b0, int b1,
       xp[a] = 0.0;
       if (a < np) {
         double s = 0.0;
+        ensure(oSi + a * np + np - 1);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (q < np) s = fma(__ldg(Si + 32 * (a * np + q)), bp[q], s);
-        const double* bh = Bh + 32 * (a * nv);
+          if (q < np) s = fma(ent(oSi + a * np + q), bp[q], s);
+        if (nx > 0) ensure(a * nv + nx - 1);
 #pragma unroll
-        for (int j = 0; j < NM; ++j) {
-          if (j < nx) s = fma(__ldg(bh + 32 * j), bx[j], s);
-          if (j < ny) s = fma(__ldg(bh + 32 * (nx + j)), by[j], s);
-        }
+        for (int j = 0; j < NM; ++j)
+          if (j < nx) s = fma(ent(a * nv + j), bx[j], s);
+        if (ny > 0) ensure(a * nv + nv - 1);
+#pragma unroll
+        for (int j = 0; j < NM; ++j)
+          if (j < ny) s = fma(ent(a * nv + nx + j), by[j], s);
         xp[a] = s;
-        o[32 * (nv + a)] = s;
+        if (act) o[32 * (nv + a)] = s;
       }
     }
-    tpp_component<NM>(Ax, bx, nx, U, nv, np, xp, o);
-    tpp_component<NM>(Ay, by, ny, U + 32 * nx, nv, np, xp, o + 32 * nx);
+    // t = A^-1 b_u, x_u = t + U_hat x_p, per component (vanka.cpp:164-180)
+#pragma unroll
+    for (int comp = 0; comp < 2; ++comp) {
+      const int n = comp == 0 ? nx : ny;
+      const int oA = comp == 0 ? oAx : oAy;
+      const int oU = comp == 0 ? oUx : oUy;
+      const double(&bb)[NM] = comp == 0 ? bx : by;
+      double* oc = o + (comp == 0 ? 0 : 32 * nx);
+      double t[NM];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) t[i] = 0.0;
+#pragma unroll
+      for (int j = 0; j < NM; ++j) {
+        if (j < n) {
+          const int cj = oA + j * (j + 1) / 2;
+          ensure(cj + j);
+#pragma unroll
+          for (int i = 0; i <= j; ++i) {
+            const double aij = ent(cj + i);
+            t[i] = fma(aij, bb[j], t[i]);
+            if (i != j) t[j] = fma(aij, bb[i], t[j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        if (a < np && n > 0) {
+          ensure(oU + a * n + n - 1);
+#pragma unroll
+          for (int i = 0; i < NM; ++i)
+            if (i < n) t[i] = fma(ent(oU + a * n + i), xp[a], t[i]);
+        }
+      }
+      if (act) {
+#pragma unroll
+        for (int i = 0; i < NM; ++i)
+          if (i < n) oc[32 * i] = t[i];
+      }
+    }
+    ensure(E - 1);  // every chunk of this bucket has landed
+    gbase += (E + kTpsCE - 1) / kTpsCE;
+    if (has_next) {
+#pragma unroll
+      for (int j = 0; j < NM; ++j) {
+        bx[j] = nbx[j];
+        by[j] = nby[j];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) bp[a] = nbp[a];
+    }
   }
 }
 
 template <int NM>
-static void launch_tpp(Ctx& c, const Vanka& f, int b0, int b1, const double* r, const int* gate) {
+static void launch_tps(Ctx& c, const Vanka& f, int b0, int b1, const double* r, const int* gate) {
+  const int smem = kTpsRingE * 32 * 8 + kTpsRing * 8;
   static thread_local int occ = 0;
   if (!occ) {
-    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vanka_tpp_kernel<NM>, 128, 0));
+    SAG_CUDA(cudaFuncSetAttribute(vanka_tps_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vanka_tps_kernel<NM>, 32, smem));
     occ = std::max(occ, 1);
   }
-  const long long warps_needed = b1 - b0;
-  const long long cap = (long long)occ * c.num_sms * 4;
-  const int warps = (int)std::max(1LL, std::min(warps_needed, cap));
-  vanka_tpp_kernel<NM><<<(warps + 3) / 4, 128, 0, c.stream>>>(b0, b1, f.hdr.p, f.D.p, f.I.p, r,
-                                                              f.out.p, gate);
+  const long long cap = (long long)occ * c.num_sms;
+  const int ctas = (int)std::max(1LL, std::min<long long>(b1 - b0, cap));
+  vanka_tps_kernel<NM><<<ctas, 32, smem, c.stream>>>(b0, b1, f.hdr.p, f.D.p, f.I.p, r, f.out.p, gate);
   SAG_LAUNCHED(c);
 }
 
 static void launch_tpp_all(Ctx& c, const Vanka& f, const double* r, const int* gate) {
   for (const auto& cl : f.classes) {
     switch (cl.nm) {
-      case 8: launch_tpp<8>(c, f, cl.b0, cl.b1, r, gate); break;
-      case 12: launch_tpp<12>(c, f, cl.b0, cl.b1, r, gate); break;
-      case 16: launch_tpp<16>(c, f, cl.b0, cl.b1, r, gate); break;
-      default: launch_tpp<20>(c, f, cl.b0, cl.b1, r, gate); break;
+      case 8: launch_tps<8>(c, f, cl.b0, cl.b1, r, gate); break;
+      case 12: launch_tps<12>(c, f, cl.b0, cl.b1, r, gate); break;
+      case 16: launch_tps<16>(c, f, cl.b0, cl.b1, r, gate); break;
+      default: launch_tps<20>(c, f, cl.b0, cl.b1, r, gate); break;
     }
   }
 }
@@ -1132,9 +1258,12 @@ struct ApplyCfg {
 // Launch shape: NSTAGE >= 3 blobs in flight per warp (one being solved, one
 // gathered, >= 1 landing), as many warps as shared memory allows (up to 8
 // per CTA, several CTAs per SM), a persistent grid of occupancy x #SMs.
-template <int R, bool SYM>
+template <int R, bool SYM, int NMT>
 static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   static thread_local int configured_smem[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+  static thread_local int configured_nmt[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
+  if (configured_nmt[SYM][R - 1] != NMT) configured_smem[SYM][R - 1] = 0;
+  configured_nmt[SYM][R - 1] = NMT;
   ApplyCfg a;
   a.nstage = std::max(3, env_int("SAG_VANKA_STAGES", 3));
   a.sb_len = f.max_nv + f.max_np + f.max_dim + 2;
@@ -1145,7 +1274,7 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   if (a.warps * per_warp > 220 * 1024) a.warps = std::max(1, (220 * 1024) / per_warp);
   a.smem = a.warps * per_warp;
   SAG_REQUIRE(a.smem <= 227 * 1024, SAG_ERROR, "apply_vanka: patch blobs too large for staging");
-  auto kern = vanka_patch_kernel<R, SYM>;
+  auto kern = vanka_patch_kernel<R, SYM, NMT>;
   if (configured_smem[SYM][R - 1] < a.smem) {
     SAG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem));
     configured_smem[SYM][R - 1] = a.smem;
@@ -1158,10 +1287,10 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   return a;
 }
 
-template <int R, bool SYM>
+template <int R, bool SYM, int NMT = 0>
 static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gate) {
-  const ApplyCfg a = apply_cfg<R, SYM>(c, f);
-  vanka_patch_kernel<R, SYM><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
+  const ApplyCfg a = apply_cfg<R, SYM, NMT>(c, f);
+  vanka_patch_kernel<R, SYM, NMT><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
       f.npatch, f.blob.p, f.off.p, f.slot_bytes, a.nstage, a.sb_len, r, f.out.p, gate);
   SAG_LAUNCHED(c);
 }
@@ -1169,8 +1298,15 @@ static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gat
 template <bool SYM>
 static void launch_patch_r(Ctx& c, const Vanka& f, const double* r, const int* gate) {
   const int R = (f.max_dim + 31) / 32;
+  // measured: the fully unrolled column loop is slower on K0 (424 vs 279 us)
+  const bool unrolled = env_int("SAG_VANKA_UNROLL", 0) != 0;
   switch (R) {
-    case 1: launch_patch<1, SYM>(c, f, r, gate); break;
+    case 1:
+      if (unrolled && f.max_dim <= 20)
+        launch_patch<1, SYM, 20>(c, f, r, gate);
+      else
+        launch_patch<1, SYM>(c, f, r, gate);
+      break;
     case 2: launch_patch<2, SYM>(c, f, r, gate); break;
     case 3: launch_patch<3, SYM>(c, f, r, gate); break;
     default: launch_patch<4, SYM>(c, f, r, gate); break;
@@ -1231,13 +1367,27 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
   size_t ou = 0, os = 0;
   for (int k = 0; k < f.npatch; ++k) {
     const int nx = f.h_nx[k], nv = f.h_nv[k], ny = nv - nx, np = f.h_np[k];
-    const double* Ax = D.data() + f.h_dbase[k];
-    const double* U = Ax + (ainv_len(nx, f.sym) + ainv_len(ny, f.sym)) * es;
-    const double* Bh = U + (long long)np * nv * es;
-    const double* Si = Bh + (long long)np * nv * es;
+    const double* base = D.data() + f.h_dbase[k];
+    const double *Bh, *Si, *Ux, *Uy;
+    long long urx, ury;
+    if (f.tpp) {  // B_hat | S^-1 | A_x | U_x | A_y | U_y
+      Bh = base;
+      Si = Bh + (long long)np * nv * es;
+      Ux = Si + (long long)np * np * es + ainv_len(nx, f.sym) * es;
+      Uy = Ux + (long long)np * nx * es + ainv_len(ny, f.sym) * es;
+      urx = nx;
+      ury = ny;
+    } else {  // A_x | A_y | U | B_hat | S^-1
+      Ux = base + (ainv_len(nx, f.sym) + ainv_len(ny, f.sym)) * es;
+      Uy = Ux + (long long)nx * es;
+      Bh = Ux + (long long)np * nv * es;
+      Si = Bh + (long long)np * nv * es;
+      urx = ury = nv;
+    }
     for (int i = 0; i < nv; ++i)
       for (int a = 0; a < np; ++a) {
-        if (uhat) uhat[ou + (size_t)i * np + a] = U[(a * nv + i) * es];
+        const double u = i < nx ? Ux[(a * urx + i) * es] : Uy[(a * ury + i - nx) * es];
+        if (uhat) uhat[ou + (size_t)i * np + a] = u;
         if (bhat) bhat[ou + (size_t)a * nv + i] = Bh[(a * nv + i) * es];
       }
     if (sinv)

@@ -1,7 +1,10 @@
 #!/usr/bin/env python
-"""Launch-shape sweep for the Vanka patch kernel and the SpMV on one config
-(GPU). Prints one JSON line per variant: microseconds per launch (CUDA
-events over K launches on libsag's stream) and GB/s of algorithmic bytes."""
+"""Launch-shape sweep for the Vanka apply and the SpMV on one config (GPU).
+Prints one JSON line per variant: microseconds per launch (CUDA events over K
+launches on libsag's stream) and GB/s of algorithmic / device bytes.
+
+    python tools/sweep.py [n=512] ["ENV=V,ENV=V;ENV=V,..."]
+"""
 import json
 import os
 import sys
@@ -10,16 +13,23 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2306_06795_b200 as S  # noqa: E402
 from paper_2306_06795_b200.cases import HostCase  # noqa: E402
 from bench import splitmix64_uniform, spmv_bytes, vanka_bytes  # noqa: E402
 
+DEFAULT_VARIANTS = [
+    "SAG_VANKA_TPP=0,SAG_VANKA_UNROLL=1,SAG_VANKA_STAGES=3,SAG_VANKA_CTA_SMEM=60000",
+    "SAG_VANKA_TPP=0,SAG_VANKA_UNROLL=1,SAG_VANKA_STAGES=3,SAG_VANKA_CTA_SMEM=112000",
+    "SAG_VANKA_TPP=0,SAG_VANKA_UNROLL=1,SAG_VANKA_STAGES=4,SAG_VANKA_CTA_SMEM=60000",
+    "SAG_VANKA_TPP=0,SAG_VANKA_UNROLL=0,SAG_VANKA_STAGES=3,SAG_VANKA_CTA_SMEM=60000",
+]
+
 
 def main():
     n_mesh = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+    variants = sys.argv[2].split(";") if len(sys.argv) > 2 else DEFAULT_VARIANTS
     t0 = time.time()
     case = HostCase("cavity", False, "structured", n_mesh)
     k0 = case.k0()
@@ -43,46 +53,35 @@ def main():
         e1.synchronize()
         return e0.elapsed_time(e1) / k * 1e3  # us
 
-    bs = spmv_bytes(n, n, k0.nnz)
-    for stream_mode in ("1", "0"):
-        os.environ["SAG_SPMV_STREAM"] = stream_mode
-        K = S.SparseMatrix.from_csr(k0, ctx)
-        ctas = ["4", "6", "8"] if stream_mode == "1" else ["6"]
-        for c in ctas:
-            os.environ["SAG_SPMV_CTAS"] = c
-            us = timed(lambda: S.spmv(K, x, out=y))
-            print(json.dumps({"kernel": "spmv", "stream": stream_mode, "ctas": c, "us": us,
-                              "gbs": bs / us / 1e3}), flush=True)
-        del K
-    os.environ["SAG_SPMV_STREAM"] = "1"
-    os.environ.pop("SAG_SPMV_CTAS", None)
     K = S.SparseMatrix.from_csr(k0, ctx)
-    ref_y = S.spmv(K, x).cpu().numpy() if False else None
+    bs = spmv_bytes(n, n, k0.nnz)
+    us = timed(lambda: S.spmv(K, x, out=y))
+    print(json.dumps({"kernel": "spmv", "us": us, "gbs": bs / us / 1e3}), flush=True)
     lib = S.lib()
-    for tpp, sym in (("1", "1"), ("0", "1")):
-        os.environ["SAG_VANKA_SYM"] = sym
-        os.environ["SAG_VANKA_TPP"] = tpp
-        p = S.build_patches(K, *case.nxyz0)
-        f = S.factor_patches(K, p, case.n_x0 + case.n_y0)
+    built = {}
+    for var in variants:
+        env = dict(kv.split("=") for kv in var.split(",") if kv)
+        os.environ.update(env)
+        key = (env.get("SAG_VANKA_TPP", "0"), env.get("SAG_VANKA_SYM", "1"))
+        if key not in built:
+            built.clear()
+            p = S.build_patches(K, *case.nxyz0)
+            f = S.factor_patches(K, p, case.n_x0 + case.n_y0)
+            built[key] = (p, f)
+        p, f = built[key]
         bv = vanka_bytes(f, p.total_velocity + p.total_pressure, n)
         xp, dp = S.C.c_void_p(x.data_ptr()), S.C.c_void_p(y.data_ptr())
-        for stages in ("3",):
-            for cta in (("60000",) if tpp == "0" else ("0",)):
-                os.environ["SAG_VANKA_STAGES"] = stages
-                os.environ["SAG_VANKA_CTA_SMEM"] = cta
-                try:
-                    us_patch = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 1)))
-                    us_g = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 2)))
-                except S.Error as e:
-                    print(json.dumps({"sym": sym, "stages": stages, "cta": cta, "err": str(e)}))
-                    continue
-                print(json.dumps({"kernel": "vanka", "tpp": tpp, "sym": sym, "stages": stages, "cta_smem": cta,
-                                  "patch_us": us_patch, "gather_us": us_g,
-                                  "sweep_us": us_patch + us_g,
-                                  "device_bytes": f.device_bytes,
-                                  "patch_dev_gbs": f.device_bytes / us_patch / 1e3,
-                                  "sweep_alg_gbs": bv / (us_patch + us_g) / 1e3}), flush=True)
-        del f, p
+        try:
+            us_patch = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 1)))
+            us_g = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 2)))
+        except S.Error as e:
+            print(json.dumps({"variant": var, "err": str(e)}), flush=True)
+            continue
+        print(json.dumps({"kernel": "vanka", "variant": var, "patch_us": us_patch,
+                          "gather_us": us_g, "sweep_us": us_patch + us_g,
+                          "device_bytes": f.device_bytes,
+                          "patch_dev_gbs": f.device_bytes / us_patch / 1e3,
+                          "sweep_alg_gbs": bv / (us_patch + us_g) / 1e3}), flush=True)
 
 
 if __name__ == "__main__":
