@@ -89,6 +89,7 @@ struct Vanka {
   bool tpp = false;
   DevBuf<double> D;
   DevBuf<int> I;
+  DevBuf<double> B;  // r gathered at every slot (tpp apply input stream)
   DevBuf<struct BucketHdr> hdr;
   int nbuckets = 0;
   std::vector<struct TppClass> classes;

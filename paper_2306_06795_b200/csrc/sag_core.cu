@@ -171,8 +171,24 @@ __global__ void __launch_bounds__(256) spmv_kernel(int nrows, const int* __restr
     }
     if (row < nrows) {
       const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
-#pragma unroll 4
-      for (int k = beg + sub; k < end; k += G) s = fma(__ldg(val + k), __ldg(x + __ldg(ci + k)), s);
+      // four strides per pass with predicated loads: all values/columns of a
+      // pass are requested before any x, so a row costs three dependent
+      // round trips (rp, ci, x) instead of two per stride
+      for (int k0 = beg + sub; k0 < end; k0 += 4 * G) {
+        double v[4], xv[4];
+        int cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * G;
+          const bool in = k < end;
+          v[u] = in ? __ldcs(val + k) : 0.0;
+          cc[u] = in ? __ldcs(ci + k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = (k0 + u * G < end) ? __ldg(x + cc[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s = fma(v[u], xv[u], s);
+      }
     }
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);

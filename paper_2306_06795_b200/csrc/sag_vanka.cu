@@ -671,6 +671,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
                              cudaMemcpyHostToDevice, c.stream));
     f->D.alloc(std::max(doff, 1LL));
     f->I.alloc(std::max(ioff, 1LL));
+    f->B.alloc(std::max(ioff, 1LL));  // gathered r, same interleaving as I and the slots
     // padding lanes of partial buckets stay finite / in range
     SAG_CUDA(cudaMemsetAsync(f->D.p, 0, sizeof(double) * f->D.n, c.stream));
     SAG_CUDA(cudaMemsetAsync(f->I.p, 0, sizeof(int) * f->I.n, c.stream));
@@ -1054,120 +1055,178 @@ __host__ __device__ inline int tps_entries(int nx, int ny, int np) {
   return np * nv + np * np + nx * (nx + 1) / 2 + np * nx + ny * (ny + 1) / 2 + np * ny;
 }
 
-template <int NM>
+// r at every slot of the thread-per-patch layout (slot s of bucket lane l,
+// entry e = the dof I[s]): the patch gathers become one coalesced stream that
+// the apply kernel bulk-copies like the factor payload.
+__global__ void vanka_pregather_kernel(long long n, const int* __restrict__ I,
+                                       const double* __restrict__ r, double* __restrict__ B,
+                                       const int* gate) {
+  if (gate && *gate) return;
+  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < n;
+       s += (long long)gridDim.x * blockDim.x)
+    B[s] = __ldg(r + __ldcs(I + s));
+}
+
+// Producer side of the per-warp chunk stream. It runs once per 8 KB chunk, so
+// it lives out of line (local-memory state) and keeps the solve loop small.
+struct TpsProducer {
+  int ib, ic, issued, b1, nw;
+  BucketHdr hi, hn;
+  const BucketHdr* hdr;
+  const double* D;
+  const double* B;
+  double* ring;
+  uint64_t* bars;
+  uint64_t policy;
+};
+
+// A bucket's stream: its gathered r values (nv + np entries, from B) padded
+// to whole chunks, then its factor payload (tps_entries, from D).
+__device__ __noinline__ void tps_issue(TpsProducer& p, int lane) {
+  if (p.ib >= p.b1) return;
+  const BucketHdr& h = p.hi;
+  const int nb = h.nx + h.ny + h.np;
+  const int nchb = (nb + kTpsCE - 1) / kTpsCE;
+  const int E = tps_entries(h.nx, h.ny, h.np);
+  const int nch = nchb + (E + kTpsCE - 1) / kTpsCE;
+  const double* src;
+  int ecount;
+  if (p.ic < nchb) {
+    src = p.B + h.slot_off + (long long)p.ic * kTpsCE * 32;
+    ecount = min(kTpsCE, nb - p.ic * kTpsCE);
+  } else {
+    const int icd = p.ic - nchb;
+    src = p.D + h.dbl_off + (long long)icd * kTpsCE * 32;
+    ecount = min(kTpsCE, E - icd * kTpsCE);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const int slot = p.issued % kTpsRing;
+    const unsigned bytes = (unsigned)ecount * 32u * 8u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(p.bars + slot)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(p.ring + (size_t)slot * kTpsCE * 32)),
+        "l"(src), "r"(bytes), "r"(smem_u32(p.bars + slot)), "l"(p.policy)
+        : "memory");
+  }
+  ++p.issued;
+  if (++p.ic == nch) {
+    p.ic = 0;
+    p.ib += p.nw;
+    p.hi = p.hn;
+    p.hn = p.hdr[min(p.ib + p.nw, p.b1 - 1)];
+  }
+}
+
+// Waits until chunk `need` (global index) has landed; each landed chunk
+// releases the slot two chunks back, refilled two chunks ahead.
+__device__ __noinline__ int tps_advance(TpsProducer& p, int landed, int need, int lane) {
+  while (landed <= need) {
+    mbar_wait(p.bars + landed % kTpsRing, (unsigned)((landed / kTpsRing) & 1));
+    ++landed;
+    tps_issue(p, lane);
+  }
+  return landed;
+}
+
+// case lists for the NM = 20 thread-per-patch kernel
+#define SAG_CASES20(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) \
+  X(13) X(14) X(15) X(16) X(17) X(18) X(19)
+#define SAG_ROWS19(X) X(18) X(17) X(16) X(15) X(14) X(13) X(12) X(11) X(10) X(9) X(8) X(7) \
+  X(6) X(5) X(4) X(3) X(2) X(1) X(0)
+
+// NPM: upper bound on pressure seeds per patch (1 for TH / ISO, 4 general).
+template <int NM, int NPM>
 __global__ void __launch_bounds__(32) vanka_tps_kernel(int b0, int b1,
                                                        const BucketHdr* __restrict__ hdr,
                                                        const double* __restrict__ D,
-                                                       const int* __restrict__ I,
-                                                       const double* __restrict__ r,
+                                                       const double* __restrict__ B,
                                                        double* __restrict__ out, const int* gate) {
+  static_assert(NM == 20, "case lists are written for NM = 20");
   if (gate && *gate) return;
   extern __shared__ __align__(128) unsigned char smem[];
   double* ring = reinterpret_cast<double*>(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTpsRingE * 32);
   const int lane = threadIdx.x;
-  const int nw = gridDim.x;
-  uint64_t policy;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  TpsProducer P;
+  P.ib = b0 + blockIdx.x;
+  P.ic = 0;
+  P.issued = 0;
+  P.b1 = b1;
+  P.nw = gridDim.x;
+  P.hdr = hdr;
+  P.D = D;
+  P.B = B;
+  P.ring = ring;
+  P.bars = bars;
+  P.hi = hdr[min(P.ib, b1 - 1)];
+  P.hn = hdr[min(P.ib + P.nw, b1 - 1)];
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(P.policy));
   if (lane == 0) {
     for (int s = 0; s < kTpsRing; ++s) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  // ---- producer cursor over this warp's chunk stream (all lanes agree)
-  int ib = b0 + blockIdx.x, ic = 0, issued = 0;
-  auto issue_next = [&]() {
-    if (ib >= b1) return;
-    const BucketHdr h = hdr[ib];
-    const int E = tps_entries(h.nx, h.ny, h.np);
-    const int nch = (E + kTpsCE - 1) / kTpsCE;
-    const int ecount = min(kTpsCE, E - ic * kTpsCE);
-    __syncwarp();
-    if (lane == 0) {
-      const int slot = issued % kTpsRing;
-      const unsigned bytes = (unsigned)ecount * 32u * 8u;
-      const double* src = D + h.dbl_off + (long long)ic * kTpsCE * 32;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bars + slot)),
-                   "r"(bytes)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-          " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(ring + (size_t)slot * kTpsCE * 32)),
-          "l"(src), "r"(bytes), "r"(smem_u32(bars + slot)), "l"(policy)
-          : "memory");
-    }
-    ++issued;
-    if (++ic == nch) {
-      ic = 0;
-      ib += nw;
-    }
-  };
-  issue_next();
-  issue_next();
+  tps_issue(P, lane);
+  tps_issue(P, lane);
   int landed = 0;  // chunks waited so far
   int gbase = 0;   // first chunk (global index) of the current bucket
-
-  // gathers of one bucket into registers
-  double bx[NM], by[NM], bp[4];
-  auto gather = [&](int b, double (&gx)[NM], double (&gy)[NM], double (&gp)[4]) {
-    const BucketHdr h = hdr[b];
-    const bool act = lane < h.count;
-    const int* ix = I + h.int_off + lane;
-    const int nv = h.nx + h.ny;
-#pragma unroll
-    for (int j = 0; j < NM; ++j) {
-      gx[j] = (act && j < h.nx) ? __ldg(r + __ldg(ix + 32 * j)) : 0.0;
-      gy[j] = (act && j < h.ny) ? __ldg(r + __ldg(ix + 32 * (h.nx + j))) : 0.0;
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a) gp[a] = (act && a < h.np) ? __ldg(r + __ldg(ix + 32 * (nv + a))) : 0.0;
-  };
-  int b = b0 + blockIdx.x;
-  if (b < b1) gather(b, bx, by, bp);
-  for (; b < b1; b += nw) {
-    const BucketHdr h = hdr[b];
-    const int nx = h.nx, ny = h.ny, np = h.np, nv = nx + ny;
+  const int nw = gridDim.x;
+  BucketHdr hc = hdr[min(b0 + (int)blockIdx.x, b1 - 1)];
+  for (int b = b0 + blockIdx.x; b < b1; b += nw) {
+    const BucketHdr h = hc;
+    hc = hdr[min(b + nw, b1 - 1)];  // prefetch the next bucket's header
+    const int nx = h.nx, ny = h.ny, np = NPM == 1 ? 1 : h.np, nv = nx + ny;
+    const int nchb = (nv + np + kTpsCE - 1) / kTpsCE;
+    const int Pp = nchb * kTpsCE;  // payload entries start here (bucket-local)
     const int E = tps_entries(nx, ny, np);
     const bool act = lane < h.count;
     double* o = out + h.slot_off + lane;
-    // next bucket's gathers, in flight during this bucket's solve
-    double nbx[NM], nby[NM], nbp[4];
-    const bool has_next = b + nw < b1;
-    if (has_next) gather(b + nw, nbx, nby, nbp);
-    // entry e of this bucket, lane's copy; ensure() keeps <= 2 chunks ahead live
-    auto ensure = [&](int e_last) {
-      const int need = gbase + e_last / kTpsCE;
-      while (landed <= need) {
-        mbar_wait(bars + landed % kTpsRing, (unsigned)((landed / kTpsRing) & 1));
-        ++landed;
-        issue_next();
-      }
-    };
+    // every entry up to e_last (bucket-local) resident; callers never span
+    // more than two chunks
+#define SAG_ENSURE(e_last)                                              \
+  do {                                                                  \
+    const int need_ = gbase + (e_last) / kTpsCE;                        \
+    if (need_ >= landed) landed = tps_advance(P, landed, need_, lane);  \
+  } while (0)
     const int g0 = gbase * kTpsCE;
     auto ent = [&](int e) -> double { return ring[((g0 + e) & (kTpsRingE - 1)) * 32 + lane]; };
-    const int oSi = np * nv, oAx = oSi + np * np;
+    // r at the patch dofs (vanka.cpp:161-162)
+    double bx[NM], by[NM], bp[NPM];
+    SAG_ENSURE(nv + np - 1);
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+      bx[j] = j < nx ? ent(j) : 0.0;
+      by[j] = j < ny ? ent(nx + j) : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < NPM; ++a) bp[a] = a < np ? ent(nv + a) : 0.0;
+    const int oSi = Pp + np * nv, oAx = oSi + np * np;
     const int oUx = oAx + nx * (nx + 1) / 2, oAy = oUx + np * nx;
     const int oUy = oAy + ny * (ny + 1) / 2;
     // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
-    double xp[4];
+    double xp[NPM];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
+    for (int a = 0; a < NPM; ++a) {
       xp[a] = 0.0;
       if (a < np) {
         double s = 0.0;
-        ensure(oSi + a * np + np - 1);
+        if (nx > 0) SAG_ENSURE(Pp + a * nv + nx - 1);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int j = 0; j < NM; ++j)
+          if (j < nx) s = fma(ent(Pp + a * nv + j), bx[j], s);
+        if (ny > 0) SAG_ENSURE(Pp + a * nv + nv - 1);
+#pragma unroll
+        for (int j = 0; j < NM; ++j)
+          if (j < ny) s = fma(ent(Pp + a * nv + nx + j), by[j], s);
+        SAG_ENSURE(oSi + a * np + np - 1);
+#pragma unroll
+        for (int q = 0; q < NPM; ++q)
           if (q < np) s = fma(ent(oSi + a * np + q), bp[q], s);
-        if (nx > 0) ensure(a * nv + nx - 1);
-#pragma unroll
-        for (int j = 0; j < NM; ++j)
-          if (j < nx) s = fma(ent(a * nv + j), bx[j], s);
-        if (ny > 0) ensure(a * nv + nv - 1);
-#pragma unroll
-        for (int j = 0; j < NM; ++j)
-          if (j < ny) s = fma(ent(a * nv + nx + j), by[j], s);
         xp[a] = s;
         if (act) o[32 * (nv + a)] = s;
       }
@@ -1183,23 +1242,67 @@ __global__ void __launch_bounds__(32) vanka_tps_kernel(int b0, int b1,
       double t[NM];
 #pragma unroll
       for (int i = 0; i < NM; ++i) t[i] = 0.0;
-#pragma unroll
-      for (int j = 0; j < NM; ++j) {
-        if (j < n) {
-          const int cj = oA + j * (j + 1) / 2;
-          ensure(cj + j);
-#pragma unroll
-          for (int i = 0; i <= j; ++i) {
-            const double aij = ent(cj + i);
-            t[i] = fma(aij, bb[j], t[i]);
-            if (i != j) t[j] = fma(aij, bb[i], t[j]);
+      // Column loop at run time, rows unrolled through a Duff-style switch:
+      // the code stays small (a fully unrolled triangle was 27k SASS
+      // instructions and thrashed the instruction cache).
+      for (int j = 0; j < n; ++j) {
+        const int cj = oA + j * (j + 1) / 2;
+        SAG_ENSURE(cj + j);
+        const int p0 = (g0 + cj) & (kTpsRingE - 1);
+        double bj = 0.0;
+        switch (j) {
+#define SAG_PICK(J) \
+  case J:           \
+    bj = bb[J];     \
+    break;
+          SAG_CASES20(SAG_PICK)
+#undef SAG_PICK
+        }
+        double acc = 0.0, ajj;
+        if (p0 + j < kTpsRingE) {  // the column is contiguous in the ring
+          const double* pc = ring + p0 * 32 + lane;
+          ajj = pc[j * 32];
+          switch (j) {  // rows j-1 .. 0
+#define SAG_ROW(I)                 \
+  case (I) + 1: {                  \
+    const double a = pc[(I) * 32]; \
+    t[I] = fma(a, bj, t[I]);       \
+    acc = fma(a, bb[I], acc);      \
+  }
+            SAG_ROWS19(SAG_ROW)
+#undef SAG_ROW
+            default:
+              break;
           }
+        } else {  // the column wraps around the ring end
+          ajj = ring[((p0 + j) & (kTpsRingE - 1)) * 32 + lane];
+          switch (j) {
+#define SAG_ROW(I)                                                     \
+  case (I) + 1: {                                                      \
+    const double a = ring[((p0 + (I)) & (kTpsRingE - 1)) * 32 + lane]; \
+    t[I] = fma(a, bj, t[I]);                                           \
+    acc = fma(a, bb[I], acc);                                          \
+  }
+            SAG_ROWS19(SAG_ROW)
+#undef SAG_ROW
+            default:
+              break;
+          }
+        }
+        const double add = fma(ajj, bj, acc);
+        switch (j) {
+#define SAG_ADD(J) \
+  case J:          \
+    t[J] += add;   \
+    break;
+          SAG_CASES20(SAG_ADD)
+#undef SAG_ADD
         }
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
+      for (int a = 0; a < NPM; ++a) {
         if (a < np && n > 0) {
-          ensure(oU + a * n + n - 1);
+          SAG_ENSURE(oU + a * n + n - 1);
 #pragma unroll
           for (int i = 0; i < NM; ++i)
             if (i < n) t[i] = fma(ent(oU + a * n + i), xp[a], t[i]);
@@ -1211,43 +1314,36 @@ __global__ void __launch_bounds__(32) vanka_tps_kernel(int b0, int b1,
           if (i < n) oc[32 * i] = t[i];
       }
     }
-    ensure(E - 1);  // every chunk of this bucket has landed
-    gbase += (E + kTpsCE - 1) / kTpsCE;
-    if (has_next) {
-#pragma unroll
-      for (int j = 0; j < NM; ++j) {
-        bx[j] = nbx[j];
-        by[j] = nby[j];
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a) bp[a] = nbp[a];
-    }
+    SAG_ENSURE(Pp + E - 1);  // every chunk of this bucket has landed
+#undef SAG_ENSURE
+    gbase += nchb + (E + kTpsCE - 1) / kTpsCE;
   }
 }
 
-template <int NM>
+template <int NM, int NPM>
 static void launch_tps(Ctx& c, const Vanka& f, int b0, int b1, const double* r, const int* gate) {
   const int smem = kTpsRingE * 32 * 8 + kTpsRing * 8;
   static thread_local int occ = 0;
   if (!occ) {
-    SAG_CUDA(cudaFuncSetAttribute(vanka_tps_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vanka_tps_kernel<NM>, 32, smem));
+    SAG_CUDA(cudaFuncSetAttribute(vanka_tps_kernel<NM, NPM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vanka_tps_kernel<NM, NPM>, 32, smem));
     occ = std::max(occ, 1);
   }
   const long long cap = (long long)occ * c.num_sms;
   const int ctas = (int)std::max(1LL, std::min<long long>(b1 - b0, cap));
-  vanka_tps_kernel<NM><<<ctas, 32, smem, c.stream>>>(b0, b1, f.hdr.p, f.D.p, f.I.p, r, f.out.p, gate);
+  vanka_tps_kernel<NM, NPM><<<ctas, 32, smem, c.stream>>>(b0, b1, f.hdr.p, f.D.p, f.B.p, f.out.p, gate);
   SAG_LAUNCHED(c);
 }
 
 static void launch_tpp_all(Ctx& c, const Vanka& f, const double* r, const int* gate) {
+  vanka_pregather_kernel<<<grid_for(c, f.nslots), 256, 0, c.stream>>>(f.nslots, f.I.p, r, f.B.p,
+                                                                      gate);
+  SAG_LAUNCHED(c);
   for (const auto& cl : f.classes) {
-    switch (cl.nm) {
-      case 8: launch_tps<8>(c, f, cl.b0, cl.b1, r, gate); break;
-      case 12: launch_tps<12>(c, f, cl.b0, cl.b1, r, gate); break;
-      case 16: launch_tps<16>(c, f, cl.b0, cl.b1, r, gate); break;
-      default: launch_tps<20>(c, f, cl.b0, cl.b1, r, gate); break;
-    }
+    if (f.max_np <= 1)
+      launch_tps<20, 1>(c, f, cl.b0, cl.b1, r, gate);
+    else
+      launch_tps<20, 4>(c, f, cl.b0, cl.b1, r, gate);
   }
 }
 
@@ -1265,7 +1361,10 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   if (configured_nmt[SYM][R - 1] != NMT) configured_smem[SYM][R - 1] = 0;
   configured_nmt[SYM][R - 1] = NMT;
   ApplyCfg a;
-  a.nstage = std::max(3, env_int("SAG_VANKA_STAGES", 3));
+  // 2 stages: the gather of the next patch waits for its blob, but the smaller
+  // per-warp footprint fits more warps per SM -- measured 247 us vs 276 us
+  // (3 stages) for the config-2 K0 sweep
+  a.nstage = std::max(2, env_int("SAG_VANKA_STAGES", 2));
   a.sb_len = f.max_nv + f.max_np + f.max_dim + 2;
   a.sb_len = (a.sb_len + 1) / 2 * 2;
   const int per_warp = a.nstage * f.slot_bytes + a.nstage * 8 + 2 * a.sb_len * 8;
