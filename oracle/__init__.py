@@ -578,6 +578,14 @@ class RefCase:
     def custom_th(n, tagger=0, jitter=0.0, force=0) -> "RefCase":
         return RefCase(rlib().ref_case_custom_th(n, tagger, jitter, force))
 
+    @staticmethod
+    def mesh_forced(path, k1, k2) -> "RefCase":
+        """BASELINE config 4 on a mesh JSON (zero velocity, f = (sin k1 x, cos k2 y))."""
+        L = rlib()
+        L.ref_case_mesh_forced.restype = vp
+        L.ref_case_mesh_forced.argtypes = [C.c_char_p, C.c_double, C.c_double]
+        return RefCase(L.ref_case_mesh_forced(path.encode(), k1, k2))
+
     def rhs(self):
         r = np.empty(self.n0)
         rlib().ref_case_rhs(self.h, dp(r))

@@ -262,6 +262,30 @@ void* ref_case_custom_th(int n, int tagger, double jitter, int force) {
   return rc == OK ? out : nullptr;
 }
 
+// BASELINE config 4 through the reference: mesh JSON read by read_mesh
+// (mesh.cpp:230-289), every boundary edge DirichletZero, body force
+// f = (sin(k1 x), cos(k2 y)), enclosed (all-Dirichlet) TH + ISO + transfer.
+void* ref_case_mesh_forced(const char* path, double k1, double k2) {
+  CaseH* out = nullptr;
+  int rc = guard([&] {
+    ProblemData prob = zero_problem();
+    prob.force = [k1, k2](double x, double y) {
+      return std::array<double, 2>{std::sin(k1 * x), std::cos(k2 * y)};
+    };
+    prob.check_compatibility = false;
+    auto* h = new CaseH;
+    h->c.enclosed = true;
+    h->c.mesh = read_mesh(path);
+    for (auto& be : h->c.mesh.boundary_edges) be.tag = BoundaryTag::DirichletZero;
+    h->c.sys0 = assemble_taylor_hood(h->c.mesh, prob);
+    auto [mf, qmap] = quadrisect(h->c.mesh);
+    h->c.sys1 = assemble_iso(h->c.mesh, mf, qmap, prob);
+    h->c.transfer = build_th_transfer(h->c.sys0, h->c.sys1);
+    out = h;
+  });
+  return rc == OK ? out : nullptr;
+}
+
 // out = [n_x0, n_y0, n_p0, n_x1, n_y1, n_p1, enclosed, sv]
 int ref_case_info(void* h, int* out) {
   const auto& c = static_cast<CaseH*>(h)->c;

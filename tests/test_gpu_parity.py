@@ -221,3 +221,80 @@ def test_solve_stokes_cavity(S, n, its):
     assert rep.final_relative_residual <= cfg.tol
     assert len(rep.residual_history) == rep.iterations + 1
     assert rel_inf(x, x_ref) <= 1e-6
+
+
+# ----------------------------------------------------- SV (config 3 family)
+def _host_device(S, case_kw, conf):
+    from paper_2306_06795_b200.cases import HostCase
+    h = HostCase(**case_kw)
+    cfg = S.SolverConfig(nu1=conf["nu1"], nu2=conf["nu2"], restart=conf["restart"],
+                         tol=conf["tol"], max_iters=conf["max_iters"],
+                         enclosed_flow=conf["enclosed_flow"], eta_u=conf.get("eta_u", 1.0),
+                         eta_p=conf.get("eta_p", 1.0), omega0=conf.get("omega0", 1.0))
+    K0, dc, _ = h.device(cfg)
+    return h, K0, dc, cfg
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_sv_dc_apply_and_solve(S, n):
+    # Scott-Vogelius: 3-seed element patches, stationary fine relaxation,
+    # pressure duplication / mass-projection transfer (transfer.cpp:18-53)
+    conf = dict(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500, enclosed_flow=True,
+                omega0=0.78, eta_u=1.0, eta_p=2.68)
+    c, d, k0, levels, _ = ref_case(n, sv=True, cfg=conf)
+    h, K0, dc, cfg = _host_device(S, dict(problem="cavity", sv=True, n=n), conf)
+    assert h.n0 == c.n0
+    r = O.splitmix64_uniform(c.n0)
+    assert rel_inf(dc.apply(r), d.apply(r)) <= 1e-8
+    x_ref, rep_ref = d.solve(c.rhs())
+    x, rep = S.solve_stokes(K0, c.rhs(), dc, cfg)
+    assert rep.converged and rep.final_relative_residual <= cfg.tol
+    assert abs(rep.iterations - rep_ref["iterations"]) <= 1
+
+
+def test_unstructured_forced_solve(S, tmp_path):
+    # BASELINE config 4 family: jittered Delaunay mesh, zero velocity, body force
+    from paper_2306_06795_b200 import meshgen
+    path = meshgen.write_mesh(str(tmp_path / "m.json"), 24, seed=7, jitter=0.3)
+    k1, k2 = meshgen.force_wavenumbers()
+    c = O.RefCase.mesh_forced(path, k1, k2)
+    conf = dict(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500, enclosed_flow=True)
+    d = O.RefDC(c, conf)
+    h, K0, dc, cfg = _host_device(S, dict(problem="cavity", mesh_kind="file_forced",
+                                          mesh_path=path, k1=k1, k2=k2), conf)
+    assert h.n0 == c.n0 and np.array_equal(h.rhs(), c.rhs())
+    r = O.splitmix64_uniform(c.n0)
+    assert rel_inf(dc.apply(r), d.apply(r)) <= 1e-9
+    x_ref, rep_ref = d.solve(c.rhs())
+    x, rep = S.solve_stokes(K0, c.rhs(), dc, cfg)
+    assert rep.converged and rep.final_relative_residual <= cfg.tol
+    assert abs(rep.iterations - rep_ref["iterations"]) <= 1
+
+
+def test_dropin_cpp_adapter_solve(S):
+    # the C++ drop-in (stokesamg::gpu::DCPreconditioner + gpu::solve_stokes)
+    # against the reference's own DCPreconditioner + solve_stokes (config 1)
+    from paper_2306_06795_b200.cases import HostCase
+    c, d, k0, levels, conf = ref_case(64)
+    h = HostCase("cavity", False, "structured", 64)
+    x, rep = h.solve_dropin(nu=1, restart=30, tol=1e-8, max_iters=500)
+    x_ref, rep_ref = d.solve(c.rhs())
+    assert rep["converged"] and abs(rep["iterations"] - rep_ref["iterations"]) <= 1
+    assert rep["final_relative_residual"] <= 1e-8
+    assert rel_inf(x, x_ref) <= 1e-6
+
+
+def test_vanka_thread_per_patch_layout(S, monkeypatch):
+    # the opt-in bucketed thread-per-patch representation gives the same apply
+    monkeypatch.setenv("SAG_VANKA_TPP", "1")
+    c, d, k0, levels, _ = ref_case(32)
+    rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0)
+    K = S.SparseMatrix.from_csr(k0)
+    p = S.build_patches(K, *d.nxyz0)
+    f = S.factor_patches(K, p, d.nxyz0[0] + d.nxyz0[1])
+    r = O.splitmix64_uniform(k0.nrows)
+    assert rel_inf(S.apply_vanka(f, r), rv.apply(r)) <= TOL
+    got = f.export(p.export())
+    want = rv.factors()
+    for key in ("uhat", "bhat", "sinv", "weights"):
+        assert np.array_equal(got[key], want[key]), key
