@@ -877,18 +877,19 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
   const int stride = gridDim.x * warps;
   uint64_t policy;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
-  auto issue = [&](int s, int kk) {
+  auto issue_at = [&](int s, long long o0, long long o1) {
     unsigned char* dst = ring + (size_t)s * slot_bytes;
-    const unsigned bytes = (unsigned)(off[kk + 1] - off[kk]);
+    const unsigned bytes = (unsigned)(o1 - o0);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bars + s)),
                  "r"(bytes)
                  : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
         " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-        "l"(blob + off[kk]), "r"(bytes), "r"(smem_u32(bars + s)), "l"(policy)
+        "l"(blob + o0), "r"(bytes), "r"(smem_u32(bars + s)), "l"(policy)
         : "memory");
   };
+  auto issue = [&](int s, int kk) { issue_at(s, off[kk], off[kk + 1]); };
   if (lane == 0) {
     for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -910,6 +911,14 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
   int it = 0;
   for (int k = first; k < npatch; k += stride, ++it) {
     const int stage = it % nstage;
+    // offsets of the blob that refills this stage, loaded now so the refill
+    // at the end of the iteration does not wait on them
+    const int kr = k + nstage * stride;
+    long long ro0 = 0, ro1 = 0;
+    if (lane == 0 && kr < npatch) {
+      ro0 = __ldg(off + kr);
+      ro1 = __ldg(off + kr + 1);
+    }
     const PatchView v = patch_view<SYM>(ring + (size_t)stage * slot_bytes);
     const double* sb = sbuf + (it & 1) * sb_len;
     // prefetch r at the next patch's dofs (its blob was issued nstage-1 solves ago)
@@ -1007,10 +1016,9 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
     }
     __syncwarp();
     if (lane == 0) {
-      const int kr = k + nstage * stride;
       if (kr < npatch) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(stage, kr);
+        issue_at(stage, ro0, ro1);
       }
     }
   }
@@ -1025,13 +1033,27 @@ __global__ void vanka_gather_kernel(int n, const int* __restrict__ dof_ptr,
                                     double* __restrict__ delta, double* __restrict__ xadd,
                                     double omega, const int* gate) {
   if (gate && *gate) return;
+  constexpr int U = 8;  // multiplicities up to U in one pass (K0/ISO0: <= 7)
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
-    const double wd = w[d];
+    const double wd = __ldg(w + d);
+    const double xo = xadd ? xadd[d] : 0.0;
+    const int s0 = __ldg(dof_ptr + d), s1 = __ldg(dof_ptr + d + 1);
     double acc = 0.0;
-    for (int s = dof_ptr[d]; s < dof_ptr[d + 1]; ++s)
-      acc = __dadd_rn(acc, __dmul_rn(wd, __ldcg(out + dof_slot[s])));
+    for (int sb = s0; sb < s1; sb += U) {
+      // all slot ids, then all values, then the ordered sum: two dependent
+      // round trips per pass instead of two per slot
+      int sl[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) sl[u] = sb + u < s1 ? __ldcs(dof_slot + sb + u) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = sb + u < s1 ? __ldcg(out + sl[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (sb + u < s1) acc = __dadd_rn(acc, __dmul_rn(wd, v[u]));
+    }
     if (xadd)
-      xadd[d] = xadd[d] + omega * acc;
+      xadd[d] = xo + omega * acc;
     else
       delta[d] = acc;
   }
