@@ -199,6 +199,123 @@ def run_reference(args, ws, rank):
     print(json.dumps(line))
 
 
+# ------------------------------------------------------- GPU arm, N > 1
+def run_dist(args, ws, rank, local):
+    """Strong scaling of the hot step: K0's patches and rows partitioned
+    across the ranks (paper_2306_06795_b200.dist), forward halo of x and
+    reverse halo of the Vanka partial sums over NCCL point-to-point (NVLink),
+    rank-local libsag kernels."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_06795_b200 as S
+    from paper_2306_06795_b200.cases import HostCase
+    from paper_2306_06795_b200.dist import DistStep, build_partition
+
+    cfg = CONFIGS[args.config]
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if not dist.is_initialized():  # --dist on one GPU without torchrun
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    t0 = time.perf_counter()
+    case = HostCase(cfg["problem"], cfg["sv"], "structured", cfg["n"])
+    k0 = case.k0()
+    host_setup_s = time.perf_counter() - t0
+    ctx = S.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+    n = k0.nrows
+    t1 = time.perf_counter()
+    K0 = S.SparseMatrix.from_csr(k0, ctx)
+    pl = S.build_patches(K0, *case.nxyz0, sv_triples=case.sv).export()
+    plans = build_partition(ws, n, k0.rp, k0.ci, k0.v, pl.pressure_ptr, pl.pressure,
+                            pl.velocity_ptr, pl.velocity)
+    plan = plans[rank]
+    lo, hi = plan.patch_lo, plan.patch_hi
+    sub = S.Patches.from_lists(pl.pressure_ptr[lo:hi + 1] - pl.pressure_ptr[lo],
+                               pl.pressure[pl.pressure_ptr[lo]:pl.pressure_ptr[hi]],
+                               pl.velocity_ptr[lo:hi + 1] - pl.velocity_ptr[lo],
+                               pl.velocity[pl.velocity_ptr[lo]:pl.velocity_ptr[hi]],
+                               pl.nx[lo:hi], ctx=ctx)
+    f = S.factor_patches(K0, sub, case.n_x0 + case.n_y0)
+    mult = np.zeros(n)
+    np.add.at(mult, pl.velocity, 1.0)
+    np.add.at(mult, pl.pressure, 1.0)
+    f.set_weights(np.divide(1.0, mult, out=np.zeros(n), where=mult > 0))
+    rows = S.SparseMatrix(len(plan.owned), n, plan.rows_rp, plan.rows_ci, plan.rows_v, ctx)
+    del K0
+    ctx.synchronize()
+    setup_gpu_s = time.perf_counter() - t1
+    x = torch.from_numpy(splitmix64_uniform(n)).to(dev)
+    delta = torch.empty_like(x)
+    y = torch.empty(len(plan.owned), dtype=torch.float64, device=dev)
+
+    def local_vanka(xv):
+        return S.apply_vanka(f, xv, out=delta)
+
+    def local_spmv(xv):
+        return S.spmv(rows, xv, out=y)
+
+    with torch.cuda.stream(stream):
+        step = DistStep(plan, local_vanka, local_spmv, torch, dist, dev)
+        dist.barrier()  # a collective before the first point-to-point batch
+        for _ in range(max(args.warmup, 3)):
+            step(x)
+        torch.cuda.synchronize(dev)
+        clocks = ClockSampler(local) if rank == 0 else None
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        l0 = ctx.launch_count()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(x)
+        e1.record(stream)
+        e1.synchronize()
+        launches = ctx.launch_count() - l0
+        t_steps = dist_max(e0.elapsed_time(e1) / 1e3, ws)
+        dist.barrier()
+        # e2e: owned inputs from pinned host memory, owned outputs back
+        own = torch.as_tensor(plan.owned, device=dev)
+        xh = torch.from_numpy(splitmix64_uniform(n)[plan.owned]).pin_memory()
+        dh = torch.empty(len(plan.owned), dtype=torch.float64).pin_memory()
+        yh = torch.empty(len(plan.owned), dtype=torch.float64).pin_memory()
+        ke = max(args.steps // 4, 5)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        te0 = time.perf_counter()
+        for _ in range(ke):
+            x.index_copy_(0, own, xh.to(dev, non_blocking=True))
+            dd, yy = step(x)
+            dh.copy_(dd.index_select(0, own), non_blocking=True)
+            yh.copy_(yy, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        t_e2e = dist_max((time.perf_counter() - te0) / ke, ws)
+    clk = clocks.stop() if clocks else None
+    ghosts = dist_max(float(plan.ghost_count()), ws)
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": n / (t_steps / args.steps) / 1e9, "unit": "GDOF/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": 1e3 * t_steps / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: reference build_case cavity + splitmix64 x (SURVEY 8(d))",
+            "config": {"workload": cfg["workload"], "k0_rows": n, "k0_nnz": k0.nnz,
+                       "parallelism": f"row/patch partition x{ws}, NCCL halo",
+                       "max_ghost_dofs_per_rank": int(ghosts),
+                       "l2": "inputs exceed L2; no flush"},
+            "gpu_launches": launches,
+            "e2e": {"value": n / t_e2e / 1e9, "unit": "GDOF/s",
+                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 16 * n},
+            "setup": {"host_reference_setup_s": host_setup_s, "gpu_setup_s": setup_gpu_s},
+        }
+        if clk:
+            out["clocks"] = clk
+        print(json.dumps(out))
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_ours(args, ws, rank, local):
     import torch
@@ -352,10 +469,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the partitioned (halo-exchange) step even at N = 1")
     args = ap.parse_args()
     ws, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif ws > 1 or args.dist:
+        run_dist(args, ws, rank, local)
     else:
         run_ours(args, ws, rank, local)
     if ws > 1:

@@ -112,6 +112,10 @@ int sag_vanka_stats(const sag_vanka* f, long long* stats);
  * weights (length n). Any pointer may be NULL. For parity tests. */
 int sag_vanka_export(sag_ctx* ctx, const sag_vanka* f, double* u_hat, double* b_hat,
                      double* s_inv, double* weights);
+/* Overrides the PoU weights (vanka.cpp:67-73) with the caller's (length n):
+ * a rank that factorizes only its share of the patches of a partitioned
+ * operator needs the global multiplicities. */
+int sag_vanka_set_weights(sag_ctx* ctx, sag_vanka* f, const double* weights);
 /* delta = sum_i V_i^T W K_i^-1 V_i r. Replaces apply_vanka (vanka.hpp:47;
  * vanka.cpp:151-184). */
 int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta);

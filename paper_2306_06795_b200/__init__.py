@@ -133,6 +133,7 @@ SIGNATURES = {
     "sag_vanka_export": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "sag_apply_vanka": (C.c_int, [vp, vp, vp, vp]),
     "sag_apply_vanka_stage": (C.c_int, [vp, vp, vp, vp, C.c_int]),
+    "sag_vanka_set_weights": (C.c_int, [vp, vp, vp]),
     "sag_vanka_relax": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_double]),
     "sag_fgmres": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, C.POINTER(sag_fgmres_options),
                              C.POINTER(sag_krylov_report), vp, C.c_int]),
@@ -400,6 +401,11 @@ class VankaFactorization:
         _check(lib().sag_vanka_export(self.ctx.h, self.h, *[C.c_void_p(a.ctypes.data)
                                                              for a in (u, b, s, w)]))
         return dict(uhat=u[:aux], bhat=b[:aux], sinv=s[:ss], weights=w)
+
+    def set_weights(self, w):
+        """Global PoU weights for a rank holding part of the patches."""
+        p, keep = _vec_in(w, self.n)
+        _check(lib().sag_vanka_set_weights(self.ctx.h, self.h, p))
 
     def __del__(self):
         try:

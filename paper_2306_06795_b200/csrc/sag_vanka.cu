@@ -857,8 +857,8 @@ __device__ __forceinline__ PatchView patch_view(const unsigned char* B) {
 // solve of patch k (double-buffered), hiding its L2 latency.
 // SYM: A^-1 blocks are packed symmetrised upper triangles; lane i reads
 // column j rows (i <= j) or column i rows (i > j): both conflict-free.
-// NMT > 0: compile-time bound on max(nx, ny) (fully unrolled column loop).
-template <int R, bool SYM, int NMT>
+// NPM: upper bound on pressure seeds per patch (1 for TH / ISO levels).
+template <int R, bool SYM, int NPM>
 __global__ void __launch_bounds__(256) vanka_patch_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, int sb_len, const double* __restrict__ r,
@@ -936,54 +936,66 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
         g[q] = i < gn ? __ldg(r + w.idx[i]) : 0.0;
       }
     }
-    const int nx = v.nx, ny = v.ny, np = v.np, nv = v.nv, sbase = v.sbase;
+    const int nx = v.nx, ny = v.ny, np = NPM == 1 ? 1 : v.np, nv = v.nv, sbase = v.sbase;
     const double* Ax = v.Ax;
     const double* Ay = v.Ay;
     const double* U = v.U;
     const double* Bh = v.Bh;
     const double* Si = v.Si;
-    // t = A^-1 b_u per component (vanka.cpp:164-166)
+    // t = A^-1 b_u per component (vanka.cpp:164-166): columns j < min(nx, ny)
+    // update both components, the rest only the larger one (no per-column
+    // component predicates); SYM column offsets j(j+1)/2 are carried along
     double tx[R], ty[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) tx[q] = ty[q] = 0.0;
-    const int nmax = nx > ny ? nx : ny;
-    auto step = [&](int j) {
+    const int nmin = nx < ny ? nx : ny, nmax = nx > ny ? nx : ny;
+    int csj = 0;
+    int j = 0;
+    for (; j < nmin; csj += ++j) {
       const double bx = sb[j];
       const double by = sb[nx + j];
-      const int csj = j * (j + 1) / 2;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int i = lane + 32 * q;
-        if (SYM) {
-          const int a = i <= j ? csj + i : csl[q] + j;
-          if (j < nx && i < nx) tx[q] = fma(Ax[a], bx, tx[q]);
-          if (j < ny && i < ny) ty[q] = fma(Ay[a], by, ty[q]);
-        } else {
-          if (j < nx && i < nx) tx[q] = fma(Ax[j * nx + i], bx, tx[q]);
-          if (j < ny && i < ny) ty[q] = fma(Ay[j * ny + i], by, ty[q]);
+        const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : 0;
+        if (i < nx) tx[q] = fma(SYM ? Ax[a] : Ax[j * nx + i], bx, tx[q]);
+        if (i < ny) ty[q] = fma(SYM ? Ay[a] : Ay[j * ny + i], by, ty[q]);
+      }
+    }
+    if (nx > ny) {
+      for (; j < nmax; csj += ++j) {
+        const double bx = sb[j];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = lane + 32 * q;
+          const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : j * nx + i;
+          if (i < nx) tx[q] = fma(Ax[a], bx, tx[q]);
         }
       }
-    };
-    if constexpr (NMT > 0) {
-      // compile-time trip count: column offsets become immediates and the
-      // shared-memory loads of successive columns overlap
-#pragma unroll
-      for (int j = 0; j < NMT; ++j)
-        if (j < nmax) step(j);
     } else {
-      for (int j = 0; j < nmax; ++j) step(j);
+      for (; j < nmax; csj += ++j) {
+        const double by = sb[nx + j];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = lane + 32 * q;
+          const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : j * ny + i;
+          if (i < ny) ty[q] = fma(Ay[a], by, ty[q]);
+        }
+      }
     }
     // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
-    double xp[4];
+    double xp[NPM];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
+    for (int a = 0; a < NPM; ++a) {
       xp[a] = 0.0;
       if (a < np) {
         double part = 0.0;
         for (int m = lane; m < nv; m += 32) part = fma(Bh[a * nv + m], sb[m], part);
         part = warp_sum(part);
         double sp = 0.0;
-        for (int j = 0; j < np; ++j) sp = fma(Si[a * np + j], sb[nv + j], sp);
+#pragma unroll
+        for (int q = 0; q < NPM; ++q)
+          if (q < np) sp = fma(Si[a * np + q], sb[nv + q], sp);
         xp[a] = sp + part;
         if (lane == 0) out[sbase + nv + a] = xp[a];
       }
@@ -995,14 +1007,14 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
       if (i < nx) {
         double v = tx[q];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < NPM; ++a)
           if (a < np) v = fma(U[a * nv + i], xp[a], v);
         out[sbase + i] = v;
       }
       if (i < ny) {
         double v = ty[q];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < NPM; ++a)
           if (a < np) v = fma(U[a * nv + nx + i], xp[a], v);
         out[sbase + nx + i] = v;
       }
@@ -1376,12 +1388,10 @@ struct ApplyCfg {
 // Launch shape: NSTAGE >= 3 blobs in flight per warp (one being solved, one
 // gathered, >= 1 landing), as many warps as shared memory allows (up to 8
 // per CTA, several CTAs per SM), a persistent grid of occupancy x #SMs.
-template <int R, bool SYM, int NMT>
+template <int R, bool SYM, int NPM>
 static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
-  static thread_local int configured_smem[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-  static thread_local int configured_nmt[2][4] = {{-1, -1, -1, -1}, {-1, -1, -1, -1}};
-  if (configured_nmt[SYM][R - 1] != NMT) configured_smem[SYM][R - 1] = 0;
-  configured_nmt[SYM][R - 1] = NMT;
+  static thread_local int configured_smem[2][4][2] = {};
+  int& configured = configured_smem[SYM][R - 1][NPM == 1 ? 0 : 1];
   ApplyCfg a;
   // 2 stages: the gather of the next patch waits for its blob, but the smaller
   // per-warp footprint fits more warps per SM -- measured 247 us vs 276 us
@@ -1395,10 +1405,10 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   if (a.warps * per_warp > 220 * 1024) a.warps = std::max(1, (220 * 1024) / per_warp);
   a.smem = a.warps * per_warp;
   SAG_REQUIRE(a.smem <= 227 * 1024, SAG_ERROR, "apply_vanka: patch blobs too large for staging");
-  auto kern = vanka_patch_kernel<R, SYM, NMT>;
-  if (configured_smem[SYM][R - 1] < a.smem) {
+  auto kern = vanka_patch_kernel<R, SYM, NPM>;
+  if (configured < a.smem) {
     SAG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem));
-    configured_smem[SYM][R - 1] = a.smem;
+    configured = a.smem;
   }
   int occ = 0;
   SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, a.warps * 32, a.smem));
@@ -1408,40 +1418,38 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   return a;
 }
 
-template <int R, bool SYM, int NMT = 0>
+template <int R, bool SYM, int NPM>
 static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gate) {
-  const ApplyCfg a = apply_cfg<R, SYM, NMT>(c, f);
-  vanka_patch_kernel<R, SYM, NMT><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
+  const ApplyCfg a = apply_cfg<R, SYM, NPM>(c, f);
+  vanka_patch_kernel<R, SYM, NPM><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
       f.npatch, f.blob.p, f.off.p, f.slot_bytes, a.nstage, a.sb_len, r, f.out.p, gate);
   SAG_LAUNCHED(c);
 }
 
-template <bool SYM>
+template <bool SYM, int NPM>
 static void launch_patch_r(Ctx& c, const Vanka& f, const double* r, const int* gate) {
   const int R = (f.max_dim + 31) / 32;
-  // measured: the fully unrolled column loop is slower on K0 (424 vs 279 us)
-  const bool unrolled = env_int("SAG_VANKA_UNROLL", 0) != 0;
   switch (R) {
-    case 1:
-      if (unrolled && f.max_dim <= 20)
-        launch_patch<1, SYM, 20>(c, f, r, gate);
-      else
-        launch_patch<1, SYM>(c, f, r, gate);
-      break;
-    case 2: launch_patch<2, SYM>(c, f, r, gate); break;
-    case 3: launch_patch<3, SYM>(c, f, r, gate); break;
-    default: launch_patch<4, SYM>(c, f, r, gate); break;
+    case 1: launch_patch<1, SYM, NPM>(c, f, r, gate); break;
+    case 2: launch_patch<2, SYM, NPM>(c, f, r, gate); break;
+    case 3: launch_patch<3, SYM, NPM>(c, f, r, gate); break;
+    default: launch_patch<4, SYM, NPM>(c, f, r, gate); break;
   }
 }
 
 static void launch_patch_any(Ctx& c, const Vanka& f, const double* r, const int* gate) {
   if (f.npatch == 0) return;
+  const bool np1 = f.max_np <= 1;  // TH / ISO levels: one pressure seed
   if (f.tpp)
     launch_tpp_all(c, f, r, gate);
+  else if (f.sym && np1)
+    launch_patch_r<true, 1>(c, f, r, gate);
   else if (f.sym)
-    launch_patch_r<true>(c, f, r, gate);
+    launch_patch_r<true, 4>(c, f, r, gate);
+  else if (np1)
+    launch_patch_r<false, 1>(c, f, r, gate);
   else
-    launch_patch_r<false>(c, f, r, gate);
+    launch_patch_r<false, 4>(c, f, r, gate);
 }
 
 void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta, const int* gate) {
@@ -1631,6 +1639,17 @@ int sag_vanka_export(sag_ctx* ctx, const sag_vanka* f, double* u_hat, double* b_
     SAG_NOTNULL(ctx);
     SAG_NOTNULL(f);
     vanka_export(ctx->c, f->f, u_hat, b_hat, s_inv, weights);
+  });
+}
+
+int sag_vanka_set_weights(sag_ctx* ctx, sag_vanka* f, const double* weights) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    SAG_NOTNULL(weights);
+    SAG_CUDA(cudaMemcpyAsync(f->f.w.p, weights, sizeof(double) * f->f.n, cudaMemcpyDefault,
+                             ctx->c.stream));
+    SAG_CUDA(cudaStreamSynchronize(ctx->c.stream));
   });
 }
 
