@@ -77,6 +77,11 @@ int sag_matrix_destroy(sag_matrix* m);
 int sag_matrix_shape(const sag_matrix* m, int* nrows, int* ncols, long long* nnz);
 /* y = m x. Replaces spmv (sparse.hpp:42; sparse.cpp:78-91). */
 int sag_spmv(sag_ctx* ctx, const sag_matrix* m, const double* x, double* y);
+/* SpMV with one of the fused epilogues the solver uses (device pointers, for
+ * per-kernel timing): 0 y = Ax; 1 y = aux - Ax; 2 y += Ax; 3 y = Ax and
+ * (y, aux); 4 y = aux - Ax and ||y||. Reductions land in device scratch. */
+int sag_spmv_fused(sag_ctx* ctx, const sag_matrix* m, const double* x, double* y,
+                   const double* aux, int epilogue);
 /* Replaces norm2 / dot (sparse.hpp:64-65; sparse.cpp:217-227). Deterministic
  * fixed-order two-stage reductions. */
 int sag_norm2(sag_ctx* ctx, int n, const double* v, double* out);

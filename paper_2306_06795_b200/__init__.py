@@ -120,6 +120,7 @@ SIGNATURES = {
     "sag_matrix_destroy": (C.c_int, [vp]),
     "sag_matrix_shape": (C.c_int, [vp, i32p, i32p, i64p]),
     "sag_spmv": (C.c_int, [vp, vp, vp, vp]),
+    "sag_spmv_fused": (C.c_int, [vp, vp, vp, vp, vp, C.c_int]),
     "sag_norm2": (C.c_int, [vp, C.c_int, vp, f64p]),
     "sag_dot": (C.c_int, [vp, C.c_int, vp, vp, f64p]),
     "sag_build_patches": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),

@@ -91,7 +91,8 @@ def kernel_table(fn, steps=1):
     rows = {}
     for e in prof.events():
         if e.device_type.name == "CUDA" or "cuda" in str(e.device_type).lower():
-            name = e.name.split("(")[0].replace("void ", "").replace("sag::", "")
+            name = e.name.replace("void ", "").replace("sag::", "")
+            name = name.split(">(")[0] + ">" if ">(" in name else name.split("(")[0]
             d = rows.setdefault(name, [0, 0.0])
             d[0] += 1
             d[1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total

@@ -58,6 +58,11 @@ def main():
     us = timed(lambda: S.spmv(K, x, out=y))
     print(json.dumps({"kernel": "spmv", "us": us, "gbs": bs / us / 1e3}), flush=True)
     lib = S.lib()
+    aux = torch.from_numpy(splitmix64_uniform(n, 7)).to(dev)
+    xp_, yp_, ap_ = (S.C.c_void_p(t.data_ptr()) for t in (x, y, aux))
+    for epi, name in ((0, "store"), (1, "resid"), (2, "add"), (3, "store_dot"), (4, "resid_ssq")):
+        us = timed(lambda: S._check(lib.sag_spmv_fused(ctx.h, K.h, xp_, yp_, ap_, epi)))
+        print(json.dumps({"kernel": "spmv_" + name, "us": us}), flush=True)
     built = {}
     for var in variants:
         env = dict(kv.split("=") for kv in var.split(",") if kv)
