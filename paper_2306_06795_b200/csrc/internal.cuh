@@ -21,13 +21,14 @@ struct Matrix {
   DevBuf<double> v;
   int group = 8;
   double norm_inf = -1.0;  // cached (sparse.cpp:229-237)
-  // row chunks of the streaming SpMV: chunk c covers rows [chunk_row[c],
-  // chunk_row[c+1]) with at most kChunkNnz entries (0 chunks: vector kernel)
-  DevBuf<int> chunk_row;
-  int nchunks = 0;
+  // TMA-staged SpMV: chunks of tma_rows consecutive rows whose rp/ci/v
+  // ranges are bulk-copied to shared memory (0: the register-path kernel)
+  int tma_rows = 0, tma_slot_nnz = 0, tma_stages = 0, nchunks = 0;
+  mutable int tma_occ[6] = {0, 0, 0, 0, 0, 0};  // resident CTAs per SM, per epilogue
 };
-constexpr int kChunkNnz = 4096;
-constexpr int kChunkRows = 512;
+// CSR arrays are allocated kTmaPad elements long so that bulk copies rounded
+// out to 16-byte boundaries stay inside the allocation
+constexpr int kTmaPad = 4;
 void build_chunks(Ctx& c, Matrix& m);
 
 // Vanka patch sets (vanka.hpp:11-15), CSR-like on device.
@@ -84,6 +85,10 @@ struct Vanka {
   long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
   long long blob_bytes = 0;
   bool sym = false;  // A^-1 blocks stored as packed symmetrised upper triangles
+  // paired blobs: patches with nx == ny <= 31 and one pressure seed store
+  // (A_x, A_y), (U_x, U_y), (B_x, B_y) interleaved element by element so the
+  // apply loads both components with one 16-byte shared-memory access
+  bool pairs = false;
   // thread-per-patch layout (tpp): shape buckets of 32 patches, entries
   // interleaved across the bucket (D: doubles, I: dof indices)
   bool tpp = false;
@@ -100,6 +105,11 @@ struct Vanka {
 
 // Krylov scalar state in device memory (one per FGMRES instance); mirrors the
 // host scalars of krylov.cpp:17-121.
+// Per-patch rule for the paired blob layout (factor, apply and export agree).
+__host__ __device__ inline bool vanka_paired(bool pairs, int nx, int ny, int np) {
+  return pairs && nx == ny && np == 1 && nx <= 31;
+}
+
 struct KState {
   double ref, tol, bd;
   double beta, rnorm, wnorm;

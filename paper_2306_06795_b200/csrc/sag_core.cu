@@ -15,6 +15,7 @@
 #include <mutex>
 
 #include "internal.cuh"
+#include "tma.cuh"
 
 namespace sag {
 
@@ -136,6 +137,37 @@ __device__ __forceinline__ void reduce_finish(double red, const Fin& fin, double
   }
 }
 
+// Epilogue operand of a row (loaded before the row product so its latency
+// overlaps the gathers) and the fused epilogue itself.
+template <Epi E>
+__device__ __forceinline__ double spmv_pre(const SpmvArgs& a, const double* y, int row, bool lead) {
+  if (!lead) return 0.0;
+  if constexpr (E == Epi::StoreDot) return __ldg(a.dotv + row);
+  if constexpr (E == Epi::Resid || E == Epi::ResidEta || E == Epi::ResidSsq) return __ldg(a.b + row);
+  if constexpr (E == Epi::Add) return y[row];
+  return 0.0;
+}
+template <Epi E>
+__device__ __forceinline__ void spmv_epi(const SpmvArgs& a, double* y, int row, double s,
+                                         double pre, double& red) {
+  if constexpr (E == Epi::Store) {
+    y[row] = s;
+  } else if constexpr (E == Epi::Resid) {
+    y[row] = pre - s;
+  } else if constexpr (E == Epi::ResidEta) {
+    y[row] = (row < a.n_u ? a.eta_u : a.eta_p) * (pre - s);
+  } else if constexpr (E == Epi::Add) {
+    y[row] = pre + s;
+  } else if constexpr (E == Epi::StoreDot) {
+    y[row] = s;
+    red = fma(s, pre, red);
+  } else if constexpr (E == Epi::ResidSsq) {
+    const double r = pre - s;
+    y[row] = r;
+    red = fma(r, r, red);
+  }
+}
+
 // ------------------------------------------------------------------ SpMV --
 // G lanes per row; the warp iterates over groups of rows with a warp-uniform
 // trip count so the segmented shuffle tree is always executed by full warps.
@@ -160,15 +192,8 @@ __global__ void __launch_bounds__(256, 8) spmv_kernel(int nrows, const int* __re
     double s = 0.0;
     // the epilogue operand is loaded before the row product so that its
     // latency overlaps the gather instead of adding a dependent round trip
-    double pre = 0.0;
     const bool lead = sub == 0 && row < nrows;
-    if constexpr (E == Epi::StoreDot) {
-      if (lead) pre = __ldg(a.dotv + row);
-    } else if constexpr (E == Epi::Resid || E == Epi::ResidEta || E == Epi::ResidSsq) {
-      if (lead) pre = __ldg(a.b + row);
-    } else if constexpr (E == Epi::Add) {
-      if (lead) pre = y[row];
-    }
+    const double pre = spmv_pre<E>(a, y, row, lead);
     if (row < nrows) {
       const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
       // four strides per pass with predicated loads: all values/columns of a
@@ -192,24 +217,7 @@ __global__ void __launch_bounds__(256, 8) spmv_kernel(int nrows, const int* __re
     }
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-    if (lead) {
-      if constexpr (E == Epi::Store) {
-        y[row] = s;
-      } else if constexpr (E == Epi::Resid) {
-        y[row] = pre - s;
-      } else if constexpr (E == Epi::ResidEta) {
-        y[row] = (row < a.n_u ? a.eta_u : a.eta_p) * (pre - s);
-      } else if constexpr (E == Epi::Add) {
-        y[row] = pre + s;
-      } else if constexpr (E == Epi::StoreDot) {
-        y[row] = s;
-        red = fma(s, pre, red);
-      } else if constexpr (E == Epi::ResidSsq) {
-        const double r = pre - s;
-        y[row] = r;
-        red = fma(r, r, red);
-      }
-    }
+    if (lead) spmv_epi<E>(a, y, row, s, pre, red);
   }
   if constexpr (kRed) reduce_finish(red, a.fin, partials, ticket);
 }
@@ -252,71 +260,157 @@ static void spmv_dispatch_e(Ctx& c, const Matrix& m, const double* x, double* y,
   SAG_LAUNCHED(c);
 }
 
-// Streaming CSR SpMV: a CTA takes a chunk of consecutive rows holding at most
-// kChunkNnz entries, streams the chunk's values/columns fully coalesced
-// (evict-first: K is read once per product, x stays in L2) while gathering x,
-// keeps the products in shared memory, then one thread per row sums its
-// products in column order -- the reference's order (sparse.cpp:85-88), so
-// with the product rounded before the sum the result is bitwise the
-// reference's. Only two dependent memory round trips per chunk, ~16
-// independent loads in flight per thread.
-template <Epi E>
-__global__ void __launch_bounds__(256) spmv_stream_kernel(
-    int nchunks, const int* __restrict__ chunk_row, const int* __restrict__ rp,
+// TMA-staged CSR SpMV. The rows are cut into chunks of 2 x (256 / G)
+// consecutive rows; a persistent CTA streams its chunks' row offsets, column
+// indices and values into an nstage-deep shared-memory ring with
+// cp.async.bulk (one producer thread, L2 evict-first: K is read once per
+// product, x stays in L2), so the HBM stream no longer depends on how many
+// loads each thread keeps in flight. The 256 threads then compute the chunk
+// G lanes per row, both passes' x gathers issued before any product, and
+// release the stage to the producer. Ranges are rounded out to 16-byte
+// boundaries (the CSR arrays carry kTmaPad elements of slack).
+constexpr int kTmaPR = 2;  // rows per row-group per chunk
+struct TmaLayout {
+  int v_off, c_off, r_off, stage_bytes;
+};
+__host__ __device__ inline TmaLayout tma_layout(int rows, int slot_nnz) {
+  TmaLayout L;
+  const int vb = ((slot_nnz + 4) * 8 + 15) & ~15;
+  const int cb = ((slot_nnz + 8) * 4 + 15) & ~15;
+  const int rb = ((rows + 8) * 4 + 15) & ~15;
+  L.v_off = 0;
+  L.c_off = vb;
+  L.r_off = vb + cb;
+  L.stage_bytes = vb + cb + rb;
+  return L;
+}
+
+template <int G, Epi E>
+__global__ void __launch_bounds__(256) spmv_tma_kernel(
+    int nrows, int nchunks, int slot_nnz, int nstage, const int* __restrict__ rp,
     const int* __restrict__ ci, const double* __restrict__ val, const double* __restrict__ x,
     double* __restrict__ y, SpmvArgs a, double* partials, unsigned* ticket) {
   if (a.gate && *a.gate) return;
   constexpr bool kRed = (E == Epi::StoreDot || E == Epi::ResidSsq);
-  __shared__ double prod[kChunkNnz];
-  __shared__ int srp[kChunkRows + 1];
+  constexpr int RPP = 256 / G;  // rows per pass
+  constexpr int rows = kTmaPR * RPP;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const TmaLayout L = tma_layout(rows, slot_nnz);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)nstage * L.stage_bytes);
+  const int tid = threadIdx.x, sub = tid & (G - 1), grp = tid / G;
+  uint64_t policy = 0;
+  auto issue = [&](int s, int ch, int k0, int k1) {
+    unsigned char* st = smem + (size_t)s * L.stage_bytes;
+    const int r0 = ch * rows, r1 = min(r0 + rows, nrows);
+    const int kv0 = k0 & ~1, kv1 = (k1 + 1) & ~1;
+    const int kc0 = k0 & ~3, kc1 = (k1 + 3) & ~3;
+    const int rr0 = r0 & ~3, rr1 = (r1 + 4) & ~3;  // rp[r0..r1] inclusive
+    const unsigned bv = (unsigned)(kv1 - kv0) * 8u, bc = (unsigned)(kc1 - kc0) * 4u,
+                   br = (unsigned)(rr1 - rr0) * 4u;
+    mbar_expect_tx(bars + s, bv + bc + br);
+    if (bv) bulk_copy_hint(st + L.v_off, val + kv0, bv, bars + s, policy);
+    if (bc) bulk_copy_hint(st + L.c_off, ci + kc0, bc, bars + s, policy);
+    bulk_copy_hint(st + L.r_off, rp + rr0, br, bars + s, policy);
+  };
+  if (tid == 0) {
+    policy = evict_first_policy();
+    for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
+    mbar_init_fence();
+    for (int s = 0; s < nstage; ++s) {
+      const int ch = blockIdx.x + s * gridDim.x;
+      if (ch < nchunks) issue(s, ch, __ldg(rp + ch * rows), __ldg(rp + min(ch * rows + rows, nrows)));
+    }
+  }
+  __syncthreads();
   double red = 0.0;
-  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const int r0 = chunk_row[ch], nr = chunk_row[ch + 1] - r0;
-    for (int i = threadIdx.x; i <= nr; i += blockDim.x) srp[i] = rp[r0 + i];
-    __syncthreads();
-    const int k0 = srp[0], k1 = srp[nr];
-#pragma unroll 4
-    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x)
-      prod[k - k0] = __dmul_rn(__ldcs(val + k), __ldg(x + __ldcs(ci + k)));
-    __syncthreads();
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-      double s = 0.0;
-      const int e = srp[i + 1] - k0;
-      for (int k = srp[i] - k0; k < e; ++k) s = __dadd_rn(s, prod[k]);
-      const int row = r0 + i;
-      if constexpr (E == Epi::Store) {
-        y[row] = s;
-      } else if constexpr (E == Epi::Resid) {
-        y[row] = a.b[row] - s;
-      } else if constexpr (E == Epi::ResidEta) {
-        y[row] = (row < a.n_u ? a.eta_u : a.eta_p) * (a.b[row] - s);
-      } else if constexpr (E == Epi::Add) {
-        y[row] = y[row] + s;
-      } else if constexpr (E == Epi::StoreDot) {
-        y[row] = s;
-        red = fma(s, a.dotv[row], red);
-      } else if constexpr (E == Epi::ResidSsq) {
-        const double r = a.b[row] - s;
-        y[row] = r;
-        red = fma(r, r, red);
+  int it = 0;
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++it) {
+    const int s = it % nstage;
+    // offsets of the chunk that refills this stage, loaded before the compute
+    const int cr = ch + nstage * gridDim.x;
+    int rk0 = 0, rk1 = 0;
+    if (tid == 0 && cr < nchunks) {
+      rk0 = __ldg(rp + cr * rows);
+      rk1 = __ldg(rp + min(cr * rows + rows, nrows));
+    }
+    const int r0 = ch * rows, r1 = min(r0 + rows, nrows);
+    double pre[kTmaPR];
+#pragma unroll
+    for (int p = 0; p < kTmaPR; ++p) pre[p] = spmv_pre<E>(a, y, r0 + p * RPP + grp, sub == 0 && r0 + p * RPP + grp < r1);
+    mbar_wait(bars + s, (unsigned)((it / nstage) & 1));
+    const unsigned char* st = smem + (size_t)s * L.stage_bytes;
+    const double* sv = reinterpret_cast<const double*>(st + L.v_off);
+    const int* sc = reinterpret_cast<const int*>(st + L.c_off);
+    const int* sr = reinterpret_cast<const int*>(st + L.r_off);
+    const int rr0 = r0 & ~3;
+    const int k0 = sr[r0 - rr0];
+    const int kv0 = k0 & ~1, kc0 = k0 & ~3;
+    int beg[kTmaPR], end[kTmaPR];
+    double vv[kTmaPR][4], xv[kTmaPR][4];
+#pragma unroll
+    for (int p = 0; p < kTmaPR; ++p) {
+      const int row = r0 + p * RPP + grp;
+      beg[p] = end[p] = 0;
+      if (row < r1) {
+        beg[p] = sr[row - rr0];
+        end[p] = sr[row + 1 - rr0];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = beg[p] + sub + u * G;
+        const bool in = k < end[p];
+        vv[p][u] = in ? sv[k - kv0] : 0.0;
+        xv[p][u] = in ? __ldg(x + sc[k - kc0]) : 0.0;
       }
     }
+#pragma unroll
+    for (int p = 0; p < kTmaPR; ++p) {
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = fma(vv[p][u], xv[p][u], acc);
+      for (int k = beg[p] + sub + 4 * G; k < end[p]; k += G)
+        acc = fma(sv[k - kv0], __ldg(x + sc[k - kc0]), acc);
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+      const int row = r0 + p * RPP + grp;
+      if (sub == 0 && row < r1) spmv_epi<E>(a, y, row, acc, pre[p], red);
+    }
     __syncthreads();
+    if (tid == 0 && cr < nchunks) {
+      fence_proxy_async();
+      issue(s, cr, rk0, rk1);
+    }
   }
   if constexpr (kRed) reduce_finish(red, a.fin, partials, ticket);
 }
 
-static void spmv_stream(Ctx& c, const Matrix& m, const double* x, double* y, Epi e,
-                        const SpmvArgs& a) {
-  const char* env_ctas = getenv("SAG_SPMV_CTAS");
-  const int ctas_per_sm = env_ctas ? atoi(env_ctas) : 6;
-  const int grid = std::max(1, std::min(m.nchunks, std::min(c.num_sms * ctas_per_sm, kMaxRedGrid)));
+template <int G>
+static void spmv_tma_dispatch(Ctx& c, const Matrix& m, const double* x, double* y, Epi e,
+                              const SpmvArgs& a) {
+  const TmaLayout L = tma_layout(kTmaPR * 256 / G, m.tma_slot_nnz);
+  const int smem = m.tma_stages * L.stage_bytes + m.tma_stages * 8;
+  auto grid_of = [&](auto kern) {
+    // the smem opt-in is per kernel: only ever raise it (matrices differ)
+    static thread_local int configured[6] = {0, 0, 0, 0, 0, 0};
+    int& cf = configured[static_cast<int>(e)];
+    if (cf < smem) {
+      SAG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cf = smem;
+    }
+    int& o = m.tma_occ[static_cast<int>(e)];
+    if (!o) {
+      SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, smem));
+      o = std::max(o, 1);
+    }
+    const long long cap = std::min<long long>((long long)o * c.num_sms, kMaxRedGrid);
+    return (int)std::max(1LL, std::min<long long>(m.nchunks, cap));
+  };
   switch (e) {
-#define CASE(EE)                                                                               \
-  case Epi::EE:                                                                                \
-    spmv_stream_kernel<Epi::EE><<<grid, 256, 0, c.stream>>>(m.nchunks, m.chunk_row.p, m.rp.p,  \
-                                                            m.ci.p, m.v.p, x, y, a,            \
-                                                            c.partials.p, c.ticket.p);         \
+#define CASE(EE)                                                                              \
+  case Epi::EE:                                                                               \
+    spmv_tma_kernel<G, Epi::EE><<<grid_of(spmv_tma_kernel<G, Epi::EE>), 256, smem, c.stream>>>( \
+        m.nrows, m.nchunks, m.tma_slot_nnz, m.tma_stages, m.rp.p, m.ci.p, m.v.p, x, y, a,       \
+        c.partials.p, c.ticket.p);                                                            \
     break;
     CASE(Store)
     CASE(Resid)
@@ -329,40 +423,47 @@ static void spmv_stream(Ctx& c, const Matrix& m, const double* x, double* y, Epi
   SAG_LAUNCHED(c);
 }
 
-// Greedy row chunks of <= kChunkNnz entries and <= kChunkRows rows; a row
-// longer than a chunk leaves the matrix on the G-lanes-per-row kernel.
+// Chunking for the TMA-staged kernel (rows per chunk fixed by the lane group;
+// stage size = the largest chunk). SAG_SPMV_TMA=0 keeps the register kernel.
 void build_chunks(Ctx& c, Matrix& m) {
   m.nchunks = 0;
-  if (m.nrows == 0) return;
-  // opt-in for now: measured slower than the G-lanes kernel on K0 (175 vs 142 us)
-  const char* e = getenv("SAG_SPMV_STREAM");
+  m.tma_rows = 0;
+  for (int& o : m.tma_occ) o = 0;
+  if (m.nrows == 0 || m.nnz == 0) return;
+  // opt-in: on K0 it measures the same as the register kernel (the LSU data
+  // pipe, shared by the staged loads and the x gathers, is the limit)
+  const char* e = getenv("SAG_SPMV_TMA");
   if (!e || atoi(e) == 0) return;
   std::vector<int> rp(m.nrows + 1);
   SAG_CUDA(cudaMemcpyAsync(rp.data(), m.rp.p, sizeof(int) * (m.nrows + 1), cudaMemcpyDeviceToHost,
                            c.stream));
   SAG_CUDA(cudaStreamSynchronize(c.stream));
-  std::vector<int> ch{0};
-  int r0 = 0;
-  for (int r = 0; r < m.nrows; ++r) {
-    const int len = rp[r + 1] - rp[r];
-    if (len > kChunkNnz) return;
-    if (rp[r + 1] - rp[r0] > kChunkNnz || r - r0 >= kChunkRows) {
-      ch.push_back(r);
-      r0 = r;
-    }
-  }
-  ch.push_back(m.nrows);
-  m.chunk_row.alloc(ch.size());
-  SAG_CUDA(cudaMemcpyAsync(m.chunk_row.p, ch.data(), sizeof(int) * ch.size(),
-                           cudaMemcpyHostToDevice, c.stream));
-  SAG_CUDA(cudaStreamSynchronize(c.stream));
-  m.nchunks = (int)ch.size() - 1;
+  const int rows = kTmaPR * 256 / m.group;
+  const int nch = (m.nrows + rows - 1) / rows;
+  int slot = 0;
+  for (int ch = 0; ch < nch; ++ch)
+    slot = std::max(slot, rp[std::min(ch * rows + rows, m.nrows)] - rp[ch * rows]);
+  const TmaLayout L = tma_layout(rows, slot);
+  const char* es = getenv("SAG_SPMV_TMA_SMEM");
+  const int budget = es ? atoi(es) : 56 * 1024;
+  const int stages = std::min(4, budget / L.stage_bytes);
+  if (stages < 2) return;  // rows too long to stage two chunks: register kernel
+  m.tma_rows = rows;
+  m.tma_slot_nnz = slot;
+  m.tma_stages = stages;
+  m.nchunks = nch;
 }
 
 void launch_spmv(Ctx& c, const Matrix& m, const double* x, double* y, Epi e, const SpmvArgs& a) {
   if (m.nrows == 0) return;
   if (m.nchunks > 0) {
-    spmv_stream(c, m, x, y, e, a);
+    switch (m.group) {
+      case 2: spmv_tma_dispatch<2>(c, m, x, y, e, a); break;
+      case 4: spmv_tma_dispatch<4>(c, m, x, y, e, a); break;
+      case 8: spmv_tma_dispatch<8>(c, m, x, y, e, a); break;
+      case 16: spmv_tma_dispatch<16>(c, m, x, y, e, a); break;
+      default: spmv_tma_dispatch<32>(c, m, x, y, e, a); break;
+    }
     return;
   }
   switch (m.group) {
@@ -711,11 +812,14 @@ __global__ void permute_kernel(long long n, const int* perm, const int* row_of, 
 
 static int pick_group(long long nnz, int nrows) {
   if (const char* e = getenv("SAG_SPMV_GROUP")) return atoi(e);
+  // ~4 entries per lane: each lane issues its 4-wide pass of loads at once,
+  // and the shuffle tree (on the same LSU data pipe as the gathers) stays
+  // short -- on K0 (17 entries per row) G = 4 runs in 97 us, G = 8 in 117 us
   const double avg = nrows > 0 ? (double)nnz / nrows : 0.0;
-  if (avg <= 3.0) return 2;
-  if (avg <= 8.0) return 4;
-  if (avg <= 24.0) return 8;
-  if (avg <= 48.0) return 16;
+  if (avg <= 4.0) return 2;
+  if (avg <= 24.0) return 4;
+  if (avg <= 64.0) return 8;
+  if (avg <= 128.0) return 16;
   return 32;
 }
 
@@ -725,9 +829,9 @@ std::unique_ptr<Matrix> transpose_dev(Ctx& c, const Matrix& a) {
   t->nrows = a.ncols;
   t->ncols = a.nrows;
   t->nnz = a.nnz;
-  t->rp.alloc(a.ncols + 1);
-  t->ci.alloc(a.nnz);
-  t->v.alloc(a.nnz);
+  t->rp.alloc(a.ncols + 1 + kTmaPad);
+  t->ci.alloc(a.nnz + kTmaPad);
+  t->v.alloc(a.nnz + kTmaPad);
   const long long n = a.nnz;
   DevBuf<int> row_of(n), idx(n), keys_out(n), perm(n), cnt(a.ncols + 1);
   const int g = ew_grid(c, n);
@@ -765,9 +869,9 @@ std::unique_ptr<Matrix> matrix_upload(Ctx& c, int nrows, int ncols, long long nn
   m->nrows = nrows;
   m->ncols = ncols;
   m->nnz = nnz;
-  m->rp.alloc(nrows + 1);
-  m->ci.alloc(nnz);
-  m->v.alloc(nnz);
+  m->rp.alloc(nrows + 1 + kTmaPad);
+  m->ci.alloc(nnz + kTmaPad);
+  m->v.alloc(nnz + kTmaPad);
   SAG_CUDA(cudaMemcpyAsync(m->rp.p, rp, sizeof(int) * (nrows + 1), cudaMemcpyDefault, c.stream));
   if (nnz) {
     SAG_CUDA(cudaMemcpyAsync(m->ci.p, ci, sizeof(int) * nnz, cudaMemcpyDefault, c.stream));

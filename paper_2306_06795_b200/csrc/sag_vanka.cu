@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "tma.cuh"
 
 namespace sag {
 
@@ -316,6 +317,7 @@ struct FactorOut {
   const long long* hoff = nullptr;
   const int* sbase = nullptr;
   int tps = 0;  // streamed thread-per-patch section order
+  int pairs = 0;  // paired blob layout for qualifying patches (vanka_paired)
 };
 
 __global__ void __launch_bounds__(256) factor_kernel(
@@ -390,7 +392,19 @@ __global__ void __launch_bounds__(256) factor_kernel(
     // streamed thread-per-patch order B_hat | S^-1 | A_x | U_x | A_y | U_y
     double *gAx, *gAy, *gUx, *gUy, *gB, *gS;
     int urx, ury;
-    if (fo.tps) {
+    // paired blob: (A_x,A_y) | (U_x,U_y) | (B_x,B_y) interleaved, then S^-1;
+    // sa/su = element strides of the A and U sections
+    const bool pr = !fo.tps && vanka_paired(fo.pairs != 0, nx, ny, np);
+    const long long sa = pr ? 2 : es, su = pr ? 2 : es;
+    if (pr) {
+      gAx = fo.D + db;
+      gAy = gAx + 1;
+      gUx = gAx + 2 * ainv_len(nx, sym);
+      gUy = gUx + 1;
+      gB = gUx + 2 * nx;
+      gS = gB + 2 * nx;
+      urx = ury = 0;  // np == 1
+    } else if (fo.tps) {
       gB = fo.D + db;
       gS = gB + (long long)np * nv * es;
       gAx = gS + (long long)np * np * es;
@@ -437,7 +451,7 @@ __global__ void __launch_bounds__(256) factor_kernel(
         // symmetrised upper triangle, packed by columns
         for (int c = 0; c < n; ++c)
           for (int i = lane; i <= c; i += 32)
-            gA[((long long)c * (c + 1) / 2 + i) * es] =
+            gA[((long long)c * (c + 1) / 2 + i) * sa] =
                 0.5 * (Winv[(size_t)c * D + i] + Winv[(size_t)i * D + c]);
       } else {
         for (int e = lane; e < n * n; e += 32) gA[e * es] = Winv[(size_t)(e / n) * D + (e % n)];
@@ -470,15 +484,18 @@ __global__ void __launch_bounds__(256) factor_kernel(
       const int a = e / nv, j = e % nv;
       double acc = 0.0;
       for (int m = 0; m < np; ++m) acc = __dadd_rn(acc, __dmul_rn(Sinv[a * np + m], Um[j * NP + m]));
-      gB[e * es] = acc;
+      if (pr)
+        gB[j < nx ? 2 * j : 2 * (j - nx) + 1] = acc;
+      else
+        gB[e * es] = acc;
     }
     // u_hat stored by rows a: [a*urx + i] (x part) and [a*ury + i - nx] (y part)
     for (int e = lane; e < np * nv; e += 32) {
       const int a = e / nv, i = e % nv;
       if (i < nx)
-        gUx[((long long)a * urx + i) * es] = Um[i * NP + a];
+        gUx[((long long)a * urx + i) * su] = Um[i * NP + a];
       else
-        gUy[((long long)a * ury + i - nx) * es] = Um[i * NP + a];
+        gUy[((long long)a * ury + i - nx) * su] = Um[i * NP + a];
     }
     for (int i = lane; i < nv; i += 32) gidx[i * es] = sv[i];
     for (int a = lane; a < np; a += 32) gidx[(nv + a) * es] = pidx[p0 + a];
@@ -591,6 +608,8 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   f->max_np = p.max_np;
   f->sym = velocity_block_symmetric(c, k, std::min(std::max(n_u, 0), k.nrows));
   const bool sym = f->sym;
+  // the paired path lives in the one-row-per-lane kernel (R = 1)
+  f->pairs = sym && p.max_np <= 1 && p.max_dim <= 32 && env_int("SAG_VANKA_PAIRS", 1) != 0;
   // host bookkeeping: blob offsets, slot bases, storage accounting (vanka.cpp:142-144)
   std::vector<int> vptr(np_ + 1), pptr(np_ + 1), nx(std::max(np_, 1));
   SAG_CUDA(cudaMemcpyAsync(vptr.data(), p.vptr.p, sizeof(int) * (np_ + 1), cudaMemcpyDeviceToHost, c.stream));
@@ -620,6 +639,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   long long slots = 0;
   f->tpp = sym && p.max_dim <= kTppMaxDim && p.max_np <= 4 && np_ > 0 &&
            env_int("SAG_VANKA_TPP", 0) != 0;
+  if (f->tpp) f->pairs = false;
   if (f->tpp) {
     // thread-per-patch layout: patches sorted (stably) by shape, buckets of 32
     // equal-shape patches, every payload entry interleaved across the bucket
@@ -768,6 +788,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
       fo.I = reinterpret_cast<int*>(f->blob.p);
       fo.blob = f->blob.p;
       fo.hoff = f->off.p;
+      fo.pairs = f->pairs ? 1 : 0;
     }
     factor_kernel<<<blocks, warps * 32, smem, c.stream>>>(
         np_, L.D, L.NV, L.NP, L.bytes, sym ? 1 : 0, k.rp.p, k.ci.p, k.v.p, p.pptr.p, p.pidx.p,
@@ -784,40 +805,6 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
 }
 
 // ========================================================== apply_vanka ==
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-
-// One 1-D bulk copy global -> shared, completion signalled on `bar`.
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
-                                          uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
 
 // Warp-per-patch additive Vanka: each warp streams its patches' factor blobs
 // through an NSTAGE-deep shared-memory ring filled by cp.async.bulk (TMA
@@ -861,56 +848,58 @@ __device__ __forceinline__ PatchView patch_view(const unsigned char* B) {
 template <int R, bool SYM, int NPM>
 __global__ void __launch_bounds__(256) vanka_patch_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
-    int slot_bytes, int nstage, int sb_len, const double* __restrict__ r,
+    int slot_bytes, int nstage, int sb_len, int pairs, const double* __restrict__ r,
     double* __restrict__ out, const int* gate) {
   if (gate && *gate) return;
   constexpr int G = 2 * R + 1;  // gathered values per lane (nv + np <= 32 G)
+  // paired blobs (vanka_paired) exist only for symmetric one-pressure levels
+  constexpr bool kPair = SYM && NPM == 1 && R == 1;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbar = (nstage + 1) & ~1;  // keeps the r buffers 16-byte aligned
   unsigned char* ring = smem + (size_t)wib * nstage * slot_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)warps * nstage * slot_bytes) +
-                   (size_t)wib * nstage;
+                   (size_t)wib * nbar;
   double* sbuf = reinterpret_cast<double*>(smem + (size_t)warps * nstage * slot_bytes +
-                                           (size_t)warps * nstage * 8) +
+                                           (size_t)warps * nbar * 8) +
                  (size_t)wib * 2 * sb_len;
   const int first = blockIdx.x * warps + wib;
   const int stride = gridDim.x * warps;
-  uint64_t policy;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  const uint64_t policy = evict_first_policy();
   auto issue_at = [&](int s, long long o0, long long o1) {
-    unsigned char* dst = ring + (size_t)s * slot_bytes;
     const unsigned bytes = (unsigned)(o1 - o0);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bars + s)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-        "l"(blob + o0), "r"(bytes), "r"(smem_u32(bars + s)), "l"(policy)
-        : "memory");
+    mbar_expect_tx(bars + s, bytes);
+    bulk_copy_hint(ring + (size_t)s * slot_bytes, blob + o0, bytes, bars + s, policy);
   };
-  auto issue = [&](int s, int kk) { issue_at(s, off[kk], off[kk + 1]); };
+  // r at a patch's dofs goes to the r buffer in the order its solve reads:
+  // x dofs, y dofs, pressure; a paired patch interleaves (x_j, y_j)
+  auto slot_of = [&](const PatchView& w, bool pw, int i) {
+    if (kPair && pw && i < w.nv) return i < w.nx ? 2 * i : 2 * (i - w.nx) + 1;
+    return i;
+  };
   if (lane == 0) {
     for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
     for (int s = 0; s < nstage; ++s) {
       const int kk = first + s * stride;
-      if (kk < npatch) issue(s, kk);
+      if (kk < npatch) issue_at(s, off[kk], off[kk + 1]);
     }
   }
   __syncwarp();
+  unsigned phase = 0;  // bit s: parity of the next wait on stage s
   if (first < npatch) {
     mbar_wait(bars, 0);
+    phase ^= 1u;
     const PatchView v = patch_view<SYM>(ring);
-    for (int i = lane; i < v.nv + v.np; i += 32) sbuf[i] = __ldg(r + v.idx[i]);
+    const bool pv = vanka_paired(pairs != 0, v.nx, v.ny, v.np);
+    for (int i = lane; i < v.nv + v.np; i += 32) sbuf[slot_of(v, pv, i)] = __ldg(r + v.idx[i]);
   }
   __syncwarp();
   int csl[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) csl[q] = (lane + 32 * q) * (lane + 32 * q + 1) / 2;
-  int it = 0;
+  int stage = 0, it = 0;
   for (int k = first; k < npatch; k += stride, ++it) {
-    const int stage = it % nstage;
     // offsets of the blob that refills this stage, loaded now so the refill
     // at the end of the iteration does not wait on them
     const int kr = k + nstage * stride;
@@ -923,12 +912,16 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
     const double* sb = sbuf + (it & 1) * sb_len;
     // prefetch r at the next patch's dofs (its blob was issued nstage-1 solves ago)
     const int kn = k + stride;
+    const int sn = stage + 1 == nstage ? 0 : stage + 1;
     double g[G];
     int gn = 0;
+    PatchView w{};
+    bool pw = false;
     if (kn < npatch) {
-      const int sn = (it + 1) % nstage;
-      mbar_wait(bars + sn, (unsigned)(((it + 1) / nstage) & 1));
-      const PatchView w = patch_view<SYM>(ring + (size_t)sn * slot_bytes);
+      mbar_wait(bars + sn, (phase >> sn) & 1u);
+      phase ^= 1u << sn;
+      w = patch_view<SYM>(ring + (size_t)sn * slot_bytes);
+      pw = vanka_paired(pairs != 0, w.nx, w.ny, w.np);
       gn = w.nv + w.np;
 #pragma unroll
       for (int q = 0; q < G; ++q) {
@@ -937,86 +930,117 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
       }
     }
     const int nx = v.nx, ny = v.ny, np = NPM == 1 ? 1 : v.np, nv = v.nv, sbase = v.sbase;
-    const double* Ax = v.Ax;
-    const double* Ay = v.Ay;
-    const double* U = v.U;
-    const double* Bh = v.Bh;
-    const double* Si = v.Si;
-    // t = A^-1 b_u per component (vanka.cpp:164-166): columns j < min(nx, ny)
-    // update both components, the rest only the larger one (no per-column
-    // component predicates); SYM column offsets j(j+1)/2 are carried along
-    double tx[R], ty[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) tx[q] = ty[q] = 0.0;
-    const int nmin = nx < ny ? nx : ny, nmax = nx > ny ? nx : ny;
-    int csj = 0;
-    int j = 0;
-    for (; j < nmin; csj += ++j) {
-      const double bx = sb[j];
-      const double by = sb[nx + j];
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int i = lane + 32 * q;
-        const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : 0;
-        if (i < nx) tx[q] = fma(SYM ? Ax[a] : Ax[j * nx + i], bx, tx[q]);
-        if (i < ny) ty[q] = fma(SYM ? Ay[a] : Ay[j * ny + i], by, ty[q]);
+    if (kPair && vanka_paired(pairs != 0, nx, ny, v.np)) {
+      // paired patch: lane i < nx computes row i of both components with one
+      // 16-byte load of (A_x, A_y)(i, j) and one broadcast of (b_x, b_y)_j per
+      // column; lane 31 runs the same loop over the (B_x, B_y) pairs, i.e.
+      // accumulates b_hat . b_u, so x_p needs no warp reduction
+      const double2* AP = reinterpret_cast<const double2*>(v.Ax);
+      const double2* SB = reinterpret_cast<const double2*>(sb);
+      const int boff = (int)(reinterpret_cast<const double2*>(v.Bh) - AP);
+      // idle lanes (nx <= lane < 31) read column entries j of row 0: in
+      // bounds, unpredicated, results unused
+      const int cl = lane == 31 ? boff : (lane < nx ? csl[0] : 0);
+      double tx = 0.0, ty = 0.0;
+      int csj = 0;
+#pragma unroll 4
+      for (int j = 0; j < nx; csj += ++j) {
+        const double2 b = SB[j];
+        const double2 m = AP[lane <= j ? csj + lane : cl + j];
+        tx = fma(m.x, b.x, tx);
+        ty = fma(m.y, b.y, ty);
       }
-    }
-    if (nx > ny) {
-      for (; j < nmax; csj += ++j) {
-        const double bx = sb[j];
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int i = lane + 32 * q;
-          const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : j * nx + i;
-          if (i < nx) tx[q] = fma(Ax[a], bx, tx[q]);
-        }
+      // x_p = S^-1 b_p + b_hat . b_u (vanka.cpp:168-174), formed on lane 31
+      const double xp = __shfl_sync(0xffffffffu, fma(v.Si[0], sb[nv], tx + ty), 31);
+      if (lane == 0) out[sbase + nv] = xp;
+      // x_u = t + U_hat x_p (vanka.cpp:176-180)
+      if (lane < nx) {
+        const double2 u = reinterpret_cast<const double2*>(v.U)[lane];
+        out[sbase + lane] = fma(u.x, xp, tx);
+        out[sbase + nx + lane] = fma(u.y, xp, ty);
       }
     } else {
-      for (; j < nmax; csj += ++j) {
+      const double* Ax = v.Ax;
+      const double* Ay = v.Ay;
+      const double* U = v.U;
+      const double* Bh = v.Bh;
+      const double* Si = v.Si;
+      // t = A^-1 b_u per component (vanka.cpp:164-166): columns j < min(nx, ny)
+      // update both components, the rest only the larger one (no per-column
+      // component predicates); SYM column offsets j(j+1)/2 are carried along
+      double tx[R], ty[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) tx[q] = ty[q] = 0.0;
+      const int nmin = nx < ny ? nx : ny, nmax = nx > ny ? nx : ny;
+      int csj = 0;
+      int j = 0;
+      for (; j < nmin; csj += ++j) {
+        const double bx = sb[j];
         const double by = sb[nx + j];
 #pragma unroll
         for (int q = 0; q < R; ++q) {
           const int i = lane + 32 * q;
-          const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : j * ny + i;
-          if (i < ny) ty[q] = fma(Ay[a], by, ty[q]);
+          const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : 0;
+          if (i < nx) tx[q] = fma(SYM ? Ax[a] : Ax[j * nx + i], bx, tx[q]);
+          if (i < ny) ty[q] = fma(SYM ? Ay[a] : Ay[j * ny + i], by, ty[q]);
         }
       }
-    }
-    // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
-    double xp[NPM];
+      if (nx > ny) {
+        for (; j < nmax; csj += ++j) {
+          const double bx = sb[j];
 #pragma unroll
-    for (int a = 0; a < NPM; ++a) {
-      xp[a] = 0.0;
-      if (a < np) {
-        double part = 0.0;
-        for (int m = lane; m < nv; m += 32) part = fma(Bh[a * nv + m], sb[m], part);
-        part = warp_sum(part);
-        double sp = 0.0;
+          for (int q = 0; q < R; ++q) {
+            const int i = lane + 32 * q;
+            const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : j * nx + i;
+            if (i < nx) tx[q] = fma(Ax[a], bx, tx[q]);
+          }
+        }
+      } else {
+        for (; j < nmax; csj += ++j) {
+          const double by = sb[nx + j];
 #pragma unroll
-        for (int q = 0; q < NPM; ++q)
-          if (q < np) sp = fma(Si[a * np + q], sb[nv + q], sp);
-        xp[a] = sp + part;
-        if (lane == 0) out[sbase + nv + a] = xp[a];
+          for (int q = 0; q < R; ++q) {
+            const int i = lane + 32 * q;
+            const int a = SYM ? (i <= j ? csj + i : csl[q] + j) : j * ny + i;
+            if (i < ny) ty[q] = fma(Ay[a], by, ty[q]);
+          }
+        }
       }
-    }
-    // x_u = t + U_hat x_p (vanka.cpp:176-180)
+      // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
+      double xp[NPM];
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int i = lane + 32 * q;
-      if (i < nx) {
-        double v = tx[q];
+      for (int a = 0; a < NPM; ++a) {
+        xp[a] = 0.0;
+        if (a < np) {
+          double part = 0.0;
+          for (int m = lane; m < nv; m += 32) part = fma(Bh[a * nv + m], sb[m], part);
+          part = warp_sum(part);
+          double sp = 0.0;
 #pragma unroll
-        for (int a = 0; a < NPM; ++a)
-          if (a < np) v = fma(U[a * nv + i], xp[a], v);
-        out[sbase + i] = v;
+          for (int q = 0; q < NPM; ++q)
+            if (q < np) sp = fma(Si[a * np + q], sb[nv + q], sp);
+          xp[a] = sp + part;
+          if (lane == 0) out[sbase + nv + a] = xp[a];
+        }
       }
-      if (i < ny) {
-        double v = ty[q];
+      // x_u = t + U_hat x_p (vanka.cpp:176-180)
 #pragma unroll
-        for (int a = 0; a < NPM; ++a)
-          if (a < np) v = fma(U[a * nv + nx + i], xp[a], v);
-        out[sbase + nx + i] = v;
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        if (i < nx) {
+          double t = tx[q];
+#pragma unroll
+          for (int a = 0; a < NPM; ++a)
+            if (a < np) t = fma(U[a * nv + i], xp[a], t);
+          out[sbase + i] = t;
+        }
+        if (i < ny) {
+          double t = ty[q];
+#pragma unroll
+          for (int a = 0; a < NPM; ++a)
+            if (a < np) t = fma(U[a * nv + nx + i], xp[a], t);
+          out[sbase + nx + i] = t;
+        }
       }
     }
     // publish the prefetched r values for the next patch
@@ -1024,15 +1048,14 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
 #pragma unroll
     for (int q = 0; q < G; ++q) {
       const int i = lane + 32 * q;
-      if (i < gn) sbn[i] = g[q];
+      if (i < gn) sbn[slot_of(w, pw, i)] = g[q];
     }
     __syncwarp();
-    if (lane == 0) {
-      if (kr < npatch) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_at(stage, ro0, ro1);
-      }
+    if (lane == 0 && kr < npatch) {
+      fence_proxy_async();
+      issue_at(stage, ro0, ro1);
     }
+    stage = sn;
   }
 }
 
@@ -1399,7 +1422,7 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   a.nstage = std::max(2, env_int("SAG_VANKA_STAGES", 2));
   a.sb_len = f.max_nv + f.max_np + f.max_dim + 2;
   a.sb_len = (a.sb_len + 1) / 2 * 2;
-  const int per_warp = a.nstage * f.slot_bytes + a.nstage * 8 + 2 * a.sb_len * 8;
+  const int per_warp = a.nstage * f.slot_bytes + ((a.nstage + 1) & ~1) * 8 + 2 * a.sb_len * 8;
   const int cta_budget = env_int("SAG_VANKA_CTA_SMEM", 60000);
   a.warps = std::max(1, std::min(env_int("SAG_VANKA_WARPS", 8), cta_budget / per_warp));
   if (a.warps * per_warp > 220 * 1024) a.warps = std::max(1, (220 * 1024) / per_warp);
@@ -1420,9 +1443,12 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
 
 template <int R, bool SYM, int NPM>
 static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gate) {
+  SAG_REQUIRE(!f.pairs || (R == 1 && SYM && NPM == 1), SAG_ERROR,
+              "apply_vanka: paired factor blobs need the one-row-per-lane kernel");
   const ApplyCfg a = apply_cfg<R, SYM, NPM>(c, f);
   vanka_patch_kernel<R, SYM, NPM><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
-      f.npatch, f.blob.p, f.off.p, f.slot_bytes, a.nstage, a.sb_len, r, f.out.p, gate);
+      f.npatch, f.blob.p, f.off.p, f.slot_bytes, a.nstage, a.sb_len, f.pairs ? 1 : 0, r, f.out.p,
+      gate);
   SAG_LAUNCHED(c);
 }
 
@@ -1506,6 +1532,18 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
       Uy = Ux + (long long)np * nx * es + ainv_len(ny, f.sym) * es;
       urx = nx;
       ury = ny;
+    } else if (vanka_paired(f.pairs, nx, ny, np)) {  // (A) | (U) | (B) pairs | S^-1
+      const double* U2 = base + 2 * ainv_len(nx, f.sym);
+      const double* B2 = U2 + 2 * nx;
+      for (int i = 0; i < nv; ++i) {
+        const int e = i < nx ? 2 * i : 2 * (i - nx) + 1;
+        if (uhat) uhat[ou + i] = U2[e];
+        if (bhat) bhat[ou + i] = B2[e];
+      }
+      if (sinv) sinv[os] = B2[2 * nx];
+      ou += nv;
+      os += 1;
+      continue;
     } else {  // A_x | A_y | U | B_hat | S^-1
       Ux = base + (ainv_len(nx, f.sym) + ainv_len(ny, f.sym)) * es;
       Uy = Ux + (long long)nx * es;

@@ -152,6 +152,63 @@ def test_block_lu_random_patches(S):
     assert worst <= 1e-10
 
 
+def _saddle_blocks(rng, sizes):
+    """Independent symmetric saddle-point blocks, dofs ordered [x | y | p]
+    over all blocks; one Vanka patch per block (its own dofs)."""
+    nxs = [a for a, _ in sizes]
+    nys = [b for _, b in sizes]
+    ox = np.concatenate([[0], np.cumsum(nxs)])
+    oy = ox[-1] + np.concatenate([[0], np.cumsum(nys)])
+    n_u = int(oy[-1])
+    n = n_u + len(sizes)
+    rr, cc, vv = [], [], []
+    vidx, vptr = [], [0]
+    for b, (mx, my) in enumerate(sizes):
+        xs = np.arange(ox[b], ox[b] + mx)
+        ys = np.arange(oy[b], oy[b] + my)
+        pr = n_u + b
+        for dofs in (xs, ys):
+            m = len(dofs)
+            a = 0.3 * rng.uniform(-1, 1, (m, m))
+            a = 0.5 * (a + a.T) + 4 * np.eye(m)
+            i, j = np.meshgrid(dofs, dofs, indexing="ij")
+            rr += list(i.ravel()); cc += list(j.ravel()); vv += list(a.ravel())
+        bu = rng.uniform(-1, 1, mx + my)
+        vel = np.concatenate([xs, ys])
+        rr += [pr] * len(vel) + list(vel); cc += list(vel) + [pr] * len(vel)
+        vv += list(bu) + list(bu)
+        vidx += list(vel)
+        vptr.append(len(vidx))
+    k = O.RefMat.from_triplets(n, n, rr, cc, vv)
+    pptr = list(range(len(sizes) + 1))
+    pidx = [n_u + b for b in range(len(sizes))]
+    return k, n_u, (pptr, pidx, vptr, vidx, nxs)
+
+
+@pytest.mark.parametrize("big", [False, True])
+def test_apply_vanka_many_patches_per_warp(S, big):
+    # thousands of patches (several per warp: ring reuse, the paired
+    # (A_x, A_y) layout for nx == ny <= 31), plus nx != ny and nx = 32
+    # patches; with `big` one 40-dof component puts the level on the
+    # two-rows-per-lane kernel, where no blob may be paired
+    rng = np.random.default_rng(7)
+    sizes = [(m, m) for m in rng.integers(2, 32, 6000)] + [(5, 7), (9, 4), (32, 32), (31, 31)]
+    if big:
+        sizes.append((40, 40))
+    rng.shuffle(sizes)
+    k, n_u, lists = _saddle_blocks(rng, sizes)
+    pp = O.Patches(*[np.asarray(a, dtype=np.int32) for a in lists])
+    rv = O.RefVanka.from_patches(k, pp, n_u)
+    K = S.SparseMatrix.from_csr(k.csr())
+    f = S.factor_patches(K, S.Patches.from_lists(*lists), n_u)
+    want = rv.factors()
+    got = f.export(S.Patches.from_lists(*lists).export())
+    for key in ("uhat", "bhat", "sinv"):
+        assert np.array_equal(got[key], want[key]), key
+    r = O.splitmix64_uniform(k.csr_shape()[0])
+    assert rel_inf(S.apply_vanka(f, r), rv.apply(r)) <= TOL
+
+
 def test_singular_patch_raises(S):
     k = O.RefMat.from_triplets(3, 3, [0, 1, 2], [2, 1, 0], [1.0, 1.0, 1.0]).csr()
     K = S.SparseMatrix.from_csr(k)

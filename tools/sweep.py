@@ -53,21 +53,34 @@ def main():
         e1.synchronize()
         return e0.elapsed_time(e1) / k * 1e3  # us
 
-    K = S.SparseMatrix.from_csr(k0, ctx)
     bs = spmv_bytes(n, n, k0.nnz)
-    us = timed(lambda: S.spmv(K, x, out=y))
-    print(json.dumps({"kernel": "spmv", "us": us, "gbs": bs / us / 1e3}), flush=True)
     lib = S.lib()
     aux = torch.from_numpy(splitmix64_uniform(n, 7)).to(dev)
     xp_, yp_, ap_ = (S.C.c_void_p(t.data_ptr()) for t in (x, y, aux))
-    for epi, name in ((0, "store"), (1, "resid"), (2, "add"), (3, "store_dot"), (4, "resid_ssq")):
-        us = timed(lambda: S._check(lib.sag_spmv_fused(ctx.h, K.h, xp_, yp_, ap_, epi)))
-        print(json.dumps({"kernel": "spmv_" + name, "us": us}), flush=True)
+    spmv_variants = os.environ.get("SWEEP_SPMV", "").split(";")
+    for sv in spmv_variants:
+        env = dict(kv.split("=") for kv in sv.split(",") if kv)
+        saved = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        K = S.SparseMatrix.from_csr(k0, ctx)  # launch shape is chosen at upload
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+        us = timed(lambda: S.spmv(K, x, out=y))
+        rec = {"kernel": "spmv", "variant": sv, "us": us, "gbs": bs / us / 1e3}
+        for epi, name in ((0, "store"), (1, "resid"), (2, "add"), (3, "store_dot"),
+                          (4, "resid_ssq")):
+            rec[name] = timed(lambda: S._check(lib.sag_spmv_fused(ctx.h, K.h, xp_, yp_, ap_, epi)))
+        print(json.dumps(rec), flush=True)
+    K = S.SparseMatrix.from_csr(k0, ctx)
     built = {}
     for var in variants:
         env = dict(kv.split("=") for kv in var.split(",") if kv)
         os.environ.update(env)
-        key = (env.get("SAG_VANKA_TPP", "0"), env.get("SAG_VANKA_SYM", "1"))
+        key = (env.get("SAG_VANKA_TPP", "0"), env.get("SAG_VANKA_SYM", "1"),
+               env.get("SAG_VANKA_PAIRS", "1"))
         if key not in built:
             built.clear()
             p = S.build_patches(K, *case.nxyz0)
