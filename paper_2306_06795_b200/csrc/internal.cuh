@@ -85,9 +85,10 @@ struct Vanka {
   long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
   long long blob_bytes = 0;
   bool sym = false;  // A^-1 blocks stored as packed symmetrised upper triangles
-  // paired blobs: patches with nx == ny <= 31 and one pressure seed store
-  // (A_x, A_y), (U_x, U_y), (B_x, B_y) interleaved element by element so the
-  // apply loads both components with one 16-byte shared-memory access
+  // paired blobs: patches with one pressure seed and max(nx, ny) = m <= 31
+  // store (A_x, A_y), (U_x, U_y), (B_x, B_y) interleaved element by element,
+  // the smaller component zero-padded to m, so the apply loads both
+  // components with one 16-byte shared-memory access
   bool pairs = false;
   // thread-per-patch layout (tpp): shape buckets of 32 patches, entries
   // interleaved across the bucket (D: doubles, I: dof indices)
@@ -107,7 +108,11 @@ struct Vanka {
 // host scalars of krylov.cpp:17-121.
 // Per-patch rule for the paired blob layout (factor, apply and export agree).
 __host__ __device__ inline bool vanka_paired(bool pairs, int nx, int ny, int np) {
-  return pairs && nx == ny && np == 1 && nx <= 31;
+  return pairs && np == 1 && nx <= 31 && ny <= 31;
+}
+// doubles of a paired blob of padded size m: A pairs | U pairs | B pairs | S
+__host__ __device__ inline long long vanka_paired_doubles(int m) {
+  return (long long)m * (m + 1) + 4LL * m + 1;
 }
 
 struct KState {

@@ -397,13 +397,18 @@ __global__ void __launch_bounds__(256) factor_kernel(
     const bool pr = !fo.tps && vanka_paired(fo.pairs != 0, nx, ny, np);
     const long long sa = pr ? 2 : es, su = pr ? 2 : es;
     if (pr) {
+      const int m = nx > ny ? nx : ny;
       gAx = fo.D + db;
       gAy = gAx + 1;
-      gUx = gAx + 2 * ainv_len(nx, sym);
+      gUx = gAx + 2 * ainv_len(m, true);
       gUy = gUx + 1;
-      gB = gUx + 2 * nx;
-      gS = gB + 2 * nx;
+      gB = gUx + 2 * m;
+      gS = gB + 2 * m;
       urx = ury = 0;  // np == 1
+      // zero padding of the smaller component
+      if (nx != ny)
+        for (long long e = lane; e < vanka_paired_doubles(m) - 1; e += 32) gAx[e] = 0.0;
+      __syncwarp();
     } else if (fo.tps) {
       gB = fo.D + db;
       gS = gB + (long long)np * nv * es;
@@ -631,6 +636,8 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   }
   auto ndbl = [&](int i) {
     const long long nv = f->h_nv[i], npp = f->h_np[i], x = f->h_nx[i], y = nv - x;
+    if (!f->tpp && vanka_paired(f->pairs, (int)x, (int)y, (int)npp))
+      return vanka_paired_doubles((int)std::max(x, y));
     return ainv_len(x, sym) + ainv_len(y, sym) + 2 * nv * npp + npp * npp;
   };
   f->h_dbase.assign(np_, 0);
@@ -812,13 +819,26 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
 // (t = A^-1 b_u; x_p = S^-1 b_p + B_hat b_u; x_u = t + U_hat x_p,
 // vanka.cpp:161-181) and writes the unweighted local result to its slots.
 // Blob pointers of one patch (layout in internal.cuh).
+// Predicated 16-byte shared load (no branch; 0 when !pred).
+__device__ __forceinline__ double2 lds_v2_pred(const double2* p, bool pred) {
+  double2 v = make_double2(0.0, 0.0);
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.b32 q, %3, 0;\n@q ld.shared.v2.f64 {%0, %1}, [%2];\n}\n"
+      : "+d"(v.x), "+d"(v.y)
+      : "r"(smem_u32(p)), "r"((int)pred));
+  return v;
+}
+
+// Paired blobs (vanka_paired): m = max(nx, ny); Ax points at the (A_x, A_y)
+// pairs, U / Bh at the (U_x, U_y) / (B_x, B_y) pairs, Ay is unused.
 struct PatchView {
-  int nx, ny, np, sbase, nv;
+  int nx, ny, np, sbase, nv, m;
+  bool paired;
   const double *Ax, *Ay, *U, *Bh, *Si;
   const int* idx;
 };
 template <bool SYM>
-__device__ __forceinline__ PatchView patch_view(const unsigned char* B) {
+__device__ __forceinline__ PatchView patch_view(const unsigned char* B, bool pairs) {
   PatchView v;
   const int4 hdr = *reinterpret_cast<const int4*>(B);
   v.nx = hdr.x;
@@ -826,7 +846,17 @@ __device__ __forceinline__ PatchView patch_view(const unsigned char* B) {
   v.np = hdr.z;
   v.sbase = hdr.w;
   v.nv = v.nx + v.ny;
+  v.m = v.nx > v.ny ? v.nx : v.ny;
+  v.paired = SYM && vanka_paired(pairs, v.nx, v.ny, v.np);
   v.Ax = reinterpret_cast<const double*>(B + 16);
+  if (v.paired) {
+    v.Ay = v.Ax + 1;
+    v.U = v.Ax + v.m * (v.m + 1);
+    v.Bh = v.U + 2 * v.m;
+    v.Si = v.Bh + 2 * v.m;
+    v.idx = reinterpret_cast<const int*>(v.Si + 1);
+    return v;
+  }
   v.Ay = v.Ax + (SYM ? v.nx * (v.nx + 1) / 2 : v.nx * v.nx);
   v.U = v.Ay + (SYM ? v.ny * (v.ny + 1) / 2 : v.ny * v.ny);
   v.Bh = v.U + v.np * v.nv;
@@ -872,10 +902,18 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
     bulk_copy_hint(ring + (size_t)s * slot_bytes, blob + o0, bytes, bars + s, policy);
   };
   // r at a patch's dofs goes to the r buffer in the order its solve reads:
-  // x dofs, y dofs, pressure; a paired patch interleaves (x_j, y_j)
-  auto slot_of = [&](const PatchView& w, bool pw, int i) {
-    if (kPair && pw && i < w.nv) return i < w.nx ? 2 * i : 2 * (i - w.nx) + 1;
+  // x dofs, y dofs, pressure; a paired patch interleaves (x_j, y_j) over
+  // j < m (padding zeroed by pad_pairs) with the pressure at 2m
+  auto slot_of = [&](const PatchView& w, int i) {
+    if (kPair && w.paired)
+      return i < w.nx ? 2 * i : (i < w.nv ? 2 * (i - w.nx) + 1 : 2 * w.m + (i - w.nv));
     return i;
+  };
+  auto pad_pairs = [&](const PatchView& w, double* dst) {
+    if (kPair && w.paired && w.nx != w.ny) {
+      if (lane >= w.nx && lane < w.m) dst[2 * lane] = 0.0;
+      if (lane >= w.ny && lane < w.m) dst[2 * lane + 1] = 0.0;
+    }
   };
   if (lane == 0) {
     for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
@@ -890,9 +928,9 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
   if (first < npatch) {
     mbar_wait(bars, 0);
     phase ^= 1u;
-    const PatchView v = patch_view<SYM>(ring);
-    const bool pv = vanka_paired(pairs != 0, v.nx, v.ny, v.np);
-    for (int i = lane; i < v.nv + v.np; i += 32) sbuf[slot_of(v, pv, i)] = __ldg(r + v.idx[i]);
+    const PatchView v = patch_view<SYM>(ring, pairs != 0);
+    for (int i = lane; i < v.nv + v.np; i += 32) sbuf[slot_of(v, i)] = __ldg(r + v.idx[i]);
+    pad_pairs(v, sbuf);
   }
   __syncwarp();
   int csl[R];
@@ -908,7 +946,7 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
       ro0 = __ldg(off + kr);
       ro1 = __ldg(off + kr + 1);
     }
-    const PatchView v = patch_view<SYM>(ring + (size_t)stage * slot_bytes);
+    const PatchView v = patch_view<SYM>(ring + (size_t)stage * slot_bytes, pairs != 0);
     const double* sb = sbuf + (it & 1) * sb_len;
     // prefetch r at the next patch's dofs (its blob was issued nstage-1 solves ago)
     const int kn = k + stride;
@@ -916,12 +954,10 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
     double g[G];
     int gn = 0;
     PatchView w{};
-    bool pw = false;
     if (kn < npatch) {
       mbar_wait(bars + sn, (phase >> sn) & 1u);
       phase ^= 1u << sn;
-      w = patch_view<SYM>(ring + (size_t)sn * slot_bytes);
-      pw = vanka_paired(pairs != 0, w.nx, w.ny, w.np);
+      w = patch_view<SYM>(ring + (size_t)sn * slot_bytes, pairs != 0);
       gn = w.nv + w.np;
 #pragma unroll
       for (int q = 0; q < G; ++q) {
@@ -930,34 +966,38 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
       }
     }
     const int nx = v.nx, ny = v.ny, np = NPM == 1 ? 1 : v.np, nv = v.nv, sbase = v.sbase;
-    if (kPair && vanka_paired(pairs != 0, nx, ny, v.np)) {
-      // paired patch: lane i < nx computes row i of both components with one
+    if (kPair && v.paired) {
+      // paired patch: lane i < m computes row i of both components with one
       // 16-byte load of (A_x, A_y)(i, j) and one broadcast of (b_x, b_y)_j per
-      // column; lane 31 runs the same loop over the (B_x, B_y) pairs, i.e.
-      // accumulates b_hat . b_u, so x_p needs no warp reduction
+      // column (zero padding beyond nx / ny); lane 31 runs the same loop over
+      // the (B_x, B_y) pairs, i.e. accumulates b_hat . b_u, so x_p needs no
+      // warp reduction
+      const int mm = v.m;
       const double2* AP = reinterpret_cast<const double2*>(v.Ax);
       const double2* SB = reinterpret_cast<const double2*>(sb);
       const int boff = (int)(reinterpret_cast<const double2*>(v.Bh) - AP);
-      // idle lanes (nx <= lane < 31) read column entries j of row 0: in
-      // bounds, unpredicated, results unused
-      const int cl = lane == 31 ? boff : (lane < nx ? csl[0] : 0);
+      // lanes 0..m-1: rows; lane m: the b_hat row; lanes above m issue no
+      // load, so a column costs ceil((m + 1) / 8) shared-memory wavefronts
+      // (the LSU data pipe is this kernel's limit), not four
+      const bool act = lane <= mm;
+      const int cl = lane == mm ? boff : csl[0];
       double tx = 0.0, ty = 0.0;
       int csj = 0;
 #pragma unroll 4
-      for (int j = 0; j < nx; csj += ++j) {
+      for (int j = 0; j < mm; csj += ++j) {
         const double2 b = SB[j];
-        const double2 m = AP[lane <= j ? csj + lane : cl + j];
-        tx = fma(m.x, b.x, tx);
-        ty = fma(m.y, b.y, ty);
+        const double2 a = lds_v2_pred(AP + (lane <= j ? csj + lane : cl + j), act);
+        tx = fma(a.x, b.x, tx);
+        ty = fma(a.y, b.y, ty);
       }
-      // x_p = S^-1 b_p + b_hat . b_u (vanka.cpp:168-174), formed on lane 31
-      const double xp = __shfl_sync(0xffffffffu, fma(v.Si[0], sb[nv], tx + ty), 31);
+      // x_p = S^-1 b_p + b_hat . b_u (vanka.cpp:168-174), formed on lane m
+      const double xp = __shfl_sync(0xffffffffu, fma(v.Si[0], sb[2 * mm], tx + ty), mm);
       if (lane == 0) out[sbase + nv] = xp;
       // x_u = t + U_hat x_p (vanka.cpp:176-180)
-      if (lane < nx) {
+      if (lane < mm) {
         const double2 u = reinterpret_cast<const double2*>(v.U)[lane];
-        out[sbase + lane] = fma(u.x, xp, tx);
-        out[sbase + nx + lane] = fma(u.y, xp, ty);
+        if (lane < nx) out[sbase + lane] = fma(u.x, xp, tx);
+        if (lane < ny) out[sbase + nx + lane] = fma(u.y, xp, ty);
       }
     } else {
       const double* Ax = v.Ax;
@@ -1048,8 +1088,9 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
 #pragma unroll
     for (int q = 0; q < G; ++q) {
       const int i = lane + 32 * q;
-      if (i < gn) sbn[slot_of(w, pw, i)] = g[q];
+      if (i < gn) sbn[slot_of(w, i)] = g[q];
     }
+    pad_pairs(w, sbn);
     __syncwarp();
     if (lane == 0 && kr < npatch) {
       fence_proxy_async();
@@ -1533,14 +1574,15 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
       urx = nx;
       ury = ny;
     } else if (vanka_paired(f.pairs, nx, ny, np)) {  // (A) | (U) | (B) pairs | S^-1
-      const double* U2 = base + 2 * ainv_len(nx, f.sym);
-      const double* B2 = U2 + 2 * nx;
+      const int m = std::max(nx, ny);
+      const double* U2 = base + 2 * ainv_len(m, true);
+      const double* B2 = U2 + 2 * m;
       for (int i = 0; i < nv; ++i) {
         const int e = i < nx ? 2 * i : 2 * (i - nx) + 1;
         if (uhat) uhat[ou + i] = U2[e];
         if (bhat) bhat[ou + i] = B2[e];
       }
-      if (sinv) sinv[os] = B2[2 * nx];
+      if (sinv) sinv[os] = B2[2 * m];
       ou += nv;
       os += 1;
       continue;
