@@ -12,9 +12,15 @@ by all ranks (GDOF/s). Inputs (K0 0.48 GB + Vanka factors 1.4 GB) exceed the
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
   python bench.py --impl reference      # the reference's CPU path, host cores
 
-Multi-GPU (torchrun): every rank runs an independent replica of the config on
-its own GPU (weak scaling; the row-partitioned halo path is future work, see
-DESIGN.md). Times are CUDA events on libsag's stream, max over ranks.
+Multi-GPU (torchrun, N > 1): K0's rows and Vanka patches are partitioned
+across the ranks (paper_2306_06795_b200.dist) with NCCL halo exchanges (strong
+scaling). Times are CUDA events on libsag's stream, max over ranks.
+
+roofline: the dominant kernel is the Vanka patch kernel; its algorithmic bytes
+are those of the representation it streams (factor blobs incl. dof indices,
+r once, the local results), `traffic` is ncu's DRAM bytes per launch from the
+committed profile (profiles/*/ncu_traffic.json). The SURVEY 8(d) formula
+bytes of the whole sweep (reference representation) are reported beside it.
 """
 from __future__ import annotations
 
@@ -136,6 +142,26 @@ def spmv_bytes(nrows, ncols, nnz):
 def vanka_bytes(f, tot_idx, n):
     # factors (a_factor + aux) + patch index lists + 24 n
     return f.a_factor_bytes + f.aux_bytes + 4 * tot_idx + 24 * n
+
+
+def vanka_patch_bytes(f, n):
+    # the patch kernel's own stream: blobs (factors, headers, dof indices),
+    # r (each entry once), one local result per slot
+    return f.device_bytes + 8 * n + 8 * f.nslots
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu capture
+    (profiles/<round>/ncu_traffic.json), or None."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json"))):
+        try:
+            with open(path) as fh:
+                best = json.load(fh).get(kernel, best)
+        except Exception:
+            pass
+    return best
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -399,6 +425,7 @@ def run_ours(args, ws, rank, local):
 
     peak, peak_kind = peak_hbm()
     b_v = vanka_bytes(f, tot_idx, n)
+    b_p = vanka_patch_bytes(f, n)
     b_s = spmv_bytes(n, n, k0.nnz)
     ms_step = 1e3 * t_steps / args.steps
     value = ws * n / (t_steps / args.steps) / 1e9
@@ -411,17 +438,21 @@ def run_ours(args, ws, rank, local):
                    "patches": f.npatch, "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
                    "l2": "inputs (K0 + factors ~1.9 GB) exceed L2; no flush"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "vanka sweep (patch + gather)",
-                     "achieved": b_v / t_vanka / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": b_v / t_vanka / 1e9 / peak, "traffic": None,
-                     "algorithmic_bytes": b_v, "peak_kind": peak_kind},
+        "roofline": {"bound": "hbm", "kernel": "vanka_patch_kernel (K0)",
+                     "achieved": b_p / t_patch / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": b_p / t_patch / 1e9 / peak, "traffic": ncu_traffic("vanka_patch"),
+                     "algorithmic_bytes": b_p, "peak_kind": peak_kind,
+                     "bytes_def": "factor blobs + 8 n (r) + 8 slots (local results)"},
         "kernels": {
             "vanka_sweep_us": 1e6 * t_vanka, "vanka_patch_us": 1e6 * t_patch,
             "vanka_gather_us": 1e6 * t_gather, "spmv_us": 1e6 * t_spmv,
             "vanka_gdofs": n / t_vanka / 1e9, "spmv_gdofs": n / t_spmv / 1e9,
-            "spmv_bytes": b_s, "spmv_gbs": b_s / t_spmv / 1e9,
-            "spmv_frac": b_s / t_spmv / 1e9 / peak,
+            "vanka_sweep_formula_bytes": b_v,
+            "vanka_sweep_formula_gbs": b_v / t_vanka / 1e9,
             "vanka_device_bytes": f.device_bytes,
+            "spmv_bytes": b_s, "spmv_gbs": b_s / t_spmv / 1e9,
+            "spmv_frac": b_s / t_spmv / 1e9 / peak, "spmv_traffic": ncu_traffic("spmv"),
+            "vanka_gather_traffic": ncu_traffic("vanka_gather"),
         },
         "e2e": {"value": ws * n / t_e2e / 1e9, "unit": "GDOF/s",
                 "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 2 * 8 * n},
