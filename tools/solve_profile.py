@@ -77,6 +77,10 @@ def main():
         tab = kernel_table(lambda: dc.apply(r, out=z), steps=3)
         out["dc_apply_kernels_us"] = [(k, c, round(t, 1)) for k, c, t in tab]
         os.environ.pop("SAG_NO_GRAPH")
+    if "--solve-table" in sys.argv:
+        tab = kernel_table(lambda: S.solve_stokes(K0, rhs, dc, cfg), steps=1)
+        out["solve_kernels_us"] = [(k, c, round(t, 1)) for k, c, t in tab[:30]]
+        out["solve_kernel_sum_us"] = round(sum(t for _, _, t in tab), 1)
     print(json.dumps(out))
 
 
