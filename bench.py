@@ -43,7 +43,41 @@ CONFIGS = {
     2: dict(workload="th_cavity_512x512", problem="cavity", sv=False, n=512),
     3: dict(workload="sv_cavity_256x256_barycentric", problem="cavity", sv=True, n=256,
             omega0=0.78, eta_p=2.68),
+    # jittered Delaunay of a 501x501 grid (251,001 points, jitter 0.3 h, seed 7),
+    # zero velocity, f = (sin k1 x, cos k2 y) with k from splitmix64
+    4: dict(workload="th_unstructured_251k_forced", problem="cavity", sv=False, n=500,
+            mesh="file_forced"),
 }
+
+
+def _mesh_file(cfg):
+    from paper_2306_06795_b200 import meshgen
+    path = os.path.join("/tmp", f"sag_mesh_{cfg['n']}_7_0.3.json")
+    if not os.path.exists(path):
+        meshgen.write_mesh(path + f".{os.getpid()}", cfg["n"], seed=7, jitter=0.3)
+        os.replace(path + f".{os.getpid()}", path)
+    return path
+
+
+def host_case(cfg):
+    """The reference-built case of a config (host adapter)."""
+    from paper_2306_06795_b200.cases import HostCase
+    if cfg.get("mesh") == "file_forced":
+        from paper_2306_06795_b200 import meshgen
+        k1, k2 = meshgen.force_wavenumbers()
+        return HostCase(cfg["problem"], False, "file_forced", 0, mesh_path=_mesh_file(cfg),
+                        k1=k1, k2=k2)
+    return HostCase(cfg["problem"], cfg["sv"], "structured", cfg["n"])
+
+
+def ref_case(cfg):
+    """The same case built by the reference library in oracle/_ref."""
+    import oracle as O
+    if cfg.get("mesh") == "file_forced":
+        from paper_2306_06795_b200 import meshgen
+        k1, k2 = meshgen.force_wavenumbers()
+        return O.RefCase.mesh_forced(_mesh_file(cfg), k1, k2)
+    return O.RefCase.build(cfg["problem"], cfg["sv"], "structured", cfg["n"])
 METRIC = "Vanka sweep + SpMV GDOF/s (frac. of HBM roofline); FGMRES solve s vs CPU"
 
 
@@ -201,7 +235,7 @@ def run_reference(args, ws, rank):
     import oracle as O
     cfg = CONFIGS[args.config]
     t0 = time.perf_counter()
-    case = O.RefCase.build(cfg["problem"], cfg["sv"], "structured", cfg["n"])
+    case = ref_case(cfg)
     k0 = case.k0().csr()
     setup_s = time.perf_counter() - t0
     threads = os.cpu_count() or 1
@@ -235,7 +269,6 @@ def run_dist(args, ws, rank, local):
     import torch.distributed as dist
 
     import paper_2306_06795_b200 as S
-    from paper_2306_06795_b200.cases import HostCase
     from paper_2306_06795_b200.dist import DistStep, build_partition
 
     cfg = CONFIGS[args.config]
@@ -246,7 +279,7 @@ def run_dist(args, ws, rank, local):
         os.environ.setdefault("MASTER_PORT", "29561")
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     t0 = time.perf_counter()
-    case = HostCase(cfg["problem"], cfg["sv"], "structured", cfg["n"])
+    case = host_case(cfg)
     k0 = case.k0()
     host_setup_s = time.perf_counter() - t0
     ctx = S.Context(local)
@@ -347,13 +380,12 @@ def run_ours(args, ws, rank, local):
     import torch
 
     import paper_2306_06795_b200 as S
-    from paper_2306_06795_b200.cases import HostCase
 
     cfg = CONFIGS[args.config]
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     t0 = time.perf_counter()
-    case = HostCase(cfg["problem"], cfg["sv"], "structured", cfg["n"])
+    case = host_case(cfg)
     k0 = case.k0()
     host_setup_s = time.perf_counter() - t0
     ctx = S.Context(local)
