@@ -39,6 +39,7 @@ enum sag_status {
   SAG_SINGULAR_PATCH = 4,      /* stokesamg::SingularPatch                  */
   SAG_CONFIG_ERROR = 5,        /* stokesamg::ConfigError                    */
   SAG_SOLVER_STAGNATION = 6,   /* stokesamg::SolverStagnation               */
+  SAG_ZERO_DIAGONAL = 7,       /* stokesamg::ZeroDiagonal (sparse.cpp:211)  */
   SAG_CUDA_ERROR = 100,        /* device / driver failure (no reference analogue) */
   SAG_INVALID_ARGUMENT = 101   /* null handle / pointer                     */
 };

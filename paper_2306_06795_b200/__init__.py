@@ -39,7 +39,7 @@ LIB_PATH = os.path.join(HERE, "libsag.so")
 
 __all__ = [
     "Error", "DimensionMismatch", "SingularMatrix", "SingularPatch", "ConfigError",
-    "SolverStagnation", "CudaError", "Context", "SparseMatrix", "Patches",
+    "SolverStagnation", "ZeroDiagonal", "CudaError", "Context", "SparseMatrix", "Patches",
     "VankaFactorization", "spmv", "norm2", "dot", "build_patches", "factor_patches",
     "apply_vanka", "vanka_relax", "RelaxMode", "FgmresOptions", "KrylovReport", "fgmres",
     "SolverConfig", "Variant", "DCPreconditioner", "solve_stokes", "default_context", "lib",
@@ -67,6 +67,10 @@ class ConfigError(Error):
     pass
 
 
+class ZeroDiagonal(Error):
+    pass
+
+
 class SolverStagnation(Error):
     pass
 
@@ -76,7 +80,7 @@ class CudaError(Error):
 
 
 _ERRORS = {1: Error, 2: DimensionMismatch, 3: SingularMatrix, 4: SingularPatch,
-           5: ConfigError, 6: SolverStagnation, 100: CudaError, 101: Error}
+           5: ConfigError, 6: SolverStagnation, 7: ZeroDiagonal, 100: CudaError, 101: Error}
 
 i32p = C.POINTER(C.c_int)
 f64p = C.POINTER(C.c_double)

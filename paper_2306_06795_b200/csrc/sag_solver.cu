@@ -904,7 +904,7 @@ int sag_fgmres(sag_ctx* ctx, const sag_matrix* a, const double* b, double* x, in
         int hb = 0;
         SAG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         SAG_CUDA(cudaStreamSynchronize(c.stream));
-        SAG_REQUIRE(!hb, SAG_ERROR, "inv_diagonal: zero diagonal");
+        SAG_REQUIRE(!hb, SAG_ZERO_DIAGONAL, "inv_diagonal: zero diagonal");
         op = [&](const double* in, double* out) { launch_mul(c, n, dinv.p, in, out); };
         break;
       }
@@ -1015,7 +1015,7 @@ int sag_dc_set_sv_transfer(sag_dc* h, const sag_matrix* p_dup, const sag_matrix*
         int hb = 0;
         SAG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
         SAG_CUDA(cudaStreamSynchronize(c.stream));
-        SAG_REQUIRE(!hb, SAG_ERROR, "inv_diagonal: zero diagonal in the Mcg hierarchy");
+        SAG_REQUIRE(!hb, SAG_ZERO_DIAGONAL, "inv_diagonal: zero diagonal in the Mcg hierarchy");
       }
     }
     t->coarse.setup(c, *t->A.back(), -1, 0.0);

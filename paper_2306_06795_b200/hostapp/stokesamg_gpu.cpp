@@ -22,6 +22,7 @@ void check(int s) {
     case SAG_SINGULAR_PATCH: throw SingularPatch(msg);
     case SAG_CONFIG_ERROR: throw ConfigError(msg);
     case SAG_SOLVER_STAGNATION: throw SolverStagnation(msg);
+    case SAG_ZERO_DIAGONAL: throw ZeroDiagonal(msg);
     default: throw Error(msg);
   }
 }
