@@ -85,11 +85,13 @@ struct Vanka {
   long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
   long long blob_bytes = 0;
   bool sym = false;  // A^-1 blocks stored as packed symmetrised upper triangles
-  // paired blobs: patches with one pressure seed and max(nx, ny) = m <= 31
-  // store (A_x, A_y), (U_x, U_y), (B_x, B_y) interleaved element by element,
-  // the smaller component zero-padded to m, so the apply loads both
-  // components with one 16-byte shared-memory access
+  // paired blobs (every patch of a level, or none): np <= 4 pressure seeds
+  // and m + np <= 64 (m = max(nx, ny)); pair_rows = max(m + np) sets the
+  // kernel's rows per lane. They store (A_x, A_y), (U_x, U_y), (B_x, B_y) interleaved
+  // element by element, the smaller component zero-padded to m, so the apply
+  // loads both components with one 16-byte shared-memory access
   bool pairs = false;
+  int pair_rows = 0;
   // thread-per-patch layout (tpp): shape buckets of 32 patches, entries
   // interleaved across the bucket (D: doubles, I: dof indices)
   bool tpp = false;
@@ -107,12 +109,15 @@ struct Vanka {
 // Krylov scalar state in device memory (one per FGMRES instance); mirrors the
 // host scalars of krylov.cpp:17-121.
 // Per-patch rule for the paired blob layout (factor, apply and export agree).
+// m rows + np b_hat rows, one or two per lane (the R <= 2 kernels)
 __host__ __device__ inline bool vanka_paired(bool pairs, int nx, int ny, int np) {
-  return pairs && np == 1 && nx <= 31 && ny <= 31;
+  const int m = nx > ny ? nx : ny;
+  return pairs && np >= 1 && np <= 4 && m + np <= 64;
 }
-// doubles of a paired blob of padded size m: A pairs | U pairs | B pairs | S
-__host__ __device__ inline long long vanka_paired_doubles(int m) {
-  return (long long)m * (m + 1) + 4LL * m + 1;
+// doubles of a paired blob of padded size m with np pressure seeds:
+// A pairs (m x m packed) | U pairs [a][i] | B pairs [a][j] | S^-1 (np x np)
+__host__ __device__ inline long long vanka_paired_doubles(int m, int np) {
+  return (long long)m * (m + 1) + 4LL * np * m + (long long)np * np;
 }
 
 struct KState {

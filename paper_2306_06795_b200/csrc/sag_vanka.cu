@@ -402,12 +402,13 @@ __global__ void __launch_bounds__(256) factor_kernel(
       gAy = gAx + 1;
       gUx = gAx + 2 * ainv_len(m, true);
       gUy = gUx + 1;
-      gB = gUx + 2 * m;
-      gS = gB + 2 * m;
-      urx = ury = 0;  // np == 1
+      gB = gUx + 2LL * np * m;
+      gS = gB + 2LL * np * m;
+      urx = ury = m;  // pair rows of U: [a * m + i]
       // zero padding of the smaller component
       if (nx != ny)
-        for (long long e = lane; e < vanka_paired_doubles(m) - 1; e += 32) gAx[e] = 0.0;
+        for (long long e = lane; e < vanka_paired_doubles(m, np) - (long long)np * np; e += 32)
+          gAx[e] = 0.0;
       __syncwarp();
     } else if (fo.tps) {
       gB = fo.D + db;
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(256) factor_kernel(
       double acc = 0.0;
       for (int m = 0; m < np; ++m) acc = __dadd_rn(acc, __dmul_rn(Sinv[a * np + m], Um[j * NP + m]));
       if (pr)
-        gB[j < nx ? 2 * j : 2 * (j - nx) + 1] = acc;
+        gB[2LL * a * (nx > ny ? nx : ny) + (j < nx ? 2 * j : 2 * (j - nx) + 1)] = acc;
       else
         gB[e * es] = acc;
     }
@@ -614,7 +615,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   f->sym = velocity_block_symmetric(c, k, std::min(std::max(n_u, 0), k.nrows));
   const bool sym = f->sym;
   // the paired path lives in the one-row-per-lane kernel (R = 1)
-  f->pairs = sym && p.max_np <= 1 && p.max_dim <= 32 && env_int("SAG_VANKA_PAIRS", 1) != 0;
+  f->pairs = sym && p.max_np <= 4 && env_int("SAG_VANKA_PAIRS", 1) != 0;
   // host bookkeeping: blob offsets, slot bases, storage accounting (vanka.cpp:142-144)
   std::vector<int> vptr(np_ + 1), pptr(np_ + 1), nx(std::max(np_, 1));
   SAG_CUDA(cudaMemcpyAsync(vptr.data(), p.vptr.p, sizeof(int) * (np_ + 1), cudaMemcpyDeviceToHost, c.stream));
@@ -637,7 +638,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   auto ndbl = [&](int i) {
     const long long nv = f->h_nv[i], npp = f->h_np[i], x = f->h_nx[i], y = nv - x;
     if (!f->tpp && vanka_paired(f->pairs, (int)x, (int)y, (int)npp))
-      return vanka_paired_doubles((int)std::max(x, y));
+      return vanka_paired_doubles((int)std::max(x, y), (int)npp);
     return ainv_len(x, sym) + ainv_len(y, sym) + 2 * nv * npp + npp * npp;
   };
   f->h_dbase.assign(np_, 0);
@@ -647,6 +648,13 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   f->tpp = sym && p.max_dim <= kTppMaxDim && p.max_np <= 4 && np_ > 0 &&
            env_int("SAG_VANKA_TPP", 0) != 0;
   if (f->tpp) f->pairs = false;
+  // a level is paired only if every patch is (one kernel path per level)
+  for (int i = 0; i < np_ && f->pairs; ++i) {
+    const int x = f->h_nx[i], y = f->h_nv[i] - x;
+    f->pairs = vanka_paired(true, x, y, f->h_np[i]);
+    f->pair_rows = std::max(f->pair_rows, std::max(x, y) + f->h_np[i]);
+  }
+  if (!f->pairs) f->pair_rows = 0;
   if (f->tpp) {
     // thread-per-patch layout: patches sorted (stably) by shape, buckets of 32
     // equal-shape patches, every payload entry interleaved across the bucket
@@ -852,9 +860,9 @@ __device__ __forceinline__ PatchView patch_view(const unsigned char* B, bool pai
   if (v.paired) {
     v.Ay = v.Ax + 1;
     v.U = v.Ax + v.m * (v.m + 1);
-    v.Bh = v.U + 2 * v.m;
-    v.Si = v.Bh + 2 * v.m;
-    v.idx = reinterpret_cast<const int*>(v.Si + 1);
+    v.Bh = v.U + 2 * v.np * v.m;
+    v.Si = v.Bh + 2 * v.np * v.m;
+    v.idx = reinterpret_cast<const int*>(v.Si + v.np * v.np);
     return v;
   }
   v.Ay = v.Ax + (SYM ? v.nx * (v.nx + 1) / 2 : v.nx * v.nx);
@@ -882,8 +890,8 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
     double* __restrict__ out, const int* gate) {
   if (gate && *gate) return;
   constexpr int G = 2 * R + 1;  // gathered values per lane (nv + np <= 32 G)
-  // paired blobs (vanka_paired) exist only for symmetric one-pressure levels
-  constexpr bool kPair = SYM && NPM == 1 && R == 1;
+  // paired blobs (vanka_paired) exist only on symmetric levels, R <= 2
+  constexpr bool kPair = SYM && R <= 2;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nbar = (nstage + 1) & ~1;  // keeps the r buffers 16-byte aligned
@@ -911,8 +919,12 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
   };
   auto pad_pairs = [&](const PatchView& w, double* dst) {
     if (kPair && w.paired && w.nx != w.ny) {
-      if (lane >= w.nx && lane < w.m) dst[2 * lane] = 0.0;
-      if (lane >= w.ny && lane < w.m) dst[2 * lane + 1] = 0.0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int j = lane + 32 * q;
+        if (j >= w.nx && j < w.m) dst[2 * j] = 0.0;
+        if (j >= w.ny && j < w.m) dst[2 * j + 1] = 0.0;
+      }
     }
   };
   if (lane == 0) {
@@ -967,37 +979,83 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
     }
     const int nx = v.nx, ny = v.ny, np = NPM == 1 ? 1 : v.np, nv = v.nv, sbase = v.sbase;
     if (kPair && v.paired) {
-      // paired patch: lane i < m computes row i of both components with one
-      // 16-byte load of (A_x, A_y)(i, j) and one broadcast of (b_x, b_y)_j per
-      // column (zero padding beyond nx / ny); lane 31 runs the same loop over
-      // the (B_x, B_y) pairs, i.e. accumulates b_hat . b_u, so x_p needs no
-      // warp reduction
-      const int mm = v.m;
+      // paired patch: virtual row i = lane + 32 q (q < R) is matrix row i
+      // (i < m) of both components -- one 16-byte load of (A_x, A_y)(i, j) and
+      // one broadcast of (b_x, b_y)_j per column, zero padding beyond nx / ny
+      // -- or, for m <= i < m + np, b_hat row i - m over the (B_x, B_y) pairs,
+      // so x_p needs no warp reduction
+      const int mm = v.m, npp = NPM == 1 ? 1 : v.np;
       const double2* AP = reinterpret_cast<const double2*>(v.Ax);
       const double2* SB = reinterpret_cast<const double2*>(sb);
       const int boff = (int)(reinterpret_cast<const double2*>(v.Bh) - AP);
-      // lanes 0..m-1: rows; lane m: the b_hat row; lanes above m issue no
-      // load, so a column costs ceil((m + 1) / 8) shared-memory wavefronts
-      // (the LSU data pipe is this kernel's limit), not four
-      const bool act = lane <= mm;
-      const int cl = lane == mm ? boff : csl[0];
-      double tx = 0.0, ty = 0.0;
+      // rows past m + np issue no load: a column costs ceil((m + np) / 8)
+      // shared-memory wavefronts (the LSU data pipe bounds this kernel)
+      bool act[R];
+      int cl[R];
+      double tx[R], ty[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        act[q] = i < mm + npp;
+        cl[q] = i >= mm ? boff + (i - mm) * mm : csl[q];
+        tx[q] = ty[q] = 0.0;
+      }
       int csj = 0;
 #pragma unroll 4
       for (int j = 0; j < mm; csj += ++j) {
         const double2 b = SB[j];
-        const double2 a = lds_v2_pred(AP + (lane <= j ? csj + lane : cl + j), act);
-        tx = fma(a.x, b.x, tx);
-        ty = fma(a.y, b.y, ty);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int i = lane + 32 * q;
+          const double2 a = lds_v2_pred(AP + (i <= j ? csj + i : cl[q] + j), act[q]);
+          tx[q] = fma(a.x, b.x, tx[q]);
+          ty[q] = fma(a.y, b.y, ty[q]);
+        }
       }
-      // x_p = S^-1 b_p + b_hat . b_u (vanka.cpp:168-174), formed on lane m
-      const double xp = __shfl_sync(0xffffffffu, fma(v.Si[0], sb[2 * mm], tx + ty), mm);
-      if (lane == 0) out[sbase + nv] = xp;
+      // x_p = S^-1 b_p + b_hat . b_u (vanka.cpp:168-174), on virtual row m + a
+      // (every lane evaluates it -- rows clamped into range -- and only the
+      // b_hat rows store: no divergent block)
+      double xl[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        const int ar = min(max(i - mm, 0), npp - 1);
+        xl[q] = tx[q] + ty[q];
+#pragma unroll
+        for (int e = 0; e < NPM; ++e)
+          if (e < npp) xl[q] = fma(v.Si[ar * npp + e], sb[2 * mm + e], xl[q]);
+        if (i >= mm && i < mm + npp) out[sbase + nv + ar] = xl[q];
+      }
+      double xp[NPM];
+#pragma unroll
+      for (int e = 0; e < NPM; ++e) {
+        xp[e] = 0.0;
+        if (e < npp) {
+          const int src = mm + e;  // warp-uniform
+          double sv = xl[0];
+#pragma unroll
+          for (int q = 1; q < R; ++q)
+            if ((src >> 5) == q) sv = xl[q];
+          xp[e] = __shfl_sync(0xffffffffu, sv, src & 31);
+        }
+      }
       // x_u = t + U_hat x_p (vanka.cpp:176-180)
-      if (lane < mm) {
-        const double2 u = reinterpret_cast<const double2*>(v.U)[lane];
-        if (lane < nx) out[sbase + lane] = fma(u.x, xp, tx);
-        if (lane < ny) out[sbase + nx + lane] = fma(u.y, xp, ty);
+      const double2* UP = reinterpret_cast<const double2*>(v.U);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int i = lane + 32 * q;
+        if (i < mm) {
+          double ox = tx[q], oy = ty[q];
+#pragma unroll
+          for (int e = 0; e < NPM; ++e)
+            if (e < npp) {
+              const double2 u = UP[e * mm + i];
+              ox = fma(u.x, xp[e], ox);
+              oy = fma(u.y, xp[e], oy);
+            }
+          if (i < nx) out[sbase + i] = ox;
+          if (i < ny) out[sbase + nx + i] = oy;
+        }
       }
     } else {
       const double* Ax = v.Ax;
@@ -1484,8 +1542,8 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
 
 template <int R, bool SYM, int NPM>
 static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gate) {
-  SAG_REQUIRE(!f.pairs || (R == 1 && SYM && NPM == 1), SAG_ERROR,
-              "apply_vanka: paired factor blobs need the one-row-per-lane kernel");
+  SAG_REQUIRE(!f.pairs || (R <= 2 && SYM), SAG_ERROR,
+              "apply_vanka: paired factor blobs need a symmetric R <= 2 kernel");
   const ApplyCfg a = apply_cfg<R, SYM, NPM>(c, f);
   vanka_patch_kernel<R, SYM, NPM><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
       f.npatch, f.blob.p, f.off.p, f.slot_bytes, a.nstage, a.sb_len, f.pairs ? 1 : 0, r, f.out.p,
@@ -1495,7 +1553,8 @@ static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gat
 
 template <bool SYM, int NPM>
 static void launch_patch_r(Ctx& c, const Vanka& f, const double* r, const int* gate) {
-  const int R = (f.max_dim + 31) / 32;
+  // rows per lane: matrix rows, or (paired levels) matrix + b_hat rows
+  const int R = f.pairs ? (f.pair_rows + 31) / 32 : (f.max_dim + 31) / 32;
   switch (R) {
     case 1: launch_patch<1, SYM, NPM>(c, f, r, gate); break;
     case 2: launch_patch<2, SYM, NPM>(c, f, r, gate); break;
@@ -1576,15 +1635,18 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
     } else if (vanka_paired(f.pairs, nx, ny, np)) {  // (A) | (U) | (B) pairs | S^-1
       const int m = std::max(nx, ny);
       const double* U2 = base + 2 * ainv_len(m, true);
-      const double* B2 = U2 + 2 * m;
-      for (int i = 0; i < nv; ++i) {
-        const int e = i < nx ? 2 * i : 2 * (i - nx) + 1;
-        if (uhat) uhat[ou + i] = U2[e];
-        if (bhat) bhat[ou + i] = B2[e];
-      }
-      if (sinv) sinv[os] = B2[2 * m];
-      ou += nv;
-      os += 1;
+      const double* B2 = U2 + 2LL * np * m;
+      const double* S2 = B2 + 2LL * np * m;
+      for (int i = 0; i < nv; ++i)
+        for (int a = 0; a < np; ++a) {
+          const long long e = 2LL * a * m + (i < nx ? 2 * i : 2 * (i - nx) + 1);
+          if (uhat) uhat[ou + (size_t)i * np + a] = U2[e];
+          if (bhat) bhat[ou + (size_t)a * nv + i] = B2[e];
+        }
+      if (sinv)
+        for (int e = 0; e < np * np; ++e) sinv[os + e] = S2[e];
+      ou += (size_t)nv * np;
+      os += (size_t)np * np;
       continue;
     } else {  // A_x | A_y | U | B_hat | S^-1
       Ux = base + (ainv_len(nx, f.sym) + ainv_len(ny, f.sym)) * es;

@@ -188,9 +188,9 @@ def _saddle_blocks(rng, sizes):
 @pytest.mark.parametrize("big", [False, True])
 def test_apply_vanka_many_patches_per_warp(S, big):
     # thousands of patches (several per warp: ring reuse, the paired
-    # (A_x, A_y) layout for nx == ny <= 31), plus nx != ny and nx = 32
+    # (A_x, A_y) layout, zero-padded when nx != ny), plus m = 31 / 32
     # patches; with `big` one 40-dof component puts the level on the
-    # two-rows-per-lane kernel, where no blob may be paired
+    # two-rows-per-lane paired kernel (m + np <= 64)
     rng = np.random.default_rng(7)
     sizes = [(m, m) for m in rng.integers(2, 32, 6000)] + [(5, 7), (9, 4), (32, 32), (31, 31)]
     if big:

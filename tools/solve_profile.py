@@ -4,7 +4,7 @@ libsag's stream): one DC preconditioner application (CUDA graph), the whole
 solve, per-iteration cost. With --nvtx, a 2-iteration solve runs inside an
 NVTX range "solve2" for `ncu --nvtx --nvtx-include solve2/` launch lists.
 
-    python tools/solve_profile.py [n=512] [--nvtx]
+    python tools/solve_profile.py [n=512] [--config C] [--table] [--solve-table] [--nvtx]
 """
 import json
 import os
@@ -25,11 +25,19 @@ def main():
     n_mesh = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 512
     nvtx = "--nvtx" in sys.argv
     t0 = time.time()
-    case = HostCase("cavity", False, "structured", n_mesh)
+    conf = {}
+    if "--config" in sys.argv:  # a bench.py config instead of the TH cavity n
+        import bench
+        conf = bench.CONFIGS[int(sys.argv[sys.argv.index("--config") + 1])]
+        case = bench.host_case(conf)
+    else:
+        case = HostCase("cavity", False, "structured", n_mesh)
     ctx = S.Context(0)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
-    cfg = S.SolverConfig(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500, enclosed_flow=True)
+    cfg = S.SolverConfig(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
+                         enclosed_flow=case.enclosed, eta_u=conf.get("eta_u", 1.0),
+                         eta_p=conf.get("eta_p", 1.0), omega0=conf.get("omega0", 1.0))
     K0, dc, _ = case.device(cfg, ctx)
     out = {"setup_s": time.time() - t0, "info": dc.info()}
     rhs = case.rhs()
