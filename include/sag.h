@@ -40,6 +40,7 @@ enum sag_status {
   SAG_CONFIG_ERROR = 5,        /* stokesamg::ConfigError                    */
   SAG_SOLVER_STAGNATION = 6,   /* stokesamg::SolverStagnation               */
   SAG_ZERO_DIAGONAL = 7,       /* stokesamg::ZeroDiagonal (sparse.cpp:211)  */
+  SAG_UNSUPPORTED_DISCRETIZATION = 8, /* stokesamg::UnsupportedDiscretization */
   SAG_CUDA_ERROR = 100,        /* device / driver failure (no reference analogue) */
   SAG_INVALID_ARGUMENT = 101   /* null handle / pointer                     */
 };
@@ -158,7 +159,8 @@ enum sag_prec_kind {
   SAG_PREC_IDENTITY = 0, /* identity_operator (krylov.cpp:13-15) */
   SAG_PREC_VANKA = 1,    /* prec = const sag_vanka*: apply_vanka  */
   SAG_PREC_JACOBI = 2,   /* prec = const sag_matrix*: z = D^-1 r (amg.cpp:266-269) */
-  SAG_PREC_DC = 3        /* prec = const sag_dc*: DCPreconditioner::apply */
+  SAG_PREC_DC = 3,       /* prec = const sag_dc*: DCPreconditioner::apply */
+  SAG_PREC_UZAWA = 4     /* prec = const sag_uzawa*: UzawaPreconditioner::apply */
 };
 /* Replaces fgmres(matrix_operator(a), b, x, prec, opt) (krylov.hpp:33-35;
  * krylov.cpp:17-121). x holds the guess on entry. history may be NULL. */
@@ -167,7 +169,9 @@ int sag_fgmres(sag_ctx* ctx, const sag_matrix* a, const double* b, double* x, in
                double* history, int history_cap);
 
 /* ---- preconditioner (preconditioner.hpp:19-148) --------------------------- */
-enum sag_variant { SAG_DC_ALL = 0, SAG_DC_LO = 1, SAG_DC_HO = 2 };
+/* Variant (preconditioner.hpp:14): DC-all / DC-LO / DC-HO and HO-AMG are
+ * sag_dc objects; Uzawa is its own object (sag_uzawa_create). */
+enum sag_variant { SAG_DC_ALL = 0, SAG_DC_LO = 1, SAG_DC_HO = 2, SAG_HOAMG = 3, SAG_UZAWA = 4 };
 
 typedef struct { /* SolverConfig, preconditioner.hpp:19-36 */
   int variant;
@@ -176,6 +180,7 @@ typedef struct { /* SolverConfig, preconditioner.hpp:19-36 */
   double tol;
   int max_iters;
   int enclosed_flow;
+  int allow_sv_hoamg; /* HO-AMG on SV is refused unless set (preconditioner.hpp:31) */
 } sag_solver_config;
 
 /* Fills the reference defaults (preconditioner.hpp:20-33). */
@@ -191,7 +196,11 @@ typedef struct {
   int n_x, n_y, n_p;
 } sag_level_desc;
 
-/* Replaces the DCPreconditioner constructor (preconditioner.cpp:90-105) and
+/* With cfg->variant == SAG_HOAMG this is the HoAmgPreconditioner constructor
+ * (preconditioner.cpp:155-172): `levels` is the monolithic hierarchy built on
+ * the high-order system itself (level 0 == k0), apply = one V-cycle
+ * (preconditioner.cpp:174-176). Otherwise it replaces
+ * the DCPreconditioner constructor (preconditioner.cpp:90-105) and
  * MonolithicSolver's (preconditioner.cpp:40-55): Vanka factors for K0 and every
  * non-coarsest level, R = P^T, coarse dense LU (with the enclosed-flow pin
  * 1e-12 * norm_inf(K of level 0), preconditioner.cpp:49-53), all on device.
@@ -228,6 +237,32 @@ int sag_dc_info(const sag_dc* d, long long* out, int cap);
 int sag_solve_stokes(sag_ctx* ctx, sag_dc* d, const double* rhs, double* x,
                      const sag_solver_config* cfg, sag_krylov_report* rep, double* history,
                      int history_cap);
+
+/* ---- inexact Uzawa (preconditioner.hpp:118-141) ----------------------------- */
+typedef struct sag_uzawa sag_uzawa;
+/* A ScalarHierarchy (amg.hpp:64-72) built on the host: nlevels matrices and
+ * nlevels - 1 prolongators; R = P^T, Jacobi diagonals and the coarse LU are
+ * formed on the device. */
+typedef struct {
+  int nlevels;
+  const sag_matrix* const* a;
+  const sag_matrix* const* p;
+} sag_scalar_hierarchy;
+/* Replaces the UzawaPreconditioner constructor (preconditioner.cpp:178-192):
+ * b = B (n_p x n_u), scalar hierarchies of A_x and A_y, and either the Mp
+ * hierarchy (TH/ISO; sv_element_areas == NULL) or the SV element areas
+ * (n_p / 3 values; hp may be NULL) for the exact element mass inverse. */
+int sag_uzawa_create(sag_ctx* ctx, const sag_matrix* b, int n_x, int n_y, int n_p,
+                     const sag_scalar_hierarchy* hx, const sag_scalar_hierarchy* hy,
+                     const sag_scalar_hierarchy* hp, const double* sv_element_areas,
+                     const sag_solver_config* cfg, sag_uzawa** out);
+int sag_uzawa_destroy(sag_uzawa* u);
+/* Replaces UzawaPreconditioner::apply (preconditioner.cpp:194-218). */
+int sag_uzawa_apply(sag_ctx* ctx, sag_uzawa* u, const double* r, double* z);
+/* solve_stokes (preconditioner.cpp:229-259) with the Uzawa preconditioner. */
+int sag_solve_stokes_uzawa(sag_ctx* ctx, const sag_matrix* k0, sag_uzawa* u, const double* rhs,
+                           double* x, const sag_solver_config* cfg, sag_krylov_report* rep,
+                           double* history, int history_cap);
 
 #ifdef __cplusplus
 }

@@ -676,6 +676,47 @@ class RefDC:
                        residual_history=hist[:min(rep.history_len, cap)].copy())
 
 
+class RefPrec:
+    """Any preconditioner variant (preconditioner.hpp:14: DC-all/LO/HO,
+    HO-AMG, Uzawa) built by the reference from a case, and solve_stokes with
+    it (experiments.cpp:124-140, :268-275)."""
+
+    def __init__(self, case: RefCase, cfg: dict):
+        c = RefConfig(cfg.get("variant", 0), cfg.get("eta_u", 1.0), cfg.get("eta_p", 1.0),
+                      cfg.get("omega0", 1.0), cfg.get("nu1", 1), cfg.get("nu2", 1),
+                      cfg.get("gamma", 1), cfg.get("restart", 30), cfg.get("tol", 1e-8),
+                      cfg.get("max_iters", 500), int(cfg.get("enclosed_flow", case.enclosed)),
+                      cfg.get("coarse_size", 0))
+        L = rlib()
+        L.ref_prec_new.restype = vp
+        L.ref_prec_new.argtypes = [vp, C.POINTER(RefConfig)]
+        self.h = C.c_void_p(_rnonnull(L.ref_prec_new(case.h, C.byref(c))))
+        self.n = case.n0
+
+    def __del__(self):
+        try:
+            rlib().ref_free(self.h)
+        except Exception:
+            pass
+
+    def apply(self, r):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.empty(self.n)
+        _rcheck(rlib().ref_prec_apply(self.h, dp(r), dp(z)))
+        return z
+
+    def solve(self, rhs, cap=1000):
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        x = np.empty(self.n)
+        rep = RefReport()
+        hist = np.zeros(cap)
+        _rcheck(rlib().ref_prec_solve(self.h, dp(rhs), dp(x), C.byref(rep), dp(hist),
+                                      C.c_int(cap)))
+        return x, dict(converged=bool(rep.converged), iterations=rep.iterations,
+                       final_relative_residual=rep.final_relative_residual,
+                       residual_history=hist[:min(rep.history_len, cap)].copy())
+
+
 def splitmix64_uniform(n: int, seed: int = 0x5EED) -> np.ndarray:
     """x_i in U[-1,1) from splitmix64(seed ^ i); identical on
     host and device."""

@@ -54,6 +54,7 @@ enum : int {
   E_CONFIG = 5,
   E_STAGNATION = 6,
   E_ZERO_DIAG = 7,
+  E_UNSUPPORTED = 8,
   E_OTHER = 99,
 };
 
@@ -80,6 +81,9 @@ int guard(F&& f) {
   } catch (const ZeroDiagonal& e) {
     g_err = e.what();
     return E_ZERO_DIAG;
+  } catch (const UnsupportedDiscretization& e) {
+    g_err = e.what();
+    return E_UNSUPPORTED;
   } catch (const Error& e) {
     g_err = e.what();
     return E_ERROR;
@@ -611,6 +615,53 @@ int ref_dc_counters(void* h, long long* out) {
   out[0] = d->prec->fine_relax_units;
   out[1] = d->prec->level1_relax_units;
   return OK;
+}
+
+// Any preconditioner variant through the reference's own classes, as
+// experiments.cpp:124-140 makes them (HOAMG, Uzawa on sys0; DC variants).
+struct PrecH : H {
+  SolverConfig cfg;
+  std::unique_ptr<StokesPreconditioner> prec;
+  SparseMatrix k0;
+};
+
+void* ref_prec_new(void* ch, const RefConfig* c) {
+  const auto& cs = static_cast<CaseH*>(ch)->c;
+  PrecH* out = nullptr;
+  int rc = guard([&] {
+    auto* h = new PrecH;
+    h->cfg = config_in(c);
+    if (h->cfg.variant == Variant::HOAMG)
+      h->prec = std::make_unique<HoAmgPreconditioner>(cs.sys0, h->cfg);
+    else if (h->cfg.variant == Variant::Uzawa)
+      h->prec = std::make_unique<UzawaPreconditioner>(cs.sys0, h->cfg);
+    else
+      h->prec = std::make_unique<DCPreconditioner>(cs.sys0, cs.sys1, cs.transfer, h->cfg);
+    h->k0 = assemble_saddle_matrix(cs.sys0);
+    out = h;
+  });
+  return rc == OK ? out : nullptr;
+}
+
+int ref_prec_apply(void* h, const double* r, double* z) {
+  auto* d = static_cast<PrecH*>(h);
+  return guard([&] {
+    const int n = d->prec->size();
+    std::vector<double> rv(r, r + n);
+    auto zv = d->prec->apply(rv);
+    std::memcpy(z, zv.data(), sizeof(double) * n);
+  });
+}
+
+int ref_prec_solve(void* h, const double* rhs, double* x, RefReport* rep, double* hist, int cap) {
+  auto* d = static_cast<PrecH*>(h);
+  return guard([&] {
+    const int n = d->prec->size();
+    std::vector<double> rv(rhs, rhs + n);
+    auto res = solve_stokes(d->k0, rv, *d->prec, d->cfg);
+    std::memcpy(x, res.x.data(), sizeof(double) * n);
+    report_out(res.report, rep, hist, cap);
+  });
 }
 
 int ref_solve_stokes(void* h, const double* rhs, double* x, RefReport* rep, double* hist,

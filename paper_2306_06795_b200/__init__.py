@@ -39,10 +39,11 @@ LIB_PATH = os.path.join(HERE, "libsag.so")
 
 __all__ = [
     "Error", "DimensionMismatch", "SingularMatrix", "SingularPatch", "ConfigError",
-    "SolverStagnation", "ZeroDiagonal", "CudaError", "Context", "SparseMatrix", "Patches",
+    "SolverStagnation", "ZeroDiagonal", "UnsupportedDiscretization", "CudaError", "Context", "SparseMatrix", "Patches",
     "VankaFactorization", "spmv", "norm2", "dot", "build_patches", "factor_patches",
     "apply_vanka", "vanka_relax", "RelaxMode", "FgmresOptions", "KrylovReport", "fgmres",
-    "SolverConfig", "Variant", "DCPreconditioner", "solve_stokes", "default_context", "lib",
+    "SolverConfig", "Variant", "DCPreconditioner", "HoAmgPreconditioner", "UzawaPreconditioner",
+    "solve_stokes", "default_context", "lib",
 ]
 
 
@@ -71,6 +72,10 @@ class ZeroDiagonal(Error):
     pass
 
 
+class UnsupportedDiscretization(Error):
+    pass
+
+
 class SolverStagnation(Error):
     pass
 
@@ -80,7 +85,8 @@ class CudaError(Error):
 
 
 _ERRORS = {1: Error, 2: DimensionMismatch, 3: SingularMatrix, 4: SingularPatch,
-           5: ConfigError, 6: SolverStagnation, 7: ZeroDiagonal, 100: CudaError, 101: Error}
+           5: ConfigError, 6: SolverStagnation, 7: ZeroDiagonal,
+           8: UnsupportedDiscretization, 100: CudaError, 101: Error}
 
 i32p = C.POINTER(C.c_int)
 f64p = C.POINTER(C.c_double)
@@ -102,7 +108,11 @@ class sag_solver_config(C.Structure):
     _fields_ = [("variant", C.c_int), ("eta_u", C.c_double), ("eta_p", C.c_double),
                 ("omega0", C.c_double), ("nu1", C.c_int), ("nu2", C.c_int), ("gamma", C.c_int),
                 ("restart", C.c_int), ("tol", C.c_double), ("max_iters", C.c_int),
-                ("enclosed_flow", C.c_int)]
+                ("enclosed_flow", C.c_int), ("allow_sv_hoamg", C.c_int)]
+
+
+class sag_scalar_hierarchy(C.Structure):
+    _fields_ = [("nlevels", C.c_int), ("a", C.POINTER(vp)), ("p", C.POINTER(vp))]
 
 
 class sag_level_desc(C.Structure):
@@ -156,6 +166,14 @@ SIGNATURES = {
     "sag_dc_info": (C.c_int, [vp, i64p, C.c_int]),
     "sag_solve_stokes": (C.c_int, [vp, vp, vp, vp, C.POINTER(sag_solver_config),
                                    C.POINTER(sag_krylov_report), vp, C.c_int]),
+    "sag_uzawa_create": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int,
+                                   C.POINTER(sag_scalar_hierarchy), C.POINTER(sag_scalar_hierarchy),
+                                   C.POINTER(sag_scalar_hierarchy), vp,
+                                   C.POINTER(sag_solver_config), C.POINTER(vp)]),
+    "sag_uzawa_destroy": (C.c_int, [vp]),
+    "sag_uzawa_apply": (C.c_int, [vp, vp, vp, vp]),
+    "sag_solve_stokes_uzawa": (C.c_int, [vp, vp, vp, vp, vp, C.POINTER(sag_solver_config),
+                                         C.POINTER(sag_krylov_report), vp, C.c_int]),
 }
 
 _lib = None
@@ -484,6 +502,8 @@ def fgmres(a: SparseMatrix, b, x, prec=None, opt: FgmresOptions = None) -> Krylo
         kind, ph = 2, prec.h
     elif isinstance(prec, DCPreconditioner):
         kind, ph = 3, prec.h
+    elif isinstance(prec, UzawaPreconditioner):
+        kind, ph = 4, prec.h
     else:
         raise ConfigError("unsupported preconditioner object")
     bp, bk = _vec_in(b, a.nrows)
@@ -500,9 +520,12 @@ def fgmres(a: SparseMatrix, b, x, prec=None, opt: FgmresOptions = None) -> Krylo
 
 # -------------------------------------------------------- preconditioner --
 class Variant:
+    """preconditioner.hpp:14"""
     DCall = 0
     DCLO = 1
     DCHO = 2
+    HOAMG = 3
+    Uzawa = 4
 
 
 @dataclass
@@ -519,12 +542,14 @@ class SolverConfig:
     tol: float = 1e-10
     max_iters: int = 200
     enclosed_flow: bool = False
+    allow_sv_hoamg: bool = False
 
     def to_c(self) -> sag_solver_config:
         return sag_solver_config(int(self.variant), float(self.eta_u), float(self.eta_p),
                                  float(self.omega0), int(self.nu1), int(self.nu2),
                                  int(self.gamma), int(self.restart), float(self.tol),
-                                 int(self.max_iters), int(bool(self.enclosed_flow)))
+                                 int(self.max_iters), int(bool(self.enclosed_flow)),
+                                 int(bool(self.allow_sv_hoamg)))
 
     def check(self):
         c = self.to_c()
@@ -616,18 +641,88 @@ class DCPreconditioner:
             pass
 
 
-def solve_stokes(k0: SparseMatrix, rhs, prec: DCPreconditioner, cfg: SolverConfig, x=None):
-    """solve_stokes (preconditioner.cpp:229-259): returns (x, KrylovReport)."""
-    if k0 is not prec.k0:
-        raise ConfigError("solve_stokes: k0 must be the preconditioner's high-order operator")
+def HoAmgPreconditioner(k0: SparseMatrix, levels, cfg: SolverConfig, sv: bool = False):
+    """HoAmgPreconditioner (preconditioner.hpp:103-118): one V-cycle of the
+    monolithic hierarchy built on the high-order system itself (levels[0] is
+    K0; build_monolithic_hierarchy(sys0) on the host). A DCPreconditioner
+    object in HO-AMG mode (sag_dc_create with variant HOAMG)."""
+    from dataclasses import replace
+    c = replace(cfg, variant=Variant.HOAMG)
+    return DCPreconditioner(k0, levels[0][2], levels, c, sv=sv)
+
+
+def _scalar_desc(levels, prolongators):
+    a = (vp * len(levels))(*[m.h.value for m in levels])
+    p = (vp * max(len(prolongators), 1))(*([m.h.value for m in prolongators] or [None]))
+    return sag_scalar_hierarchy(len(levels), a, p), (a, p)
+
+
+class UzawaPreconditioner:
+    """UzawaPreconditioner (preconditioner.hpp:118-141): scalar V-cycles on
+    A_x and A_y, t = B du - r_p, then the Mp V-cycle (TH/ISO) or the exact SV
+    element mass inverse. ``hx``/``hy``/``hp``: (matrices, prolongators) of the
+    host-built ScalarHierarchy objects; ``sv_element_areas`` for SV."""
+
+    def __init__(self, b: SparseMatrix, n_x: int, n_y: int, n_p: int, hx, hy, hp=None,
+                 sv_element_areas=None, cfg: SolverConfig = None):
+        self.ctx = b.ctx
+        self.n = n_x + n_y + n_p
+        self.n_p = n_p
+        self._keep = (b, hx, hy, hp)
+        dx, kx = _scalar_desc(*hx)
+        dy, ky = _scalar_desc(*hy)
+        dp, kp = _scalar_desc(*hp) if hp is not None else (None, None)
+        areas = None
+        if sv_element_areas is not None:
+            areas = np.ascontiguousarray(sv_element_areas, dtype=np.float64)
+        self._descs = (dx, dy, dp, kx, ky, kp, areas)
+        c = (cfg or SolverConfig()).to_c()
+        h = vp()
+        _check(lib().sag_uzawa_create(
+            self.ctx.h, b.h, int(n_x), int(n_y), int(n_p), C.byref(dx), C.byref(dy),
+            C.byref(dp) if dp is not None else None,
+            C.c_void_p(areas.ctypes.data) if areas is not None else None, C.byref(c),
+            C.byref(h)))
+        self.h = h
+
+    def apply(self, r, out=None):
+        rp, rk = _vec_in(r, self.n)
+        zp, z = _vec_out(out, self.n, like=r)
+        _check(lib().sag_uzawa_apply(self.ctx.h, self.h, rp, zp))
+        return z
+
+    def size(self):
+        return self.n
+
+    def pressure_size(self):
+        return self.n_p
+
+    def __del__(self):
+        try:
+            lib().sag_uzawa_destroy(self.h)
+        except Exception:
+            pass
+
+
+def solve_stokes(k0: SparseMatrix, rhs, prec, cfg: SolverConfig, x=None):
+    """solve_stokes (preconditioner.cpp:229-259) with a DC / HO-AMG or an Uzawa
+    preconditioner: returns (x, KrylovReport)."""
     bp, bk = _vec_in(rhs, prec.n)
     xp, xo = _vec_out(x, prec.n, like=rhs)
     rep = sag_krylov_report()
     cap = cfg.max_iters + 2
     hist = np.zeros(cap)
     c = cfg.to_c()
-    _check(lib().sag_solve_stokes(prec.ctx.h, prec.h, bp, xp, C.byref(c), C.byref(rep),
-                                  C.c_void_p(hist.ctypes.data), cap))
+    if isinstance(prec, UzawaPreconditioner):
+        if k0.nrows != prec.n:
+            raise DimensionMismatch("solve_stokes: K0 does not match the preconditioner size")
+        _check(lib().sag_solve_stokes_uzawa(prec.ctx.h, k0.h, prec.h, bp, xp, C.byref(c),
+                                            C.byref(rep), C.c_void_p(hist.ctypes.data), cap))
+    else:
+        if k0 is not prec.k0:
+            raise ConfigError("solve_stokes: k0 must be the preconditioner's high-order operator")
+        _check(lib().sag_solve_stokes(prec.ctx.h, prec.h, bp, xp, C.byref(c), C.byref(rep),
+                                      C.c_void_p(hist.ctypes.data), cap))
     return xo, KrylovReport(bool(rep.converged), rep.iterations,
                             hist[:min(rep.history_len, cap)].copy(),
                             rep.final_relative_residual)

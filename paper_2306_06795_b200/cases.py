@@ -40,6 +40,13 @@ def hlib():
         L.sagh_case_matrix_copy.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                             C.c_void_p]
         L.sagh_case_rhs.argtypes = [C.c_void_p, C.c_void_p]
+        L.sagh_case_build_extra.argtypes = [C.c_void_p, C.c_int]
+        L.sagh_case_info_extra.argtypes = [C.c_void_p, C.c_void_p]
+        L.sagh_case_ho_level.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.sagh_case_sv_areas.argtypes = [C.c_void_p, C.c_void_p]
+        L.sagh_case_solve_variant.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                              C.c_double, C.c_int, C.c_double, C.c_double,
+                                              C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
         L.sagh_case_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                       C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
@@ -136,14 +143,56 @@ class HostCase:
             dc.set_sv_transfer(pd, mm, A, P)
         return K0, dc, (k0, host)
 
+    def _extra(self, what):
+        if hlib().sagh_case_build_extra(self.h, what):
+            raise RuntimeError(hlib().sagh_last_error().decode())
+        info = np.zeros(5, dtype=np.int64)
+        hlib().sagh_case_info_extra(self.h, info.ctypes.data)
+        return [int(v) for v in info]
+
+    def hoamg_device(self, cfg: SolverConfig, ctx: Context = None):
+        """(K0, HoAmgPreconditioner) from the reference's HO hierarchy
+        (build_monolithic_hierarchy on sys0)."""
+        from . import HoAmgPreconditioner
+        nl = self._extra(1)[0]
+        lv = []
+        for l in range(nl):
+            nxyz = np.zeros(3, dtype=np.int32)
+            hlib().sagh_case_ho_level(self.h, l, nxyz.ctypes.data)
+            k = SparseMatrix.from_csr(self.matrix(2000 + 2 * l), ctx)
+            p = SparseMatrix.from_csr(self.matrix(2001 + 2 * l), ctx) if l + 1 < nl else None
+            lv.append((k, p, tuple(int(v) for v in nxyz)))
+        return lv[0][0], HoAmgPreconditioner(lv[0][0], lv, cfg, sv=self.sv)
+
+    def uzawa_device(self, cfg: SolverConfig, ctx: Context = None):
+        """(K0, UzawaPreconditioner) from the reference's scalar hierarchies."""
+        from . import UzawaPreconditioner
+        _, nx_l, ny_l, mp_l, n_el = self._extra(2)
+
+        def sh(base, nl):
+            a = [SparseMatrix.from_csr(self.matrix(base + 2 * s), ctx) for s in range(nl)]
+            p = [SparseMatrix.from_csr(self.matrix(base + 2 * s + 1), ctx) for s in range(nl - 1)]
+            return a, p
+        B = SparseMatrix.from_csr(self.matrix(3000), ctx)
+        areas = None
+        if self.sv:
+            areas = np.empty(n_el)
+            hlib().sagh_case_sv_areas(self.h, areas.ctypes.data)
+        u = UzawaPreconditioner(B, self.n_x0, self.n_y0, self.n_p0, sh(3100, nx_l),
+                                sh(3200, ny_l), sh(3300, mp_l) if not self.sv else None,
+                                sv_element_areas=areas, cfg=cfg)
+        return SparseMatrix.from_csr(self.k0(), ctx), u
+
     def solve_dropin(self, device=0, nu=1, restart=30, tol=1e-8, max_iters=500, eta_u=1.0,
-                     eta_p=1.0, omega0=1.0):
-        """The C++ drop-in (gpu::DCPreconditioner + gpu::solve_stokes) end to end."""
+                     eta_p=1.0, omega0=1.0, variant=0):
+        """The C++ drop-in (gpu::DCPreconditioner / HoAmgPreconditioner /
+        UzawaPreconditioner + gpu::solve_stokes) end to end."""
         x = np.empty(self.n0)
         rep = np.zeros(2, dtype=np.int32)
         res = C.c_double()
-        rc = hlib().sagh_case_solve(self.h, device, nu, restart, tol, max_iters, eta_u, eta_p,
-                                    omega0, x.ctypes.data, rep.ctypes.data, C.byref(res))
+        rc = hlib().sagh_case_solve_variant(self.h, device, variant, nu, restart, tol, max_iters,
+                                            eta_u, eta_p, omega0, x.ctypes.data, rep.ctypes.data,
+                                            C.byref(res))
         if rc:
             raise RuntimeError(hlib().sagh_last_error().decode())
         return x, dict(converged=bool(rep[0]), iterations=int(rep[1]),

@@ -444,18 +444,44 @@ struct Level {
 
 // SV transfer pieces (transfer.cpp:18-53): duplication P^p, mixed mass M_mix,
 // Mcg with its scalar SA hierarchy (amg.cpp:231-296).
-struct SvTransfer {
-  const Matrix* pdup = nullptr;
-  const Matrix* mmix = nullptr;
-  std::vector<const Matrix*> A;  // scalar levels
+// ScalarHierarchy (amg.hpp:64-72) on device: levels A_l, prolongators P_l,
+// R_l = P_l^T, Jacobi diagonals, V-cycle workspaces, dense coarse solve.
+struct ScalarH {
+  std::vector<const Matrix*> A;
   std::vector<const Matrix*> P;
   std::vector<std::unique_ptr<Matrix>> R;
   std::vector<DevBuf<double>> dinv, sb, sx, sr;
   std::vector<Krylov> kr;        // Jacobi-FGMRES(2) smoothing workspaces
   Coarse coarse;
+  int n() const { return A.empty() ? 0 : A[0]->nrows; }
+};
+
+struct SvTransfer {
+  const Matrix* pdup = nullptr;
+  const Matrix* mmix = nullptr;
+  ScalarH sh;                    // scalar SA hierarchy of Mcg
   Krylov outer;                  // FGMRES(20) on Mcg
   DevBuf<double> rhs, pcg;
   std::vector<int> iterations;
+};
+
+// UzawaPreconditioner (preconditioner.hpp:118-141) on device.
+struct Uzawa {
+  Ctx* ctx = nullptr;
+  const Matrix* B = nullptr;     // n_p x n_u
+  int n_x = 0, n_y = 0, n_p = 0;
+  ScalarH hx, hy, hp;            // hp unused for SV
+  bool sv_exact_mass = false;
+  DevBuf<double> areas;          // SV element areas (n_p / 3)
+  DevBuf<double> t;              // r_p - B du
+  DevBuf<double> pv;             // V(r_p - B du) before the sign flip (TH)
+  DevBuf<double> din, dout;
+  cudaGraphExec_t graph = nullptr;
+  bool graph_ok = false;
+  long long graph_launches = 0;
+  ~Uzawa() {
+    if (graph) cudaGraphExecDestroy(graph);
+  }
 };
 
 struct Dc {
@@ -470,6 +496,7 @@ struct Dc {
   std::vector<Level> lv;
   Coarse coarse;
   std::unique_ptr<SvTransfer> svt;
+  bool ho = false;  // HoAmgPreconditioner: V-cycle on a hierarchy whose level 0 is K0
   long long fine_units = 0, l1_units = 0;
   // outer solve workspace
   Krylov outer;
@@ -518,13 +545,13 @@ static void cycle_level(Ctx& c, Dc& d, int l, int nu1, int nu2, bool skip_finest
   if (relax_here && nu2 > 0) relax_kw(c, *L.K, *L.vanka, L.kry, L.x.p, L.b.p, nu2, false);
 }
 
-// ---- SV restriction: p_cg = Mcg^-1 (M_mix p_dg) (transfer.cpp:18-37) ------
+// ---- scalar V-cycle (amg.cpp:258-296) ---------------------------------------
 
-// scalar_vcycle (amg.cpp:258-296) on level l of the Mcg hierarchy: FGMRES(2)
-// Jacobi smoothing from the current x, R = P^T, dense coarse solve.
-static void scalar_level(Ctx& c, SvTransfer& t, int l, const double* b, double* x);
+// scalar_vcycle on level l of a scalar hierarchy: FGMRES(2) Jacobi smoothing
+// from the current x, R = P^T, dense coarse solve.
+static void scalar_level(Ctx& c, ScalarH& t, int l, const double* b, double* x);
 
-static void jacobi_fgmres2(Ctx& c, SvTransfer& t, int l, const double* b, double* x, bool x_zero) {
+static void jacobi_fgmres2(Ctx& c, ScalarH& t, int l, const double* b, double* x, bool x_zero) {
   // fgmres(matrix_operator(a), b, x, jacobi, {tol 0, max 2, restart 2}) with x in/out:
   // bnorm = ||b|| is the reference (krylov.cpp:23-24), the residual b - a x.
   const Matrix& A = *t.A[l];
@@ -562,7 +589,7 @@ static void jacobi_fgmres2(Ctx& c, SvTransfer& t, int l, const double* b, double
   launch_update(c, n, x, K.Z.p, (size_t)n, K.st, x_zero);
 }
 
-static void scalar_level(Ctx& c, SvTransfer& t, int l, const double* b, double* x) {
+static void scalar_level(Ctx& c, ScalarH& t, int l, const double* b, double* x) {
   const int nl = (int)t.A.size();
   if (l == nl - 1) {
     t.coarse.solve(c, b, x);
@@ -579,12 +606,24 @@ static void scalar_level(Ctx& c, SvTransfer& t, int l, const double* b, double* 
   jacobi_fgmres2(c, t, l, b, x, false);
 }
 
+// scalar_vcycle (amg.cpp:290-296) from x = 0: x <- V(2,2) b
+static void scalar_vcycle(Ctx& c, ScalarH& t, const double* b, double* x) {
+  scalar_level(c, t, 0, b, x);
+}
+
+// build_scalar_hierarchy's device half: levels and prolongators come from
+// the host build (amg.cpp:200-253); R = P^T, d_inv, coarse LU here.
+static void scalar_setup(Ctx& c, ScalarH& t, int nl, const sag_matrix* const* a,
+                         const sag_matrix* const* p, const char* what);
+
+// ---- SV restriction: p_cg = Mcg^-1 (M_mix p_dg) (transfer.cpp:18-37) ------
+
 static void sv_restrict(Ctx& c, Dc& d, const double* p_dg, double* p_cg) {
   SvTransfer& t = *d.svt;
   launch_spmv(c, *t.mmix, p_dg, t.rhs.p, Epi::Store);
   launch_zero(c, t.mmix->nrows, p_cg);
-  DevOp prec = [&](const double* in, double* out) { scalar_level(c, t, 0, in, out); };
-  FgmresOut o = fgmres_dev(c, *t.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, 20, 1e-30, t.outer);
+  DevOp prec = [&](const double* in, double* out) { scalar_vcycle(c, t.sh, in, out); };
+  FgmresOut o = fgmres_dev(c, *t.sh.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, 20, 1e-30, t.outer);
   if (!o.converged)
     throw Error(SAG_SOLVER_STAGNATION,
                 "SvPressureRestrict: mass projection did not reach tolerance in 200 iterations");
@@ -594,6 +633,16 @@ static void sv_restrict(Ctx& c, Dc& d, const double* p_dg, double* p_cg) {
 // DCPreconditioner::apply (preconditioner.cpp:114-153), r -> z on device.
 static void dc_apply_dev(Ctx& c, Dc& d, const double* r, double* z) {
   const sag_solver_config& cf = d.cfg;
+  if (d.ho) {
+    // HoAmgPreconditioner::apply (preconditioner.cpp:174-176): one V-cycle of
+    // the hierarchy built on the high-order system itself, from x = 0
+    Level& L0 = d.lv[0];
+    launch_copy(c, L0.n, r, L0.b.p);
+    cycle_level(c, d, 0, cf.nu1, cf.nu2, false);
+    launch_copy(c, L0.n, L0.x.p, z);
+    if (d.lv.size() > 1) d.fine_units += cf.nu1 + cf.nu2;
+    return;
+  }
   const bool relax_fine = cf.variant != SAG_DC_LO;
   const bool pre = relax_fine && cf.nu1 > 0;
   double* x = z;
@@ -679,7 +728,7 @@ static void check_config(const sag_solver_config& c) {
   SAG_REQUIRE(c.restart >= 1, SAG_CONFIG_ERROR, "restart must be at least 1");
   SAG_REQUIRE(c.tol > 0.0, SAG_CONFIG_ERROR, "tol must be positive");
   SAG_REQUIRE(c.max_iters >= 1, SAG_CONFIG_ERROR, "max_iters must be at least 1");
-  SAG_REQUIRE(c.variant >= 0 && c.variant <= 2, SAG_CONFIG_ERROR, "unknown solver variant");
+  SAG_REQUIRE(c.variant >= 0 && c.variant <= 4, SAG_CONFIG_ERROR, "unknown solver variant");
 }
 
 // DC apply as a CUDA graph over the fixed buffers din -> dout (SV excluded:
@@ -713,9 +762,124 @@ static void dc_apply_graph(Ctx& c, Dc& d) {
   SAG_CUDA(cudaGraphLaunch(d.graph, c.stream));
   c.launches += d.graph_launches;
   const sag_solver_config& cf = d.cfg;
+  if (d.ho) {
+    if (d.lv.size() > 1) d.fine_units += cf.nu1 + cf.nu2;
+    return;
+  }
   if (cf.variant != SAG_DC_LO) d.fine_units += cf.nu1 + cf.nu2;
   if (cf.variant != SAG_DC_HO && d.lv.size() > 1)
     d.l1_units += (long long)cf.gamma * (cf.nu1 + cf.nu2);
+}
+
+__global__ void neg_copy_kernel(int n, const double* __restrict__ in, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = -in[i];
+}
+
+// SV exact element mass inverse (preconditioner.cpp:201-211) applied to
+// s = r_p - B du = -t: dp = (3/a)[[3,-1,-1],[-1,3,-1],[-1,-1,3]] t, the
+// reference's operation order (negation is exact).
+__global__ void sv_mass_inv_kernel(int ne, const double* __restrict__ areas,
+                                   const double* __restrict__ s, double* __restrict__ dp) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
+    const double cc = __ddiv_rn(3.0, areas[e]);
+    const double t0 = -s[3 * e], t1 = -s[3 * e + 1], t2 = -s[3 * e + 2];
+    dp[3 * e] = __dmul_rn(cc, __dsub_rn(__dsub_rn(__dmul_rn(3.0, t0), t1), t2));
+    dp[3 * e + 1] = __dmul_rn(cc, __dsub_rn(__dadd_rn(-t0, __dmul_rn(3.0, t1)), t2));
+    dp[3 * e + 2] = __dmul_rn(cc, __dadd_rn(__dsub_rn(-t0, t1), __dmul_rn(3.0, t2)));
+  }
+}
+
+// UzawaPreconditioner::apply (preconditioner.cpp:186-218): du = scalar
+// V-cycles on A_x, A_y; t = B du - r_p; dp = Q_B^-1 t (exact element mass
+// inverse for SV, scalar V-cycle on Mp for TH/ISO). Computed as s = -t (the
+// residual epilogue) and dp = -V(s) = V(t): FGMRES from x = 0 is odd in b.
+static void uzawa_apply_dev(Ctx& c, Uzawa& u, const double* r, double* z) {
+  const int n_u = u.n_x + u.n_y;
+  scalar_vcycle(c, u.hx, r, z);
+  scalar_vcycle(c, u.hy, r + u.n_x, z + u.n_x);
+  SpmvArgs a;
+  a.b = r + n_u;
+  launch_spmv(c, *u.B, z, u.t.p, Epi::Resid, a);
+  const int g = std::max(1, std::min((u.n_p + 255) / 256, c.num_sms * 8));
+  if (u.sv_exact_mass) {
+    sv_mass_inv_kernel<<<g, 256, 0, c.stream>>>(u.n_p / 3, u.areas.p, u.t.p, z + n_u);
+    SAG_LAUNCHED(c);
+  } else {
+    scalar_vcycle(c, u.hp, u.t.p, u.pv.p);
+    neg_copy_kernel<<<g, 256, 0, c.stream>>>(u.n_p, u.pv.p, z + n_u);
+    SAG_LAUNCHED(c);
+  }
+}
+
+// Uzawa apply din -> dout captured once into a CUDA graph (fixed sequence).
+static void uzawa_apply_graph(Ctx& c, Uzawa& u) {
+  const bool use_graph = !(getenv("SAG_NO_GRAPH") && atoi(getenv("SAG_NO_GRAPH")));
+  if (!use_graph) {
+    uzawa_apply_dev(c, u, u.din.p, u.dout.p);
+    return;
+  }
+  if (!u.graph_ok) {
+    const long long la = c.launches;
+    cudaGraph_t g;
+    SAG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      uzawa_apply_dev(c, u, u.din.p, u.dout.p);
+    } catch (...) {
+      cudaStreamEndCapture(c.stream, &g);
+      throw;
+    }
+    SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
+    if (u.graph) cudaGraphExecDestroy(u.graph);
+    SAG_CUDA(cudaGraphInstantiate(&u.graph, g, 0));
+    cudaGraphDestroy(g);
+    u.graph_ok = true;
+    u.graph_launches = c.launches - la;
+    c.launches = la;
+  }
+  SAG_CUDA(cudaGraphLaunch(u.graph, c.stream));
+  c.launches += u.graph_launches;
+}
+
+static void scalar_setup(Ctx& c, ScalarH& t, int nl, const sag_matrix* const* a,
+                         const sag_matrix* const* p, const char* what) {
+  SAG_REQUIRE(nl >= 1, SAG_DIMENSION_MISMATCH, std::string(what) + ": empty scalar hierarchy");
+  SAG_NOTNULL(a);
+  for (int l = 0; l < nl; ++l) {
+    SAG_NOTNULL(a[l]);
+    t.A.push_back(&a[l]->m);
+    SAG_REQUIRE(t.A[l]->nrows == t.A[l]->ncols, SAG_DIMENSION_MISMATCH,
+                std::string(what) + ": scalar level is not square");
+  }
+  t.kr.resize(nl);
+  t.dinv.resize(nl);
+  t.sb.resize(nl);
+  t.sx.resize(nl);
+  t.sr.resize(nl);
+  for (int l = 0; l < nl; ++l) {
+    const int n = t.A[l]->nrows;
+    t.sb[l].alloc(n);
+    t.sx[l].alloc(n);
+    if (l + 1 < nl) {
+      SAG_NOTNULL(p);
+      SAG_NOTNULL(p[l]);
+      t.P.push_back(&p[l]->m);
+      SAG_REQUIRE(t.P[l]->nrows == n && t.P[l]->ncols == t.A[l + 1]->nrows,
+                  SAG_DIMENSION_MISMATCH, std::string(what) + ": prolongator shape mismatch");
+      t.R.push_back(transpose_dev(c, *t.P.back()));
+      t.kr[l].init(n, 2, 0);
+      t.dinv[l].alloc(n);
+      t.sr[l].alloc(n);
+      int* bad = reinterpret_cast<int*>(c.scal.p + 8);
+      SAG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+      launch_inv_diag(c, *t.A[l], t.dinv[l].p, bad);
+      int hb = 0;
+      SAG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      SAG_CUDA(cudaStreamSynchronize(c.stream));
+      SAG_REQUIRE(!hb, SAG_ZERO_DIAGONAL, std::string("inv_diagonal: zero diagonal (") + what + ")");
+    }
+  }
+  t.coarse.setup(c, *t.A.back(), -1, 0.0);
 }
 
 }  // namespace sag
@@ -725,6 +889,10 @@ using namespace sag;
 
 struct sag_dc {
   Dc d;
+};
+struct sag_uzawa {
+  Uzawa u;
+  Krylov outer;
 };
 
 namespace {
@@ -743,13 +911,28 @@ void dc_setup(Ctx& c, Dc& d, const Matrix* k0, int n_x0, int n_y0, int n_p0, int
   d.n0 = k0->nrows;
   d.sv = sv != 0;
   d.cfg = cfg;
+  SAG_REQUIRE(cfg.variant != SAG_UZAWA, SAG_CONFIG_ERROR,
+              "sag_dc_create: the Uzawa preconditioner is built by sag_uzawa_create");
+  // HoAmgPreconditioner (preconditioner.cpp:155-172): the hierarchy is built
+  // on the high-order system, so its level 0 is K0 and there is no separate
+  // fine relaxation or transfer
+  d.ho = cfg.variant == SAG_HOAMG;
+  if (d.ho) {
+    SAG_REQUIRE(!d.sv || cfg.allow_sv_hoamg, SAG_UNSUPPORTED_DISCRETIZATION,
+                "HO-AMG on Scott-Vogelius is refused by default (known poorly convergent); set "
+                "the override to force it");
+    SAG_REQUIRE(levels[0].k && levels[0].k->m.nrows == d.n0 && levels[0].n_x == n_x0 &&
+                    levels[0].n_y == n_y0 && levels[0].n_p == n_p0,
+                SAG_DIMENSION_MISMATCH, "HO-AMG: level 0 of the hierarchy must be K0");
+    d.sv = false;
+  }
   const int mrelax = std::max(std::max(cfg.nu1, cfg.nu2), 1);
   // fine-level Vanka (preconditioner.cpp:95-97)
-  {
+  if (!d.ho) {
     auto p = build_patches_dev(c, *k0, n_x0, n_y0, n_p0, d.sv);
     d.fine = factor_patches_dev(c, *k0, *p, n_x0 + n_y0);
+    if (!d.sv) d.fine_kry.init(d.n0, mrelax, 0);
   }
-  if (!d.sv) d.fine_kry.init(d.n0, mrelax, 0);
   d.fine_r.alloc(d.n0);
   // low-order hierarchy (preconditioner.cpp:40-55)
   d.lv.resize(nlevels);
@@ -788,11 +971,11 @@ void dc_setup(Ctx& c, Dc& d, const Matrix* k0, int n_x0, int n_y0, int n_p0, int
     pin = 1e-12 * K1.norm_inf;  // preconditioner.cpp:49-53 (norm of the FINEST level)
   }
   d.coarse.setup(c, *B.K, pin_row, pin);
-  if (!d.sv) {
+  if (!d.ho && !d.sv) {
     SAG_REQUIRE(d.lv[0].n == d.n0 && d.lv[0].n_x + d.lv[0].n_y == n_x0 + n_y0,
                 SAG_DIMENSION_MISMATCH,
                 "DCPreconditioner: transfer does not match the low-order system");
-  } else {
+  } else if (!d.ho) {
     SAG_REQUIRE(d.lv[0].n_x + d.lv[0].n_y == n_x0 + n_y0, SAG_DIMENSION_MISMATCH,
                 "DCPreconditioner: transfer does not match the low-order system");
   }
@@ -807,6 +990,59 @@ void dc_setup(Ctx& c, Dc& d, const Matrix* k0, int n_x0, int n_y0, int n_p0, int
 void require_ready(Dc& d) {
   SAG_REQUIRE(!d.sv || d.svt, SAG_CONFIG_ERROR,
               "SV preconditioner needs sag_dc_set_sv_transfer before use");
+}
+
+// solve_stokes (preconditioner.cpp:229-259): outer FGMRES on K0 from x = 0 with
+// apply_prec = project -> prec -> project when enclosed_flow. The
+// preconditioner runs on the fixed buffers din -> dout (`run`).
+template <class Run>
+void solve_stokes_dev(Ctx& c, const Matrix& K0, int n_u, int n_p, double* din, double* dout,
+                      Run run, Krylov& outer, const sag_solver_config& cfg, const double* rhs,
+                      double* x, sag_krylov_report* rep, double* history, int history_cap) {
+  const int n = K0.nrows;
+  InVec bi(c, rhs, n, 0);
+  OutVec xo(c, x, n, 1, false);
+  launch_zero(c, n, xo.d);
+  const int hist_cap = cfg.max_iters + 2;
+  if (outer.n != n || outer.m < cfg.restart || outer.hist_cap < hist_cap)
+    outer.init(n, cfg.restart, hist_cap);
+  double* mean_r = c.scal.p + 1;
+  double* mean_z = c.scal.p + 2;
+  const bool enclosed = cfg.enclosed_flow != 0;
+  DevOp prec = [&](const double* v, double* z) {
+    if (enclosed) {
+      Fin f;
+      f.kind = FIN_MEAN;
+      f.i = n_p;
+      f.out = mean_r;
+      launch_sum(c, n_p, v + n_u, f);
+      launch_project(c, n, n_u, v, mean_r, din);
+    } else {
+      launch_copy(c, n, v, din);
+    }
+    run();
+    if (enclosed) {
+      Fin f;
+      f.kind = FIN_MEAN;
+      f.i = n_p;
+      f.out = mean_z;
+      launch_sum(c, n_p, dout + n_u, f);
+      launch_project(c, n, n_u, dout, mean_z, z);
+    } else {
+      launch_copy(c, n, dout, z);
+    }
+  };
+  FgmresOut o = fgmres_dev(c, K0, bi.d, xo.d, prec, cfg.tol, cfg.max_iters, cfg.restart, 1e-30,
+                           outer);
+  xo.finish();
+  if (rep) {
+    rep->converged = o.converged;
+    rep->iterations = o.iterations;
+    rep->final_relative_residual = o.final_rel;
+    rep->history_len = (int)o.hist.size();
+  }
+  if (history)
+    for (int i = 0; i < history_cap && i < (int)o.hist.size(); ++i) history[i] = o.hist[i];
 }
 
 }  // namespace
@@ -828,6 +1064,7 @@ int sag_solver_config_default(sag_solver_config* cfg) {
     cfg->tol = 1e-10;
     cfg->max_iters = 200;
     cfg->enclosed_flow = 0;
+    cfg->allow_sv_hoamg = 0;
   });
 }
 
@@ -916,6 +1153,14 @@ int sag_fgmres(sag_ctx* ctx, const sag_matrix* a, const double* b, double* x, in
         op = [&c, &d](const double* in, double* out) { dc_apply_dev(c, d, in, out); };
         break;
       }
+      case SAG_PREC_UZAWA: {
+        SAG_NOTNULL(prec);
+        Uzawa& u = const_cast<sag_uzawa*>(static_cast<const sag_uzawa*>(prec))->u;
+        SAG_REQUIRE(u.n_x + u.n_y + u.n_p == n, SAG_DIMENSION_MISMATCH,
+                    "fgmres: preconditioner size mismatch");
+        op = [&c, &u](const double* in, double* out) { uzawa_apply_dev(c, u, in, out); };
+        break;
+      }
       default:
         throw Error(SAG_CONFIG_ERROR, "fgmres: unknown preconditioner kind");
     }
@@ -989,36 +1234,9 @@ int sag_dc_set_sv_transfer(sag_dc* h, const sag_matrix* p_dup, const sag_matrix*
     SAG_REQUIRE(t->pdup->nrows == d.n_p0 && t->pdup->ncols == n_p1 && t->mmix->nrows == n_p1 &&
                     t->mmix->ncols == d.n_p0,
                 SAG_DIMENSION_MISMATCH, "sag_dc_set_sv_transfer: transfer shapes mismatch");
-    SAG_REQUIRE(nsl >= 1, SAG_DIMENSION_MISMATCH, "sag_dc_set_sv_transfer: empty hierarchy");
-    for (int l = 0; l < nsl; ++l) t->A.push_back(&scalar_levels[l]->m);
-    SAG_REQUIRE(t->A[0]->nrows == n_p1, SAG_DIMENSION_MISMATCH,
+    scalar_setup(c, t->sh, nsl, scalar_levels, scalar_prolongators, "Mcg hierarchy");
+    SAG_REQUIRE(t->sh.n() == n_p1, SAG_DIMENSION_MISMATCH,
                 "sag_dc_set_sv_transfer: Mcg size mismatch");
-    t->kr.resize(nsl);
-    t->dinv.resize(nsl);
-    t->sb.resize(nsl);
-    t->sx.resize(nsl);
-    t->sr.resize(nsl);
-    for (int l = 0; l < nsl; ++l) {
-      const int n = t->A[l]->nrows;
-      t->sb[l].alloc(n);
-      t->sx[l].alloc(n);
-      if (l + 1 < nsl) {
-        SAG_NOTNULL(scalar_prolongators);
-        t->P.push_back(&scalar_prolongators[l]->m);
-        t->R.push_back(transpose_dev(c, *t->P.back()));
-        t->kr[l].init(n, 2, 0);
-        t->dinv[l].alloc(n);
-        t->sr[l].alloc(n);
-        int* bad = reinterpret_cast<int*>(c.scal.p + 8);
-        SAG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
-        launch_inv_diag(c, *t->A[l], t->dinv[l].p, bad);
-        int hb = 0;
-        SAG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-        SAG_CUDA(cudaStreamSynchronize(c.stream));
-        SAG_REQUIRE(!hb, SAG_ZERO_DIAGONAL, "inv_diagonal: zero diagonal in the Mcg hierarchy");
-      }
-    }
-    t->coarse.setup(c, *t->A.back(), -1, 0.0);
     t->outer.init(n_p1, 20, 202);
     t->rhs.alloc(n_p1);
     d.svt = std::move(t);
@@ -1099,52 +1317,98 @@ int sag_solve_stokes(sag_ctx* ctx, sag_dc* h, const double* rhs, double* x,
     auto& c = ctx->c;
     Dc& d = h->d;
     require_ready(d);
-    const int n = d.n0;
-    const int n_u = d.n_x0 + d.n_y0, n_p = d.n_p0;
-    InVec bi(c, rhs, n, 0);
-    OutVec xo(c, x, n, 1, false);
-    launch_zero(c, n, xo.d);
-    const int hist_cap = cfg->max_iters + 2;
-    if (d.outer.n != n || d.outer.m < cfg->restart || d.outer.hist_cap < hist_cap)
-      d.outer.init(n, cfg->restart, hist_cap);
-    double* mean_r = c.scal.p + 1;
-    double* mean_z = c.scal.p + 2;
-    const bool enclosed = cfg->enclosed_flow != 0;
-    // apply_prec (preconditioner.cpp:241-250)
-    DevOp prec = [&](const double* v, double* z) {
-      if (enclosed) {
-        Fin f;
-        f.kind = FIN_MEAN;
-        f.i = n_p;
-        f.out = mean_r;
-        launch_sum(c, n_p, v + n_u, f);
-        launch_project(c, n, n_u, v, mean_r, d.din.p);
-      } else {
-        launch_copy(c, n, v, d.din.p);
-      }
-      dc_apply_graph(c, d);
-      if (enclosed) {
-        Fin f;
-        f.kind = FIN_MEAN;
-        f.i = n_p;
-        f.out = mean_z;
-        launch_sum(c, n_p, d.dout.p + n_u, f);
-        launch_project(c, n, n_u, d.dout.p, mean_z, z);
-      } else {
-        launch_copy(c, n, d.dout.p, z);
-      }
-    };
-    FgmresOut o = fgmres_dev(c, *d.K0, bi.d, xo.d, prec, cfg->tol, cfg->max_iters, cfg->restart,
-                             1e-30, d.outer);
-    xo.finish();
-    if (rep) {
-      rep->converged = o.converged;
-      rep->iterations = o.iterations;
-      rep->final_relative_residual = o.final_rel;
-      rep->history_len = (int)o.hist.size();
+    solve_stokes_dev(c, *d.K0, d.n_x0 + d.n_y0, d.n_p0, d.din.p, d.dout.p,
+                     [&] { dc_apply_graph(c, d); }, d.outer, *cfg, rhs, x, rep, history,
+                     history_cap);
+  });
+}
+
+int sag_uzawa_create(sag_ctx* ctx, const sag_matrix* b, int n_x, int n_y, int n_p,
+                     const sag_scalar_hierarchy* hx, const sag_scalar_hierarchy* hy,
+                     const sag_scalar_hierarchy* hp, const double* sv_element_areas,
+                     const sag_solver_config* cfg, sag_uzawa** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(b);
+    SAG_NOTNULL(hx);
+    SAG_NOTNULL(hy);
+    SAG_NOTNULL(cfg);
+    SAG_NOTNULL(out);
+    check_config(*cfg);
+    auto& c = ctx->c;
+    auto u = std::make_unique<sag_uzawa>();
+    Uzawa& z = u->u;
+    z.ctx = &c;
+    z.B = &b->m;
+    z.n_x = n_x;
+    z.n_y = n_y;
+    z.n_p = n_p;
+    SAG_REQUIRE(z.B->nrows == n_p && z.B->ncols == n_x + n_y, SAG_DIMENSION_MISMATCH,
+                "UzawaPreconditioner: B must be n_p x n_u");
+    scalar_setup(c, z.hx, hx->nlevels, hx->a, hx->p, "A_x hierarchy");
+    scalar_setup(c, z.hy, hy->nlevels, hy->a, hy->p, "A_y hierarchy");
+    SAG_REQUIRE(z.hx.n() == n_x && z.hy.n() == n_y, SAG_DIMENSION_MISMATCH,
+                "UzawaPreconditioner: velocity hierarchies do not match n_x / n_y");
+    if (sv_element_areas) {
+      // SV: exact element mass inverse (preconditioner.cpp:191-193)
+      SAG_REQUIRE(n_p % 3 == 0, SAG_DIMENSION_MISMATCH,
+                  "UzawaPreconditioner: SV pressure count must be 3 per element");
+      z.sv_exact_mass = true;
+      z.areas.alloc(std::max(n_p / 3, 1));
+      SAG_CUDA(cudaMemcpyAsync(z.areas.p, sv_element_areas, sizeof(double) * (n_p / 3),
+                               cudaMemcpyDefault, c.stream));
+    } else {
+      SAG_NOTNULL(hp);
+      scalar_setup(c, z.hp, hp->nlevels, hp->a, hp->p, "Mp hierarchy");
+      SAG_REQUIRE(z.hp.n() == n_p, SAG_DIMENSION_MISMATCH,
+                  "UzawaPreconditioner: pressure mass hierarchy does not match n_p");
+      z.pv.alloc(n_p);
     }
-    if (history)
-      for (int i = 0; i < history_cap && i < (int)o.hist.size(); ++i) history[i] = o.hist[i];
+    z.t.alloc(std::max(n_p, 1));
+    z.din.alloc(n_x + n_y + n_p);
+    z.dout.alloc(n_x + n_y + n_p);
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    *out = u.release();
+  });
+}
+
+int sag_uzawa_destroy(sag_uzawa* u) {
+  delete u;
+  return SAG_OK;
+}
+
+int sag_uzawa_apply(sag_ctx* ctx, sag_uzawa* h, const double* r, double* z) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(h);
+    auto& c = ctx->c;
+    Uzawa& u = h->u;
+    const int n = u.n_x + u.n_y + u.n_p;
+    InVec ri(c, r, n, 0);
+    OutVec zo(c, z, n, 1, false);
+    launch_copy(c, n, ri.d, u.din.p);
+    uzawa_apply_graph(c, u);
+    launch_copy(c, n, u.dout.p, zo.d);
+    zo.finish();
+  });
+}
+
+int sag_solve_stokes_uzawa(sag_ctx* ctx, const sag_matrix* k0, sag_uzawa* h, const double* rhs,
+                           double* x, const sag_solver_config* cfg, sag_krylov_report* rep,
+                           double* history, int history_cap) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(k0);
+    SAG_NOTNULL(h);
+    SAG_NOTNULL(cfg);
+    check_config(*cfg);
+    auto& c = ctx->c;
+    Uzawa& u = h->u;
+    const int n_u = u.n_x + u.n_y;
+    SAG_REQUIRE(k0->m.nrows == n_u + u.n_p && k0->m.ncols == k0->m.nrows, SAG_DIMENSION_MISMATCH,
+                "solve_stokes: K0 does not match the preconditioner size");
+    solve_stokes_dev(c, k0->m, n_u, u.n_p, u.din.p, u.dout.p, [&] { uzawa_apply_graph(c, u); },
+                     h->outer, *cfg, rhs, x, rep, history, history_cap);
   });
 }
 

@@ -23,6 +23,7 @@ void check(int s) {
     case SAG_CONFIG_ERROR: throw ConfigError(msg);
     case SAG_SOLVER_STAGNATION: throw SolverStagnation(msg);
     case SAG_ZERO_DIAGONAL: throw ZeroDiagonal(msg);
+    case SAG_UNSUPPORTED_DISCRETIZATION: throw UnsupportedDiscretization(msg);
     default: throw Error(msg);
   }
 }
@@ -68,8 +69,13 @@ std::vector<double> apply_vanka(Device& dev, const VankaFactorization& f,
 
 static sag_solver_config to_c(const SolverConfig& c) {
   sag_solver_config s;
-  s.variant = c.variant == Variant::DCLO ? SAG_DC_LO : c.variant == Variant::DCHO ? SAG_DC_HO
-                                                                                   : SAG_DC_ALL;
+  switch (c.variant) {
+    case Variant::DCLO: s.variant = SAG_DC_LO; break;
+    case Variant::DCHO: s.variant = SAG_DC_HO; break;
+    case Variant::HOAMG: s.variant = SAG_HOAMG; break;
+    case Variant::Uzawa: s.variant = SAG_UZAWA; break;
+    default: s.variant = SAG_DC_ALL; break;
+  }
   s.eta_u = c.eta_u;
   s.eta_p = c.eta_p;
   s.omega0 = c.omega0;
@@ -80,6 +86,7 @@ static sag_solver_config to_c(const SolverConfig& c) {
   s.tol = c.tol;
   s.max_iters = c.max_iters;
   s.enclosed_flow = c.enclosed_flow ? 1 : 0;
+  s.allow_sv_hoamg = c.allow_sv_hoamg ? 1 : 0;
   return s;
 }
 
@@ -159,24 +166,166 @@ void DCPreconditioner::set_parameters(double eta_u, double eta_p, double omega0)
   check(sag_dc_set_parameters(dc_, eta_u, eta_p, omega0));
 }
 
-SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
-                         const DCPreconditioner& prec, const SolverConfig& cfg) {
-  if (cfg.validate) cfg.check();
-  if (k0.nrows != prec.size() || static_cast<int>(rhs.size()) != prec.size())
-    throw DimensionMismatch("solve_stokes: size mismatch");
+namespace {
+SolveResult report_in(std::vector<double> x, const sag_krylov_report& rep,
+                      const std::vector<double>& hist) {
   SolveResult res;
-  res.x.assign(rhs.size(), 0.0);
-  const sag_solver_config c = to_c(cfg);
-  sag_krylov_report rep{};
-  std::vector<double> hist(cfg.max_iters + 2);
-  check(sag_solve_stokes(prec.device().handle(), prec.handle(), rhs.data(), res.x.data(), &c,
-                         &rep, hist.data(), static_cast<int>(hist.size())));
+  res.x = std::move(x);
   res.report.converged = rep.converged != 0;
   res.report.iterations = rep.iterations;
   res.report.final_relative_residual = rep.final_relative_residual;
-  res.report.residual_history.assign(hist.begin(),
-                                     hist.begin() + std::min<int>(rep.history_len, hist.size()));
+  res.report.residual_history.assign(
+      hist.begin(), hist.begin() + std::min<size_t>(rep.history_len, hist.size()));
   return res;
+}
+
+SolveResult solve_dc(const SparseMatrix& k0, const std::vector<double>& rhs, Device& dev,
+                     sag_dc* dc, int n, const SolverConfig& cfg) {
+  if (cfg.validate) cfg.check();
+  if (k0.nrows != n || static_cast<int>(rhs.size()) != n)
+    throw DimensionMismatch("solve_stokes: size mismatch");
+  std::vector<double> x(rhs.size(), 0.0);
+  const sag_solver_config c = to_c(cfg);
+  sag_krylov_report rep{};
+  std::vector<double> hist(cfg.max_iters + 2);
+  check(sag_solve_stokes(dev.handle(), dc, rhs.data(), x.data(), &c, &rep, hist.data(),
+                         static_cast<int>(hist.size())));
+  return report_in(std::move(x), rep, hist);
+}
+
+// a ScalarHierarchy uploaded level by level
+struct ScalarUpload {
+  std::vector<const sag_matrix*> a, p;
+  sag_scalar_hierarchy desc{};
+};
+ScalarUpload upload_scalar(Device& dev, const ScalarHierarchy& h,
+                           std::vector<std::unique_ptr<DeviceMatrix>>& keep) {
+  ScalarUpload u;
+  for (const auto& m : h.matrices) {
+    keep.push_back(std::make_unique<DeviceMatrix>(dev, m));
+    u.a.push_back(keep.back()->handle());
+  }
+  for (const auto& m : h.prolongators) {
+    keep.push_back(std::make_unique<DeviceMatrix>(dev, m));
+    u.p.push_back(keep.back()->handle());
+  }
+  u.desc.nlevels = static_cast<int>(u.a.size());
+  u.desc.a = u.a.data();
+  u.desc.p = u.p.empty() ? nullptr : u.p.data();
+  return u;
+}
+}  // namespace
+
+SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
+                         const DCPreconditioner& prec, const SolverConfig& cfg) {
+  return solve_dc(k0, rhs, prec.device(), prec.handle(), prec.size(), cfg);
+}
+
+HoAmgPreconditioner::HoAmgPreconditioner(Device& dev, const SaddleSystem& sys0, SolverConfig cfg)
+    : dev_(dev), cfg_(std::move(cfg)) {
+  if (cfg_.validate) cfg_.check();
+  const bool sv = sys0.disc == Discretization::SV;
+  if (sv && !cfg_.allow_sv_hoamg)
+    throw UnsupportedDiscretization(
+        "HO-AMG on Scott-Vogelius is refused by default (known poorly convergent); set the "
+        "override to force it");
+  n_ = sys0.total_dofs();
+  n_p_ = sys0.n_p;
+  if (sv) {
+    // the dg pressure space guides coarsening with its mass matrix
+    // (preconditioner.cpp:163-168)
+    SaddleSystem tmp = sys0;
+    tmp.Ap = sys0.Mp;
+    h_ = build_monolithic_hierarchy(tmp, cfg_.amg);
+  } else {
+    h_ = build_monolithic_hierarchy(sys0, cfg_.amg);
+  }
+  std::vector<sag_level_desc> lv(h_.num_levels());
+  for (int l = 0; l < h_.num_levels(); ++l) {
+    const auto& L = h_.levels[l];
+    mats_.push_back(std::make_unique<DeviceMatrix>(dev, L.k));
+    lv[l].k = mats_.back()->handle();
+    lv[l].p = nullptr;
+    if (l + 1 < h_.num_levels()) {
+      mats_.push_back(std::make_unique<DeviceMatrix>(dev, L.p));
+      lv[l].p = mats_.back()->handle();
+    }
+    lv[l].n_x = L.n_x;
+    lv[l].n_y = L.n_y;
+    lv[l].n_p = L.n_p;
+  }
+  sag_solver_config c = to_c(cfg_);
+  c.variant = SAG_HOAMG;
+  const auto& L0 = h_.levels.front();
+  check(sag_dc_create(dev.handle(), lv[0].k, L0.n_x, L0.n_y, L0.n_p, sv ? 1 : 0, h_.num_levels(),
+                      lv.data(), &c, &dc_));
+}
+
+HoAmgPreconditioner::~HoAmgPreconditioner() { sag_dc_destroy(dc_); }
+
+std::vector<double> HoAmgPreconditioner::apply(const std::vector<double>& r) const {
+  if (static_cast<int>(r.size()) != size())
+    throw DimensionMismatch("HoAmgPreconditioner::apply: size mismatch");
+  std::vector<double> z(r.size());
+  check(sag_dc_apply(dev_.handle(), dc_, r.data(), z.data()));
+  long long cnt[2];
+  check(sag_dc_counters(dc_, cnt));
+  fine_relax_units = cnt[0];
+  return z;
+}
+
+SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
+                         const HoAmgPreconditioner& prec, const SolverConfig& cfg) {
+  return solve_dc(k0, rhs, prec.device(), prec.handle(), prec.size(), cfg);
+}
+
+UzawaPreconditioner::UzawaPreconditioner(Device& dev, const SaddleSystem& sys, SolverConfig cfg)
+    : dev_(dev), cfg_(std::move(cfg)) {
+  if (cfg_.validate) cfg_.check();
+  const int n_x = sys.n_x;
+  n_u_ = sys.n_u();
+  n_p_ = sys.n_p;
+  ScalarHierarchy hx = build_scalar_hierarchy(extract_block(sys.A, 0, n_x, 0, n_x), cfg_.amg);
+  ScalarHierarchy hy =
+      build_scalar_hierarchy(extract_block(sys.A, n_x, n_u_, n_x, n_u_), cfg_.amg);
+  mats_.push_back(std::make_unique<DeviceMatrix>(dev, sys.B));
+  const sag_matrix* b = mats_.back()->handle();
+  ScalarUpload ux = upload_scalar(dev, hx, mats_), uy = upload_scalar(dev, hy, mats_);
+  const sag_solver_config c = to_c(cfg_);
+  if (sys.disc == Discretization::SV) {
+    check(sag_uzawa_create(dev.handle(), b, n_x, n_u_ - n_x, n_p_, &ux.desc, &uy.desc, nullptr,
+                           sys.sv_element_areas.data(), &c, &u_));
+  } else {
+    ScalarHierarchy hp = build_scalar_hierarchy(sys.Mp, cfg_.amg);
+    ScalarUpload up = upload_scalar(dev, hp, mats_);
+    check(sag_uzawa_create(dev.handle(), b, n_x, n_u_ - n_x, n_p_, &ux.desc, &uy.desc, &up.desc,
+                           nullptr, &c, &u_));
+  }
+}
+
+UzawaPreconditioner::~UzawaPreconditioner() { sag_uzawa_destroy(u_); }
+
+std::vector<double> UzawaPreconditioner::apply(const std::vector<double>& r) const {
+  if (static_cast<int>(r.size()) != size())
+    throw DimensionMismatch("UzawaPreconditioner::apply: size mismatch");
+  std::vector<double> z(r.size());
+  check(sag_uzawa_apply(dev_.handle(), u_, r.data(), z.data()));
+  return z;
+}
+
+SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
+                         const UzawaPreconditioner& prec, const SolverConfig& cfg) {
+  if (cfg.validate) cfg.check();
+  if (k0.nrows != prec.size() || static_cast<int>(rhs.size()) != prec.size())
+    throw DimensionMismatch("solve_stokes: size mismatch");
+  DeviceMatrix k(prec.device(), k0);
+  std::vector<double> x(rhs.size(), 0.0);
+  const sag_solver_config c = to_c(cfg);
+  sag_krylov_report rep{};
+  std::vector<double> hist(cfg.max_iters + 2);
+  check(sag_solve_stokes_uzawa(prec.device().handle(), k.handle(), prec.handle(), rhs.data(),
+                               x.data(), &c, &rep, hist.data(), static_cast<int>(hist.size())));
+  return report_in(std::move(x), rep, hist);
 }
 
 }  // namespace stokesamg::gpu
@@ -195,6 +344,9 @@ struct HostCase {
   SparseMatrix k0;
   MonolithicHierarchy h;
   ScalarHierarchy sh;  // SV only
+  // HO-AMG / Uzawa inputs (sagh_case_build_extra)
+  MonolithicHierarchy ho;
+  ScalarHierarchy ux, uy, ump;
 };
 
 template <class F>
@@ -218,6 +370,20 @@ const SparseMatrix* pick(const HostCase& hc, int which) {
   }
   if (which == 1000) return &hc.c.transfer.p0_pressure;
   if (which == 1001) return &hc.c.sys0.M_mix;
+  if (which >= 2000 && which < 3000) {  // HO-AMG hierarchy: 2000 + 2l K, 2001 + 2l P
+    const int l = (which - 2000) / 2;
+    if (l >= hc.ho.num_levels()) return nullptr;
+    if ((which - 2000) % 2 == 0) return &hc.ho.levels[l].k;
+    return l + 1 < hc.ho.num_levels() ? &hc.ho.levels[l].p : nullptr;
+  }
+  if (which == 3000) return &hc.c.sys0.B;
+  if (which > 3000 && which < 4000) {  // Uzawa: 3100/3200/3300 + 2s A_s, + 2s + 1 P_s
+    const int f = (which - 3000) / 100, k = (which - 3000) % 100, s = k / 2;
+    const ScalarHierarchy* sh = f == 1 ? &hc.ux : f == 2 ? &hc.uy : f == 3 ? &hc.ump : nullptr;
+    if (!sh) return nullptr;
+    if (k % 2 == 0) return s < sh->levels() ? &sh->matrices[s] : nullptr;
+    return s + 1 < sh->levels() ? &sh->prolongators[s] : nullptr;
+  }
   const int s = (which - 1002) / 2;
   if ((which - 1002) % 2 == 0) return s < hc.sh.levels() ? &hc.sh.matrices[s] : nullptr;
   return s + 1 < hc.sh.levels() ? &hc.sh.prolongators[s] : nullptr;
@@ -245,6 +411,9 @@ AssembledCase mesh_case(const char* path, double k1, double k2) {
 extern "C" {
 
 const char* sagh_last_error() { return g_err.c_str(); }
+int sagh_case_solve_variant(void* h, int device, int variant, int nu, int restart, double tol,
+                            int max_iters, double eta_u, double eta_p, double omega0, double* x,
+                            int* rep, double* res);
 
 // problem/sv/mesh_kind/n as ExperimentSpec (experiments.hpp:24-38); mesh_kind
 // "file" reads mesh_path; "file_forced" builds BASELINE config 4 from
@@ -278,6 +447,58 @@ void* sagh_case_build(const char* problem, int sv, const char* mesh_kind, int n,
 }
 
 void sagh_case_free(void* h) { delete static_cast<HostCase*>(h); }
+
+// The reference's setup for the other preconditioners of this case, with the
+// default AmgConfig: what = 1 -> HoAmgPreconditioner's hierarchy
+// (preconditioner.cpp:155-172), what = 2 -> UzawaPreconditioner's scalar
+// hierarchies (preconditioner.cpp:178-192).
+int sagh_case_build_extra(void* h, int what) {
+  return guarded([&] {
+    auto& hc = *static_cast<HostCase*>(h);
+    const SaddleSystem& s0 = hc.c.sys0;
+    if (what == 1) {
+      if (s0.disc == Discretization::SV) {
+        SaddleSystem tmp = s0;
+        tmp.Ap = s0.Mp;
+        hc.ho = build_monolithic_hierarchy(tmp, AmgConfig{});
+      } else {
+        hc.ho = build_monolithic_hierarchy(s0, AmgConfig{});
+      }
+    } else if (what == 2) {
+      hc.ux = build_scalar_hierarchy(extract_block(s0.A, 0, s0.n_x, 0, s0.n_x), AmgConfig{});
+      hc.uy = build_scalar_hierarchy(extract_block(s0.A, s0.n_x, s0.n_u(), s0.n_x, s0.n_u()),
+                                     AmgConfig{});
+      if (s0.disc != Discretization::SV) hc.ump = build_scalar_hierarchy(s0.Mp, AmgConfig{});
+    } else {
+      throw ConfigError("sagh_case_build_extra: what must be 1 or 2");
+    }
+  });
+}
+
+// out = [HO levels, A_x levels, A_y levels, Mp levels, SV element count]
+int sagh_case_info_extra(void* h, long long* out) {
+  const auto& hc = *static_cast<HostCase*>(h);
+  out[0] = hc.ho.num_levels();
+  out[1] = hc.ux.levels();
+  out[2] = hc.uy.levels();
+  out[3] = hc.ump.levels();
+  out[4] = static_cast<long long>(hc.c.sys0.sv_element_areas.size());
+  return 0;
+}
+
+int sagh_case_ho_level(void* h, int l, int* nxyz) {
+  const auto& lev = static_cast<HostCase*>(h)->ho.levels.at(l);
+  nxyz[0] = lev.n_x;
+  nxyz[1] = lev.n_y;
+  nxyz[2] = lev.n_p;
+  return 0;
+}
+
+int sagh_case_sv_areas(void* h, double* out) {
+  const auto& a = static_cast<HostCase*>(h)->c.sys0.sv_element_areas;
+  std::memcpy(out, a.data(), sizeof(double) * a.size());
+  return 0;
+}
 
 // out = [n_x0, n_y0, n_p0, nlevels, enclosed, sv, scalar levels]
 int sagh_case_info(void* h, long long* out) {
@@ -335,10 +556,20 @@ int sagh_case_rhs(void* h, double* rhs) {
 // relative residual.
 int sagh_case_solve(void* h, int device, int nu, int restart, double tol, int max_iters,
                     double eta_u, double eta_p, double omega0, double* x, int* rep, double* res) {
+  return sagh_case_solve_variant(h, device, 0, nu, restart, tol, max_iters, eta_u, eta_p, omega0,
+                                 x, rep, res);
+}
+
+// as sagh_case_solve with the preconditioner variant (preconditioner.hpp:14):
+// 0-2 gpu::DCPreconditioner, 3 gpu::HoAmgPreconditioner, 4 gpu::UzawaPreconditioner
+int sagh_case_solve_variant(void* h, int device, int variant, int nu, int restart, double tol,
+                            int max_iters, double eta_u, double eta_p, double omega0, double* x,
+                            int* rep, double* res) {
   return guarded([&] {
     auto& hc = *static_cast<HostCase*>(h);
     gpu::Device dev(device);
     SolverConfig cfg;
+    cfg.variant = static_cast<Variant>(variant);
     cfg.nu1 = cfg.nu2 = nu;
     cfg.restart = restart;
     cfg.tol = tol;
@@ -347,8 +578,17 @@ int sagh_case_solve(void* h, int device, int nu, int restart, double tol, int ma
     cfg.eta_p = eta_p;
     cfg.omega0 = omega0;
     cfg.enclosed_flow = hc.c.enclosed;
-    gpu::DCPreconditioner prec(dev, hc.c.sys0, hc.c.sys1, hc.c.transfer, cfg);
-    SolveResult r = gpu::solve_stokes(prec.k0(), hc.c.sys0.rhs, prec, cfg);
+    SolveResult r;
+    if (variant == 3) {
+      gpu::HoAmgPreconditioner prec(dev, hc.c.sys0, cfg);
+      r = gpu::solve_stokes(hc.k0, hc.c.sys0.rhs, prec, cfg);
+    } else if (variant == 4) {
+      gpu::UzawaPreconditioner prec(dev, hc.c.sys0, cfg);
+      r = gpu::solve_stokes(hc.k0, hc.c.sys0.rhs, prec, cfg);
+    } else {
+      gpu::DCPreconditioner prec(dev, hc.c.sys0, hc.c.sys1, hc.c.transfer, cfg);
+      r = gpu::solve_stokes(prec.k0(), hc.c.sys0.rhs, prec, cfg);
+    }
     std::memcpy(x, r.x.data(), sizeof(double) * r.x.size());
     rep[0] = r.report.converged ? 1 : 0;
     rep[1] = r.report.iterations;

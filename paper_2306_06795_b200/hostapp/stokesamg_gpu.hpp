@@ -102,9 +102,59 @@ class DCPreconditioner : public StokesPreconditioner {
   sag_dc* dc_ = nullptr;
 };
 
+// HoAmgPreconditioner (preconditioner.hpp:103-118): the monolithic hierarchy
+// built by the reference on the high-order system itself, one V-cycle per
+// apply on the device (a sag_dc in HO-AMG mode).
+class HoAmgPreconditioner : public StokesPreconditioner {
+ public:
+  HoAmgPreconditioner(Device& dev, const SaddleSystem& sys0, SolverConfig cfg);
+  ~HoAmgPreconditioner() override;
+
+  std::vector<double> apply(const std::vector<double>& r) const override;
+  int size() const override { return n_; }
+  int pressure_size() const override { return n_p_; }
+  const MonolithicHierarchy& hierarchy() const { return h_; }
+  sag_dc* handle() const { return dc_; }
+  Device& device() const { return dev_; }
+
+ private:
+  Device& dev_;
+  SolverConfig cfg_;
+  int n_ = 0, n_p_ = 0;
+  MonolithicHierarchy h_;
+  std::vector<std::unique_ptr<DeviceMatrix>> mats_;
+  sag_dc* dc_ = nullptr;
+};
+
+// UzawaPreconditioner (preconditioner.hpp:118-141): scalar hierarchies of
+// A_x, A_y (and Mp for TH/ISO) built by the reference on the host, all
+// V-cycles and the SV exact element mass inverse on the device.
+class UzawaPreconditioner : public StokesPreconditioner {
+ public:
+  UzawaPreconditioner(Device& dev, const SaddleSystem& sys, SolverConfig cfg);
+  ~UzawaPreconditioner() override;
+
+  std::vector<double> apply(const std::vector<double>& r) const override;
+  int size() const override { return n_u_ + n_p_; }
+  int pressure_size() const override { return n_p_; }
+  sag_uzawa* handle() const { return u_; }
+  Device& device() const { return dev_; }
+
+ private:
+  Device& dev_;
+  SolverConfig cfg_;
+  int n_u_ = 0, n_p_ = 0;
+  std::vector<std::unique_ptr<DeviceMatrix>> mats_;
+  sag_uzawa* u_ = nullptr;
+};
+
 // solve_stokes (preconditioner.hpp:147-148): the outer FGMRES with all
 // vectors resident on the device.
 SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
                          const DCPreconditioner& prec, const SolverConfig& cfg);
+SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
+                         const HoAmgPreconditioner& prec, const SolverConfig& cfg);
+SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
+                         const UzawaPreconditioner& prec, const SolverConfig& cfg);
 
 }  // namespace stokesamg::gpu

@@ -228,3 +228,53 @@ def test_config2_solve_fullsize(S, config2):
     # the true residual, recomputed by the reference's own spmv
     res = rhs - O.RefMat.from_csr(k0).spmv(x)
     assert np.linalg.norm(res) / np.linalg.norm(rhs) <= 1.01e-8
+
+
+# --------------------------------------- HO-AMG and Uzawa --
+def _prec_pair(S, n, variant, sv=False, extra=None):
+    from paper_2306_06795_b200.cases import HostCase
+    conf = dict(variant=variant, nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500)
+    conf.update(extra or {})
+    c = O.RefCase.build("cavity", sv, "structured", n)
+    conf["enclosed_flow"] = c.enclosed
+    ref = O.RefPrec(c, conf)
+    h = HostCase("cavity", sv, "structured", n)
+    cfg = S.SolverConfig(variant=variant, nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
+                         enclosed_flow=c.enclosed, **{k: v for k, v in (extra or {}).items()
+                                                     if k in ("eta_u", "eta_p", "omega0")})
+    if variant == 3:
+        K0, prec = h.hoamg_device(cfg)
+    else:
+        K0, prec = h.uzawa_device(cfg)
+    return c, ref, h, K0, prec, cfg
+
+
+@pytest.mark.parametrize("variant,n,sv", [(3, 16, False), (3, 32, False), (4, 16, False),
+                                          (4, 32, False), (4, 8, True)])
+def test_hoamg_uzawa_match_reference(S, variant, n, sv):
+    # HoAmgPreconditioner / UzawaPreconditioner (preconditioner.cpp:155-218)
+    c, ref, h, K0, prec, cfg = _prec_pair(S, n, variant, sv)
+    r = O.splitmix64_uniform(c.n0)
+    assert rel_inf(prec.apply(r), ref.apply(r)) <= 1e-9
+    x_ref, rep_ref = ref.solve(c.rhs())
+    x, rep = S.solve_stokes(K0, c.rhs(), prec, cfg)
+    assert rep.converged == rep_ref["converged"]
+    assert abs(rep.iterations - rep_ref["iterations"]) <= 1
+    if rep_ref["converged"]:
+        assert rep.final_relative_residual <= cfg.tol
+        assert rel_inf(x, x_ref) <= 1e-6
+    # the C++ drop-in (gpu::HoAmgPreconditioner / gpu::UzawaPreconditioner)
+    xd, repd = h.solve_dropin(variant=variant, nu=1, restart=30, tol=1e-8, max_iters=500)
+    assert abs(repd["iterations"] - rep_ref["iterations"]) <= 1
+
+
+def test_hoamg_refused_on_sv(S):
+    from paper_2306_06795_b200.cases import HostCase
+    c = O.RefCase.build("cavity", True, "structured", 8)
+    with pytest.raises(O.OracleError):
+        O.RefPrec(c, dict(variant=3, enclosed_flow=True))
+    h = HostCase("cavity", True, "structured", 8)
+    with pytest.raises(S.UnsupportedDiscretization):
+        h.hoamg_device(S.SolverConfig(variant=3, enclosed_flow=True))
+    K0, prec = h.hoamg_device(S.SolverConfig(variant=3, enclosed_flow=True, allow_sv_hoamg=True))
+    assert prec.apply(np.ones(h.n0)).shape == (h.n0,)
