@@ -58,6 +58,9 @@ const char* sag_last_error(void);
 /* Creates a context on CUDA device `device` (fails with SAG_CUDA_ERROR if it
  * is not an sm_100 part). No reference analogue (the reference is host-only). */
 int sag_create(int device, sag_ctx** out);
+/* The same on a caller-owned CUDA stream (cudaStream_t passed as void*), e.g.
+ * a framework's stream: libsag launches on it and never destroys it. */
+int sag_create_on_stream(int device, void* stream, sag_ctx** out);
 int sag_destroy(sag_ctx* ctx);
 int sag_synchronize(sag_ctx* ctx);
 /* Device buffers for callers that keep vectors resident (bench, pipelines). */

@@ -123,6 +123,7 @@ class sag_level_desc(C.Structure):
 SIGNATURES = {
     "sag_last_error": (C.c_char_p, []),
     "sag_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+    "sag_create_on_stream": (C.c_int, [C.c_int, vp, C.POINTER(vp)]),
     "sag_destroy": (C.c_int, [vp]),
     "sag_synchronize": (C.c_int, [vp]),
     "sag_alloc": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
@@ -245,9 +246,14 @@ def _ints(a):
 class Context:
     """One CUDA device + stream + workspaces (no reference analogue)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, stream: int = None):
+        """``stream``: a caller-owned cudaStream_t (e.g. ``torch.cuda.Stream().cuda_stream``)
+        to launch on; libsag then never destroys it (sag_create_on_stream)."""
         h = vp()
-        _check(lib().sag_create(device, C.byref(h)))
+        if stream is None:
+            _check(lib().sag_create(device, C.byref(h)))
+        else:
+            _check(lib().sag_create_on_stream(device, C.c_void_p(stream), C.byref(h)))
         self.h = h
         self.device = device
 

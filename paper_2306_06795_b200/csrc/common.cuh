@@ -92,6 +92,7 @@ struct Ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
+  bool own_stream = true;  // false: the stream belongs to the caller (sag_create_on_stream)
   long long launches = 0;
   DevBuf<double> partials;   // kMaxRedGrid * 2 (two independent sums per kernel)
   DevBuf<unsigned> ticket;   // reduction tickets

@@ -919,7 +919,19 @@ extern "C" {
 
 const char* sag_last_error(void) { return g_last_error.c_str(); }
 
-int sag_create(int device, sag_ctx** out) {
+static int create_ctx(int device, cudaStream_t stream, sag_ctx** out);
+
+int sag_create(int device, sag_ctx** out) { return create_ctx(device, nullptr, out); }
+
+int sag_create_on_stream(int device, void* stream, sag_ctx** out) {
+  if (!stream) {
+    sag::set_last_error("sag_create_on_stream: null stream");
+    return SAG_INVALID_ARGUMENT;
+  }
+  return create_ctx(device, static_cast<cudaStream_t>(stream), out);
+}
+
+static int create_ctx(int device, cudaStream_t stream, sag_ctx** out) {
   return guard([&] {
     NOTNULL(out);
     *out = nullptr;
@@ -934,7 +946,12 @@ int sag_create(int device, sag_ctx** out) {
     auto* h = new sag_ctx;
     h->c.device = device;
     h->c.num_sms = prop.multiProcessorCount;
-    SAG_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+    if (stream) {
+      h->c.stream = stream;
+      h->c.own_stream = false;
+    } else {
+      SAG_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+    }
     h->c.partials.alloc(sag::kMaxRedGrid * 2);
     h->c.ticket.alloc(64);
     SAG_CUDA(cudaMemset(h->c.ticket.p, 0, sizeof(unsigned) * 64));
@@ -948,7 +965,7 @@ int sag_destroy(sag_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
-    cudaStreamDestroy(ctx->c.stream);
+    if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });
 }
