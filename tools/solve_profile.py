@@ -32,9 +32,9 @@ def main():
         case = bench.host_case(conf)
     else:
         case = HostCase("cavity", False, "structured", n_mesh)
-    ctx = S.Context(0)
     dev = torch.device("cuda", 0)
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+    stream = torch.cuda.Stream(device=dev)  # torch-owned: libsag never destroys it
+    ctx = S.Context(0, stream=stream.cuda_stream)
     cfg = S.SolverConfig(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
                          enclosed_flow=case.enclosed, eta_u=conf.get("eta_u", 1.0),
                          eta_p=conf.get("eta_p", 1.0), omega0=conf.get("omega0", 1.0))

@@ -33,9 +33,9 @@ def main():
     t0 = time.time()
     case = HostCase("cavity", False, "structured", n_mesh)
     k0 = case.k0()
-    ctx = S.Context(0)
     dev = torch.device("cuda", 0)
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=dev)
+    stream = torch.cuda.Stream(device=dev)  # torch-owned: libsag never destroys it
+    ctx = S.Context(0, stream=stream.cuda_stream)
     n = k0.nrows
     x = torch.from_numpy(splitmix64_uniform(n)).to(dev)
     y = torch.empty_like(x)

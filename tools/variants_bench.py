@@ -33,8 +33,8 @@ def main():
     t0 = time.perf_counter()
     case = bench.host_case(conf)
     setup = time.perf_counter() - t0
-    ctx = S.Context(0)
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr(), device=torch.device("cuda", 0))
+    stream = torch.cuda.Stream(device=torch.device("cuda", 0))
+    ctx = S.Context(0, stream=stream.cuda_stream)
     rhs = case.rhs()
     print(json.dumps({"config": conf["workload"], "n0": case.n0, "host_setup_s": setup}),
           flush=True)
