@@ -80,6 +80,7 @@ struct Vanka {
   long long nslots = 0;
   DevBuf<double> out;     // per-patch local results (nslots)
   DevBuf<double> w;       // PoU weights (n)
+  bool w_ext = false;     // w set by sag_vanka_set_weights (else 1/multiplicity on the fly)
   DevBuf<int> dof_ptr;    // n + 1
   DevBuf<int> dof_slot;   // nslots
   long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;

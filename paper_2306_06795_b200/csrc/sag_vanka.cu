@@ -1161,6 +1161,9 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
 // Owner-computes scatter-add: delta_d = sum over d's slots (ascending patch
 // order) of w_d * x_slot (vanka.cpp:179-181); with xadd: x_d += omega*delta_d
 // (vanka.cpp:195).
+// w == nullptr: w_d = 1 / multiplicity computed here -- the same IEEE
+// division as weights_kernel (vanka.cpp:67-73), one HBM stream fewer;
+// stored weights only after sag_vanka_set_weights (global partition of unity).
 __global__ void vanka_gather_kernel(int n, const int* __restrict__ dof_ptr,
                                     const int* __restrict__ dof_slot,
                                     const double* __restrict__ out, const double* __restrict__ w,
@@ -1169,9 +1172,9 @@ __global__ void vanka_gather_kernel(int n, const int* __restrict__ dof_ptr,
   if (gate && *gate) return;
   constexpr int U = 8;  // multiplicities up to U in one pass (K0/ISO0: <= 7)
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
-    const double wd = __ldg(w + d);
     const double xo = xadd ? xadd[d] : 0.0;
     const int s0 = __ldg(dof_ptr + d), s1 = __ldg(dof_ptr + d + 1);
+    const double wd = w ? __ldg(w + d) : (s1 > s0 ? 1.0 / (double)(s1 - s0) : 0.0);
     double acc = 0.0;
     for (int sb = s0; sb < s1; sb += U) {
       // all slot ids, then all values, then the ordered sum: two dependent
@@ -1580,9 +1583,9 @@ static void launch_patch_any(Ctx& c, const Vanka& f, const double* r, const int*
 
 void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta, const int* gate) {
   launch_patch_any(c, f, r, gate);
-  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(f.n, f.dof_ptr.p, f.dof_slot.p,
-                                                              f.out.p, f.w.p, delta, nullptr, 1.0,
-                                                              gate);
+  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(
+      f.n, f.dof_ptr.p, f.dof_slot.p, f.out.p, f.w_ext ? f.w.p : nullptr, delta, nullptr, 1.0,
+      gate);
   SAG_LAUNCHED(c);
 }
 
@@ -1590,18 +1593,18 @@ void vanka_apply_stage(Ctx& c, const Vanka& f, const double* r, double* delta, i
   if (stage == 1) {
     launch_patch_any(c, f, r, nullptr);
   } else {
-    vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(f.n, f.dof_ptr.p, f.dof_slot.p,
-                                                                f.out.p, f.w.p, delta, nullptr,
-                                                                1.0, nullptr);
+    vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(
+        f.n, f.dof_ptr.p, f.dof_slot.p, f.out.p, f.w_ext ? f.w.p : nullptr, delta, nullptr, 1.0,
+        nullptr);
     SAG_LAUNCHED(c);
   }
 }
 
 void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega) {
   launch_patch_any(c, f, r, nullptr);
-  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(f.n, f.dof_ptr.p, f.dof_slot.p,
-                                                              f.out.p, f.w.p, nullptr, x, omega,
-                                                              nullptr);
+  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(
+      f.n, f.dof_ptr.p, f.dof_slot.p, f.out.p, f.w_ext ? f.w.p : nullptr, nullptr, x, omega,
+      nullptr);
   SAG_LAUNCHED(c);
 }
 
@@ -1792,6 +1795,7 @@ int sag_vanka_set_weights(sag_ctx* ctx, sag_vanka* f, const double* weights) {
     SAG_CUDA(cudaMemcpyAsync(f->f.w.p, weights, sizeof(double) * f->f.n, cudaMemcpyDefault,
                              ctx->c.stream));
     SAG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    f->f.w_ext = true;
   });
 }
 
