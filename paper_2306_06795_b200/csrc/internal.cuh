@@ -76,6 +76,13 @@ struct Vanka {
   DevBuf<unsigned char> blob;
   DevBuf<long long> off;  // npatch + 1, bytes
   int slot_bytes = 0;     // max blob bytes
+  // blob size classes (rows per lane R), stored contiguously: patches
+  // [k0, k1) of the blob order, max blob bytes of the class
+  struct RClass {
+    int R, k0, k1;
+    long long slot_bytes;
+  };
+  std::vector<RClass> rclasses;
   int max_dim = 0, max_nv = 0, max_np = 0;
   long long nslots = 0;
   DevBuf<double> out;     // per-patch local results (nslots)

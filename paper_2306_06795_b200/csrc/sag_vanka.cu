@@ -643,6 +643,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   };
   f->h_dbase.assign(np_, 0);
   f->h_ibase.assign(np_, 0);
+  std::vector<long long> h_hoff;  // blob byte offset per patch id
   std::vector<int> sbase(std::max(np_, 1), 0);
   long long slots = 0;
   f->tpp = sym && p.max_dim <= kTppMaxDim && p.max_np <= 4 && np_ > 0 &&
@@ -712,15 +713,39 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     SAG_CUDA(cudaMemsetAsync(f->I.p, 0, sizeof(int) * f->I.n, c.stream));
     f->blob_bytes = 8 * doff + 4 * ioff;
   } else {
+    // size classes: the rows per lane the apply needs (paired: m + np, else
+    // max(nx, ny)) -> R = ceil(rows / 32). Blobs are stored class by class
+    // (stable in patch order), so each class is one contiguous launch with
+    // its own stage size; slots stay in patch order.
+    auto r_of = [&](int i) {
+      const int x = f->h_nx[i], y = f->h_nv[i] - x;
+      const int rows = std::max(x, y) + (f->pairs ? f->h_np[i] : 0);
+      return std::max(1, (rows + 31) / 32);
+    };
+    std::vector<int> order(np_);
+    for (int i = 0; i < np_; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return r_of(a) < r_of(b); });
     std::vector<long long> off(np_ + 1, 0);
+    h_hoff.assign(np_, 0);
     int maxbytes = 16;
-    for (int i = 0; i < np_; ++i) {
+    f->rclasses.clear();
+    for (int q = 0; q < np_; ++q) {
+      const int i = order[q];
       long long bytes = 16 + 8 * ndbl(i) + 4 * (f->h_nv[i] + f->h_np[i]);
       bytes = (bytes + 15) / 16 * 16;
-      off[i + 1] = off[i] + bytes;
+      h_hoff[i] = off[q];
+      off[q + 1] = off[q] + bytes;
       maxbytes = std::max<long long>(maxbytes, bytes);
-      f->h_dbase[i] = (off[i] + 16) / 8;
-      f->h_ibase[i] = (off[i] + 16 + 8 * ndbl(i)) / 4;
+      f->h_dbase[i] = (off[q] + 16) / 8;
+      f->h_ibase[i] = (off[q] + 16 + 8 * ndbl(i)) / 4;
+      const int R = r_of(i);
+      if (f->rclasses.empty() || f->rclasses.back().R != R)
+        f->rclasses.push_back({R, q, q + 1, 16});
+      auto& cl = f->rclasses.back();
+      cl.k1 = q + 1;
+      cl.slot_bytes = std::max<long long>(cl.slot_bytes, bytes);
+    }
+    for (int i = 0; i < np_; ++i) {
       sbase[i] = (int)slots;
       slots += f->h_nv[i] + f->h_np[i];
       SAG_REQUIRE(slots < (1LL << 31), SAG_DIMENSION_MISMATCH, "factor_patches: too many slots");
@@ -790,6 +815,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     SAG_CUDA(cudaMemcpyAsync(err.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
     const int blocks = std::max(1, std::min((np_ + warps - 1) / warps, c.num_sms * 8));
     FactorOut fo;
+    DevBuf<long long> dhoff;
     fo.es = es;
     fo.dbase = ddbase.p;
     fo.ibase = dibase.p;
@@ -802,7 +828,11 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
       fo.D = reinterpret_cast<double*>(f->blob.p);
       fo.I = reinterpret_cast<int*>(f->blob.p);
       fo.blob = f->blob.p;
-      fo.hoff = f->off.p;
+      dhoff.alloc(std::max(np_, 1));
+      if (np_)
+        SAG_CUDA(cudaMemcpyAsync(dhoff.p, h_hoff.data(), sizeof(long long) * np_,
+                                 cudaMemcpyHostToDevice, c.stream));
+      fo.hoff = dhoff.p;
       fo.pairs = f->pairs ? 1 : 0;
     }
     factor_kernel<<<blocks, warps * 32, smem, c.stream>>>(
@@ -1514,7 +1544,7 @@ struct ApplyCfg {
 // gathered, >= 1 landing), as many warps as shared memory allows (up to 8
 // per CTA, several CTAs per SM), a persistent grid of occupancy x #SMs.
 template <int R, bool SYM, int NPM>
-static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
+static ApplyCfg apply_cfg(Ctx& c, const Vanka& f, int npatch, int slot_bytes) {
   static thread_local int configured_smem[2][4][2] = {};
   int& configured = configured_smem[SYM][R - 1][NPM == 1 ? 0 : 1];
   ApplyCfg a;
@@ -1524,7 +1554,7 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   a.nstage = std::max(2, env_int("SAG_VANKA_STAGES", 2));
   a.sb_len = f.max_nv + f.max_np + f.max_dim + 2;
   a.sb_len = (a.sb_len + 1) / 2 * 2;
-  const int per_warp = a.nstage * f.slot_bytes + ((a.nstage + 1) & ~1) * 8 + 2 * a.sb_len * 8;
+  const int per_warp = a.nstage * slot_bytes + ((a.nstage + 1) & ~1) * 8 + 2 * a.sb_len * 8;
   const int cta_budget = env_int("SAG_VANKA_CTA_SMEM", 60000);
   a.warps = std::max(1, std::min(env_int("SAG_VANKA_WARPS", 8), cta_budget / per_warp));
   if (a.warps * per_warp > 220 * 1024) a.warps = std::max(1, (220 * 1024) / per_warp);
@@ -1538,31 +1568,37 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f) {
   int occ = 0;
   SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, a.warps * 32, a.smem));
   occ = std::max(occ, 1);
-  const long long need = (f.npatch + a.warps - 1) / a.warps;
+  const long long need = (npatch + a.warps - 1) / a.warps;
   a.blocks = (int)std::max(1LL, std::min<long long>(need, (long long)occ * c.num_sms));
   return a;
 }
 
+// One size class: patches [k0, k1) of the blob order (contiguous blobs).
 template <int R, bool SYM, int NPM>
-static void launch_patch(Ctx& c, const Vanka& f, const double* r, const int* gate) {
+static void launch_patch(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const double* r,
+                         const int* gate) {
   SAG_REQUIRE(!f.pairs || (R <= 2 && SYM), SAG_ERROR,
               "apply_vanka: paired factor blobs need a symmetric R <= 2 kernel");
-  const ApplyCfg a = apply_cfg<R, SYM, NPM>(c, f);
+  const int npatch = cl.k1 - cl.k0;
+  const ApplyCfg a = apply_cfg<R, SYM, NPM>(c, f, npatch, (int)cl.slot_bytes);
   vanka_patch_kernel<R, SYM, NPM><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
-      f.npatch, f.blob.p, f.off.p, f.slot_bytes, a.nstage, a.sb_len, f.pairs ? 1 : 0, r, f.out.p,
-      gate);
+      npatch, f.blob.p, f.off.p + cl.k0, (int)cl.slot_bytes, a.nstage, a.sb_len,
+      f.pairs ? 1 : 0, r, f.out.p, gate);
   SAG_LAUNCHED(c);
 }
 
 template <bool SYM, int NPM>
 static void launch_patch_r(Ctx& c, const Vanka& f, const double* r, const int* gate) {
-  // rows per lane: matrix rows, or (paired levels) matrix + b_hat rows
-  const int R = f.pairs ? (f.pair_rows + 31) / 32 : (f.max_dim + 31) / 32;
-  switch (R) {
-    case 1: launch_patch<1, SYM, NPM>(c, f, r, gate); break;
-    case 2: launch_patch<2, SYM, NPM>(c, f, r, gate); break;
-    case 3: launch_patch<3, SYM, NPM>(c, f, r, gate); break;
-    default: launch_patch<4, SYM, NPM>(c, f, r, gate); break;
+  // one launch per size class (rows per lane: matrix rows, or on paired
+  // levels matrix + b_hat rows)
+  for (const auto& cl : f.rclasses) {
+    SAG_REQUIRE(cl.R <= 4, SAG_ERROR, "apply_vanka: patch with more than 128 rows");
+    switch (cl.R) {
+      case 1: launch_patch<1, SYM, NPM>(c, f, cl, r, gate); break;
+      case 2: launch_patch<2, SYM, NPM>(c, f, cl, r, gate); break;
+      case 3: launch_patch<3, SYM, NPM>(c, f, cl, r, gate); break;
+      default: launch_patch<4, SYM, NPM>(c, f, cl, r, gate); break;
+    }
   }
 }
 
