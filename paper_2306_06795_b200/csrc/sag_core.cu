@@ -483,9 +483,20 @@ __global__ void __launch_bounds__(kRedBlock) dot_kernel(int n, const double* __r
                                                         const int* gate, double* partials,
                                                         unsigned* ticket) {
   if (gate && *gate) return;
+  // four grid strides per pass: eight independent loads in flight per thread
+  // (these vectors are streamed once; one load per trip leaves HBM idle)
+  const int st = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    s = fma(a[i], b[i], s);
+  for (; i + 3 * st < n; i += 4 * st) {
+    const double a0 = a[i], a1 = a[i + st], a2 = a[i + 2 * st], a3 = a[i + 3 * st];
+    const double b0 = b[i], b1 = b[i + st], b2 = b[i + 2 * st], b3 = b[i + 3 * st];
+    s = fma(a0, b0, s);
+    s = fma(a1, b1, s);
+    s = fma(a2, b2, s);
+    s = fma(a3, b3, s);
+  }
+  for (; i < n; i += st) s = fma(a[i], b[i], s);
   reduce_finish(s, fin, partials, ticket);
 }
 
@@ -514,8 +525,27 @@ __global__ void __launch_bounds__(kRedBlock) mgs_kernel(int n, double* __restric
                                                         double* partials, unsigned* ticket) {
   if (gate && *gate) return;
   const double hh = vprev ? *h : 0.0;
+  const int st = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  if (vprev) {
+    for (; i + 3 * st < n; i += 4 * st) {
+      double wv[4], pv[4], nv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        wv[u] = w[i + u * st];
+        pv[u] = vprev[i + u * st];
+        nv[u] = vnext[i + u * st];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        wv[u] = fma(-hh, pv[u], wv[u]);
+        w[i + u * st] = wv[u];
+        s = fma(wv[u], nv[u], s);
+      }
+    }
+  }
+  for (; i < n; i += st) {
     double wi = w[i];
     if (vprev) {
       wi = fma(-hh, vprev[i], wi);
@@ -536,8 +566,24 @@ __global__ void __launch_bounds__(kRedBlock) mgs_last_kernel(int n, double* __re
                                                              double* partials, unsigned* ticket) {
   if (gate && *gate) return;
   const double hh = *h;
+  const int st = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (; i + 3 * st < n; i += 4 * st) {
+    double wv[4], vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      wv[u] = w[i + u * st];
+      vv[u] = v[i + u * st];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double wi = fma(-hh, vv[u], wv[u]);
+      if (write_w) w[i + u * st] = wi;
+      s = fma(wi, wi, s);
+    }
+  }
+  for (; i < n; i += st) {
     const double wi = fma(-hh, v[i], w[i]);
     if (write_w) w[i] = wi;
     s = fma(wi, wi, s);
@@ -580,6 +626,7 @@ __global__ void update_kernel(int n, double* __restrict__ x, const double* __res
   const double* y = ks_y(const_cast<KState*>(st));
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     double corr = 0.0;
+#pragma unroll 4
     for (int i = 0; i < j; ++i) corr = fma(y[i], Z[(size_t)i * zs + k], corr);
     x[k] = store ? corr : x[k] + corr;
   }
@@ -654,14 +701,27 @@ static int ew_grid(Ctx& c, long long n) {
   return (int)std::max(1LL, std::min(g, (long long)c.num_sms * 16));
 }
 
+// Reduction grids: red_grid(n), but never more blocks than are resident at
+// once -- a partial second wave of a grid-stride reduction idles most SMs at
+// the tail (as measured for the fused SpMV reductions).
+template <class K>
+static int red_grid_fit(Ctx& c, K kern, long long n) {
+  static thread_local int occ = 0;
+  if (!occ) {
+    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRedBlock, 0));
+    occ = std::max(occ, 1);
+  }
+  return std::max(1, std::min(red_grid(n), occ * c.num_sms));
+}
+
 void launch_dot(Ctx& c, int n, const double* a, const double* b, const Fin& fin,
                 const int* gate) {
-  dot_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, a, b, fin, gate, c.partials.p,
+  dot_kernel<<<red_grid_fit(c, dot_kernel, n), kRedBlock, 0, c.stream>>>(n, a, b, fin, gate, c.partials.p,
                                                       c.ticket.p);
   SAG_LAUNCHED(c);
 }
 void launch_ssq(Ctx& c, int n, const double* a, const Fin& fin, const int* gate) {
-  dot_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, a, a, fin, gate, c.partials.p,
+  dot_kernel<<<red_grid_fit(c, dot_kernel, n), kRedBlock, 0, c.stream>>>(n, a, a, fin, gate, c.partials.p,
                                                       c.ticket.p);
   SAG_LAUNCHED(c);
 }
@@ -676,13 +736,13 @@ void launch_div(Ctx& c, int n, const double* x, const double* s, double* y, cons
 }
 void launch_mgs(Ctx& c, int n, double* w, const double* vprev, const double* h,
                 const double* vnext, const Fin& fin, const int* gate) {
-  mgs_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, w, vprev, h, vnext, fin, gate,
+  mgs_kernel<<<red_grid_fit(c, mgs_kernel, n), kRedBlock, 0, c.stream>>>(n, w, vprev, h, vnext, fin, gate,
                                                       c.partials.p, c.ticket.p);
   SAG_LAUNCHED(c);
 }
 void launch_mgs_last(Ctx& c, int n, double* w, const double* v, const double* h, const Fin& fin,
                      const int* gate, bool write_w) {
-  mgs_last_kernel<<<red_grid(n), kRedBlock, 0, c.stream>>>(n, w, v, h, fin, gate, write_w ? 1 : 0,
+  mgs_last_kernel<<<red_grid_fit(c, mgs_last_kernel, n), kRedBlock, 0, c.stream>>>(n, w, v, h, fin, gate, write_w ? 1 : 0,
                                                            c.partials.p, c.ticket.p);
   SAG_LAUNCHED(c);
 }
