@@ -509,6 +509,23 @@ __global__ void __launch_bounds__(kRedBlock) sum_kernel(int n, const double* __r
   reduce_finish(s, fin, partials, ticket);
 }
 
+// Elementwise pass with four grid strides per trip: all loads of a trip are
+// issued before any use (load(i) returns the operands, store(i, ops) writes),
+// so each thread keeps several independent requests in flight.
+template <class Load, class Store>
+__device__ __forceinline__ void ew4(int n, Load load, Store store) {
+  const int st = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * st < n; i += 4 * st) {
+    const auto o0 = load(i), o1 = load(i + st), o2 = load(i + 2 * st), o3 = load(i + 3 * st);
+    store(i, o0);
+    store(i + st, o1);
+    store(i + 2 * st, o2);
+    store(i + 3 * st, o3);
+  }
+  for (; i < n; i += st) store(i, load(i));
+}
+
 __global__ void div_kernel(int n, const double* __restrict__ x, const double* s,
                            double* __restrict__ y, const int* gate, const int* gate2) {
   if ((gate && *gate) || (gate2 && *gate2)) return;
@@ -599,10 +616,11 @@ __global__ void lin_resid_kernel(int n, int n_u, double eu, double ep,
                                  const KState* st, double* __restrict__ r) {
   const bool step = st->jeff > 0;
   const double y0 = step ? ks_y(const_cast<KState*>(st))[0] : 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const double v = step ? fma(-y0, w[i], b[i]) : b[i];
-    r[i] = (i < n_u ? eu : ep) * v;
-  }
+  ew4(n, [&](int i) { return make_double2(b[i], step ? w[i] : 0.0); },
+      [&](int i, double2 v) {
+        const double t = step ? fma(-y0, v.y, v.x) : v.x;
+        r[i] = (i < n_u ? eu : ep) * t;
+      });
 }
 
 // krylov.cpp:102-107, one thread (j <= restart)
@@ -668,8 +686,7 @@ __global__ void kinit_kernel(KState* st, int m, double tol, double bd, int hist_
 }
 
 __global__ void copy_kernel(int n, const double* __restrict__ x, double* __restrict__ y) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    y[i] = x[i];
+  ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = v; });
 }
 __global__ void zero_kernel(int n, double* __restrict__ y) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -678,17 +695,15 @@ __global__ void zero_kernel(int n, double* __restrict__ y) {
 __global__ void project_kernel(int n, int n_u, const double* __restrict__ x, const double* mean,
                                double* __restrict__ y) {
   const double mu = *mean;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    y[i] = i < n_u ? x[i] : x[i] - mu;
+  ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = i < n_u ? v : v - mu; });
 }
 __global__ void eta_kernel(int n, int n_u, double eu, double ep, const double* __restrict__ x,
                            double* __restrict__ y) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    y[i] = (i < n_u ? eu : ep) * x[i];
+  ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = (i < n_u ? eu : ep) * v; });
 }
 __global__ void add_kernel(int n, double* __restrict__ x, const double* __restrict__ y) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    x[i] = x[i] + y[i];
+  ew4(n, [&](int i) { return make_double2(x[i], y[i]); },
+      [&](int i, double2 v) { x[i] = v.x + v.y; });
 }
 __global__ void axpy_kernel(int n, double* __restrict__ x, double omega,
                             const double* __restrict__ d) {
