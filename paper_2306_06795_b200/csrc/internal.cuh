@@ -81,6 +81,7 @@ struct Vanka {
   struct RClass {
     int R, k0, k1;
     long long slot_bytes;
+    int lpp;  // lanes per patch: 32, or 16 / 8 for the sub-warp kernel
   };
   std::vector<RClass> rclasses;
   int max_dim = 0, max_nv = 0, max_np = 0;

@@ -717,10 +717,24 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     // max(nx, ny)) -> R = ceil(rows / 32). Blobs are stored class by class
     // (stable in patch order), so each class is one contiguous launch with
     // its own stage size; slots stay in patch order.
-    auto r_of = [&](int i) {
+    // class key 4 R + (lanes per patch: 32 / 16 / 8 -> 0 / 1 / 2); small
+    // paired patches go to the sub-warp kernel (several patches per warp)
+    const bool subwarp = f->pairs && env_int("SAG_VANKA_SUBWARP", 1) != 0;
+    auto key_of = [&](int i) {
       const int x = f->h_nx[i], y = f->h_nv[i] - x;
       const int rows = std::max(x, y) + (f->pairs ? f->h_np[i] : 0);
-      return std::max(1, (rows + 31) / 32);
+      const int R = std::max(1, (rows + 31) / 32);
+      const int l = !subwarp ? 0 : rows <= 8 ? 2 : rows <= 16 ? 1 : 0;
+      return 4 * R + l;
+    };
+    // a sub-warp class only pays off when it is a large share of the level
+    // (a separate launch with its own grid): stragglers join the 32-lane class
+    int nkey[16] = {0};
+    for (int i = 0; i < np_; ++i) ++nkey[std::min(key_of(i), 15)];
+    const int min_sub = std::max(4096, np_ / 8);
+    auto r_of = [&](int i) {
+      const int k = key_of(i);
+      return (k % 4 != 0 && nkey[std::min(k, 15)] < min_sub) ? 4 * (k / 4) : k;
     };
     std::vector<int> order(np_);
     for (int i = 0; i < np_; ++i) order[i] = i;
@@ -738,9 +752,9 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
       maxbytes = std::max<long long>(maxbytes, bytes);
       f->h_dbase[i] = (off[q] + 16) / 8;
       f->h_ibase[i] = (off[q] + 16 + 8 * ndbl(i)) / 4;
-      const int R = r_of(i);
-      if (f->rclasses.empty() || f->rclasses.back().R != R)
-        f->rclasses.push_back({R, q, q + 1, 16});
+      const int key = r_of(i), R = key / 4, lpp = 32 >> (key % 4);
+      if (f->rclasses.empty() || f->rclasses.back().R != R || f->rclasses.back().lpp != lpp)
+        f->rclasses.push_back({R, q, q + 1, 16, lpp});
       auto& cl = f->rclasses.back();
       cl.k1 = q + 1;
       cl.slot_bytes = std::max<long long>(cl.slot_bytes, bytes);
@@ -1188,6 +1202,180 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
   }
 }
 
+// Sub-warp paired Vanka for small patches (m + np <= LPP < 32): the warp
+// solves P = 32 / LPP consecutive patches at once, lane group g = lane / LPP
+// on patch q P + g, with the row / b_hat-row mapping of the paired path of
+// vanka_patch_kernel inside each group. The P blobs of a group are adjacent
+// in the class-ordered blob array and arrive with one cp.async.bulk; the
+// per-patch overhead (header, gather, epilogue, refill) is shared by P
+// patches. Used for the element-triple patches of SV fine levels (m + np = 9).
+template <int LPP, int NPM>
+__global__ void __launch_bounds__(256) vanka_subwarp_kernel(
+    int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
+    int slot_bytes, int nstage, int sb_len, const double* __restrict__ r,
+    double* __restrict__ out, const int* gate) {
+  if (gate && *gate) return;
+  constexpr int P = 32 / LPP;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane / LPP, gl = lane % LPP;
+  const int nbar = (nstage + 1) & ~1;
+  const size_t stage_bytes = (size_t)P * slot_bytes;
+  unsigned char* ring = smem + (size_t)wib * nstage * stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)warps * nstage * stage_bytes) +
+                   (size_t)wib * nbar;
+  double* sbuf = reinterpret_cast<double*>(smem + (size_t)warps * nstage * stage_bytes +
+                                           (size_t)warps * nbar * 8) +
+                 (size_t)wib * 2 * P * sb_len;
+  const int ngroups = (npatch + P - 1) / P;
+  const int first = blockIdx.x * warps + wib;
+  const int stride = gridDim.x * warps;
+  const uint64_t policy = evict_first_policy();
+  auto grp_end = [&](int q) { return q * P + P < npatch ? q * P + P : npatch; };
+  auto issue_at = [&](int s, long long o0, long long o1) {
+    const unsigned bytes = (unsigned)(o1 - o0);
+    mbar_expect_tx(bars + s, bytes);
+    bulk_copy_hint(ring + (size_t)s * stage_bytes, blob + o0, bytes, bars + s, policy);
+  };
+  // this group's patch of group q in stage s (valid when q P + g < npatch)
+  auto view_at = [&](int s, long long base, long long own) {
+    return patch_view<true>(ring + (size_t)s * stage_bytes + (size_t)(own - base), true);
+  };
+  auto gather_to = [&](const PatchView& w, double* dst) {
+    // (x_j, y_j) pairs over j < m, padding zeroed, pressure at 2m
+    for (int i = gl; i < w.nv + w.np; i += LPP) {
+      const int d = i < w.nx ? 2 * i : (i < w.nv ? 2 * (i - w.nx) + 1 : 2 * w.m + (i - w.nv));
+      dst[d] = __ldg(r + w.idx[i]);
+    }
+    if (w.nx != w.ny)
+      for (int j = gl; j < w.m; j += LPP) {
+        if (j >= w.nx) dst[2 * j] = 0.0;
+        if (j >= w.ny) dst[2 * j + 1] = 0.0;
+      }
+  };
+  if (lane == 0) {
+    for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
+    mbar_init_fence();
+    for (int s = 0; s < nstage; ++s) {
+      const int q = first + s * stride;
+      if (q < ngroups) issue_at(s, off[q * P], off[grp_end(q)]);
+    }
+  }
+  __syncwarp();
+  unsigned phase = 0;
+  // offsets of the current group: stage base and this group's blob
+  long long cb = 0, co = 0;
+  if (first < ngroups) {
+    cb = __ldg(off + first * P);
+    co = __ldg(off + min(first * P + g, npatch));
+    mbar_wait(bars, 0);
+    phase ^= 1u;
+    if (first * P + g < npatch) gather_to(view_at(0, cb, co), sbuf + g * sb_len);
+  }
+  __syncwarp();
+  const int cs0 = gl * (gl + 1) / 2;
+  int stage = 0, it = 0;
+  for (int q = first; q < ngroups; q += stride, ++it) {
+    const int qr = q + nstage * stride;
+    long long ro0 = 0, ro1 = 0;
+    if (lane == 0 && qr < ngroups) {
+      ro0 = __ldg(off + qr * P);
+      ro1 = __ldg(off + grp_end(qr));
+    }
+    const int qn = q + stride;
+    long long nb = 0, no = 0;
+    if (qn < ngroups) {
+      nb = __ldg(off + qn * P);
+      no = __ldg(off + min(qn * P + g, npatch));
+    }
+    const bool valid = q * P + g < npatch;
+    const PatchView v = view_at(stage, cb, co);
+    const double* sb = sbuf + ((it & 1) * P + g) * sb_len;
+    const int sn = stage + 1 == nstage ? 0 : stage + 1;
+    double gv[2];
+    int gd[2];
+    PatchView w{};
+    bool wvalid = false;
+    if (qn < ngroups) {
+      mbar_wait(bars + sn, (phase >> sn) & 1u);
+      phase ^= 1u << sn;
+      wvalid = qn * P + g < npatch;
+      if (wvalid) w = view_at(sn, nb, no);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = gl + LPP * u;
+        const bool in = wvalid && i < w.nv + w.np;
+        gd[u] = i < w.nx ? 2 * i : (i < w.nv ? 2 * (i - w.nx) + 1 : 2 * w.m + (i - w.nv));
+        gv[u] = in ? __ldg(r + w.idx[i]) : 0.0;
+      }
+    }
+    // the paired solve of vanka_patch_kernel within each group
+    const int mm = valid ? v.m : 0, npp = valid ? (NPM == 1 ? 1 : v.np) : 0;
+    int M = mm;
+#pragma unroll
+    for (int o = LPP; o < 32; o <<= 1) M = max(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const double2* AP = reinterpret_cast<const double2*>(v.Ax);
+    const double2* SB = reinterpret_cast<const double2*>(sb);
+    const int boff = valid ? (int)(reinterpret_cast<const double2*>(v.Bh) - AP) : 0;
+    const bool act = gl < mm + npp;
+    const int cl = gl >= mm ? boff + (gl - mm) * mm : cs0;
+    double tx = 0.0, ty = 0.0;
+    int csj = 0;
+#pragma unroll 4
+    for (int j = 0; j < M; csj += ++j) {
+      const bool col = j < mm;
+      const double2 b = lds_v2_pred(SB + j, col);
+      const double2 a = lds_v2_pred(AP + (gl <= j ? csj + gl : cl + j), col && act);
+      tx = fma(a.x, b.x, tx);
+      ty = fma(a.y, b.y, ty);
+    }
+    double xl = tx + ty;
+    const int ar = min(max(gl - mm, 0), max(npp - 1, 0));
+    if (valid) {
+#pragma unroll
+      for (int e = 0; e < NPM; ++e)
+        if (e < npp) xl = fma(v.Si[ar * npp + e], sb[2 * mm + e], xl);
+      if (gl >= mm && gl < mm + npp) out[v.sbase + v.nv + ar] = xl;
+    }
+    double xp[NPM];
+#pragma unroll
+    for (int e = 0; e < NPM; ++e)
+      xp[e] = __shfl_sync(0xffffffffu, xl, g * LPP + min(mm + e, LPP - 1));
+    if (valid && gl < mm) {
+      const double2* UP = reinterpret_cast<const double2*>(v.U);
+      double ox = tx, oy = ty;
+#pragma unroll
+      for (int e = 0; e < NPM; ++e)
+        if (e < npp) {
+          const double2 u = UP[e * mm + gl];
+          ox = fma(u.x, xp[e], ox);
+          oy = fma(u.y, xp[e], oy);
+        }
+      if (gl < v.nx) out[v.sbase + gl] = ox;
+      if (gl < v.ny) out[v.sbase + v.nx + gl] = oy;
+    }
+    // publish the prefetched r of the next group
+    if (wvalid) {
+      double* sbn = sbuf + (((it + 1) & 1) * P + g) * sb_len;
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (gl + LPP * u < w.nv + w.np) sbn[gd[u]] = gv[u];
+      if (w.nx != w.ny && gl < w.m) {
+        if (gl >= w.nx) sbn[2 * gl] = 0.0;
+        if (gl >= w.ny) sbn[2 * gl + 1] = 0.0;
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && qr < ngroups) {
+      fence_proxy_async();
+      issue_at(stage, ro0, ro1);
+    }
+    stage = sn;
+    cb = nb;
+    co = no;
+  }
+}
+
 // Owner-computes scatter-add: delta_d = sum over d's slots (ascending patch
 // order) of w_d * x_slot (vanka.cpp:179-181); with xadd: x_d += omega*delta_d
 // (vanka.cpp:195).
@@ -1573,6 +1761,38 @@ static ApplyCfg apply_cfg(Ctx& c, const Vanka& f, int npatch, int slot_bytes) {
   return a;
 }
 
+template <int LPP, int NPM>
+static void launch_subwarp(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const double* r,
+                           const int* gate) {
+  static thread_local int configured = 0;
+  constexpr int P = 32 / LPP;
+  const int npatch = cl.k1 - cl.k0;
+  const int nstage = std::max(2, env_int("SAG_VANKA_STAGES", 2));
+  int sb_len = f.max_nv + f.max_np + f.max_dim + 2;
+  sb_len = (sb_len + 1) / 2 * 2;
+  const int per_warp = nstage * P * (int)cl.slot_bytes + ((nstage + 1) & ~1) * 8 + 2 * P * sb_len * 8;
+  const int cta_budget = env_int("SAG_VANKA_CTA_SMEM", 60000);
+  int warps = std::max(1, std::min(env_int("SAG_VANKA_WARPS", 8), cta_budget / per_warp));
+  if (warps * per_warp > 220 * 1024) warps = std::max(1, (220 * 1024) / per_warp);
+  const int smem = warps * per_warp;
+  SAG_REQUIRE(smem <= 227 * 1024, SAG_ERROR, "apply_vanka: patch blobs too large for staging");
+  auto kern = vanka_subwarp_kernel<LPP, NPM>;
+  if (configured < smem) {
+    SAG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = smem;
+  }
+  int occ = 0;
+  SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem));
+  occ = std::max(occ, 1);
+  const long long ngroups = (npatch + P - 1) / P;
+  const int blocks = (int)std::max(1LL, std::min<long long>((ngroups + warps - 1) / warps,
+                                                          (long long)occ * c.num_sms));
+  kern<<<blocks, warps * 32, smem, c.stream>>>(npatch, f.blob.p, f.off.p + cl.k0,
+                                                (int)cl.slot_bytes, nstage, sb_len, r, f.out.p,
+                                                gate);
+  SAG_LAUNCHED(c);
+}
+
 // One size class: patches [k0, k1) of the blob order (contiguous blobs).
 template <int R, bool SYM, int NPM>
 static void launch_patch(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const double* r,
@@ -1593,6 +1813,15 @@ static void launch_patch_r(Ctx& c, const Vanka& f, const double* r, const int* g
   // levels matrix + b_hat rows)
   for (const auto& cl : f.rclasses) {
     SAG_REQUIRE(cl.R <= 4, SAG_ERROR, "apply_vanka: patch with more than 128 rows");
+    if (cl.lpp < 32) {
+      if constexpr (SYM) {
+        if (cl.lpp == 8)
+          launch_subwarp<8, NPM>(c, f, cl, r, gate);
+        else
+          launch_subwarp<16, NPM>(c, f, cl, r, gate);
+        continue;
+      }
+    }
     switch (cl.R) {
       case 1: launch_patch<1, SYM, NPM>(c, f, cl, r, gate); break;
       case 2: launch_patch<2, SYM, NPM>(c, f, cl, r, gate); break;

@@ -209,6 +209,39 @@ def test_apply_vanka_many_patches_per_warp(S, big):
     assert rel_inf(S.apply_vanka(f, r), rv.apply(r)) <= TOL
 
 
+@pytest.mark.parametrize("lo,hi", [(2, 8), (8, 16)])
+def test_apply_vanka_subwarp_classes(S, lo, hi):
+    # >= 4096 small paired patches form their own class and run on the
+    # sub-warp kernel (m + np <= 8: four patches per warp; <= 16: two)
+    rng = np.random.default_rng(11)
+    sizes = [(int(m), int(m)) for m in rng.integers(lo - 1, hi, 9000)]
+    sizes += [(int(a), int(b)) for a, b in rng.integers(max(lo - 2, 1), hi - 1, (500, 2))]
+    rng.shuffle(sizes)
+    k, n_u, lists = _saddle_blocks(rng, sizes)
+    pp = O.Patches(*[np.asarray(a, dtype=np.int32) for a in lists])
+    rv = O.RefVanka.from_patches(k, pp, n_u)
+    K = S.SparseMatrix.from_csr(k.csr())
+    f = S.factor_patches(K, S.Patches.from_lists(*lists), n_u)
+    r = O.splitmix64_uniform(k.csr_shape()[0])
+    assert rel_inf(S.apply_vanka(f, r), rv.apply(r)) <= TOL
+
+
+def test_apply_vanka_sv_subwarp(S):
+    # SV fine level (element triples, m + np = 9): 6144 patches at n = 32 run
+    # on the two-patches-per-warp kernel
+    c, d, k0, levels, _ = ref_case(32, sv=True, cfg=dict(omega0=0.78, eta_p=2.68))
+    rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0, sv_triples=True)
+    K = S.SparseMatrix.from_csr(k0)
+    f = S.factor_patches(K, S.build_patches(K, *d.nxyz0, sv_triples=True),
+                         d.nxyz0[0] + d.nxyz0[1])
+    r = O.splitmix64_uniform(k0.nrows)
+    assert rel_inf(S.apply_vanka(f, r), rv.apply(r)) <= TOL
+    x0 = np.sin(0.1 * np.arange(k0.nrows))
+    want = rv.relax(x0, r, 1, 2, 0.78)
+    got = S.vanka_relax(K, f, x0.copy(), r, 1, 2, 0.78)
+    assert rel_inf(got, want) <= 1e-11
+
+
 def test_singular_patch_raises(S):
     k = O.RefMat.from_triplets(3, 3, [0, 1, 2], [2, 1, 0], [1.0, 1.0, 1.0]).csr()
     K = S.SparseMatrix.from_csr(k)
