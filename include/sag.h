@@ -267,6 +267,41 @@ int sag_solve_stokes_uzawa(sag_ctx* ctx, const sag_matrix* k0, sag_uzawa* u, con
                            double* x, const sag_solver_config* cfg, sag_krylov_report* rep,
                            double* history, int history_cap);
 
+/* ---- partitioned-solve primitives ---------------------------
+ * Building blocks for a caller that row-partitions the solve across ranks
+ * (one process per GPU, paper_2306_06795_b200/dist.py). All pointers are
+ * DEVICE pointers and no call synchronises with the host: scalars stay in
+ * device memory, so a partial reduction, the caller's all-reduce (NCCL on
+ * the same stream) and the axpy that consumes it are stream-ordered.
+ * They restate the vector operations of fgmres (krylov.cpp:42-110), norm2 /
+ * dot (sparse.cpp:217-227) and project_pressure (preconditioner.cpp:235-240)
+ * on a rank's share of the rows. */
+/* out[0] = sum_{i: mask[i] != 0} a_i b_i (mask NULL: all i) -- a rank's
+ * partial of dot / norm2 over the rows it owns (sparse.cpp:217-227). */
+int sag_dot_async(sag_ctx* ctx, int n, const double* a, const double* b,
+                  const unsigned char* mask, double* out);
+/* y = y + sign * s[0] x  (MGS update w -= h_ij v_i, krylov.cpp:66). */
+int sag_axpy_async(sag_ctx* ctx, int n, const double* s, double sign, const double* x, double* y);
+/* y = x / d with d = s[0] or sqrt(s[0])  (v = r / ||r||, krylov.cpp:47-48, :71). */
+int sag_div_async(sag_ctx* ctx, int n, const double* x, const double* s, int take_sqrt, double* y);
+/* y = x - sum[0] / count  (pressure-mean projection, preconditioner.cpp:235-240). */
+int sag_sub_mean_async(sag_ctx* ctx, int n, const double* x, const double* sum, double count,
+                       double* y);
+/* y = a x + b y (a == b == 0: y = 0; b == 0: y = a x; b == 1: y += a x,
+ * krylov.cpp:108-110). */
+int sag_axpby_async(sag_ctx* ctx, int n, double a, const double* x, double b, double* y);
+/* Halo pack / unpack: dst[i] = src[idx[i]]; dst[idx[i]] = src[i] or
+ * dst[idx[i]] += src[i] (add != 0); idx entries unique. */
+int sag_gather_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* dst);
+int sag_scatter_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* dst, int add);
+/* norm_inf (sparse.cpp:229-237): max absolute row sum (host out). */
+int sag_matrix_norm_inf(sag_ctx* ctx, const sag_matrix* m, double* out);
+/* Refactors the coarse dense LU with the enclosed-flow pin
+ * 1e-12 * level0_norm_inf (preconditioner.cpp:49-53) when the caller's
+ * hierarchy starts below the level whose norm the reference uses -- a rank
+ * that holds the agglomerated coarse levels of a partitioned hierarchy. */
+int sag_dc_set_coarse_pin(sag_ctx* ctx, sag_dc* d, double level0_norm_inf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -175,6 +175,16 @@ SIGNATURES = {
     "sag_uzawa_apply": (C.c_int, [vp, vp, vp, vp]),
     "sag_solve_stokes_uzawa": (C.c_int, [vp, vp, vp, vp, vp, C.POINTER(sag_solver_config),
                                          C.POINTER(sag_krylov_report), vp, C.c_int]),
+    # partitioned-solve primitives (device pointers, no host sync)
+    "sag_dot_async": (C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
+    "sag_axpy_async": (C.c_int, [vp, C.c_int, vp, C.c_double, vp, vp]),
+    "sag_div_async": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, vp]),
+    "sag_sub_mean_async": (C.c_int, [vp, C.c_int, vp, vp, C.c_double, vp]),
+    "sag_axpby_async": (C.c_int, [vp, C.c_int, C.c_double, vp, C.c_double, vp]),
+    "sag_gather_async": (C.c_int, [vp, C.c_int, vp, vp, vp]),
+    "sag_scatter_async": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int]),
+    "sag_matrix_norm_inf": (C.c_int, [vp, vp, f64p]),
+    "sag_dc_set_coarse_pin": (C.c_int, [vp, vp, C.c_double]),
 }
 
 _lib = None

@@ -975,6 +975,72 @@ std::unique_ptr<Matrix> matrix_upload(Ctx& c, int nrows, int ncols, long long nn
   return m;
 }
 
+// ------------------------------------------ partitioned-solve primitives --
+// Building blocks for a caller that distributes the solve over ranks
+// (paper_2306_06795_b200/dist.py): every scalar stays in device memory, so a
+// reduction -> all-reduce -> axpy chain is stream-ordered with no host sync.
+
+// *out = sum over i with mask[i] (all i when mask is null) of a_i b_i
+__global__ void __launch_bounds__(kRedBlock) dot_mask_kernel(int n, const double* __restrict__ a,
+                                                             const double* __restrict__ b,
+                                                             const unsigned char* __restrict__ mask,
+                                                             Fin fin, double* partials,
+                                                             unsigned* ticket) {
+  const int st = gridDim.x * blockDim.x;
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    if (!mask || mask[i]) s = fma(a[i], b[i], s);
+  reduce_finish(s, fin, partials, ticket);
+}
+// y = y + sign * (*s) x   (MGS: w[k] -= h_ij v_i[k], krylov.cpp:66)
+__global__ void axpy_dev_kernel(int n, const double* s, double sign, const double* __restrict__ x,
+                                double* __restrict__ y) {
+  const double h = *s;
+  ew4(n, [&](int i) { return make_double2(y[i], x[i]); },
+      [&](int i, double2 v) { y[i] = sign < 0.0 ? v.x - h * v.y : v.x + h * v.y; });
+}
+// y = x / d, d = *s or sqrt(*s)   (v_0 = r / ||r||, krylov.cpp:47-48)
+__global__ void div_dev_kernel(int n, const double* __restrict__ x, const double* s, int take_sqrt,
+                               double* __restrict__ y) {
+  const double d = take_sqrt ? sqrt(*s) : *s;
+  ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = v / d; });
+}
+// y = x - (*sum) / count   (project_pressure, preconditioner.cpp:235-240)
+__global__ void sub_mean_kernel(int n, const double* __restrict__ x, const double* sum,
+                                double count, double* __restrict__ y) {
+  const double mean = *sum / count;
+  ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = v - mean; });
+}
+// y = a x + b y; a == b == 0: y = 0; b == 0: y = a x; b == 1: y = y + a x
+// (x += y_i z_i, krylov.cpp:108-110)
+__global__ void axpby_kernel(int n, double a, const double* __restrict__ x, double b,
+                             double* __restrict__ y) {
+  if (a == 0.0 && b == 0.0) {
+    ew4(n, [&](int i) { return 0.0; }, [&](int i, double v) { y[i] = v; });
+  } else if (b == 0.0) {
+    ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = a * v; });
+  } else if (b == 1.0) {
+    ew4(n, [&](int i) { return make_double2(y[i], x[i]); },
+        [&](int i, double2 v) { y[i] = v.x + a * v.y; });
+  } else {
+    ew4(n, [&](int i) { return make_double2(y[i], x[i]); },
+        [&](int i, double2 v) { y[i] = a * v.y + b * v.x; });
+  }
+}
+// halo pack / unpack: dst[i] = src[idx[i]]; dst[idx[i]] (+)= src[i] (idx unique)
+__global__ void gather_idx_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
+                                  double* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+__global__ void scatter_idx_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
+                                   double* __restrict__ dst, int add) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int d = idx[i];
+    dst[d] = add ? dst[d] + src[i] : src[i];
+  }
+}
+
 }  // namespace sag
 
 // =================================================================== C-ABI
@@ -1193,6 +1259,103 @@ int sag_dot(sag_ctx* ctx, int n, const double* a, const double* b, double* out) 
     sag::launch_dot(c, n, ai.d, bi.d, f);
     SAG_CUDA(cudaMemcpyAsync(out, c.scal.p, sizeof(double), cudaMemcpyDefault, c.stream));
     SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+// ---- partitioned-solve primitives (device pointers, no host sync) ----------
+static void require_dev(std::initializer_list<const void*> ps) {
+  for (const void* p : ps)
+    SAG_REQUIRE(p == nullptr || sag::is_device_ptr(p), SAG_INVALID_ARGUMENT,
+                "partitioned-solve primitives take device pointers");
+}
+
+int sag_dot_async(sag_ctx* ctx, int n, const double* a, const double* b,
+                  const unsigned char* mask, double* out) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(out);
+    require_dev({a, b, mask, out});
+    auto& c = ctx->c;
+    sag::Fin f;
+    f.kind = sag::FIN_STORE;
+    f.out = out;
+    sag::dot_mask_kernel<<<sag::red_grid_fit(c, sag::dot_mask_kernel, n), sag::kRedBlock, 0,
+                           c.stream>>>(n, a, b, mask, f, c.partials.p, c.ticket.p);
+    SAG_LAUNCHED(c);
+  });
+}
+
+int sag_axpy_async(sag_ctx* ctx, int n, const double* s, double sign, const double* x, double* y) {
+  return guard([&] {
+    NOTNULL(ctx);
+    require_dev({s, x, y});
+    auto& c = ctx->c;
+    sag::axpy_dev_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, s, sign, x, y);
+    SAG_LAUNCHED(c);
+  });
+}
+
+int sag_div_async(sag_ctx* ctx, int n, const double* x, const double* s, int take_sqrt, double* y) {
+  return guard([&] {
+    NOTNULL(ctx);
+    require_dev({x, s, y});
+    auto& c = ctx->c;
+    sag::div_dev_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, x, s, take_sqrt, y);
+    SAG_LAUNCHED(c);
+  });
+}
+
+int sag_sub_mean_async(sag_ctx* ctx, int n, const double* x, const double* sum, double count,
+                       double* y) {
+  return guard([&] {
+    NOTNULL(ctx);
+    require_dev({x, sum, y});
+    auto& c = ctx->c;
+    sag::sub_mean_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, x, sum, count, y);
+    SAG_LAUNCHED(c);
+  });
+}
+
+int sag_axpby_async(sag_ctx* ctx, int n, double a, const double* x, double b, double* y) {
+  return guard([&] {
+    NOTNULL(ctx);
+    require_dev({x, y});
+    auto& c = ctx->c;
+    sag::axpby_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, a, x, b, y);
+    SAG_LAUNCHED(c);
+  });
+}
+
+int sag_gather_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* dst) {
+  return guard([&] {
+    NOTNULL(ctx);
+    require_dev({idx, src, dst});
+    if (n <= 0) return;
+    auto& c = ctx->c;
+    sag::gather_idx_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, idx, src, dst);
+    SAG_LAUNCHED(c);
+  });
+}
+
+int sag_scatter_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* dst, int add) {
+  return guard([&] {
+    NOTNULL(ctx);
+    require_dev({idx, src, dst});
+    if (n <= 0) return;
+    auto& c = ctx->c;
+    sag::scatter_idx_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, idx, src, dst, add);
+    SAG_LAUNCHED(c);
+  });
+}
+
+int sag_matrix_norm_inf(sag_ctx* ctx, const sag_matrix* m, double* out) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(m);
+    NOTNULL(out);
+    auto& mm = const_cast<sag_matrix*>(m)->m;
+    sag::compute_norm_inf(ctx->c, mm);
+    *out = mm.norm_inf;
   });
 }
 

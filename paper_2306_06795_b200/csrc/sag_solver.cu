@@ -1203,6 +1203,21 @@ int sag_dc_destroy(sag_dc* d) {
   return guard([&] { delete d; });
 }
 
+int sag_dc_set_coarse_pin(sag_ctx* ctx, sag_dc* h, double level0_norm_inf) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(h);
+    Dc& d = h->d;
+    SAG_REQUIRE(level0_norm_inf >= 0.0, SAG_CONFIG_ERROR, "norm must be non-negative");
+    if (!d.cfg.enclosed_flow) return;
+    Level& B = d.lv.back();
+    // preconditioner.cpp:49-53 with the norm of the hierarchy's finest level
+    // supplied by the caller (a rank holding only the coarse levels)
+    d.coarse.setup(ctx->c, *B.K, B.n_x + B.n_y, 1e-12 * level0_norm_inf);
+    d.graph_ok = false;
+  });
+}
+
 int sag_dc_set_parameters(sag_dc* h, double eta_u, double eta_p, double omega0) {
   return guard([&] {
     SAG_NOTNULL(h);

@@ -1,0 +1,506 @@
+"""Distributed solve_stokes: FGMRES(m) with the DC-all preconditioner over a
+row/patch partition, one process per GPU.
+
+Per rank (partition.RankSystem, rank-local numbering):
+  * K0 and the low-order level 0 (L0, same dofs) are distributed: SpMV over
+    the owned rows, Vanka over the rank's own patches with the global
+    partition-of-unity weights, halo exchanges with the neighbours only
+    (forward: owned values to the ranks that read them as ghosts; reverse:
+    partial Vanka sums at ghosts, added by the owner in rank order);
+  * the coarser levels are agglomerated: the restriction is a partial
+    (P0 restricted to the owned rows)^T r on every rank followed by an
+    all-reduce of the level-1 vector (1.3 MB at config 2), the V-cycle below
+    level 0 runs replicated (libsag's device V-cycle, the coarsest pinned with
+    the norm of L0 as preconditioner.cpp:49-53 does), and the prolongation is
+    the owned rows of P0;
+  * FGMRES dots and norms are masked partial reductions + an all-reduce of
+    one scalar; every scalar stays in device memory (reduction -> all-reduce
+    -> axpy is stream-ordered); the host reads one column of the Hessenberg
+    matrix per Arnoldi step and runs the Givens rotations itself, in the
+    reference's operation order (krylov.cpp:75-100).
+Summation order differs from one process only where partial sums from
+several ranks meet (dots, the reverse halo, the restriction); at one rank the
+operations are the single-GPU ones.
+
+The kernels come from a backend: :class:`LibsagBackend` (libsag's sm_100a
+kernels through the C-ABI, the product path) or, in the CPU tests, a checker
+backend supplied by the tests. Communication is a :class:`Comm` over
+torch.distributed (NCCL on B200; gloo staged through host memory when
+several ranks share one device, and in the CPU tests).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+# ----------------------------------------------------------------- comm --
+class Comm:
+    """torch.distributed point-to-point + all-reduce on backend vectors.
+    stage=True copies device tensors through host memory (gloo)."""
+
+    def __init__(self, dist, torch, stage=False):
+        self.dist, self.torch, self.stage = dist, torch, stage
+        self.rank = dist.get_rank()
+        self.size = dist.get_world_size()
+
+    def _host(self, t):
+        return t.cpu() if (self.stage and t.is_cuda) else t
+
+    def allreduce(self, t, op="sum"):
+        if self.size == 1:
+            return t
+        o = self.dist.ReduceOp.SUM if op == "sum" else self.dist.ReduceOp.MAX
+        h = self._host(t)
+        self.dist.all_reduce(h, op=o)
+        if h is not t:
+            t.copy_(h)
+        return t
+
+    def exchange(self, sends: dict, recvs: dict):
+        """sends: q -> tensor to send; recvs: q -> tensor to receive into."""
+        if not sends and not recvs:
+            return
+        ops, back = [], []
+        for q in sorted(sends):
+            ops.append(self.dist.P2POp(self.dist.isend, self._host(sends[q]).contiguous(), q))
+        for q in sorted(recvs):
+            h = self._host(recvs[q])
+            if h is not recvs[q]:
+                back.append((recvs[q], h))
+            ops.append(self.dist.P2POp(self.dist.irecv, h, q))
+        for req in self.dist.batch_isend_irecv(ops):
+            req.wait()
+        for dst, h in back:
+            dst.copy_(h)
+
+
+# -------------------------------------------------------------- backend --
+class LibsagBackend:
+    """Rank-local kernels on the GPU: libsag (include/sag.h) on device
+    pointers of torch tensors, all on the context's (torch-owned) stream."""
+
+    def __init__(self, ctx, device, torch):
+        from . import lib, _check  # noqa: F401  (fails loudly without libsag)
+        self.ctx, self.device, self.torch = ctx, device, torch
+        self.L, self._check = lib(), _check
+        import ctypes as C
+        self.C = C
+
+    # allocation / transfer
+    def vec(self, n):
+        return self.torch.zeros(max(n, 1), dtype=self.torch.float64, device=self.device)[:n]
+
+    def ivec(self, a):
+        return self.torch.as_tensor(np.asarray(a, dtype=np.int32), device=self.device)
+
+    def u8(self, a):
+        return self.torch.as_tensor(np.asarray(a, dtype=np.uint8), device=self.device)
+
+    def from_host(self, a):
+        return self.torch.as_tensor(np.ascontiguousarray(a, dtype=np.float64), device=self.device)
+
+    def to_host(self, t):
+        return t.cpu().numpy()
+
+    def p(self, t):
+        return self.C.c_void_p(t.data_ptr()) if t is not None else None
+
+    # setup objects
+    def matrix(self, nrows, ncols, rp, ci, v):
+        from . import SparseMatrix
+        return SparseMatrix(nrows, ncols, rp, ci, v, self.ctx)
+
+    def vanka(self, nl, ext, patches, n_u, weights):
+        from . import Patches, SparseMatrix, factor_patches
+        k = SparseMatrix(nl, nl, *ext, ctx=self.ctx)
+        pt = Patches.from_lists(*patches, ctx=self.ctx)
+        f = factor_patches(k, pt, n_u)
+        f.set_weights(weights)
+        return f
+
+    def coarse(self, levels, cfg, norm0):
+        """The agglomerated V-cycle below level 0: libsag's device V-cycle
+        (HoAmgPreconditioner form: one V-cycle of `levels` from x = 0)."""
+        from . import HoAmgPreconditioner, SparseMatrix
+        lv = [(SparseMatrix.from_csr(k, self.ctx),
+               SparseMatrix.from_csr(p, self.ctx) if p is not None else None, nxyz)
+              for k, p, nxyz in levels]
+        h = HoAmgPreconditioner(lv[0][0], lv, cfg)
+        if cfg.enclosed_flow:
+            self._check(self.L.sag_dc_set_coarse_pin(self.ctx.h, h.h, self.C.c_double(norm0)))
+        return h
+
+    def norm_inf(self, m):
+        out = self.C.c_double()
+        self._check(self.L.sag_matrix_norm_inf(self.ctx.h, m.h, self.C.byref(out)))
+        return out.value
+
+    # kernels
+    def spmv(self, m, x, y, epi="store", aux=None):
+        e = {"store": 0, "resid": 1, "add": 2}[epi]
+        self._check(self.L.sag_spmv_fused(self.ctx.h, m.h, self.p(x), self.p(y), self.p(aux), e))
+
+    def vanka_apply(self, f, r, delta):
+        self._check(self.L.sag_apply_vanka(self.ctx.h, f.h, self.p(r), self.p(delta)))
+
+    def coarse_apply(self, h, b, x):
+        self._check(self.L.sag_dc_apply(self.ctx.h, h.h, self.p(b), self.p(x)))
+
+    def dot(self, a, b, mask, out):
+        self._check(self.L.sag_dot_async(self.ctx.h, a.numel(), self.p(a), self.p(b),
+                                         self.p(mask), self.p(out)))
+
+    def axpy_s(self, s, sign, x, y):
+        self._check(self.L.sag_axpy_async(self.ctx.h, y.numel(), self.p(s), float(sign),
+                                          self.p(x), self.p(y)))
+
+    def div_s(self, x, s, take_sqrt, y):
+        self._check(self.L.sag_div_async(self.ctx.h, y.numel(), self.p(x), self.p(s),
+                                         int(take_sqrt), self.p(y)))
+
+    def sub_mean(self, x, s, count, y):
+        self._check(self.L.sag_sub_mean_async(self.ctx.h, y.numel(), self.p(x), self.p(s),
+                                              float(count), self.p(y)))
+
+    def axpby(self, a, x, b, y):
+        self._check(self.L.sag_axpby_async(self.ctx.h, y.numel(), float(a), self.p(x), float(b),
+                                           self.p(y)))
+
+    def gather(self, idx, src, dst):
+        self._check(self.L.sag_gather_async(self.ctx.h, idx.numel(), self.p(idx), self.p(src),
+                                            self.p(dst)))
+
+    def scatter(self, idx, src, dst, add):
+        self._check(self.L.sag_scatter_async(self.ctx.h, idx.numel(), self.p(idx), self.p(src),
+                                             self.p(dst), int(add)))
+
+    def launches(self):
+        return self.ctx.launch_count()
+
+
+# --------------------------------------------------------------- solver --
+@dataclass
+class DistReport:
+    converged: bool
+    iterations: int
+    final_relative_residual: float
+    residual_history: list
+
+
+class _Level:
+    """A distributed level: local SpMV matrix + Vanka factors + relaxation
+    workspaces."""
+
+    def __init__(self, be, rs, ll, mrelax):
+        nl = rs.nl
+        self.K = be.matrix(nl, nl, ll.rows_rp, ll.rows_ci, ll.rows_v)
+        self.f = be.vanka(nl, (ll.ext_rp, ll.ext_ci, ll.ext_v), ll.patches, rs.n_u_loc,
+                          ll.weights)
+        self.kry = _Krylov(be, nl, mrelax)
+        self.r = be.vec(nl)
+        self.corr = be.vec(nl)
+
+
+class _Krylov:
+    def __init__(self, be, n, m):
+        self.m = m
+        self.sc = be.vec(m + 4)   # device scalars: ||b||^2, ||r||^2, h column
+        self.V = [be.vec(n) for _ in range(m + 1)]
+        self.Z = [be.vec(n) for _ in range(m)]
+        self.w = be.vec(n)
+        self.r = be.vec(n)
+
+
+class DistSolver:
+    """solve_stokes (preconditioner.cpp:229-259) with the DC preconditioner
+    (preconditioner.cpp:114-153) on one rank of a partition.
+
+    rs: this rank's partition.RankSystem; levels: the global low-order
+    hierarchy [(K, P, nxyz), ...] (host CSR) -- level 0 is distributed
+    through rs, levels 1.. are agglomerated; cfg: SolverConfig."""
+
+    def __init__(self, rs, levels, cfg, be, comm):
+        if cfg.variant not in (0, 1, 2):
+            raise ValueError("DistSolver: DC-all / DC-LO / DC-HO only")
+        self.rs, self.cfg, self.be, self.comm = rs, cfg, be, comm
+        nl = rs.nl
+        mrelax = max(cfg.nu1, cfg.nu2, 1)
+        self.mask = be.u8(rs.owned)
+        self.ones = be.from_host(np.ones(nl))
+        self.sc = be.vec(4)   # device scalars of the projection
+        self._ix = {k: {q: be.ivec(i) for q, i in getattr(rs, k).items()}
+                    for k in ("fwd_send", "fwd_recv", "rev_send", "rev_recv")}
+        self._buf = {k: {q: be.vec(len(i)) for q, i in getattr(rs, k).items()}
+                     for k in ("fwd_send", "fwd_recv", "rev_send", "rev_recv")}
+        self.k0 = _Level(be, rs, rs.levels["K0"], mrelax)
+        self.l0 = _Level(be, rs, rs.levels["L0"], mrelax)
+        self.outer = _Krylov(be, nl, cfg.restart)
+        self.din, self.dout = be.vec(nl), be.vec(nl)
+        self.t = be.vec(nl)
+        self.b0, self.x0 = be.vec(nl), be.vec(nl)
+        self.gam_rc, self.gam_e = be.vec(nl), be.vec(nl)
+        self.nlev = len(levels)
+        norm0 = self._norm_inf(self.l0.K)
+        if self.nlev > 1:
+            self.P = be.matrix(nl, rs.n1, rs.p_rp, rs.p_ci, rs.p_v)
+            self.R = be.matrix(rs.n1, nl, rs.r_rp, rs.r_ci, rs.r_v)
+            self.rc, self.xc = be.vec(rs.n1), be.vec(rs.n1)
+            self.coarse = be.coarse(levels[1:], cfg, norm0)
+        else:
+            # level 0 is the coarsest: agglomerate it whole (every rank solves)
+            own = np.nonzero(rs.owned)[0]
+            self.own_l = be.ivec(own)
+            self.own_g = be.ivec(rs.l2g[own])
+            self.l2g = be.ivec(rs.l2g)
+            self.tmp = be.vec(len(own))
+            self.gb, self.gx = be.vec(rs.n), be.vec(rs.n)
+            self.coarse = be.coarse(levels, cfg, norm0)
+
+    # ---- communication ------------------------------------------------
+    def halo(self, x):
+        """Forward halo: ghost entries of x from their owners."""
+        be, ix, buf = self.be, self._ix, self._buf
+        for q, i in ix["fwd_send"].items():
+            be.gather(i, x, buf["fwd_send"][q])
+        self.comm.exchange(buf["fwd_send"], buf["fwd_recv"])
+        for q in sorted(ix["fwd_recv"]):
+            be.scatter(ix["fwd_recv"][q], buf["fwd_recv"][q], x, False)
+
+    def halo_reduce(self, d):
+        """Reverse halo: partial sums at ghosts added by their owners, in rank order."""
+        be, ix, buf = self.be, self._ix, self._buf
+        for q, i in ix["rev_send"].items():
+            be.gather(i, d, buf["rev_send"][q])
+        self.comm.exchange(buf["rev_send"], buf["rev_recv"])
+        for q in sorted(ix["rev_recv"]):
+            be.scatter(ix["rev_recv"][q], buf["rev_recv"][q], d, True)
+
+    def _norm_inf(self, m):
+        t = self.be.from_host(np.array([self.be.norm_inf(m)]))
+        self.comm.allreduce(t, "max")
+        return float(self.be.to_host(t)[0])
+
+    # ---- reductions into device scalars ---------------------------------
+    def dot(self, a, b, s):
+        """s (a 1-element device view) = global (a, b) over the owned rows."""
+        self.be.dot(a, b, self.mask, s)
+        self.comm.allreduce(s)
+        return s
+
+    # ---- operators ------------------------------------------------------
+    def apply_op(self, L, x, y, epi="store", aux=None):
+        self.halo(x)
+        self.be.spmv(L.K, x, y, epi, aux)
+
+    def vanka(self, L, v, z):
+        self.halo(v)
+        self.be.vanka_apply(L.f, v, z)
+        self.halo_reduce(z)
+
+    # ---- fgmres (krylov.cpp:17-121) ---------------------------------------
+    def fgmres(self, L, b, x, prec, tol, max_iters, m, kry, x_zero=False, final=True,
+               bd=1e-30):
+        """fgmres(matrix_operator(L.K), b, x, prec, {tol, max_iters, restart m})
+        (krylov.cpp:17-121); x_zero: x is known to be zero on entry (it is
+        zeroed here and r = b exactly, as spmv of a zero vector is zero)."""
+        be = self.be
+        sc = kry.sc
+        host = lambda k0, k1: be.to_host(sc[k0:k1])  # noqa: E731
+        self.dot(b, b, sc[0:1])
+        bnorm = math.sqrt(float(host(0, 1)[0]))
+        ref = bnorm if bnorm > 0.0 else 1.0
+        hist = []
+        if x_zero:
+            be.axpby(0.0, b, 0.0, x)
+            be.axpby(1.0, b, 0.0, kry.r)
+            be.axpby(1.0, sc[0:1], 0.0, sc[1:2])
+            rnorm = bnorm
+        else:
+            self.apply_op(L, x, kry.r, "resid", b)
+            self.dot(kry.r, kry.r, sc[1:2])
+            rnorm = math.sqrt(float(host(1, 2)[0]))
+        hist.append(rnorm)
+        if rnorm / ref <= tol:
+            return DistReport(True, 0, rnorm / ref, hist)
+        it, converged, first = 0, False, True
+        h = np.zeros((m + 1) * m)
+        cs, sn = np.zeros(m), np.zeros(m)
+        base = 2
+        while it < max_iters:
+            if not first:   # restart from the true residual (krylov.cpp:43-53)
+                self.apply_op(L, x, kry.r, "resid", b)
+                self.dot(kry.r, kry.r, sc[1:2])
+                rnorm = math.sqrt(float(host(1, 2)[0]))
+                if rnorm / ref <= tol:
+                    converged = True
+                    break
+            first = False
+            be.div_s(kry.r, sc[1:2], True, kry.V[0])
+            g = np.zeros(m + 1)
+            g[0] = rnorm
+            h[:] = 0.0
+            j = 0
+            while j < m and it < max_iters:
+                prec(kry.V[j], kry.Z[j])
+                self.apply_op(L, kry.Z[j], kry.w)
+                for i in range(j + 1):  # modified Gram-Schmidt (krylov.cpp:63-67)
+                    s = self.dot(kry.w, kry.V[i], sc[base + i:base + i + 1])
+                    be.axpy_s(s, -1.0, kry.V[i], kry.w)
+                self.dot(kry.w, kry.w, sc[base + j + 1:base + j + 2])
+                col = host(base, base + j + 2)
+                for i in range(j + 1):
+                    h[i * m + j] = col[i]
+                wnorm = math.sqrt(float(col[j + 1]))
+                h[(j + 1) * m + j] = wnorm
+                breakdown = wnorm < bd
+                if not breakdown:       # v_(j+1) = w / ||w|| (krylov.cpp:70-73)
+                    be.div_s(kry.w, sc[base + j + 1:base + j + 2], True, kry.V[j + 1])
+                for i in range(j):      # Givens (krylov.cpp:75-93)
+                    t = cs[i] * h[i * m + j] + sn[i] * h[(i + 1) * m + j]
+                    h[(i + 1) * m + j] = -sn[i] * h[i * m + j] + cs[i] * h[(i + 1) * m + j]
+                    h[i * m + j] = t
+                denom = float(np.hypot(h[j * m + j], h[(j + 1) * m + j]))
+                if denom > 0.0:
+                    cs[j] = h[j * m + j] / denom
+                    sn[j] = h[(j + 1) * m + j] / denom
+                else:
+                    cs[j], sn[j] = 1.0, 0.0
+                h[j * m + j] = cs[j] * h[j * m + j] + sn[j] * h[(j + 1) * m + j]
+                h[(j + 1) * m + j] = 0.0
+                g[j + 1] = -sn[j] * g[j]
+                g[j] = cs[j] * g[j]
+                it += 1
+                rnorm = abs(g[j + 1])
+                hist.append(rnorm)
+                j += 1
+                if rnorm / ref <= tol or breakdown:
+                    break
+            y = np.zeros(j)             # back substitution (krylov.cpp:102-107)
+            for i in range(j - 1, -1, -1):
+                acc = g[i]
+                for k in range(i + 1, j):
+                    acc -= h[i * m + k] * y[k]
+                y[i] = acc / h[i * m + i]
+            for i in range(j):          # x += y_i z_i (krylov.cpp:108-110)
+                be.axpby(float(y[i]), kry.Z[i], 1.0, x)
+            if rnorm / ref <= tol:
+                converged = True
+                break
+        final_rel = float("nan")
+        if final:                       # final true residual (krylov.cpp:116-119)
+            self.apply_op(L, x, kry.r, "resid", b)
+            self.dot(kry.r, kry.r, sc[1:2])
+            final_rel = math.sqrt(float(host(1, 2)[0])) / ref
+            if final_rel <= tol:
+                converged = True
+        return DistReport(converged, it, final_rel, hist)
+
+    # ---- vanka_relax, Krylov-wrapped (vanka.cpp:199-208) -----------------
+    def relax_kw(self, L, x, b, nu, x_zero):
+        if nu <= 0:
+            if x_zero:
+                self.be.axpby(0.0, b, 0.0, x)
+            return
+        if x_zero:
+            r = b                                   # spmv of a zero vector is exactly zero
+        else:
+            self.apply_op(L, x, L.r, "resid", b)
+            r = L.r
+        prec = lambda v, z: self.vanka(L, v, z)  # noqa: E731
+        if x_zero:
+            self.fgmres(L, r, x, prec, 0.0, nu, nu, L.kry, x_zero=True, final=False)
+        else:
+            self.fgmres(L, r, L.corr, prec, 0.0, nu, nu, L.kry, x_zero=True, final=False)
+            self.be.axpby(1.0, L.corr, 1.0, x)
+
+    # ---- V-cycle level 0 (preconditioner.cpp:57-81) ---------------------------
+    def cycle0(self, b, x, skip_finest):
+        cf, be = self.cfg, self.be
+        if self.nlev == 1:              # coarsest (preconditioner.cpp:60-63), agglomerated
+            be.axpby(0.0, self.gb, 0.0, self.gb)
+            be.gather(self.own_l, b, self.tmp)
+            be.scatter(self.own_g, self.tmp, self.gb, False)
+            self.comm.allreduce(self.gb)
+            be.coarse_apply(self.coarse, self.gb, self.gx)
+            be.gather(self.l2g, self.gx, x)
+            return
+        relax = not skip_finest
+        pre = relax and cf.nu1 > 0
+        if pre:
+            self.relax_kw(self.l0, x, b, cf.nu1, True)
+            self.apply_op(self.l0, x, self.l0.r, "resid", b)
+            r = self.l0.r
+        else:
+            be.axpby(0.0, b, 0.0, x)
+            r = b
+        be.spmv(self.R, r, self.rc)                 # partial restriction (owned rows)
+        self.comm.allreduce(self.rc)
+        be.coarse_apply(self.coarse, self.rc, self.xc)
+        be.spmv(self.P, self.xc, x, "add")          # x += P xc on the owned rows
+        if relax and cf.nu2 > 0:
+            self.relax_kw(self.l0, x, b, cf.nu2, False)
+
+    # ---- DCPreconditioner::apply (preconditioner.cpp:114-153), TH ------------
+    def dc_apply(self, r, z):
+        cf, be, rs = self.cfg, self.be, self.rs
+        nu_loc = rs.n_u_loc
+        relax_fine = cf.variant != 1
+        pre = relax_fine and cf.nu1 > 0
+        x = z
+        if pre:
+            self.relax_kw(self.k0, x, r, cf.nu1, True)
+            self.apply_op(self.k0, x, self.t, "resid", r)
+            r1 = self.t
+        else:
+            be.axpby(0.0, r, 0.0, x)
+            r1 = r
+        # eta weighting (transfer.cpp:127-135) and TH restriction (copy)
+        be.axpby(cf.eta_u, r1[:nu_loc], 0.0, self.b0[:nu_loc])
+        be.axpby(cf.eta_p, r1[nu_loc:], 0.0, self.b0[nu_loc:])
+        skip = cf.variant == 2
+        if cf.gamma <= 1:
+            self.cycle0(self.b0, self.x0, skip)
+            be.axpby(1.0, self.x0, 1.0, x)          # x += prolong(e) (TH: copy)
+        else:
+            be.axpby(1.0, self.b0, 0.0, self.gam_rc)
+            be.axpby(0.0, self.b0, 0.0, self.gam_e)
+            for gi in range(cf.gamma):
+                if gi > 0:
+                    self.apply_op(self.l0, self.gam_e, self.b0, "resid", self.gam_rc)
+                else:
+                    be.axpby(1.0, self.gam_rc, 0.0, self.b0)
+                self.cycle0(self.b0, self.x0, skip)
+                be.axpby(1.0, self.x0, 1.0, self.gam_e)
+            be.axpby(1.0, self.gam_e, 1.0, x)
+        if relax_fine and cf.nu2 > 0:
+            self.relax_kw(self.k0, x, r, cf.nu2, False)
+
+    # ---- solve_stokes (preconditioner.cpp:229-259) --------------------------
+    def project(self, src, dst, k):
+        """dst = src with the global pressure mean removed (pressure block is
+        the local tail [n_u_loc, nl))."""
+        nu = self.rs.n_u_loc
+        s = self.sc[k:k + 1]
+        self.be.dot(src[nu:], self.ones[nu:], self.mask[nu:], s)
+        self.comm.allreduce(s)
+        if dst is not src:
+            self.be.axpby(1.0, src[:nu], 0.0, dst[:nu])
+        self.be.sub_mean(src[nu:], s, float(self.rs.n_p), dst[nu:])
+
+    def apply_prec(self, v, z):
+        if self.cfg.enclosed_flow:
+            self.project(v, self.din, 0)
+            self.dc_apply(self.din, self.dout)
+            self.project(self.dout, z, 1)
+        else:
+            self.dc_apply(v, z)
+
+    def solve(self, rhs_local, x):
+        """rhs_local: backend vector (nl, owned entries valid); x: output (nl)."""
+        cf = self.cfg
+        self.be.axpby(0.0, rhs_local, 0.0, x)
+        return self.fgmres(self.k0, rhs_local, x, self.apply_prec, cf.tol, cf.max_iters,
+                           cf.restart, self.outer, x_zero=True, final=True)
