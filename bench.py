@@ -263,17 +263,24 @@ def run_reference(args, ws, rank):
 
 # ------------------------------------------------------- GPU arm, N > 1
 def run_dist(args, ws, rank, local):
-    """Strong scaling of the hot step: K0's patches and rows partitioned
-    across the ranks (paper_2306_06795_b200.dist), forward halo of x and
-    reverse halo of the Vanka partial sums over NCCL point-to-point (NVLink),
-    rank-local libsag kernels."""
+    """Strong scaling across the ranks of one node: K0's rows and
+    Vanka patches partitioned in rank-local numbering
+    (paper_2306_06795_b200.partition), forward halo of x and reverse halo of
+    the Vanka partial sums over NCCL point-to-point (NVLink), rank-local
+    libsag kernels (paper_2306_06795_b200.dsolve.DistStep). Unless --no-solve,
+    also the distributed FGMRES(30) + DC-all solve (dsolve.DistSolver: L0
+    partitioned the same way, coarser levels agglomerated, MGS dots as
+    all-reduces)."""
     import torch
     import torch.distributed as dist
 
     import paper_2306_06795_b200 as S
-    from paper_2306_06795_b200.dist import DistStep, build_partition
+    from paper_2306_06795_b200.dsolve import Comm, DistSolver, DistStep, LibsagBackend
+    from paper_2306_06795_b200.partition import build_rank_systems
 
     cfg = CONFIGS[args.config]
+    if cfg["sv"]:
+        raise SystemExit("bench --gpus N: the partitioned path covers Taylor-Hood configs")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     own_pg = not dist.is_initialized()
@@ -284,76 +291,67 @@ def run_dist(args, ws, rank, local):
     t0 = time.perf_counter()
     case = host_case(cfg)
     k0 = case.k0()
+    levels = case.levels()
     host_setup_s = time.perf_counter() - t0
+    n = k0.nrows
+    t1 = time.perf_counter()
+    l0, p0, nxyz_l0 = levels[0]
+    rs = build_rank_systems(ws, k0, l0, p0, case.nxyz0, nxyz_l0, ranks=[rank])[0]
+    plan_s = time.perf_counter() - t1
     # libsag launches on a torch-owned stream: tensors, NCCL work and libsag
     # kernels share it, and tearing the context down never destroys a stream
     # torch still references
     stream = torch.cuda.Stream(device=dev)
     ctx = S.Context(local, stream=stream.cuda_stream)
-    n = k0.nrows
-    t1 = time.perf_counter()
-    K0 = S.SparseMatrix.from_csr(k0, ctx)
-    pl = S.build_patches(K0, *case.nxyz0, sv_triples=case.sv).export()
-    plans = build_partition(ws, n, k0.rp, k0.ci, k0.v, pl.pressure_ptr, pl.pressure,
-                            pl.velocity_ptr, pl.velocity)
-    plan = plans[rank]
-    lo, hi = plan.patch_lo, plan.patch_hi
-    sub = S.Patches.from_lists(pl.pressure_ptr[lo:hi + 1] - pl.pressure_ptr[lo],
-                               pl.pressure[pl.pressure_ptr[lo]:pl.pressure_ptr[hi]],
-                               pl.velocity_ptr[lo:hi + 1] - pl.velocity_ptr[lo],
-                               pl.velocity[pl.velocity_ptr[lo]:pl.velocity_ptr[hi]],
-                               pl.nx[lo:hi], ctx=ctx)
-    f = S.factor_patches(K0, sub, case.n_x0 + case.n_y0)
-    mult = np.zeros(n)
-    np.add.at(mult, pl.velocity, 1.0)
-    np.add.at(mult, pl.pressure, 1.0)
-    f.set_weights(np.divide(1.0, mult, out=np.zeros(n), where=mult > 0))
-    rows = S.SparseMatrix(len(plan.owned), n, plan.rows_rp, plan.rows_ci, plan.rows_v, ctx)
-    del K0
-    ctx.synchronize()
-    setup_gpu_s = time.perf_counter() - t1
-    x = torch.from_numpy(splitmix64_uniform(n)).to(dev)
-    delta = torch.empty_like(x)
-    y = torch.empty(len(plan.owned), dtype=torch.float64, device=dev)
-
-    def local_vanka(xv):
-        return S.apply_vanka(f, xv, out=delta)
-
-    def local_spmv(xv):
-        return S.spmv(rows, xv, out=y)
-
+    comm = Comm(dist, torch)
     with torch.cuda.stream(stream):
-        step = DistStep(plan, local_vanka, local_spmv, torch, dist, dev)
+        be = LibsagBackend(ctx, dev, torch)
+        t2 = time.perf_counter()
+        step = DistStep(rs, be, comm)
+        torch.cuda.synchronize(dev)
+        setup_gpu_s = time.perf_counter() - t2
+        x = be.from_host(splitmix64_uniform(n)[rs.l2g])
+        delta, y = be.vec(rs.nl), be.vec(rs.nl)
         dist.barrier()  # a collective before the first point-to-point batch
         for _ in range(max(args.warmup, 3)):
-            step(x)
+            step.step(x, delta, y)
         torch.cuda.synchronize(dev)
         clocks = ClockSampler(local) if rank == 0 else None
         dist.barrier()
         torch.cuda.synchronize(dev)
-        l0 = ctx.launch_count()
+        l0n = ctx.launch_count()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            step(x)
+            step.step(x, delta, y)
         e1.record(stream)
         e1.synchronize()
-        launches = ctx.launch_count() - l0
+        launches = ctx.launch_count() - l0n
         t_steps = dist_max(e0.elapsed_time(e1) / 1e3, ws)
+        # per-rank patch kernel (roofline of the dominant kernel)
+        f = step.k0.f
+        xp, dp = S.C.c_void_p(x.data_ptr()), S.C.c_void_p(delta.data_ptr())
+        kper = max(args.steps // 2, 10)
+        e0.record(stream)
+        for _ in range(kper):
+            S._check(S.lib().sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 1))
+        e1.record(stream)
+        e1.synchronize()
+        t_patch = e0.elapsed_time(e1) / 1e3 / kper
         dist.barrier()
         # e2e: owned inputs from pinned host memory, owned outputs back
-        own = torch.as_tensor(plan.owned, device=dev)
-        xh = torch.from_numpy(splitmix64_uniform(n)[plan.owned]).pin_memory()
-        dh = torch.empty(len(plan.owned), dtype=torch.float64).pin_memory()
-        yh = torch.empty(len(plan.owned), dtype=torch.float64).pin_memory()
+        own = torch.as_tensor(np.nonzero(rs.owned)[0], device=dev)
+        xh = torch.from_numpy(splitmix64_uniform(n)[rs.l2g[rs.owned.astype(bool)]]).pin_memory()
+        dh = torch.empty(rs.n_own, dtype=torch.float64).pin_memory()
+        yh = torch.empty(rs.n_own, dtype=torch.float64).pin_memory()
         ke = max(args.steps // 4, 5)
 
         def e2e_step():
             x.index_copy_(0, own, xh.to(dev, non_blocking=True))
-            dd, yy = step(x)
-            dh.copy_(dd.index_select(0, own), non_blocking=True)
-            yh.copy_(yy, non_blocking=True)
+            step.step(x, delta, y)
+            dh.copy_(delta.index_select(0, own), non_blocking=True)
+            yh.copy_(y.index_select(0, own), non_blocking=True)
             torch.cuda.current_stream(dev).synchronize()
 
         for _ in range(2):  # warm-up: allocator, pinned staging
@@ -364,9 +362,38 @@ def run_dist(args, ws, rank, local):
         for _ in range(ke):
             e2e_step()
         t_e2e = dist_max((time.perf_counter() - te0) / ke, ws)
-    clk = clocks.stop() if clocks else None
-    ghosts = dist_max(float(plan.ghost_count()), ws)
+        clk = clocks.stop() if clocks else None
+
+        solve = None
+        if not args.no_solve:
+            scfg = S.SolverConfig(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
+                                  enclosed_flow=case.enclosed)
+            del step
+            ts0 = time.perf_counter()
+            solver = DistSolver(rs, levels, scfg, be, comm)
+            torch.cuda.synchronize(dev)
+            solver_setup_s = time.perf_counter() - ts0
+            rhs = be.from_host(case.rhs()[rs.l2g])
+            xs = be.vec(rs.nl)
+            solver.solve(rhs, xs)   # warm-up (coarse graph capture)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            ts = time.perf_counter()
+            rep = solver.solve(rhs, xs)
+            torch.cuda.synchronize(dev)
+            t_solve = dist_max(time.perf_counter() - ts, ws)
+            solve = {"gpu_s": t_solve, "iterations": rep.iterations,
+                     "final_relative_residual": rep.final_relative_residual,
+                     "converged": rep.converged, "setup_s": solver_setup_s,
+                     "path": "dsolve.DistSolver (partitioned K0/L0, agglomerated coarse "
+                             "levels, NCCL all-reduce dots)",
+                     "reference_cpu_s_1core": {1: 1.21, 2: 152.9}.get(args.config)}
+    ghosts = dist_max(float(rs.ghost_count()), ws)
+    own_max = dist_max(float(rs.n_own), ws)
+    t_patch = dist_max(t_patch, ws)
     if rank == 0:
+        peak, peak_kind = peak_hbm()
+        b_p = vanka_patch_bytes(f, rs.nl)
         out = {
             "metric": METRIC, "value": n / (t_steps / args.steps) / 1e9, "unit": "GDOF/s",
             "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
@@ -375,13 +402,22 @@ def run_dist(args, ws, rank, local):
             "data": "synthetic: reference build_case cavity + splitmix64 x (SURVEY 8(d))",
             "config": {"workload": cfg["workload"], "k0_rows": n, "k0_nnz": k0.nnz,
                        "parallelism": f"row/patch partition x{ws}, NCCL halo",
+                       "max_owned_dofs_per_rank": int(own_max),
                        "max_ghost_dofs_per_rank": int(ghosts),
                        "l2": "inputs exceed L2; no flush"},
             "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "kernel": "vanka_patch_kernel (rank 0's K0 patches)",
+                         "achieved": b_p / t_patch / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": b_p / t_patch / 1e9 / peak, "traffic": None,
+                         "algorithmic_bytes": b_p, "peak_kind": peak_kind,
+                         "bytes_def": "factor blobs + 8 n_local (r) + 8 slots"},
             "e2e": {"value": n / t_e2e / 1e9, "unit": "GDOF/s",
                     "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 16 * n},
-            "setup": {"host_reference_setup_s": host_setup_s, "gpu_setup_s": setup_gpu_s},
+            "setup": {"host_reference_setup_s": host_setup_s, "partition_plan_s": plan_s,
+                      "gpu_setup_s": setup_gpu_s},
         }
+        if solve:
+            out["solve"] = solve
         if clk:
             out["clocks"] = clk
         print(json.dumps(out))

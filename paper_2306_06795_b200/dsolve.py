@@ -214,20 +214,16 @@ class _Krylov:
         self.r = be.vec(n)
 
 
-class DistSolver:
-    """solve_stokes (preconditioner.cpp:229-259) with the DC preconditioner
-    (preconditioner.cpp:114-153) on one rank of a partition.
+class DistStep:
+    """The partitioned hot step on one rank: the halos, the masked reductions
+    and the distributed K0 (local SpMV rows + own Vanka patches).
 
-    rs: this rank's partition.RankSystem; levels: the global low-order
-    hierarchy [(K, P, nxyz), ...] (host CSR) -- level 0 is distributed
-    through rs, levels 1.. are agglomerated; cfg: SolverConfig."""
+    step(x, delta, y): delta = apply_vanka(x) (vanka.cpp:151-184) and y = K0 x
+    (sparse.cpp:78-91) on the rank's owned dofs -- the bench's unit of work."""
 
-    def __init__(self, rs, levels, cfg, be, comm):
-        if cfg.variant not in (0, 1, 2):
-            raise ValueError("DistSolver: DC-all / DC-LO / DC-HO only")
-        self.rs, self.cfg, self.be, self.comm = rs, cfg, be, comm
+    def __init__(self, rs, be, comm, mrelax=1):
+        self.rs, self.be, self.comm = rs, be, comm
         nl = rs.nl
-        mrelax = max(cfg.nu1, cfg.nu2, 1)
         self.mask = be.u8(rs.owned)
         self.ones = be.from_host(np.ones(nl))
         self.sc = be.vec(4)   # device scalars of the projection
@@ -236,28 +232,10 @@ class DistSolver:
         self._buf = {k: {q: be.vec(len(i)) for q, i in getattr(rs, k).items()}
                      for k in ("fwd_send", "fwd_recv", "rev_send", "rev_recv")}
         self.k0 = _Level(be, rs, rs.levels["K0"], mrelax)
-        self.l0 = _Level(be, rs, rs.levels["L0"], mrelax)
-        self.outer = _Krylov(be, nl, cfg.restart)
-        self.din, self.dout = be.vec(nl), be.vec(nl)
-        self.t = be.vec(nl)
-        self.b0, self.x0 = be.vec(nl), be.vec(nl)
-        self.gam_rc, self.gam_e = be.vec(nl), be.vec(nl)
-        self.nlev = len(levels)
-        norm0 = self._norm_inf(self.l0.K)
-        if self.nlev > 1:
-            self.P = be.matrix(nl, rs.n1, rs.p_rp, rs.p_ci, rs.p_v)
-            self.R = be.matrix(rs.n1, nl, rs.r_rp, rs.r_ci, rs.r_v)
-            self.rc, self.xc = be.vec(rs.n1), be.vec(rs.n1)
-            self.coarse = be.coarse(levels[1:], cfg, norm0)
-        else:
-            # level 0 is the coarsest: agglomerate it whole (every rank solves)
-            own = np.nonzero(rs.owned)[0]
-            self.own_l = be.ivec(own)
-            self.own_g = be.ivec(rs.l2g[own])
-            self.l2g = be.ivec(rs.l2g)
-            self.tmp = be.vec(len(own))
-            self.gb, self.gx = be.vec(rs.n), be.vec(rs.n)
-            self.coarse = be.coarse(levels, cfg, norm0)
+
+    def step(self, x, delta, y):
+        self.vanka(self.k0, x, delta)
+        self.be.spmv(self.k0.K, x, y)    # x's ghosts are fresh from the Vanka halo
 
     # ---- communication ------------------------------------------------
     def halo(self, x):
@@ -299,6 +277,46 @@ class DistSolver:
         self.halo(v)
         self.be.vanka_apply(L.f, v, z)
         self.halo_reduce(z)
+
+
+
+class DistSolver(DistStep):
+    """solve_stokes (preconditioner.cpp:229-259) with the DC preconditioner
+    (preconditioner.cpp:114-153) on one rank of a partition.
+
+    rs: this rank's partition.RankSystem; levels: the global low-order
+    hierarchy [(K, P, nxyz), ...] (host CSR) -- level 0 is distributed
+    through rs, levels 1.. are agglomerated; cfg: SolverConfig."""
+
+    def __init__(self, rs, levels, cfg, be, comm):
+        if cfg.variant not in (0, 1, 2):
+            raise ValueError("DistSolver: DC-all / DC-LO / DC-HO only")
+        mrelax = max(cfg.nu1, cfg.nu2, 1)
+        super().__init__(rs, be, comm, mrelax)
+        self.cfg = cfg
+        nl = rs.nl
+        self.l0 = _Level(be, rs, rs.levels["L0"], mrelax)
+        self.outer = _Krylov(be, nl, cfg.restart)
+        self.din, self.dout = be.vec(nl), be.vec(nl)
+        self.t = be.vec(nl)
+        self.b0, self.x0 = be.vec(nl), be.vec(nl)
+        self.gam_rc, self.gam_e = be.vec(nl), be.vec(nl)
+        self.nlev = len(levels)
+        norm0 = self._norm_inf(self.l0.K)
+        if self.nlev > 1:
+            self.P = be.matrix(nl, rs.n1, rs.p_rp, rs.p_ci, rs.p_v)
+            self.R = be.matrix(rs.n1, nl, rs.r_rp, rs.r_ci, rs.r_v)
+            self.rc, self.xc = be.vec(rs.n1), be.vec(rs.n1)
+            self.coarse = be.coarse(levels[1:], cfg, norm0)
+        else:
+            # level 0 is the coarsest: agglomerate it whole (every rank solves)
+            own = np.nonzero(rs.owned)[0]
+            self.own_l = be.ivec(own)
+            self.own_g = be.ivec(rs.l2g[own])
+            self.l2g = be.ivec(rs.l2g)
+            self.tmp = be.vec(len(own))
+            self.gb, self.gx = be.vec(rs.n), be.vec(rs.n)
+            self.coarse = be.coarse(levels, cfg, norm0)
 
     # ---- fgmres (krylov.cpp:17-121) ---------------------------------------
     def fgmres(self, L, b, x, prec, tol, max_iters, m, kry, x_zero=False, final=True,

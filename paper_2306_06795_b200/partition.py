@@ -1,10 +1,9 @@
 """Row/patch partition of the solve across ranks in rank-local numbering
 (SURVEY.md 8(e)).
 
-Ownership is the one of :func:`dist.build_partition`: rank r owns the
-contiguous range of Vanka patches [lo_r, hi_r) (pressure seeds are numbered by
-mesh vertex, so ranges are strips of the domain) and every dof whose
-lowest-numbered K0 patch it owns. The fine levels that live on the n0 dofs --
+Ownership: rank r owns the contiguous range of Vanka patches [lo_r, hi_r)
+(pressure seeds are numbered by mesh vertex, so ranges are strips of the
+domain) and every dof whose lowest-numbered K0 patch it owns. The fine levels that live on the n0 dofs --
 K0 and, for Taylor-Hood, level 0 of the low-order hierarchy (the P1isoP2/P1
 operator on the same dofs, transfer.cpp:97-110) -- are distributed by that
 map; the coarser levels are agglomerated (every rank holds them whole).
@@ -141,7 +140,8 @@ class RankSystem:
 
 
 def _owner_map(n, nranks, pptr, pidx, vptr, vidx):
-    """Rank of the lowest-numbered patch containing each dof (dist.build_partition)."""
+    """Rank of the lowest-numbered patch containing each dof; patch ranges
+    [bounds[r], bounds[r + 1]) per rank."""
     npatch = len(pptr) - 1
     bounds = np.array([(npatch * r) // nranks for r in range(nranks + 1)], dtype=np.int64)
     first = np.full(n, np.iinfo(np.int64).max, dtype=np.int64)
