@@ -12,9 +12,11 @@ by all ranks (GDOF/s). Inputs (K0 0.48 GB + Vanka factors 1.4 GB) exceed the
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
   python bench.py --impl reference      # the reference's CPU path, host cores
 
-Multi-GPU (torchrun, N > 1): K0's rows and Vanka patches are partitioned
-across the ranks (paper_2306_06795_b200.dist) with NCCL halo exchanges (strong
-scaling). Times are CUDA events on libsag's stream, max over ranks.
+Multi-GPU (torchrun, N > 1; --dist at N = 1): K0's rows and Vanka patches are
+partitioned across the ranks in rank-local numbering
+(paper_2306_06795_b200.partition, .dsolve) with NCCL halo exchanges (strong
+scaling); the line also carries the distributed FGMRES + DC-all solve. Times
+are CUDA events on libsag's stream, max over ranks.
 
 roofline: the dominant kernel is the Vanka patch kernel; its algorithmic bytes
 are those of the representation it streams (factor blobs incl. dof indices,
@@ -141,8 +143,9 @@ class ClockSampler:
 
 
 def dist_setup():
-    # keep rank 0's stdout to the one JSON line (no NCCL version banner)
-    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # keep rank 0's stdout to the one JSON line: NCCL prints its version
+    # banner to stdout at NCCL_DEBUG=VERSION/INFO (set SAG_NCCL_DEBUG to see it)
+    os.environ["NCCL_DEBUG"] = os.environ.get("SAG_NCCL_DEBUG", "WARN")
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
