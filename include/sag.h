@@ -130,6 +130,14 @@ int sag_vanka_set_weights(sag_ctx* ctx, sag_vanka* f, const double* weights);
  * vanka.cpp:151-184). */
 int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta);
 
+/* The hot step as one call: y = K x (spmv, sparse.cpp:78-91) and delta =
+ * apply_vanka(x) (vanka.cpp:151-184) on the same input. With host buffers x
+ * crosses the host link once and y's copy back overlaps the Vanka sweep (a
+ * second stream); results are complete on return. Same results as
+ * sag_spmv + sag_apply_vanka. */
+int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const double* x,
+                   double* delta, double* y);
+
 /* One stage of sag_apply_vanka, for per-kernel timing (device pointers):
  * stage 1 = patch kernel (local solves into the slot buffer),
  * stage 2 = owner-computes gather (slots -> delta). */

@@ -41,7 +41,7 @@ __all__ = [
     "Error", "DimensionMismatch", "SingularMatrix", "SingularPatch", "ConfigError",
     "SolverStagnation", "ZeroDiagonal", "UnsupportedDiscretization", "CudaError", "Context", "SparseMatrix", "Patches",
     "VankaFactorization", "spmv", "norm2", "dot", "build_patches", "factor_patches",
-    "apply_vanka", "vanka_relax", "RelaxMode", "FgmresOptions", "KrylovReport", "fgmres",
+    "apply_vanka", "vanka_spmv_step", "vanka_relax", "RelaxMode", "FgmresOptions", "KrylovReport", "fgmres",
     "SolverConfig", "Variant", "DCPreconditioner", "HoAmgPreconditioner", "UzawaPreconditioner",
     "solve_stokes", "default_context", "lib",
 ]
@@ -149,6 +149,7 @@ SIGNATURES = {
     "sag_vanka_export": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "sag_apply_vanka": (C.c_int, [vp, vp, vp, vp]),
     "sag_apply_vanka_stage": (C.c_int, [vp, vp, vp, vp, C.c_int]),
+    "sag_vanka_spmv": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "sag_vanka_set_weights": (C.c_int, [vp, vp, vp]),
     "sag_vanka_relax": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_double]),
     "sag_fgmres": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, C.POINTER(sag_fgmres_options),
@@ -466,6 +467,16 @@ def apply_vanka(f: VankaFactorization, r, out=None):
     dp, d = _vec_out(out, f.n, like=r)
     _check(lib().sag_apply_vanka(f.ctx.h, f.h, rp, dp))
     return d
+
+
+def vanka_spmv_step(f: VankaFactorization, k: SparseMatrix, x, delta=None, y=None):
+    """The hot step in one call: (apply_vanka(f, x), spmv(k, x)) with x read
+    once (sag_vanka_spmv; vanka.cpp:151-184, sparse.cpp:78-91)."""
+    xp, xk = _vec_in(x, f.n)
+    dp, d = _vec_out(delta, f.n, like=x)
+    yp, yy = _vec_out(y, k.nrows, like=x)
+    _check(lib().sag_vanka_spmv(f.ctx.h, f.h, k.h, xp, dp, yp))
+    return d, yy
 
 
 class RelaxMode:

@@ -97,6 +97,17 @@ struct Ctx {
   DevBuf<double> partials;   // kMaxRedGrid * 2 (two independent sums per kernel)
   DevBuf<unsigned> ticket;   // reduction tickets
   DevBuf<double> scal;       // general device scalars (sag_dot/norm outputs)
+  // second stream for device->host copies that overlap compute on `stream`
+  // (created on first use, owned by the context)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_ev = nullptr;
+  cudaStream_t copy() {
+    if (!copy_stream) {
+      SAG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+      SAG_CUDA(cudaEventCreateWithFlags(&copy_ev, cudaEventDisableTiming));
+    }
+    return copy_stream;
+  }
   // staging for host vectors passed to the C-ABI
   std::vector<DevBuf<double>> stage;
   double* stage_buf(int slot, size_t n) {

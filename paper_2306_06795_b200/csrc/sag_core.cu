@@ -1106,6 +1106,11 @@ int sag_destroy(sag_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.copy_stream) {
+      cudaStreamSynchronize(ctx->c.copy_stream);
+      cudaStreamDestroy(ctx->c.copy_stream);
+      cudaEventDestroy(ctx->c.copy_ev);
+    }
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });

@@ -2076,6 +2076,33 @@ int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* d
   });
 }
 
+int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const double* x,
+                   double* delta, double* y) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    SAG_NOTNULL(k);
+    auto& c = ctx->c;
+    const int n = f->f.n;
+    SAG_REQUIRE(k->m.nrows == n && k->m.ncols == n, SAG_DIMENSION_MISMATCH,
+                "sag_vanka_spmv: operator and factorization sizes differ");
+    InVec xi(c, x, n, 0);                 // x crosses the host link once
+    OutVec yo(c, y, n, 2, false);
+    OutVec d(c, delta, n, 1, false);
+    launch_spmv(c, k->m, xi.d, yo.d, Epi::Store);
+    if (yo.host) {
+      // y's device->host copy runs on the copy stream under the Vanka sweep
+      cudaStream_t cs = c.copy();
+      SAG_CUDA(cudaEventRecord(c.copy_ev, c.stream));
+      SAG_CUDA(cudaStreamWaitEvent(cs, c.copy_ev, 0));
+      SAG_CUDA(cudaMemcpyAsync(yo.host, yo.d, sizeof(double) * n, cudaMemcpyDeviceToHost, cs));
+    }
+    vanka_apply(c, f->f, xi.d, d.d);
+    d.finish();
+    if (yo.host) SAG_CUDA(cudaStreamSynchronize(c.copy()));
+  });
+}
+
 int sag_apply_vanka_stage(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta,
                           int stage) {
   return guard([&] {

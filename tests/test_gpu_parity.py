@@ -107,6 +107,31 @@ def test_apply_vanka_parity(S, n):
         assert np.all(z == 0.0)  # tests/test_vanka.cpp:264-271
 
 
+@pytest.mark.parametrize("device", [False, True])
+def test_vanka_spmv_step(S, device):
+    """sag_vanka_spmv (x read once, y copied back under the sweep) equals
+    spmv + apply_vanka of the reference, with host (pinned) and device buffers."""
+    import torch
+    c, d, k0, levels, _ = ref_case(64)
+    rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0)
+    K = S.SparseMatrix.from_csr(k0)
+    f = S.factor_patches(K, S.build_patches(K, *d.nxyz0), d.nxyz0[0] + d.nxyz0[1])
+    x = O.splitmix64_uniform(k0.nrows)
+    if device:
+        xt = torch.from_numpy(x).cuda()
+        dt, yt = S.vanka_spmv_step(f, K, xt)
+        dl, y = dt.cpu().numpy(), yt.cpu().numpy()
+    else:
+        xh = torch.from_numpy(x).pin_memory().numpy()
+        dh = torch.empty(k0.nrows, dtype=torch.float64).pin_memory().numpy()
+        yh = torch.empty(k0.nrows, dtype=torch.float64).pin_memory().numpy()
+        dl, y = S.vanka_spmv_step(f, K, xh, dh, yh)
+        assert dl is dh and y is yh
+    assert rel_inf(y, O.RefMat.from_csr(k0).spmv(x)) <= TOL
+    assert rel_inf(dl, rv.apply(x)) <= TOL
+    assert np.array_equal(dl, S.apply_vanka(f, x)) and np.array_equal(y, S.spmv(K, x))
+
+
 def test_apply_vanka_sv(S):
     c, d, k0, levels, _ = ref_case(8, sv=True, cfg=dict(omega0=0.78, eta_p=2.68))
     rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0, sv_triples=True)
