@@ -130,6 +130,12 @@ int sag_vanka_set_weights(sag_ctx* ctx, sag_vanka* f, const double* weights);
  * vanka.cpp:151-184). */
 int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* delta);
 
+/* x += omega * apply_vanka(r) (the update of vanka_relax's stationary mode,
+ * vanka.cpp:195), fused into the gather: a partitioned sweep adds its boundary
+ * patches' contributions onto the interior ones. */
+int sag_apply_vanka_add(sag_ctx* ctx, const sag_vanka* f, const double* r, double* x,
+                        double omega);
+
 /* The hot step as one call: y = K x (spmv, sparse.cpp:78-91) and delta =
  * apply_vanka(x) (vanka.cpp:151-184) on the same input. With host buffers x
  * crosses the host link once and y's copy back overlaps the Vanka sweep (a

@@ -2076,6 +2076,19 @@ int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* d
   });
 }
 
+int sag_apply_vanka_add(sag_ctx* ctx, const sag_vanka* f, const double* r, double* x,
+                        double omega) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    auto& c = ctx->c;
+    InVec ri(c, r, f->f.n, 0);
+    OutVec xo(c, x, f->f.n, 1, true);
+    vanka_apply_stationary(c, f->f, ri.d, xo.d, omega);
+    xo.finish();
+  });
+}
+
 int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const double* x,
                    double* delta, double* y) {
   return guard([&] {

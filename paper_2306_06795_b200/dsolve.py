@@ -59,10 +59,12 @@ class Comm:
             t.copy_(h)
         return t
 
-    def exchange(self, sends: dict, recvs: dict):
-        """sends: q -> tensor to send; recvs: q -> tensor to receive into."""
+    def start(self, sends: dict, recvs: dict):
+        """Posts a grouped point-to-point exchange (sends: q -> tensor to send;
+        recvs: q -> tensor to receive into). With NCCL the transfers run on
+        NCCL's stream while the caller keeps launching work on its own."""
         if not sends and not recvs:
-            return
+            return None
         ops, back = [], []
         for q in sorted(sends):
             ops.append(self.dist.P2POp(self.dist.isend, self._host(sends[q]).contiguous(), q))
@@ -71,10 +73,21 @@ class Comm:
             if h is not recvs[q]:
                 back.append((recvs[q], h))
             ops.append(self.dist.P2POp(self.dist.irecv, h, q))
-        for req in self.dist.batch_isend_irecv(ops):
+        return self.dist.batch_isend_irecv(ops), back
+
+    def finish(self, handle):
+        """Completes an exchange: the caller's stream waits for it (NCCL), the
+        staged receives are copied back (gloo)."""
+        if handle is None:
+            return
+        reqs, back = handle
+        for req in reqs:
             req.wait()
         for dst, h in back:
             dst.copy_(h)
+
+    def exchange(self, sends: dict, recvs: dict):
+        self.finish(self.start(sends, recvs))
 
 
 # -------------------------------------------------------------- backend --
@@ -146,6 +159,10 @@ class LibsagBackend:
     def vanka_apply(self, f, r, delta):
         self._check(self.L.sag_apply_vanka(self.ctx.h, f.h, self.p(r), self.p(delta)))
 
+    def vanka_add(self, f, r, x):
+        self._check(self.L.sag_apply_vanka_add(self.ctx.h, f.h, self.p(r), self.p(x),
+                                               self.C.c_double(1.0)))
+
     def coarse_apply(self, h, b, x):
         self._check(self.L.sag_dc_apply(self.ctx.h, h.h, self.p(b), self.p(x)))
 
@@ -191,14 +208,24 @@ class DistReport:
 
 
 class _Level:
-    """A distributed level: local SpMV matrix + Vanka factors + relaxation
-    workspaces."""
+    """A distributed level: its local rows split into interior rows (owned
+    columns only) and boundary rows, its own Vanka patches split into interior
+    patches (owned dofs only) and boundary patches, relaxation workspaces.
+    The interior parts run while the halo exchange is in flight."""
 
     def __init__(self, be, rs, ll, mrelax):
         nl = rs.nl
-        self.K = be.matrix(nl, nl, ll.rows_rp, ll.rows_ci, ll.rows_v)
-        self.f = be.vanka(nl, (ll.ext_rp, ll.ext_ci, ll.ext_v), ll.patches, rs.n_u_loc,
-                          ll.weights)
+        self.K_int = be.matrix(nl, nl, *ll.rows_int)
+        self.K_bnd = be.matrix(nl, nl, *ll.rows_bnd) if len(ll.rows_bnd[1]) else None
+        ext = (ll.ext_rp, ll.ext_ci, ll.ext_v)
+        self.f_int = self.f_bnd = None
+        if len(ll.patches_int[0]) > 1:
+            self.f_int = be.vanka(nl, ext, ll.patches_int, rs.n_u_loc, ll.weights)
+        if len(ll.patches_bnd[0]) > 1:
+            self.f_bnd = be.vanka(nl, ext, ll.patches_bnd, rs.n_u_loc, ll.weights)
+        k = be.matrix(nl, nl, ll.rows_rp, ll.rows_ci, ll.rows_v)
+        self.norm_inf_local = be.norm_inf(k)
+        del k
         self.kry = _Krylov(be, nl, mrelax)
         self.r = be.vec(nl)
         self.corr = be.vec(nl)
@@ -234,30 +261,48 @@ class DistStep:
         self.k0 = _Level(be, rs, rs.levels["K0"], mrelax)
 
     def step(self, x, delta, y):
-        self.vanka(self.k0, x, delta)
-        self.be.spmv(self.k0.K, x, y)    # x's ghosts are fresh from the Vanka halo
+        """delta = apply_vanka(x), y = K0 x: interior patches and rows under
+        the forward halo, boundary rows under the reverse halo."""
+        be, L = self.be, self.k0
+        h = self.halo_start(x)
+        self._vanka_int(L, x, delta)
+        be.spmv(L.K_int, x, y)
+        self.halo_finish(h, x)
+        if L.f_bnd is not None:
+            be.vanka_add(L.f_bnd, x, delta)
+        h = self.reduce_start(delta)
+        if L.K_bnd is not None:
+            be.spmv(L.K_bnd, x, y, "add")
+        self.reduce_finish(h, delta)
 
     # ---- communication ------------------------------------------------
-    def halo(self, x):
-        """Forward halo: ghost entries of x from their owners."""
+    def halo_start(self, x):
+        """Forward halo, posted: owned values the neighbours read as ghosts."""
         be, ix, buf = self.be, self._ix, self._buf
         for q, i in ix["fwd_send"].items():
             be.gather(i, x, buf["fwd_send"][q])
-        self.comm.exchange(buf["fwd_send"], buf["fwd_recv"])
-        for q in sorted(ix["fwd_recv"]):
-            be.scatter(ix["fwd_recv"][q], buf["fwd_recv"][q], x, False)
+        return self.comm.start(buf["fwd_send"], buf["fwd_recv"])
 
-    def halo_reduce(self, d):
-        """Reverse halo: partial sums at ghosts added by their owners, in rank order."""
+    def halo_finish(self, h, x):
+        self.comm.finish(h)
+        for q in sorted(self._ix["fwd_recv"]):
+            self.be.scatter(self._ix["fwd_recv"][q], self._buf["fwd_recv"][q], x, False)
+
+    def reduce_start(self, d):
+        """Reverse halo, posted: partial sums at ghosts to their owners."""
         be, ix, buf = self.be, self._ix, self._buf
         for q, i in ix["rev_send"].items():
             be.gather(i, d, buf["rev_send"][q])
-        self.comm.exchange(buf["rev_send"], buf["rev_recv"])
-        for q in sorted(ix["rev_recv"]):
-            be.scatter(ix["rev_recv"][q], buf["rev_recv"][q], d, True)
+        return self.comm.start(buf["rev_send"], buf["rev_recv"])
 
-    def _norm_inf(self, m):
-        t = self.be.from_host(np.array([self.be.norm_inf(m)]))
+    def reduce_finish(self, h, d):
+        """... added by the owner in rank order."""
+        self.comm.finish(h)
+        for q in sorted(self._ix["rev_recv"]):
+            self.be.scatter(self._ix["rev_recv"][q], self._buf["rev_recv"][q], d, True)
+
+    def _norm_inf(self, L):
+        t = self.be.from_host(np.array([L.norm_inf_local]))
         self.comm.allreduce(t, "max")
         return float(self.be.to_host(t)[0])
 
@@ -270,14 +315,35 @@ class DistStep:
 
     # ---- operators ------------------------------------------------------
     def apply_op(self, L, x, y, epi="store", aux=None):
-        self.halo(x)
-        self.be.spmv(L.K, x, y, epi, aux)
+        """y = K x (store), aux - K x (resid) or y + K x (add) on the owned
+        rows; interior rows under the forward halo of x."""
+        be = self.be
+        h = self.halo_start(x)
+        be.spmv(L.K_int, x, y, epi, aux)
+        self.halo_finish(h, x)
+        if L.K_bnd is not None:
+            if epi == "resid":      # boundary rows: y = y - K_b x (y holds aux there)
+                be.spmv(L.K_bnd, x, y, "resid", y)
+            else:
+                be.spmv(L.K_bnd, x, y, "add")
+
+    def _vanka_int(self, L, v, z):
+        if L.f_int is not None:
+            self.be.vanka_apply(L.f_int, v, z)
+        else:
+            self.be.axpby(0.0, z, 0.0, z)
 
     def vanka(self, L, v, z):
-        self.halo(v)
-        self.be.vanka_apply(L.f, v, z)
-        self.halo_reduce(z)
-
+        """z = apply_vanka(v) over the partition: interior patches under the
+        forward halo, boundary patches added after it, partial sums at ghosts
+        to their owners."""
+        h = self.halo_start(v)
+        self._vanka_int(L, v, z)
+        self.halo_finish(h, v)
+        if L.f_bnd is not None:
+            self.be.vanka_add(L.f_bnd, v, z)
+        h = self.reduce_start(z)
+        self.reduce_finish(h, z)
 
 
 class DistSolver(DistStep):
@@ -302,7 +368,7 @@ class DistSolver(DistStep):
         self.b0, self.x0 = be.vec(nl), be.vec(nl)
         self.gam_rc, self.gam_e = be.vec(nl), be.vec(nl)
         self.nlev = len(levels)
-        norm0 = self._norm_inf(self.l0.K)
+        norm0 = self._norm_inf(self.l0)
         if self.nlev > 1:
             self.P = be.matrix(nl, rs.n1, rs.p_rp, rs.p_ci, rs.p_v)
             self.R = be.matrix(rs.n1, nl, rs.r_rp, rs.r_ci, rs.r_v)

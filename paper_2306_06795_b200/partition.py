@@ -94,6 +94,12 @@ class LocalLevel:
     patches: tuple           # (pptr, pidx, vptr, vidx, nx) of the rank's own patches, local ids
     weights: np.ndarray      # global PoU weights at the local dofs
     nxyz: tuple              # global (n_x, n_y, n_p) of the level
+    # interior / boundary split for overlapping the halo exchanges: interior
+    # patches touch owned dofs only, interior rows read owned columns only
+    patches_int: tuple = None
+    patches_bnd: tuple = None
+    rows_int: tuple = None   # (rp, ci, v), nl x nl, boundary rows empty
+    rows_bnd: tuple = None   # (rp, ci, v), nl x nl, interior rows empty
 
 
 @dataclass
@@ -245,8 +251,10 @@ def build_rank_systems(nranks, k0, l0, p0, nxyz0, nxyz_l0, ranks=None):
                   g2l[vidx[vptr[lo]:vptr[hi]]].astype(np.int32),
                   nx[lo:hi].astype(np.int32))
             assert (lp[1] >= 0).all() and (lp[3] >= 0).all()
-            rs.levels[name] = LocalLevel(rrp, rci, rv, erp, eci, ev, lp, w[l2g].copy(),
-                                         (n_x, n_y, n_p))
+            ll = LocalLevel(rrp, rci, rv, erp, eci, ev, lp, w[l2g].copy(), (n_x, n_y, n_p))
+            ll.patches_int, ll.patches_bnd = _split_patches(lp, owned.astype(bool))
+            ll.rows_int, ll.rows_bnd = _split_rows(rrp, rci, rv, owned.astype(bool))
+            rs.levels[name] = ll
         if p0 is not None:
             rs.n1 = int(p0.ncols)
             prp, pci, pv = _local_csr_cols_global(p0, l2g, owned.astype(bool))
@@ -277,3 +285,46 @@ def _transpose(nrows, ncols, rp, ci, v):
     trp = np.zeros(ncols + 1, dtype=np.int64)
     np.cumsum(np.bincount(ci, minlength=ncols), out=trp[1:])
     return trp.astype(np.int32), rowid[order].astype(np.int32), np.asarray(v)[order].copy()
+
+
+def _select_patches(pt, keep):
+    """The patches with keep[i], in their order (local patch lists)."""
+    pptr, pidx, vptr, vidx, nx = pt
+    ids = np.nonzero(keep)[0]
+    pl = (pptr[ids + 1] - pptr[ids]).astype(np.int64)
+    vl = (vptr[ids + 1] - vptr[ids]).astype(np.int64)
+    npp = np.zeros(len(ids) + 1, dtype=np.int32)
+    nvp = np.zeros(len(ids) + 1, dtype=np.int32)
+    np.cumsum(pl, out=npp[1:])
+    np.cumsum(vl, out=nvp[1:])
+    return (npp, pidx[_ranges(pptr[ids], pl)].astype(np.int32), nvp,
+            vidx[_ranges(vptr[ids], vl)].astype(np.int32), nx[ids].astype(np.int32))
+
+
+def _split_patches(pt, owned):
+    """(interior, boundary): a patch is interior when every dof it touches is
+    owned -- it needs no ghost values and contributes to no other rank."""
+    pptr, pidx, vptr, vidx, _ = pt
+    npatch = len(pptr) - 1
+    bad = np.zeros(npatch, dtype=bool)
+    pid_v = np.repeat(np.arange(npatch), np.diff(vptr))
+    pid_p = np.repeat(np.arange(npatch), np.diff(pptr))
+    np.logical_or.at(bad, pid_v, ~owned[vidx])
+    np.logical_or.at(bad, pid_p, ~owned[pidx])
+    return _select_patches(pt, ~bad), _select_patches(pt, bad)
+
+
+def _split_rows(rp, ci, v, owned):
+    """(interior, boundary) copies of an nl x nl CSR: a row is interior when
+    all its columns are owned; each copy keeps the other rows empty."""
+    nl = len(rp) - 1
+    rowid = np.repeat(np.arange(nl), np.diff(rp))
+    bad = np.zeros(nl, dtype=bool)
+    np.logical_or.at(bad, rowid, ~owned[ci])
+    out = []
+    for sel in (~bad, bad):
+        keep = sel[rowid]
+        nrp = np.zeros(nl + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rowid[keep], minlength=nl), out=nrp[1:])
+        out.append((nrp.astype(np.int32), ci[keep].copy(), v[keep].copy()))
+    return out[0], out[1]

@@ -107,6 +107,9 @@ class CheckerBackend:
     def vanka_apply(self, f, r, delta):
         delta.copy_(torch.from_numpy(f.apply(r.numpy())))
 
+    def vanka_add(self, f, r, x):
+        x.copy_(x + 1.0 * torch.from_numpy(f.apply(r.numpy())))
+
     def coarse_apply(self, h, b, x):
         x.copy_(torch.from_numpy(h.apply(b.numpy())))
 

@@ -159,6 +159,14 @@ def test_rank_plans_are_consistent():
                 assert not rs.owned[idx].any() and rss[q_].owned[rss[q_].fwd_send[rs.rank]].all()
             for q_, idx in rs.rev_send.items():
                 assert np.array_equal(rs.l2g[idx], rss[q_].l2g[rss[q_].rev_recv[rs.rank]])
+            # interior / boundary split: a partition of the patches and rows
+            pi, pb = ll.patches_int, ll.patches_bnd
+            assert len(pi[0]) - 1 + len(pb[0]) - 1 == len(pptr) - 1
+            assert rs.owned[pi[3]].all() and rs.owned[pi[1]].all()
+            ri, rb = ll.rows_int, ll.rows_bnd
+            assert np.array_equal(np.diff(ri[0]) + np.diff(rb[0]), np.diff(ll.rows_rp))
+            assert rs.owned[ri[1]].all()
             if world == 1:
                 assert rs.ghost_count() == 0
+                assert len(pb[0]) == 1 and len(rb[1]) == 0
         assert (seen == 1).all()
