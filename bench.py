@@ -142,6 +142,30 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+_JSON_FD = None
+
+
+def quiet_stdout():
+    """Route fd 1 to stderr for the whole run (NCCL prints its version banner
+    to stdout from inside communicator creation, also for the lazily created
+    point-to-point communicators) and keep the original stdout for the one
+    JSON line."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line)
+
+
 def dist_setup():
     # keep rank 0's stdout to the one JSON line: NCCL prints its version
     # banner to stdout at NCCL_DEBUG=VERSION/INFO (set SAG_NCCL_DEBUG to see it)
@@ -261,7 +285,7 @@ def run_reference(args, ws, rank):
                 "d2h_bytes_per_step": 0},
         "setup_s": setup_s,
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 # ------------------------------------------------------- GPU arm, N > 1
@@ -423,7 +447,7 @@ def run_dist(args, ws, rank, local):
             out["solve"] = solve
         if clk:
             out["clocks"] = clk
-        print(json.dumps(out))
+        emit(out)
     if own_pg:
         torch.cuda.synchronize(dev)
         dist.destroy_process_group()
@@ -586,7 +610,7 @@ def run_ours(args, ws, rank, local):
                                "sample": f"{done} whole steps (apply_vanka + spmv on K0) of the "
                                          f"reference build (oracle/_ref), {threads} threads"}
     if rank == 0:
-        print(json.dumps(out))
+        emit(out)
 
 
 def main():
@@ -601,6 +625,7 @@ def main():
     ap.add_argument("--dist", action="store_true",
                     help="use the partitioned (halo-exchange) step even at N = 1")
     args = ap.parse_args()
+    quiet_stdout()
     ws, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference(args, ws, rank)
