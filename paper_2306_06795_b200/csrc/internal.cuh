@@ -91,6 +91,11 @@ struct Vanka {
   bool w_ext = false;     // w set by sag_vanka_set_weights (else 1/multiplicity on the fly)
   DevBuf<int> dof_ptr;    // n + 1
   DevBuf<int> dof_slot;   // nslots
+  // dof-ordered results (seq): each blob also carries, after its dof indices,
+  // the position of each local result in the dof-sorted order (dof, then
+  // patch), so the patch kernel writes there and the gather reads every
+  // dof's contributions as one contiguous run -- no dof_slot indirection
+  bool seq = false;
   long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
   long long blob_bytes = 0;
   bool sym = false;  // A^-1 blocks stored as packed symmetrised upper triangles

@@ -600,6 +600,23 @@ static bool velocity_block_symmetric(Ctx& c, const Matrix& k, int n_u) {
   return d <= 1e-12 * a;
 }
 
+__global__ void inverse_perm_kernel(long long n, const int* __restrict__ perm, int* __restrict__ inv) {
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x)
+    inv[perm[t]] = (int)t;
+}
+// blob of patch i: its nv + np result positions right after its dof indices
+__global__ void blob_pos_kernel(int npatch, const int* __restrict__ vptr,
+                                const int* __restrict__ pptr, const long long* __restrict__ ibase,
+                                const int* __restrict__ sbase, const int* __restrict__ pos,
+                                int* __restrict__ I) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npatch; i += gridDim.x * blockDim.x) {
+    const int cnt = (vptr[i + 1] - vptr[i]) + (pptr[i + 1] - pptr[i]);
+    int* dst = I + ibase[i] + cnt;
+    for (int e = 0; e < cnt; ++e) dst[e] = pos[sbase[i] + e];
+  }
+}
+
 std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches& p, int n_u) {
   SAG_REQUIRE(k.nrows == k.ncols, SAG_DIMENSION_MISMATCH, "factor_patches: K must be square");
   SAG_REQUIRE(p.max_np <= 4, SAG_ERROR, "factor_patches: at most 4 pressure seeds per patch");
@@ -720,6 +737,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     // class key 4 R + (lanes per patch: 32 / 16 / 8 -> 0 / 1 / 2); small
     // paired patches go to the sub-warp kernel (several patches per warp)
     const bool subwarp = f->pairs && env_int("SAG_VANKA_SUBWARP", 1) != 0;
+    f->seq = env_int("SAG_VANKA_SEQGATHER", 1) != 0;
     auto key_of = [&](int i) {
       const int x = f->h_nx[i], y = f->h_nv[i] - x;
       const int rows = std::max(x, y) + (f->pairs ? f->h_np[i] : 0);
@@ -745,7 +763,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     f->rclasses.clear();
     for (int q = 0; q < np_; ++q) {
       const int i = order[q];
-      long long bytes = 16 + 8 * ndbl(i) + 4 * (f->h_nv[i] + f->h_np[i]);
+      long long bytes = 16 + 8 * ndbl(i) + 4 * (f->h_nv[i] + f->h_np[i]) * (f->seq ? 2 : 1);
       bytes = (bytes + 15) / 16 * 16;
       h_hoff[i] = off[q];
       off[q + 1] = off[q] + bytes;
@@ -860,6 +878,17 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
       throw Error(SAG_SINGULAR_PATCH,
                   "factor_patches: singular velocity or Schur block in patch " + std::to_string(herr));
   }
+  // dof-ordered result positions into the blobs (Vanka::seq): position of
+  // slot t in the dof-sorted order = its rank in dof_slot
+  if (f->seq && slots > 0) {
+    DevBuf<int> pos(slots);
+    inverse_perm_kernel<<<grid_for(c, slots), 256, 0, c.stream>>>(slots, f->dof_slot.p, pos.p);
+    SAG_LAUNCHED(c);
+    blob_pos_kernel<<<grid_for(c, np_), 256, 0, c.stream>>>(
+        np_, p.vptr.p, p.pptr.p, dibase.p, dsbase.p, pos.p, reinterpret_cast<int*>(f->blob.p));
+    SAG_LAUNCHED(c);
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  }
   return f;
 }
 
@@ -888,6 +917,9 @@ struct PatchView {
   bool paired;
   const double *Ax, *Ay, *U, *Bh, *Si;
   const int* idx;
+  const int* pos;  // dof-ordered result positions (Vanka::seq), after idx
+  // where local result i goes: its dof-ordered position, or slot sbase + i
+  __device__ __forceinline__ int opos(int seq, int i) const { return seq ? pos[i] : sbase + i; }
 };
 template <bool SYM>
 __device__ __forceinline__ PatchView patch_view(const unsigned char* B, bool pairs) {
@@ -907,6 +939,7 @@ __device__ __forceinline__ PatchView patch_view(const unsigned char* B, bool pai
     v.Bh = v.U + 2 * v.np * v.m;
     v.Si = v.Bh + 2 * v.np * v.m;
     v.idx = reinterpret_cast<const int*>(v.Si + v.np * v.np);
+    v.pos = v.idx + v.nv + v.np;
     return v;
   }
   v.Ay = v.Ax + (SYM ? v.nx * (v.nx + 1) / 2 : v.nx * v.nx);
@@ -914,6 +947,7 @@ __device__ __forceinline__ PatchView patch_view(const unsigned char* B, bool pai
   v.Bh = v.U + v.np * v.nv;
   v.Si = v.Bh + v.np * v.nv;
   v.idx = reinterpret_cast<const int*>(v.Si + v.np * v.np);
+  v.pos = v.idx + v.nv + v.np;
   return v;
 }
 
@@ -931,7 +965,7 @@ template <int R, bool SYM, int NPM>
 __global__ void __launch_bounds__(256) vanka_patch_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, int sb_len, int pairs, const double* __restrict__ r,
-    double* __restrict__ out, const int* gate) {
+    double* __restrict__ out, int seq, const int* gate) {
   if (gate && *gate) return;
   constexpr int G = 2 * R + 1;  // gathered values per lane (nv + np <= 32 G)
   // paired blobs (vanka_paired) exist only on symmetric levels, R <= 2
@@ -1021,7 +1055,7 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
         g[q] = i < gn ? __ldg(r + w.idx[i]) : 0.0;
       }
     }
-    const int nx = v.nx, ny = v.ny, np = NPM == 1 ? 1 : v.np, nv = v.nv, sbase = v.sbase;
+    const int nx = v.nx, ny = v.ny, np = NPM == 1 ? 1 : v.np, nv = v.nv;
     if (kPair && v.paired) {
       // paired patch: virtual row i = lane + 32 q (q < R) is matrix row i
       // (i < m) of both components -- one 16-byte load of (A_x, A_y)(i, j) and
@@ -1068,7 +1102,7 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
 #pragma unroll
         for (int e = 0; e < NPM; ++e)
           if (e < npp) xl[q] = fma(v.Si[ar * npp + e], sb[2 * mm + e], xl[q]);
-        if (i >= mm && i < mm + npp) out[sbase + nv + ar] = xl[q];
+        if (i >= mm && i < mm + npp) out[v.opos(seq, nv + ar)] = xl[q];
       }
       double xp[NPM];
 #pragma unroll
@@ -1097,8 +1131,8 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
               ox = fma(u.x, xp[e], ox);
               oy = fma(u.y, xp[e], oy);
             }
-          if (i < nx) out[sbase + i] = ox;
-          if (i < ny) out[sbase + nx + i] = oy;
+          if (i < nx) out[v.opos(seq, i)] = ox;
+          if (i < ny) out[v.opos(seq, nx + i)] = oy;
         }
       }
     } else {
@@ -1162,7 +1196,7 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
           for (int q = 0; q < NPM; ++q)
             if (q < np) sp = fma(Si[a * np + q], sb[nv + q], sp);
           xp[a] = sp + part;
-          if (lane == 0) out[sbase + nv + a] = xp[a];
+          if (lane == 0) out[v.opos(seq, nv + a)] = xp[a];
         }
       }
       // x_u = t + U_hat x_p (vanka.cpp:176-180)
@@ -1174,14 +1208,14 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
 #pragma unroll
           for (int a = 0; a < NPM; ++a)
             if (a < np) t = fma(U[a * nv + i], xp[a], t);
-          out[sbase + i] = t;
+          out[v.opos(seq, i)] = t;
         }
         if (i < ny) {
           double t = ty[q];
 #pragma unroll
           for (int a = 0; a < NPM; ++a)
             if (a < np) t = fma(U[a * nv + nx + i], xp[a], t);
-          out[sbase + nx + i] = t;
+          out[v.opos(seq, nx + i)] = t;
         }
       }
     }
@@ -1213,7 +1247,7 @@ template <int LPP, int NPM>
 __global__ void __launch_bounds__(256) vanka_subwarp_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, int sb_len, const double* __restrict__ r,
-    double* __restrict__ out, const int* gate) {
+    double* __restrict__ out, int seq, const int* gate) {
   if (gate && *gate) return;
   constexpr int P = 32 / LPP;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1335,7 +1369,7 @@ __global__ void __launch_bounds__(256) vanka_subwarp_kernel(
 #pragma unroll
       for (int e = 0; e < NPM; ++e)
         if (e < npp) xl = fma(v.Si[ar * npp + e], sb[2 * mm + e], xl);
-      if (gl >= mm && gl < mm + npp) out[v.sbase + v.nv + ar] = xl;
+      if (gl >= mm && gl < mm + npp) out[v.opos(seq, v.nv + ar)] = xl;
     }
     double xp[NPM];
 #pragma unroll
@@ -1351,8 +1385,8 @@ __global__ void __launch_bounds__(256) vanka_subwarp_kernel(
           ox = fma(u.x, xp[e], ox);
           oy = fma(u.y, xp[e], oy);
         }
-      if (gl < v.nx) out[v.sbase + gl] = ox;
-      if (gl < v.ny) out[v.sbase + v.nx + gl] = oy;
+      if (gl < v.nx) out[v.opos(seq, gl)] = ox;
+      if (gl < v.ny) out[v.opos(seq, v.nx + gl)] = oy;
     }
     // publish the prefetched r of the next group
     if (wvalid) {
@@ -1412,6 +1446,48 @@ __global__ void vanka_gather_kernel(int n, const int* __restrict__ dof_ptr,
     else
       delta[d] = acc;
   }
+}
+
+// The gather of dof-ordered results (Vanka::seq): d's contributions are the
+// contiguous run out[dof_ptr[d] .. dof_ptr[d+1]) (ascending patch order), so
+// neighbouring threads read neighbouring runs -- a coalesced stream with no
+// slot-id indirection. Same arithmetic as vanka_gather_kernel.
+__global__ void vanka_gather_seq_kernel(int n, const int* __restrict__ dof_ptr,
+                                        const double* __restrict__ out,
+                                        const double* __restrict__ w, double* __restrict__ delta,
+                                        double* __restrict__ xadd, double omega, const int* gate) {
+  if (gate && *gate) return;
+  constexpr int U = 8;
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const double xo = xadd ? xadd[d] : 0.0;
+    const int s0 = __ldg(dof_ptr + d), s1 = __ldg(dof_ptr + d + 1);
+    const double wd = w ? __ldg(w + d) : (s1 > s0 ? 1.0 / (double)(s1 - s0) : 0.0);
+    double acc = 0.0;
+    for (int sb = s0; sb < s1; sb += U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = sb + u < s1 ? __ldcs(out + sb + u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (sb + u < s1) acc = __dadd_rn(acc, __dmul_rn(wd, v[u]));
+    }
+    if (xadd)
+      xadd[d] = xo + omega * acc;
+    else
+      delta[d] = acc;
+  }
+}
+
+static void launch_gather(Ctx& c, const Vanka& f, double* delta, double* xadd, double omega,
+                          const int* gate) {
+  const double* w = f.w_ext ? f.w.p : nullptr;
+  if (f.seq)
+    vanka_gather_seq_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(f.n, f.dof_ptr.p, f.out.p, w,
+                                                                    delta, xadd, omega, gate);
+  else
+    vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(
+        f.n, f.dof_ptr.p, f.dof_slot.p, f.out.p, w, delta, xadd, omega, gate);
+  SAG_LAUNCHED(c);
 }
 
 // -------------------------------------- streamed thread-per-patch apply --
@@ -1789,7 +1865,7 @@ static void launch_subwarp(Ctx& c, const Vanka& f, const Vanka::RClass& cl, cons
                                                           (long long)occ * c.num_sms));
   kern<<<blocks, warps * 32, smem, c.stream>>>(npatch, f.blob.p, f.off.p + cl.k0,
                                                 (int)cl.slot_bytes, nstage, sb_len, r, f.out.p,
-                                                gate);
+                                                f.seq ? 1 : 0, gate);
   SAG_LAUNCHED(c);
 }
 
@@ -1803,7 +1879,7 @@ static void launch_patch(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const 
   const ApplyCfg a = apply_cfg<R, SYM, NPM>(c, f, npatch, (int)cl.slot_bytes);
   vanka_patch_kernel<R, SYM, NPM><<<a.blocks, a.warps * 32, a.smem, c.stream>>>(
       npatch, f.blob.p, f.off.p + cl.k0, (int)cl.slot_bytes, a.nstage, a.sb_len,
-      f.pairs ? 1 : 0, r, f.out.p, gate);
+      f.pairs ? 1 : 0, r, f.out.p, f.seq ? 1 : 0, gate);
   SAG_LAUNCHED(c);
 }
 
@@ -1848,29 +1924,20 @@ static void launch_patch_any(Ctx& c, const Vanka& f, const double* r, const int*
 
 void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta, const int* gate) {
   launch_patch_any(c, f, r, gate);
-  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(
-      f.n, f.dof_ptr.p, f.dof_slot.p, f.out.p, f.w_ext ? f.w.p : nullptr, delta, nullptr, 1.0,
-      gate);
-  SAG_LAUNCHED(c);
+  launch_gather(c, f, delta, nullptr, 1.0, gate);
 }
 
 void vanka_apply_stage(Ctx& c, const Vanka& f, const double* r, double* delta, int stage) {
   if (stage == 1) {
     launch_patch_any(c, f, r, nullptr);
   } else {
-    vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(
-        f.n, f.dof_ptr.p, f.dof_slot.p, f.out.p, f.w_ext ? f.w.p : nullptr, delta, nullptr, 1.0,
-        nullptr);
-    SAG_LAUNCHED(c);
+    launch_gather(c, f, delta, nullptr, 1.0, nullptr);
   }
 }
 
 void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega) {
   launch_patch_any(c, f, r, nullptr);
-  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(
-      f.n, f.dof_ptr.p, f.dof_slot.p, f.out.p, f.w_ext ? f.w.p : nullptr, nullptr, x, omega,
-      nullptr);
-  SAG_LAUNCHED(c);
+  launch_gather(c, f, nullptr, x, omega, nullptr);
 }
 
 // The reference's factor layout (vanka.hpp:31-33), unpacked on the host for
