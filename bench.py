@@ -332,7 +332,7 @@ def run_dist(args, ws, rank, local):
     ctx = S.Context(local, stream=stream.cuda_stream)
     comm = Comm(dist, torch)
     with torch.cuda.stream(stream):
-        be = LibsagBackend(ctx, dev, torch)
+        be = LibsagBackend(ctx, dev, torch, stream)
         t2 = time.perf_counter()
         step = DistStep(rs, be, comm)
         torch.cuda.synchronize(dev)
@@ -410,6 +410,8 @@ def run_dist(args, ws, rank, local):
             torch.cuda.synchronize(dev)
             t_solve = dist_max(time.perf_counter() - ts, ws)
             solve = {"gpu_s": t_solve, "iterations": rep.iterations,
+                     "prec_cuda_graph": solver.graph is not None,
+                     "prec_graph_error": solver.graph_error,
                      "final_relative_residual": rep.final_relative_residual,
                      "converged": rep.converged, "setup_s": solver_setup_s,
                      "path": "dsolve.DistSolver (partitioned K0/L0, agglomerated coarse "

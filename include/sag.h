@@ -296,8 +296,15 @@ int sag_dot_async(sag_ctx* ctx, int n, const double* a, const double* b,
                   const unsigned char* mask, double* out);
 /* y = y + sign * s[0] x  (MGS update w -= h_ij v_i, krylov.cpp:66). */
 int sag_axpy_async(sag_ctx* ctx, int n, const double* s, double sign, const double* x, double* y);
-/* y = x / d with d = s[0] or sqrt(s[0])  (v = r / ||r||, krylov.cpp:47-48, :71). */
+/* y = x / d with d = s[0] or sqrt(s[0])  (v = r / ||r||, krylov.cpp:47-48, :71);
+ * y = 0 when d == 0 (a zero residual, whose Krylov step the reference skips). */
 int sag_div_async(sag_ctx* ctx, int n, const double* x, const double* s, int take_sqrt, double* y);
+/* The coefficient y_0 of a one-step FGMRES from a zero guess (vanka_relax with
+ * nu = 1, vanka.cpp:199-208 -> krylov.cpp:42-110): from ||r||^2, h_00 and
+ * ||w||^2 after the MGS step, the Givens rotation and back substitution;
+ * y_0[0] = 0 when r = 0. Device scalars: a relaxation needs no host sync. */
+int sag_fgmres1_coef_async(sag_ctx* ctx, const double* ssq_r, const double* h00,
+                           const double* ssq_w, double* y0);
 /* y = x - sum[0] / count  (pressure-mean projection, preconditioner.cpp:235-240). */
 int sag_sub_mean_async(sag_ctx* ctx, int n, const double* x, const double* sum, double count,
                        double* y);

@@ -182,6 +182,7 @@ SIGNATURES = {
     "sag_axpy_async": (C.c_int, [vp, C.c_int, vp, C.c_double, vp, vp]),
     "sag_div_async": (C.c_int, [vp, C.c_int, vp, vp, C.c_int, vp]),
     "sag_sub_mean_async": (C.c_int, [vp, C.c_int, vp, vp, C.c_double, vp]),
+    "sag_fgmres1_coef_async": (C.c_int, [vp, vp, vp, vp, vp]),
     "sag_axpby_async": (C.c_int, [vp, C.c_int, C.c_double, vp, C.c_double, vp]),
     "sag_gather_async": (C.c_int, [vp, C.c_int, vp, vp, vp]),
     "sag_scatter_async": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int]),

@@ -999,11 +999,33 @@ __global__ void axpy_dev_kernel(int n, const double* s, double sign, const doubl
   ew4(n, [&](int i) { return make_double2(y[i], x[i]); },
       [&](int i, double2 v) { y[i] = sign < 0.0 ? v.x - h * v.y : v.x + h * v.y; });
 }
-// y = x / d, d = *s or sqrt(*s)   (v_0 = r / ||r||, krylov.cpp:47-48)
+// y = x / d, d = *s or sqrt(*s)   (v_0 = r / ||r||, krylov.cpp:47-48); y = 0
+// when d == 0 (a zero residual, whose Krylov step the reference skips)
 __global__ void div_dev_kernel(int n, const double* __restrict__ x, const double* s, int take_sqrt,
                                double* __restrict__ y) {
   const double d = take_sqrt ? sqrt(*s) : *s;
-  ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = v / d; });
+  ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = d != 0.0 ? v / d : 0.0; });
+}
+// One-step FGMRES coefficient (krylov.cpp:42-110 with m = max_iters = 1, tol
+// 0, zero guess): from ||r||^2, h_00 = (A z_0, v_0) and ||w||^2 after the MGS
+// step, the Givens rotation and the back substitution give y_0 (x += y_0 z_0);
+// 0 when r = 0 (the reference returns before the step).
+__global__ void fgmres1_coef_kernel(const double* ssq_r, const double* h00p, const double* ssq_w,
+                                    double* y0) {
+  const double beta = sqrt(*ssq_r), h00 = *h00p, h10 = sqrt(*ssq_w);
+  if (beta == 0.0) {
+    *y0 = 0.0;
+    return;
+  }
+  const double denom = hypot(h00, h10);
+  double cs = 1.0, sn = 0.0;
+  if (denom > 0.0) {
+    cs = h00 / denom;
+    sn = h10 / denom;
+  }
+  const double hjj = cs * h00 + sn * h10;
+  const double g0 = cs * beta;
+  *y0 = g0 / hjj;
 }
 // y = x - (*sum) / count   (project_pressure, preconditioner.cpp:235-240)
 __global__ void sub_mean_kernel(int n, const double* __restrict__ x, const double* sum,
@@ -1306,6 +1328,17 @@ int sag_div_async(sag_ctx* ctx, int n, const double* x, const double* s, int tak
     require_dev({x, s, y});
     auto& c = ctx->c;
     sag::div_dev_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, x, s, take_sqrt, y);
+    SAG_LAUNCHED(c);
+  });
+}
+
+int sag_fgmres1_coef_async(sag_ctx* ctx, const double* ssq_r, const double* h00,
+                           const double* ssq_w, double* y0) {
+  return guard([&] {
+    NOTNULL(ctx);
+    require_dev({ssq_r, h00, ssq_w, y0});
+    auto& c = ctx->c;
+    sag::fgmres1_coef_kernel<<<1, 1, 0, c.stream>>>(ssq_r, h00, ssq_w, y0);
     SAG_LAUNCHED(c);
   });
 }

@@ -1270,8 +1270,7 @@ int sag_dc_apply(sag_ctx* ctx, sag_dc* h, const double* r, double* z) {
     launch_copy(c, d.n0, ri.d, d.din.p);
     dc_apply_graph(c, d);
     launch_copy(c, d.n0, d.dout.p, zo.d);
-    zo.finish();
-    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    zo.finish();  // host output: copied back and synchronised; device: stream-ordered
   });
 }
 

@@ -95,9 +95,12 @@ class LibsagBackend:
     """Rank-local kernels on the GPU: libsag (include/sag.h) on device
     pointers of torch tensors, all on the context's (torch-owned) stream."""
 
-    def __init__(self, ctx, device, torch):
+    def __init__(self, ctx, device, torch, stream=None):
+        """stream: the torch.cuda.Stream libsag's context launches on (needed
+        to capture the preconditioner into a CUDA graph)."""
         from . import lib, _check  # noqa: F401  (fails loudly without libsag)
         self.ctx, self.device, self.torch = ctx, device, torch
+        self.stream = stream
         self.L, self._check = lib(), _check
         import ctypes as C
         self.C = C
@@ -181,6 +184,10 @@ class LibsagBackend:
     def sub_mean(self, x, s, count, y):
         self._check(self.L.sag_sub_mean_async(self.ctx.h, y.numel(), self.p(x), self.p(s),
                                               float(count), self.p(y)))
+
+    def fgmres1_coef(self, ssq_r, h00, ssq_w, y0):
+        self._check(self.L.sag_fgmres1_coef_async(self.ctx.h, self.p(ssq_r), self.p(h00),
+                                                  self.p(ssq_w), self.p(y0)))
 
     def axpby(self, a, x, b, y):
         self._check(self.L.sag_axpby_async(self.ctx.h, y.numel(), float(a), self.p(x), float(b),
@@ -367,6 +374,13 @@ class DistSolver(DistStep):
         self.t = be.vec(nl)
         self.b0, self.x0 = be.vec(nl), be.vec(nl)
         self.gam_rc, self.gam_e = be.vec(nl), be.vec(nl)
+        self.gin, self.gout = be.vec(nl), be.vec(nl)
+        # CUDA graph of the preconditioner: NCCL (or a single rank) and
+        # sync-free relaxations only; gloo staging synchronises with the host
+        self.graph, self.graph_error, self._napply = None, None, 0
+        self.stream = getattr(be, "stream", None)
+        self.use_graph = (self.stream is not None and not comm.stage
+                          and max(cfg.nu1, cfg.nu2) <= 1 and cfg.gamma >= 1)
         self.nlev = len(levels)
         norm0 = self._norm_inf(self.l0)
         if self.nlev > 1:
@@ -493,12 +507,33 @@ class DistSolver(DistStep):
         else:
             self.apply_op(L, x, L.r, "resid", b)
             r = L.r
+        if nu == 1:
+            self._relax1(L, x, r, x_zero)
+            return
         prec = lambda v, z: self.vanka(L, v, z)  # noqa: E731
         if x_zero:
             self.fgmres(L, r, x, prec, 0.0, nu, nu, L.kry, x_zero=True, final=False)
         else:
             self.fgmres(L, r, L.corr, prec, 0.0, nu, nu, L.kry, x_zero=True, final=False)
             self.be.axpby(1.0, L.corr, 1.0, x)
+
+    def _relax1(self, L, x, r, x_zero):
+        """nu = 1: x += y_0 z_0 with the one-step FGMRES on device scalars
+        (krylov.cpp:42-110 with m = 1, tol 0): no host synchronisation, so a
+        DC application is one stream of kernels and collectives."""
+        be, k = self.be, L.kry
+        sc = k.sc
+        self.dot(r, r, sc[0:1])                       # ||r||^2
+        be.div_s(r, sc[0:1], True, k.V[0])            # v_0 = r / ||r||
+        self.vanka(L, k.V[0], k.Z[0])                 # z_0 = M v_0
+        self.apply_op(L, k.Z[0], k.w)                 # w = K z_0
+        self.dot(k.w, k.V[0], sc[1:2])                # h_00
+        be.axpy_s(sc[1:2], -1.0, k.V[0], k.w)         # w -= h_00 v_0
+        self.dot(k.w, k.w, sc[2:3])                   # ||w||^2 = h_10^2
+        be.fgmres1_coef(sc[0:1], sc[1:2], sc[2:3], sc[3:4])
+        if x_zero:
+            be.axpby(0.0, x, 0.0, x)
+        be.axpy_s(sc[3:4], 1.0, k.Z[0], x)            # x += y_0 z_0 (vanka.cpp:208)
 
     # ---- V-cycle level 0 (preconditioner.cpp:57-81) ---------------------------
     def cycle0(self, b, x, skip_finest):
@@ -574,13 +609,42 @@ class DistSolver(DistStep):
             self.be.axpby(1.0, src[:nu], 0.0, dst[:nu])
         self.be.sub_mean(src[nu:], s, float(self.rs.n_p), dst[nu:])
 
-    def apply_prec(self, v, z):
+    def _prec_body(self):
+        """gin -> gout: project, DC apply, project (preconditioner.cpp:241-250)."""
         if self.cfg.enclosed_flow:
-            self.project(v, self.din, 0)
+            self.project(self.gin, self.din, 0)
             self.dc_apply(self.din, self.dout)
-            self.project(self.dout, z, 1)
+            self.project(self.dout, self.gout, 1)
         else:
-            self.dc_apply(v, z)
+            self.dc_apply(self.gin, self.gout)
+
+    def apply_prec(self, v, z):
+        """The preconditioner on fixed buffers; with nu = 1 it contains no
+        host synchronisation, so after one eager application it is captured
+        into a CUDA graph (collectives included) and replayed."""
+        be = self.be
+        be.axpby(1.0, v, 0.0, self.gin)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._prec_body()
+            self._napply += 1
+            if self._napply == 1 and self.use_graph:
+                self._capture()
+        be.axpby(1.0, self.gout, 0.0, z)
+
+    def _capture(self):
+        torch = self.be.torch
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g, stream=self.stream):
+                self._prec_body()
+        except Exception as e:  # noqa: BLE001 -- eager application stays correct
+            self.use_graph = False
+            self.graph_error = repr(e)
+            torch.cuda.synchronize()
+            return
+        self.graph = g
 
     def solve(self, rhs_local, x):
         """rhs_local: backend vector (nl, owned entries valid); x: output (nl)."""

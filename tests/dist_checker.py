@@ -123,7 +123,17 @@ class CheckerBackend:
 
     def div_s(self, x, s, take_sqrt, y):
         d = float(s[0])
-        y.copy_(x / (np.sqrt(d) if take_sqrt else d))
+        d = np.sqrt(d) if take_sqrt else d
+        y.copy_(x / d if d != 0.0 else torch.zeros_like(x))
+
+    def fgmres1_coef(self, ssq_r, h00, ssq_w, y0):
+        beta, h, h10 = np.sqrt(float(ssq_r[0])), float(h00[0]), np.sqrt(float(ssq_w[0]))
+        if beta == 0.0:
+            y0[0] = 0.0
+            return
+        denom = float(np.hypot(h, h10))
+        cs, sn = (h / denom, h10 / denom) if denom > 0.0 else (1.0, 0.0)
+        y0[0] = cs * beta / (cs * h + sn * h10)
 
     def sub_mean(self, x, s, count, y):
         y.copy_(x - float(s[0]) / count)

@@ -56,7 +56,7 @@ def _worker(rank, world, port, n, backend, q):
         stream = torch.cuda.Stream(device=dev)
         ctx = S.Context(0, stream=stream.cuda_stream)
         with torch.cuda.stream(stream):
-            be = LibsagBackend(ctx, dev, torch)
+            be = LibsagBackend(ctx, dev, torch, stream)
             solver = DistSolver(rs, levels, cfg, be, Comm(dist, torch, stage=backend == "gloo"))
             rhs = be.from_host(g["rhs"][rs.l2g])
             x = be.vec(rs.nl)
@@ -65,6 +65,8 @@ def _worker(rank, world, port, n, backend, q):
             torch.cuda.synchronize(dev)
             launches = ctx.launch_count() - l0n
         own = np.nonzero(rs.owned)[0]
+        # the preconditioner runs as a CUDA graph whenever the communicator allows
+        assert (solver.graph is not None) == (backend == "nccl"), solver.graph_error
         q.put((rank, rs.l2g[own], x.cpu().numpy()[own], rep.iterations,
                rep.final_relative_residual, rep.converged, launches))
     finally:
