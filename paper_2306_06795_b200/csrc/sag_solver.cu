@@ -733,8 +733,17 @@ static void check_config(const sag_solver_config& c) {
 
 // DC apply as a CUDA graph over the fixed buffers din -> dout (SV excluded:
 // its mass projection synchronises with the host for convergence).
+// A caller capturing its own CUDA graph on the context stream (a graph launch
+// cannot be captured): the launches go straight into the caller's graph.
+static bool stream_capturing(Ctx& c) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  SAG_CUDA(cudaStreamIsCapturing(c.stream, &st));
+  return st != cudaStreamCaptureStatusNone;
+}
+
 static void dc_apply_graph(Ctx& c, Dc& d) {
-  const bool use_graph = !d.sv && !(getenv("SAG_NO_GRAPH") && atoi(getenv("SAG_NO_GRAPH")));
+  const bool use_graph = !d.sv && !(getenv("SAG_NO_GRAPH") && atoi(getenv("SAG_NO_GRAPH"))) &&
+                         !stream_capturing(c);
   if (!use_graph) {
     dc_apply_dev(c, d, d.din.p, d.dout.p);
     return;
@@ -814,7 +823,8 @@ static void uzawa_apply_dev(Ctx& c, Uzawa& u, const double* r, double* z) {
 
 // Uzawa apply din -> dout captured once into a CUDA graph (fixed sequence).
 static void uzawa_apply_graph(Ctx& c, Uzawa& u) {
-  const bool use_graph = !(getenv("SAG_NO_GRAPH") && atoi(getenv("SAG_NO_GRAPH")));
+  const bool use_graph = !(getenv("SAG_NO_GRAPH") && atoi(getenv("SAG_NO_GRAPH"))) &&
+                         !stream_capturing(c);
   if (!use_graph) {
     uzawa_apply_dev(c, u, u.din.p, u.dout.p);
     return;

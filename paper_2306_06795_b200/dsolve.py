@@ -379,8 +379,12 @@ class DistSolver(DistStep):
         # sync-free relaxations only; gloo staging synchronises with the host
         self.graph, self.graph_error, self._napply = None, None, 0
         self.stream = getattr(be, "stream", None)
+        # (several ranks: collectives inside a captured graph are opt-in,
+        # SAG_DIST_GRAPH=1 -- this build has not been run on more than one GPU)
+        import os
         self.use_graph = (self.stream is not None and not comm.stage
-                          and max(cfg.nu1, cfg.nu2) <= 1 and cfg.gamma >= 1)
+                          and max(cfg.nu1, cfg.nu2) <= 1
+                          and (comm.size == 1 or os.environ.get("SAG_DIST_GRAPH") == "1"))
         self.nlev = len(levels)
         norm0 = self._norm_inf(self.l0)
         if self.nlev > 1:
@@ -637,13 +641,19 @@ class DistSolver(DistStep):
         torch = self.be.torch
         g = torch.cuda.CUDAGraph()
         try:
-            with torch.cuda.graph(g, stream=self.stream):
-                self._prec_body()
-        except Exception as e:  # noqa: BLE001 -- eager application stays correct
+            # relaxed: libsag's pointer-kind queries (cudaPointerGetAttributes)
+            # are legal while this thread captures
+            with torch.cuda.graph(g, stream=self.stream, capture_error_mode="relaxed"):
+                try:
+                    self._prec_body()
+                except Exception as e:  # noqa: BLE001
+                    self.graph_error = repr(e)
+                    raise
+        except Exception as e:
             self.use_graph = False
-            self.graph_error = repr(e)
-            torch.cuda.synchronize()
-            return
+            self.graph_error = self.graph_error or repr(e)
+            raise RuntimeError("DistSolver: capturing the preconditioner into a CUDA graph "
+                               f"failed ({self.graph_error}); set use_graph = False") from e
         self.graph = g
 
     def solve(self, rhs_local, x):

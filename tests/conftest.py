@@ -51,3 +51,21 @@ def ref_case(n, sv=False, problem="cavity", cfg=None):
 def ctx():
     import paper_2306_06795_b200 as S
     return S.default_context()
+
+
+def collect_results(q, procs, n, timeout=600):
+    """n results from worker processes: fails fast when a worker dies (a dead
+    worker never puts its result, and waiting for it would hang the suite)."""
+    import queue
+    import time
+    out, deadline = [], time.time() + timeout
+    while len(out) < n:
+        try:
+            out.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead:
+                raise AssertionError(f"worker exited with {dead}")
+            if time.time() > deadline:
+                raise TimeoutError("workers did not report in time")
+    return out

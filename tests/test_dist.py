@@ -10,6 +10,7 @@ import socket
 
 import numpy as np
 import pytest
+from conftest import collect_results
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = os.path.join(ROOT, "tests", "golden")
@@ -60,12 +61,12 @@ def test_partitioned_step_matches_single_process(name, world):
     pytest.importorskip("torch")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
+    q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = [q.get() for _ in range(world)]
+    out = collect_results(q, procs, world)
     for p in procs:
         p.join(120)
         assert p.exitcode == 0

@@ -9,6 +9,7 @@ import socket
 
 import numpy as np
 import pytest
+from conftest import collect_results
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = os.path.join(ROOT, "tests", "golden")
@@ -89,12 +90,12 @@ def _worker(rank, world, port, source, q):
 def _run(world, source):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
+    q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, source, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = [q.get() for _ in range(world)]   # before join: a full pipe blocks the sender
+    out = collect_results(q, procs, world)  # before join: a full pipe blocks the sender
     for p in procs:
         p.join(600)
         assert p.exitcode == 0

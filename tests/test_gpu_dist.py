@@ -15,6 +15,7 @@ import socket
 
 import numpy as np
 import pytest
+from conftest import collect_results
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -76,13 +77,13 @@ def _worker(rank, world, port, n, backend, q):
 def _run(world, n, backend):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
-    q = ctx.SimpleQueue()
+    q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, n, backend, q))
              for r in range(world)]
     for p in procs:
         p.start()
-    out = [q.get() for _ in range(world)]
+    out = collect_results(q, procs, world)
     for p in procs:
         p.join(600)
         assert p.exitcode == 0
