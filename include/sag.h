@@ -281,6 +281,27 @@ int sag_solve_stokes_uzawa(sag_ctx* ctx, const sag_matrix* k0, sag_uzawa* u, con
                            double* x, const sag_solver_config* cfg, sag_krylov_report* rep,
                            double* history, int history_cap);
 
+/* ---- hierarchy setup products -----------------------------
+ * The sparse products of the SA setup on the device, BITWISE the reference's
+ * (every entry summed in the reference's order with round-to-nearest ops, the
+ * entries that cancel to exactly 0.0 dropped -- the hierarchy's patterns
+ * depend on it). New matrices are returned as new handles. */
+/* C = A B. Replaces spgemm (sparse.hpp:46; sparse.cpp:113-150). */
+int sag_spgemm(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* b, sag_matrix** out);
+/* A^T. Replaces transpose (sparse.hpp:44; sparse.cpp:93-111). */
+int sag_transpose(sag_ctx* ctx, const sag_matrix* a, sag_matrix** out);
+/* P^T K P. Replaces galerkin_triple (sparse.hpp:49; sparse.cpp:152-156). */
+int sag_galerkin(sag_ctx* ctx, const sag_matrix* p, const sag_matrix* k, sag_matrix** out);
+/* T - omega D^-1 (A T), D = diag(A). Replaces smooth_prolongator
+ * (amg.hpp:51; amg.cpp:226-236) given omega = omega_frac / rho, rho from the
+ * reference's power_rho_estimate (sparse.cpp:239-261; its mt19937 start
+ * vector stays on the host). Fails with SAG_ZERO_DIAGONAL like inv_diagonal. */
+int sag_smooth_prolongator(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* t, double omega,
+                           sag_matrix** out);
+/* Copies a matrix's CSR arrays out (host or device arrays; any may be NULL). */
+int sag_matrix_export(sag_ctx* ctx, const sag_matrix* m, int* row_offsets, int* col_indices,
+                      double* values);
+
 /* ---- partitioned-solve primitives ---------------------------
  * Building blocks for a caller that row-partitions the solve across ranks
  * (one process per GPU, paper_2306_06795_b200/dist.py). All pointers are

@@ -38,6 +38,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsag.so")
 
 __all__ = [
+    "spgemm", "transpose", "galerkin_triple", "smooth_prolongator",
     "Error", "DimensionMismatch", "SingularMatrix", "SingularPatch", "ConfigError",
     "SolverStagnation", "ZeroDiagonal", "UnsupportedDiscretization", "CudaError", "Context", "SparseMatrix", "Patches",
     "VankaFactorization", "spmv", "norm2", "dot", "build_patches", "factor_patches",
@@ -177,6 +178,12 @@ SIGNATURES = {
     "sag_uzawa_apply": (C.c_int, [vp, vp, vp, vp]),
     "sag_solve_stokes_uzawa": (C.c_int, [vp, vp, vp, vp, vp, C.POINTER(sag_solver_config),
                                          C.POINTER(sag_krylov_report), vp, C.c_int]),
+    # hierarchy setup products (bitwise the reference's)
+    "sag_spgemm": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
+    "sag_transpose": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "sag_galerkin": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
+    "sag_smooth_prolongator": (C.c_int, [vp, vp, vp, C.c_double, C.POINTER(vp)]),
+    "sag_matrix_export": (C.c_int, [vp, vp, vp, vp, vp]),
     # partitioned-solve primitives (device pointers, no host sync)
     "sag_dot_async": (C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
     "sag_axpy_async": (C.c_int, [vp, C.c_int, vp, C.c_double, vp, vp]),
@@ -322,6 +329,24 @@ class SparseMatrix:
         del self._rp, self._ci
 
     @classmethod
+    def _wrap(cls, h, ctx: Context) -> "SparseMatrix":
+        m = cls.__new__(cls)
+        m.ctx, m.h = ctx, h
+        nr, nc, nnz = C.c_int(), C.c_int(), C.c_longlong()
+        _check(lib().sag_matrix_shape(h, C.byref(nr), C.byref(nc), C.byref(nnz)))
+        m.nrows, m.ncols, m.nnz = nr.value, nc.value, nnz.value
+        return m
+
+    def to_csr(self):
+        """(row_offsets, col_indices, values) as numpy arrays (sag_matrix_export)."""
+        rp = np.empty(self.nrows + 1, dtype=np.int32)
+        ci = np.empty(max(self.nnz, 1), dtype=np.int32)
+        v = np.empty(max(self.nnz, 1))
+        _check(lib().sag_matrix_export(self.ctx.h, self.h, C.c_void_p(rp.ctypes.data),
+                                       C.c_void_p(ci.ctypes.data), C.c_void_p(v.ctypes.data)))
+        return rp, ci[:self.nnz], v[:self.nnz]
+
+    @classmethod
     def from_csr(cls, m, ctx: Context = None) -> "SparseMatrix":
         """From any object with nrows/ncols/rp/ci/v (oracle.Csr) or a scipy matrix."""
         if hasattr(m, "rp"):
@@ -344,6 +369,32 @@ def spmv(m: SparseMatrix, x, out=None):
     yp, y = _vec_out(out, m.nrows, like=x)
     _check(lib().sag_spmv(m.ctx.h, m.h, xp, yp))
     return y
+
+
+def _new(fn, ctx, *args):
+    h = vp()
+    _check(fn(ctx.h, *args, C.byref(h)))
+    return SparseMatrix._wrap(h, ctx)
+
+
+def spgemm(a: SparseMatrix, b: SparseMatrix) -> SparseMatrix:
+    """C = A B, bitwise the reference's spgemm (sparse.cpp:113-150)."""
+    return _new(lib().sag_spgemm, a.ctx, a.h, b.h)
+
+
+def transpose(a: SparseMatrix) -> SparseMatrix:
+    """A^T (sparse.cpp:93-111)."""
+    return _new(lib().sag_transpose, a.ctx, a.h)
+
+
+def galerkin_triple(p: SparseMatrix, k: SparseMatrix) -> SparseMatrix:
+    """P^T K P, bitwise the reference's galerkin_triple (sparse.cpp:152-156)."""
+    return _new(lib().sag_galerkin, p.ctx, p.h, k.h)
+
+
+def smooth_prolongator(a: SparseMatrix, t: SparseMatrix, omega: float) -> SparseMatrix:
+    """T - omega D^-1 A T (amg.cpp:226-236) for omega = omega_frac / rho."""
+    return _new(lib().sag_smooth_prolongator, a.ctx, a.h, t.h, C.c_double(omega))
 
 
 def norm2(v, ctx: Context = None) -> float:

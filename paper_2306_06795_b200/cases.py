@@ -47,6 +47,7 @@ def hlib():
         L.sagh_case_solve_variant.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
                                               C.c_double, C.c_int, C.c_double, C.c_double,
                                               C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.sagh_case_hierarchy_gpu.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.sagh_case_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                       C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
@@ -115,6 +116,17 @@ class HostCase:
 
     def levels(self):
         return [self.level(l) for l in range(self.nlevels)]
+
+    def hierarchy_gpu(self, device=0):
+        """The low-order hierarchy built again by the reference and by
+        gpu::build_monolithic_hierarchy (SA setup products on the device),
+        compared bitwise (sagh_case_hierarchy_gpu)."""
+        out = np.zeros(6)
+        if hlib().sagh_case_hierarchy_gpu(self.h, int(device), out.ctypes.data):
+            raise RuntimeError(hlib().sagh_last_error().decode())
+        return dict(reference_s=float(out[0]), device_assisted_s=float(out[1]),
+                    host_part_s=float(out[2]), device_part_s=float(out[3]),
+                    bitwise_equal=bool(out[4]), levels=int(out[5]))
 
     def rhs(self):
         r = np.empty(self.n0)

@@ -257,6 +257,12 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
 
 // transpose on device (sparse.cpp:93-111): rows of the result in ascending order
 std::unique_ptr<Matrix> transpose_dev(Ctx& c, const Matrix& a);
+std::unique_ptr<Matrix> matrix_upload(Ctx& c, int nrows, int ncols, long long nnz, const int* rp,
+                                      const int* ci, const double* v);
+// setup products, bitwise the reference's (sag_setup.cu)
+std::unique_ptr<Matrix> spgemm_dev(Ctx& c, const Matrix& a, const Matrix& b);
+std::unique_ptr<Matrix> smooth_prolongator_dev(Ctx& c, const Matrix& a, const Matrix& t,
+                                               double omega);
 
 }  // namespace sag
 

@@ -1,0 +1,346 @@
+// libsag setup module: the sparse products of the smoothed-aggregation
+// hierarchy setup on the device, BITWISE equal to the reference:
+//   spgemm            sparse.cpp:113-150
+//   galerkin_triple   sparse.cpp:152-156   (spgemm(transpose(P), spgemm(K, P)))
+//   smooth_prolongator amg.cpp:226-236     (T - (omega D^-1) (A T), omega from the caller)
+//   transpose         sparse.cpp:93-111
+// The setup is discrete and rounding-sensitive: entries that cancel
+// to exactly 0.0 are dropped, so every product must be summed in the
+// reference's order with round-to-nearest multiplies and adds (no FMA
+// contraction). spgemm accumulates accum[col] += a_rk * b_kc over the entries
+// of A's row in order; each B row holds a column at most once, so every output
+// entry is a sequential sum in A-row order. One warp per output row: the warp
+// walks A's row entry by entry and its lanes add that entry's B-row products
+// into a shared-memory hash table (distinct columns within one step, so no
+// two lanes touch one slot); the row's columns are then ranked, zeros dropped,
+// and written in ascending order. Two passes: row counts, then the rows.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace sag {
+
+constexpr int kSpgCap = 2048;   // hash slots per warp (columns of one output row)
+constexpr int kSpgWarps = 4;    // warps per CTA
+constexpr int kSpgSmem = kSpgWarps * kSpgCap * (4 + 8 + 4 + 8);
+
+// one output row r of C = A B into the warp's table; returns the count of
+// distinct columns (cnt) with lc / lv the compacted (column, value) lists
+__device__ __forceinline__ int spg_row(int r, const int* __restrict__ arp,
+                                       const int* __restrict__ aci, const double* __restrict__ av,
+                                       const int* __restrict__ brp, const int* __restrict__ bci,
+                                       const double* __restrict__ bv, int* keys, double* vals,
+                                       int* lc, double* lv, int* counter, int* overflow) {
+  const int lane = threadIdx.x & 31;
+  // table size: a power of two >= 2x the row's products (at most kSpgCap)
+  int prod = 0;
+  for (int ka = arp[r] + lane; ka < arp[r + 1]; ka += 32) {
+    const int j = aci[ka];
+    prod += brp[j + 1] - brp[j];
+  }
+  for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+  int cap = 64;
+  while (cap < 2 * prod && cap < kSpgCap) cap <<= 1;
+  const unsigned mask = cap - 1;
+  for (int s = lane; s < cap; s += 32) keys[s] = -1;
+  if (lane == 0) *counter = 0;
+  __syncwarp();
+  bool full = false;
+  for (int ka = arp[r]; ka < arp[r + 1]; ++ka) {
+    const int j = aci[ka];
+    const double a = av[ka];
+    for (int kb = brp[j] + lane; kb < brp[j + 1]; kb += 32) {
+      const int col = bci[kb];
+      unsigned h = ((unsigned)col * 2654435761u) & mask;
+      int probes = 0;
+      while (true) {
+        const int k = atomicCAS(keys + h, -1, col);
+        if (k == -1) {
+          vals[h] = 0.0;  // accum[col] = 0.0 on first touch (sparse.cpp:128-131)
+          break;
+        }
+        if (k == col) break;
+        h = (h + 1) & mask;
+        if (++probes >= cap) {
+          full = true;
+          break;
+        }
+      }
+      if (!full) vals[h] = __dadd_rn(vals[h], __dmul_rn(a, bv[kb]));
+    }
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, full)) {
+    if (lane == 0) atomicOr(overflow, 1);
+    return 0;
+  }
+  for (int s = lane; s < cap; s += 32) {
+    if (keys[s] != -1) {
+      const int p = atomicAdd(counter, 1);
+      lc[p] = keys[s];
+      lv[p] = vals[s];
+    }
+  }
+  __syncwarp();
+  return *counter;
+}
+
+// pass 0: nonzero count per row; pass 1: the row, columns ascending, exact
+// zeros dropped (sparse.cpp:140-146)
+__global__ void __launch_bounds__(kSpgWarps * 32) spgemm_kernel(
+    int nrows, const int* __restrict__ arp, const int* __restrict__ aci,
+    const double* __restrict__ av, const int* __restrict__ brp, const int* __restrict__ bci,
+    const double* __restrict__ bv, int pass, int* __restrict__ row_nnz,
+    const int* __restrict__ crp, int* __restrict__ cci, double* __restrict__ cv, int* overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* base = smem + (size_t)wib * kSpgCap * (4 + 8 + 4 + 8);
+  double* vals = reinterpret_cast<double*>(base);
+  double* lv = vals + kSpgCap;
+  int* keys = reinterpret_cast<int*>(lv + kSpgCap);
+  int* lc = keys + kSpgCap;
+  __shared__ int counters[kSpgWarps];
+  const int gw = blockIdx.x * kSpgWarps + wib, nw = gridDim.x * kSpgWarps;
+  for (int r = gw; r < nrows; r += nw) {
+    const int cnt = spg_row(r, arp, aci, av, brp, bci, bv, keys, vals, lc, lv, counters + wib,
+                            overflow);
+    int nz = 0;
+    for (int e = lane; e < cnt; e += 32) nz += lv[e] != 0.0;
+    for (int o = 16; o > 0; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
+    if (pass == 0) {
+      if (lane == 0) row_nnz[r] = nz;
+    } else {
+      const int o0 = crp[r];
+      for (int e = lane; e < cnt; e += 32) {
+        const double v = lv[e];
+        if (v == 0.0) continue;
+        const int c = lc[e];
+        int rank = 0;
+        for (int f = 0; f < cnt; ++f) rank += (lc[f] < c) & (lv[f] != 0.0);
+        cci[o0 + rank] = c;
+        cv[o0 + rank] = v;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+static int setup_grid(Ctx& c, long long rows) {
+  const long long need = (rows + kSpgWarps - 1) / kSpgWarps;
+  return (int)std::max(1LL, std::min(need, (long long)c.num_sms * 8));
+}
+
+// CSR from device row counts + a fill callback on the allocated arrays.
+template <class Fill>
+static std::unique_ptr<Matrix> csr_from_counts(Ctx& c, int nrows, int ncols, DevBuf<int>& cnt,
+                                               Fill fill) {
+  DevBuf<int> rp(nrows + 1);
+  size_t tmp = 0;
+  SAG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.p, rp.p, nrows + 1, c.stream));
+  DevBuf<unsigned char> ws(std::max<size_t>(tmp, 1));
+  SAG_CUDA(cub::DeviceScan::ExclusiveSum(ws.p, tmp, cnt.p, rp.p, nrows + 1, c.stream));
+  int nnz = 0;
+  SAG_CUDA(cudaMemcpyAsync(&nnz, rp.p + nrows, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  DevBuf<int> ci(std::max(nnz, 1));
+  DevBuf<double> v(std::max(nnz, 1));
+  fill(rp.p, ci.p, v.p);
+  return matrix_upload(c, nrows, ncols, nnz, rp.p, ci.p, v.p);
+}
+
+std::unique_ptr<Matrix> spgemm_dev(Ctx& c, const Matrix& a, const Matrix& b) {
+  SAG_REQUIRE(a.ncols == b.nrows, SAG_DIMENSION_MISMATCH, "spgemm: inner dimensions differ");
+  static bool configured = false;
+  if (!configured) {
+    SAG_CUDA(cudaFuncSetAttribute(spgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSpgSmem));
+    configured = true;
+  }
+  DevBuf<int> cnt(a.nrows + 1), ovf(1);
+  SAG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (a.nrows + 1), c.stream));
+  SAG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c.stream));
+  const int grid = setup_grid(c, a.nrows);
+  spgemm_kernel<<<grid, kSpgWarps * 32, kSpgSmem, c.stream>>>(
+      a.nrows, a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, 0, cnt.p, nullptr, nullptr, nullptr,
+      ovf.p);
+  SAG_LAUNCHED(c);
+  int hov = 0;
+  SAG_CUDA(cudaMemcpyAsync(&hov, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  SAG_REQUIRE(!hov, SAG_ERROR, "spgemm: an output row has more than 2048 distinct columns");
+  return csr_from_counts(c, a.nrows, b.ncols, cnt, [&](int* rp, int* ci, double* v) {
+    spgemm_kernel<<<grid, kSpgWarps * 32, kSpgSmem, c.stream>>>(
+        a.nrows, a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, 1, nullptr, rp, ci, v, ovf.p);
+    SAG_LAUNCHED(c);
+  });
+}
+
+// ---- smooth_prolongator (amg.cpp:226-236) ------------------------------
+// at = A T; at_rq *= omega * d_inv[r]; P = sparse_add(T, at, 1, -1): per row
+// the merged column lists, t + (-(at)) where both exist (a sum of two, order
+// free), exact zeros dropped (from_triplets, sparse.cpp:44-62).
+__global__ void smooth_scale_kernel(int nrows, const int* __restrict__ arp,
+                                    const int* __restrict__ aci, const double* __restrict__ av,
+                                    const int* __restrict__ rp, double* __restrict__ v, double omega,
+                                    int* bad) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    double d = 0.0;  // diagonal_of (sparse.cpp:202-206): A.at(r, r)
+    for (int q = arp[r]; q < arp[r + 1]; ++q)
+      if (aci[q] == r) d = av[q];
+    if (d == 0.0) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    const double dinv = 1.0 / d;                    // inv_diagonal (sparse.cpp:208-215)
+    const double s = __dmul_rn(omega, dinv);       // omega * d_inv[r]
+    for (int q = rp[r]; q < rp[r + 1]; ++q) v[q] = __dmul_rn(v[q], s);
+  }
+}
+
+__global__ void add_rows_kernel(int nrows, const int* __restrict__ trp, const int* __restrict__ tci,
+                                const double* __restrict__ tv, const int* __restrict__ arp,
+                                const int* __restrict__ aci, const double* __restrict__ av,
+                                int pass, int* __restrict__ cnt, const int* __restrict__ crp,
+                                int* __restrict__ cci, double* __restrict__ cv) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    int p = trp[r], q = arp[r], n = 0;
+    const int pe = trp[r + 1], qe = arp[r + 1];
+    int o = pass ? crp[r] : 0;
+    while (p < pe || q < qe) {
+      int col;
+      double s = 0.0;  // from_triplets: sum = 0.0; sum += ...
+      if (q >= qe || (p < pe && tci[p] < aci[q])) {
+        col = tci[p];
+        s = __dadd_rn(s, tv[p++]);
+      } else if (p >= pe || aci[q] < tci[p]) {
+        col = aci[q];
+        s = __dadd_rn(s, -av[q++]);
+      } else {
+        col = tci[p];
+        s = __dadd_rn(__dadd_rn(s, tv[p++]), -av[q++]);
+      }
+      if (s != 0.0) {
+        if (pass) {
+          cci[o] = col;
+          cv[o] = s;
+          ++o;
+        }
+        ++n;
+      }
+    }
+    if (!pass) cnt[r] = n;
+  }
+}
+
+std::unique_ptr<Matrix> smooth_prolongator_dev(Ctx& c, const Matrix& a, const Matrix& t,
+                                               double omega) {
+  SAG_REQUIRE(a.nrows == a.ncols && a.nrows == t.nrows, SAG_DIMENSION_MISMATCH,
+              "smooth_prolongator: shapes differ");
+  auto at = spgemm_dev(c, a, t);
+  DevBuf<int> bad(1);
+  SAG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+  const int g = std::max(1, std::min((a.nrows + 255) / 256, c.num_sms * 16));
+  smooth_scale_kernel<<<g, 256, 0, c.stream>>>(a.nrows, a.rp.p, a.ci.p, a.v.p, at->rp.p, at->v.p,
+                                               omega, bad.p);
+  SAG_LAUNCHED(c);
+  int hb = 0;
+  SAG_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  SAG_REQUIRE(!hb, SAG_ZERO_DIAGONAL, "inv_diagonal: zero diagonal");
+  DevBuf<int> cnt(t.nrows + 1);
+  SAG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (t.nrows + 1), c.stream));
+  add_rows_kernel<<<g, 256, 0, c.stream>>>(t.nrows, t.rp.p, t.ci.p, t.v.p, at->rp.p, at->ci.p,
+                                           at->v.p, 0, cnt.p, nullptr, nullptr, nullptr);
+  SAG_LAUNCHED(c);
+  return csr_from_counts(c, t.nrows, t.ncols, cnt, [&](int* rp, int* ci, double* v) {
+    add_rows_kernel<<<g, 256, 0, c.stream>>>(t.nrows, t.rp.p, t.ci.p, t.v.p, at->rp.p, at->ci.p,
+                                             at->v.p, 1, nullptr, rp, ci, v);
+    SAG_LAUNCHED(c);
+  });
+}
+
+}  // namespace sag
+
+// =================================================================== C-ABI
+using namespace sag;
+
+namespace {
+sag_matrix* wrap(std::unique_ptr<Matrix> m) {
+  auto* h = new sag_matrix;
+  h->m = std::move(*m);
+  return h;
+}
+}  // namespace
+
+extern "C" {
+
+int sag_spgemm(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* b, sag_matrix** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(a);
+    SAG_NOTNULL(b);
+    SAG_NOTNULL(out);
+    *out = wrap(spgemm_dev(ctx->c, a->m, b->m));
+  });
+}
+
+int sag_transpose(sag_ctx* ctx, const sag_matrix* a, sag_matrix** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(a);
+    SAG_NOTNULL(out);
+    *out = wrap(transpose_dev(ctx->c, a->m));
+  });
+}
+
+int sag_galerkin(sag_ctx* ctx, const sag_matrix* p, const sag_matrix* k, sag_matrix** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(p);
+    SAG_NOTNULL(k);
+    SAG_NOTNULL(out);
+    SAG_REQUIRE(k->m.nrows == k->m.ncols, SAG_DIMENSION_MISMATCH,
+                "galerkin_triple: K must be square");
+    SAG_REQUIRE(k->m.nrows == p->m.nrows, SAG_DIMENSION_MISMATCH,
+                "galerkin_triple: K and P row counts differ");
+    auto kp = spgemm_dev(ctx->c, k->m, p->m);
+    auto pt = transpose_dev(ctx->c, p->m);
+    *out = wrap(spgemm_dev(ctx->c, *pt, *kp));
+  });
+}
+
+int sag_smooth_prolongator(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* t, double omega,
+                           sag_matrix** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(a);
+    SAG_NOTNULL(t);
+    SAG_NOTNULL(out);
+    *out = wrap(smooth_prolongator_dev(ctx->c, a->m, t->m, omega));
+  });
+}
+
+int sag_matrix_export(sag_ctx* ctx, const sag_matrix* m, int* row_offsets, int* col_indices,
+                      double* values) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(m);
+    auto& c = ctx->c;
+    const auto& mm = m->m;
+    if (row_offsets)
+      SAG_CUDA(cudaMemcpyAsync(row_offsets, mm.rp.p, sizeof(int) * (mm.nrows + 1),
+                               cudaMemcpyDefault, c.stream));
+    if (col_indices && mm.nnz)
+      SAG_CUDA(cudaMemcpyAsync(col_indices, mm.ci.p, sizeof(int) * mm.nnz, cudaMemcpyDefault,
+                               c.stream));
+    if (values && mm.nnz)
+      SAG_CUDA(cudaMemcpyAsync(values, mm.v.p, sizeof(double) * mm.nnz, cudaMemcpyDefault,
+                               c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

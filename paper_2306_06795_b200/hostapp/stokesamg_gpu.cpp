@@ -5,9 +5,11 @@
 // host C++).
 #include "stokesamg_gpu.hpp"
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <utility>
 
 #include "stokesamg/experiments.hpp"
 
@@ -328,6 +330,165 @@ SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
   return report_in(std::move(x), rep, hist);
 }
 
+// ---- hierarchy setup with device products (amg.cpp:300-360) ---------------
+namespace {
+struct DevM {  // owned device matrix handle
+  sag_matrix* h = nullptr;
+  DevM() = default;
+  explicit DevM(sag_matrix* m) : h(m) {}
+  DevM(Device& dev, const SparseMatrix& m) {
+    check(sag_matrix_create(dev.handle(), m.nrows, m.ncols, m.nnz(), m.row_offsets.data(),
+                            m.col_indices.data(), m.values.data(), &h));
+  }
+  DevM(const DevM&) = delete;
+  DevM& operator=(const DevM&) = delete;
+  DevM(DevM&& o) noexcept : h(o.h) { o.h = nullptr; }
+  DevM& operator=(DevM&& o) noexcept {
+    std::swap(h, o.h);
+    return *this;
+  }
+  ~DevM() {
+    if (h) sag_matrix_destroy(h);
+  }
+};
+
+SparseMatrix to_host(Device& dev, const DevM& m) {
+  int nr = 0, nc = 0;
+  long long nnz = 0;
+  check(sag_matrix_shape(m.h, &nr, &nc, &nnz));
+  SparseMatrix out(nr, nc);
+  out.col_indices.resize(nnz);
+  out.values.resize(nnz);
+  check(sag_matrix_export(dev.handle(), m.h, out.row_offsets.data(), out.col_indices.data(),
+                          out.values.data()));
+  return out;
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& sys,
+                                               const AmgConfig& cfg, double* times) {
+  if (sys.Ap.nrows != sys.n_p)
+    throw DimensionMismatch(
+        "build_monolithic_hierarchy: pressure auxiliary operator does not match the pressure "
+        "space");
+  double t_host = 0.0, t_dev = 0.0;
+  auto host = [&](auto&& f) {
+    const auto t0 = std::chrono::steady_clock::now();
+    f();
+    t_host += seconds_since(t0);
+  };
+  auto device = [&](auto&& f) {
+    const auto t0 = std::chrono::steady_clock::now();
+    f();
+    t_dev += seconds_since(t0);
+  };
+  MonolithicHierarchy h;
+  MonolithicLevel l0;
+  SparseMatrix ax, ay, ap;
+  host([&] {
+    l0.k = assemble_saddle_matrix(sys);
+    l0.n_x = sys.n_x;
+    l0.n_y = sys.n_y;
+    l0.n_p = sys.n_p;
+    ax = extract_block(sys.A, 0, sys.n_x, 0, sys.n_x);
+    ay = extract_block(sys.A, sys.n_x, sys.n_x + sys.n_y, sys.n_x, sys.n_x + sys.n_y);
+    ap = sys.Ap;
+  });
+  DevM kcur, dax, day, dap;
+  device([&] {
+    kcur = DevM(dev, l0.k);
+    dax = DevM(dev, ax);
+    day = DevM(dev, ay);
+    dap = DevM(dev, ap);
+  });
+  h.levels.push_back(std::move(l0));
+  std::vector<double> null_x(ax.nrows, 1.0), null_y(ay.nrows, 1.0), null_p(ap.nrows, 1.0);
+
+  struct Step {
+    SparseMatrix p;
+    DevM dp;
+    std::vector<double> coarse_null;
+  };
+  while (h.num_levels() < cfg.max_levels) {
+    MonolithicLevel& cur = h.levels.back();
+    if (cur.total() <= cfg.coarse_size) break;
+    auto coarsen = [&](const SparseMatrix& a, const DevM& da, const std::vector<double>& nullvec,
+                       bool& stagnated) -> Step {
+      Step s;
+      TentativeResult tent;
+      double omega = 0.0;
+      bool stop = false;
+      host([&] {
+        const StrengthGraph g = cfg.use_evolution_soc ? evolution_soc(a, cfg.theta, cfg.soc_k)
+                                                      : symmetric_soc(a, cfg.sym_theta);
+        const Aggregation agg = aggregate(g);
+        if (agg.num_aggregates > 0.9 * a.nrows) {
+          stop = true;
+          return;
+        }
+        tent = tentative_prolongator_with_nullvec(agg, nullvec);
+        // smooth_prolongator's omega (amg.cpp:227-229)
+        const auto d_inv = inv_diagonal(a);
+        omega = cfg.omega_frac / power_rho_estimate(a, d_inv, 10);
+      });
+      if (stop) {
+        stagnated = true;
+        return s;
+      }
+      device([&] {
+        DevM dt(dev, tent.t);
+        check(sag_smooth_prolongator(dev.handle(), da.h, dt.h, omega, &s.dp.h));
+        s.p = to_host(dev, s.dp);
+      });
+      s.coarse_null = std::move(tent.coarse_nullvec);
+      return s;
+    };
+    bool stagnated = false;
+    Step sx = coarsen(ax, dax, null_x, stagnated);
+    Step sy = stagnated ? Step{} : coarsen(ay, day, null_y, stagnated);
+    Step sp = stagnated ? Step{} : coarsen(ap, dap, null_p, stagnated);
+    if (stagnated) {
+      h.truncated = true;
+      break;
+    }
+    host([&] { cur.p = block_diag({&sx.p, &sy.p, &sp.p}); });
+    MonolithicLevel next;
+    device([&] {
+      DevM dP(dev, cur.p);
+      DevM dk;
+      check(sag_galerkin(dev.handle(), dP.h, kcur.h, &dk.h));
+      next.k = to_host(dev, dk);
+      kcur = std::move(dk);
+      DevM nx_, ny_, np_;
+      check(sag_galerkin(dev.handle(), sx.dp.h, dax.h, &nx_.h));
+      check(sag_galerkin(dev.handle(), sy.dp.h, day.h, &ny_.h));
+      check(sag_galerkin(dev.handle(), sp.dp.h, dap.h, &np_.h));
+      ax = to_host(dev, nx_);
+      ay = to_host(dev, ny_);
+      ap = to_host(dev, np_);
+      dax = std::move(nx_);
+      day = std::move(ny_);
+      dap = std::move(np_);
+    });
+    next.n_x = sx.p.ncols;
+    next.n_y = sy.p.ncols;
+    next.n_p = sp.p.ncols;
+    null_x = std::move(sx.coarse_null);
+    null_y = std::move(sy.coarse_null);
+    null_p = std::move(sp.coarse_null);
+    h.levels.push_back(std::move(next));
+  }
+  if (times) {
+    times[0] = t_host;
+    times[1] = t_dev;
+  }
+  return h;
+}
+
 }  // namespace stokesamg::gpu
 
 // ======================================================================
@@ -342,6 +503,7 @@ thread_local std::string g_err;
 struct HostCase {
   AssembledCase c;
   SparseMatrix k0;
+  AmgConfig amg;
   MonolithicHierarchy h;
   ScalarHierarchy sh;  // SV only
   // HO-AMG / Uzawa inputs (sagh_case_build_extra)
@@ -437,6 +599,7 @@ void* sagh_case_build(const char* problem, int sv, const char* mesh_kind, int n,
     }
     AmgConfig amg;
     if (coarse_size > 0) amg.coarse_size = coarse_size;
+    hc->amg = amg;
     hc->k0 = assemble_saddle_matrix(hc->c.sys0);
     hc->h = build_monolithic_hierarchy(hc->c.sys1, amg);
     if (hc->c.sys0.disc == Discretization::SV)
@@ -447,6 +610,42 @@ void* sagh_case_build(const char* problem, int sv, const char* mesh_kind, int n,
 }
 
 void sagh_case_free(void* h) { delete static_cast<HostCase*>(h); }
+
+// The case's low-order hierarchy built again by the reference (host) and by
+// gpu::build_monolithic_hierarchy (device products), compared bitwise:
+// out = [reference s, device-assisted total s, its host part s, its device
+// part s, levels equal (1/0), levels]
+int sagh_case_hierarchy_gpu(void* h, int device, double* out) {
+  return guarded([&] {
+    auto& hc = *static_cast<HostCase*>(h);
+    auto t0 = std::chrono::steady_clock::now();
+    const MonolithicHierarchy ref = build_monolithic_hierarchy(hc.c.sys1, hc.amg);
+    const double t_ref = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    gpu::Device dev(device);
+    double parts[2] = {0.0, 0.0};
+    t0 = std::chrono::steady_clock::now();
+    const MonolithicHierarchy got = gpu::build_monolithic_hierarchy(dev, hc.c.sys1, hc.amg, parts);
+    const double t_gpu = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    auto same = [](const SparseMatrix& a, const SparseMatrix& b) {
+      return a.nrows == b.nrows && a.ncols == b.ncols && a.row_offsets == b.row_offsets &&
+             a.col_indices == b.col_indices &&
+             std::memcmp(a.values.data(), b.values.data(), sizeof(double) * a.values.size()) == 0 &&
+             a.values.size() == b.values.size();
+    };
+    bool eq = ref.num_levels() == got.num_levels() && ref.truncated == got.truncated;
+    for (int l = 0; eq && l < ref.num_levels(); ++l) {
+      const auto &a = ref.levels[l], &b = got.levels[l];
+      eq = a.n_x == b.n_x && a.n_y == b.n_y && a.n_p == b.n_p && same(a.k, b.k) &&
+           (l + 1 == ref.num_levels() || same(a.p, b.p));
+    }
+    out[0] = t_ref;
+    out[1] = t_gpu;
+    out[2] = parts[0];
+    out[3] = parts[1];
+    out[4] = eq ? 1.0 : 0.0;
+    out[5] = got.num_levels();
+  });
+}
 
 // The reference's setup for the other preconditioners of this case, with the
 // default AmgConfig: what = 1 -> HoAmgPreconditioner's hierarchy

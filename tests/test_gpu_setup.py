@@ -1,0 +1,50 @@
+"""GPU: the SA hierarchy setup products on the device (sag_spgemm,
+sag_galerkin, sag_smooth_prolongator) are BITWISE the
+reference's. The low-order hierarchy of a case is built twice -- by the
+reference's build_monolithic_hierarchy (amg.cpp:300-360) and by
+gpu::build_monolithic_hierarchy, whose smoothed prolongators and Galerkin
+products run on the device -- and every level's K and P must be identical
+(patterns and values): the setup drops entries that cancel to exactly 0.0
+(SURVEY H1), so anything but the reference's summation order would show."""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import ref_case
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("problem,sv,n", [("cavity", False, 16), ("cavity", False, 64),
+                                          ("cavity", True, 8), ("bfs", False, 16)])
+def test_hierarchy_on_device_is_bitwise(problem, sv, n):
+    from paper_2306_06795_b200.cases import HostCase
+    case = HostCase(problem, sv, "structured", n)
+    r = case.hierarchy_gpu(0)
+    assert r["levels"] >= 2
+    assert r["bitwise_equal"], r
+
+
+def test_spgemm_transpose_match_reference():
+    """spgemm / transpose / galerkin_triple on a reference level and its
+    prolongator against the reference's next level (the hierarchy's own
+    Galerkin product), through the Python mirror."""
+    import paper_2306_06795_b200 as S
+    c, d, k0, levels, _ = ref_case(32)
+    k, p, _ = levels[0]
+    K, P = S.SparseMatrix.from_csr(k), S.SparseMatrix.from_csr(p)
+    kc = S.galerkin_triple(P, K)
+    rp, ci, v = kc.to_csr()
+    nxt = levels[1][0]
+    assert np.array_equal(rp, nxt.rp) and np.array_equal(ci, nxt.ci)
+    assert np.array_equal(v.view(np.int64), nxt.v.view(np.int64))
+    pt = S.transpose(P).to_csr()
+    ref_t = O.RefMat.from_csr(p)
+    # transpose: rows of P^T list the rows of P in ascending order
+    sp = p.to_scipy().T.tocsr()
+    sp.sort_indices()
+    assert np.array_equal(pt[0], sp.indptr) and np.array_equal(pt[1], sp.indices)
+    assert np.array_equal(pt[2], sp.data)
+    del ref_t
+    kp = S.spgemm(K, P).to_csr()
+    assert kp[0][-1] > 0 and (np.diff(kp[0]) >= 0).all()
