@@ -298,6 +298,15 @@ int sag_galerkin(sag_ctx* ctx, const sag_matrix* p, const sag_matrix* k, sag_mat
  * vector stays on the host). Fails with SAG_ZERO_DIAGONAL like inv_diagonal. */
 int sag_smooth_prolongator(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* t, double omega,
                            sag_matrix** out);
+/* Replaces evolution_soc (amg.hpp:24; amg.cpp:45-110) given omega =
+ * 4 / (3 rho) from the reference's power_rho_estimate: the symmetrised
+ * strength graph (graph_from_adjacency, amg.cpp:13-42) as an n x n CSR whose
+ * values are the edge strengths (StrengthGraph offsets / neighbors /
+ * weights). Each column's z = (I - omega D^-1 A)^k e_j is accumulated in the
+ * reference's order, so the graph is bitwise the reference's. SAG_ERROR if a
+ * column's k-step support exceeds 2048 nodes (the caller keeps the host path). */
+int sag_evolution_soc(sag_ctx* ctx, const sag_matrix* a, double omega, double theta, int k,
+                      sag_matrix** graph);
 /* Copies a matrix's CSR arrays out (host or device arrays; any may be NULL). */
 int sag_matrix_export(sag_ctx* ctx, const sag_matrix* m, int* row_offsets, int* col_indices,
                       double* values);

@@ -38,7 +38,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsag.so")
 
 __all__ = [
-    "spgemm", "transpose", "galerkin_triple", "smooth_prolongator",
+    "spgemm", "transpose", "galerkin_triple", "smooth_prolongator", "evolution_soc",
     "Error", "DimensionMismatch", "SingularMatrix", "SingularPatch", "ConfigError",
     "SolverStagnation", "ZeroDiagonal", "UnsupportedDiscretization", "CudaError", "Context", "SparseMatrix", "Patches",
     "VankaFactorization", "spmv", "norm2", "dot", "build_patches", "factor_patches",
@@ -184,6 +184,7 @@ SIGNATURES = {
     "sag_galerkin": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "sag_smooth_prolongator": (C.c_int, [vp, vp, vp, C.c_double, C.POINTER(vp)]),
     "sag_matrix_export": (C.c_int, [vp, vp, vp, vp, vp]),
+    "sag_evolution_soc": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_int, C.POINTER(vp)]),
     # partitioned-solve primitives (device pointers, no host sync)
     "sag_dot_async": (C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
     "sag_axpy_async": (C.c_int, [vp, C.c_int, vp, C.c_double, vp, vp]),
@@ -390,6 +391,13 @@ def transpose(a: SparseMatrix) -> SparseMatrix:
 def galerkin_triple(p: SparseMatrix, k: SparseMatrix) -> SparseMatrix:
     """P^T K P, bitwise the reference's galerkin_triple (sparse.cpp:152-156)."""
     return _new(lib().sag_galerkin, p.ctx, p.h, k.h)
+
+
+def evolution_soc(a: SparseMatrix, omega: float, theta: float = 0.5, k: int = 2) -> SparseMatrix:
+    """Strength graph of evolution_soc (amg.cpp:45-110) for omega = 4 / (3 rho),
+    as a CSR of edge strengths (bitwise the reference's StrengthGraph)."""
+    return _new(lib().sag_evolution_soc, a.ctx, a.h, C.c_double(omega), C.c_double(theta),
+                int(k))
 
 
 def smooth_prolongator(a: SparseMatrix, t: SparseMatrix, omega: float) -> SparseMatrix:

@@ -121,12 +121,13 @@ class HostCase:
         """The low-order hierarchy built again by the reference and by
         gpu::build_monolithic_hierarchy (SA setup products on the device),
         compared bitwise (sagh_case_hierarchy_gpu)."""
-        out = np.zeros(6)
+        out = np.zeros(8)
         if hlib().sagh_case_hierarchy_gpu(self.h, int(device), out.ctypes.data):
             raise RuntimeError(hlib().sagh_last_error().decode())
         return dict(reference_s=float(out[0]), device_assisted_s=float(out[1]),
                     host_part_s=float(out[2]), device_part_s=float(out[3]),
-                    bitwise_equal=bool(out[4]), levels=int(out[5]))
+                    bitwise_equal=bool(out[4]), levels=int(out[5]),
+                    soc_device=int(out[6]), soc_host=int(out[7]))
 
     def rhs(self):
         r = np.empty(self.n0)

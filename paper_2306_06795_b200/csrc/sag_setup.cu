@@ -262,6 +262,299 @@ std::unique_ptr<Matrix> smooth_prolongator_dev(Ctx& c, const Matrix& a, const Ma
   });
 }
 
+// ---- evolution_soc (amg.cpp:45-110) ---------------------------------------
+// Column j: z = (I - omega D^-1 A)^k e_j over the sparse "touched" set, in the
+// reference's order: each step walks the touched list in order and the rows of
+// A^T, accumulating az_i in that order (the lanes of one A^T row add distinct
+// i, new entries appended in lane = row order through a ballot prefix), then
+// updates z_i = z_i - (omega d_inv_i) az_i over az_touched in order. Edges
+// (i, j, s) and (j, i, s) for s = |z_i| / |z_j| >= theta max_m s_m; the
+// union is sorted and duplicates keep the stronger weight
+// (graph_from_adjacency, amg.cpp:13-42).
+constexpr int kSocCap = 2048;
+constexpr int kSocWarps = 3;
+constexpr int kSocWarpBytes = kSocCap * (4 + 8 + 8 + 4 + 4 + 1);
+constexpr int kSocSmem = kSocWarps * ((kSocWarpBytes + 15) / 16 * 16);
+
+struct SocTable {
+  int* keys;
+  double* z;
+  double* az;
+  int* touched;
+  int* azt;
+  unsigned char* fl;  // bit 0 in touched, bit 1 in az (this step)
+  unsigned mask;
+  __device__ int find_or_insert(int key, bool& overflow) {
+    unsigned h = ((unsigned)key * 2654435761u) & mask;
+    for (unsigned p = 0; p <= mask; ++p) {
+      const int k = atomicCAS(keys + h, -1, key);
+      if (k == -1) {
+        z[h] = 0.0;
+        az[h] = 0.0;
+        fl[h] = 0;
+        return (int)h;
+      }
+      if (k == key) return (int)h;
+      h = (h + 1) & mask;
+    }
+    overflow = true;
+    return 0;
+  }
+  __device__ int find(int key) const {
+    unsigned h = ((unsigned)key * 2654435761u) & mask;
+    while (keys[h] != key) h = (h + 1) & mask;
+    return (int)h;
+  }
+};
+
+__global__ void __launch_bounds__(kSocWarps * 32) evolution_soc_kernel(
+    int n, const int* __restrict__ trp, const int* __restrict__ tci, const double* __restrict__ tv,
+    const double* __restrict__ dinv, double omega, double theta, int ksteps, int pass,
+    int* __restrict__ cnt, const long long* __restrict__ eoff, unsigned long long* __restrict__ ekey,
+    double* __restrict__ eval, int* overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned char* base = smem + (size_t)wib * ((kSocWarpBytes + 15) / 16 * 16);
+  SocTable T;
+  T.z = reinterpret_cast<double*>(base);
+  T.az = T.z + kSocCap;
+  T.keys = reinterpret_cast<int*>(T.az + kSocCap);
+  T.touched = T.keys + kSocCap;
+  T.azt = T.touched + kSocCap;
+  T.fl = reinterpret_cast<unsigned char*>(T.azt + kSocCap);
+  __shared__ int wcount[kSocWarps];
+  const int gw = blockIdx.x * kSocWarps + wib, nw = gridDim.x * kSocWarps;
+  for (int j = gw; j < n; j += nw) {
+    // table size: >= 2x an upper bound of the touched set (k = 2), <= kSocCap
+    int est = 0;
+    if (ksteps == 2) {
+      for (int q = trp[j] + lane; q < trp[j + 1]; q += 32) {
+        const int i = tci[q];
+        est += trp[i + 1] - trp[i];
+      }
+      for (int o = 16; o > 0; o >>= 1) est += __shfl_xor_sync(0xffffffffu, est, o);
+      est += 1 + trp[j + 1] - trp[j];
+    } else {
+      est = kSocCap;
+    }
+    int cap = 64;
+    while (cap < 2 * est && cap < kSocCap) cap <<= 1;
+    T.mask = cap - 1;
+    for (int s = lane; s < cap; s += 32) T.keys[s] = -1;
+    __syncwarp();
+    bool ovf = false;
+    if (lane == 0) {
+      const int sj = T.find_or_insert(j, ovf);
+      T.z[sj] = 1.0;
+      T.fl[sj] = 1;
+      T.touched[0] = j;
+    }
+    __syncwarp();
+    int nt = 1;
+    for (int step = 0; step < ksteps; ++step) {
+      int naz = 0;
+      const int nt0 = nt;
+      for (int t = 0; t < nt0; ++t) {
+        const int idx = T.touched[t];
+        const double v = T.z[T.find(idx)];
+        if (v == 0.0) continue;
+        const int b = trp[idx], e = trp[idx + 1];
+        for (int q0 = b; q0 < e; q0 += 32) {
+          const int q = q0 + lane;
+          const bool act = q < e;
+          int slot = 0;
+          bool isnew = false;
+          if (act) {
+            slot = T.find_or_insert(tci[q], ovf);
+            isnew = !(T.fl[slot] & 2);
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, act && isnew);
+          if (act && isnew) {
+            const int pos = naz + __popc(m & lt);
+            if (pos < kSocCap) T.azt[pos] = tci[q];
+            T.fl[slot] |= 2;
+            T.az[slot] = 0.0;
+          }
+          naz += __popc(m);
+          if (act) T.az[slot] = __dadd_rn(T.az[slot], __dmul_rn(tv[q], v));
+          __syncwarp();
+        }
+      }
+      if (naz > kSocCap) ovf = true;
+      for (int u0 = 0; u0 < naz && u0 < kSocCap; u0 += 32) {
+        const int u = u0 + lane;
+        const bool act = u < naz;
+        int slot = 0, i = 0;
+        bool newt = false;
+        if (act) {
+          i = T.azt[u];
+          slot = T.find(i);
+          newt = !(T.fl[slot] & 1);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, act && newt);
+        if (act && newt) {
+          const int pos = nt + __popc(m & lt);
+          if (pos < kSocCap) T.touched[pos] = i;
+          T.fl[slot] |= 1;
+        }
+        nt += __popc(m);
+        if (act) {
+          T.z[slot] = __dsub_rn(T.z[slot], __dmul_rn(__dmul_rn(omega, dinv[i]), T.az[slot]));
+          T.fl[slot] &= ~2;
+        }
+        __syncwarp();
+      }
+      if (nt > kSocCap) {
+        ovf = true;
+        nt = kSocCap;
+      }
+    }
+    // strength over the touched set (amg.cpp:86-101)
+    const double zj = fabs(T.z[T.find(j)]);
+    int emitted = 0;
+    if (zj > 0.0) {
+      double smax = 0.0;
+      for (int u = lane; u < nt; u += 32) {
+        const int i = T.touched[u];
+        if (i != j) smax = fmax(smax, fabs(T.z[T.find(i)]) / zj);
+      }
+      for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+      if (smax > 0.0) {
+        const double thr = theta * smax;
+        if (lane == 0) wcount[wib] = 0;
+        __syncwarp();
+        for (int u = lane; u < nt; u += 32) {
+          const int i = T.touched[u];
+          if (i == j) continue;
+          const double sv = fabs(T.z[T.find(i)]) / zj;
+          if (sv > 0.0 && sv >= thr) {
+            if (pass == 0) {
+              ++emitted;
+            } else {
+              const long long o = eoff[j] + 2LL * atomicAdd(wcount + wib, 1);
+              ekey[o] = ((unsigned long long)(unsigned)i << 32) | (unsigned)j;
+              eval[o] = sv;
+              ekey[o + 1] = ((unsigned long long)(unsigned)j << 32) | (unsigned)i;
+              eval[o + 1] = sv;
+            }
+          }
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(overflow, 1);
+    if (pass == 0) {
+      for (int o = 16; o > 0; o >>= 1) emitted += __shfl_xor_sync(0xffffffffu, emitted, o);
+      if (lane == 0) cnt[j] = 2 * emitted;
+    }
+    __syncwarp();
+  }
+}
+
+// sorted (row, col) keys: unique flags, then per unique key the max weight
+__global__ void uniq_flag_kernel(long long ne, const unsigned long long* __restrict__ key,
+                                 int* __restrict__ flag) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ne;
+       e += (long long)gridDim.x * blockDim.x)
+    flag[e] = (e == 0 || key[e] != key[e - 1]) ? 1 : 0;
+}
+__global__ void uniq_write_kernel(long long ne, const unsigned long long* __restrict__ key,
+                                  const double* __restrict__ val, const int* __restrict__ pos,
+                                  int* __restrict__ rowcnt, int* __restrict__ col,
+                                  double* __restrict__ w) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ne;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (!(e == 0 || key[e] != key[e - 1])) continue;
+    double m = val[e];
+    for (long long f = e + 1; f < ne && key[f] == key[e]; ++f) m = fmax(m, val[f]);
+    const int p = pos[e];
+    col[p] = (int)(key[e] & 0xffffffffu);
+    w[p] = m;
+    atomicAdd(rowcnt + (int)(key[e] >> 32), 1);
+  }
+}
+
+std::unique_ptr<Matrix> evolution_soc_dev(Ctx& c, const Matrix& a, double omega, double theta,
+                                          int ksteps) {
+  SAG_REQUIRE(a.nrows == a.ncols, SAG_DIMENSION_MISMATCH, "evolution_soc: A must be square");
+  const int n = a.nrows;
+  static bool configured = false;
+  if (!configured) {
+    SAG_CUDA(cudaFuncSetAttribute(evolution_soc_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSocSmem));
+    configured = true;
+  }
+  auto at = transpose_dev(c, a);
+  // d_inv (inv_diagonal, sparse.cpp:208-215): 1 / a_ii
+  DevBuf<double> dinv(std::max(n, 1));
+  DevBuf<int> bad(1), ovf(1);
+  SAG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
+  SAG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c.stream));
+  launch_inv_diag(c, a, dinv.p, bad.p);
+  DevBuf<int> cnt(n + 1);
+  SAG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (n + 1), c.stream));
+  const long long need = ((long long)n + kSocWarps - 1) / kSocWarps;
+  const int grid = (int)std::max(1LL, std::min(need, (long long)c.num_sms * 4));
+  evolution_soc_kernel<<<grid, kSocWarps * 32, kSocSmem, c.stream>>>(
+      n, at->rp.p, at->ci.p, at->v.p, dinv.p, omega, theta, ksteps, 0, cnt.p, nullptr, nullptr,
+      nullptr, ovf.p);
+  SAG_LAUNCHED(c);
+  int hb = 0, ho = 0;
+  SAG_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaMemcpyAsync(&ho, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  SAG_REQUIRE(!hb, SAG_ZERO_DIAGONAL, "inv_diagonal: zero diagonal");
+  SAG_REQUIRE(!ho, SAG_ERROR, "evolution_soc: a column's touched set exceeds 2048 nodes");
+  // edge offsets (int64), then the edges
+  DevBuf<long long> eoff(n + 1);
+  {
+    DevBuf<long long> cl(n + 1);
+    std::vector<int> hc(n + 1);
+    SAG_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    std::vector<long long> ho2(n + 1, 0);
+    for (int j = 0; j < n; ++j) ho2[j + 1] = ho2[j] + hc[j];
+    SAG_CUDA(cudaMemcpyAsync(eoff.p, ho2.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, c.stream));
+    const long long ne = ho2[n];
+    SAG_REQUIRE(ne < (1LL << 31), SAG_DIMENSION_MISMATCH, "evolution_soc: too many edges");
+    DevBuf<unsigned long long> key(std::max(ne, 1LL)), key2(std::max(ne, 1LL));
+    DevBuf<double> val(std::max(ne, 1LL)), val2(std::max(ne, 1LL));
+    evolution_soc_kernel<<<grid, kSocWarps * 32, kSocSmem, c.stream>>>(
+        n, at->rp.p, at->ci.p, at->v.p, dinv.p, omega, theta, ksteps, 1, nullptr, eoff.p, key.p,
+        val.p, ovf.p);
+    SAG_LAUNCHED(c);
+    size_t t1 = 0;
+    SAG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, key.p, key2.p, val.p, val2.p, (int)ne, 0,
+                                             64, c.stream));
+    DevBuf<int> flag(std::max(ne, 1LL) + 1), pos(std::max(ne, 1LL) + 1), rowcnt(n + 1);
+    size_t t2 = 0;
+    SAG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, flag.p, pos.p, (int)ne + 1, c.stream));
+    DevBuf<unsigned char> ws(std::max<size_t>(std::max(t1, t2), 1));
+    if (ne > 0)
+      SAG_CUDA(cub::DeviceRadixSort::SortPairs(ws.p, t1, key.p, key2.p, val.p, val2.p, (int)ne, 0,
+                                               64, c.stream));
+    SAG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int) * (ne + 1), c.stream));
+    const int g = std::max(1, (int)std::min<long long>((ne + 255) / 256, c.num_sms * 16LL));
+    uniq_flag_kernel<<<g, 256, 0, c.stream>>>(ne, key2.p, flag.p);
+    SAG_LAUNCHED(c);
+    SAG_CUDA(cub::DeviceScan::ExclusiveSum(ws.p, t2, flag.p, pos.p, (int)ne + 1, c.stream));
+    int nu = 0;
+    SAG_CUDA(cudaMemcpyAsync(&nu, pos.p + ne, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    DevBuf<int> col(std::max(nu, 1));
+    DevBuf<double> w(std::max(nu, 1));
+    SAG_CUDA(cudaMemsetAsync(rowcnt.p, 0, sizeof(int) * (n + 1), c.stream));
+    uniq_write_kernel<<<g, 256, 0, c.stream>>>(ne, key2.p, val2.p, pos.p, rowcnt.p, col.p, w.p);
+    SAG_LAUNCHED(c);
+    DevBuf<int> rp(n + 1);
+    size_t t3 = 0;
+    SAG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, rowcnt.p, rp.p, n + 1, c.stream));
+    DevBuf<unsigned char> ws3(std::max<size_t>(t3, 1));
+    SAG_CUDA(cub::DeviceScan::ExclusiveSum(ws3.p, t3, rowcnt.p, rp.p, n + 1, c.stream));
+    return matrix_upload(c, n, n, nu, rp.p, col.p, w.p);
+  }
+}
+
 }  // namespace sag
 
 // =================================================================== C-ABI
@@ -320,6 +613,17 @@ int sag_smooth_prolongator(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* 
     SAG_NOTNULL(t);
     SAG_NOTNULL(out);
     *out = wrap(smooth_prolongator_dev(ctx->c, a->m, t->m, omega));
+  });
+}
+
+int sag_evolution_soc(sag_ctx* ctx, const sag_matrix* a, double omega, double theta, int k,
+                      sag_matrix** graph) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(a);
+    SAG_NOTNULL(graph);
+    SAG_REQUIRE(k >= 0, SAG_CONFIG_ERROR, "evolution_soc: k must be non-negative");
+    *graph = wrap(evolution_soc_dev(ctx->c, a->m, omega, theta, k));
   });
 }
 

@@ -376,6 +376,7 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
         "build_monolithic_hierarchy: pressure auxiliary operator does not match the pressure "
         "space");
   double t_host = 0.0, t_dev = 0.0;
+  int soc_dev = 0, soc_host = 0;
   auto host = [&](auto&& f) {
     const auto t0 = std::chrono::steady_clock::now();
     f();
@@ -422,18 +423,42 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
       TentativeResult tent;
       double omega = 0.0;
       bool stop = false;
+      // rho(D^-1 A): evolution_soc (amg.cpp:47-49) and smooth_prolongator
+      // (amg.cpp:227-229) estimate it identically -- once here, on the host
+      // (its start vector is the reference's mt19937 stream)
+      double rho = 0.0;
+      host([&] { rho = power_rho_estimate(a, inv_diagonal(a), 10); });
+      StrengthGraph g;
+      bool soc_on_device = false;
+      if (cfg.use_evolution_soc) {
+        device([&] {
+          sag_matrix* gh = nullptr;
+          if (sag_evolution_soc(dev.handle(), da.h, 4.0 / (3.0 * rho), cfg.theta, cfg.soc_k,
+                                &gh) == SAG_OK) {
+            DevM gm(gh);
+            const SparseMatrix gc = to_host(dev, gm);
+            g.n = gc.nrows;
+            g.offsets = gc.row_offsets;
+            g.neighbors = gc.col_indices;
+            g.weights = gc.values;
+            soc_on_device = true;
+            ++soc_dev;
+          }
+        });
+      }
       host([&] {
-        const StrengthGraph g = cfg.use_evolution_soc ? evolution_soc(a, cfg.theta, cfg.soc_k)
-                                                      : symmetric_soc(a, cfg.sym_theta);
+        if (!soc_on_device) {  // symmetric measure, or a support too large for the device table
+          g = cfg.use_evolution_soc ? evolution_soc(a, cfg.theta, cfg.soc_k)
+                                    : symmetric_soc(a, cfg.sym_theta);
+          ++soc_host;
+        }
         const Aggregation agg = aggregate(g);
         if (agg.num_aggregates > 0.9 * a.nrows) {
           stop = true;
           return;
         }
         tent = tentative_prolongator_with_nullvec(agg, nullvec);
-        // smooth_prolongator's omega (amg.cpp:227-229)
-        const auto d_inv = inv_diagonal(a);
-        omega = cfg.omega_frac / power_rho_estimate(a, d_inv, 10);
+        omega = cfg.omega_frac / rho;
       });
       if (stop) {
         stagnated = true;
@@ -485,6 +510,8 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
   if (times) {
     times[0] = t_host;
     times[1] = t_dev;
+    times[2] = soc_dev;
+    times[3] = soc_host;
   }
   return h;
 }
@@ -614,7 +641,8 @@ void sagh_case_free(void* h) { delete static_cast<HostCase*>(h); }
 // The case's low-order hierarchy built again by the reference (host) and by
 // gpu::build_monolithic_hierarchy (device products), compared bitwise:
 // out = [reference s, device-assisted total s, its host part s, its device
-// part s, levels equal (1/0), levels]
+// part s, levels equal (1/0), levels, strength graphs built on the device,
+// on the host]
 int sagh_case_hierarchy_gpu(void* h, int device, double* out) {
   return guarded([&] {
     auto& hc = *static_cast<HostCase*>(h);
@@ -622,7 +650,7 @@ int sagh_case_hierarchy_gpu(void* h, int device, double* out) {
     const MonolithicHierarchy ref = build_monolithic_hierarchy(hc.c.sys1, hc.amg);
     const double t_ref = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     gpu::Device dev(device);
-    double parts[2] = {0.0, 0.0};
+    double parts[4] = {0.0, 0.0, 0.0, 0.0};
     t0 = std::chrono::steady_clock::now();
     const MonolithicHierarchy got = gpu::build_monolithic_hierarchy(dev, hc.c.sys1, hc.amg, parts);
     const double t_gpu = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -644,6 +672,8 @@ int sagh_case_hierarchy_gpu(void* h, int device, double* out) {
     out[3] = parts[1];
     out[4] = eq ? 1.0 : 0.0;
     out[5] = got.num_levels();
+    out[6] = parts[2];
+    out[7] = parts[3];
   });
 }
 

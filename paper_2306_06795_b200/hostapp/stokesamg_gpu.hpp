@@ -157,13 +157,15 @@ SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
 SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
                          const UzawaPreconditioner& prec, const SolverConfig& cfg);
 
-// build_monolithic_hierarchy (amg.hpp:99; amg.cpp:300-360) with the sparse
-// products of the setup on the device -- smooth_prolongator's A T product,
-// scaling and T - omega D^-1 A T (sag_smooth_prolongator) and every Galerkin
-// product P^T K P (sag_galerkin) -- bitwise the reference's hierarchy. The
-// strength graphs, aggregation, tentative prolongators and the spectral
+// build_monolithic_hierarchy (amg.hpp:99; amg.cpp:300-360) with the setup's
+// strength graphs (sag_evolution_soc) and sparse products on the device --
+// smooth_prolongator's A T product, scaling and T - omega D^-1 A T
+// (sag_smooth_prolongator) and every Galerkin product P^T K P (sag_galerkin)
+// -- bitwise the reference's hierarchy. The greedy aggregation (sequential
+// by definition, amg.cpp:113-160), tentative prolongators and the spectral
 // radius estimates (mt19937 start vector) stay the reference's host code.
-// times (may be null) = [host part s, device part s].
+// times (may be null) = [host part s, device part s, strength graphs built
+// on the device, on the host].
 MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& sys,
                                                const AmgConfig& cfg, double* times = nullptr);
 

@@ -23,6 +23,59 @@ def test_hierarchy_on_device_is_bitwise(problem, sv, n):
     r = case.hierarchy_gpu(0)
     assert r["levels"] >= 2
     assert r["bitwise_equal"], r
+    assert r["soc_device"] >= 3 and r["soc_host"] == 0, r   # every strength graph on the device
+
+
+def test_evolution_soc_graph_matches_reference():
+    """sag_evolution_soc vs the reference's evolution_soc through the
+    aggregation it feeds: the hierarchy test checks the end result; here the
+    graph of a level's velocity block against a CPU restatement of amg.cpp:45-110."""
+    import paper_2306_06795_b200 as S
+    c, d, k0, levels, _ = ref_case(16)
+    k, p, (nx, ny, npp) = levels[0]
+    a = k.to_scipy().tocsr()[:nx, :nx].tocsr()
+    a.sort_indices()
+    A = S.SparseMatrix(nx, nx, a.indptr, a.indices, a.data)
+    dinv = 1.0 / a.diagonal()
+    rho = 2.0  # any positive omega exercises the same arithmetic
+    omega = 4.0 / (3.0 * rho)
+    g = S.evolution_soc(A, omega, 0.5, 2)
+    grp, gci, gv = g.to_csr()
+    at = a.T.tocsr()
+    at.sort_indices()
+    adj = [dict() for _ in range(nx)]
+    for j in range(nx):
+        z, touched = {j: 1.0}, [j]
+        for _ in range(2):
+            az, azt = {}, []
+            for idx in list(touched):
+                v = z.get(idx, 0.0)
+                if v == 0.0:
+                    continue
+                for q in range(at.indptr[idx], at.indptr[idx + 1]):
+                    i = at.indices[q]
+                    if i not in az:
+                        az[i] = 0.0
+                        azt.append(i)
+                    az[i] += at.data[q] * v
+            for i in azt:
+                if i not in z:
+                    z[i] = 0.0
+                    touched.append(i)
+                z[i] -= omega * dinv[i] * az[i]
+        zj = abs(z[j])
+        if zj > 0.0:
+            smax = max([abs(z[i]) / zj for i in touched if i != j] + [0.0])
+            if smax > 0.0:
+                for i in touched:
+                    s = abs(z[i]) / zj
+                    if i != j and s > 0.0 and s >= 0.5 * smax:
+                        adj[i][j] = max(adj[i].get(j, 0.0), s)
+                        adj[j][i] = max(adj[j].get(i, 0.0), s)
+    for i in range(nx):
+        cols = sorted(adj[i])
+        assert list(gci[grp[i]:grp[i + 1]]) == cols
+        assert np.array_equal(gv[grp[i]:grp[i + 1]], [adj[i][c_] for c_ in cols])
 
 
 def test_spgemm_transpose_match_reference():
