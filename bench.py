@@ -617,6 +617,12 @@ def run_ours(args, ws, rank, local):
                         "reference_cpu_note": "BASELINE.md 2 (1 core, measured at survey time)",
                         "dc_info": dc.info()}
 
+    if rank == 0 and ws == 1 and not args.no_setup and not case.sv:
+        # the low-order hierarchy built by the reference (host) and with the
+        # setup's strength graphs and sparse products on the device
+        # (gpu::build_monolithic_hierarchy), compared bitwise
+        out["setup"]["hierarchy"] = case.hierarchy_gpu(local)
+
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         done, wall = cpu_steps(k0, case.nxyz0, 4 * threads, threads, budget_s=20.0)
@@ -638,6 +644,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-setup", action="store_true",
+                    help="skip the device-assisted hierarchy setup measurement")
     ap.add_argument("--dist", action="store_true",
                     help="use the partitioned (halo-exchange) step even at N = 1")
     args = ap.parse_args()

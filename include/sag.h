@@ -307,6 +307,10 @@ int sag_smooth_prolongator(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* 
  * column's k-step support exceeds 2048 nodes (the caller keeps the host path). */
 int sag_evolution_soc(sag_ctx* ctx, const sag_matrix* a, double omega, double theta, int k,
                       sag_matrix** graph);
+/* K = [[A, B^T], [B, 0]] from the velocity block A (n_u x n_u) and the
+ * divergence B (n_p x n_u). Replaces assemble_saddle_matrix (fem.hpp;
+ * fem.cpp:290-306): the blocks never overlap, so K is bitwise the reference's. */
+int sag_saddle_matrix(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* b, sag_matrix** out);
 /* Copies a matrix's CSR arrays out (host or device arrays; any may be NULL). */
 int sag_matrix_export(sag_ctx* ctx, const sag_matrix* m, int* row_offsets, int* col_indices,
                       double* values);

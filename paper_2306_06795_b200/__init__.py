@@ -39,6 +39,7 @@ LIB_PATH = os.path.join(HERE, "libsag.so")
 
 __all__ = [
     "spgemm", "transpose", "galerkin_triple", "smooth_prolongator", "evolution_soc",
+    "saddle_matrix",
     "Error", "DimensionMismatch", "SingularMatrix", "SingularPatch", "ConfigError",
     "SolverStagnation", "ZeroDiagonal", "UnsupportedDiscretization", "CudaError", "Context", "SparseMatrix", "Patches",
     "VankaFactorization", "spmv", "norm2", "dot", "build_patches", "factor_patches",
@@ -184,6 +185,7 @@ SIGNATURES = {
     "sag_galerkin": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "sag_smooth_prolongator": (C.c_int, [vp, vp, vp, C.c_double, C.POINTER(vp)]),
     "sag_matrix_export": (C.c_int, [vp, vp, vp, vp, vp]),
+    "sag_saddle_matrix": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "sag_evolution_soc": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_int, C.POINTER(vp)]),
     # partitioned-solve primitives (device pointers, no host sync)
     "sag_dot_async": (C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
@@ -391,6 +393,11 @@ def transpose(a: SparseMatrix) -> SparseMatrix:
 def galerkin_triple(p: SparseMatrix, k: SparseMatrix) -> SparseMatrix:
     """P^T K P, bitwise the reference's galerkin_triple (sparse.cpp:152-156)."""
     return _new(lib().sag_galerkin, p.ctx, p.h, k.h)
+
+
+def saddle_matrix(a: SparseMatrix, b: SparseMatrix) -> SparseMatrix:
+    """[[A, B^T], [B, 0]] (assemble_saddle_matrix, fem.cpp:290-306)."""
+    return _new(lib().sag_saddle_matrix, a.ctx, a.h, b.h)
 
 
 def evolution_soc(a: SparseMatrix, omega: float, theta: float = 0.5, k: int = 2) -> SparseMatrix:

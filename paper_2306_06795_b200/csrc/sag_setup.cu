@@ -555,6 +555,62 @@ std::unique_ptr<Matrix> evolution_soc_dev(Ctx& c, const Matrix& a, double omega,
   }
 }
 
+// ---- assemble_saddle_matrix (fem.cpp:290-306) ------------------------------
+// K = [[A, B^T], [B, 0]]: the reference sums the triplets of A, B and B^T in
+// from_triplets; the three blocks never share a position and canonical
+// A / B hold no zeros, so every entry is the single stored value (0.0 + v)
+// and K's rows are the concatenations A row | (B^T row shifted by n_u) for
+// velocity rows and B row for pressure rows.
+__global__ void saddle_rows_kernel(int nu, int np, const int* __restrict__ arp,
+                                   const int* __restrict__ aci, const double* __restrict__ av,
+                                   const int* __restrict__ btrp, const int* __restrict__ btci,
+                                   const double* __restrict__ btv, const int* __restrict__ brp,
+                                   const int* __restrict__ bci, const double* __restrict__ bv,
+                                   int pass, int* __restrict__ cnt, const int* __restrict__ krp,
+                                   int* __restrict__ kci, double* __restrict__ kv) {
+  const int n = nu + np;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    int o = pass ? krp[r] : 0, c = 0;
+    auto put = [&](int col, double v) {
+      const double sum = 0.0 + v;  // from_triplets: sum = 0.0; sum += value
+      if (sum == 0.0) return;
+      if (pass) {
+        kci[o] = col;
+        kv[o] = sum;
+        ++o;
+      }
+      ++c;
+    };
+    if (r < nu) {
+      for (int q = arp[r]; q < arp[r + 1]; ++q) put(aci[q], av[q]);
+      for (int q = btrp[r]; q < btrp[r + 1]; ++q) put(nu + btci[q], btv[q]);
+    } else {
+      for (int q = brp[r - nu]; q < brp[r - nu + 1]; ++q) put(bci[q], bv[q]);
+    }
+    if (!pass) cnt[r] = c;
+  }
+}
+
+std::unique_ptr<Matrix> saddle_matrix_dev(Ctx& c, const Matrix& a, const Matrix& b) {
+  SAG_REQUIRE(a.nrows == a.ncols && b.ncols == a.nrows, SAG_DIMENSION_MISMATCH,
+              "assemble_saddle_matrix: A is n_u x n_u and B is n_p x n_u");
+  const int nu = a.nrows, np = b.nrows, n = nu + np;
+  auto bt = transpose_dev(c, b);
+  DevBuf<int> cnt(n + 1);
+  SAG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (n + 1), c.stream));
+  const int g = std::max(1, std::min((n + 255) / 256, c.num_sms * 16));
+  saddle_rows_kernel<<<g, 256, 0, c.stream>>>(nu, np, a.rp.p, a.ci.p, a.v.p, bt->rp.p, bt->ci.p,
+                                              bt->v.p, b.rp.p, b.ci.p, b.v.p, 0, cnt.p, nullptr,
+                                              nullptr, nullptr);
+  SAG_LAUNCHED(c);
+  return csr_from_counts(c, n, n, cnt, [&](int* rp, int* ci, double* v) {
+    saddle_rows_kernel<<<g, 256, 0, c.stream>>>(nu, np, a.rp.p, a.ci.p, a.v.p, bt->rp.p,
+                                                bt->ci.p, bt->v.p, b.rp.p, b.ci.p, b.v.p, 1,
+                                                nullptr, rp, ci, v);
+    SAG_LAUNCHED(c);
+  });
+}
+
 }  // namespace sag
 
 // =================================================================== C-ABI
@@ -624,6 +680,16 @@ int sag_evolution_soc(sag_ctx* ctx, const sag_matrix* a, double omega, double th
     SAG_NOTNULL(graph);
     SAG_REQUIRE(k >= 0, SAG_CONFIG_ERROR, "evolution_soc: k must be non-negative");
     *graph = wrap(evolution_soc_dev(ctx->c, a->m, omega, theta, k));
+  });
+}
+
+int sag_saddle_matrix(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* b, sag_matrix** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(a);
+    SAG_NOTNULL(b);
+    SAG_NOTNULL(out);
+    *out = wrap(saddle_matrix_dev(ctx->c, a->m, b->m));
   });
 }
 

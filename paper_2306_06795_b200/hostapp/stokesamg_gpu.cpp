@@ -391,7 +391,6 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
   MonolithicLevel l0;
   SparseMatrix ax, ay, ap;
   host([&] {
-    l0.k = assemble_saddle_matrix(sys);
     l0.n_x = sys.n_x;
     l0.n_y = sys.n_y;
     l0.n_p = sys.n_p;
@@ -401,7 +400,10 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
   });
   DevM kcur, dax, day, dap;
   device([&] {
-    kcur = DevM(dev, l0.k);
+    // assemble_saddle_matrix (fem.cpp:290-306) on the device
+    DevM da(dev, sys.A), db(dev, sys.B);
+    check(sag_saddle_matrix(dev.handle(), da.h, db.h, &kcur.h));
+    l0.k = to_host(dev, kcur);
     dax = DevM(dev, ax);
     day = DevM(dev, ay);
     dap = DevM(dev, ap);
