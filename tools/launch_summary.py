@@ -12,7 +12,7 @@ import re
 import sys
 from collections import OrderedDict
 
-STEP = ("vanka_patch_kernel", "vanka_gather_kernel", "spmv_kernel")
+STEP = ("vanka_patch_kernel", "vanka_gather_kernel", "vanka_gather_seq_kernel", "spmv_kernel")
 
 
 def short(name):
