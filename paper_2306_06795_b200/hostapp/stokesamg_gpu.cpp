@@ -103,7 +103,7 @@ DCPreconditioner::DCPreconditioner(Device& dev, const SaddleSystem& sys0, const 
   n_p0_ = sys0.n_p;
   if (transfer.n_u0 != sys0.n_u() || transfer.n_p0 != n_p0_)
     throw DimensionMismatch("DCPreconditioner: transfer does not match the high-order system");
-  h_ = build_monolithic_hierarchy(sys1, cfg_.amg);
+  h_ = build_monolithic_hierarchy(dev, sys1, cfg_.amg);  // device setup, bitwise the reference's
   const bool sv = sys0.disc == Discretization::SV;
   mats_.push_back(std::make_unique<DeviceMatrix>(dev, k0_));
   const sag_matrix* k0h = mats_.back()->handle();
@@ -127,7 +127,7 @@ DCPreconditioner::DCPreconditioner(Device& dev, const SaddleSystem& sys0, const 
   if (sv) {
     // SvPressureRestrict's own hierarchy (transfer.cpp:18-23), rebuilt by the
     // reference's build_scalar_hierarchy with the default AmgConfig
-    ScalarHierarchy sh = build_scalar_hierarchy(sys0.Mp_cg, AmgConfig{});
+    ScalarHierarchy sh = build_scalar_hierarchy(dev, sys0.Mp_cg, AmgConfig{});
     mats_.push_back(std::make_unique<DeviceMatrix>(dev, transfer.p0_pressure));
     const sag_matrix* pdup = mats_.back()->handle();
     mats_.push_back(std::make_unique<DeviceMatrix>(dev, sys0.M_mix));
@@ -238,9 +238,9 @@ HoAmgPreconditioner::HoAmgPreconditioner(Device& dev, const SaddleSystem& sys0, 
     // (preconditioner.cpp:163-168)
     SaddleSystem tmp = sys0;
     tmp.Ap = sys0.Mp;
-    h_ = build_monolithic_hierarchy(tmp, cfg_.amg);
+    h_ = build_monolithic_hierarchy(dev, tmp, cfg_.amg);
   } else {
-    h_ = build_monolithic_hierarchy(sys0, cfg_.amg);
+    h_ = build_monolithic_hierarchy(dev, sys0, cfg_.amg);
   }
   std::vector<sag_level_desc> lv(h_.num_levels());
   for (int l = 0; l < h_.num_levels(); ++l) {
@@ -287,9 +287,10 @@ UzawaPreconditioner::UzawaPreconditioner(Device& dev, const SaddleSystem& sys, S
   const int n_x = sys.n_x;
   n_u_ = sys.n_u();
   n_p_ = sys.n_p;
-  ScalarHierarchy hx = build_scalar_hierarchy(extract_block(sys.A, 0, n_x, 0, n_x), cfg_.amg);
+  ScalarHierarchy hx =
+      build_scalar_hierarchy(dev, extract_block(sys.A, 0, n_x, 0, n_x), cfg_.amg);
   ScalarHierarchy hy =
-      build_scalar_hierarchy(extract_block(sys.A, n_x, n_u_, n_x, n_u_), cfg_.amg);
+      build_scalar_hierarchy(dev, extract_block(sys.A, n_x, n_u_, n_x, n_u_), cfg_.amg);
   mats_.push_back(std::make_unique<DeviceMatrix>(dev, sys.B));
   const sag_matrix* b = mats_.back()->handle();
   ScalarUpload ux = upload_scalar(dev, hx, mats_), uy = upload_scalar(dev, hy, mats_);
@@ -298,7 +299,7 @@ UzawaPreconditioner::UzawaPreconditioner(Device& dev, const SaddleSystem& sys, S
     check(sag_uzawa_create(dev.handle(), b, n_x, n_u_ - n_x, n_p_, &ux.desc, &uy.desc, nullptr,
                            sys.sv_element_areas.data(), &c, &u_));
   } else {
-    ScalarHierarchy hp = build_scalar_hierarchy(sys.Mp, cfg_.amg);
+    ScalarHierarchy hp = build_scalar_hierarchy(dev, sys.Mp, cfg_.amg);
     ScalarUpload up = upload_scalar(dev, hp, mats_);
     check(sag_uzawa_create(dev.handle(), b, n_x, n_u_ - n_x, n_p_, &ux.desc, &uy.desc, &up.desc,
                            nullptr, &c, &u_));
@@ -369,28 +370,116 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 }
 }  // namespace
 
+// One coarsening step of a scalar block (amg.cpp:219-236, :317-329), the
+// setup timers and the strength-graph counters shared by both builders.
+struct DeviceSetup {
+  Device& dev;
+  const AmgConfig& cfg;
+  double t_host = 0.0, t_dev = 0.0;
+  int soc_dev = 0, soc_host = 0;
+  template <class F>
+  void host(F&& f) {
+    const auto t0 = std::chrono::steady_clock::now();
+    f();
+    t_host += seconds_since(t0);
+  }
+  template <class F>
+  void device(F&& f) {
+    const auto t0 = std::chrono::steady_clock::now();
+    f();
+    t_dev += seconds_since(t0);
+  }
+  struct Step {
+    SparseMatrix p;
+    DevM dp;
+    std::vector<double> coarse_null;
+  };
+  // SoC -> aggregate -> tentative -> smoothed prolongator; stagnated when
+  // the aggregation keeps more than 90% of the nodes (amg.cpp:216-219)
+  Step coarsen(const SparseMatrix& a, const DevM& da, const std::vector<double>& nullvec,
+               bool& stagnated) {
+    Step s;
+    TentativeResult tent;
+    double omega = 0.0;
+    bool stop = false;
+    // rho(D^-1 A): evolution_soc (amg.cpp:47-49) and smooth_prolongator
+    // (amg.cpp:227-229) estimate it identically -- once here, on the host
+    // (its start vector is the reference's mt19937 stream)
+    double rho = 0.0;
+    host([&] { rho = power_rho_estimate(a, inv_diagonal(a), 10); });
+    StrengthGraph g;
+    bool soc_on_device = false;
+    if (cfg.use_evolution_soc) {
+      device([&] {
+        sag_matrix* gh = nullptr;
+        if (sag_evolution_soc(dev.handle(), da.h, 4.0 / (3.0 * rho), cfg.theta, cfg.soc_k,
+                              &gh) == SAG_OK) {
+          DevM gm(gh);
+          const SparseMatrix gc = to_host(dev, gm);
+          g.n = gc.nrows;
+          g.offsets = gc.row_offsets;
+          g.neighbors = gc.col_indices;
+          g.weights = gc.values;
+          soc_on_device = true;
+          ++soc_dev;
+        }
+      });
+    }
+    host([&] {
+      if (!soc_on_device) {  // symmetric measure, or a support too large for the device table
+        g = cfg.use_evolution_soc ? evolution_soc(a, cfg.theta, cfg.soc_k)
+                                  : symmetric_soc(a, cfg.sym_theta);
+        ++soc_host;
+      }
+      const Aggregation agg = aggregate(g);
+      if (agg.num_aggregates > 0.9 * a.nrows) {
+        stop = true;
+        return;
+      }
+      tent = tentative_prolongator_with_nullvec(agg, nullvec);
+      omega = cfg.omega_frac / rho;
+    });
+    if (stop) {
+      stagnated = true;
+      return s;
+    }
+    device([&] {
+      DevM dt(dev, tent.t);
+      check(sag_smooth_prolongator(dev.handle(), da.h, dt.h, omega, &s.dp.h));
+      s.p = to_host(dev, s.dp);
+    });
+    s.coarse_null = std::move(tent.coarse_nullvec);
+    return s;
+  }
+  // P^T K P on the device; the result kept on the device and copied out
+  DevM galerkin(const DevM& p, const DevM& k, SparseMatrix& out) {
+    DevM r;
+    device([&] {
+      check(sag_galerkin(dev.handle(), p.h, k.h, &r.h));
+      out = to_host(dev, r);
+    });
+    return r;
+  }
+  void report(double* times) const {
+    if (!times) return;
+    times[0] = t_host;
+    times[1] = t_dev;
+    times[2] = soc_dev;
+    times[3] = soc_host;
+  }
+};
+
 MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& sys,
                                                const AmgConfig& cfg, double* times) {
   if (sys.Ap.nrows != sys.n_p)
     throw DimensionMismatch(
         "build_monolithic_hierarchy: pressure auxiliary operator does not match the pressure "
         "space");
-  double t_host = 0.0, t_dev = 0.0;
-  int soc_dev = 0, soc_host = 0;
-  auto host = [&](auto&& f) {
-    const auto t0 = std::chrono::steady_clock::now();
-    f();
-    t_host += seconds_since(t0);
-  };
-  auto device = [&](auto&& f) {
-    const auto t0 = std::chrono::steady_clock::now();
-    f();
-    t_dev += seconds_since(t0);
-  };
+  DeviceSetup S{dev, cfg};
   MonolithicHierarchy h;
   MonolithicLevel l0;
   SparseMatrix ax, ay, ap;
-  host([&] {
+  S.host([&] {
     l0.n_x = sys.n_x;
     l0.n_y = sys.n_y;
     l0.n_p = sys.n_p;
@@ -399,7 +488,7 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
     ap = sys.Ap;
   });
   DevM kcur, dax, day, dap;
-  device([&] {
+  S.device([&] {
     // assemble_saddle_matrix (fem.cpp:290-306) on the device
     DevM da(dev, sys.A), db(dev, sys.B);
     check(sag_saddle_matrix(dev.handle(), da.h, db.h, &kcur.h));
@@ -410,97 +499,26 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
   });
   h.levels.push_back(std::move(l0));
   std::vector<double> null_x(ax.nrows, 1.0), null_y(ay.nrows, 1.0), null_p(ap.nrows, 1.0);
-
-  struct Step {
-    SparseMatrix p;
-    DevM dp;
-    std::vector<double> coarse_null;
-  };
+  using Step = DeviceSetup::Step;
   while (h.num_levels() < cfg.max_levels) {
     MonolithicLevel& cur = h.levels.back();
     if (cur.total() <= cfg.coarse_size) break;
-    auto coarsen = [&](const SparseMatrix& a, const DevM& da, const std::vector<double>& nullvec,
-                       bool& stagnated) -> Step {
-      Step s;
-      TentativeResult tent;
-      double omega = 0.0;
-      bool stop = false;
-      // rho(D^-1 A): evolution_soc (amg.cpp:47-49) and smooth_prolongator
-      // (amg.cpp:227-229) estimate it identically -- once here, on the host
-      // (its start vector is the reference's mt19937 stream)
-      double rho = 0.0;
-      host([&] { rho = power_rho_estimate(a, inv_diagonal(a), 10); });
-      StrengthGraph g;
-      bool soc_on_device = false;
-      if (cfg.use_evolution_soc) {
-        device([&] {
-          sag_matrix* gh = nullptr;
-          if (sag_evolution_soc(dev.handle(), da.h, 4.0 / (3.0 * rho), cfg.theta, cfg.soc_k,
-                                &gh) == SAG_OK) {
-            DevM gm(gh);
-            const SparseMatrix gc = to_host(dev, gm);
-            g.n = gc.nrows;
-            g.offsets = gc.row_offsets;
-            g.neighbors = gc.col_indices;
-            g.weights = gc.values;
-            soc_on_device = true;
-            ++soc_dev;
-          }
-        });
-      }
-      host([&] {
-        if (!soc_on_device) {  // symmetric measure, or a support too large for the device table
-          g = cfg.use_evolution_soc ? evolution_soc(a, cfg.theta, cfg.soc_k)
-                                    : symmetric_soc(a, cfg.sym_theta);
-          ++soc_host;
-        }
-        const Aggregation agg = aggregate(g);
-        if (agg.num_aggregates > 0.9 * a.nrows) {
-          stop = true;
-          return;
-        }
-        tent = tentative_prolongator_with_nullvec(agg, nullvec);
-        omega = cfg.omega_frac / rho;
-      });
-      if (stop) {
-        stagnated = true;
-        return s;
-      }
-      device([&] {
-        DevM dt(dev, tent.t);
-        check(sag_smooth_prolongator(dev.handle(), da.h, dt.h, omega, &s.dp.h));
-        s.p = to_host(dev, s.dp);
-      });
-      s.coarse_null = std::move(tent.coarse_nullvec);
-      return s;
-    };
     bool stagnated = false;
-    Step sx = coarsen(ax, dax, null_x, stagnated);
-    Step sy = stagnated ? Step{} : coarsen(ay, day, null_y, stagnated);
-    Step sp = stagnated ? Step{} : coarsen(ap, dap, null_p, stagnated);
+    Step sx = S.coarsen(ax, dax, null_x, stagnated);
+    Step sy = stagnated ? Step{} : S.coarsen(ay, day, null_y, stagnated);
+    Step sp = stagnated ? Step{} : S.coarsen(ap, dap, null_p, stagnated);
     if (stagnated) {
       h.truncated = true;
       break;
     }
-    host([&] { cur.p = block_diag({&sx.p, &sy.p, &sp.p}); });
+    S.host([&] { cur.p = block_diag({&sx.p, &sy.p, &sp.p}); });
     MonolithicLevel next;
-    device([&] {
-      DevM dP(dev, cur.p);
-      DevM dk;
-      check(sag_galerkin(dev.handle(), dP.h, kcur.h, &dk.h));
-      next.k = to_host(dev, dk);
-      kcur = std::move(dk);
-      DevM nx_, ny_, np_;
-      check(sag_galerkin(dev.handle(), sx.dp.h, dax.h, &nx_.h));
-      check(sag_galerkin(dev.handle(), sy.dp.h, day.h, &ny_.h));
-      check(sag_galerkin(dev.handle(), sp.dp.h, dap.h, &np_.h));
-      ax = to_host(dev, nx_);
-      ay = to_host(dev, ny_);
-      ap = to_host(dev, np_);
-      dax = std::move(nx_);
-      day = std::move(ny_);
-      dap = std::move(np_);
-    });
+    DevM dP;
+    S.device([&] { dP = DevM(dev, cur.p); });
+    kcur = S.galerkin(dP, kcur, next.k);
+    dax = S.galerkin(sx.dp, dax, ax);
+    day = S.galerkin(sy.dp, day, ay);
+    dap = S.galerkin(sp.dp, dap, ap);
     next.n_x = sx.p.ncols;
     next.n_y = sy.p.ncols;
     next.n_p = sp.p.ncols;
@@ -509,12 +527,39 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
     null_p = std::move(sp.coarse_null);
     h.levels.push_back(std::move(next));
   }
-  if (times) {
-    times[0] = t_host;
-    times[1] = t_dev;
-    times[2] = soc_dev;
-    times[3] = soc_host;
+  S.report(times);
+  return h;
+}
+
+ScalarHierarchy build_scalar_hierarchy(Device& dev, const SparseMatrix& a, const AmgConfig& cfg,
+                                       double* times) {
+  DeviceSetup S{dev, cfg};
+  ScalarHierarchy h;
+  h.matrices.push_back(a);
+  std::vector<double> nullvec(a.nrows, 1.0);
+  DevM dcur;
+  S.device([&] { dcur = DevM(dev, a); });
+  while (h.levels() < cfg.max_levels) {
+    const SparseMatrix& cur = h.matrices.back();
+    if (cur.nrows <= cfg.coarse_size) break;
+    bool stagnated = false;
+    DeviceSetup::Step st = S.coarsen(cur, dcur, nullvec, stagnated);
+    if (stagnated) {
+      h.truncated = true;
+      break;
+    }
+    SparseMatrix coarse;
+    dcur = S.galerkin(st.dp, dcur, coarse);
+    h.prolongators.push_back(std::move(st.p));
+    h.matrices.push_back(std::move(coarse));
+    nullvec = std::move(st.coarse_null);
   }
+  S.host([&] {
+    for (size_t l = 0; l + 1 < h.matrices.size(); ++l)
+      h.d_inv.push_back(inv_diagonal(h.matrices[l]));
+    h.coarse_lu = dense_lu_factor(to_dense(h.matrices.back()));
+  });
+  S.report(times);
   return h;
 }
 
@@ -639,6 +684,48 @@ void* sagh_case_build(const char* problem, int sv, const char* mesh_kind, int n,
 }
 
 void sagh_case_free(void* h) { delete static_cast<HostCase*>(h); }
+
+// build_scalar_hierarchy by the reference and on the device for the case's
+// scalar operators -- A_x of the high-order system (Uzawa) and the pressure
+// auxiliary operator (TH: Mp; SV: the continuous mass matrix of the pressure
+// projection) -- compared bitwise: out = [equal (1/0), operators compared,
+// levels of the last, strength graphs on the device]
+int sagh_case_scalar_hierarchy_gpu(void* h, int device, double* out) {
+  return guarded([&] {
+    auto& hc = *static_cast<HostCase*>(h);
+    const SaddleSystem& s0 = hc.c.sys0;
+    std::vector<SparseMatrix> ops;
+    ops.push_back(extract_block(s0.A, 0, s0.n_x, 0, s0.n_x));
+    ops.push_back(s0.disc == Discretization::SV ? s0.Mp_cg : s0.Mp);
+    gpu::Device dev(device);
+    auto same = [](const SparseMatrix& a, const SparseMatrix& b) {
+      return a.nrows == b.nrows && a.ncols == b.ncols && a.row_offsets == b.row_offsets &&
+             a.col_indices == b.col_indices && a.values.size() == b.values.size() &&
+             std::memcmp(a.values.data(), b.values.data(), sizeof(double) * a.values.size()) == 0;
+    };
+    bool eq = true;
+    int levels = 0;
+    double soc = 0.0;
+    for (const auto& a : ops) {
+      const ScalarHierarchy ref = build_scalar_hierarchy(a, AmgConfig{});
+      double parts[4] = {0, 0, 0, 0};
+      const ScalarHierarchy got = gpu::build_scalar_hierarchy(dev, a, AmgConfig{}, parts);
+      soc += parts[2];
+      eq = eq && ref.levels() == got.levels() && ref.truncated == got.truncated &&
+           ref.coarse_lu.lu.values == got.coarse_lu.lu.values && ref.coarse_lu.pivot == got.coarse_lu.pivot;
+      for (int l = 0; eq && l < ref.levels(); ++l) {
+        eq = same(ref.matrices[l], got.matrices[l]) &&
+             (l + 1 == ref.levels() || same(ref.prolongators[l], got.prolongators[l]));
+        if (eq && l + 1 < ref.levels()) eq = ref.d_inv[l] == got.d_inv[l];
+      }
+      levels = got.levels();
+    }
+    out[0] = eq ? 1.0 : 0.0;
+    out[1] = (double)ops.size();
+    out[2] = levels;
+    out[3] = soc;
+  });
+}
 
 // The case's low-order hierarchy built again by the reference (host) and by
 // gpu::build_monolithic_hierarchy (device products), compared bitwise:

@@ -168,5 +168,9 @@ SolveResult solve_stokes(const SparseMatrix& k0, const std::vector<double>& rhs,
 // on the device, on the host].
 MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& sys,
                                                const AmgConfig& cfg, double* times = nullptr);
+// build_scalar_hierarchy (amg.hpp:74; amg.cpp:200-256) likewise: the scalar SA
+// hierarchies of the Uzawa preconditioner and the SV mass projection.
+ScalarHierarchy build_scalar_hierarchy(Device& dev, const SparseMatrix& a, const AmgConfig& cfg,
+                                       double* times = nullptr);
 
 }  // namespace stokesamg::gpu
