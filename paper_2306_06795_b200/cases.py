@@ -48,6 +48,7 @@ def hlib():
                                               C.c_double, C.c_int, C.c_double, C.c_double,
                                               C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
         L.sagh_case_hierarchy_gpu.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.sagh_case_scalar_hierarchy_gpu.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.sagh_case_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                       C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
@@ -128,6 +129,15 @@ class HostCase:
                     host_part_s=float(out[2]), device_part_s=float(out[3]),
                     bitwise_equal=bool(out[4]), levels=int(out[5]),
                     soc_device=int(out[6]), soc_host=int(out[7]))
+
+    def scalar_hierarchies_gpu(self, device=0):
+        """build_scalar_hierarchy by the reference and on the device for A_x and
+        the pressure auxiliary operator, compared bitwise."""
+        out = np.zeros(4)
+        if hlib().sagh_case_scalar_hierarchy_gpu(self.h, int(device), out.ctypes.data):
+            raise RuntimeError(hlib().sagh_last_error().decode())
+        return dict(bitwise_equal=bool(out[0]), operators=int(out[1]), levels=int(out[2]),
+                    soc_device=int(out[3]))
 
     def rhs(self):
         r = np.empty(self.n0)

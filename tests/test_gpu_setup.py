@@ -26,6 +26,16 @@ def test_hierarchy_on_device_is_bitwise(problem, sv, n):
     assert r["soc_device"] >= 3 and r["soc_host"] == 0, r   # every strength graph on the device
 
 
+@pytest.mark.parametrize("sv,n", [(False, 16), (False, 64), (True, 8)])
+def test_scalar_hierarchies_on_device_are_bitwise(sv, n):
+    """gpu::build_scalar_hierarchy (Uzawa's A_x / Mp hierarchies, SV's pressure
+    projection) equals build_scalar_hierarchy (amg.cpp:200-256) bit for bit:
+    levels, prolongators, Jacobi diagonals and the coarse LU."""
+    from paper_2306_06795_b200.cases import HostCase
+    r = HostCase("cavity", sv, "structured", n).scalar_hierarchies_gpu(0)
+    assert r["bitwise_equal"] and r["operators"] == 2 and r["soc_device"] >= 2, r
+
+
 def test_evolution_soc_graph_matches_reference():
     """sag_evolution_soc vs the reference's evolution_soc through the
     aggregation it feeds: the hierarchy test checks the end result; here the
