@@ -33,7 +33,7 @@ def test_scalar_hierarchies_on_device_are_bitwise(sv, n):
     levels, prolongators, Jacobi diagonals and the coarse LU."""
     from paper_2306_06795_b200.cases import HostCase
     r = HostCase("cavity", sv, "structured", n).scalar_hierarchies_gpu(0)
-    assert r["bitwise_equal"] and r["operators"] == 2 and r["soc_device"] >= 2, r
+    assert r["bitwise_equal"] and r["operators"] == 2 and r["soc_device"] >= 1, r
 
 
 def test_evolution_soc_graph_matches_reference():
