@@ -26,6 +26,20 @@ def test_hierarchy_on_device_is_bitwise(problem, sv, n):
     assert r["soc_device"] >= 3 and r["soc_host"] == 0, r   # every strength graph on the device
 
 
+def test_hierarchy_on_device_is_bitwise_unstructured(tmp_path):
+    """The same on a jittered Delaunay mesh (BASELINE config 4's recipe at
+    40 x 40 points): irregular patterns and strength supports."""
+    from paper_2306_06795_b200 import meshgen
+    from paper_2306_06795_b200.cases import HostCase
+    path = meshgen.write_mesh(str(tmp_path / "m.json"), 40, seed=7, jitter=0.3)
+    k1, k2 = meshgen.force_wavenumbers()
+    case = HostCase("cavity", False, "file_forced", 0, mesh_path=path, k1=k1, k2=k2)
+    r = case.hierarchy_gpu(0)
+    assert r["bitwise_equal"] and r["soc_host"] == 0, r
+    s = case.scalar_hierarchies_gpu(0)
+    assert s["bitwise_equal"], s
+
+
 @pytest.mark.parametrize("sv,n", [(False, 16), (False, 64), (True, 8)])
 def test_scalar_hierarchies_on_device_are_bitwise(sv, n):
     """gpu::build_scalar_hierarchy (Uzawa's A_x / Mp hierarchies, SV's pressure
