@@ -23,19 +23,56 @@
 
 namespace sag {
 
-constexpr int kSpgCap = 2048;   // hash slots per warp (columns of one output row)
-constexpr int kSpgWarps = 4;    // warps per CTA
-constexpr int kSpgSmem = kSpgWarps * kSpgCap * (4 + 8 + 4 + 8);
+// Per-warp tables are sized per launch from the largest row (a pre-pass):
+// a power of two >= 2x the row's products, so CTAs hold as many warps as the
+// shared memory allows (4096 slots at most).
+constexpr int kSetupMaxCap = 4096;
+constexpr int kSpgSlot = 4 + 8 + 4 + 8;  // key, value, listed column, listed value
+constexpr int kSetupSmem = 200 * 1024;
+
+// upper bound of the distinct columns of each output row (mode 0, spgemm:
+// sum of the B-row lengths over A's row) or of a column's 2-step support
+// (mode 1, evolution_soc: 1 + deg(j) + sum of its neighbours' degrees); max
+__global__ void max_est_kernel(int nrows, const int* __restrict__ arp,
+                               const int* __restrict__ aci, const int* __restrict__ brp, int mode,
+                               int* __restrict__ out) {
+  int best = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    int e = mode ? 1 + arp[r + 1] - arp[r] : 0;
+    for (int q = arp[r]; q < arp[r + 1]; ++q) {
+      const int j = aci[q];
+      e += brp[j + 1] - brp[j];
+    }
+    best = max(best, e);
+  }
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+static int table_cap(Ctx& c, int nrows, const int* arp, const int* aci, const int* brp, int mode) {
+  DevBuf<int> m(1);
+  SAG_CUDA(cudaMemsetAsync(m.p, 0, sizeof(int), c.stream));
+  const int g = std::max(1, std::min((nrows + 255) / 256, c.num_sms * 8));
+  max_est_kernel<<<g, 256, 0, c.stream>>>(nrows, arp, aci, brp, mode, m.p);
+  SAG_LAUNCHED(c);
+  int h = 0;
+  SAG_CUDA(cudaMemcpyAsync(&h, m.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  int cap = 64;
+  while (cap < 2 * h && cap < kSetupMaxCap) cap <<= 1;
+  return cap;
+}
 
 // one output row r of C = A B into the warp's table; returns the count of
 // distinct columns (cnt) with lc / lv the compacted (column, value) lists
 __device__ __forceinline__ int spg_row(int r, const int* __restrict__ arp,
                                        const int* __restrict__ aci, const double* __restrict__ av,
                                        const int* __restrict__ brp, const int* __restrict__ bci,
-                                       const double* __restrict__ bv, int* keys, double* vals,
-                                       int* lc, double* lv, int* counter, int* overflow) {
+                                       const double* __restrict__ bv, int capw, int* keys,
+                                       double* vals, int* lc, double* lv, int* counter,
+                                       int* overflow) {
   const int lane = threadIdx.x & 31;
-  // table size: a power of two >= 2x the row's products (at most kSpgCap)
+  // table size: a power of two >= 2x the row's products (at most capw)
   int prod = 0;
   for (int ka = arp[r] + lane; ka < arp[r + 1]; ka += 32) {
     const int j = aci[ka];
@@ -43,7 +80,7 @@ __device__ __forceinline__ int spg_row(int r, const int* __restrict__ arp,
   }
   for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
   int cap = 64;
-  while (cap < 2 * prod && cap < kSpgCap) cap <<= 1;
+  while (cap < 2 * prod && cap < capw) cap <<= 1;
   const unsigned mask = cap - 1;
   for (int s = lane; s < cap; s += 32) keys[s] = -1;
   if (lane == 0) *counter = 0;
@@ -90,23 +127,23 @@ __device__ __forceinline__ int spg_row(int r, const int* __restrict__ arp,
 
 // pass 0: nonzero count per row; pass 1: the row, columns ascending, exact
 // zeros dropped (sparse.cpp:140-146)
-__global__ void __launch_bounds__(kSpgWarps * 32) spgemm_kernel(
+__global__ void __launch_bounds__(512) spgemm_kernel(
     int nrows, const int* __restrict__ arp, const int* __restrict__ aci,
     const double* __restrict__ av, const int* __restrict__ brp, const int* __restrict__ bci,
-    const double* __restrict__ bv, int pass, int* __restrict__ row_nnz,
+    const double* __restrict__ bv, int capw, int pass, int* __restrict__ row_nnz,
     const int* __restrict__ crp, int* __restrict__ cci, double* __restrict__ cv, int* overflow) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* base = smem + (size_t)wib * kSpgCap * (4 + 8 + 4 + 8);
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+  unsigned char* base = smem + (size_t)wib * capw * kSpgSlot;
   double* vals = reinterpret_cast<double*>(base);
-  double* lv = vals + kSpgCap;
-  int* keys = reinterpret_cast<int*>(lv + kSpgCap);
-  int* lc = keys + kSpgCap;
-  __shared__ int counters[kSpgWarps];
-  const int gw = blockIdx.x * kSpgWarps + wib, nw = gridDim.x * kSpgWarps;
+  double* lv = vals + capw;
+  int* keys = reinterpret_cast<int*>(lv + capw);
+  int* lc = keys + capw;
+  __shared__ int counters[16];
+  const int gw = blockIdx.x * warps + wib, nw = gridDim.x * warps;
   for (int r = gw; r < nrows; r += nw) {
-    const int cnt = spg_row(r, arp, aci, av, brp, bci, bv, keys, vals, lc, lv, counters + wib,
-                            overflow);
+    const int cnt = spg_row(r, arp, aci, av, brp, bci, bv, capw, keys, vals, lc, lv,
+                            counters + wib, overflow);
     int nz = 0;
     for (int e = lane; e < cnt; e += 32) nz += lv[e] != 0.0;
     for (int o = 16; o > 0; o >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, o);
@@ -128,9 +165,11 @@ __global__ void __launch_bounds__(kSpgWarps * 32) spgemm_kernel(
   }
 }
 
-static int setup_grid(Ctx& c, long long rows) {
-  const long long need = (rows + kSpgWarps - 1) / kSpgWarps;
-  return (int)std::max(1LL, std::min(need, (long long)c.num_sms * 8));
+// warps per CTA for a per-warp table of `bytes`, and the grid over `rows`
+static int setup_warps(int bytes) { return std::max(1, std::min(16, kSetupSmem / bytes)); }
+static int setup_grid(Ctx& c, long long rows, int warps) {
+  const long long need = (rows + warps - 1) / warps;
+  return (int)std::max(1LL, std::min(need, (long long)c.num_sms * 32));
 }
 
 // CSR from device row counts + a fill callback on the allocated arrays.
@@ -156,24 +195,27 @@ std::unique_ptr<Matrix> spgemm_dev(Ctx& c, const Matrix& a, const Matrix& b) {
   static bool configured = false;
   if (!configured) {
     SAG_CUDA(cudaFuncSetAttribute(spgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSpgSmem));
+                                  kSetupSmem));
     configured = true;
   }
+  const int capw = table_cap(c, a.nrows, a.rp.p, a.ci.p, b.rp.p, 0);
+  const int warps = setup_warps(capw * kSpgSlot), smem = warps * capw * kSpgSlot;
   DevBuf<int> cnt(a.nrows + 1), ovf(1);
   SAG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (a.nrows + 1), c.stream));
   SAG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c.stream));
-  const int grid = setup_grid(c, a.nrows);
-  spgemm_kernel<<<grid, kSpgWarps * 32, kSpgSmem, c.stream>>>(
-      a.nrows, a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, 0, cnt.p, nullptr, nullptr, nullptr,
-      ovf.p);
+  const int grid = setup_grid(c, a.nrows, warps);
+  spgemm_kernel<<<grid, warps * 32, smem, c.stream>>>(a.nrows, a.rp.p, a.ci.p, a.v.p, b.rp.p,
+                                                      b.ci.p, b.v.p, capw, 0, cnt.p, nullptr,
+                                                      nullptr, nullptr, ovf.p);
   SAG_LAUNCHED(c);
   int hov = 0;
   SAG_CUDA(cudaMemcpyAsync(&hov, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SAG_CUDA(cudaStreamSynchronize(c.stream));
-  SAG_REQUIRE(!hov, SAG_ERROR, "spgemm: an output row has more than 2048 distinct columns");
+  SAG_REQUIRE(!hov, SAG_ERROR, "spgemm: an output row has more than 4096 distinct columns");
   return csr_from_counts(c, a.nrows, b.ncols, cnt, [&](int* rp, int* ci, double* v) {
-    spgemm_kernel<<<grid, kSpgWarps * 32, kSpgSmem, c.stream>>>(
-        a.nrows, a.rp.p, a.ci.p, a.v.p, b.rp.p, b.ci.p, b.v.p, 1, nullptr, rp, ci, v, ovf.p);
+    spgemm_kernel<<<grid, warps * 32, smem, c.stream>>>(a.nrows, a.rp.p, a.ci.p, a.v.p, b.rp.p,
+                                                        b.ci.p, b.v.p, capw, 1, nullptr, rp, ci,
+                                                        v, ovf.p);
     SAG_LAUNCHED(c);
   });
 }
@@ -271,10 +313,8 @@ std::unique_ptr<Matrix> smooth_prolongator_dev(Ctx& c, const Matrix& a, const Ma
 // (i, j, s) and (j, i, s) for s = |z_i| / |z_j| >= theta max_m s_m; the
 // union is sorted and duplicates keep the stronger weight
 // (graph_from_adjacency, amg.cpp:13-42).
-constexpr int kSocCap = 2048;
-constexpr int kSocWarps = 3;
-constexpr int kSocWarpBytes = kSocCap * (4 + 8 + 8 + 4 + 4 + 1);
-constexpr int kSocSmem = kSocWarps * ((kSocWarpBytes + 15) / 16 * 16);
+constexpr int kSocSlot = 4 + 8 + 8 + 4 + 4 + 1;  // key, z, az, touched, az_touched, flags
+static int soc_warp_bytes(int capw) { return (capw * kSocSlot + 15) / 16 * 16; }
 
 struct SocTable {
   int* keys;
@@ -307,26 +347,26 @@ struct SocTable {
   }
 };
 
-__global__ void __launch_bounds__(kSocWarps * 32) evolution_soc_kernel(
+__global__ void __launch_bounds__(512) evolution_soc_kernel(
     int n, const int* __restrict__ trp, const int* __restrict__ tci, const double* __restrict__ tv,
-    const double* __restrict__ dinv, double omega, double theta, int ksteps, int pass,
+    const double* __restrict__ dinv, double omega, double theta, int ksteps, int capw, int pass,
     int* __restrict__ cnt, const long long* __restrict__ eoff, unsigned long long* __restrict__ ekey,
     double* __restrict__ eval, int* overflow) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31, warps = blockDim.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  unsigned char* base = smem + (size_t)wib * ((kSocWarpBytes + 15) / 16 * 16);
+  unsigned char* base = smem + (size_t)wib * ((capw * kSocSlot + 15) / 16 * 16);
   SocTable T;
   T.z = reinterpret_cast<double*>(base);
-  T.az = T.z + kSocCap;
-  T.keys = reinterpret_cast<int*>(T.az + kSocCap);
-  T.touched = T.keys + kSocCap;
-  T.azt = T.touched + kSocCap;
-  T.fl = reinterpret_cast<unsigned char*>(T.azt + kSocCap);
-  __shared__ int wcount[kSocWarps];
-  const int gw = blockIdx.x * kSocWarps + wib, nw = gridDim.x * kSocWarps;
+  T.az = T.z + capw;
+  T.keys = reinterpret_cast<int*>(T.az + capw);
+  T.touched = T.keys + capw;
+  T.azt = T.touched + capw;
+  T.fl = reinterpret_cast<unsigned char*>(T.azt + capw);
+  __shared__ int wcount[16];
+  const int gw = blockIdx.x * warps + wib, nw = gridDim.x * warps;
   for (int j = gw; j < n; j += nw) {
-    // table size: >= 2x an upper bound of the touched set (k = 2), <= kSocCap
+    // table size: >= 2x an upper bound of the touched set (k = 2), <= capw
     int est = 0;
     if (ksteps == 2) {
       for (int q = trp[j] + lane; q < trp[j + 1]; q += 32) {
@@ -336,10 +376,10 @@ __global__ void __launch_bounds__(kSocWarps * 32) evolution_soc_kernel(
       for (int o = 16; o > 0; o >>= 1) est += __shfl_xor_sync(0xffffffffu, est, o);
       est += 1 + trp[j + 1] - trp[j];
     } else {
-      est = kSocCap;
+      est = capw;
     }
     int cap = 64;
-    while (cap < 2 * est && cap < kSocCap) cap <<= 1;
+    while (cap < 2 * est && cap < capw) cap <<= 1;
     T.mask = cap - 1;
     for (int s = lane; s < cap; s += 32) T.keys[s] = -1;
     __syncwarp();
@@ -372,7 +412,7 @@ __global__ void __launch_bounds__(kSocWarps * 32) evolution_soc_kernel(
           const unsigned m = __ballot_sync(0xffffffffu, act && isnew);
           if (act && isnew) {
             const int pos = naz + __popc(m & lt);
-            if (pos < kSocCap) T.azt[pos] = tci[q];
+            if (pos < capw) T.azt[pos] = tci[q];
             T.fl[slot] |= 2;
             T.az[slot] = 0.0;
           }
@@ -381,8 +421,8 @@ __global__ void __launch_bounds__(kSocWarps * 32) evolution_soc_kernel(
           __syncwarp();
         }
       }
-      if (naz > kSocCap) ovf = true;
-      for (int u0 = 0; u0 < naz && u0 < kSocCap; u0 += 32) {
+      if (naz > capw) ovf = true;
+      for (int u0 = 0; u0 < naz && u0 < capw; u0 += 32) {
         const int u = u0 + lane;
         const bool act = u < naz;
         int slot = 0, i = 0;
@@ -395,7 +435,7 @@ __global__ void __launch_bounds__(kSocWarps * 32) evolution_soc_kernel(
         const unsigned m = __ballot_sync(0xffffffffu, act && newt);
         if (act && newt) {
           const int pos = nt + __popc(m & lt);
-          if (pos < kSocCap) T.touched[pos] = i;
+          if (pos < capw) T.touched[pos] = i;
           T.fl[slot] |= 1;
         }
         nt += __popc(m);
@@ -405,9 +445,9 @@ __global__ void __launch_bounds__(kSocWarps * 32) evolution_soc_kernel(
         }
         __syncwarp();
       }
-      if (nt > kSocCap) {
+      if (nt > capw) {
         ovf = true;
-        nt = kSocCap;
+        nt = capw;
       }
     }
     // strength over the touched set (amg.cpp:86-101)
@@ -481,7 +521,7 @@ std::unique_ptr<Matrix> evolution_soc_dev(Ctx& c, const Matrix& a, double omega,
   static bool configured = false;
   if (!configured) {
     SAG_CUDA(cudaFuncSetAttribute(evolution_soc_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSocSmem));
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSetupSmem));
     configured = true;
   }
   auto at = transpose_dev(c, a);
@@ -491,20 +531,21 @@ std::unique_ptr<Matrix> evolution_soc_dev(Ctx& c, const Matrix& a, double omega,
   SAG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), c.stream));
   SAG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c.stream));
   launch_inv_diag(c, a, dinv.p, bad.p);
+  const int capw = ksteps == 2 ? table_cap(c, n, at->rp.p, at->ci.p, at->rp.p, 1) : kSetupMaxCap;
+  const int warps = setup_warps(soc_warp_bytes(capw)), smem = warps * soc_warp_bytes(capw);
   DevBuf<int> cnt(n + 1);
   SAG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (n + 1), c.stream));
-  const long long need = ((long long)n + kSocWarps - 1) / kSocWarps;
-  const int grid = (int)std::max(1LL, std::min(need, (long long)c.num_sms * 4));
-  evolution_soc_kernel<<<grid, kSocWarps * 32, kSocSmem, c.stream>>>(
-      n, at->rp.p, at->ci.p, at->v.p, dinv.p, omega, theta, ksteps, 0, cnt.p, nullptr, nullptr,
-      nullptr, ovf.p);
+  const int grid = setup_grid(c, n, warps);
+  evolution_soc_kernel<<<grid, warps * 32, smem, c.stream>>>(
+      n, at->rp.p, at->ci.p, at->v.p, dinv.p, omega, theta, ksteps, capw, 0, cnt.p, nullptr,
+      nullptr, nullptr, ovf.p);
   SAG_LAUNCHED(c);
   int hb = 0, ho = 0;
   SAG_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SAG_CUDA(cudaMemcpyAsync(&ho, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   SAG_CUDA(cudaStreamSynchronize(c.stream));
   SAG_REQUIRE(!hb, SAG_ZERO_DIAGONAL, "inv_diagonal: zero diagonal");
-  SAG_REQUIRE(!ho, SAG_ERROR, "evolution_soc: a column's touched set exceeds 2048 nodes");
+  SAG_REQUIRE(!ho, SAG_ERROR, "evolution_soc: a column's touched set exceeds the device table");
   // edge offsets (int64), then the edges
   DevBuf<long long> eoff(n + 1);
   {
@@ -519,9 +560,9 @@ std::unique_ptr<Matrix> evolution_soc_dev(Ctx& c, const Matrix& a, double omega,
     SAG_REQUIRE(ne < (1LL << 31), SAG_DIMENSION_MISMATCH, "evolution_soc: too many edges");
     DevBuf<unsigned long long> key(std::max(ne, 1LL)), key2(std::max(ne, 1LL));
     DevBuf<double> val(std::max(ne, 1LL)), val2(std::max(ne, 1LL));
-    evolution_soc_kernel<<<grid, kSocWarps * 32, kSocSmem, c.stream>>>(
-        n, at->rp.p, at->ci.p, at->v.p, dinv.p, omega, theta, ksteps, 1, nullptr, eoff.p, key.p,
-        val.p, ovf.p);
+    evolution_soc_kernel<<<grid, warps * 32, smem, c.stream>>>(
+        n, at->rp.p, at->ci.p, at->v.p, dinv.p, omega, theta, ksteps, capw, 1, nullptr, eoff.p,
+        key.p, val.p, ovf.p);
     SAG_LAUNCHED(c);
     size_t t1 = 0;
     SAG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t1, key.p, key2.p, val.p, val2.p, (int)ne, 0,
