@@ -31,6 +31,7 @@ several ranks share one device, and in the CPU tests).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -86,8 +87,6 @@ class Comm:
         for dst, h in back:
             dst.copy_(h)
 
-    def exchange(self, sends: dict, recvs: dict):
-        self.finish(self.start(sends, recvs))
 
 
 # -------------------------------------------------------------- backend --
@@ -381,7 +380,6 @@ class DistSolver(DistStep):
         self.stream = getattr(be, "stream", None)
         # (several ranks: collectives inside a captured graph are opt-in,
         # SAG_DIST_GRAPH=1 -- this build has not been run on more than one GPU)
-        import os
         self.use_graph = (self.stream is not None and not comm.stage
                           and max(cfg.nu1, cfg.nu2) <= 1
                           and (comm.size == 1 or os.environ.get("SAG_DIST_GRAPH") == "1"))

@@ -40,14 +40,16 @@ def golden_system(name):
     return g, k0, levels, nxyz0
 
 
-def reference_system(n):
-    """A deeper hierarchy straight from the reference build (oracle/_ref)."""
+def reference_system(n, variant=0, gamma=1):
+    """A deeper hierarchy straight from the reference build (oracle/_ref), and
+    the reference's solve with preconditioner `variant` (DC-all / DC-LO /
+    DC-HO) and gamma V-cycles."""
     from conftest import ref_case
-    c, d, k0, levels, conf = ref_case(n)
+    c, d, k0, levels, conf = ref_case(n, cfg=dict(variant=variant, gamma=gamma))
     xs, rep = d.solve(c.rhs())
     g = {"rhs": c.rhs(), "solve_x": xs, "solve_iterations": np.array(rep["iterations"]),
          "config": np.array([1, 1, 30, 500]), "config_f": np.array([1e-8, 1.0, 1.0, 1.0]),
-         "enclosed": np.array(int(c.enclosed))}
+         "enclosed": np.array(int(c.enclosed)), "variant": variant, "gamma": gamma}
     return g, k0, levels, (c.n_x0, c.n_y0, c.n_p0)
 
 
@@ -68,11 +70,12 @@ def _worker(rank, world, port, source, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         g, k0, levels, nxyz0 = (golden_system(source) if isinstance(source, str)
-                                else reference_system(source))
+                                else reference_system(*source))
         nu1, nu2, restart, max_iters = (int(v) for v in g["config"])
         tol = float(g["config_f"][0])
         cfg = S.SolverConfig(nu1=nu1, nu2=nu2, restart=restart, tol=tol, max_iters=max_iters,
-                             enclosed_flow=bool(int(g["enclosed"])))
+                             enclosed_flow=bool(int(g["enclosed"])),
+                             variant=int(g.get("variant", 0)), gamma=int(g.get("gamma", 1)))
         l0, p0, nxyz_l0 = levels[0]
         rs = build_rank_systems(world, k0, l0, p0, nxyz0, nxyz_l0, ranks=[rank])[0]
         be = CheckerBackend()
@@ -104,10 +107,13 @@ def _run(world, source):
 
 @pytest.mark.parametrize("world,source", [(1, "th_cavity_8"), (2, "th_cavity_8"),
                                           (1, "th_cavity_16"), (2, "th_cavity_16"),
-                                          (1, 32), (2, 32), (3, 32)])
+                                          (1, (32,)), (2, (32,)), (3, (32,)),
+                                          (2, (32, 1)), (2, (32, 2)), (2, (32, 0, 2))])
 def test_distributed_solve_matches_reference(world, source):
+    """source: a golden case, or (n, variant, gamma) of a reference-built one
+    (DC-all / DC-LO / DC-HO, gamma V-cycles)."""
     pytest.importorskip("torch")
-    g = (golden_system(source)[0] if isinstance(source, str) else reference_system(source)[0])
+    g = (golden_system(source)[0] if isinstance(source, str) else reference_system(*source)[0])
     out = _run(world, source)
     n = len(g["rhs"])
     x = np.full(n, np.nan)

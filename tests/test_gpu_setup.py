@@ -125,3 +125,22 @@ def test_spgemm_transpose_match_reference():
     del ref_t
     kp = S.spgemm(K, P).to_csr()
     assert kp[0][-1] > 0 and (np.diff(kp[0]) >= 0).all()
+
+
+def test_spgemm_drops_exact_cancellation_and_keeps_empty_rows():
+    """sparse.cpp:140-146: an entry whose products cancel to exactly 0.0 is
+    not stored; rows without products stay empty; columns ascend."""
+    import paper_2306_06795_b200 as S
+    # A = [[1, 1, 0], [0, 0, 0], [2, 0, 3]], B = [[1, 2], [-1, 5], [0, 1]]
+    a = S.SparseMatrix(3, 3, [0, 2, 2, 4], [0, 1, 0, 2], [1.0, 1.0, 2.0, 3.0])
+    b = S.SparseMatrix(3, 2, [0, 2, 4, 5], [0, 1, 0, 1, 1], [1.0, 2.0, -1.0, 5.0, 1.0])
+    rp, ci, v = S.spgemm(a, b).to_csr()
+    # row 0: (1 - 1, 2 + 5) -> col 0 cancels exactly; row 1 empty; row 2: (2, 4 + 3)
+    assert list(rp) == [0, 1, 1, 3]
+    assert list(ci) == [1, 0, 1] and list(v) == [7.0, 2.0, 7.0]
+    # transpose of the result and a Galerkin product with an identity prolongator
+    t = S.transpose(S.spgemm(a, b)).to_csr()
+    assert list(t[0]) == [0, 1, 3] and list(t[1]) == [2, 0, 2]
+    eye = S.SparseMatrix(3, 3, [0, 1, 2, 3], [0, 1, 2], [1.0, 1.0, 1.0])
+    g = S.galerkin_triple(eye, a).to_csr()
+    assert list(g[0]) == [0, 2, 2, 4] and list(g[2]) == [1.0, 1.0, 2.0, 3.0]
