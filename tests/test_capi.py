@@ -102,3 +102,38 @@ def test_host_case_builds_reference_hierarchy():
         assert tuple(nxyz) == tuple(gold[f"L{l}_nxyz"])
     assert np.array_equal(h.rhs(), gold["rhs"])
     _ = O  # the host case and the oracle agree through the golden fixture
+
+
+@pytest.mark.parametrize("name,args", [
+    ("sag_spgemm", (None, None, None, None)),
+    ("sag_transpose", (None, None, None)),
+    ("sag_galerkin", (None, None, None, None)),
+    ("sag_smooth_prolongator", (None, None, None, C.c_double(1.0), None)),
+    ("sag_evolution_soc", (None, None, C.c_double(1.0), C.c_double(0.5), 2, None)),
+    ("sag_saddle_matrix", (None, None, None, None)),
+    ("sag_matrix_export", (None, None, None, None, None)),
+    ("sag_dot_async", (None, 0, None, None, None, None)),
+    ("sag_axpy_async", (None, 0, None, C.c_double(-1.0), None, None)),
+    ("sag_gather_async", (None, 0, None, None, None)),
+    ("sag_vanka_spmv", (None, None, None, None, None, None)),
+    ("sag_apply_vanka_add", (None, None, None, None, C.c_double(1.0))),
+    ("sag_dc_set_coarse_pin", (None, None, C.c_double(1.0))),
+])
+def test_entry_points_reject_null_handles(name, args):
+    """The boundary's error convention (errors.hpp:8-58 + SAG_INVALID_ARGUMENT):
+    a null handle is a status code and a message, never a crash -- checkable
+    without a GPU."""
+    fn = getattr(S.lib(), name)
+    assert fn(*args) == 101
+    assert S.lib().sag_last_error()
+
+
+def test_host_case_device_setup_entry_exported():
+    path = os.path.join(ROOT, "paper_2306_06795_b200", "libsag_stokesamg.so")
+    if not os.path.exists(path):
+        pytest.skip("host adapter not built")
+    out = os.popen(f"nm -DC {path}").read()
+    assert "stokesamg::gpu::build_monolithic_hierarchy" in out
+    assert "stokesamg::gpu::build_scalar_hierarchy" in out
+    lib = C.CDLL(path)
+    assert hasattr(lib, "sagh_case_hierarchy_gpu") and hasattr(lib, "sagh_case_scalar_hierarchy_gpu")

@@ -53,6 +53,33 @@ def reference_system(n, variant=0, gamma=1):
     return g, k0, levels, (c.n_x0, c.n_y0, c.n_p0)
 
 
+def unstructured_system(n):
+    """BASELINE config 4's recipe (jittered Delaunay, zero velocity, forced)
+    at n x n points, built and solved by the reference (oracle/_ref)."""
+    import tempfile
+    import oracle as O
+    from paper_2306_06795_b200 import meshgen
+    path = os.path.join(tempfile.gettempdir(), f"sag_test_mesh_{n}_{os.getpid()}.json")
+    meshgen.write_mesh(path, n, seed=7, jitter=0.3)
+    k1, k2 = meshgen.force_wavenumbers()
+    c = O.RefCase.mesh_forced(path, k1, k2)
+    conf = dict(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500, enclosed_flow=c.enclosed)
+    d = O.RefDC(c, conf)
+    xs, rep = d.solve(c.rhs())
+    g = {"rhs": c.rhs(), "solve_x": xs, "solve_iterations": np.array(rep["iterations"]),
+         "config": np.array([1, 1, 30, 500]), "config_f": np.array([1e-8, 1.0, 1.0, 1.0]),
+         "enclosed": np.array(int(c.enclosed))}
+    return g, d.k0().csr(), d.levels_csr(), (c.n_x0, c.n_y0, c.n_p0)
+
+
+def _system(source):
+    if isinstance(source, str):
+        return golden_system(source)
+    if source[0] == "mesh":
+        return unstructured_system(source[1])
+    return reference_system(*source)
+
+
 def _worker(rank, world, port, source, q):
     import sys
     sys.path.insert(0, ROOT)
@@ -69,8 +96,7 @@ def _worker(rank, world, port, source, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        g, k0, levels, nxyz0 = (golden_system(source) if isinstance(source, str)
-                                else reference_system(*source))
+        g, k0, levels, nxyz0 = _system(source)
         nu1, nu2, restart, max_iters = (int(v) for v in g["config"])
         tol = float(g["config_f"][0])
         cfg = S.SolverConfig(nu1=nu1, nu2=nu2, restart=restart, tol=tol, max_iters=max_iters,
@@ -108,12 +134,13 @@ def _run(world, source):
 @pytest.mark.parametrize("world,source", [(1, "th_cavity_8"), (2, "th_cavity_8"),
                                           (1, "th_cavity_16"), (2, "th_cavity_16"),
                                           (1, (32,)), (2, (32,)), (3, (32,)),
-                                          (2, (32, 1)), (2, (32, 2)), (2, (32, 0, 2))])
+                                          (2, (32, 1)), (2, (32, 2)), (2, (32, 0, 2)),
+                                          (3, ("mesh", 24))])
 def test_distributed_solve_matches_reference(world, source):
     """source: a golden case, or (n, variant, gamma) of a reference-built one
     (DC-all / DC-LO / DC-HO, gamma V-cycles)."""
     pytest.importorskip("torch")
-    g = (golden_system(source)[0] if isinstance(source, str) else reference_system(*source)[0])
+    g = _system(source)[0]
     out = _run(world, source)
     n = len(g["rhs"])
     x = np.full(n, np.nan)
