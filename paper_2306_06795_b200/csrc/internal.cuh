@@ -96,8 +96,6 @@ struct Vanka {
   // patch), so the patch kernel writes there and the gather reads every
   // dof's contributions as one contiguous run -- no dof_slot indirection
   bool seq = false;
-  // one-seed paired patches of the 32-lane classes store no b_hat (nob)
-  std::vector<unsigned char> h_nob;  // per patch (patch order)
   long long a_factor_bytes = 0, aux_bytes = 0, dense_inverse_bytes = 0;
   long long blob_bytes = 0;
   bool sym = false;  // A^-1 blocks stored as packed symmetrised upper triangles
@@ -134,13 +132,6 @@ __host__ __device__ inline bool vanka_paired(bool pairs, int nx, int ny, int np)
 // A pairs (m x m packed) | U pairs [a][i] | B pairs [a][j] | S^-1 (np x np)
 __host__ __device__ inline long long vanka_paired_doubles(int m, int np) {
   return (long long)m * (m + 1) + 4LL * np * m + (long long)np * np;
-}
-
-// Paired blob without the b_hat pairs (one pressure seed: b_hat = S^-1 u_hat^T
-// is one product per entry, vanka.cpp:133-140, formed in the apply):
-// A pairs | U pairs | S^-1
-__host__ __device__ inline long long vanka_paired_doubles_nob(int m, int np) {
-  return (long long)m * (m + 1) + 2LL * np * m + (long long)np * np;
 }
 
 struct KState {

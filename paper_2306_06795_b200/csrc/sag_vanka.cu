@@ -318,7 +318,6 @@ struct FactorOut {
   const int* sbase = nullptr;
   int tps = 0;  // streamed thread-per-patch section order
   int pairs = 0;  // paired blob layout for qualifying patches (vanka_paired)
-  const unsigned char* nob = nullptr;  // per patch: paired blob without b_hat
 };
 
 __global__ void __launch_bounds__(256) factor_kernel(
@@ -396,7 +395,6 @@ __global__ void __launch_bounds__(256) factor_kernel(
     // paired blob: (A_x,A_y) | (U_x,U_y) | (B_x,B_y) interleaved, then S^-1;
     // sa/su = element strides of the A and U sections
     const bool pr = !fo.tps && vanka_paired(fo.pairs != 0, nx, ny, np);
-    const bool nob = pr && fo.nob && fo.nob[k];
     const long long sa = pr ? 2 : es, su = pr ? 2 : es;
     if (pr) {
       const int m = nx > ny ? nx : ny;
@@ -404,14 +402,12 @@ __global__ void __launch_bounds__(256) factor_kernel(
       gAy = gAx + 1;
       gUx = gAx + 2 * ainv_len(m, true);
       gUy = gUx + 1;
-      gB = nob ? nullptr : gUx + 2LL * np * m;
-      gS = gUx + (nob ? 2LL : 4LL) * np * m;
+      gB = gUx + 2LL * np * m;
+      gS = gB + 2LL * np * m;
       urx = ury = m;  // pair rows of U: [a * m + i]
       // zero padding of the smaller component
       if (nx != ny)
-        for (long long e = lane; e < (nob ? vanka_paired_doubles_nob(m, np)
-                                          : vanka_paired_doubles(m, np)) - (long long)np * np;
-             e += 32)
+        for (long long e = lane; e < vanka_paired_doubles(m, np) - (long long)np * np; e += 32)
           gAx[e] = 0.0;
       __syncwarp();
     } else if (fo.tps) {
@@ -494,9 +490,7 @@ __global__ void __launch_bounds__(256) factor_kernel(
       const int a = e / nv, j = e % nv;
       double acc = 0.0;
       for (int m = 0; m < np; ++m) acc = __dadd_rn(acc, __dmul_rn(Sinv[a * np + m], Um[j * NP + m]));
-      if (nob)
-        continue;  // formed in the apply
-      else if (pr)
+      if (pr)
         gB[2LL * a * (nx > ny ? nx : ny) + (j < nx ? 2 * j : 2 * (j - nx) + 1)] = acc;
       else
         gB[e * es] = acc;
@@ -515,7 +509,7 @@ __global__ void __launch_bounds__(256) factor_kernel(
       int* hdr = reinterpret_cast<int*>(fo.blob + fo.hoff[k]);
       hdr[0] = nx;
       hdr[1] = ny;
-      hdr[2] = np | (nob ? 1 << 17 : 0);
+      hdr[2] = np;
       hdr[3] = fo.sbase[k];
     }
     __syncwarp();
@@ -661,9 +655,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   auto ndbl = [&](int i) {
     const long long nv = f->h_nv[i], npp = f->h_np[i], x = f->h_nx[i], y = nv - x;
     if (!f->tpp && vanka_paired(f->pairs, (int)x, (int)y, (int)npp))
-      return !f->h_nob.empty() && f->h_nob[i]
-                 ? vanka_paired_doubles_nob((int)std::max(x, y), (int)npp)
-                 : vanka_paired_doubles((int)std::max(x, y), (int)npp);
+      return vanka_paired_doubles((int)std::max(x, y), (int)npp);
     return ainv_len(x, sym) + ainv_len(y, sym) + 2 * nv * npp + npp * npp;
   };
   f->h_dbase.assign(np_, 0);
@@ -746,8 +738,6 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     // paired patches go to the sub-warp kernel (several patches per warp)
     const bool subwarp = f->pairs && env_int("SAG_VANKA_SUBWARP", 1) != 0;
     f->seq = env_int("SAG_VANKA_SEQGATHER", 1) != 0;
-    f->h_nob.assign(np_, 0);
-    const bool nob_on = f->pairs && env_int("SAG_VANKA_NOB", 1) != 0;
     auto key_of = [&](int i) {
       const int x = f->h_nx[i], y = f->h_nv[i] - x;
       const int rows = std::max(x, y) + (f->pairs ? f->h_np[i] : 0);
@@ -773,7 +763,6 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     f->rclasses.clear();
     for (int q = 0; q < np_; ++q) {
       const int i = order[q];
-      f->h_nob[i] = nob_on && f->h_np[i] == 1 && r_of(i) % 4 == 0 ? 1 : 0;
       long long bytes = 16 + 8 * ndbl(i) + 4 * (f->h_nv[i] + f->h_np[i]) * (f->seq ? 2 : 1);
       bytes = (bytes + 15) / 16 * 16;
       h_hoff[i] = off[q];
@@ -859,7 +848,6 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     const int blocks = std::max(1, std::min((np_ + warps - 1) / warps, c.num_sms * 8));
     FactorOut fo;
     DevBuf<long long> dhoff;
-    DevBuf<unsigned char> dnob;
     fo.es = es;
     fo.dbase = ddbase.p;
     fo.ibase = dibase.p;
@@ -878,11 +866,6 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
                                  cudaMemcpyHostToDevice, c.stream));
       fo.hoff = dhoff.p;
       fo.pairs = f->pairs ? 1 : 0;
-      if (!f->h_nob.empty()) {
-        dnob.alloc(np_);
-        SAG_CUDA(cudaMemcpyAsync(dnob.p, f->h_nob.data(), np_, cudaMemcpyHostToDevice, c.stream));
-        fo.nob = dnob.p;
-      }
     }
     factor_kernel<<<blocks, warps * 32, smem, c.stream>>>(
         np_, L.D, L.NV, L.NP, L.bytes, sym ? 1 : 0, k.rp.p, k.ci.p, k.v.p, p.pptr.p, p.pidx.p,
@@ -931,7 +914,7 @@ __device__ __forceinline__ double2 lds_v2_pred(const double2* p, bool pred) {
 // pairs, U / Bh at the (U_x, U_y) / (B_x, B_y) pairs, Ay is unused.
 struct PatchView {
   int nx, ny, np, sbase, nv, m;
-  bool paired, nob;
+  bool paired;
   const double *Ax, *Ay, *U, *Bh, *Si;
   const int* idx;
   const int* pos;  // dof-ordered result positions (Vanka::seq), after idx
@@ -944,18 +927,16 @@ __device__ __forceinline__ PatchView patch_view(const unsigned char* B, bool pai
   const int4 hdr = *reinterpret_cast<const int4*>(B);
   v.nx = hdr.x;
   v.ny = hdr.y;
-  v.np = hdr.z & 0xffff;
+  v.np = hdr.z;
   v.sbase = hdr.w;
   v.nv = v.nx + v.ny;
   v.m = v.nx > v.ny ? v.nx : v.ny;
   v.paired = SYM && vanka_paired(pairs, v.nx, v.ny, v.np);
-  v.nob = v.paired && ((hdr.z >> 17) & 1);
   v.Ax = reinterpret_cast<const double*>(B + 16);
   if (v.paired) {
     v.Ay = v.Ax + 1;
     v.U = v.Ax + v.m * (v.m + 1);
-    // no b_hat pairs: the b_hat row reads the U pairs (scaled by S^-1 after)
-    v.Bh = v.nob ? v.U : v.U + 2 * v.np * v.m;
+    v.Bh = v.U + 2 * v.np * v.m;
     v.Si = v.Bh + 2 * v.np * v.m;
     v.idx = reinterpret_cast<const int*>(v.Si + v.np * v.np);
     v.pos = v.idx + v.nv + v.np;
@@ -1117,8 +1098,7 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
       for (int q = 0; q < R; ++q) {
         const int i = lane + 32 * q;
         const int ar = min(max(i - mm, 0), npp - 1);
-        // nob: the b_hat row summed u_j . b_j; b_hat b_u = S^-1 (u . b_u)
-        xl[q] = v.nob ? v.Si[0] * (tx[q] + ty[q]) : tx[q] + ty[q];
+        xl[q] = tx[q] + ty[q];
 #pragma unroll
         for (int e = 0; e < NPM; ++e)
           if (e < npp) xl[q] = fma(v.Si[ar * npp + e], sb[2 * mm + e], xl[q]);
@@ -1989,16 +1969,14 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
       ury = ny;
     } else if (vanka_paired(f.pairs, nx, ny, np)) {  // (A) | (U) | (B) pairs | S^-1
       const int m = std::max(nx, ny);
-      const bool nob = !f.h_nob.empty() && f.h_nob[k];
       const double* U2 = base + 2 * ainv_len(m, true);
       const double* B2 = U2 + 2LL * np * m;
-      const double* S2 = nob ? B2 : B2 + 2LL * np * m;
+      const double* S2 = B2 + 2LL * np * m;
       for (int i = 0; i < nv; ++i)
         for (int a = 0; a < np; ++a) {
           const long long e = 2LL * a * m + (i < nx ? 2 * i : 2 * (i - nx) + 1);
           if (uhat) uhat[ou + (size_t)i * np + a] = U2[e];
-          // nob (np = 1): b_hat = 0 + s_inv * u_hat, the reference's product
-          if (bhat) bhat[ou + (size_t)a * nv + i] = nob ? 0.0 + S2[0] * U2[e] : B2[e];
+          if (bhat) bhat[ou + (size_t)a * nv + i] = B2[e];
         }
       if (sinv)
         for (int e = 0; e < np * np; ++e) sinv[os + e] = S2[e];
