@@ -101,6 +101,9 @@ struct Ctx {
   // (created on first use, owned by the context)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t copy_ev = nullptr;
+  // streams that capture the bodies of conditional graph nodes (by depth)
+  cudaStream_t body_streams[4] = {nullptr, nullptr, nullptr, nullptr};
+  int body_depth = 0;
   cudaStream_t copy() {
     if (!copy_stream) {
       SAG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));

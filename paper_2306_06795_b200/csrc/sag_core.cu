@@ -1133,6 +1133,8 @@ int sag_destroy(sag_ctx* ctx) {
       cudaStreamDestroy(ctx->c.copy_stream);
       cudaEventDestroy(ctx->c.copy_ev);
     }
+    for (cudaStream_t bs : ctx->c.body_streams)
+      if (bs) cudaStreamDestroy(bs);
     if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
     delete ctx;
   });

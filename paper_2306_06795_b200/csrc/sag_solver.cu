@@ -235,6 +235,127 @@ static FgmresOut fgmres_dev(Ctx& c, const Matrix& A, const double* b, double* x,
   return out;
 }
 
+// ============================================ device-side convergence loop ==
+// fgmres_dev decides convergence on the host (one status read per Arnoldi
+// step). Inside a CUDA graph capture the same algorithm runs with conditional
+// nodes (CUDA 12.4+): a WHILE node over restart cycles (condition: not
+// converged and iterations < max_iters, krylov.cpp:42) whose body holds the
+// restart residual and `restart` IF nodes, one per Arnoldi step (condition:
+// not stopped and iterations < max_iters, krylov.cpp:58); the conditions are
+// set on the device from KState. Same operations, same order, no host sync.
+
+__global__ void cond_set_kernel(cudaGraphConditionalHandle h, const KState* st, int mode,
+                                int max_iters) {
+  const unsigned v = mode == 0 ? (!st->converged && st->iterations < max_iters)
+                               : (!st->stop && st->iterations < max_iters);
+  cudaGraphSetConditional(h, v);
+}
+
+// Adds a conditional node at the current point of c.stream's capture: set(h)
+// launches the kernel that sets its condition (before the node); body(h) is
+// captured into the node's body graph on a body stream (c.stream switched).
+template <class Set, class Body>
+static void cond_node(Ctx& c, cudaGraphConditionalNodeType type, Set set, Body body) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  SAG_CUDA(cudaStreamGetCaptureInfo(c.stream, &cs, nullptr, &g, &deps, &nd));
+  SAG_REQUIRE(cs == cudaStreamCaptureStatusActive, SAG_CUDA_ERROR,
+              "conditional node outside a stream capture");
+  cudaGraphConditionalHandle h;
+  SAG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 0, 0));
+  set(h);
+  SAG_CUDA(cudaStreamGetCaptureInfo(c.stream, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  SAG_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+  SAG_CUDA(cudaStreamUpdateCaptureDependencies(c.stream, &node, 1,
+                                               cudaStreamSetCaptureDependencies));
+  const int d = c.body_depth;
+  SAG_REQUIRE(d < 4, SAG_ERROR, "conditional nodes nested too deep");
+  if (!c.body_streams[d])
+    SAG_CUDA(cudaStreamCreateWithFlags(&c.body_streams[d], cudaStreamNonBlocking));
+  cudaStream_t outer = c.stream, bs = c.body_streams[d];
+  SAG_CUDA(cudaStreamBeginCaptureToGraph(bs, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+  c.stream = bs;
+  c.body_depth = d + 1;
+  cudaGraph_t done = nullptr;
+  try {
+    body(h);
+  } catch (...) {
+    c.stream = outer;
+    c.body_depth = d;
+    cudaStreamEndCapture(bs, &done);
+    throw;
+  }
+  c.stream = outer;
+  c.body_depth = d;
+  SAG_CUDA(cudaStreamEndCapture(bs, &done));
+}
+
+static bool stream_capturing(Ctx& c);
+
+// fgmres (krylov.cpp:17-121) as conditional graph nodes, for a caller that is
+// capturing c.stream; the result (x, KState) is the one fgmres_dev computes.
+static void fgmres_graph(Ctx& c, const Matrix& A, const double* b, double* x, const DevOp& prec,
+                         double tol, int max_iters, int restart, double bd, Krylov& K) {
+  const int n = A.nrows;
+  launch_kinit(c, K.st, restart, tol, bd, K.hist_cap, false);
+  {
+    Fin f;
+    f.kind = FIN_REF;
+    f.st = K.st;
+    launch_ssq(c, n, b, f);
+  }
+  {
+    SpmvArgs a;
+    a.b = b;
+    a.fin.kind = FIN_BETA;
+    a.fin.st = K.st;
+    a.fin.i = 2;
+    launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
+  }
+  auto set = [&](int mode) {
+    return [&, mode](cudaGraphConditionalHandle h) {
+      cond_set_kernel<<<1, 1, 0, c.stream>>>(h, K.st, mode, max_iters);
+      SAG_LAUNCHED(c);
+    };
+  };
+  cond_node(c, cudaGraphCondTypeWhile, set(0), [&](cudaGraphConditionalHandle hw) {
+    SpmvArgs a;  // restart from the true residual (krylov.cpp:43-53)
+    a.b = b;
+    a.fin.kind = FIN_BETA;
+    a.fin.st = K.st;
+    a.fin.i = 0;
+    launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
+    launch_div(c, n, K.r.p, K.beta(), K.v(0), K.stop());
+    for (int j = 0; j < restart; ++j) {
+      cond_node(c, cudaGraphCondTypeIf, set(1), [&](cudaGraphConditionalHandle) {
+        prec(K.v(j), K.z(j));
+        arnoldi_step(c, A, K, restart, j, K.stop());
+      });
+    }
+    launch_backsub(c, K.st);
+    launch_update(c, n, x, K.Z.p, (size_t)n, K.st, false);
+    cond_set_kernel<<<1, 1, 0, c.stream>>>(hw, K.st, 0, max_iters);
+    SAG_LAUNCHED(c);
+  });
+  {
+    SpmvArgs a;  // final true residual (krylov.cpp:116-119)
+    a.b = b;
+    a.fin.kind = FIN_FINAL;
+    a.fin.st = K.st;
+    a.fin.out = c.scal.p + 8;
+    launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
+  }
+}
+
 // ========================================================== coarse solve ==
 // MonolithicSolver coarse level (preconditioner.cpp:47-54, :60-63): dense LU
 // with partial pivoting of to_dense(K_L) (+ enclosed-flow pin), factorised on
@@ -463,7 +584,12 @@ struct SvTransfer {
   Krylov outer;                  // FGMRES(20) on Mcg
   DevBuf<double> rhs, pcg;
   std::vector<int> iterations;
+  DevBuf<int> fail;              // set when a graph-run projection did not converge
 };
+
+__global__ void proj_check_kernel(const KState* st, int* fail) {
+  if (!st->converged) *fail = 1;
+}
 
 // UzawaPreconditioner (preconditioner.hpp:118-141) on device.
 struct Uzawa {
@@ -623,6 +749,14 @@ static void sv_restrict(Ctx& c, Dc& d, const double* p_dg, double* p_cg) {
   launch_spmv(c, *t.mmix, p_dg, t.rhs.p, Epi::Store);
   launch_zero(c, t.mmix->nrows, p_cg);
   DevOp prec = [&](const double* in, double* out) { scalar_vcycle(c, t.sh, in, out); };
+  if (stream_capturing(c)) {
+    // inside the DC apply's CUDA graph: the device-side convergence loop; a
+    // failure is flagged on the device and raised at the next host check
+    fgmres_graph(c, *t.sh.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, 20, 1e-30, t.outer);
+    proj_check_kernel<<<1, 1, 0, c.stream>>>(t.outer.st, t.fail.p);
+    SAG_LAUNCHED(c);
+    return;
+  }
   FgmresOut o = fgmres_dev(c, *t.sh.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, 20, 1e-30, t.outer);
   if (!o.converged)
     throw Error(SAG_SOLVER_STAGNATION,
@@ -742,7 +876,9 @@ static bool stream_capturing(Ctx& c) {
 }
 
 static void dc_apply_graph(Ctx& c, Dc& d) {
-  const bool use_graph = !d.sv && !(getenv("SAG_NO_GRAPH") && atoi(getenv("SAG_NO_GRAPH"))) &&
+  // SV included: its mass projection runs as conditional graph nodes
+  const bool use_graph = !(getenv("SAG_NO_GRAPH") && atoi(getenv("SAG_NO_GRAPH"))) &&
+                         !(d.sv && getenv("SAG_SV_GRAPH") && !atoi(getenv("SAG_SV_GRAPH"))) &&
                          !stream_capturing(c);
   if (!use_graph) {
     dc_apply_dev(c, d, d.din.p, d.dout.p);
@@ -995,6 +1131,20 @@ void dc_setup(Ctx& c, Dc& d, const Matrix* k0, int n_x0, int n_y0, int n_p0, int
   }
   d.din.alloc(d.n0);
   d.dout.alloc(d.n0);
+}
+
+// A mass projection run inside the DC graph that missed its tolerance
+// (transfer.cpp:32-34) is flagged on the device; raised here at a host sync.
+void check_sv_projection(Ctx& c, Dc& d) {
+  if (!d.svt) return;
+  int f = 0;
+  SAG_CUDA(cudaMemcpyAsync(&f, d.svt->fail.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  if (f) {
+    SAG_CUDA(cudaMemsetAsync(d.svt->fail.p, 0, sizeof(int), c.stream));
+    throw Error(SAG_SOLVER_STAGNATION,
+                "SvPressureRestrict: mass projection did not reach tolerance in 200 iterations");
+  }
 }
 
 void require_ready(Dc& d) {
@@ -1264,7 +1414,10 @@ int sag_dc_set_sv_transfer(sag_dc* h, const sag_matrix* p_dup, const sag_matrix*
                 "sag_dc_set_sv_transfer: Mcg size mismatch");
     t->outer.init(n_p1, 20, 202);
     t->rhs.alloc(n_p1);
+    t->fail.alloc(1);
+    SAG_CUDA(cudaMemsetAsync(t->fail.p, 0, sizeof(int), c.stream));
     d.svt = std::move(t);
+    d.graph_ok = false;
   });
 }
 
@@ -1281,6 +1434,7 @@ int sag_dc_apply(sag_ctx* ctx, sag_dc* h, const double* r, double* z) {
     dc_apply_graph(c, d);
     launch_copy(c, d.n0, d.dout.p, zo.d);
     zo.finish();  // host output: copied back and synchronised; device: stream-ordered
+    if (d.sv && !stream_capturing(c)) check_sv_projection(c, d);
   });
 }
 
@@ -1344,6 +1498,7 @@ int sag_solve_stokes(sag_ctx* ctx, sag_dc* h, const double* rhs, double* x,
     solve_stokes_dev(c, *d.K0, d.n_x0 + d.n_y0, d.n_p0, d.din.p, d.dout.p,
                      [&] { dc_apply_graph(c, d); }, d.outer, *cfg, rhs, x, rep, history,
                      history_cap);
+    if (d.sv) check_sv_projection(c, d);
   });
 }
 
