@@ -1202,7 +1202,10 @@ int sag_matrix_create(sag_ctx* ctx, int nrows, int ncols, long long nnz, const i
 }
 
 int sag_matrix_destroy(sag_matrix* m) {
-  return guard([&] { delete m; });
+  return guard([&] {
+    if (m) cudaDeviceSynchronize();  // no kernel or graph still reads it
+    delete m;
+  });
 }
 
 int sag_matrix_shape(const sag_matrix* m, int* nrows, int* ncols, long long* nnz) {

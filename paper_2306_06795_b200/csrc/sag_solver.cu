@@ -163,6 +163,8 @@ using DevOp = std::function<void(const double* in, double* out)>;
 static FgmresOut fgmres_dev(Ctx& c, const Matrix& A, const double* b, double* x, const DevOp& prec,
                             double tol, int max_iters, int restart, double bd, Krylov& K) {
   const int n = A.nrows;
+  // reduction tickets start from zero (a fresh solve never inherits a count)
+  SAG_CUDA(cudaMemsetAsync(c.ticket.p, 0, sizeof(unsigned) * c.ticket.n, c.stream));
   SAG_REQUIRE(restart >= 1 && K.m >= restart && K.n == n, SAG_CONFIG_ERROR,
               "fgmres: workspace does not match restart / size");
   launch_kinit(c, K.st, restart, tol, bd, K.hist_cap, false);
@@ -1360,7 +1362,10 @@ int sag_dc_create(sag_ctx* ctx, const sag_matrix* k0, int n_x0, int n_y0, int n_
 }
 
 int sag_dc_destroy(sag_dc* d) {
-  return guard([&] { delete d; });
+  return guard([&] {
+    if (d) cudaDeviceSynchronize();  // its graph and buffers may still be in flight
+    delete d;
+  });
 }
 
 int sag_dc_set_coarse_pin(sag_ctx* ctx, sag_dc* h, double level0_norm_inf) {
@@ -1552,8 +1557,10 @@ int sag_uzawa_create(sag_ctx* ctx, const sag_matrix* b, int n_x, int n_y, int n_
 }
 
 int sag_uzawa_destroy(sag_uzawa* u) {
-  delete u;
-  return SAG_OK;
+  return guard([&] {
+    if (u) cudaDeviceSynchronize();  // its graph and buffers may still be in flight
+    delete u;
+  });
 }
 
 int sag_uzawa_apply(sag_ctx* ctx, sag_uzawa* h, const double* r, double* z) {

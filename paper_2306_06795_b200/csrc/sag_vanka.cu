@@ -2092,7 +2092,10 @@ int sag_factor_patches(sag_ctx* ctx, const sag_matrix* k, const sag_patches* p, 
 }
 
 int sag_vanka_destroy(sag_vanka* f) {
-  return guard([&] { delete f; });
+  return guard([&] {
+    if (f) cudaDeviceSynchronize();
+    delete f;
+  });
 }
 
 int sag_vanka_stats(const sag_vanka* f, long long* s) {
