@@ -349,6 +349,17 @@ int sag_axpby_async(sag_ctx* ctx, int n, double a, const double* x, double b, do
  * dst[idx[i]] += src[i] (add != 0); idx entries unique. */
 int sag_gather_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* dst);
 int sag_scatter_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* dst, int add);
+/* Peer memory for a partitioned sweep: a rank exports a device buffer
+ * (64-byte CUDA IPC handle) and its neighbours map it, so the reverse halo of
+ * the Vanka sweep is written straight into the owner's receive buffer over
+ * NVLink (sag_gather_async with the peer pointer as destination) instead of
+ * a send / receive pair. */
+int sag_ipc_get_handle(sag_ctx* ctx, void* dptr, unsigned char* handle);
+int sag_ipc_open_handle(sag_ctx* ctx, const unsigned char* handle, void** dptr);
+int sag_ipc_close_handle(sag_ctx* ctx, void* dptr);
+/* peer_dst[i] = src[idx[i]] into a mapped neighbour buffer (NVLink stores,
+ * system-scope fence): the reverse halo's send half. */
+int sag_push_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* peer_dst);
 /* norm_inf (sparse.cpp:229-237): max absolute row sum (host out). */
 int sag_matrix_norm_inf(sag_ctx* ctx, const sag_matrix* m, double* out);
 /* Refactors the coarse dense LU with the enclosed-flow pin

@@ -197,6 +197,10 @@ SIGNATURES = {
     "sag_gather_async": (C.c_int, [vp, C.c_int, vp, vp, vp]),
     "sag_scatter_async": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int]),
     "sag_matrix_norm_inf": (C.c_int, [vp, vp, f64p]),
+    "sag_ipc_get_handle": (C.c_int, [vp, vp, vp]),
+    "sag_ipc_open_handle": (C.c_int, [vp, vp, C.POINTER(vp)]),
+    "sag_ipc_close_handle": (C.c_int, [vp, vp]),
+    "sag_push_async": (C.c_int, [vp, C.c_int, vp, vp, vp]),
     "sag_dc_set_coarse_pin": (C.c_int, [vp, vp, C.c_double]),
 }
 

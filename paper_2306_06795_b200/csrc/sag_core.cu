@@ -1055,6 +1055,15 @@ __global__ void gather_idx_kernel(int n, const int* __restrict__ idx, const doub
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     dst[i] = src[idx[i]];
 }
+// reverse halo over peer memory: dst (a neighbour's buffer, mapped by CUDA
+// IPC) receives src[idx[i]] by NVLink stores; the system-scope fence orders
+// them before the kernel's completion is observed by the neighbour
+__global__ void push_idx_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
+                                double* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+  __threadfence_system();
+}
 __global__ void scatter_idx_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
                                    double* __restrict__ dst, int add) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -1380,6 +1389,17 @@ int sag_gather_async(sag_ctx* ctx, int n, const int* idx, const double* src, dou
   });
 }
 
+int sag_push_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* peer_dst) {
+  return guard([&] {
+    NOTNULL(ctx);
+    require_dev({idx, src, peer_dst});
+    if (n <= 0) return;
+    auto& c = ctx->c;
+    sag::push_idx_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, idx, src, peer_dst);
+    SAG_LAUNCHED(c);
+  });
+}
+
 int sag_scatter_async(sag_ctx* ctx, int n, const int* idx, const double* src, double* dst, int add) {
   return guard([&] {
     NOTNULL(ctx);
@@ -1388,6 +1408,38 @@ int sag_scatter_async(sag_ctx* ctx, int n, const int* idx, const double* src, do
     auto& c = ctx->c;
     sag::scatter_idx_kernel<<<sag::ew_grid(c, n), 256, 0, c.stream>>>(n, idx, src, dst, add);
     SAG_LAUNCHED(c);
+  });
+}
+
+int sag_ipc_get_handle(sag_ctx* ctx, void* dptr, unsigned char* handle) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(dptr);
+    NOTNULL(handle);
+    cudaIpcMemHandle_t h;
+    SAG_CUDA(cudaIpcGetMemHandle(&h, dptr));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+int sag_ipc_open_handle(sag_ctx* ctx, const unsigned char* handle, void** dptr) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(handle);
+    NOTNULL(dptr);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    SAG_CUDA(cudaSetDevice(ctx->c.device));
+    SAG_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int sag_ipc_close_handle(sag_ctx* ctx, void* dptr) {
+  return guard([&] {
+    NOTNULL(ctx);
+    NOTNULL(dptr);
+    SAG_CUDA(cudaIpcCloseMemHandle(dptr));
   });
 }
 

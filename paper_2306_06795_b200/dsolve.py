@@ -60,6 +60,25 @@ class Comm:
             t.copy_(h)
         return t
 
+    def all_gather_object(self, obj):
+        if self.size == 1:
+            return [obj]
+        out = [None] * self.size
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def fence(self, flag):
+        """Every rank's preceding work on its stream is complete before any
+        rank's following work: NCCL -- an all-reduce of one element, ordered
+        on the device; gloo -- stream synchronisation and a barrier."""
+        if self.size == 1:
+            return
+        if self.stage:
+            self.torch.cuda.current_stream().synchronize()
+            self.dist.barrier()
+        else:
+            self.dist.all_reduce(flag)
+
     def start(self, sends: dict, recvs: dict):
         """Posts a grouped point-to-point exchange (sends: q -> tensor to send;
         recvs: q -> tensor to receive into). With NCCL the transfers run on
@@ -200,6 +219,21 @@ class LibsagBackend:
         self._check(self.L.sag_scatter_async(self.ctx.h, idx.numel(), self.p(idx), self.p(src),
                                              self.p(dst), int(add)))
 
+    def ipc_handle(self, t):
+        h = (self.C.c_ubyte * 64)()
+        self._check(self.L.sag_ipc_get_handle(self.ctx.h, self.p(t), h))
+        return bytes(h)
+
+    def ipc_open(self, handle: bytes) -> int:
+        h = (self.C.c_ubyte * 64).from_buffer_copy(handle)
+        ptr = self.C.c_void_p()
+        self._check(self.L.sag_ipc_open_handle(self.ctx.h, h, self.C.byref(ptr)))
+        return ptr.value
+
+    def push(self, idx, src, peer_ptr: int):
+        self._check(self.L.sag_push_async(self.ctx.h, idx.numel(), self.p(idx), self.p(src),
+                                          self.C.c_void_p(peer_ptr)))
+
     def launches(self):
         return self.ctx.launch_count()
 
@@ -247,6 +281,35 @@ class _Krylov:
         self.r = be.vec(n)
 
 
+class PeerHalo:
+    """The reverse halo over peer memory (the sweep's only collective): each
+    rank maps, by CUDA IPC, the receive buffers its neighbours keep for it and
+    writes its partial sums at their dofs straight into them (NVLink stores,
+    `sag_push_async`); one fence (Comm.fence) orders every rank's stores before
+    the owners add them, in rank order. Two buffer sets alternate, so a rank's
+    next stores never overwrite sums its neighbour has not added yet (a forward
+    halo and a fence separate them)."""
+
+    def __init__(self, rs, be, comm):
+        self.be, self.comm = be, comm
+        self.recv = [{q: be.vec(len(i)) for q, i in rs.rev_recv.items()} for _ in range(2)]
+        mine = {q: [be.ipc_handle(self.recv[k][q]) for k in range(2)] for q in rs.rev_recv}
+        allh = comm.all_gather_object(mine)
+        self.dst = {q: [be.ipc_open(allh[q][rs.rank][k]) for k in range(2)] for q in rs.rev_send}
+        self.flag = be.vec(1)
+        self.k = 0
+
+    def start(self, d, ix_send):
+        for q, idx in ix_send.items():
+            self.be.push(idx, d, self.dst[q][self.k])
+        self.comm.fence(self.flag)
+
+    def finish(self, d, ix_recv):
+        for q in sorted(ix_recv):
+            self.be.scatter(ix_recv[q], self.recv[self.k][q], d, True)
+        self.k ^= 1
+
+
 class DistStep:
     """The partitioned hot step on one rank: the halos, the masked reductions
     and the distributed K0 (local SpMV rows + own Vanka patches).
@@ -254,7 +317,9 @@ class DistStep:
     step(x, delta, y): delta = apply_vanka(x) (vanka.cpp:151-184) and y = K0 x
     (sparse.cpp:78-91) on the rank's owned dofs -- the bench's unit of work."""
 
-    def __init__(self, rs, be, comm, mrelax=1):
+    def __init__(self, rs, be, comm, mrelax=1, peer=None):
+        """peer: reverse halo over peer memory (PeerHalo; default from
+        SAG_P2P_HALO=1) instead of NCCL send / receive."""
         self.rs, self.be, self.comm = rs, be, comm
         nl = rs.nl
         self.mask = be.u8(rs.owned)
@@ -265,6 +330,9 @@ class DistStep:
         self._buf = {k: {q: be.vec(len(i)) for q, i in getattr(rs, k).items()}
                      for k in ("fwd_send", "fwd_recv", "rev_send", "rev_recv")}
         self.k0 = _Level(be, rs, rs.levels["K0"], mrelax)
+        if peer is None:
+            peer = os.environ.get("SAG_P2P_HALO") == "1"
+        self.peer = PeerHalo(rs, be, comm) if peer and comm.size > 1 else None
 
     def step(self, x, delta, y):
         """delta = apply_vanka(x), y = K0 x: interior patches and rows under
@@ -297,12 +365,18 @@ class DistStep:
     def reduce_start(self, d):
         """Reverse halo, posted: partial sums at ghosts to their owners."""
         be, ix, buf = self.be, self._ix, self._buf
+        if self.peer is not None:
+            self.peer.start(d, ix["rev_send"])
+            return "peer"
         for q, i in ix["rev_send"].items():
             be.gather(i, d, buf["rev_send"][q])
         return self.comm.start(buf["rev_send"], buf["rev_recv"])
 
     def reduce_finish(self, h, d):
         """... added by the owner in rank order."""
+        if h == "peer":
+            self.peer.finish(d, self._ix["rev_recv"])
+            return
         self.comm.finish(h)
         for q in sorted(self._ix["rev_recv"]):
             self.be.scatter(self._ix["rev_recv"][q], self._buf["rev_recv"][q], d, True)
@@ -360,11 +434,11 @@ class DistSolver(DistStep):
     hierarchy [(K, P, nxyz), ...] (host CSR) -- level 0 is distributed
     through rs, levels 1.. are agglomerated; cfg: SolverConfig."""
 
-    def __init__(self, rs, levels, cfg, be, comm):
+    def __init__(self, rs, levels, cfg, be, comm, peer=None):
         if cfg.variant not in (0, 1, 2):
             raise ValueError("DistSolver: DC-all / DC-LO / DC-HO only")
         mrelax = max(cfg.nu1, cfg.nu2, 1)
-        super().__init__(rs, be, comm, mrelax)
+        super().__init__(rs, be, comm, mrelax, peer)
         self.cfg = cfg
         nl = rs.nl
         self.l0 = _Level(be, rs, rs.levels["L0"], mrelax)

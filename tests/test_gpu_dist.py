@@ -8,8 +8,10 @@ final relative residual <= tol, same solution.
   over gloo staged through host memory -- the ranks' kernels never wait on
   one another (every exchange is a host-synchronised copy), so this is the
   multi-rank host logic (halos, masked reductions, all-reduces, agglomerated
-  coarse levels) driving the real device kernels. NCCL across GPUs is the
-  bench's --gpus N path."""
+  coarse levels) driving the real device kernels; with "gloo-peer" the
+  reverse halo of every sweep goes over peer memory (each rank writes its
+  partial sums into the neighbour's buffer mapped by CUDA IPC). NCCL across
+  GPUs is the bench's --gpus N path."""
 import os
 import socket
 
@@ -44,6 +46,7 @@ def _worker(rank, world, port, n, backend, q):
     os.environ["MASTER_PORT"] = str(port)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
+    peer = backend == "gloo-peer"   # reverse halo over peer memory (CUDA IPC)
     if backend == "nccl":
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     else:
@@ -58,7 +61,9 @@ def _worker(rank, world, port, n, backend, q):
         ctx = S.Context(0, stream=stream.cuda_stream)
         with torch.cuda.stream(stream):
             be = LibsagBackend(ctx, dev, torch, stream)
-            solver = DistSolver(rs, levels, cfg, be, Comm(dist, torch, stage=backend == "gloo"))
+            solver = DistSolver(rs, levels, cfg, be, Comm(dist, torch, stage=backend != "nccl"),
+                                peer=peer)
+            assert (solver.peer is not None) == peer
             rhs = be.from_host(g["rhs"][rs.l2g])
             x = be.vec(rs.nl)
             l0n = ctx.launch_count()
@@ -68,6 +73,9 @@ def _worker(rank, world, port, n, backend, q):
         own = np.nonzero(rs.owned)[0]
         # the preconditioner runs as a CUDA graph whenever the communicator allows
         assert (solver.graph is not None) == (backend == "nccl"), solver.graph_error
+        if peer:
+            torch.cuda.synchronize(dev)
+            dist.barrier()  # no rank unmaps before its neighbour's last stores
         q.put((rank, rs.l2g[own], x.cpu().numpy()[own], rep.iterations,
                rep.final_relative_residual, rep.converged, launches))
     finally:
@@ -92,7 +100,8 @@ def _run(world, n, backend):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,n,backend", [(1, 32, "nccl"), (1, 64, "nccl"),
-                                             (2, 32, "gloo"), (2, 64, "gloo")])
+                                             (2, 32, "gloo"), (2, 64, "gloo"),
+                                             (2, 32, "gloo-peer"), (2, 64, "gloo-peer")])
 def test_gpu_distributed_solve_matches_reference(world, n, backend):
     from test_dist_solve import reference_system
     g = reference_system(n)[0]
