@@ -219,6 +219,12 @@ class LibsagBackend:
         self._check(self.L.sag_scatter_async(self.ctx.h, idx.numel(), self.p(idx), self.p(src),
                                              self.p(dst), int(add)))
 
+    def raw(self, n):
+        """A device buffer of its own allocation (cudaMalloc via sag_alloc): a
+        CUDA IPC handle maps the whole allocation, so buffers shared with peer
+        ranks must not be sub-allocated by torch's caching allocator."""
+        return _RawBuffer(self, n)
+
     def ipc_handle(self, t):
         h = (self.C.c_ubyte * 64)()
         self._check(self.L.sag_ipc_get_handle(self.ctx.h, self.p(t), h))
@@ -281,6 +287,29 @@ class _Krylov:
         self.r = be.vec(n)
 
 
+class _RawBuffer:
+    """n doubles of device memory owned by libsag (numel / data_ptr like a tensor)."""
+
+    def __init__(self, be, n):
+        self.be, self.n = be, n
+        ptr = be.C.c_void_p()
+        be._check(be.L.sag_alloc(be.ctx.h, max(n, 1) * 8, be.C.byref(ptr)))
+        be._check(be.L.sag_memcpy(be.ctx.h, ptr, (be.C.c_double * max(n, 1))(), max(n, 1) * 8))
+        self.ptr = ptr.value
+
+    def numel(self):
+        return self.n
+
+    def data_ptr(self):
+        return self.ptr
+
+    def __del__(self):
+        try:
+            self.be.L.sag_free(self.be.ctx.h, self.be.C.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
 class PeerHalo:
     """The reverse halo over peer memory (the sweep's only collective): each
     rank maps, by CUDA IPC, the receive buffers its neighbours keep for it and
@@ -292,7 +321,7 @@ class PeerHalo:
 
     def __init__(self, rs, be, comm):
         self.be, self.comm = be, comm
-        self.recv = [{q: be.vec(len(i)) for q, i in rs.rev_recv.items()} for _ in range(2)]
+        self.recv = [{q: be.raw(len(i)) for q, i in rs.rev_recv.items()} for _ in range(2)]
         mine = {q: [be.ipc_handle(self.recv[k][q]) for k in range(2)] for q in rs.rev_recv}
         allh = comm.all_gather_object(mine)
         self.dst = {q: [be.ipc_open(allh[q][rs.rank][k]) for k in range(2)] for q in rs.rev_send}
@@ -308,6 +337,13 @@ class PeerHalo:
         for q in sorted(ix_recv):
             self.be.scatter(ix_recv[q], self.recv[self.k][q], d, True)
         self.k ^= 1
+
+    def close(self):
+        """Unmaps the neighbours' buffers (call after a fence: no stores in flight)."""
+        for ptrs in self.dst.values():
+            for p in ptrs:
+                self.be.L.sag_ipc_close_handle(self.be.ctx.h, self.be.C.c_void_p(p))
+        self.dst = {}
 
 
 class DistStep:
