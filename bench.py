@@ -501,8 +501,9 @@ def run_ours(args, ws, rank, local):
     y = torch.empty(n, dtype=torch.float64, device=dev)
     lib = S.lib()
 
-    def step():  # sag_vanka_spmv: the sweep and the SpMV overlap (two streams)
-        S.vanka_spmv_step(f, K0, x, delta, y)
+    def step():
+        S.apply_vanka(f, x, out=delta)
+        S.spmv(K0, x, out=y)
 
     def timed(fn, k):
         e0 = torch.cuda.Event(enable_timing=True)

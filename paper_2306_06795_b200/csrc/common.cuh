@@ -100,7 +100,7 @@ struct Ctx {
   // second stream for device->host copies that overlap compute on `stream`
   // (created on first use, owned by the context)
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t copy_ev = nullptr, join_ev = nullptr;
+  cudaEvent_t copy_ev = nullptr;
   // streams that capture the bodies of conditional graph nodes (by depth)
   cudaStream_t body_streams[4] = {nullptr, nullptr, nullptr, nullptr};
   int body_depth = 0;
@@ -108,7 +108,6 @@ struct Ctx {
     if (!copy_stream) {
       SAG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
       SAG_CUDA(cudaEventCreateWithFlags(&copy_ev, cudaEventDisableTiming));
-      SAG_CUDA(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
     }
     return copy_stream;
   }

@@ -1141,7 +1141,6 @@ int sag_destroy(sag_ctx* ctx) {
       cudaStreamSynchronize(ctx->c.copy_stream);
       cudaStreamDestroy(ctx->c.copy_stream);
       cudaEventDestroy(ctx->c.copy_ev);
-      cudaEventDestroy(ctx->c.join_ev);
     }
     for (cudaStream_t bs : ctx->c.body_streams)
       if (bs) cudaStreamDestroy(bs);

@@ -2172,21 +2172,6 @@ int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const 
     InVec xi(c, x, n, 0);                 // x crosses the host link once
     OutVec yo(c, y, n, 2, false);
     OutVec d(c, delta, n, 1, false);
-    if (!yo.host && !d.host && xi.d == x &&
-        !(getenv("SAG_STEP_CONCURRENT") && !atoi(getenv("SAG_STEP_CONCURRENT")))) {
-      // device buffers: the two independent products overlap -- the SpMV on
-      // a second stream fills the SMs the Vanka sweep's tail leaves idle
-      cudaStream_t side = c.copy(), main = c.stream;
-      SAG_CUDA(cudaEventRecord(c.copy_ev, main));
-      SAG_CUDA(cudaStreamWaitEvent(side, c.copy_ev, 0));
-      vanka_apply(c, f->f, xi.d, d.d);
-      c.stream = side;
-      launch_spmv(c, k->m, xi.d, yo.d, Epi::Store);
-      c.stream = main;
-      SAG_CUDA(cudaEventRecord(c.join_ev, side));
-      SAG_CUDA(cudaStreamWaitEvent(main, c.join_ev, 0));
-      return;
-    }
     launch_spmv(c, k->m, xi.d, yo.d, Epi::Store);
     if (yo.host) {
       // y's device->host copy runs on the copy stream under the Vanka sweep
