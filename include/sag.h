@@ -136,6 +136,16 @@ int sag_apply_vanka(sag_ctx* ctx, const sag_vanka* f, const double* r, double* d
 int sag_apply_vanka_add(sag_ctx* ctx, const sag_vanka* f, const double* r, double* x,
                         double omega);
 
+/* sag_apply_vanka_add fused with the reverse halo of a partitioned sweep:
+ * where slot[d] >= 0 (a ghost dof of this rank), the updated x_d -- this
+ * rank's complete partial sum there -- is also stored into
+ * peers[nbr[d]][slot[d]], a neighbour's receive buffer mapped by
+ * sag_ipc_open_handle (NVLink stores, system-scope fence). Device pointers;
+ * at most 8 neighbours; dof-ordered result layout (default). */
+int sag_apply_vanka_add_push(sag_ctx* ctx, const sag_vanka* f, const double* r, double* x,
+                             double omega, const int* slot, const unsigned char* nbr, int npeer,
+                             double* const* peers);
+
 /* The hot step as one call: y = K x (spmv, sparse.cpp:78-91) and delta =
  * apply_vanka(x) (vanka.cpp:151-184) on the same input. With host buffers x
  * crosses the host link once and y's copy back overlaps the Vanka sweep (a

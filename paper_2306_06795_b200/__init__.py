@@ -153,6 +153,8 @@ SIGNATURES = {
     "sag_apply_vanka_stage": (C.c_int, [vp, vp, vp, vp, C.c_int]),
     "sag_vanka_spmv": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "sag_apply_vanka_add": (C.c_int, [vp, vp, vp, vp, C.c_double]),
+    "sag_apply_vanka_add_push": (C.c_int, [vp, vp, vp, vp, C.c_double, vp, vp, C.c_int,
+                                           C.POINTER(vp)]),
     "sag_vanka_set_weights": (C.c_int, [vp, vp, vp]),
     "sag_vanka_relax": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_double]),
     "sag_fgmres": (C.c_int, [vp, vp, vp, vp, C.c_int, vp, C.POINTER(sag_fgmres_options),

@@ -1478,6 +1478,41 @@ __global__ void vanka_gather_seq_kernel(int n, const int* __restrict__ dof_ptr,
   }
 }
 
+// The gather of the boundary patches of a partitioned sweep fused with the
+// reverse halo: x_d += omega * delta_d as vanka_gather_seq_kernel, and where
+// d is a ghost dof its value -- this rank's complete partial sum at d -- is
+// also stored into the owner's receive buffer (peer[nbr[d]][slot[d]], mapped
+// by CUDA IPC: NVLink stores), ended by a system-scope fence.
+struct PeerMap {
+  double* peer[8];
+};
+__global__ void vanka_gather_push_kernel(int n, const int* __restrict__ dof_ptr,
+                                         const double* __restrict__ out,
+                                         const double* __restrict__ w, double* __restrict__ x,
+                                         double omega, const int* __restrict__ slot,
+                                         const unsigned char* __restrict__ nbr, PeerMap pm) {
+  constexpr int U = 8;
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const double xo = x[d];
+    const int s0 = __ldg(dof_ptr + d), s1 = __ldg(dof_ptr + d + 1);
+    const double wd = w ? __ldg(w + d) : (s1 > s0 ? 1.0 / (double)(s1 - s0) : 0.0);
+    double acc = 0.0;
+    for (int sb = s0; sb < s1; sb += U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = sb + u < s1 ? __ldcs(out + sb + u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (sb + u < s1) acc = __dadd_rn(acc, __dmul_rn(wd, v[u]));
+    }
+    const double val = xo + omega * acc;
+    x[d] = val;
+    const int sl = __ldg(slot + d);
+    if (sl >= 0) pm.peer[__ldg(nbr + d)][sl] = val;
+  }
+  __threadfence_system();
+}
+
 static void launch_gather(Ctx& c, const Vanka& f, double* delta, double* xadd, double omega,
                           const int* gate) {
   const double* w = f.w_ext ? f.w.p : nullptr;
@@ -2156,6 +2191,29 @@ int sag_apply_vanka_add(sag_ctx* ctx, const sag_vanka* f, const double* r, doubl
     OutVec xo(c, x, f->f.n, 1, true);
     vanka_apply_stationary(c, f->f, ri.d, xo.d, omega);
     xo.finish();
+  });
+}
+
+int sag_apply_vanka_add_push(sag_ctx* ctx, const sag_vanka* f, const double* r, double* x,
+                             double omega, const int* slot, const unsigned char* nbr, int npeer,
+                             double* const* peers) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    SAG_REQUIRE(npeer >= 0 && npeer <= 8 && (npeer == 0 || peers), SAG_INVALID_ARGUMENT,
+                "sag_apply_vanka_add_push: 0..8 peer buffers");
+    SAG_REQUIRE(f->f.seq, SAG_CONFIG_ERROR,
+                "sag_apply_vanka_add_push needs the dof-ordered result layout");
+    auto& c = ctx->c;
+    for (const void* p : {(const void*)r, (const void*)x, (const void*)slot, (const void*)nbr})
+      SAG_REQUIRE(is_device_ptr(p), SAG_INVALID_ARGUMENT, "device pointers only");
+    PeerMap pm{};
+    for (int i = 0; i < npeer; ++i) pm.peer[i] = peers[i];
+    launch_patch_any(c, f->f, r, nullptr);
+    const double* w = f->f.w_ext ? f->f.w.p : nullptr;
+    vanka_gather_push_kernel<<<grid_for(c, f->f.n), 256, 0, c.stream>>>(
+        f->f.n, f->f.dof_ptr.p, f->f.out.p, w, x, omega, slot, nbr, pm);
+    SAG_LAUNCHED(c);
   });
 }
 

@@ -236,6 +236,12 @@ class LibsagBackend:
         self._check(self.L.sag_ipc_open_handle(self.ctx.h, h, self.C.byref(ptr)))
         return ptr.value
 
+    def vanka_add_push(self, f, r, x, slot, nbr, peers):
+        arr = (self.C.c_void_p * max(len(peers), 1))(*peers)
+        self._check(self.L.sag_apply_vanka_add_push(self.ctx.h, f.h, self.p(r), self.p(x),
+                                                    self.C.c_double(1.0), self.p(slot),
+                                                    self.p(nbr), len(peers), arr))
+
     def push(self, idx, src, peer_ptr: int):
         self._check(self.L.sag_push_async(self.ctx.h, idx.numel(), self.p(idx), self.p(src),
                                           self.C.c_void_p(peer_ptr)))
@@ -327,6 +333,23 @@ class PeerHalo:
         self.dst = {q: [be.ipc_open(allh[q][rs.rank][k]) for k in range(2)] for q in rs.rev_send}
         self.flag = be.vec(1)
         self.k = 0
+        # per local dof: where its partial sum goes (neighbour index, slot), for
+        # the gather that stores straight into the owners' buffers
+        self.order = sorted(rs.rev_send)
+        slot = np.full(rs.nl, -1, dtype=np.int32)
+        nbr = np.zeros(rs.nl, dtype=np.uint8)
+        for qi, q in enumerate(self.order):
+            slot[rs.rev_send[q]] = np.arange(len(rs.rev_send[q]), dtype=np.int32)
+            nbr[rs.rev_send[q]] = qi
+        self.fusable = len(self.order) <= 8
+        self.slot, self.nbr = be.ivec(slot), be.u8(nbr)
+
+    def add_push(self, f_bnd, v, z):
+        """z += apply_vanka(v) over the boundary patches, each ghost's partial
+        sum stored into its owner's buffer by the same kernel; then the fence."""
+        self.be.vanka_add_push(f_bnd, v, z, self.slot, self.nbr,
+                               [self.dst[q][self.k] for q in self.order])
+        self.comm.fence(self.flag)
 
     def start(self, d, ix_send):
         for q, idx in ix_send.items():
@@ -378,12 +401,22 @@ class DistStep:
         self._vanka_int(L, x, delta)
         be.spmv(L.K_int, x, y)
         self.halo_finish(h, x)
-        if L.f_bnd is not None:
-            be.vanka_add(L.f_bnd, x, delta)
-        h = self.reduce_start(delta)
+        h = self._bnd_reduce_start(L, x, delta)
         if L.K_bnd is not None:
             be.spmv(L.K_bnd, x, y, "add")
         self.reduce_finish(h, delta)
+
+    def _bnd_reduce_start(self, L, v, z):
+        """z += the boundary patches' contributions, then the reverse halo
+        posted; over peer memory the boundary gather itself stores the ghosts'
+        partial sums into their owners' buffers (compute + collective in one
+        kernel)."""
+        if self.peer is not None and L.f_bnd is not None and self.peer.fusable:
+            self.peer.add_push(L.f_bnd, v, z)
+            return "peer"
+        if L.f_bnd is not None:
+            self.be.vanka_add(L.f_bnd, v, z)
+        return self.reduce_start(z)
 
     # ---- communication ------------------------------------------------
     def halo_start(self, x):
@@ -456,9 +489,7 @@ class DistStep:
         h = self.halo_start(v)
         self._vanka_int(L, v, z)
         self.halo_finish(h, v)
-        if L.f_bnd is not None:
-            self.be.vanka_add(L.f_bnd, v, z)
-        h = self.reduce_start(z)
+        h = self._bnd_reduce_start(L, v, z)
         self.reduce_finish(h, z)
 
 
