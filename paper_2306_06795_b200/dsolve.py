@@ -343,6 +343,7 @@ class PeerHalo:
             nbr[rs.rev_send[q]] = qi
         self.fusable = len(self.order) <= 8
         self.slot, self.nbr = be.ivec(slot), be.u8(nbr)
+        self.fused = self.unfused = 0   # reverse halos done each way
 
     def add_push(self, f_bnd, v, z):
         """z += apply_vanka(v) over the boundary patches, each ghost's partial
@@ -350,11 +351,13 @@ class PeerHalo:
         self.be.vanka_add_push(f_bnd, v, z, self.slot, self.nbr,
                                [self.dst[q][self.k] for q in self.order])
         self.comm.fence(self.flag)
+        self.fused += 1
 
     def start(self, d, ix_send):
         for q, idx in ix_send.items():
             self.be.push(idx, d, self.dst[q][self.k])
         self.comm.fence(self.flag)
+        self.unfused += 1
 
     def finish(self, d, ix_recv):
         for q in sorted(ix_recv):

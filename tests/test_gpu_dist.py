@@ -74,6 +74,8 @@ def _worker(rank, world, port, n, backend, q):
         # the preconditioner runs as a CUDA graph whenever the communicator allows
         assert (solver.graph is not None) == (backend == "nccl"), solver.graph_error
         if peer:
+            # the boundary gathers stored the halo themselves (fused path)
+            assert solver.peer.fused > 0
             torch.cuda.synchronize(dev)
             dist.barrier()  # no rank unmaps before its neighbour's last stores
         q.put((rank, rs.l2g[own], x.cpu().numpy()[own], rep.iterations,
