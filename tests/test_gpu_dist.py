@@ -74,8 +74,9 @@ def _worker(rank, world, port, n, backend, q):
         # the preconditioner runs as a CUDA graph whenever the communicator allows
         assert (solver.graph is not None) == (backend == "nccl"), solver.graph_error
         if peer:
-            # the boundary gathers stored the halo themselves (fused path)
-            assert solver.peer.fused > 0
+            # a rank with ghost partial sums sent them from its boundary gathers
+            # (fused path; the lowest rank owns every dof its patches touch)
+            assert solver.peer.fused > 0 or not rs.rev_send
             torch.cuda.synchronize(dev)
             dist.barrier()  # no rank unmaps before its neighbour's last stores
         q.put((rank, rs.l2g[own], x.cpu().numpy()[own], rep.iterations,
