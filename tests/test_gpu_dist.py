@@ -104,7 +104,8 @@ def _run(world, n, backend):
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,n,backend", [(1, 32, "nccl"), (1, 64, "nccl"),
                                              (2, 32, "gloo"), (2, 64, "gloo"),
-                                             (2, 32, "gloo-peer"), (2, 64, "gloo-peer")])
+                                             (2, 32, "gloo-peer"), (2, 64, "gloo-peer"),
+                                             (4, 32, "gloo"), (4, 32, "gloo-peer")])
 def test_gpu_distributed_solve_matches_reference(world, n, backend):
     from test_dist_solve import reference_system
     g = reference_system(n)[0]
