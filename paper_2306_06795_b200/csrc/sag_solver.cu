@@ -306,8 +306,10 @@ static bool stream_capturing(Ctx& c);
 // fgmres (krylov.cpp:17-121) as conditional graph nodes, for a caller that is
 // capturing c.stream; the result (x, KState) is the one fgmres_dev computes.
 static void fgmres_graph(Ctx& c, const Matrix& A, const double* b, double* x, const DevOp& prec,
-                         double tol, int max_iters, int restart, double bd, Krylov& K) {
+                         double tol, int max_iters, int restart, double bd, Krylov& K,
+                         double* final_out) {
   const int n = A.nrows;
+  SAG_CUDA(cudaMemsetAsync(c.ticket.p, 0, sizeof(unsigned) * c.ticket.n, c.stream));
   launch_kinit(c, K.st, restart, tol, bd, K.hist_cap, false);
   {
     Fin f;
@@ -353,7 +355,7 @@ static void fgmres_graph(Ctx& c, const Matrix& A, const double* b, double* x, co
     a.b = b;
     a.fin.kind = FIN_FINAL;
     a.fin.st = K.st;
-    a.fin.out = c.scal.p + 8;
+    a.fin.out = final_out;
     launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
   }
 }
@@ -555,6 +557,21 @@ struct Coarse {
 
 // ==================================================== monolithic solver ==
 
+// A whole solve_stokes (FGMRES with its preconditioner) as one CUDA graph:
+// the convergence loop as conditional nodes (fgmres_graph), every
+// preconditioner application inline. Re-captured when the buffers or
+// settings it was captured with change.
+struct SolveGraph {
+  cudaGraphExec_t exec = nullptr;
+  const void* key[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int restart = 0, max_iters = 0, enclosed = 0;
+  double tol = 0.0;
+  long long apply_fine = 0, apply_l1 = 0;  // relaxation units per application
+  ~SolveGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
 struct Level {
   const Matrix* K = nullptr;
   const Matrix* P = nullptr;
@@ -607,6 +624,7 @@ struct Uzawa {
   cudaGraphExec_t graph = nullptr;
   bool graph_ok = false;
   long long graph_launches = 0;
+  SolveGraph solve_graph;
   ~Uzawa() {
     if (graph) cudaGraphExecDestroy(graph);
   }
@@ -634,6 +652,7 @@ struct Dc {
   cudaGraphExec_t graph = nullptr;
   bool graph_ok = false;
   long long graph_launches = 0;
+  SolveGraph solve_graph;
   ~Dc() {
     if (graph) cudaGraphExecDestroy(graph);
   }
@@ -754,7 +773,8 @@ static void sv_restrict(Ctx& c, Dc& d, const double* p_dg, double* p_cg) {
   if (stream_capturing(c)) {
     // inside the DC apply's CUDA graph: the device-side convergence loop; a
     // failure is flagged on the device and raised at the next host check
-    fgmres_graph(c, *t.sh.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, 20, 1e-30, t.outer);
+    fgmres_graph(c, *t.sh.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, 20, 1e-30, t.outer,
+                 c.scal.p + 8);
     proj_check_kernel<<<1, 1, 0, c.stream>>>(t.outer.st, t.fail.p);
     SAG_LAUNCHED(c);
     return;
@@ -1160,7 +1180,9 @@ void require_ready(Dc& d) {
 template <class Run>
 void solve_stokes_dev(Ctx& c, const Matrix& K0, int n_u, int n_p, double* din, double* dout,
                       Run run, Krylov& outer, const sag_solver_config& cfg, const double* rhs,
-                      double* x, sag_krylov_report* rep, double* history, int history_cap) {
+                      double* x, sag_krylov_report* rep, double* history, int history_cap,
+                      SolveGraph* sg = nullptr, long long* units_fine = nullptr,
+                      long long* units_l1 = nullptr) {
   const int n = K0.nrows;
   InVec bi(c, rhs, n, 0);
   OutVec xo(c, x, n, 1, false);
@@ -1194,8 +1216,63 @@ void solve_stokes_dev(Ctx& c, const Matrix& K0, int n_u, int n_p, double* din, d
       launch_copy(c, n, dout, z);
     }
   };
-  FgmresOut o = fgmres_dev(c, K0, bi.d, xo.d, prec, cfg.tol, cfg.max_iters, cfg.restart, 1e-30,
-                           outer);
+  const bool whole = sg && !(getenv("SAG_SOLVE_GRAPH") && !atoi(getenv("SAG_SOLVE_GRAPH")));
+  FgmresOut o;
+  if (whole) {
+    // the whole solve as one CUDA graph: no host synchronisation per Arnoldi step
+    const void* key[6] = {bi.d, xo.d, &K0, din, dout, outer.st};
+    const bool same = sg->exec && std::equal(key, key + 6, sg->key) &&
+                      sg->restart == cfg.restart && sg->max_iters == cfg.max_iters &&
+                      sg->tol == cfg.tol && sg->enclosed == cfg.enclosed_flow;
+    if (!same) {
+      const long long f0 = units_fine ? *units_fine : 0, l0 = units_l1 ? *units_l1 : 0;
+      const long long la = c.launches;
+      cudaGraph_t g;
+      SAG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        launch_zero(c, n, xo.d);
+        fgmres_graph(c, K0, bi.d, xo.d, prec, cfg.tol, cfg.max_iters, cfg.restart, 1e-30, outer,
+                     c.scal.p);
+      } catch (...) {
+        cudaStreamEndCapture(c.stream, &g);
+        throw;
+      }
+      SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
+      if (sg->exec) cudaGraphExecDestroy(sg->exec);
+      sg->exec = nullptr;
+      SAG_CUDA(cudaGraphInstantiate(&sg->exec, g, 0));
+      cudaGraphDestroy(g);
+      std::copy(key, key + 6, sg->key);
+      sg->restart = cfg.restart;
+      sg->max_iters = cfg.max_iters;
+      sg->tol = cfg.tol;
+      sg->enclosed = cfg.enclosed_flow;
+      // one application per Arnoldi step was captured `restart` times
+      sg->apply_fine = units_fine ? (*units_fine - f0) / std::max(cfg.restart, 1) : 0;
+      sg->apply_l1 = units_l1 ? (*units_l1 - l0) / std::max(cfg.restart, 1) : 0;
+      if (units_fine) *units_fine = f0;
+      if (units_l1) *units_l1 = l0;
+      c.launches = la;
+    }
+    SAG_CUDA(cudaGraphLaunch(sg->exec, c.stream));
+    const KHeader hd = read_header(c, outer.st);
+    o.iterations = hd.iterations;
+    o.converged = hd.converged;
+    SAG_CUDA(cudaMemcpyAsync(&o.final_rel, c.scal.p, sizeof(double), cudaMemcpyDeviceToHost,
+                             c.stream));
+    const int hl = std::min(hd.hist_len, outer.hist_cap);
+    o.hist.resize(hl);
+    if (hl)
+      SAG_CUDA(cudaMemcpyAsync(o.hist.data(),
+                               ks_h(outer.st) + (size_t)(cfg.restart + 1) * cfg.restart +
+                                   cfg.restart + cfg.restart + (cfg.restart + 1) + cfg.restart,
+                               sizeof(double) * hl, cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    if (units_fine) *units_fine += sg->apply_fine * o.iterations;
+    if (units_l1) *units_l1 += sg->apply_l1 * o.iterations;
+  } else {
+    o = fgmres_dev(c, K0, bi.d, xo.d, prec, cfg.tol, cfg.max_iters, cfg.restart, 1e-30, outer);
+  }
   xo.finish();
   if (rep) {
     rep->converged = o.converged;
@@ -1502,7 +1579,7 @@ int sag_solve_stokes(sag_ctx* ctx, sag_dc* h, const double* rhs, double* x,
     require_ready(d);
     solve_stokes_dev(c, *d.K0, d.n_x0 + d.n_y0, d.n_p0, d.din.p, d.dout.p,
                      [&] { dc_apply_graph(c, d); }, d.outer, *cfg, rhs, x, rep, history,
-                     history_cap);
+                     history_cap, &d.solve_graph, &d.fine_units, &d.l1_units);
     if (d.sv) check_sv_projection(c, d);
   });
 }
@@ -1594,7 +1671,7 @@ int sag_solve_stokes_uzawa(sag_ctx* ctx, const sag_matrix* k0, sag_uzawa* h, con
     SAG_REQUIRE(k0->m.nrows == n_u + u.n_p && k0->m.ncols == k0->m.nrows, SAG_DIMENSION_MISMATCH,
                 "solve_stokes: K0 does not match the preconditioner size");
     solve_stokes_dev(c, k0->m, n_u, u.n_p, u.din.p, u.dout.p, [&] { uzawa_apply_graph(c, u); },
-                     h->outer, *cfg, rhs, x, rep, history, history_cap);
+                     h->outer, *cfg, rhs, x, rep, history, history_cap, &u.solve_graph);
   });
 }
 
