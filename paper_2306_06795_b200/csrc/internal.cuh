@@ -224,6 +224,34 @@ void launch_update(Ctx& c, int n, double* x, const double* Z, size_t zstride, KS
 void launch_mul(Ctx& c, int n, const double* a, const double* b, double* y);
 // dinv_i = 1 / a_ii; returns false (via *bad) if a diagonal entry is missing/zero
 void launch_inv_diag(Ctx& c, const Matrix& m, double* dinv, int* bad);
+
+// The small levels of a scalar V(2,2) cycle (amg.cpp:258-296) in ONE launch:
+// a thread-block cluster whose CTAs split each level's rows, with cluster
+// barriers between the phases and the Krylov scalars of every
+// Jacobi-FGMRES(2) smoother computed redundantly (identically) in each CTA
+// from DSMEM-gathered partial sums. Replaces ~30 dependent small launches per
+// level; levels run from L[0] (b given, x out) down to the coarse L[nlev-1].
+constexpr int kTailMaxLev = 6;
+struct TailLevel {
+  int n = 0;
+  const int *arp = nullptr, *aci = nullptr;
+  const double* av = nullptr;           // A_l
+  const int *rrp = nullptr, *rci = nullptr;
+  const double* rv = nullptr;           // R_l = P_l^T (not on the coarse level)
+  const int *prp = nullptr, *pci = nullptr;
+  const double* pv = nullptr;           // P_l
+  const double* dinv = nullptr;
+  double *b = nullptr, *x = nullptr, *r = nullptr, *rs = nullptr, *w = nullptr;
+  double *v0 = nullptr, *v1 = nullptr, *z0 = nullptr, *z1 = nullptr;
+};
+struct TailParams {
+  int nlev = 0;                 // the last level is the coarse one (dense inverse)
+  TailLevel L[kTailMaxLev];
+  const double* cinv = nullptr; // n x n row-major inverse of the coarse level
+};
+// 0 when no cluster of the tail kernel can be resident (then the tail is not used)
+int scalar_tail_cluster(Ctx& c);
+void launch_scalar_tail(Ctx& c, const TailParams& p);
 // KState (re)initialisation for a new solve: ref/tol/bd/m/iterations
 void launch_kinit(Ctx& c, KState* st, int m, double tol, double bd, int hist_cap,
                   bool keep_ref);

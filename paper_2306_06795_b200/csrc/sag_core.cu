@@ -8,6 +8,7 @@
 //   norm_inf        sparse.cpp:229-237
 //   transpose       sparse.cpp:93-111  (rows of P^T in ascending order)
 //   FGMRES scalars  krylov.cpp:42-110  (finishers below)
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -18,6 +19,8 @@
 #include "tma.cuh"
 
 namespace sag {
+
+namespace cg = cooperative_groups;
 
 // ------------------------------------------------------------ finishers --
 
@@ -1070,6 +1073,384 @@ __global__ void scatter_idx_kernel(int n, const int* __restrict__ idx, const dou
     const int d = idx[i];
     dst[d] = add ? dst[d] + src[i] : src[i];
   }
+}
+
+// ------------------------------------------------- scalar V-cycle tail --
+// One cluster runs the small levels of scalar_vcycle (amg.cpp:258-296). CTA q
+// of the cluster owns rows [n q / CS, n (q+1) / CS) of every level; vectors
+// live in global memory (L2-resident at these sizes) and are read with
+// L2-only loads after the cluster barrier that published them. A reduction is
+// a fixed-order block sum, a cluster barrier, and a fixed-order sum of the CS
+// block partials read over DSMEM -- the same total in every CTA, so the
+// Krylov scalars (KState in shared memory, updated by apply_fin exactly as
+// the multi-launch path does) and every branch on them agree cluster-wide.
+
+
+// cluster barrier with release/acquire at cluster scope: publishes the
+// global-memory vector writes of the phase to the other CTAs
+__device__ __forceinline__ void cluster_bar() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+constexpr int kTailThreads = 1024;
+constexpr int kTailWarps = kTailThreads / 32;
+
+struct TailSh {
+  double part[2][4];            // this CTA's partials (two alternating slots)
+  double wp[kTailWarps][4];
+  double tot[4];
+  double ks[32];                // KState for m = 2, no history (kstate_bytes(2, 0) <= 256)
+};
+
+template <int K>
+__device__ __forceinline__ void tail_reduce(cg::cluster_group& cl, TailSh& s, int& slot,
+                                            double (&v)[K]) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double t = warp_sum(v[k]);
+    if (lane == 0) s.wp[wid][k] = t;
+  }
+  __syncthreads();
+  if (wid < K) {
+    const double t = warp_sum(s.wp[lane][wid]);
+    if (lane == 0) s.part[slot][wid] = t;
+  }
+  cluster_bar();
+  if (wid < K) {
+    double t = 0.0;
+    if (lane < (int)cl.num_blocks()) t = *cl.map_shared_rank(&s.part[slot][wid], lane);
+    t = warp_sum(t);
+    if (lane == 0) s.tot[wid] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = s.tot[k];
+  slot ^= 1;
+}
+
+// rows [r0, r1) of y = A x, 4 lanes per row, four strides per pass with all
+// value/column loads issued before the x gathers (two dependent L2 round
+// trips per pass); epi(row, sum) on the lead lane
+template <class F>
+__device__ __forceinline__ void tail_spmv(const int* __restrict__ rp, const int* __restrict__ ci,
+                                          const double* __restrict__ v, const double* x, int r0,
+                                          int r1, F epi) {
+  const int lane = threadIdx.x & 31, sub = lane & 3, grp = lane >> 2, wid = threadIdx.x >> 5;
+  for (int base = r0 + wid * 8; base < r1; base += kTailWarps * 8) {
+    const int row = base + grp;
+    double s = 0.0;
+    if (row < r1) {
+      const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
+      for (int k0 = beg + sub; k0 < end; k0 += 16) {
+        double vv[4], xv[4];
+        int cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + 4 * u;
+          vv[u] = k < end ? __ldg(v + k) : 0.0;
+          cc[u] = k < end ? __ldg(ci + k) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = cc[u] >= 0 ? __ldcg(x + cc[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s = fma(vv[u], xv[u], s);
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (sub == 0 && row < r1) epi(row, s);
+  }
+}
+
+__device__ __forceinline__ void tail_rows(int n, int q, int cs, int& r0, int& r1) {
+  r0 = (int)((long long)n * q / cs);
+  r1 = (int)((long long)n * (q + 1) / cs);
+}
+
+__device__ __forceinline__ void tail_fin(TailSh& s, Fin f, double tot) {
+  if (threadIdx.x == 0) {
+    f.st = reinterpret_cast<KState*>(s.ks);
+    apply_fin(f, tot);
+  }
+  __syncthreads();
+}
+
+// fgmres(A, b, x, jacobi, {tol 0, max 2, restart 2}) (amg.cpp:265-276,
+// krylov.cpp:17-121) on level L, x in/out (x_zero: x is known to be zero)
+__device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const TailLevel& L,
+                            bool x_zero) {
+  const int q = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  int r0, r1;
+  tail_rows(L.n, q, cs, r0, r1);
+  const int t0 = r0 + threadIdx.x;
+  KState* st = reinterpret_cast<KState*>(s.ks);
+  // ref = ||b|| and the (re)start residual r = b - A x, beta = ||r||
+  {
+    double red[2] = {0.0, 0.0};
+    for (int i = t0; i < r1; i += kTailThreads) {
+      const double bi = __ldcg(L.b + i);
+      red[0] = fma(bi, bi, red[0]);
+    }
+    if (x_zero) {
+      red[1] = red[0];
+    } else {
+      const double* b = L.b;
+      double* rs = L.rs;
+      double acc = 0.0;
+      tail_spmv(L.arp, L.aci, L.av, L.x, r0, r1, [&](int row, double sum) {
+        const double ri = __ldcg(b + row) - sum;
+        rs[row] = ri;
+        acc = fma(ri, ri, acc);
+      });
+      red[1] = acc;
+    }
+    tail_reduce<2>(cl, s, slot, red);
+    Fin f;
+    f.kind = FIN_REF;
+    tail_fin(s, f, red[0]);
+    f.kind = FIN_BETA;
+    f.i = 4;
+    f.j = 2;
+    f.tol = 0.0;
+    tail_fin(s, f, red[1]);
+  }
+  const double* r = x_zero ? L.b : L.rs;
+  if (!st->stop) {
+    const double beta = st->beta;
+    for (int i = t0; i < r1; i += kTailThreads) {
+      const double vi = __ldcg(r + i) / beta;
+      L.v0[i] = vi;
+      L.z0[i] = __ldg(L.dinv + i) * vi;
+    }
+    cluster_bar();
+    // Arnoldi step 0: w = A z0, h00 = (w, v0); w -= h00 v0, ||w||
+    {
+      double red[1] = {0.0};
+      double* w = L.w;
+      const double* v0 = L.v0;
+      tail_spmv(L.arp, L.aci, L.av, L.z0, r0, r1, [&](int row, double sum) {
+        w[row] = sum;
+        red[0] = fma(sum, __ldcg(v0 + row), red[0]);
+      });
+      tail_reduce<1>(cl, s, slot, red);
+      Fin f;
+      f.kind = FIN_H;
+      f.i = 0;
+      f.j = 0;
+      tail_fin(s, f, red[0]);
+    }
+    {
+      const double h = ks_h(st)[0];
+      double red[1] = {0.0};
+      for (int i = t0; i < r1; i += kTailThreads) {
+        const double wi = fma(-h, __ldcg(L.v0 + i), __ldcg(L.w + i));
+        L.w[i] = wi;
+        red[0] = fma(wi, wi, red[0]);
+      }
+      tail_reduce<1>(cl, s, slot, red);
+      Fin f;
+      f.kind = FIN_ARNOLDI;
+      f.j = 0;
+      tail_fin(s, f, red[0]);
+    }
+    if (!st->stop) {
+      const double wn = st->wnorm;
+      for (int i = t0; i < r1; i += kTailThreads) {
+        const double vi = __ldcg(L.w + i) / wn;
+        L.v1[i] = vi;
+        L.z1[i] = __ldg(L.dinv + i) * vi;
+      }
+      cluster_bar();
+      // Arnoldi step 1: w = A z1, h01 = (w, v0); w -= h01 v0, h11 = (w, v1);
+      // w -= h11 v1, ||w|| (v2 is never used by the update, so not formed)
+      {
+        double red[1] = {0.0};
+        double* w = L.w;
+        const double* v0 = L.v0;
+        tail_spmv(L.arp, L.aci, L.av, L.z1, r0, r1, [&](int row, double sum) {
+          w[row] = sum;
+          red[0] = fma(sum, __ldcg(v0 + row), red[0]);
+        });
+        tail_reduce<1>(cl, s, slot, red);
+        Fin f;
+        f.kind = FIN_H;
+        f.i = 0;
+        f.j = 1;
+        tail_fin(s, f, red[0]);
+      }
+      {
+        const double h = ks_h(st)[1];
+        double red[1] = {0.0};
+        for (int i = t0; i < r1; i += kTailThreads) {
+          const double wi = fma(-h, __ldcg(L.v0 + i), __ldcg(L.w + i));
+          L.w[i] = wi;
+          red[0] = fma(wi, __ldcg(L.v1 + i), red[0]);
+        }
+        tail_reduce<1>(cl, s, slot, red);
+        Fin f;
+        f.kind = FIN_H;
+        f.i = 1;
+        f.j = 1;
+        tail_fin(s, f, red[0]);
+      }
+      {
+        const double h = ks_h(st)[3];
+        double red[1] = {0.0};
+        for (int i = t0; i < r1; i += kTailThreads) {
+          const double wi = fma(-h, __ldcg(L.v1 + i), __ldcg(L.w + i));
+          L.w[i] = wi;
+          red[0] = fma(wi, wi, red[0]);
+        }
+        tail_reduce<1>(cl, s, slot, red);
+        Fin f;
+        f.kind = FIN_ARNOLDI;
+        f.j = 1;
+        tail_fin(s, f, red[0]);
+      }
+    }
+  }
+  // back-substitution (krylov.cpp:102-107) and x (+)= y_0 z_0 + y_1 z_1
+  if (threadIdx.x == 0) {
+    const int j = st->jeff, m = st->m;
+    const double* h = ks_h(st);
+    const double* g = ks_g(st);
+    double* y = ks_y(st);
+    for (int i = j - 1; i >= 0; --i) {
+      double sum = g[i];
+      for (int k = i + 1; k < j; ++k) sum -= h[i * m + k] * y[k];
+      y[i] = sum / h[i * m + i];
+    }
+  }
+  __syncthreads();
+  const int j = st->jeff;
+  if (j > 0 || x_zero) {
+    const double* y = ks_y(st);
+    for (int i = t0; i < r1; i += kTailThreads) {
+      double corr = 0.0;
+      if (j > 0) corr = fma(y[0], __ldcg(L.z0 + i), corr);
+      if (j > 1) corr = fma(y[1], __ldcg(L.z1 + i), corr);
+      L.x[i] = x_zero ? corr : __ldcg(L.x + i) + corr;
+    }
+  }
+  cluster_bar();
+}
+
+__global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams p) {
+  __shared__ TailSh s;
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  int slot = 0;
+  const int nl = p.nlev;
+  // down: pre-smoothing from zero, r = b - A x, b_(l+1) = R r
+  for (int l = 0; l + 1 < nl; ++l) {
+    const TailLevel& L = p.L[l];
+    tail_smooth(cl, s, slot, L, true);
+    int r0, r1;
+    tail_rows(L.n, q, cs, r0, r1);
+    {
+      const double* b = L.b;
+      double* r = L.r;
+      tail_spmv(L.arp, L.aci, L.av, L.x, r0, r1,
+                [&](int row, double sum) { r[row] = __ldcg(b + row) - sum; });
+    }
+    cluster_bar();
+    const TailLevel& C = p.L[l + 1];
+    tail_rows(C.n, q, cs, r0, r1);
+    {
+      double* bc = C.b;
+      tail_spmv(L.rrp, L.rci, L.rv, L.r, r0, r1, [&](int row, double sum) { bc[row] = sum; });
+    }
+    cluster_bar();
+  }
+  // coarse: x = K^-1 b (dense inverse), one warp per row
+  {
+    const TailLevel& C = p.L[nl - 1];
+    int r0, r1;
+    tail_rows(C.n, q, cs, r0, r1);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int row = r0 + wid; row < r1; row += kTailWarps) {
+      const double* a = p.cinv + (size_t)row * C.n;
+      double sum = 0.0;
+      for (int j0 = lane; j0 < C.n; j0 += 128) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + 32 * u;
+          av[u] = j < C.n ? __ldg(a + j) : 0.0;
+          bv[u] = j < C.n ? __ldcg(C.b + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sum = fma(av[u], bv[u], sum);
+      }
+      sum = warp_sum(sum);
+      if (lane == 0) C.x[row] = sum;
+    }
+    cluster_bar();
+  }
+  // up: x_l += P x_(l+1), post-smoothing
+  for (int l = nl - 2; l >= 0; --l) {
+    const TailLevel& L = p.L[l];
+    const TailLevel& C = p.L[l + 1];
+    int r0, r1;
+    tail_rows(L.n, q, cs, r0, r1);
+    {
+      double* x = L.x;
+      tail_spmv(L.prp, L.pci, L.pv, C.x, r0, r1,
+                [&](int row, double sum) { x[row] = __ldcg(x + row) + sum; });
+    }
+    cluster_bar();
+    tail_smooth(cl, s, slot, L, false);
+  }
+}
+
+static int g_tail_cluster = -1;
+int scalar_tail_cluster(Ctx& c) {
+  if (g_tail_cluster >= 0) return g_tail_cluster;
+  int best = 0;
+  if (cudaFuncSetAttribute(scalar_tail_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+      cudaSuccess)
+    cudaGetLastError();
+  for (int cs : {16, 8, 4}) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kTailThreads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, scalar_tail_kernel, &cfg) == cudaSuccess && nc > 0) {
+      best = cs;
+      break;
+    }
+    cudaGetLastError();
+  }
+  (void)c;
+  g_tail_cluster = best;
+  return best;
+}
+
+void launch_scalar_tail(Ctx& c, const TailParams& p) {
+  const int cs = scalar_tail_cluster(c);
+  SAG_REQUIRE(cs > 0 && p.nlev >= 1 && p.nlev <= kTailMaxLev, SAG_ERROR,
+              "scalar V-cycle tail: no resident cluster / bad level count");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(kTailThreads);
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  SAG_CUDA(cudaLaunchKernelEx(&cfg, scalar_tail_kernel, p));
+  SAG_LAUNCHED(c);
 }
 
 }  // namespace sag

@@ -593,6 +593,8 @@ struct ScalarH {
   std::vector<DevBuf<double>> dinv, sb, sx, sr;
   std::vector<Krylov> kr;        // Jacobi-FGMRES(2) smoothing workspaces
   Coarse coarse;
+  int tail_from = -1;            // levels >= tail_from run as one cluster launch
+  TailParams tail;
   int n() const { return A.empty() ? 0 : A[0]->nrows; }
 };
 
@@ -740,6 +742,13 @@ static void scalar_level(Ctx& c, ScalarH& t, int l, const double* b, double* x) 
   const int nl = (int)t.A.size();
   if (l == nl - 1) {
     t.coarse.solve(c, b, x);
+    return;
+  }
+  if (l == t.tail_from) {
+    TailParams p = t.tail;
+    p.L[0].b = const_cast<double*>(b);
+    p.L[0].x = x;
+    launch_scalar_tail(c, p);
     return;
   }
   const Matrix& A = *t.A[l];
@@ -1009,6 +1018,8 @@ static void uzawa_apply_graph(Ctx& c, Uzawa& u) {
   c.launches += u.graph_launches;
 }
 
+constexpr int kTailRows = 65536;  // largest level the cluster tail takes
+
 static void scalar_setup(Ctx& c, ScalarH& t, int nl, const sag_matrix* const* a,
                          const sag_matrix* const* p, const char* what) {
   SAG_REQUIRE(nl >= 1, SAG_DIMENSION_MISMATCH, std::string(what) + ": empty scalar hierarchy");
@@ -1048,6 +1059,44 @@ static void scalar_setup(Ctx& c, ScalarH& t, int nl, const sag_matrix* const* a,
     }
   }
   t.coarse.setup(c, *t.A.back(), -1, 0.0);
+  // the small levels as one cluster launch (SAG_SCALAR_TAIL=0: per-kernel path)
+  const char* e = getenv("SAG_SCALAR_TAIL");
+  if ((e && std::strcmp(e, "0") == 0) || !t.coarse.use_inv || scalar_tail_cluster(c) == 0) return;
+  const char* er = getenv("SAG_TAIL_ROWS");
+  const int rows_max = er ? atoi(er) : kTailRows;
+  int from = nl - 1;
+  while (from > 0 && t.A[from - 1]->nrows <= rows_max && nl - (from - 1) <= kTailMaxLev) --from;
+  if (nl - from < 2) return;
+  t.tail_from = from;
+  t.tail.nlev = nl - from;
+  t.tail.cinv = t.coarse.inv.p;
+  for (int l = from; l < nl; ++l) {
+    TailLevel& L = t.tail.L[l - from];
+    const Matrix& A = *t.A[l];
+    L.n = A.nrows;
+    L.arp = A.rp.p;
+    L.aci = A.ci.p;
+    L.av = A.v.p;
+    L.b = t.sb[l].p;
+    L.x = t.sx[l].p;
+    if (l + 1 < nl) {
+      L.rrp = t.R[l]->rp.p;
+      L.rci = t.R[l]->ci.p;
+      L.rv = t.R[l]->v.p;
+      L.prp = t.P[l]->rp.p;
+      L.pci = t.P[l]->ci.p;
+      L.pv = t.P[l]->v.p;
+      L.dinv = t.dinv[l].p;
+      L.r = t.sr[l].p;
+      Krylov& K = t.kr[l];
+      L.rs = K.r.p;
+      L.w = K.w.p;
+      L.v0 = K.v(0);
+      L.v1 = K.v(1);
+      L.z0 = K.z(0);
+      L.z1 = K.z(1);
+    }
+  }
 }
 
 }  // namespace sag

@@ -413,3 +413,24 @@ def test_vanka_thread_per_patch_layout(S, monkeypatch):
     want = rv.factors()
     for key in ("uhat", "bhat", "sinv", "weights"):
         assert np.array_equal(got[key], want[key]), key
+
+
+@pytest.mark.parametrize("tail", ["0", "1", "rows"])
+def test_sv_scalar_tail(S, monkeypatch, tail):
+    # the mass projection's scalar V(2,2) cycles with their small levels as one
+    # cluster launch (all levels; from level 1 with SAG_TAIL_ROWS) against the
+    # per-kernel path and the reference
+    conf = dict(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500, enclosed_flow=True,
+                omega0=0.78, eta_u=1.0, eta_p=2.68)
+    c, d, k0, levels, _ = ref_case(64, sv=True, cfg=conf)
+    monkeypatch.setenv("SAG_SCALAR_TAIL", "0" if tail == "0" else "1")
+    if tail == "rows":
+        monkeypatch.setenv("SAG_TAIL_ROWS", "1000")
+    h, K0, dc, cfg = _host_device(S, dict(problem="cavity", sv=True, n=64), conf)
+    r = O.splitmix64_uniform(c.n0)
+    z = dc.apply(r)
+    assert rel_inf(z, d.apply(r)) <= 1e-8
+    assert np.array_equal(z, dc.apply(r))          # deterministic
+    x, rep = S.solve_stokes(K0, c.rhs(), dc, cfg)
+    assert rep.converged and rep.final_relative_residual <= cfg.tol
+    assert abs(rep.iterations - d.solve(c.rhs())[1]["iterations"]) <= 1
