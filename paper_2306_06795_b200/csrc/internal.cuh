@@ -226,31 +226,36 @@ void launch_mul(Ctx& c, int n, const double* a, const double* b, double* y);
 void launch_inv_diag(Ctx& c, const Matrix& m, double* dinv, int* bad);
 
 // The small levels of a scalar V(2,2) cycle (amg.cpp:258-296) in ONE launch:
-// a thread-block cluster whose CTAs split each level's rows, with cluster
-// barriers between the phases and the Krylov scalars of every
-// Jacobi-FGMRES(2) smoother computed redundantly (identically) in each CTA
-// from DSMEM-gathered partial sums. Replaces ~30 dependent small launches per
-// level; levels run from L[0] (b given, x out) down to the coarse L[nlev-1].
+// a thread-block cluster whose CTAs own contiguous row chunks of every level.
+// All level vectors live in the CTAs' shared memory (SpMV gathers read the
+// other CTAs' chunks over DSMEM), cluster barriers separate the phases, and
+// the Krylov scalars of every Jacobi-FGMRES(2) smoother are computed
+// redundantly (identically) in each CTA from DSMEM-gathered partial sums.
+// Replaces ~30 dependent small launches per level; levels run from L[0]
+// (b0 given, x0 out, global memory) down to the coarse L[nlev-1].
 constexpr int kTailMaxLev = 6;
+constexpr int kTailVecs = 9;  // b x r rs w v0 v1 z0 z1 per level
 struct TailLevel {
-  int n = 0;
+  int n = 0, chunk = 0, off = 0;  // rows, rows per CTA, shared-memory offset (doubles)
   const int *arp = nullptr, *aci = nullptr;
-  const double* av = nullptr;           // A_l
+  const double* av = nullptr;     // A_l
   const int *rrp = nullptr, *rci = nullptr;
-  const double* rv = nullptr;           // R_l = P_l^T (not on the coarse level)
+  const double* rv = nullptr;     // R_l = P_l^T (not on the coarse level)
   const int *prp = nullptr, *pci = nullptr;
-  const double* pv = nullptr;           // P_l
+  const double* pv = nullptr;     // P_l
   const double* dinv = nullptr;
-  double *b = nullptr, *x = nullptr, *r = nullptr, *rs = nullptr, *w = nullptr;
-  double *v0 = nullptr, *v1 = nullptr, *z0 = nullptr, *z1 = nullptr;
 };
 struct TailParams {
-  int nlev = 0;                 // the last level is the coarse one (dense inverse)
+  int nlev = 0, cs = 0;           // levels (the last is the coarse one), CTAs per cluster
+  size_t smem = 0;                // dynamic shared memory per CTA
   TailLevel L[kTailMaxLev];
-  const double* cinv = nullptr; // n x n row-major inverse of the coarse level
+  const double* cinv = nullptr;   // n x n row-major inverse of the coarse level
+  const double* b0 = nullptr;     // per launch: right-hand side of L[0]
+  double* x0 = nullptr;           // per launch: result on L[0]
 };
-// 0 when no cluster of the tail kernel can be resident (then the tail is not used)
-int scalar_tail_cluster(Ctx& c);
+// cluster size, row chunks and shared-memory layout for p.L[0..nlev) (n set);
+// false when no resident cluster can hold the levels
+bool scalar_tail_plan(Ctx& c, TailParams& p);
 void launch_scalar_tail(Ctx& c, const TailParams& p);
 // KState (re)initialisation for a new solve: ref/tol/bd/m/iterations
 void launch_kinit(Ctx& c, KState* st, int m, double tol, double bd, int hist_cap,

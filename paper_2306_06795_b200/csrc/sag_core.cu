@@ -1077,30 +1077,59 @@ __global__ void scatter_idx_kernel(int n, const int* __restrict__ idx, const dou
 
 // ------------------------------------------------- scalar V-cycle tail --
 // One cluster runs the small levels of scalar_vcycle (amg.cpp:258-296). CTA q
-// of the cluster owns rows [n q / CS, n (q+1) / CS) of every level; vectors
-// live in global memory (L2-resident at these sizes) and are read with
-// L2-only loads after the cluster barrier that published them. A reduction is
-// a fixed-order block sum, a cluster barrier, and a fixed-order sum of the CS
-// block partials read over DSMEM -- the same total in every CTA, so the
-// Krylov scalars (KState in shared memory, updated by apply_fin exactly as
-// the multi-launch path does) and every branch on them agree cluster-wide.
-
-
-// cluster barrier with release/acquire at cluster scope: publishes the
-// global-memory vector writes of the phase to the other CTAs
-__device__ __forceinline__ void cluster_bar() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
+// of the cluster owns rows [q chunk, (q+1) chunk) of every level and keeps
+// that chunk of each level vector in its shared memory; SpMV gathers of other
+// rows are DSMEM loads from the owning CTA. A reduction is a fixed-order
+// block sum, a cluster barrier, and a fixed-order sum of the CS block
+// partials read over DSMEM -- the same total in every CTA, so the Krylov
+// scalars (KState in shared memory, updated by apply_fin exactly as the
+// multi-launch path does) and every branch on them agree cluster-wide.
+// Measured (tools/cluster_phase_probe.cu): a barrier phase with one
+// dependent L2 load + store costs ~1.2 us, ~0.3 us with shared memory only.
 
 constexpr int kTailThreads = 1024;
 constexpr int kTailWarps = kTailThreads / 32;
+constexpr int kTailMaxCs = 16;
+enum { TB = 0, TX, TR, TRS, TW, TV0, TV1, TZ0, TZ1 };
+
+// cluster barrier with release/acquire at cluster scope
+__device__ __forceinline__ void cluster_bar() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 struct TailSh {
   double part[2][4];            // this CTA's partials (two alternating slots)
   double wp[kTailWarps][4];
   double tot[4];
   double ks[32];                // KState for m = 2, no history (kstate_bytes(2, 0) <= 256)
+  double* base[kTailMaxCs];     // generic address of each CTA's dynamic shared memory
 };
+
+// a level as seen by one CTA
+struct TL {
+  int n, chunk, off, r0, nloc;
+  float inv;
+};
+__device__ __forceinline__ TL tl_make(const TailLevel& L, int q) {
+  TL t;
+  t.n = L.n;
+  t.chunk = L.chunk;
+  t.off = L.off;
+  t.r0 = q * L.chunk;
+  t.nloc = max(0, min(L.n - t.r0, L.chunk));
+  t.inv = 1.0f / (float)L.chunk;
+  return t;
+}
+__device__ __forceinline__ double* tl_vec(double* sm, const TL& t, int k) {
+  return sm + t.off + k * t.chunk;
+}
+// vector k of level t at global row col (any CTA's chunk)
+__device__ __forceinline__ double tl_get(const TailSh& s, const TL& t, int k, int col) {
+  int q = (int)((float)col * t.inv);
+  if (q * t.chunk > col) --q;
+  else if ((q + 1) * t.chunk <= col) ++q;
+  return s.base[q][t.off + k * t.chunk + col - q * t.chunk];
+}
 
 template <int K>
 __device__ __forceinline__ void tail_reduce(cg::cluster_group& cl, TailSh& s, int& slot,
@@ -1129,43 +1158,40 @@ __device__ __forceinline__ void tail_reduce(cg::cluster_group& cl, TailSh& s, in
   slot ^= 1;
 }
 
-// rows [r0, r1) of y = A x, 4 lanes per row, four strides per pass with all
-// value/column loads issued before the x gathers (two dependent L2 round
-// trips per pass); epi(row, sum) on the lead lane
+// own rows of y = A x (x = vector k of level xt, gathered over DSMEM),
+// 4 lanes per row, four strides per pass with the value/column loads issued
+// before the gathers; epi(local row, sum) on the lead lane
 template <class F>
-__device__ __forceinline__ void tail_spmv(const int* __restrict__ rp, const int* __restrict__ ci,
-                                          const double* __restrict__ v, const double* x, int r0,
-                                          int r1, F epi) {
+__device__ __forceinline__ void tail_spmv(const TailSh& s, const int* __restrict__ rp,
+                                          const int* __restrict__ ci,
+                                          const double* __restrict__ v, int r0, int nloc,
+                                          const TL& xt, int k, F epi) {
   const int lane = threadIdx.x & 31, sub = lane & 3, grp = lane >> 2, wid = threadIdx.x >> 5;
-  for (int base = r0 + wid * 8; base < r1; base += kTailWarps * 8) {
-    const int row = base + grp;
-    double s = 0.0;
-    if (row < r1) {
+  for (int base = wid * 8; base < nloc; base += kTailWarps * 8) {
+    const int li = base + grp;
+    double acc = 0.0;
+    if (li < nloc) {
+      const int row = r0 + li;
       const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
       for (int k0 = beg + sub; k0 < end; k0 += 16) {
         double vv[4], xv[4];
         int cc[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int k = k0 + 4 * u;
-          vv[u] = k < end ? __ldg(v + k) : 0.0;
-          cc[u] = k < end ? __ldg(ci + k) : -1;
+          const int kk = k0 + 4 * u;
+          vv[u] = kk < end ? __ldg(v + kk) : 0.0;
+          cc[u] = kk < end ? __ldg(ci + kk) : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) xv[u] = cc[u] >= 0 ? __ldcg(x + cc[u]) : 0.0;
+        for (int u = 0; u < 4; ++u) xv[u] = cc[u] >= 0 ? tl_get(s, xt, k, cc[u]) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) s = fma(vv[u], xv[u], s);
+        for (int u = 0; u < 4; ++u) acc = fma(vv[u], xv[u], acc);
       }
     }
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (sub == 0 && row < r1) epi(row, s);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (sub == 0 && li < nloc) epi(li, acc);
   }
-}
-
-__device__ __forceinline__ void tail_rows(int n, int q, int cs, int& r0, int& r1) {
-  r0 = (int)((long long)n * q / cs);
-  r1 = (int)((long long)n * (q + 1) / cs);
 }
 
 __device__ __forceinline__ void tail_fin(TailSh& s, Fin f, double tot) {
@@ -1177,30 +1203,31 @@ __device__ __forceinline__ void tail_fin(TailSh& s, Fin f, double tot) {
 }
 
 // fgmres(A, b, x, jacobi, {tol 0, max 2, restart 2}) (amg.cpp:265-276,
-// krylov.cpp:17-121) on level L, x in/out (x_zero: x is known to be zero)
-__device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const TailLevel& L,
-                            bool x_zero) {
-  const int q = (int)cl.block_rank(), cs = (int)cl.num_blocks();
-  int r0, r1;
-  tail_rows(L.n, q, cs, r0, r1);
-  const int t0 = r0 + threadIdx.x;
+// krylov.cpp:17-121) on level t, x in/out (x_zero: x is known to be zero)
+__device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, double* sm, int& slot,
+                            const TailLevel& L, const TL& t, bool x_zero) {
   KState* st = reinterpret_cast<KState*>(s.ks);
+  const int i0 = threadIdx.x, nloc = t.nloc;
+  double* b = tl_vec(sm, t, TB);
+  double* x = tl_vec(sm, t, TX);
+  double* rs = tl_vec(sm, t, TRS);
+  double* w = tl_vec(sm, t, TW);
+  double* v0 = tl_vec(sm, t, TV0);
+  double* v1 = tl_vec(sm, t, TV1);
+  double* z0 = tl_vec(sm, t, TZ0);
+  double* z1 = tl_vec(sm, t, TZ1);
+  const double* dinv = L.dinv + t.r0;
   // ref = ||b|| and the (re)start residual r = b - A x, beta = ||r||
   {
     double red[2] = {0.0, 0.0};
-    for (int i = t0; i < r1; i += kTailThreads) {
-      const double bi = __ldcg(L.b + i);
-      red[0] = fma(bi, bi, red[0]);
-    }
+    for (int i = i0; i < nloc; i += kTailThreads) red[0] = fma(b[i], b[i], red[0]);
     if (x_zero) {
       red[1] = red[0];
     } else {
-      const double* b = L.b;
-      double* rs = L.rs;
       double acc = 0.0;
-      tail_spmv(L.arp, L.aci, L.av, L.x, r0, r1, [&](int row, double sum) {
-        const double ri = __ldcg(b + row) - sum;
-        rs[row] = ri;
+      tail_spmv(s, L.arp, L.aci, L.av, t.r0, nloc, t, TX, [&](int li, double sum) {
+        const double ri = b[li] - sum;
+        rs[li] = ri;
         acc = fma(ri, ri, acc);
       });
       red[1] = acc;
@@ -1215,23 +1242,21 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const T
     f.tol = 0.0;
     tail_fin(s, f, red[1]);
   }
-  const double* r = x_zero ? L.b : L.rs;
+  const double* r = x_zero ? b : rs;
   if (!st->stop) {
     const double beta = st->beta;
-    for (int i = t0; i < r1; i += kTailThreads) {
-      const double vi = __ldcg(r + i) / beta;
-      L.v0[i] = vi;
-      L.z0[i] = __ldg(L.dinv + i) * vi;
+    for (int i = i0; i < nloc; i += kTailThreads) {
+      const double vi = r[i] / beta;
+      v0[i] = vi;
+      z0[i] = __ldg(dinv + i) * vi;
     }
     cluster_bar();
     // Arnoldi step 0: w = A z0, h00 = (w, v0); w -= h00 v0, ||w||
     {
       double red[1] = {0.0};
-      double* w = L.w;
-      const double* v0 = L.v0;
-      tail_spmv(L.arp, L.aci, L.av, L.z0, r0, r1, [&](int row, double sum) {
-        w[row] = sum;
-        red[0] = fma(sum, __ldcg(v0 + row), red[0]);
+      tail_spmv(s, L.arp, L.aci, L.av, t.r0, nloc, t, TZ0, [&](int li, double sum) {
+        w[li] = sum;
+        red[0] = fma(sum, v0[li], red[0]);
       });
       tail_reduce<1>(cl, s, slot, red);
       Fin f;
@@ -1243,9 +1268,9 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const T
     {
       const double h = ks_h(st)[0];
       double red[1] = {0.0};
-      for (int i = t0; i < r1; i += kTailThreads) {
-        const double wi = fma(-h, __ldcg(L.v0 + i), __ldcg(L.w + i));
-        L.w[i] = wi;
+      for (int i = i0; i < nloc; i += kTailThreads) {
+        const double wi = fma(-h, v0[i], w[i]);
+        w[i] = wi;
         red[0] = fma(wi, wi, red[0]);
       }
       tail_reduce<1>(cl, s, slot, red);
@@ -1256,21 +1281,19 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const T
     }
     if (!st->stop) {
       const double wn = st->wnorm;
-      for (int i = t0; i < r1; i += kTailThreads) {
-        const double vi = __ldcg(L.w + i) / wn;
-        L.v1[i] = vi;
-        L.z1[i] = __ldg(L.dinv + i) * vi;
+      for (int i = i0; i < nloc; i += kTailThreads) {
+        const double vi = w[i] / wn;
+        v1[i] = vi;
+        z1[i] = __ldg(dinv + i) * vi;
       }
       cluster_bar();
       // Arnoldi step 1: w = A z1, h01 = (w, v0); w -= h01 v0, h11 = (w, v1);
       // w -= h11 v1, ||w|| (v2 is never used by the update, so not formed)
       {
         double red[1] = {0.0};
-        double* w = L.w;
-        const double* v0 = L.v0;
-        tail_spmv(L.arp, L.aci, L.av, L.z1, r0, r1, [&](int row, double sum) {
-          w[row] = sum;
-          red[0] = fma(sum, __ldcg(v0 + row), red[0]);
+        tail_spmv(s, L.arp, L.aci, L.av, t.r0, nloc, t, TZ1, [&](int li, double sum) {
+          w[li] = sum;
+          red[0] = fma(sum, v0[li], red[0]);
         });
         tail_reduce<1>(cl, s, slot, red);
         Fin f;
@@ -1282,10 +1305,10 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const T
       {
         const double h = ks_h(st)[1];
         double red[1] = {0.0};
-        for (int i = t0; i < r1; i += kTailThreads) {
-          const double wi = fma(-h, __ldcg(L.v0 + i), __ldcg(L.w + i));
-          L.w[i] = wi;
-          red[0] = fma(wi, __ldcg(L.v1 + i), red[0]);
+        for (int i = i0; i < nloc; i += kTailThreads) {
+          const double wi = fma(-h, v0[i], w[i]);
+          w[i] = wi;
+          red[0] = fma(wi, v1[i], red[0]);
         }
         tail_reduce<1>(cl, s, slot, red);
         Fin f;
@@ -1297,9 +1320,9 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const T
       {
         const double h = ks_h(st)[3];
         double red[1] = {0.0};
-        for (int i = t0; i < r1; i += kTailThreads) {
-          const double wi = fma(-h, __ldcg(L.v1 + i), __ldcg(L.w + i));
-          L.w[i] = wi;
+        for (int i = i0; i < nloc; i += kTailThreads) {
+          const double wi = fma(-h, v1[i], w[i]);
+          w[i] = wi;
           red[0] = fma(wi, wi, red[0]);
         }
         tail_reduce<1>(cl, s, slot, red);
@@ -1326,11 +1349,11 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const T
   const int j = st->jeff;
   if (j > 0 || x_zero) {
     const double* y = ks_y(st);
-    for (int i = t0; i < r1; i += kTailThreads) {
+    for (int i = i0; i < nloc; i += kTailThreads) {
       double corr = 0.0;
-      if (j > 0) corr = fma(y[0], __ldcg(L.z0 + i), corr);
-      if (j > 1) corr = fma(y[1], __ldcg(L.z1 + i), corr);
-      L.x[i] = x_zero ? corr : __ldcg(L.x + i) + corr;
+      if (j > 0) corr = fma(y[0], z0[i], corr);
+      if (j > 1) corr = fma(y[1], z1[i], corr);
+      x[i] = x_zero ? corr : x[i] + corr;
     }
   }
   cluster_bar();
@@ -1338,83 +1361,111 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, int& slot, const T
 
 __global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams p) {
   __shared__ TailSh s;
+  extern __shared__ double sm[];
   cg::cluster_group cl = cg::this_cluster();
   const int q = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  if (threadIdx.x < cs) s.base[threadIdx.x] = cl.map_shared_rank(sm, (int)threadIdx.x);
   int slot = 0;
   const int nl = p.nlev;
+  {
+    const TL t = tl_make(p.L[0], q);
+    double* b = tl_vec(sm, t, TB);
+    for (int i = threadIdx.x; i < t.nloc; i += kTailThreads) b[i] = __ldg(p.b0 + t.r0 + i);
+  }
+  cluster_bar();
   // down: pre-smoothing from zero, r = b - A x, b_(l+1) = R r
   for (int l = 0; l + 1 < nl; ++l) {
     const TailLevel& L = p.L[l];
-    tail_smooth(cl, s, slot, L, true);
-    int r0, r1;
-    tail_rows(L.n, q, cs, r0, r1);
+    const TL t = tl_make(L, q);
+    tail_smooth(cl, s, sm, slot, L, t, true);
     {
-      const double* b = L.b;
-      double* r = L.r;
-      tail_spmv(L.arp, L.aci, L.av, L.x, r0, r1,
-                [&](int row, double sum) { r[row] = __ldcg(b + row) - sum; });
+      const double* b = tl_vec(sm, t, TB);
+      double* r = tl_vec(sm, t, TR);
+      tail_spmv(s, L.arp, L.aci, L.av, t.r0, t.nloc, t, TX,
+                [&](int li, double sum) { r[li] = b[li] - sum; });
     }
     cluster_bar();
-    const TailLevel& C = p.L[l + 1];
-    tail_rows(C.n, q, cs, r0, r1);
+    const TL tc = tl_make(p.L[l + 1], q);
     {
-      double* bc = C.b;
-      tail_spmv(L.rrp, L.rci, L.rv, L.r, r0, r1, [&](int row, double sum) { bc[row] = sum; });
+      double* bc = tl_vec(sm, tc, TB);
+      tail_spmv(s, L.rrp, L.rci, L.rv, tc.r0, tc.nloc, t, TR,
+                [&](int li, double sum) { bc[li] = sum; });
     }
     cluster_bar();
   }
   // coarse: x = K^-1 b (dense inverse), one warp per row
   {
-    const TailLevel& C = p.L[nl - 1];
-    int r0, r1;
-    tail_rows(C.n, q, cs, r0, r1);
+    const TL tc = tl_make(p.L[nl - 1], q);
+    double* xc = tl_vec(sm, tc, TX);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int row = r0 + wid; row < r1; row += kTailWarps) {
-      const double* a = p.cinv + (size_t)row * C.n;
+    for (int li = wid; li < tc.nloc; li += kTailWarps) {
+      const double* a = p.cinv + (size_t)(tc.r0 + li) * tc.n;
       double sum = 0.0;
-      for (int j0 = lane; j0 < C.n; j0 += 128) {
+      for (int j0 = lane; j0 < tc.n; j0 += 128) {
         double av[4], bv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int j = j0 + 32 * u;
-          av[u] = j < C.n ? __ldg(a + j) : 0.0;
-          bv[u] = j < C.n ? __ldcg(C.b + j) : 0.0;
+          av[u] = j < tc.n ? __ldg(a + j) : 0.0;
+          bv[u] = j < tc.n ? tl_get(s, tc, TB, j) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) sum = fma(av[u], bv[u], sum);
       }
       sum = warp_sum(sum);
-      if (lane == 0) C.x[row] = sum;
+      if (lane == 0) xc[li] = sum;
     }
     cluster_bar();
   }
   // up: x_l += P x_(l+1), post-smoothing
   for (int l = nl - 2; l >= 0; --l) {
     const TailLevel& L = p.L[l];
-    const TailLevel& C = p.L[l + 1];
-    int r0, r1;
-    tail_rows(L.n, q, cs, r0, r1);
+    const TL t = tl_make(L, q);
+    const TL tc = tl_make(p.L[l + 1], q);
     {
-      double* x = L.x;
-      tail_spmv(L.prp, L.pci, L.pv, C.x, r0, r1,
-                [&](int row, double sum) { x[row] = __ldcg(x + row) + sum; });
+      double* x = tl_vec(sm, t, TX);
+      tail_spmv(s, L.prp, L.pci, L.pv, t.r0, t.nloc, tc, TX,
+                [&](int li, double sum) { x[li] = x[li] + sum; });
     }
     cluster_bar();
-    tail_smooth(cl, s, slot, L, false);
+    tail_smooth(cl, s, sm, slot, L, t, false);
   }
+  {
+    const TL t = tl_make(p.L[0], q);
+    const double* x = tl_vec(sm, t, TX);
+    for (int i = threadIdx.x; i < t.nloc; i += kTailThreads) p.x0[t.r0 + i] = x[i];
+  }
+  // no CTA may exit while another can still read its shared memory
+  cluster_bar();
 }
 
-static int g_tail_cluster = -1;
-int scalar_tail_cluster(Ctx& c) {
-  if (g_tail_cluster >= 0) return g_tail_cluster;
-  int best = 0;
-  if (cudaFuncSetAttribute(scalar_tail_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-      cudaSuccess)
-    cudaGetLastError();
-  for (int cs : {16, 8, 4}) {
+bool scalar_tail_plan(Ctx& c, TailParams& p) {
+  (void)c;
+  if (p.nlev < 1 || p.nlev > kTailMaxLev) return false;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(scalar_tail_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) != cudaSuccess)
+      cudaGetLastError();
+    if (cudaFuncSetAttribute(scalar_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024) != cudaSuccess)
+      cudaGetLastError();
+    attr = true;
+  }
+  for (int cs : {16, 8}) {
+    size_t off = 0;
+    for (int l = 0; l < p.nlev; ++l) {
+      TailLevel& L = p.L[l];
+      L.chunk = (L.n + cs - 1) / cs;
+      L.off = (int)off;
+      off += (size_t)kTailVecs * L.chunk;
+    }
+    const size_t bytes = off * sizeof(double);
+    if (bytes > 200 * 1024) continue;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(kTailThreads);
+    cfg.dynamicSmemBytes = bytes;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = cs;
@@ -1424,27 +1475,26 @@ int scalar_tail_cluster(Ctx& c) {
     cfg.numAttrs = 1;
     int nc = 0;
     if (cudaOccupancyMaxActiveClusters(&nc, scalar_tail_kernel, &cfg) == cudaSuccess && nc > 0) {
-      best = cs;
-      break;
+      p.cs = cs;
+      p.smem = bytes;
+      return true;
     }
     cudaGetLastError();
   }
-  (void)c;
-  g_tail_cluster = best;
-  return best;
+  return false;
 }
 
 void launch_scalar_tail(Ctx& c, const TailParams& p) {
-  const int cs = scalar_tail_cluster(c);
-  SAG_REQUIRE(cs > 0 && p.nlev >= 1 && p.nlev <= kTailMaxLev, SAG_ERROR,
-              "scalar V-cycle tail: no resident cluster / bad level count");
+  SAG_REQUIRE(p.cs > 0 && p.nlev >= 1 && p.nlev <= kTailMaxLev && p.b0 && p.x0, SAG_ERROR,
+              "scalar V-cycle tail: not planned");
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(cs);
+  cfg.gridDim = dim3(p.cs);
   cfg.blockDim = dim3(kTailThreads);
+  cfg.dynamicSmemBytes = p.smem;
   cfg.stream = c.stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.x = p.cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;

@@ -746,8 +746,8 @@ static void scalar_level(Ctx& c, ScalarH& t, int l, const double* b, double* x) 
   }
   if (l == t.tail_from) {
     TailParams p = t.tail;
-    p.L[0].b = const_cast<double*>(b);
-    p.L[0].x = x;
+    p.b0 = b;
+    p.x0 = x;
     launch_scalar_tail(c, p);
     return;
   }
@@ -1061,41 +1061,35 @@ static void scalar_setup(Ctx& c, ScalarH& t, int nl, const sag_matrix* const* a,
   t.coarse.setup(c, *t.A.back(), -1, 0.0);
   // the small levels as one cluster launch (SAG_SCALAR_TAIL=0: per-kernel path)
   const char* e = getenv("SAG_SCALAR_TAIL");
-  if ((e && std::strcmp(e, "0") == 0) || !t.coarse.use_inv || scalar_tail_cluster(c) == 0) return;
+  if ((e && std::strcmp(e, "0") == 0) || !t.coarse.use_inv) return;
   const char* er = getenv("SAG_TAIL_ROWS");
   const int rows_max = er ? atoi(er) : kTailRows;
-  int from = nl - 1;
-  while (from > 0 && t.A[from - 1]->nrows <= rows_max && nl - (from - 1) <= kTailMaxLev) --from;
-  if (nl - from < 2) return;
-  t.tail_from = from;
-  t.tail.nlev = nl - from;
-  t.tail.cinv = t.coarse.inv.p;
-  for (int l = from; l < nl; ++l) {
-    TailLevel& L = t.tail.L[l - from];
-    const Matrix& A = *t.A[l];
-    L.n = A.nrows;
-    L.arp = A.rp.p;
-    L.aci = A.ci.p;
-    L.av = A.v.p;
-    L.b = t.sb[l].p;
-    L.x = t.sx[l].p;
-    if (l + 1 < nl) {
-      L.rrp = t.R[l]->rp.p;
-      L.rci = t.R[l]->ci.p;
-      L.rv = t.R[l]->v.p;
-      L.prp = t.P[l]->rp.p;
-      L.pci = t.P[l]->ci.p;
-      L.pv = t.P[l]->v.p;
-      L.dinv = t.dinv[l].p;
-      L.r = t.sr[l].p;
-      Krylov& K = t.kr[l];
-      L.rs = K.r.p;
-      L.w = K.w.p;
-      L.v0 = K.v(0);
-      L.v1 = K.v(1);
-      L.z0 = K.z(0);
-      L.z1 = K.z(1);
+  for (int from = 0; from + 1 < nl; ++from) {
+    if (t.A[from]->nrows > rows_max || nl - from > kTailMaxLev) continue;
+    TailParams tp;
+    tp.nlev = nl - from;
+    tp.cinv = t.coarse.inv.p;
+    for (int l = from; l < nl; ++l) {
+      TailLevel& L = tp.L[l - from];
+      const Matrix& A = *t.A[l];
+      L.n = A.nrows;
+      L.arp = A.rp.p;
+      L.aci = A.ci.p;
+      L.av = A.v.p;
+      if (l + 1 < nl) {
+        L.rrp = t.R[l]->rp.p;
+        L.rci = t.R[l]->ci.p;
+        L.rv = t.R[l]->v.p;
+        L.prp = t.P[l]->rp.p;
+        L.pci = t.P[l]->ci.p;
+        L.pv = t.P[l]->v.p;
+        L.dinv = t.dinv[l].p;
+      }
     }
+    if (!scalar_tail_plan(c, tp)) continue;  // too large for the shared memory: next level
+    t.tail = tp;
+    t.tail_from = from;
+    return;
   }
 }
 
