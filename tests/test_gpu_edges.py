@@ -278,3 +278,22 @@ def test_hoamg_refused_on_sv(S):
         h.hoamg_device(S.SolverConfig(variant=3, enclosed_flow=True))
     K0, prec = h.hoamg_device(S.SolverConfig(variant=3, enclosed_flow=True, allow_sv_hoamg=True))
     assert prec.apply(np.ones(h.n0)).shape == (h.n0,)
+
+
+def test_uzawa_scalar_tail(S, monkeypatch):
+    # Uzawa's scalar V(2,2) cycles (A_x: three levels at n = 64) with the
+    # cluster tail off, from level 1 on, and over the whole cycle: same
+    # operator as the reference, fewer launches as the tail grows
+    ctx = S.default_context()
+    launches = {}
+    for tail in ("0", "from1", "all"):
+        monkeypatch.setenv("SAG_SCALAR_TAIL", "0" if tail == "0" else "1")
+        monkeypatch.setenv("SAG_TAIL_ROWS", "5000" if tail == "from1" else "65536")
+        c, ref, h, K0, prec, cfg = _prec_pair(S, 64, 4)
+        r = O.splitmix64_uniform(c.n0)
+        z = prec.apply(r)
+        assert rel_inf(z, ref.apply(r)) <= 1e-9, tail
+        l0 = ctx.launch_count()
+        assert np.array_equal(z, prec.apply(r))
+        launches[tail] = ctx.launch_count() - l0
+    assert launches["all"] < launches["from1"] < launches["0"], launches

@@ -415,17 +415,15 @@ def test_vanka_thread_per_patch_layout(S, monkeypatch):
         assert np.array_equal(got[key], want[key]), key
 
 
-@pytest.mark.parametrize("tail", ["0", "1", "rows"])
+@pytest.mark.parametrize("tail", ["0", "1"])
 def test_sv_scalar_tail(S, monkeypatch, tail):
     # the mass projection's scalar V(2,2) cycles with their small levels as one
-    # cluster launch (all levels; from level 1 with SAG_TAIL_ROWS) against the
-    # per-kernel path and the reference
+    # cluster launch (here the whole two-level cycle) against the per-kernel
+    # path and the reference
     conf = dict(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500, enclosed_flow=True,
                 omega0=0.78, eta_u=1.0, eta_p=2.68)
     c, d, k0, levels, _ = ref_case(64, sv=True, cfg=conf)
-    monkeypatch.setenv("SAG_SCALAR_TAIL", "0" if tail == "0" else "1")
-    if tail == "rows":
-        monkeypatch.setenv("SAG_TAIL_ROWS", "1000")
+    monkeypatch.setenv("SAG_SCALAR_TAIL", tail)
     h, K0, dc, cfg = _host_device(S, dict(problem="cavity", sv=True, n=64), conf)
     r = O.splitmix64_uniform(c.n0)
     z = dc.apply(r)
