@@ -222,6 +222,16 @@ void launch_update(Ctx& c, int n, double* x, const double* Z, size_t zstride, KS
                    bool store = false);
 // z = dinv * r
 void launch_mul(Ctx& c, int n, const double* a, const double* b, double* y);
+// ||a||^2 applied to two finishers (one pass)
+void launch_ssq2(Ctx& c, int n, const double* a, const Fin& f1, const Fin& f2);
+// y = x / *s, z = d .* y (skipped when *gate)
+void launch_div_mul(Ctx& c, int n, const double* x, const double* s, double* y, const double* d,
+                    double* z, const int* gate);
+// launch_backsub + launch_update in one launch when the restart length m is
+// at most kUpdBsMax (else the two launches)
+constexpr int kUpdBsMax = 4;
+void launch_update_bs(Ctx& c, int n, double* x, const double* Z, size_t zstride, KState* st,
+                      int m, bool store = false);
 // dinv_i = 1 / a_ii; returns false (via *bad) if a diagonal entry is missing/zero
 void launch_inv_diag(Ctx& c, const Matrix& m, double* dinv, int* bad);
 

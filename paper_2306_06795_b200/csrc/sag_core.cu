@@ -503,6 +503,35 @@ __global__ void __launch_bounds__(kRedBlock) dot_kernel(int n, const double* __r
   reduce_finish(s, fin, partials, ticket);
 }
 
+// ||a||^2 finished twice (e.g. FIN_REF then FIN_BETA of an inner solve whose
+// residual is its right-hand side): one pass instead of two identical ones
+__global__ void __launch_bounds__(kRedBlock) ssq2_kernel(int n, const double* __restrict__ a,
+                                                         Fin f1, Fin f2, double* partials,
+                                                         unsigned* ticket) {
+  const int st = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0;
+  for (; i + 3 * st < n; i += 4 * st) {
+    const double a0 = a[i], a1 = a[i + st], a2 = a[i + 2 * st], a3 = a[i + 3 * st];
+    s = fma(a0, a0, s);
+    s = fma(a1, a1, s);
+    s = fma(a2, a2, s);
+    s = fma(a3, a3, s);
+  }
+  for (; i < n; i += st) s = fma(a[i], a[i], s);
+  __shared__ double sh[32];
+  const double bs = block_sum(s, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = bs;
+  if (last_block(ticket)) {
+    const double tot = sum_partials(partials, gridDim.x, sh);
+    if (threadIdx.x == 0) {
+      apply_fin(f1, tot);
+      apply_fin(f2, tot);
+      *ticket = 0u;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kRedBlock) sum_kernel(int n, const double* __restrict__ a,
                                                         Fin fin, double* partials,
                                                         unsigned* ticket) {
@@ -653,6 +682,51 @@ __global__ void update_kernel(int n, double* __restrict__ x, const double* __res
   }
 }
 
+// y = x / *s and z = d .* y in one pass (v_0 = r / beta, z_0 = M v_0 for a
+// Jacobi-preconditioned inner solve, amg.cpp:265-276)
+__global__ void div_mul_kernel(int n, const double* __restrict__ x, const double* s,
+                               double* __restrict__ y, const double* __restrict__ d,
+                               double* __restrict__ z, const int* gate) {
+  if (gate && *gate) return;
+  const double q = *s;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double v = x[i] / q;
+    y[i] = v;
+    z[i] = d[i] * v;
+  }
+}
+
+// backsub_kernel + update_kernel in one launch for short inner solves
+// (jeff <= kUpdBsMax): every block back-substitutes the small Hessenberg
+// system itself (the same operations as backsub_kernel), block 0 stores y
+__global__ void update_bs_kernel(int n, double* __restrict__ x, const double* __restrict__ Z,
+                                 size_t zs, KState* st, int store) {
+  __shared__ double ys[kUpdBsMax];
+  const int j = st->jeff, m = st->m;
+  if (threadIdx.x == 0) {
+    const double* h = ks_h(st);
+    const double* g = ks_g(st);
+    double y[kUpdBsMax];
+    for (int i = j - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int k = i + 1; k < j; ++k) s -= h[(size_t)i * m + k] * y[k];
+      y[i] = s / h[(size_t)i * m + i];
+    }
+    for (int i = 0; i < j; ++i) {
+      ys[i] = y[i];
+      if (blockIdx.x == 0) ks_y(st)[i] = y[i];
+    }
+  }
+  __syncthreads();
+  if (j == 0 && !store) return;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    double corr = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < j; ++i) corr = fma(ys[i], Z[(size_t)i * zs + k], corr);
+    x[k] = store ? corr : x[k] + corr;
+  }
+}
+
 __global__ void mul_kernel(int n, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ y) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -776,6 +850,26 @@ void launch_backsub(Ctx& c, KState* st) {
 void launch_update(Ctx& c, int n, double* x, const double* Z, size_t zstride, KState* st,
                    bool store) {
   update_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, Z, zstride, st, store ? 1 : 0);
+  SAG_LAUNCHED(c);
+}
+void launch_ssq2(Ctx& c, int n, const double* a, const Fin& f1, const Fin& f2) {
+  ssq2_kernel<<<red_grid_fit(c, ssq2_kernel, n), kRedBlock, 0, c.stream>>>(n, a, f1, f2,
+                                                                           c.partials.p, c.ticket.p);
+  SAG_LAUNCHED(c);
+}
+void launch_div_mul(Ctx& c, int n, const double* x, const double* s, double* y, const double* d,
+                    double* z, const int* gate) {
+  div_mul_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, s, y, d, z, gate);
+  SAG_LAUNCHED(c);
+}
+void launch_update_bs(Ctx& c, int n, double* x, const double* Z, size_t zstride, KState* st,
+                      int m, bool store) {
+  if (m > kUpdBsMax) {
+    launch_backsub(c, st);
+    launch_update(c, n, x, Z, zstride, st, store);
+    return;
+  }
+  update_bs_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, Z, zstride, st, store ? 1 : 0);
   SAG_LAUNCHED(c);
 }
 void launch_mul(Ctx& c, int n, const double* a, const double* b, double* y) {

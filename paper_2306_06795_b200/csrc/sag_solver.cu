@@ -55,8 +55,9 @@ struct Krylov {
 //   v_(j+1) = w / ||w|| unless breakdown
 // last: final step of a fixed-length inner solve -- v_(j+1) is never used, so
 // it is not formed and w keeps A z_j (reused by lin_resid for nu = 1).
+// jac: also form z_(j+1) = jac .* v_(j+1) (Jacobi preconditioner) in the same pass.
 static void arnoldi_step(Ctx& c, const Matrix& A, Krylov& K, int mm, int j, const int* gate,
-                         bool last = false) {
+                         bool last = false, const double* jac = nullptr) {
   const int n = K.n;
   {
     SpmvArgs a;
@@ -81,7 +82,11 @@ static void arnoldi_step(Ctx& c, const Matrix& A, Krylov& K, int mm, int j, cons
   f.st = K.st;
   f.j = j;
   launch_mgs_last(c, n, K.w.p, K.v(j), K.h(mm, j, j), f, gate, !last);
-  if (!last) launch_div(c, n, K.w.p, K.wnorm(), K.v(j + 1), gate, K.breakdown());
+  if (last) return;
+  if (jac)  // breakdown sets stop (FIN_ARNOLDI), so the stop gate covers it
+    launch_div_mul(c, n, K.w.p, K.wnorm(), K.v(j + 1), jac, K.z(j + 1), gate);
+  else
+    launch_div(c, n, K.w.p, K.wnorm(), K.v(j + 1), gate, K.breakdown());
 }
 
 // vanka_relax, KrylovWrapped (vanka.cpp:199-208): x += FGMRES_nu(K, b - K x;
@@ -117,8 +122,7 @@ static void relax_kw(Ctx& c, const Matrix& K, const Vanka& f, Krylov& kr, double
     vanka_apply(c, f, kr.v(j), kr.z(j), kr.stop());
     arnoldi_step(c, K, kr, nu, j, kr.stop(), j == nu - 1);
   }
-  launch_backsub(c, kr.st);
-  launch_update(c, n, x, kr.Z.p, (size_t)n, kr.st, x_zero);
+  launch_update_bs(c, n, x, kr.Z.p, (size_t)n, kr.st, nu, x_zero);
 }
 
 // vanka_relax, Stationary (vanka.cpp:190-197): x += omega * vanka(b - K x).
@@ -703,15 +707,14 @@ static void scalar_level(Ctx& c, ScalarH& t, int l, const double* b, double* x);
 static void jacobi_fgmres2(Ctx& c, ScalarH& t, int l, const double* b, double* x, bool x_zero) {
   // fgmres(matrix_operator(a), b, x, jacobi, {tol 0, max 2, restart 2}) with x in/out:
   // bnorm = ||b|| is the reference (krylov.cpp:23-24), the residual b - a x.
+  // z_j = jacobi(v_j) is formed in the pass that forms v_j; v_2 (never used
+  // by the update) is not formed.
   const Matrix& A = *t.A[l];
   Krylov& K = t.kr[l];
   const int n = A.nrows;
-  {
-    Fin f;
-    f.kind = FIN_REF;
-    f.st = K.st;
-    launch_ssq(c, n, b, f);
-  }
+  Fin fr;
+  fr.kind = FIN_REF;
+  fr.st = K.st;
   Fin fb;
   fb.kind = FIN_BETA;
   fb.st = K.st;
@@ -720,22 +723,21 @@ static void jacobi_fgmres2(Ctx& c, ScalarH& t, int l, const double* b, double* x
   fb.tol = 0.0;
   const double* r;
   if (x_zero) {
-    launch_ssq(c, n, b, fb);
+    launch_ssq2(c, n, b, fr, fb);  // r = b: ||b|| is both
     r = b;
   } else {
+    launch_ssq(c, n, b, fr);
     SpmvArgs a;
     a.b = b;
     a.fin = fb;
     launch_spmv(c, A, x, K.r.p, Epi::ResidSsq, a);
     r = K.r.p;
   }
-  launch_div(c, n, r, K.beta(), K.v(0), K.stop());
-  for (int j = 0; j < 2; ++j) {
-    launch_mul(c, n, t.dinv[l].p, K.v(j), K.z(j));
-    arnoldi_step(c, A, K, 2, j, K.stop());
-  }
-  launch_backsub(c, K.st);
-  launch_update(c, n, x, K.Z.p, (size_t)n, K.st, x_zero);
+  const double* dinv = t.dinv[l].p;
+  launch_div_mul(c, n, r, K.beta(), K.v(0), dinv, K.z(0), K.stop());
+  arnoldi_step(c, A, K, 2, 0, K.stop(), false, dinv);
+  arnoldi_step(c, A, K, 2, 1, K.stop(), true);
+  launch_update_bs(c, n, x, K.Z.p, (size_t)n, K.st, 2, x_zero);
 }
 
 static void scalar_level(Ctx& c, ScalarH& t, int l, const double* b, double* x) {
