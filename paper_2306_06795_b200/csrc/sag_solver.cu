@@ -726,7 +726,8 @@ static void jacobi_fgmres2(Ctx& c, ScalarH& t, int l, const double* b, double* x
     launch_ssq2(c, n, b, fr, fb);  // r = b: ||b|| is both
     r = b;
   } else {
-    launch_ssq(c, n, b, fr);
+    // post-smoothing follows the pre-smoothing of the same b on this level's
+    // KState, whose ref = ||b|| is still in place (same value, no pass)
     SpmvArgs a;
     a.b = b;
     a.fin = fb;
