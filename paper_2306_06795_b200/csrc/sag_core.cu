@@ -1536,15 +1536,18 @@ __global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams
 bool scalar_tail_plan(Ctx& c, TailParams& p) {
   (void)c;
   if (p.nlev < 1 || p.nlev > kTailMaxLev) return false;
-  static bool attr = false;
-  if (!attr) {
+  // function attributes are per device
+  static bool attr[64] = {};
+  int dev = 0;
+  SAG_CUDA(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && !attr[dev]) {
     if (cudaFuncSetAttribute(scalar_tail_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
                              1) != cudaSuccess)
       cudaGetLastError();
     if (cudaFuncSetAttribute(scalar_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024) != cudaSuccess)
       cudaGetLastError();
-    attr = true;
+    attr[dev] = true;
   }
   for (int cs : {16, 8}) {
     size_t off = 0;
