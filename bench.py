@@ -213,18 +213,52 @@ def vanka_patch_bytes(f, n):
     return f.device_bytes + 8 * n + 8 * f.nslots
 
 
-def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the newest committed ncu capture
-    (profiles/<round>/ncu_traffic.json), or None."""
+def ncu_traffic(workload, kernel):
+    """DRAM bytes per launch of `kernel` ("vanka_patch": the patch stage's
+    kernels of one sweep, "vanka_gather", "spmv") on `workload` (and level)
+    from the newest committed ncu capture (profiles/<round>/ncu_traffic.json,
+    {"workloads": {workload: {kernel: bytes}}}), or None when no capture of
+    that kernel on that workload exists."""
     import glob
     best = None
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json"))):
         try:
             with open(path) as fh:
-                best = json.load(fh).get(kernel, best)
+                d = json.load(fh)
         except Exception:
-            pass
+            continue
+        w = d.get("workloads", {}).get(workload, {})
+        if kernel in w:
+            best = w[kernel]
     return best
+
+
+def config_dict(cfg, k0):
+    """The `config` object, identical in both arms."""
+    return {"workload": cfg["workload"], "k0_rows": int(k0.nrows), "k0_nnz": int(k0.nnz)}
+
+
+def golden_solve(config):
+    """The reference's solve_stokes report on this config's exact inputs,
+    measured in the build container (tests/golden/fullsize_config<N>.json)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", f"fullsize_config{config}.json")) as f:
+            return json.load(f)["solve"]
+    except Exception:
+        return None
+
+
+def host_cpu():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -258,10 +292,39 @@ def cpu_steps(k0csr, nxyz, steps, threads, budget_s=None):
     return sum(done), time.perf_counter() - t0
 
 
+def ref_solve_1core(case, cfg, repeats):
+    """solve_stokes (preconditioner.cpp:229-259) of the reference (oracle/_ref)
+    with DC-all V(1,1), FGMRES(30), rtol 1e-8, pinned to ONE host core (the
+    reference is single-threaded): min wall time over `repeats` solves; the
+    preconditioner's setup timed apart."""
+    import oracle as O
+    core = max(os.sched_getaffinity(0))
+    prev = os.sched_getaffinity(0)
+    os.sched_setaffinity(0, {core})   # the calling thread: taskset -c <core>
+    try:
+        conf = dict(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
+                    enclosed_flow=case.enclosed, eta_u=cfg.get("eta_u", 1.0),
+                    eta_p=cfg.get("eta_p", 1.0), omega0=cfg.get("omega0", 1.0))
+        t0 = time.perf_counter()
+        d = O.RefDC(case, conf)
+        setup = time.perf_counter() - t0
+        rhs = case.rhs()
+        times, rep = [], None
+        for _ in range(repeats):
+            t1 = time.perf_counter()
+            _, rep = d.solve(rhs)
+            times.append(time.perf_counter() - t1)
+    finally:
+        os.sched_setaffinity(0, prev)
+    return {"solve_s": min(times), "solves_s": times, "repeats": repeats,
+            "prec_setup_s": setup, "iterations": rep["iterations"],
+            "final_relative_residual": rep["final_relative_residual"],
+            "core": core, **host_cpu()}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    import oracle as O
     cfg = CONFIGS[args.config]
     t0 = time.perf_counter()
     case = ref_case(cfg)
@@ -271,9 +334,9 @@ def run_reference(args, ws, rank):
     if args.warmup:
         cpu_steps(k0, (case.n_x0, case.n_y0, case.n_p0), threads, threads)
     # one step = `threads` concurrent whole passes (every host thread busy
-    # whatever K is), bounded to ~2 minutes of wall time
+    # whatever K is), bounded in wall time
     done, wall = cpu_steps(k0, (case.n_x0, case.n_y0, case.n_p0), args.steps * threads, threads,
-                           budget_s=120.0)
+                           budget_s=45.0)
     val = done * k0.nrows / wall / 1e9
     steps_done = done / threads
     line = {
@@ -281,15 +344,23 @@ def run_reference(args, ws, rank):
         "steps": args.steps, "steps_done": round(steps_done, 3), "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / max(steps_done, 1e-9),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference build_case, splitmix64 input)",
-        "config": {"workload": cfg["workload"], "k0_rows": k0.nrows, "k0_nnz": k0.nnz},
+        "data": "synthetic: reference build_case cavity + splitmix64 x (SURVEY 8(d))",
+        "config": config_dict(cfg, k0),
         "cpu_baseline": {"value": val, "unit": "GDOF/s", "cores": threads, "kind": "reference",
                          "sample": f"{done} whole passes (apply_vanka + spmv on K0), "
                                    f"{threads} threads x independent passes"},
         "e2e": {"value": val, "unit": "GDOF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "setup_s": setup_s,
+        "setup_s": setup_s, "host": host_cpu(),
     }
+    if not args.no_solve:
+        # the whole reference solve on one core of this host:
+        # config 1 five times, and this config's once
+        sol = {"config1": ref_solve_1core(case if args.config == 1 else ref_case(CONFIGS[1]),
+                                          CONFIGS[1], 5)}
+        if args.config != 1:
+            sol[f"config{args.config}"] = ref_solve_1core(case, cfg, 1)
+        line["solve"] = sol
     emit(line)
 
 
@@ -318,13 +389,16 @@ def dist_solve(case, rs, levels, be, comm, dev, ws, args):
     rep = solver.solve(rhs, xs)
     torch.cuda.synchronize(dev)
     t_solve = dist_max(time.perf_counter() - ts, ws)
+    solver.close()
     return {"gpu_s": t_solve, "iterations": rep.iterations,
             "final_relative_residual": rep.final_relative_residual,
             "converged": rep.converged, "setup_s": setup_s,
             "prec_cuda_graph": solver.graph is not None,
             "path": "dsolve.DistSolver (partitioned K0/L0, agglomerated coarse levels, "
                     "NCCL all-reduce dots)",
-            "reference_cpu_s_1core": {1: 1.21, 2: 152.9}.get(args.config)}
+            "reference": golden_solve(args.config) and {
+                k: golden_solve(args.config)[k] for k in ("iterations", "cpu_s_1core",
+                                                          "final_relative_residual")}}
 
 
 def run_dist(args, ws, rank, local):
@@ -431,6 +505,7 @@ def run_dist(args, ws, rank, local):
 
         solve = None
         if not args.no_solve:
+            step.close()
             del step
             try:
                 solve = dist_solve(case, rs, levels, be, comm, dev, ws, args)
@@ -448,8 +523,8 @@ def run_dist(args, ws, rank, local):
             "ms_per_step": 1e3 * t_steps / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: reference build_case cavity + splitmix64 x (SURVEY 8(d))",
-            "config": {"workload": cfg["workload"], "k0_rows": n, "k0_nnz": k0.nnz,
-                       "parallelism": f"row/patch partition x{ws}, NCCL halo",
+            "config": config_dict(cfg, k0),
+            "layout": {"parallelism": f"row/patch partition x{ws}, NCCL halo",
                        "max_owned_dofs_per_rank": int(own_max),
                        "max_ghost_dofs_per_rank": int(ghosts),
                        "l2": "inputs exceed L2; no flush"},
@@ -475,6 +550,44 @@ def run_dist(args, ws, rank, local):
 
 
 # ------------------------------------------------------------------ GPU arm
+def level_measure(S, ctx, timed, k, nxyz, sv_triples, kper):
+    """One level's Vanka sweep and SpMV on the device (splitmix64 input):
+    times (CUDA events), SURVEY 8(d) formula bytes, the patch stage's
+    representation bytes and its launch classes."""
+    import torch
+    dev = torch.device("cuda", ctx.device)
+    K = S.SparseMatrix.from_csr(k, ctx)
+    p = S.build_patches(K, *nxyz, sv_triples=sv_triples)
+    f = S.factor_patches(K, p, nxyz[0] + nxyz[1])
+    n = k.nrows
+    x = torch.from_numpy(splitmix64_uniform(n)).to(dev)
+    d = torch.empty_like(x)
+    y = torch.empty_like(x)
+    lib = S.lib()
+    xp, dp = S.C.c_void_p(x.data_ptr()), S.C.c_void_p(d.data_ptr())
+    for _ in range(3):
+        S.apply_vanka(f, x, out=d)
+        S.spmv(K, x, out=y)
+    t_patch = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 1)), kper) / kper
+    t_gather = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 2)), kper) / kper
+    t_vanka = timed(lambda: S.apply_vanka(f, x, out=d), kper) / kper
+    t_spmv = timed(lambda: S.spmv(K, x, out=y), kper) / kper
+    tot_idx = p.total_velocity + p.total_pressure
+    b_v = vanka_bytes(f, tot_idx, n)
+    b_p = vanka_patch_bytes(f, n)
+    b_s = spmv_bytes(n, n, k.nnz)
+    cls = f.classes()
+    return {"rows": n, "nnz": int(k.nnz), "patches": f.npatch,
+            "vanka_sweep_us": 1e6 * t_vanka, "vanka_patch_us": 1e6 * t_patch,
+            "vanka_gather_us": 1e6 * t_gather, "spmv_us": 1e6 * t_spmv,
+            "vanka_gdofs": n / t_vanka / 1e9, "spmv_gdofs": n / t_spmv / 1e9,
+            "vanka_sweep_formula_bytes": b_v, "vanka_sweep_formula_gbs": b_v / t_vanka / 1e9,
+            "vanka_patch_bytes": b_p, "vanka_patch_gbs": b_p / t_patch / 1e9,
+            "spmv_bytes": b_s, "spmv_gbs": b_s / t_spmv / 1e9,
+            "patch_classes": [{"kernel": c[0], "patches": c[3], "blob_bytes": c[4]} for c in cls],
+            "_f": f, "_K": K, "_x": x}
+
+
 def run_ours(args, ws, rank, local):
     import torch
 
@@ -499,12 +612,10 @@ def run_ours(args, ws, rank, local):
     ctx.synchronize()
     factor_s = time.perf_counter() - t1
     n = k0.nrows
-    tot_idx = patches.total_velocity + patches.total_pressure
     x_host = splitmix64_uniform(n)
     x = torch.from_numpy(x_host).to(dev)
     delta = torch.empty(n, dtype=torch.float64, device=dev)
     y = torch.empty(n, dtype=torch.float64, device=dev)
-    lib = S.lib()
 
     def step():
         S.apply_vanka(f, x, out=delta)
@@ -533,13 +644,14 @@ def run_ours(args, ws, rank, local):
     barrier(ws)
     t_steps = dist_max(t_steps, ws)
 
-    # per-kernel breakdown (same stream, CUDA events)
-    xp, dp = S.C.c_void_p(x.data_ptr()), S.C.c_void_p(delta.data_ptr())
+    # per-level breakdown (same stream, CUDA events): K0 and ISO0, level 0 of
+    # the low-order hierarchy (for SV the level with the most Vanka bytes)
     kper = max(args.steps // 2, 10)
-    t_patch = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 1)), kper) / kper
-    t_gather = timed(lambda: S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 2)), kper) / kper
-    t_vanka = timed(lambda: S.apply_vanka(f, x, out=delta), kper) / kper
-    t_spmv = timed(lambda: S.spmv(K0, x, out=y), kper) / kper
+    lv = {"K0": level_measure(S, ctx, timed, k0, case.nxyz0, case.sv, kper)}
+    if not args.no_levels:
+        iso0, _, nxyz1 = case.level(0)
+        lv["ISO0"] = level_measure(S, ctx, timed, iso0, nxyz1, False, kper)
+        del iso0
     clk = clocks.stop()
 
     # e2e: the same step through the C-ABI with pinned HOST buffers, every step
@@ -564,36 +676,40 @@ def run_ours(args, ws, rank, local):
     t_e2e2 = e2e(lambda: (S.apply_vanka(f, xh, out=dh), S.spmv(K0, xh, out=yh)))
 
     peak, peak_kind = peak_hbm()
-    b_v = vanka_bytes(f, tot_idx, n)
-    b_p = vanka_patch_bytes(f, n)
-    b_s = spmv_bytes(n, n, k0.nnz)
+    L0 = lv["K0"]
+    t_patch = L0["vanka_patch_us"] * 1e-6
+    b_p = L0["vanka_patch_bytes"]
     ms_step = 1e3 * t_steps / args.steps
     value = ws * n / (t_steps / args.steps) / 1e9
+    cls = L0["patch_classes"]
+    kname = " + ".join(f"{c['kernel']} x{c['patches']}" for c in cls)
+    wl = cfg["workload"]
+    levels_out = {}
+    for name, m in lv.items():
+        mm = {k: v for k, v in m.items() if not k.startswith("_")}
+        mm["vanka_patch_frac"] = mm["vanka_patch_gbs"] / peak
+        mm["spmv_frac"] = mm["spmv_gbs"] / peak
+        key = wl if name == "K0" else f"{wl}/{name}"
+        mm["vanka_patch_traffic"] = ncu_traffic(key, "vanka_patch")
+        mm["vanka_gather_traffic"] = ncu_traffic(key, "vanka_gather")
+        mm["spmv_traffic"] = ncu_traffic(key, "spmv")
+        levels_out[name] = mm
     out = {
         "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference build_case cavity + splitmix64 x (SURVEY 8(d))",
-        "config": {"workload": cfg["workload"], "k0_rows": n, "k0_nnz": k0.nnz,
-                   "patches": f.npatch, "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
-                   "l2": "inputs (K0 + factors ~1.9 GB) exceed L2; no flush"},
+        "config": config_dict(cfg, k0),
+        "layout": {"patches": f.npatch, "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                   "l2": "inputs (K0 + factors > 1 GB) exceed the 126 MB L2; no flush"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "vanka_patch_kernel (K0)",
+        "roofline": {"bound": "hbm", "kernel": f"Vanka patch stage on K0: {kname}",
                      "achieved": b_p / t_patch / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": b_p / t_patch / 1e9 / peak, "traffic": ncu_traffic("vanka_patch"),
+                     "frac": b_p / t_patch / 1e9 / peak,
+                     "traffic": ncu_traffic(wl, "vanka_patch"),
                      "algorithmic_bytes": b_p, "peak_kind": peak_kind,
                      "bytes_def": "factor blobs + 8 n (r) + 8 slots (local results)"},
-        "kernels": {
-            "vanka_sweep_us": 1e6 * t_vanka, "vanka_patch_us": 1e6 * t_patch,
-            "vanka_gather_us": 1e6 * t_gather, "spmv_us": 1e6 * t_spmv,
-            "vanka_gdofs": n / t_vanka / 1e9, "spmv_gdofs": n / t_spmv / 1e9,
-            "vanka_sweep_formula_bytes": b_v,
-            "vanka_sweep_formula_gbs": b_v / t_vanka / 1e9,
-            "vanka_device_bytes": f.device_bytes,
-            "spmv_bytes": b_s, "spmv_gbs": b_s / t_spmv / 1e9,
-            "spmv_frac": b_s / t_spmv / 1e9 / peak, "spmv_traffic": ncu_traffic("spmv"),
-            "vanka_gather_traffic": ncu_traffic("vanka_gather"),
-        },
+        "levels": levels_out,
         "e2e": {"value": ws * n / t_e2e / 1e9, "unit": "GDOF/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 2 * 8 * n,
                 "call": "sag_vanka_spmv, pinned host buffers",
@@ -603,6 +719,7 @@ def run_ours(args, ws, rank, local):
     }
     if clk:
         out["clocks"] = clk
+    del lv, L0
 
     if not args.no_solve:
         scfg = S.SolverConfig(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
@@ -615,12 +732,25 @@ def run_ours(args, ws, rank, local):
         ts = time.perf_counter()
         xs, rep = S.solve_stokes(K0s, rhs, dc, scfg)
         t_solve = dist_max(time.perf_counter() - ts, ws)
+        # one DC-all application (preconditioner.cpp:114-153) on the device
+        r = torch.from_numpy(splitmix64_uniform(n)).to(dev)
+        z = torch.empty_like(r)
+        dc.apply(r, out=z)
+        t_apply = timed(lambda: dc.apply(r, out=z), 10) / 10
+        g = golden_solve(args.config)
         out["solve"] = {"gpu_s": t_solve, "iterations": rep.iterations,
+                        "ms_per_iteration": 1e3 * t_solve / max(rep.iterations, 1),
+                        "dc_apply_ms": 1e3 * t_apply,
                         "final_relative_residual": rep.final_relative_residual,
-                        "converged": rep.converged,
-                        "reference_cpu_s_1core": {1: 1.21, 2: 152.9, 3: 178.0}.get(args.config),
-                        "reference_cpu_note": "BASELINE.md 2 (1 core, measured at survey time)",
-                        "dc_info": dc.info()}
+                        "converged": rep.converged, "dc_info": dc.info()}
+        if g:
+            out["solve"]["reference"] = {
+                "iterations": g["iterations"],
+                "final_relative_residual": g["final_relative_residual"],
+                "cpu_s_1core": g["cpu_s_1core"],
+                "note": "reference solve_stokes on these inputs, 1 core of the build "
+                        "container (tests/golden/fullsize_config<N>.json); the reference "
+                        "arm (--impl reference) re-times it on this host"}
 
     if rank == 0 and ws == 1 and not args.no_setup and not case.sv:
         # the low-order hierarchy built by the reference (host) and with the
@@ -649,6 +779,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-levels", action="store_true",
+                    help="skip the ISO0 level measurement")
     ap.add_argument("--no-setup", action="store_true",
                     help="skip the device-assisted hierarchy setup measurement")
     ap.add_argument("--dist", action="store_true",

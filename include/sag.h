@@ -117,6 +117,11 @@ int sag_vanka_destroy(sag_vanka* f);
 /* stats = [a_factor_bytes, aux_bytes, dense_inverse_bytes (vanka.hpp:36-39),
  *          device bytes of the apply representation, npatch, n, n_slots]      */
 int sag_vanka_stats(const sag_vanka* f, long long* stats);
+/* Apply launch classes (no reference counterpart: the device layout). Class i
+ * fills out[4i..4i+3] = [rows per lane R, lanes per patch (32: warp per
+ * patch, vanka_patch_kernel<R>; 16 / 8: vanka_subwarp_kernel<LPP>), patches,
+ * blob bytes], for i < cap; *nclasses = the number of classes. */
+int sag_vanka_classes(const sag_vanka* f, long long* out, int cap, int* nclasses);
 /* Factor payload in the reference's layout (vanka.hpp:31-33), concatenated in
  * patch order: u_hat (nv x np), b_hat (np x nv), s_inv (np x np), row-major;
  * weights (length n). Any pointer may be NULL. For parity tests. */

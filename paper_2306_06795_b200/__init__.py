@@ -148,6 +148,7 @@ SIGNATURES = {
     "sag_factor_patches": (C.c_int, [vp, vp, vp, C.c_int, C.POINTER(vp)]),
     "sag_vanka_destroy": (C.c_int, [vp]),
     "sag_vanka_stats": (C.c_int, [vp, i64p]),
+    "sag_vanka_classes": (C.c_int, [vp, i64p, C.c_int, C.POINTER(C.c_int)]),
     "sag_vanka_export": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "sag_apply_vanka": (C.c_int, [vp, vp, vp, vp]),
     "sag_apply_vanka_stage": (C.c_int, [vp, vp, vp, vp, C.c_int]),
@@ -502,6 +503,19 @@ class VankaFactorization:
         _check(lib().sag_vanka_stats(h, s.ctypes.data_as(i64p)))
         (self.a_factor_bytes, self.aux_bytes, self.dense_inverse_bytes, self.device_bytes,
          self.npatch, self.n, self.nslots) = (int(v) for v in s)
+
+    def classes(self):
+        """The apply's launch classes: [(kernel, R, lanes per patch, patches,
+        blob bytes)] in launch order."""
+        out = np.zeros(4 * 16, dtype=np.int64)
+        nc = C.c_int()
+        _check(lib().sag_vanka_classes(self.h, out.ctypes.data_as(i64p), 16, C.byref(nc)))
+        res = []
+        for i in range(min(nc.value, 16)):
+            R, lpp, npch, nb = (int(v) for v in out[4 * i:4 * i + 4])
+            kern = (f"vanka_subwarp_kernel<{lpp}>" if lpp < 32 else f"vanka_patch_kernel<R={R}>")
+            res.append((kern, R, lpp, npch, nb))
+        return res
 
     def export(self, patches: PatchLists):
         nv = np.diff(patches.velocity_ptr).astype(np.int64)

@@ -21,15 +21,10 @@ struct Matrix {
   DevBuf<double> v;
   int group = 8;
   double norm_inf = -1.0;  // cached (sparse.cpp:229-237)
-  // TMA-staged SpMV: chunks of tma_rows consecutive rows whose rp/ci/v
-  // ranges are bulk-copied to shared memory (0: the register-path kernel)
-  int tma_rows = 0, tma_slot_nnz = 0, tma_stages = 0, nchunks = 0;
-  mutable int tma_occ[6] = {0, 0, 0, 0, 0, 0};  // resident CTAs per SM, per epilogue
 };
-// CSR arrays are allocated kTmaPad elements long so that bulk copies rounded
-// out to 16-byte boundaries stay inside the allocation
-constexpr int kTmaPad = 4;
-void build_chunks(Ctx& c, Matrix& m);
+// CSR arrays carry kCsrPad elements of slack (vectorised tail loads stay
+// inside the allocation)
+constexpr int kCsrPad = 4;
 
 // Vanka patch sets (vanka.hpp:11-15), CSR-like on device.
 struct Patches {
@@ -37,27 +32,6 @@ struct Patches {
   long long tot_p = 0, tot_v = 0;
   int max_nv = 0, max_np = 0, max_dim = 0;  // max_dim = max over patches of max(nx, ny)
   DevBuf<int> pptr, pidx, vptr, vidx, nx;
-};
-
-// Thread-per-patch Vanka buckets: 32 patches of one shape (nx, ny, np); the
-// payload entry e of bucket lane l sits at D[dbl_off + 32 e + l] (A_x^-1
-// packed, A_y^-1 packed, U_hat, B_hat, S^-1) and I[int_off + 32 e + l]
-// (velocity then pressure dofs); local results at out[slot_off + 32 e + l].
-constexpr int kTppMaxDim = 20;
-__host__ __device__ inline int tpp_class(int d) {
-  // one class: per-class launches ran small classes on a few SMs (measured
-  // 35 us for a 34 MB class); the unrolled NM = 20 code skips unused
-  // columns with uniform branches
-  (void)d;
-  return 20;
-}
-struct BucketHdr {
-  int nx, ny, np, count;
-  long long dbl_off, int_off;
-  int slot_off, nm;
-};
-struct TppClass {
-  int nm, b0, b1;
 };
 
 // Device factorization (vanka.hpp:23-40) in the apply representation: one
@@ -82,6 +56,7 @@ struct Vanka {
     int R, k0, k1;
     long long slot_bytes;
     int lpp;  // lanes per patch: 32, or 16 / 8 for the sub-warp kernel
+    long long bytes = 0;  // blob bytes of the class
   };
   std::vector<RClass> rclasses;
   int max_dim = 0, max_nv = 0, max_np = 0;
@@ -106,15 +81,6 @@ struct Vanka {
   // loads both components with one 16-byte shared-memory access
   bool pairs = false;
   int pair_rows = 0;
-  // thread-per-patch layout (tpp): shape buckets of 32 patches, entries
-  // interleaved across the bucket (D: doubles, I: dof indices)
-  bool tpp = false;
-  DevBuf<double> D;
-  DevBuf<int> I;
-  DevBuf<double> B;  // r gathered at every slot (tpp apply input stream)
-  DevBuf<struct BucketHdr> hdr;
-  int nbuckets = 0;
-  std::vector<struct TppClass> classes;
   // per-patch payload bases and shapes (host copies, for export)
   std::vector<long long> h_dbase, h_ibase;
   std::vector<int> h_nx, h_nv, h_np;

@@ -55,6 +55,12 @@ __device__ void apply_fin(const Fin& f, double tot) {
         st->hist_cap = 0;
       }
       if (f.i & 1) st->ref = beta > 0.0 ? beta : 1.0;
+      // a restart whose ref was never set (a KState fresh from Krylov::init,
+      // ref = 0): FIN_REF's own zero-norm rule. Exact for the tol = 0 inner
+      // solves (stop iff beta == 0); a caller that needs a tolerance relative
+      // to ||b|| must run FIN_REF first (jacobi_fgmres2's post-smoothing keeps
+      // the pre-smoothing's ref of the same b).
+      if (!(st->ref > 0.0)) st->ref = 1.0;
       st->beta = beta;
       st->rnorm = beta;
       double* g = ks_g(st);
@@ -264,212 +270,8 @@ static void spmv_dispatch_e(Ctx& c, const Matrix& m, const double* x, double* y,
   SAG_LAUNCHED(c);
 }
 
-// TMA-staged CSR SpMV. The rows are cut into chunks of 2 x (256 / G)
-// consecutive rows; a persistent CTA streams its chunks' row offsets, column
-// indices and values into an nstage-deep shared-memory ring with
-// cp.async.bulk (one producer thread, L2 evict-first: K is read once per
-// product, x stays in L2), so the HBM stream no longer depends on how many
-// loads each thread keeps in flight. The 256 threads then compute the chunk
-// G lanes per row, both passes' x gathers issued before any product, and
-// release the stage to the producer. Ranges are rounded out to 16-byte
-// boundaries (the CSR arrays carry kTmaPad elements of slack).
-constexpr int kTmaPR = 2;  // rows per row-group per chunk
-struct TmaLayout {
-  int v_off, c_off, r_off, stage_bytes;
-};
-__host__ __device__ inline TmaLayout tma_layout(int rows, int slot_nnz) {
-  TmaLayout L;
-  const int vb = ((slot_nnz + 4) * 8 + 15) & ~15;
-  const int cb = ((slot_nnz + 8) * 4 + 15) & ~15;
-  const int rb = ((rows + 8) * 4 + 15) & ~15;
-  L.v_off = 0;
-  L.c_off = vb;
-  L.r_off = vb + cb;
-  L.stage_bytes = vb + cb + rb;
-  return L;
-}
-
-template <int G, Epi E>
-__global__ void __launch_bounds__(256) spmv_tma_kernel(
-    int nrows, int nchunks, int slot_nnz, int nstage, const int* __restrict__ rp,
-    const int* __restrict__ ci, const double* __restrict__ val, const double* __restrict__ x,
-    double* __restrict__ y, SpmvArgs a, double* partials, unsigned* ticket) {
-  if (a.gate && *a.gate) return;
-  constexpr bool kRed = (E == Epi::StoreDot || E == Epi::ResidSsq);
-  constexpr int RPP = 256 / G;  // rows per pass
-  constexpr int rows = kTmaPR * RPP;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const TmaLayout L = tma_layout(rows, slot_nnz);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)nstage * L.stage_bytes);
-  const int tid = threadIdx.x, sub = tid & (G - 1), grp = tid / G;
-  uint64_t policy = 0;
-  auto issue = [&](int s, int ch, int k0, int k1) {
-    unsigned char* st = smem + (size_t)s * L.stage_bytes;
-    const int r0 = ch * rows, r1 = min(r0 + rows, nrows);
-    const int kv0 = k0 & ~1, kv1 = (k1 + 1) & ~1;
-    const int kc0 = k0 & ~3, kc1 = (k1 + 3) & ~3;
-    const int rr0 = r0 & ~3, rr1 = (r1 + 4) & ~3;  // rp[r0..r1] inclusive
-    const unsigned bv = (unsigned)(kv1 - kv0) * 8u, bc = (unsigned)(kc1 - kc0) * 4u,
-                   br = (unsigned)(rr1 - rr0) * 4u;
-    mbar_expect_tx(bars + s, bv + bc + br);
-    if (bv) bulk_copy_hint(st + L.v_off, val + kv0, bv, bars + s, policy);
-    if (bc) bulk_copy_hint(st + L.c_off, ci + kc0, bc, bars + s, policy);
-    bulk_copy_hint(st + L.r_off, rp + rr0, br, bars + s, policy);
-  };
-  if (tid == 0) {
-    policy = evict_first_policy();
-    for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
-    mbar_init_fence();
-    for (int s = 0; s < nstage; ++s) {
-      const int ch = blockIdx.x + s * gridDim.x;
-      if (ch < nchunks) issue(s, ch, __ldg(rp + ch * rows), __ldg(rp + min(ch * rows + rows, nrows)));
-    }
-  }
-  __syncthreads();
-  double red = 0.0;
-  int it = 0;
-  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x, ++it) {
-    const int s = it % nstage;
-    // offsets of the chunk that refills this stage, loaded before the compute
-    const int cr = ch + nstage * gridDim.x;
-    int rk0 = 0, rk1 = 0;
-    if (tid == 0 && cr < nchunks) {
-      rk0 = __ldg(rp + cr * rows);
-      rk1 = __ldg(rp + min(cr * rows + rows, nrows));
-    }
-    const int r0 = ch * rows, r1 = min(r0 + rows, nrows);
-    double pre[kTmaPR];
-#pragma unroll
-    for (int p = 0; p < kTmaPR; ++p) pre[p] = spmv_pre<E>(a, y, r0 + p * RPP + grp, sub == 0 && r0 + p * RPP + grp < r1);
-    mbar_wait(bars + s, (unsigned)((it / nstage) & 1));
-    const unsigned char* st = smem + (size_t)s * L.stage_bytes;
-    const double* sv = reinterpret_cast<const double*>(st + L.v_off);
-    const int* sc = reinterpret_cast<const int*>(st + L.c_off);
-    const int* sr = reinterpret_cast<const int*>(st + L.r_off);
-    const int rr0 = r0 & ~3;
-    const int k0 = sr[r0 - rr0];
-    const int kv0 = k0 & ~1, kc0 = k0 & ~3;
-    int beg[kTmaPR], end[kTmaPR];
-    double vv[kTmaPR][4], xv[kTmaPR][4];
-#pragma unroll
-    for (int p = 0; p < kTmaPR; ++p) {
-      const int row = r0 + p * RPP + grp;
-      beg[p] = end[p] = 0;
-      if (row < r1) {
-        beg[p] = sr[row - rr0];
-        end[p] = sr[row + 1 - rr0];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k = beg[p] + sub + u * G;
-        const bool in = k < end[p];
-        vv[p][u] = in ? sv[k - kv0] : 0.0;
-        xv[p][u] = in ? __ldg(x + sc[k - kc0]) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < kTmaPR; ++p) {
-      double acc = 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc = fma(vv[p][u], xv[p][u], acc);
-      for (int k = beg[p] + sub + 4 * G; k < end[p]; k += G)
-        acc = fma(sv[k - kv0], __ldg(x + sc[k - kc0]), acc);
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
-      const int row = r0 + p * RPP + grp;
-      if (sub == 0 && row < r1) spmv_epi<E>(a, y, row, acc, pre[p], red);
-    }
-    __syncthreads();
-    if (tid == 0 && cr < nchunks) {
-      fence_proxy_async();
-      issue(s, cr, rk0, rk1);
-    }
-  }
-  if constexpr (kRed) reduce_finish(red, a.fin, partials, ticket);
-}
-
-template <int G>
-static void spmv_tma_dispatch(Ctx& c, const Matrix& m, const double* x, double* y, Epi e,
-                              const SpmvArgs& a) {
-  const TmaLayout L = tma_layout(kTmaPR * 256 / G, m.tma_slot_nnz);
-  const int smem = m.tma_stages * L.stage_bytes + m.tma_stages * 8;
-  auto grid_of = [&](auto kern) {
-    // the smem opt-in is per kernel: only ever raise it (matrices differ)
-    static thread_local int configured[6] = {0, 0, 0, 0, 0, 0};
-    int& cf = configured[static_cast<int>(e)];
-    if (cf < smem) {
-      SAG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cf = smem;
-    }
-    int& o = m.tma_occ[static_cast<int>(e)];
-    if (!o) {
-      SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, smem));
-      o = std::max(o, 1);
-    }
-    const long long cap = std::min<long long>((long long)o * c.num_sms, kMaxRedGrid);
-    return (int)std::max(1LL, std::min<long long>(m.nchunks, cap));
-  };
-  switch (e) {
-#define CASE(EE)                                                                              \
-  case Epi::EE:                                                                               \
-    spmv_tma_kernel<G, Epi::EE><<<grid_of(spmv_tma_kernel<G, Epi::EE>), 256, smem, c.stream>>>( \
-        m.nrows, m.nchunks, m.tma_slot_nnz, m.tma_stages, m.rp.p, m.ci.p, m.v.p, x, y, a,       \
-        c.partials.p, c.ticket.p);                                                            \
-    break;
-    CASE(Store)
-    CASE(Resid)
-    CASE(ResidEta)
-    CASE(Add)
-    CASE(StoreDot)
-    CASE(ResidSsq)
-#undef CASE
-  }
-  SAG_LAUNCHED(c);
-}
-
-// Chunking for the TMA-staged kernel (rows per chunk fixed by the lane group;
-// stage size = the largest chunk). SAG_SPMV_TMA=0 keeps the register kernel.
-void build_chunks(Ctx& c, Matrix& m) {
-  m.nchunks = 0;
-  m.tma_rows = 0;
-  for (int& o : m.tma_occ) o = 0;
-  if (m.nrows == 0 || m.nnz == 0) return;
-  // opt-in: on K0 it measures the same as the register kernel (the LSU data
-  // pipe, shared by the staged loads and the x gathers, is the limit)
-  const char* e = getenv("SAG_SPMV_TMA");
-  if (!e || atoi(e) == 0) return;
-  std::vector<int> rp(m.nrows + 1);
-  SAG_CUDA(cudaMemcpyAsync(rp.data(), m.rp.p, sizeof(int) * (m.nrows + 1), cudaMemcpyDeviceToHost,
-                           c.stream));
-  SAG_CUDA(cudaStreamSynchronize(c.stream));
-  const int rows = kTmaPR * 256 / m.group;
-  const int nch = (m.nrows + rows - 1) / rows;
-  int slot = 0;
-  for (int ch = 0; ch < nch; ++ch)
-    slot = std::max(slot, rp[std::min(ch * rows + rows, m.nrows)] - rp[ch * rows]);
-  const TmaLayout L = tma_layout(rows, slot);
-  const char* es = getenv("SAG_SPMV_TMA_SMEM");
-  const int budget = es ? atoi(es) : 56 * 1024;
-  const int stages = std::min(4, budget / L.stage_bytes);
-  if (stages < 2) return;  // rows too long to stage two chunks: register kernel
-  m.tma_rows = rows;
-  m.tma_slot_nnz = slot;
-  m.tma_stages = stages;
-  m.nchunks = nch;
-}
-
 void launch_spmv(Ctx& c, const Matrix& m, const double* x, double* y, Epi e, const SpmvArgs& a) {
   if (m.nrows == 0) return;
-  if (m.nchunks > 0) {
-    switch (m.group) {
-      case 2: spmv_tma_dispatch<2>(c, m, x, y, e, a); break;
-      case 4: spmv_tma_dispatch<4>(c, m, x, y, e, a); break;
-      case 8: spmv_tma_dispatch<8>(c, m, x, y, e, a); break;
-      case 16: spmv_tma_dispatch<16>(c, m, x, y, e, a); break;
-      default: spmv_tma_dispatch<32>(c, m, x, y, e, a); break;
-    }
-    return;
-  }
   switch (m.group) {
     case 2: spmv_dispatch_e<2>(c, m, x, y, e, a); break;
     case 4: spmv_dispatch_e<4>(c, m, x, y, e, a); break;
@@ -1002,9 +804,9 @@ std::unique_ptr<Matrix> transpose_dev(Ctx& c, const Matrix& a) {
   t->nrows = a.ncols;
   t->ncols = a.nrows;
   t->nnz = a.nnz;
-  t->rp.alloc(a.ncols + 1 + kTmaPad);
-  t->ci.alloc(a.nnz + kTmaPad);
-  t->v.alloc(a.nnz + kTmaPad);
+  t->rp.alloc(a.ncols + 1 + kCsrPad);
+  t->ci.alloc(a.nnz + kCsrPad);
+  t->v.alloc(a.nnz + kCsrPad);
   const long long n = a.nnz;
   DevBuf<int> row_of(n), idx(n), keys_out(n), perm(n), cnt(a.ncols + 1);
   const int g = ew_grid(c, n);
@@ -1027,7 +829,6 @@ std::unique_ptr<Matrix> transpose_dev(Ctx& c, const Matrix& a) {
   SAG_LAUNCHED(c);
   SAG_CUDA(cudaStreamSynchronize(c.stream));
   t->group = pick_group(t->nnz, t->nrows);
-  build_chunks(c, *t);
   return t;
 }
 
@@ -1042,9 +843,9 @@ std::unique_ptr<Matrix> matrix_upload(Ctx& c, int nrows, int ncols, long long nn
   m->nrows = nrows;
   m->ncols = ncols;
   m->nnz = nnz;
-  m->rp.alloc(nrows + 1 + kTmaPad);
-  m->ci.alloc(nnz + kTmaPad);
-  m->v.alloc(nnz + kTmaPad);
+  m->rp.alloc(nrows + 1 + kCsrPad);
+  m->ci.alloc(nnz + kCsrPad);
+  m->v.alloc(nnz + kCsrPad);
   SAG_CUDA(cudaMemcpyAsync(m->rp.p, rp, sizeof(int) * (nrows + 1), cudaMemcpyDefault, c.stream));
   if (nnz) {
     SAG_CUDA(cudaMemcpyAsync(m->ci.p, ci, sizeof(int) * nnz, cudaMemcpyDefault, c.stream));
@@ -1068,7 +869,6 @@ std::unique_ptr<Matrix> matrix_upload(Ctx& c, int nrows, int ncols, long long nn
   SAG_REQUIRE(!(hb & 4), SAG_ERROR,
               "sag_matrix_create: rows must be canonical (strictly increasing columns)");
   m->group = pick_group(nnz, nrows);
-  build_chunks(c, *m);
   return m;
 }
 

@@ -727,7 +727,11 @@ static void jacobi_fgmres2(Ctx& c, ScalarH& t, int l, const double* b, double* x
     r = b;
   } else {
     // post-smoothing follows the pre-smoothing of the same b on this level's
-    // KState, whose ref = ||b|| is still in place (same value, no pass)
+    // KState, whose ref = ||b|| is still in place (same value, no pass).
+    // Invariant: only scalar_level calls this with x_zero = false, right
+    // after the x_zero = true call on the same level and b. With tol = 0 the
+    // value of ref only matters as a positive number, and FIN_BETA falls
+    // back to 1 when it was never set.
     SpmvArgs a;
     a.b = b;
     a.fin = fb;
@@ -1491,6 +1495,18 @@ int sag_dc_destroy(sag_dc* d) {
   });
 }
 
+// Every setter that changes what a captured graph computes (parameters baked
+// into kernel arguments by value, buffers re-allocated) drops both graphs:
+// the standalone apply graph and the whole-solve graph.
+static void invalidate_graphs(Dc& d) {
+  if (d.ctx) SAG_CUDA(cudaStreamSynchronize(d.ctx->stream));  // nothing in flight uses them
+  d.graph_ok = false;
+  if (d.solve_graph.exec) {
+    cudaGraphExecDestroy(d.solve_graph.exec);
+    d.solve_graph.exec = nullptr;
+  }
+}
+
 int sag_dc_set_coarse_pin(sag_ctx* ctx, sag_dc* h, double level0_norm_inf) {
   return guard([&] {
     SAG_NOTNULL(ctx);
@@ -1501,8 +1517,8 @@ int sag_dc_set_coarse_pin(sag_ctx* ctx, sag_dc* h, double level0_norm_inf) {
     Level& B = d.lv.back();
     // preconditioner.cpp:49-53 with the norm of the hierarchy's finest level
     // supplied by the caller (a rank holding only the coarse levels)
+    invalidate_graphs(d);
     d.coarse.setup(ctx->c, *B.K, B.n_x + B.n_y, 1e-12 * level0_norm_inf);
-    d.graph_ok = false;
   });
 }
 
@@ -1515,7 +1531,7 @@ int sag_dc_set_parameters(sag_dc* h, double eta_u, double eta_p, double omega0) 
     c.omega0 = omega0;
     check_config(c);
     h->d.cfg = c;
-    h->d.graph_ok = false;
+    invalidate_graphs(h->d);
   });
 }
 
@@ -1544,8 +1560,8 @@ int sag_dc_set_sv_transfer(sag_dc* h, const sag_matrix* p_dup, const sag_matrix*
     t->rhs.alloc(n_p1);
     t->fail.alloc(1);
     SAG_CUDA(cudaMemsetAsync(t->fail.p, 0, sizeof(int), c.stream));
+    invalidate_graphs(d);
     d.svt = std::move(t);
-    d.graph_ok = false;
   });
 }
 

@@ -316,7 +316,6 @@ struct FactorOut {
   unsigned char* blob = nullptr;
   const long long* hoff = nullptr;
   const int* sbase = nullptr;
-  int tps = 0;  // streamed thread-per-patch section order
   int pairs = 0;  // paired blob layout for qualifying patches (vanka_paired)
 };
 
@@ -394,7 +393,7 @@ __global__ void __launch_bounds__(256) factor_kernel(
     int urx, ury;
     // paired blob: (A_x,A_y) | (U_x,U_y) | (B_x,B_y) interleaved, then S^-1;
     // sa/su = element strides of the A and U sections
-    const bool pr = !fo.tps && vanka_paired(fo.pairs != 0, nx, ny, np);
+    const bool pr = vanka_paired(fo.pairs != 0, nx, ny, np);
     const long long sa = pr ? 2 : es, su = pr ? 2 : es;
     if (pr) {
       const int m = nx > ny ? nx : ny;
@@ -410,15 +409,6 @@ __global__ void __launch_bounds__(256) factor_kernel(
         for (long long e = lane; e < vanka_paired_doubles(m, np) - (long long)np * np; e += 32)
           gAx[e] = 0.0;
       __syncwarp();
-    } else if (fo.tps) {
-      gB = fo.D + db;
-      gS = gB + (long long)np * nv * es;
-      gAx = gS + (long long)np * np * es;
-      gUx = gAx + ainv_len(nx, sym) * es;
-      gAy = gUx + (long long)np * nx * es;
-      gUy = gAy + ainv_len(ny, sym) * es;
-      urx = nx;
-      ury = ny;
     } else {
       gAx = fo.D + db;
       gAy = gAx + ainv_len(nx, sym) * es;
@@ -654,7 +644,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   }
   auto ndbl = [&](int i) {
     const long long nv = f->h_nv[i], npp = f->h_np[i], x = f->h_nx[i], y = nv - x;
-    if (!f->tpp && vanka_paired(f->pairs, (int)x, (int)y, (int)npp))
+    if (vanka_paired(f->pairs, (int)x, (int)y, (int)npp))
       return vanka_paired_doubles((int)std::max(x, y), (int)npp);
     return ainv_len(x, sym) + ainv_len(y, sym) + 2 * nv * npp + npp * npp;
   };
@@ -663,9 +653,6 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   std::vector<long long> h_hoff;  // blob byte offset per patch id
   std::vector<int> sbase(std::max(np_, 1), 0);
   long long slots = 0;
-  f->tpp = sym && p.max_dim <= kTppMaxDim && p.max_np <= 4 && np_ > 0 &&
-           env_int("SAG_VANKA_TPP", 0) != 0;
-  if (f->tpp) f->pairs = false;
   // a level is paired only if every patch is (one kernel path per level)
   for (int i = 0; i < np_ && f->pairs; ++i) {
     const int x = f->h_nx[i], y = f->h_nv[i] - x;
@@ -673,63 +660,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     f->pair_rows = std::max(f->pair_rows, std::max(x, y) + f->h_np[i]);
   }
   if (!f->pairs) f->pair_rows = 0;
-  if (f->tpp) {
-    // thread-per-patch layout: patches sorted (stably) by shape, buckets of 32
-    // equal-shape patches, every payload entry interleaved across the bucket
-    std::vector<int> order(np_);
-    for (int i = 0; i < np_; ++i) order[i] = i;
-    auto key = [&](int i) {
-      const int x = f->h_nx[i], y = f->h_nv[i] - x;
-      const int nm = tpp_class(std::max(x, y));
-      return (((long long)nm * 256 + x) * 256 + y) * 8 + f->h_np[i];
-    };
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
-    std::vector<BucketHdr> hdr;
-    long long doff = 0, ioff = 0;
-    for (int s = 0; s < np_;) {
-      const int i0 = order[s];
-      int e = s + 1;
-      while (e < np_ && e - s < 32 && key(order[e]) == key(i0)) ++e;
-      BucketHdr h;
-      h.nx = f->h_nx[i0];
-      h.ny = f->h_nv[i0] - h.nx;
-      h.np = f->h_np[i0];
-      h.count = e - s;
-      h.dbl_off = doff;
-      h.int_off = ioff;
-      h.slot_off = (int)slots;
-      h.nm = tpp_class(std::max(h.nx, h.ny));
-      for (int q = s; q < e; ++q) {
-        const int i = order[q], lane = q - s;
-        f->h_dbase[i] = doff + lane;
-        f->h_ibase[i] = ioff + lane;
-        sbase[i] = (int)slots + lane;
-      }
-      doff += 32 * ndbl(i0);
-      ioff += 32LL * (f->h_nv[i0] + h.np);
-      slots += 32LL * (f->h_nv[i0] + h.np);
-      SAG_REQUIRE(slots < (1LL << 31), SAG_DIMENSION_MISMATCH, "factor_patches: too many slots");
-      hdr.push_back(h);
-      s = e;
-    }
-    f->nbuckets = (int)hdr.size();
-    for (int b = 0; b < f->nbuckets;) {
-      int e = b;
-      while (e < f->nbuckets && hdr[e].nm == hdr[b].nm) ++e;
-      f->classes.push_back({hdr[b].nm, b, e});
-      b = e;
-    }
-    f->hdr.alloc(hdr.size());
-    SAG_CUDA(cudaMemcpyAsync(f->hdr.p, hdr.data(), sizeof(BucketHdr) * hdr.size(),
-                             cudaMemcpyHostToDevice, c.stream));
-    f->D.alloc(std::max(doff, 1LL));
-    f->I.alloc(std::max(ioff, 1LL));
-    f->B.alloc(std::max(ioff, 1LL));  // gathered r, same interleaving as I and the slots
-    // padding lanes of partial buckets stay finite / in range
-    SAG_CUDA(cudaMemsetAsync(f->D.p, 0, sizeof(double) * f->D.n, c.stream));
-    SAG_CUDA(cudaMemsetAsync(f->I.p, 0, sizeof(int) * f->I.n, c.stream));
-    f->blob_bytes = 8 * doff + 4 * ioff;
-  } else {
+  {
     // size classes: the rows per lane the apply needs (paired: m + np, else
     // max(nx, ny)) -> R = ceil(rows / 32). Blobs are stored class by class
     // (stable in patch order), so each class is one contiguous launch with
@@ -776,6 +707,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
       auto& cl = f->rclasses.back();
       cl.k1 = q + 1;
       cl.slot_bytes = std::max<long long>(cl.slot_bytes, bytes);
+      cl.bytes += bytes;
     }
     for (int i = 0; i < np_; ++i) {
       sbase[i] = (int)slots;
@@ -799,7 +731,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     SAG_CUDA(cudaMemcpyAsync(dibase.p, f->h_ibase.data(), sizeof(long long) * np_,
                              cudaMemcpyHostToDevice, c.stream));
   }
-  const int es = f->tpp ? 32 : 1;
+  const int es = 1;
 
   // dof -> slot map (stable sort of slot ids by dof) and PoU weights
   const int n = k.nrows;
@@ -852,11 +784,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     fo.dbase = ddbase.p;
     fo.ibase = dibase.p;
     fo.sbase = dsbase.p;
-    if (f->tpp) {
-      fo.D = f->D.p;
-      fo.I = f->I.p;
-      fo.tps = 1;
-    } else {
+    {
       fo.D = reinterpret_cast<double*>(f->blob.p);
       fo.I = reinterpret_cast<int*>(f->blob.p);
       fo.blob = f->blob.p;
@@ -1525,316 +1453,6 @@ static void launch_gather(Ctx& c, const Vanka& f, double* delta, double* xadd, d
   SAG_LAUNCHED(c);
 }
 
-// -------------------------------------- streamed thread-per-patch apply --
-// Thread-per-patch Vanka over shape buckets (layout in internal.cuh, TPPS
-// section order Bh | S^-1 | A_x^-1 | U_x | A_y^-1 | U_y, entries interleaved
-// across the 32 patches of a bucket). One warp per CTA streams its buckets'
-// payload through a 4-chunk shared-memory ring (8 KB cp.async.bulk copies,
-// L2 evict-first) and lane l solves patch l with r, t and x_p in registers:
-// every stored entry of A^-1 is read once from shared memory
-// (t_i += a_ij b_j, t_j += a_ij b_i). ~1/10 of the warp-per-patch kernel's
-// instructions; the r gathers of the next bucket are issued one bucket ahead.
-constexpr int kTpsCE = 32;                   // entries per chunk (x 32 lanes x 8 B = 8 KB)
-constexpr int kTpsRing = 4;                  // chunks in the ring
-constexpr int kTpsRingE = kTpsCE * kTpsRing; // 128 entries
-
-__host__ __device__ inline int tps_entries(int nx, int ny, int np) {
-  const int nv = nx + ny;
-  return np * nv + np * np + nx * (nx + 1) / 2 + np * nx + ny * (ny + 1) / 2 + np * ny;
-}
-
-// r at every slot of the thread-per-patch layout (slot s of bucket lane l,
-// entry e = the dof I[s]): the patch gathers become one coalesced stream that
-// the apply kernel bulk-copies like the factor payload.
-__global__ void vanka_pregather_kernel(long long n, const int* __restrict__ I,
-                                       const double* __restrict__ r, double* __restrict__ B,
-                                       const int* gate) {
-  if (gate && *gate) return;
-  for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < n;
-       s += (long long)gridDim.x * blockDim.x)
-    B[s] = __ldg(r + __ldcs(I + s));
-}
-
-// Producer side of the per-warp chunk stream. It runs once per 8 KB chunk, so
-// it lives out of line (local-memory state) and keeps the solve loop small.
-struct TpsProducer {
-  int ib, ic, issued, b1, nw;
-  BucketHdr hi, hn;
-  const BucketHdr* hdr;
-  const double* D;
-  const double* B;
-  double* ring;
-  uint64_t* bars;
-  uint64_t policy;
-};
-
-// A bucket's stream: its gathered r values (nv + np entries, from B) padded
-// to whole chunks, then its factor payload (tps_entries, from D).
-__device__ __noinline__ void tps_issue(TpsProducer& p, int lane) {
-  if (p.ib >= p.b1) return;
-  const BucketHdr& h = p.hi;
-  const int nb = h.nx + h.ny + h.np;
-  const int nchb = (nb + kTpsCE - 1) / kTpsCE;
-  const int E = tps_entries(h.nx, h.ny, h.np);
-  const int nch = nchb + (E + kTpsCE - 1) / kTpsCE;
-  const double* src;
-  int ecount;
-  if (p.ic < nchb) {
-    src = p.B + h.slot_off + (long long)p.ic * kTpsCE * 32;
-    ecount = min(kTpsCE, nb - p.ic * kTpsCE);
-  } else {
-    const int icd = p.ic - nchb;
-    src = p.D + h.dbl_off + (long long)icd * kTpsCE * 32;
-    ecount = min(kTpsCE, E - icd * kTpsCE);
-  }
-  __syncwarp();
-  if (lane == 0) {
-    const int slot = p.issued % kTpsRing;
-    const unsigned bytes = (unsigned)ecount * 32u * 8u;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(p.bars + slot)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(p.ring + (size_t)slot * kTpsCE * 32)),
-        "l"(src), "r"(bytes), "r"(smem_u32(p.bars + slot)), "l"(p.policy)
-        : "memory");
-  }
-  ++p.issued;
-  if (++p.ic == nch) {
-    p.ic = 0;
-    p.ib += p.nw;
-    p.hi = p.hn;
-    p.hn = p.hdr[min(p.ib + p.nw, p.b1 - 1)];
-  }
-}
-
-// Waits until chunk `need` (global index) has landed; each landed chunk
-// releases the slot two chunks back, refilled two chunks ahead.
-__device__ __noinline__ int tps_advance(TpsProducer& p, int landed, int need, int lane) {
-  while (landed <= need) {
-    mbar_wait(p.bars + landed % kTpsRing, (unsigned)((landed / kTpsRing) & 1));
-    ++landed;
-    tps_issue(p, lane);
-  }
-  return landed;
-}
-
-// case lists for the NM = 20 thread-per-patch kernel
-#define SAG_CASES20(X) X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) \
-  X(13) X(14) X(15) X(16) X(17) X(18) X(19)
-#define SAG_ROWS19(X) X(18) X(17) X(16) X(15) X(14) X(13) X(12) X(11) X(10) X(9) X(8) X(7) \
-  X(6) X(5) X(4) X(3) X(2) X(1) X(0)
-
-// NPM: upper bound on pressure seeds per patch (1 for TH / ISO, 4 general).
-template <int NM, int NPM>
-__global__ void __launch_bounds__(32) vanka_tps_kernel(int b0, int b1,
-                                                       const BucketHdr* __restrict__ hdr,
-                                                       const double* __restrict__ D,
-                                                       const double* __restrict__ B,
-                                                       double* __restrict__ out, const int* gate) {
-  static_assert(NM == 20, "case lists are written for NM = 20");
-  if (gate && *gate) return;
-  extern __shared__ __align__(128) unsigned char smem[];
-  double* ring = reinterpret_cast<double*>(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kTpsRingE * 32);
-  const int lane = threadIdx.x;
-  TpsProducer P;
-  P.ib = b0 + blockIdx.x;
-  P.ic = 0;
-  P.issued = 0;
-  P.b1 = b1;
-  P.nw = gridDim.x;
-  P.hdr = hdr;
-  P.D = D;
-  P.B = B;
-  P.ring = ring;
-  P.bars = bars;
-  P.hi = hdr[min(P.ib, b1 - 1)];
-  P.hn = hdr[min(P.ib + P.nw, b1 - 1)];
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(P.policy));
-  if (lane == 0) {
-    for (int s = 0; s < kTpsRing; ++s) mbar_init(bars + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  tps_issue(P, lane);
-  tps_issue(P, lane);
-  int landed = 0;  // chunks waited so far
-  int gbase = 0;   // first chunk (global index) of the current bucket
-  const int nw = gridDim.x;
-  BucketHdr hc = hdr[min(b0 + (int)blockIdx.x, b1 - 1)];
-  for (int b = b0 + blockIdx.x; b < b1; b += nw) {
-    const BucketHdr h = hc;
-    hc = hdr[min(b + nw, b1 - 1)];  // prefetch the next bucket's header
-    const int nx = h.nx, ny = h.ny, np = NPM == 1 ? 1 : h.np, nv = nx + ny;
-    const int nchb = (nv + np + kTpsCE - 1) / kTpsCE;
-    const int Pp = nchb * kTpsCE;  // payload entries start here (bucket-local)
-    const int E = tps_entries(nx, ny, np);
-    const bool act = lane < h.count;
-    double* o = out + h.slot_off + lane;
-    // every entry up to e_last (bucket-local) resident; callers never span
-    // more than two chunks
-#define SAG_ENSURE(e_last)                                              \
-  do {                                                                  \
-    const int need_ = gbase + (e_last) / kTpsCE;                        \
-    if (need_ >= landed) landed = tps_advance(P, landed, need_, lane);  \
-  } while (0)
-    const int g0 = gbase * kTpsCE;
-    auto ent = [&](int e) -> double { return ring[((g0 + e) & (kTpsRingE - 1)) * 32 + lane]; };
-    // r at the patch dofs (vanka.cpp:161-162)
-    double bx[NM], by[NM], bp[NPM];
-    SAG_ENSURE(nv + np - 1);
-#pragma unroll
-    for (int j = 0; j < NM; ++j) {
-      bx[j] = j < nx ? ent(j) : 0.0;
-      by[j] = j < ny ? ent(nx + j) : 0.0;
-    }
-#pragma unroll
-    for (int a = 0; a < NPM; ++a) bp[a] = a < np ? ent(nv + a) : 0.0;
-    const int oSi = Pp + np * nv, oAx = oSi + np * np;
-    const int oUx = oAx + nx * (nx + 1) / 2, oAy = oUx + np * nx;
-    const int oUy = oAy + ny * (ny + 1) / 2;
-    // x_p = S^-1 b_p + B_hat b_u (vanka.cpp:168-174)
-    double xp[NPM];
-#pragma unroll
-    for (int a = 0; a < NPM; ++a) {
-      xp[a] = 0.0;
-      if (a < np) {
-        double s = 0.0;
-        if (nx > 0) SAG_ENSURE(Pp + a * nv + nx - 1);
-#pragma unroll
-        for (int j = 0; j < NM; ++j)
-          if (j < nx) s = fma(ent(Pp + a * nv + j), bx[j], s);
-        if (ny > 0) SAG_ENSURE(Pp + a * nv + nv - 1);
-#pragma unroll
-        for (int j = 0; j < NM; ++j)
-          if (j < ny) s = fma(ent(Pp + a * nv + nx + j), by[j], s);
-        SAG_ENSURE(oSi + a * np + np - 1);
-#pragma unroll
-        for (int q = 0; q < NPM; ++q)
-          if (q < np) s = fma(ent(oSi + a * np + q), bp[q], s);
-        xp[a] = s;
-        if (act) o[32 * (nv + a)] = s;
-      }
-    }
-    // t = A^-1 b_u, x_u = t + U_hat x_p, per component (vanka.cpp:164-180)
-#pragma unroll
-    for (int comp = 0; comp < 2; ++comp) {
-      const int n = comp == 0 ? nx : ny;
-      const int oA = comp == 0 ? oAx : oAy;
-      const int oU = comp == 0 ? oUx : oUy;
-      const double(&bb)[NM] = comp == 0 ? bx : by;
-      double* oc = o + (comp == 0 ? 0 : 32 * nx);
-      double t[NM];
-#pragma unroll
-      for (int i = 0; i < NM; ++i) t[i] = 0.0;
-      // Column loop at run time, rows unrolled through a Duff-style switch:
-      // the code stays small (a fully unrolled triangle was 27k SASS
-      // instructions and thrashed the instruction cache).
-      for (int j = 0; j < n; ++j) {
-        const int cj = oA + j * (j + 1) / 2;
-        SAG_ENSURE(cj + j);
-        const int p0 = (g0 + cj) & (kTpsRingE - 1);
-        double bj = 0.0;
-        switch (j) {
-#define SAG_PICK(J) \
-  case J:           \
-    bj = bb[J];     \
-    break;
-          SAG_CASES20(SAG_PICK)
-#undef SAG_PICK
-        }
-        double acc = 0.0, ajj;
-        if (p0 + j < kTpsRingE) {  // the column is contiguous in the ring
-          const double* pc = ring + p0 * 32 + lane;
-          ajj = pc[j * 32];
-          switch (j) {  // rows j-1 .. 0
-#define SAG_ROW(I)                 \
-  case (I) + 1: {                  \
-    const double a = pc[(I) * 32]; \
-    t[I] = fma(a, bj, t[I]);       \
-    acc = fma(a, bb[I], acc);      \
-  }
-            SAG_ROWS19(SAG_ROW)
-#undef SAG_ROW
-            default:
-              break;
-          }
-        } else {  // the column wraps around the ring end
-          ajj = ring[((p0 + j) & (kTpsRingE - 1)) * 32 + lane];
-          switch (j) {
-#define SAG_ROW(I)                                                     \
-  case (I) + 1: {                                                      \
-    const double a = ring[((p0 + (I)) & (kTpsRingE - 1)) * 32 + lane]; \
-    t[I] = fma(a, bj, t[I]);                                           \
-    acc = fma(a, bb[I], acc);                                          \
-  }
-            SAG_ROWS19(SAG_ROW)
-#undef SAG_ROW
-            default:
-              break;
-          }
-        }
-        const double add = fma(ajj, bj, acc);
-        switch (j) {
-#define SAG_ADD(J) \
-  case J:          \
-    t[J] += add;   \
-    break;
-          SAG_CASES20(SAG_ADD)
-#undef SAG_ADD
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < NPM; ++a) {
-        if (a < np && n > 0) {
-          SAG_ENSURE(oU + a * n + n - 1);
-#pragma unroll
-          for (int i = 0; i < NM; ++i)
-            if (i < n) t[i] = fma(ent(oU + a * n + i), xp[a], t[i]);
-        }
-      }
-      if (act) {
-#pragma unroll
-        for (int i = 0; i < NM; ++i)
-          if (i < n) oc[32 * i] = t[i];
-      }
-    }
-    SAG_ENSURE(Pp + E - 1);  // every chunk of this bucket has landed
-#undef SAG_ENSURE
-    gbase += nchb + (E + kTpsCE - 1) / kTpsCE;
-  }
-}
-
-template <int NM, int NPM>
-static void launch_tps(Ctx& c, const Vanka& f, int b0, int b1, const double* r, const int* gate) {
-  const int smem = kTpsRingE * 32 * 8 + kTpsRing * 8;
-  static thread_local int occ = 0;
-  if (!occ) {
-    SAG_CUDA(cudaFuncSetAttribute(vanka_tps_kernel<NM, NPM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, vanka_tps_kernel<NM, NPM>, 32, smem));
-    occ = std::max(occ, 1);
-  }
-  const long long cap = (long long)occ * c.num_sms;
-  const int ctas = (int)std::max(1LL, std::min<long long>(b1 - b0, cap));
-  vanka_tps_kernel<NM, NPM><<<ctas, 32, smem, c.stream>>>(b0, b1, f.hdr.p, f.D.p, f.B.p, f.out.p, gate);
-  SAG_LAUNCHED(c);
-}
-
-static void launch_tpp_all(Ctx& c, const Vanka& f, const double* r, const int* gate) {
-  vanka_pregather_kernel<<<grid_for(c, f.nslots), 256, 0, c.stream>>>(f.nslots, f.I.p, r, f.B.p,
-                                                                      gate);
-  SAG_LAUNCHED(c);
-  for (const auto& cl : f.classes) {
-    if (f.max_np <= 1)
-      launch_tps<20, 1>(c, f, cl.b0, cl.b1, r, gate);
-    else
-      launch_tps<20, 4>(c, f, cl.b0, cl.b1, r, gate);
-  }
-}
-
 struct ApplyCfg {
   int warps, nstage, sb_len, smem, blocks;
 };
@@ -1945,9 +1563,7 @@ static void launch_patch_r(Ctx& c, const Vanka& f, const double* r, const int* g
 static void launch_patch_any(Ctx& c, const Vanka& f, const double* r, const int* gate) {
   if (f.npatch == 0) return;
   const bool np1 = f.max_np <= 1;  // TH / ISO levels: one pressure seed
-  if (f.tpp)
-    launch_tpp_all(c, f, r, gate);
-  else if (f.sym && np1)
+  if (f.sym && np1)
     launch_patch_r<true, 1>(c, f, r, gate);
   else if (f.sym)
     launch_patch_r<true, 4>(c, f, r, gate);
@@ -1979,30 +1595,17 @@ void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, 
 // parity tests.
 void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* sinv,
                   double* weights) {
-  std::vector<double> D;
-  if (f.tpp) {
-    D.resize(f.D.n);
-    SAG_CUDA(cudaMemcpyAsync(D.data(), f.D.p, sizeof(double) * f.D.n, cudaMemcpyDeviceToHost, c.stream));
-  } else {
-    D.resize((f.blob_bytes + 7) / 8);
-    SAG_CUDA(cudaMemcpyAsync(D.data(), f.blob.p, f.blob_bytes, cudaMemcpyDeviceToHost, c.stream));
-  }
+  std::vector<double> D((f.blob_bytes + 7) / 8);
+  SAG_CUDA(cudaMemcpyAsync(D.data(), f.blob.p, f.blob_bytes, cudaMemcpyDeviceToHost, c.stream));
   SAG_CUDA(cudaStreamSynchronize(c.stream));
-  const long long es = f.tpp ? 32 : 1;
+  const long long es = 1;
   size_t ou = 0, os = 0;
   for (int k = 0; k < f.npatch; ++k) {
     const int nx = f.h_nx[k], nv = f.h_nv[k], ny = nv - nx, np = f.h_np[k];
     const double* base = D.data() + f.h_dbase[k];
     const double *Bh, *Si, *Ux, *Uy;
     long long urx, ury;
-    if (f.tpp) {  // B_hat | S^-1 | A_x | U_x | A_y | U_y
-      Bh = base;
-      Si = Bh + (long long)np * nv * es;
-      Ux = Si + (long long)np * np * es + ainv_len(nx, f.sym) * es;
-      Uy = Ux + (long long)np * nx * es + ainv_len(ny, f.sym) * es;
-      urx = nx;
-      ury = ny;
-    } else if (vanka_paired(f.pairs, nx, ny, np)) {  // (A) | (U) | (B) pairs | S^-1
+    if (vanka_paired(f.pairs, nx, ny, np)) {  // (A) | (U) | (B) pairs | S^-1
       const int m = std::max(nx, ny);
       const double* U2 = base + 2 * ainv_len(m, true);
       const double* B2 = U2 + 2LL * np * m;
@@ -2145,6 +1748,21 @@ int sag_vanka_stats(const sag_vanka* f, long long* s) {
     s[4] = v.npatch;
     s[5] = v.n;
     s[6] = v.nslots;
+  });
+}
+
+int sag_vanka_classes(const sag_vanka* f, long long* out, int cap, int* nclasses) {
+  return guard([&] {
+    SAG_NOTNULL(f);
+    SAG_NOTNULL(nclasses);
+    const auto& cls = f->f.rclasses;
+    *nclasses = (int)cls.size();
+    for (int i = 0; i < (int)cls.size() && i < cap; ++i) {
+      out[4 * i + 0] = cls[i].R;
+      out[4 * i + 1] = cls[i].lpp;
+      out[4 * i + 2] = cls[i].k1 - cls[i].k0;
+      out[4 * i + 3] = cls[i].bytes;
+    }
   });
 }
 

@@ -67,6 +67,10 @@ class Comm:
         self.dist.all_gather_object(out, obj)
         return out
 
+    def barrier(self):
+        if self.size > 1:
+            self.dist.barrier()
+
     def fence(self, flag):
         """Every rank's preceding work on its stream is complete before any
         rank's following work: NCCL -- an all-reduce of one element, ordered
@@ -395,6 +399,27 @@ class DistStep:
         if peer is None:
             peer = os.environ.get("SAG_P2P_HALO") == "1"
         self.peer = PeerHalo(rs, be, comm) if peer and comm.size > 1 else None
+
+    def close(self):
+        """Releases the peer-memory halo in the only safe order: a fence (no
+        rank's stores are in flight), every rank unmaps its neighbours'
+        buffers, a barrier (nobody still maps ours), then our receive buffers
+        are freed. Idempotent; also the context-manager exit."""
+        if self.peer is None:
+            return
+        self.comm.fence(self.peer.flag)
+        self.be.torch.cuda.synchronize(self.be.device)
+        self.peer.close()
+        self.comm.barrier()
+        self.peer.recv = []
+        self.peer = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
 
     def step(self, x, delta, y):
         """delta = apply_vanka(x), y = K0 x: interior patches and rows under

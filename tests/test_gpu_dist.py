@@ -77,8 +77,9 @@ def _worker(rank, world, port, n, backend, q):
             # a rank with ghost partial sums sent them from its boundary gathers
             # (fused path; the lowest rank owns every dof its patches touch)
             assert solver.peer.fused > 0 or not rs.rev_send
-            torch.cuda.synchronize(dev)
-            dist.barrier()  # no rank unmaps before its neighbour's last stores
+        # fence, unmap the neighbours' buffers, barrier, free ours
+        solver.close()
+        assert solver.peer is None
         q.put((rank, rs.l2g[own], x.cpu().numpy()[own], rep.iterations,
                rep.final_relative_residual, rep.converged, launches))
     finally:

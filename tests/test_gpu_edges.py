@@ -297,3 +297,29 @@ def test_uzawa_scalar_tail(S, monkeypatch):
         assert np.array_equal(z, prec.apply(r))
         launches[tail] = ctx.launch_count() - l0
     assert launches["all"] < launches["from1"] < launches["0"], launches
+
+
+# ------------------------------------------ parameter scan --
+def test_set_parameters_recaptures_solve_graph(S):
+    # parameter_scan (preconditioner.cpp:261-277): one preconditioner, its
+    # (eta_u, eta_p, omega0) changed between solves. Every scan point must
+    # solve with its own parameters -- the whole-solve CUDA graph captured for
+    # the previous point bakes them into kernel arguments and must be dropped.
+    c, d, k0, levels, conf = ref_case(16)
+    K0, dc, cfg = _device_dc(S, k0, d.nxyz0, levels, conf)
+    rhs = c.rhs()
+    x1, rep1 = S.solve_stokes(K0, rhs, dc, cfg)
+    points = [(0.5, 0.5, 0.8), (0.75, 0.75, 1.0), (1.0, 1.0, 1.0)]
+    for eu, ep, om in points:
+        dc.set_parameters(eu, ep, om)
+        x, rep = S.solve_stokes(K0, rhs, dc, cfg)
+        _, fresh, _ = _device_dc(S, k0, d.nxyz0, levels, conf)
+        fresh.set_parameters(eu, ep, om)
+        xf, repf = S.solve_stokes(K0, rhs, fresh, cfg)
+        assert rep.iterations == repf.iterations, (eu, ep, om)
+        assert np.array_equal(x, xf), (eu, ep, om)
+        d.set_parameters(eu, ep, om)
+        _, rr = d.solve(rhs)
+        assert abs(rep.iterations - rr["iterations"]) <= 1, (eu, ep, om, rr["iterations"])
+    # back at the first point: the first solve exactly
+    assert np.array_equal(x, x1) and rep.iterations == rep1.iterations

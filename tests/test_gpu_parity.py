@@ -399,22 +399,6 @@ def test_dropin_cpp_adapter_solve(S):
     assert rel_inf(x, x_ref) <= 1e-6
 
 
-def test_vanka_thread_per_patch_layout(S, monkeypatch):
-    # the opt-in bucketed thread-per-patch representation gives the same apply
-    monkeypatch.setenv("SAG_VANKA_TPP", "1")
-    c, d, k0, levels, _ = ref_case(32)
-    rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0)
-    K = S.SparseMatrix.from_csr(k0)
-    p = S.build_patches(K, *d.nxyz0)
-    f = S.factor_patches(K, p, d.nxyz0[0] + d.nxyz0[1])
-    r = O.splitmix64_uniform(k0.nrows)
-    assert rel_inf(S.apply_vanka(f, r), rv.apply(r)) <= TOL
-    got = f.export(p.export())
-    want = rv.factors()
-    for key in ("uhat", "bhat", "sinv", "weights"):
-        assert np.array_equal(got[key], want[key]), key
-
-
 @pytest.mark.parametrize("tail", ["0", "1"])
 def test_sv_scalar_tail(S, monkeypatch, tail):
     # the mass projection's scalar V(2,2) cycles with their small levels as one

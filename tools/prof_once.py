@@ -1,13 +1,16 @@
 #!/usr/bin/env python
-"""One launch of each hot kernel of the bench step on config 2's K0 (after one
-untimed warm-up round), for `ncu --set full` captures:
+"""Two rounds of the hot kernels of one level of a bench config (the first
+round warms up; ncu_traffic.py keeps the second), for ncu captures:
 
-    ncu --set full --import-source on --clock-control none -s <warm-up launches> \
-        -o gpurun_out/prof python tools/prof_once.py [n=512]
+    ncu --set full --import-source on --clock-control none \
+        -k regex:"spmv_kernel|vanka_patch_kernel|vanka_subwarp_kernel|vanka_gather" \
+        -o gpurun_out/prof python tools/prof_once.py --config 3 --level ISO0
 
-Order per round: spmv (Store), spmv (StoreDot), Vanka patch kernel, Vanka
-gather kernel.
+Order per round: spmv (Store), Vanka patch stage (one launch per size class),
+Vanka gather. --level K0 (default) or ISO0 (level 0 of the low-order
+hierarchy).
 """
+import argparse
 import os
 import sys
 
@@ -17,31 +20,36 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_2306_06795_b200 as S  # noqa: E402
-from paper_2306_06795_b200.cases import HostCase  # noqa: E402
-from bench import splitmix64_uniform  # noqa: E402
+import bench  # noqa: E402
 
 
 def main():
-    n_mesh = int(sys.argv[1]) if len(sys.argv) > 1 else 512
-    case = HostCase("cavity", False, "structured", n_mesh)
-    k0 = case.k0()
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--level", default="K0", choices=["K0", "ISO0"])
+    a = ap.parse_args()
+    case = bench.host_case(bench.CONFIGS[a.config])
+    if a.level == "K0":
+        k, nxyz, sv = case.k0(), case.nxyz0, case.sv
+    else:
+        k, _, nxyz = case.level(0)
+        sv = False
     ctx = S.Context(0)
     dev = torch.device("cuda", 0)
-    n = k0.nrows
-    x = torch.from_numpy(splitmix64_uniform(n)).to(dev)
+    n = k.nrows
+    x = torch.from_numpy(bench.splitmix64_uniform(n)).to(dev)
     y = torch.empty_like(x)
-    aux = torch.from_numpy(splitmix64_uniform(n, 7)).to(dev)
-    K = S.SparseMatrix.from_csr(k0, ctx)
-    p = S.build_patches(K, *case.nxyz0)
-    f = S.factor_patches(K, p, case.n_x0 + case.n_y0)
+    K = S.SparseMatrix.from_csr(k, ctx)
+    f = S.factor_patches(K, S.build_patches(K, *nxyz, sv_triples=sv), nxyz[0] + nxyz[1])
     lib = S.lib()
-    xp, yp, ap = (S.C.c_void_p(t.data_ptr()) for t in (x, y, aux))
+    xp, yp = (S.C.c_void_p(t.data_ptr()) for t in (x, y))
     for _ in range(2):
-        S._check(lib.sag_spmv_fused(ctx.h, K.h, xp, yp, ap, 0))
-        S._check(lib.sag_spmv_fused(ctx.h, K.h, xp, yp, ap, 3))
+        S._check(lib.sag_spmv_fused(ctx.h, K.h, xp, yp, None, 0))
         S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, yp, 1))
         S._check(lib.sag_apply_vanka_stage(ctx.h, f.h, xp, yp, 2))
         ctx.synchronize()
+    print({"config": a.config, "level": a.level, "rows": n, "classes": f.classes(),
+           "patch_bytes": bench.vanka_patch_bytes(f, n), "spmv_bytes": bench.spmv_bytes(n, n, k.nnz)})
 
 
 if __name__ == "__main__":
