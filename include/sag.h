@@ -330,6 +330,55 @@ int sag_saddle_matrix(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* b, sa
 int sag_matrix_export(sag_ctx* ctx, const sag_matrix* m, int* row_offsets, int* col_indices,
                       double* values);
 
+/* ---- FEM assembly on the device, bitwise the reference ---
+ * A 2D triangle mesh (mesh.hpp:24-43) as plain arrays: vertices (x, y) pairs,
+ * triangles (3 vertex ids each, positively oriented), tri_edges[t][k] = edge
+ * opposite local vertex k (may be NULL where no P2 space is built),
+ * num_edges = size of the lexicographic edge table. Arrays may be host or
+ * device memory. */
+typedef struct sag_mesh2d {
+  int num_vertices, num_triangles, num_edges;
+  const double* vertices;
+  const int* triangles;
+  const int* tri_edges;
+} sag_mesh2d;
+/* from_triplets (sparse.hpp:37; sparse.cpp:43-66): duplicates summed in the
+ * order libstdc++'s std::sort leaves them (reproduced on the device), exact
+ * zeros dropped. rows / cols / values: n entries in generation order. */
+int sag_from_triplets(sag_ctx* ctx, int nrows, int ncols, long long n, const int* rows,
+                      const int* cols, const double* values, sag_matrix** out);
+/* perm[i] = the original index of the element std::sort (comparator on the
+ * key only) places at position i of the n keys (test hook of the above);
+ * *heap_ranges (may be NULL) = ranges that reached introsort's depth limit. */
+int sag_sort_permutation(sag_ctx* ctx, long long n, const unsigned long long* keys, int* perm,
+                         int* heap_ranges);
+/* The P2 element loop of assemble_taylor_hood (sv = 0; fem.cpp:354-389) or
+ * assemble_scott_vogelius (sv = 1; fem.cpp:452-498): the full scalar
+ * Laplacian a_full (n_s x n_s, n_s = V + E) and divergence b_full (n_p x 2 n_s),
+ * the load fx, fy (length n_s; may be NULL) from force_qp = the body force at
+ * the 6 quadrature points of each triangle (f_x, f_y pairs, triangle-major;
+ * NULL = zero force), and for SV the element mass Mp, the mixed mass M_mix and
+ * the element areas (each may be NULL). */
+int sag_assemble_p2(sag_ctx* ctx, const sag_mesh2d* mesh, int sv, const double* force_qp,
+                    sag_matrix** a_full, sag_matrix** b_full, double* fx, double* fy,
+                    sag_matrix** mp, sag_matrix** m_mix, double* areas);
+/* assemble_p1_stiffness / assemble_p1_mass (fem.cpp:310-335); either may be NULL. */
+int sag_assemble_p1(sag_ctx* ctx, const sag_mesh2d* mesh, sag_matrix** stiffness,
+                    sag_matrix** mass);
+/* The fine-mesh element loop of assemble_iso (fem.cpp:568-608): a_full
+ * (nvf x nvf), b_fine (nvf x 2 nvf) and the load (may be NULL). */
+int sag_assemble_iso(sag_ctx* ctx, const sag_mesh2d* fine, const double* force_qp,
+                     sag_matrix** a_full, sag_matrix** b_fine, double* fx, double* fy);
+/* Dirichlet elimination: reduce_scalar (fem.cpp:207-229) of a_full and
+ * reduce_divergence (:233-252) of b_full (columns [x | y], scalar width n_s).
+ * old_to_new[n_s] (-1 = constrained), gx / gy[n_s] the Dirichlet values (read
+ * at constrained dofs). Outputs a_red, b_red, lift_x / lift_y (kept rows) and
+ * rhs_p (b_full rows); the vectors may be NULL. */
+int sag_reduce_dirichlet(sag_ctx* ctx, const sag_matrix* a_full, const sag_matrix* b_full,
+                         int n_s, const int* old_to_new, const double* gx, const double* gy,
+                         sag_matrix** a_red, sag_matrix** b_red, double* lift_x, double* lift_y,
+                         double* rhs_p);
+
 /* ---- partitioned-solve primitives ---------------------------
  * Building blocks for a caller that row-partitions the solve across ranks
  * (one process per GPU, paper_2306_06795_b200/dist.py). All pointers are

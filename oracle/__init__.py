@@ -717,6 +717,27 @@ class RefPrec:
                        residual_history=hist[:min(rep.history_len, cap)].copy())
 
 
+def ref_sort_permutation(keys) -> np.ndarray:
+    """std::sort's permutation under from_triplets' comparator (sparse.cpp:44-46)
+    on the reference's own Triplet, keys = row << 32 | col."""
+    L = rlib()
+    L.ref_sort_permutation.argtypes = [C.c_longlong, vp, vp]
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    p = np.empty(len(k), dtype=np.int32)
+    _rcheck(L.ref_sort_permutation(len(k), k.ctypes.data, p.ctypes.data))
+    return p
+
+
+def ref_antiqsort_keys(n: int) -> np.ndarray:
+    """McIlroy's quicksort adversary run against std::sort: keys that push
+    introsort to its heap-sort fallback."""
+    L = rlib()
+    L.ref_antiqsort_keys.argtypes = [C.c_int, vp]
+    k = np.empty(n, dtype=np.uint64)
+    _rcheck(L.ref_antiqsort_keys(n, k.ctypes.data))
+    return k
+
+
 def splitmix64_uniform(n: int, seed: int = 0x5EED) -> np.ndarray:
     """x_i in U[-1,1) from splitmix64(seed ^ i); identical on
     host and device."""

@@ -9,6 +9,7 @@
 // (preconditioner.cpp:114-153) and solve_stokes (preconditioner.cpp:229-259).
 // Nothing in here re-implements reference arithmetic; it only marshals arrays.
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -673,6 +674,45 @@ int ref_solve_stokes(void* h, const double* rhs, double* x, RefReport* rep, doub
     auto res = solve_stokes(d->prec->k0(), rv, *d->prec, d->cfg);
     std::memcpy(x, res.x.data(), sizeof(double) * n);
     report_out(res.report, rep, hist, cap);
+  });
+}
+
+// std::sort's permutation under from_triplets' comparator (sparse.cpp:44-46)
+// on the reference's own Triplet: keys = row << 32 | col, the value carries
+// the original index. The device reproduces this (sag_sort_permutation).
+int ref_sort_permutation(long long n, const unsigned long long* keys, int* perm) {
+  return guard([&] {
+    std::vector<Triplet> t(n);
+    for (long long i = 0; i < n; ++i)
+      t[i] = {static_cast<int>(keys[i] >> 32), static_cast<int>(keys[i] & 0xffffffffu),
+              static_cast<double>(i)};
+    std::sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
+      return a.row != b.row ? a.row < b.row : a.col < b.col;
+    });
+    for (long long i = 0; i < n; ++i) perm[i] = static_cast<int>(t[i].value);
+  });
+}
+
+// McIlroy's adversary ("A killer adversary for quicksort", 1999) against
+// std::sort: keys that drive libstdc++'s introsort towards its depth limit
+// (the heap-sort fallback); gas elements left at the end share one key.
+int ref_antiqsort_keys(int n, unsigned long long* keys) {
+  return guard([&] {
+    std::vector<int> val(n, n), ptr(n);
+    int nsolid = 0, candidate = 0;
+    const int gas = n;
+    for (int i = 0; i < n; ++i) ptr[i] = i;
+    auto cmp = [&](int x, int y) {
+      if (val[x] == gas && val[y] == gas) {
+        if (x == candidate) val[x] = nsolid++;
+        else val[y] = nsolid++;
+      }
+      if (val[x] == gas) candidate = x;
+      else if (val[y] == gas) candidate = y;
+      return val[x] < val[y];
+    };
+    std::sort(ptr.begin(), ptr.end(), cmp);
+    for (int i = 0; i < n; ++i) keys[i] = static_cast<unsigned long long>(val[i]);
   });
 }
 

@@ -121,6 +121,11 @@ class sag_level_desc(C.Structure):
     _fields_ = [("k", vp), ("p", vp), ("n_x", C.c_int), ("n_y", C.c_int), ("n_p", C.c_int)]
 
 
+class sag_mesh2d(C.Structure):
+    _fields_ = [("num_vertices", C.c_int), ("num_triangles", C.c_int), ("num_edges", C.c_int),
+                ("vertices", vp), ("triangles", vp), ("tri_edges", vp)]
+
+
 #: every entry point declared in include/sag.h, with its ctypes signature
 SIGNATURES = {
     "sag_last_error": (C.c_char_p, []),
@@ -190,6 +195,17 @@ SIGNATURES = {
     "sag_matrix_export": (C.c_int, [vp, vp, vp, vp, vp]),
     "sag_saddle_matrix": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "sag_evolution_soc": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_int, C.POINTER(vp)]),
+    # FEM assembly (bitwise the reference's)
+    "sag_from_triplets": (C.c_int, [vp, C.c_int, C.c_int, C.c_longlong, vp, vp, vp,
+                                    C.POINTER(vp)]),
+    "sag_sort_permutation": (C.c_int, [vp, C.c_longlong, vp, vp, C.POINTER(C.c_int)]),
+    "sag_assemble_p2": (C.c_int, [vp, C.POINTER(sag_mesh2d), C.c_int, vp, C.POINTER(vp),
+                                  C.POINTER(vp), vp, vp, C.POINTER(vp), C.POINTER(vp), vp]),
+    "sag_assemble_p1": (C.c_int, [vp, C.POINTER(sag_mesh2d), C.POINTER(vp), C.POINTER(vp)]),
+    "sag_assemble_iso": (C.c_int, [vp, C.POINTER(sag_mesh2d), vp, C.POINTER(vp), C.POINTER(vp),
+                                   vp, vp]),
+    "sag_reduce_dirichlet": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp, C.POINTER(vp),
+                                       C.POINTER(vp), vp, vp, vp]),
     # partitioned-solve primitives (device pointers, no host sync)
     "sag_dot_async": (C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
     "sag_axpy_async": (C.c_int, [vp, C.c_int, vp, C.c_double, vp, vp]),
@@ -385,6 +401,32 @@ def _new(fn, ctx, *args):
     h = vp()
     _check(fn(ctx.h, *args, C.byref(h)))
     return SparseMatrix._wrap(h, ctx)
+
+
+def from_triplets(nrows: int, ncols: int, rows, cols, values, ctx: Context = None) -> SparseMatrix:
+    """from_triplets (sparse.cpp:43-66) on the device: duplicates summed in
+    the order libstdc++'s std::sort leaves them, exact zeros dropped."""
+    ctx = ctx or default_context()
+    r = np.ascontiguousarray(rows, dtype=np.int32)
+    c = np.ascontiguousarray(cols, dtype=np.int32)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if not (len(r) == len(c) == len(v)):
+        raise DimensionMismatch("from_triplets: rows, cols and values differ in length")
+    h = vp()
+    _check(lib().sag_from_triplets(ctx.h, int(nrows), int(ncols), len(v), r.ctypes.data,
+                                   c.ctypes.data, v.ctypes.data, C.byref(h)))
+    return SparseMatrix._wrap(h, ctx)
+
+
+def sort_permutation(keys, ctx: Context = None):
+    """(perm, heap_ranges): std::sort's permutation of uint64 keys reproduced
+    on the device (the order from_triplets sums duplicates in)."""
+    ctx = ctx or default_context()
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    p = np.empty(len(k), dtype=np.int32)
+    nh = C.c_int()
+    _check(lib().sag_sort_permutation(ctx.h, len(k), k.ctypes.data, p.ctypes.data, C.byref(nh)))
+    return p, nh.value
 
 
 def spgemm(a: SparseMatrix, b: SparseMatrix) -> SparseMatrix:

@@ -49,6 +49,7 @@ def hlib():
                                               C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]
         L.sagh_case_hierarchy_gpu.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.sagh_case_scalar_hierarchy_gpu.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.sagh_case_assembly_gpu.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
         L.sagh_case_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                       C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
@@ -138,6 +139,20 @@ class HostCase:
             raise RuntimeError(hlib().sagh_last_error().decode())
         return dict(bitwise_equal=bool(out[0]), operators=int(out[1]), levels=int(out[2]),
                     soc_device=int(out[3]))
+
+    def assembly_gpu(self, device=0, time_reference=False):
+        """The case's systems assembled again on the device (gpu::assemble_*:
+        element loops, from_triplets and Dirichlet elimination in libsag) and
+        compared with the reference's bitwise: diff bits per system (0 =
+        identical; 1 A, 2 B, 4 Ap, 8 Mp, 16 rhs, 32 sizes, 64 coords, 128 bc,
+        256 SV extras), K0 equality and timings."""
+        out = np.zeros(8)
+        if hlib().sagh_case_assembly_gpu(self.h, int(device), int(time_reference),
+                                         out.ctypes.data):
+            raise RuntimeError(hlib().sagh_last_error().decode())
+        return dict(sys0_diff=int(out[0]), sys1_diff=int(out[1]), k0_equal=bool(out[2]),
+                    device_s=float(out[3]), reference_s=float(out[4]) if out[4] >= 0 else None,
+                    sys0_s=float(out[5]), sys1_s=float(out[6]), k0_s=float(out[7]))
 
     def rhs(self):
         r = np.empty(self.n0)

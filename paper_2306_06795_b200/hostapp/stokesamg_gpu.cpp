@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <string>
 #include <utility>
 
@@ -563,6 +564,381 @@ ScalarHierarchy build_scalar_hierarchy(Device& dev, const SparseMatrix& a, const
   return h;
 }
 
+// ---- FEM assembly on the device --------------------------
+// The host keeps the mesh, the user's callbacks (Dirichlet values, body force,
+// Neumann data) and the boundary bookkeeping; the element loops, every
+// from_triplets and the Dirichlet elimination run in libsag (sag_fem.cu),
+// bitwise the reference's.
+namespace {
+
+// tri_quadrature (fem.cpp:21-36) and line_quadrature (:41-50)
+struct QuadPt {
+  std::array<double, 3> l;
+  double w;
+};
+const std::array<QuadPt, 6>& quad6() {
+  static const double a1 = 0.445948490915965, w1 = 0.223381589678011;
+  static const double a2 = 0.091576213509771, w2 = 0.109951743655322;
+  static const std::array<QuadPt, 6> q = {{{{a1, a1, 1 - 2 * a1}, w1},
+                                           {{a1, 1 - 2 * a1, a1}, w1},
+                                           {{1 - 2 * a1, a1, a1}, w1},
+                                           {{a2, a2, 1 - 2 * a2}, w2},
+                                           {{a2, 1 - 2 * a2, a2}, w2},
+                                           {{1 - 2 * a2, a2, a2}, w2}}};
+  return q;
+}
+struct LinePt {
+  double s, w;
+};
+const std::array<LinePt, 3>& quad_line() {
+  static const double c = std::sqrt(3.0 / 5.0);
+  static const std::array<LinePt, 3> q = {
+      {{0.5 * (1 - c), 5.0 / 18.0}, {0.5, 8.0 / 18.0}, {0.5 * (1 + c), 5.0 / 18.0}}};
+  return q;
+}
+
+// the mesh as plain arrays for the C-ABI
+struct MeshView {
+  std::vector<double> v;
+  std::vector<int> t, te;
+  sag_mesh2d m{};
+  explicit MeshView(const SimplicialMesh2D& mesh, bool edges) {
+    v.resize(2 * mesh.vertices.size());
+    for (size_t i = 0; i < mesh.vertices.size(); ++i) {
+      v[2 * i] = mesh.vertices[i][0];
+      v[2 * i + 1] = mesh.vertices[i][1];
+    }
+    t.resize(3 * mesh.triangles.size());
+    for (size_t i = 0; i < mesh.triangles.size(); ++i)
+      for (int k = 0; k < 3; ++k) t[3 * i + k] = mesh.triangles[i][k];
+    if (edges) {
+      te.resize(3 * mesh.tri_edges.size());
+      for (size_t i = 0; i < mesh.tri_edges.size(); ++i)
+        for (int k = 0; k < 3; ++k) te[3 * i + k] = mesh.tri_edges[i][k];
+    }
+    m.num_vertices = mesh.num_vertices();
+    m.num_triangles = mesh.num_triangles();
+    m.num_edges = mesh.num_edges();
+    m.vertices = v.data();
+    m.triangles = t.data();
+    m.tri_edges = edges ? te.data() : nullptr;
+  }
+};
+
+// The body force at every quadrature point (point_at, fem.cpp:73-76), the
+// user's callback evaluated here on the host; empty when it vanishes
+// everywhere (the element loop then adds nothing, fem.cpp:382).
+std::vector<double> force_at_quadrature(const SimplicialMesh2D& m, const ProblemData& prob) {
+  std::vector<double> f(12 * (size_t)m.num_triangles());
+  bool any = false;
+  for (int t = 0; t < m.num_triangles(); ++t) {
+    const auto& c0 = m.vertices[m.triangles[t][0]];
+    const auto& c1 = m.vertices[m.triangles[t][1]];
+    const auto& c2 = m.vertices[m.triangles[t][2]];
+    for (int q = 0; q < 6; ++q) {
+      const auto& l = quad6()[q].l;
+      const double x = l[0] * c0[0] + l[1] * c1[0] + l[2] * c2[0];
+      const double y = l[0] * c0[1] + l[1] * c1[1] + l[2] * c2[1];
+      const auto v = prob.force(x, y);
+      f[12 * (size_t)t + 2 * q] = v[0];
+      f[12 * (size_t)t + 2 * q + 1] = v[1];
+      any = any || v[0] != 0.0 || v[1] != 0.0;
+    }
+  }
+  if (!any) f.clear();
+  return f;
+}
+
+// p2_dirichlet_values / p1_dirichlet_values (fem.cpp:120-146)
+std::map<int, std::array<double, 2>> dirichlet_values(const SimplicialMesh2D& m,
+                                                      const ProblemData& prob, bool p2) {
+  std::map<int, std::array<double, 2>> vals;
+  for (const auto& be : m.boundary_edges) {
+    if (be.tag == BoundaryTag::Neumann) continue;
+    const auto& pa = m.vertices[be.a];
+    const auto& pb = m.vertices[be.b];
+    vals[be.a] = prob.dirichlet(be.tag, pa[0], pa[1]);
+    vals[be.b] = prob.dirichlet(be.tag, pb[0], pb[1]);
+    if (p2)
+      vals[m.num_vertices() + m.edge_index(be.a, be.b)] =
+          prob.dirichlet(be.tag, 0.5 * (pa[0] + pb[0]), 0.5 * (pa[1] + pb[1]));
+  }
+  return vals;
+}
+
+// check_compatibility (fem.cpp:148-196): the enclosed-flow net boundary flux.
+// A boundary edge has exactly one incident triangle, found here through an
+// edge map instead of a scan over all triangles (same triangle, same flux).
+void compatibility(const SimplicialMesh2D& m, const ProblemData& prob) {
+  if (!prob.check_compatibility) return;
+  for (const auto& be : m.boundary_edges)
+    if (be.tag == BoundaryTag::Neumann) return;
+  std::map<std::array<int, 2>, int> opposite;  // boundary edge -> third vertex
+  for (const auto& be : m.boundary_edges)
+    opposite[{std::min(be.a, be.b), std::max(be.a, be.b)}] = -1;
+  for (int t = 0; t < m.num_triangles(); ++t)
+    for (int k = 0; k < 3; ++k) {
+      const int a = m.triangles[t][(k + 1) % 3], b = m.triangles[t][(k + 2) % 3];
+      auto it = opposite.find({std::min(a, b), std::max(a, b)});
+      if (it != opposite.end() && it->second < 0) it->second = m.triangles[t][k];
+    }
+  double flux = 0.0, scale = 0.0;
+  for (const auto& be : m.boundary_edges) {
+    const auto& pa = m.vertices[be.a];
+    const auto& pb = m.vertices[be.b];
+    const double tx = pb[0] - pa[0], ty = pb[1] - pa[1];
+    const double len = std::hypot(tx, ty);
+    scale += len;
+    std::array<double, 2> n{ty / len, -tx / len};
+    const int other = opposite[{std::min(be.a, be.b), std::max(be.a, be.b)}];
+    if (other >= 0) {
+      const auto& po = m.vertices[other];
+      const double dx = po[0] - 0.5 * (pa[0] + pb[0]);
+      const double dy = po[1] - 0.5 * (pa[1] + pb[1]);
+      if (n[0] * dx + n[1] * dy > 0) {
+        n[0] = -n[0];
+        n[1] = -n[1];
+      }
+    }
+    for (const auto& q : quad_line()) {
+      const auto g = prob.dirichlet(be.tag, pa[0] + q.s * tx, pa[1] + q.s * ty);
+      flux += q.w * len * (g[0] * n[0] + g[1] * n[1]);
+    }
+  }
+  if (std::abs(flux) > 1e-10 * std::max(scale, 1.0))
+    throw CompatibilityError("enclosed flow with nonzero net boundary flux");
+}
+
+// Neumann edge loads (fem.cpp:391-414 P2, :610-627 ISO), after the element loop
+void neumann_loads(const SimplicialMesh2D& m, const ProblemData& prob, bool p2,
+                   std::vector<double>& fx, std::vector<double>& fy) {
+  if (!prob.neumann) return;
+  for (const auto& be : m.boundary_edges) {
+    if (be.tag != BoundaryTag::Neumann) continue;
+    const auto& pa = m.vertices[be.a];
+    const auto& pb = m.vertices[be.b];
+    const double len = std::hypot(pb[0] - pa[0], pb[1] - pa[1]);
+    const int mid = p2 ? m.num_vertices() + m.edge_index(be.a, be.b) : -1;
+    for (const auto& q : quad_line()) {
+      const double x = pa[0] + q.s * (pb[0] - pa[0]);
+      const double y = pa[1] + q.s * (pb[1] - pa[1]);
+      const auto gn = (*prob.neumann)(x, y);
+      const double w = q.w * len;
+      if (p2) {
+        const double na = (1 - q.s) * (1 - 2 * q.s);
+        const double nb = q.s * (2 * q.s - 1);
+        const double nm = 4 * q.s * (1 - q.s);
+        fx[be.a] += w * na * gn[0];
+        fy[be.a] += w * na * gn[1];
+        fx[be.b] += w * nb * gn[0];
+        fy[be.b] += w * nb * gn[1];
+        fx[mid] += w * nm * gn[0];
+        fy[mid] += w * nm * gn[1];
+      } else {
+        fx[be.a] += w * (1 - q.s) * gn[0];
+        fy[be.a] += w * (1 - q.s) * gn[1];
+        fx[be.b] += w * q.s * gn[0];
+        fy[be.b] += w * q.s * gn[1];
+      }
+    }
+  }
+}
+
+// make_reduction (fem.cpp:198-205) + the device elimination (reduce_scalar,
+// reduce_divergence) + the system's remaining fields (fem.cpp:420-449)
+void finish_system(Device& dev, SaddleSystem& sys, const DevM& a_full, const DevM& b_full,
+                   int n_s, const std::map<int, std::array<double, 2>>& vals,
+                   const std::vector<double>& fx, const std::vector<double>& fy) {
+  std::vector<int> o2n(n_s, -1), kept;
+  std::vector<double> gx(n_s, 0.0), gy(n_s, 0.0);
+  for (int i = 0; i < n_s; ++i) {
+    auto it = vals.find(i);
+    if (it == vals.end()) {
+      o2n[i] = static_cast<int>(kept.size());
+      kept.push_back(i);
+    } else {
+      gx[i] = it->second[0];
+      gy[i] = it->second[1];
+    }
+  }
+  const int ns_red = static_cast<int>(kept.size());
+  int nbr = 0, nbc = 0;
+  long long nbz = 0;
+  check(sag_matrix_shape(b_full.h, &nbr, &nbc, &nbz));
+  std::vector<double> lift_x(ns_red), lift_y(ns_red), rhs_p(nbr);
+  DevM a_red, b_red;
+  check(sag_reduce_dirichlet(dev.handle(), a_full.h, b_full.h, n_s, o2n.data(), gx.data(),
+                             gy.data(), &a_red.h, &b_red.h, lift_x.data(), lift_y.data(),
+                             rhs_p.data()));
+  sys.n_x = sys.n_y = ns_red;
+  sys.n_p = nbr;
+  SparseMatrix ar = to_host(dev, a_red);
+  sys.B = to_host(dev, b_red);
+  sys.A = block_diag({&ar, &ar});
+  sys.rhs.assign(sys.total_dofs(), 0.0);
+  for (int i = 0; i < ns_red; ++i) {
+    sys.rhs[i] = fx[kept[i]] - lift_x[i];
+    sys.rhs[ns_red + i] = fy[kept[i]] - lift_y[i];
+  }
+  for (int i = 0; i < nbr; ++i) sys.rhs[2 * ns_red + i] = rhs_p[i];
+  for (const auto& [dof, g] : vals) {
+    sys.bc.constrained.push_back(dof);
+    sys.bc.values_x.push_back(g[0]);
+    sys.bc.values_y.push_back(g[1]);
+  }
+  sys.velocity_coords.clear();
+  sys.velocity_coords.reserve(ns_red);
+}
+
+std::vector<std::array<double, 2>> p2_coords(const SimplicialMesh2D& m) {  // fem.cpp:110-118
+  std::vector<std::array<double, 2>> c = m.vertices;
+  c.reserve(m.num_vertices() + m.num_edges());
+  for (const auto& e : m.edges)
+    c.push_back({0.5 * (m.vertices[e[0]][0] + m.vertices[e[1]][0]),
+                 0.5 * (m.vertices[e[0]][1] + m.vertices[e[1]][1])});
+  return c;
+}
+
+void p1_operators(Device& dev, const SimplicialMesh2D& m, SparseMatrix* ap, SparseMatrix* mp) {
+  MeshView mv(m, false);
+  DevM s, ms;
+  check(sag_assemble_p1(dev.handle(), &mv.m, ap ? &s.h : nullptr, mp ? &ms.h : nullptr));
+  if (ap) *ap = to_host(dev, s);
+  if (mp) *mp = to_host(dev, ms);
+}
+
+SaddleSystem assemble_p2(Device& dev, const SimplicialMesh2D& m, const ProblemData& prob,
+                         bool sv) {
+  const int nv = m.num_vertices(), nt = m.num_triangles();
+  const int n_s = nv + m.num_edges();
+  MeshView mv(m, true);
+  const std::vector<double> fq = force_at_quadrature(m, prob);
+  std::vector<double> fx(n_s), fy(n_s), areas(sv ? nt : 0);
+  DevM a_full, b_full, mp, mix;
+  check(sag_assemble_p2(dev.handle(), &mv.m, sv ? 1 : 0, fq.empty() ? nullptr : fq.data(),
+                        &a_full.h, &b_full.h, fx.data(), fy.data(), sv ? &mp.h : nullptr,
+                        sv ? &mix.h : nullptr, sv ? areas.data() : nullptr));
+  neumann_loads(m, prob, true, fx, fy);
+  const auto vals = dirichlet_values(m, prob, true);
+  SaddleSystem sys;
+  sys.disc = sv ? Discretization::SV : Discretization::TH;
+  finish_system(dev, sys, a_full, b_full, n_s, vals, fx, fy);
+  const auto coords = p2_coords(m);
+  for (int i = 0; i < n_s; ++i)
+    if (!vals.count(i)) sys.velocity_coords.push_back(coords[i]);
+  if (sv) {
+    p1_operators(dev, m, &sys.Ap, &sys.Mp_cg);
+    sys.Mp = to_host(dev, mp);
+    sys.M_mix = to_host(dev, mix);
+    sys.sv_element_areas = std::move(areas);
+    sys.pressure_coords.reserve(3 * (size_t)nt);
+    sys.sv_pressure_vertices.reserve(nt);
+    for (int t = 0; t < nt; ++t) {
+      sys.sv_pressure_vertices.push_back(m.triangles[t]);
+      for (int k = 0; k < 3; ++k) sys.pressure_coords.push_back(m.vertices[m.triangles[t][k]]);
+    }
+  } else {
+    p1_operators(dev, m, &sys.Ap, &sys.Mp);
+    sys.pressure_coords = m.vertices;
+  }
+  return sys;
+}
+
+}  // namespace
+
+SaddleSystem assemble_taylor_hood(Device& dev, const SimplicialMesh2D& m,
+                                  const ProblemData& prob) {
+  if (m.boundary_edges.empty()) throw UntaggedBoundary("assemble_taylor_hood: no boundary tags");
+  compatibility(m, prob);
+  return assemble_p2(dev, m, prob, false);
+}
+
+SaddleSystem assemble_scott_vogelius(Device& dev, const SimplicialMesh2D& m,
+                                     const ProblemData& prob, bool force_unrefined) {
+  if (!m.barycentric && !force_unrefined)
+    throw StabilityWarning("assemble_scott_vogelius: mesh is not barycentrically refined");
+  if (m.boundary_edges.empty()) throw UntaggedBoundary("assemble_scott_vogelius: no boundary tags");
+  compatibility(m, prob);
+  return assemble_p2(dev, m, prob, true);
+}
+
+SaddleSystem assemble_iso(Device& dev, const SimplicialMesh2D& m, const SimplicialMesh2D& m_fine,
+                          const RefinementMap& map, const ProblemData& prob) {
+  if (m_fine.num_vertices() != m.num_vertices() + m.num_edges() ||
+      m_fine.num_triangles() != 4 * m.num_triangles())
+    throw DimensionMismatch("assemble_iso: fine mesh is not a quadrisection of the coarse mesh");
+  compatibility(m, prob);
+  const int nvf = m_fine.num_vertices(), nvc = m.num_vertices();
+  MeshView mv(m_fine, false);
+  const std::vector<double> fq = force_at_quadrature(m_fine, prob);
+  std::vector<double> fx(nvf), fy(nvf);
+  DevM a_full, b_fine;
+  check(sag_assemble_iso(dev.handle(), &mv.m, fq.empty() ? nullptr : fq.data(), &a_full.h,
+                         &b_fine.h, fx.data(), fy.data()));
+  neumann_loads(m_fine, prob, false, fx, fy);
+  // p1_interpolation (fem.cpp:337-352): one or two entries per fine vertex,
+  // already in CSR order; b_coarse_p = transpose(E) b_fine on the device
+  if (static_cast<int>(map.vertex_origin.size()) != nvf)
+    throw DimensionMismatch("p1_interpolation: refinement map does not match fine mesh");
+  SparseMatrix e(nvf, nvc);
+  for (int i = 0; i < nvf; ++i) {
+    const auto& org = map.vertex_origin[i];
+    if (const auto* cv = std::get_if<CoarseVertex>(&org)) {
+      e.col_indices.push_back(cv->index);
+      e.values.push_back(1.0);
+    } else if (const auto* em = std::get_if<EdgeMidpoint>(&org)) {
+      const int lo = std::min(em->a, em->b), hi = std::max(em->a, em->b);
+      e.col_indices.push_back(lo);
+      e.values.push_back(0.5);
+      e.col_indices.push_back(hi);
+      e.values.push_back(0.5);
+    } else {
+      throw DimensionMismatch("p1_interpolation: barycentric lineage not supported here");
+    }
+    e.row_offsets[i + 1] = static_cast<int>(e.col_indices.size());
+  }
+  DevM de(dev, e), et, bcp;
+  check(sag_transpose(dev.handle(), de.h, &et.h));
+  check(sag_spgemm(dev.handle(), et.h, b_fine.h, &bcp.h));
+  const auto vals = dirichlet_values(m_fine, prob, false);
+  SaddleSystem sys;
+  sys.disc = Discretization::ISO;
+  finish_system(dev, sys, a_full, bcp, nvf, vals, fx, fy);
+  sys.n_p = nvc;
+  for (int i = 0; i < nvf; ++i)
+    if (!vals.count(i)) sys.velocity_coords.push_back(m_fine.vertices[i]);
+  p1_operators(dev, m, &sys.Ap, &sys.Mp);
+  sys.pressure_coords = m.vertices;
+  return sys;
+}
+
+SparseMatrix assemble_saddle_matrix(Device& dev, const SaddleSystem& sys) {
+  DevM a(dev, sys.A), b(dev, sys.B), k;
+  check(sag_saddle_matrix(dev.handle(), a.h, b.h, &k.h));
+  return to_host(dev, k);
+}
+
+AssembledCase build_case(Device& dev, const SimplicialMesh2D& base, const ProblemData& prob,
+                         Discretization disc, bool enclosed) {
+  AssembledCase c;
+  c.enclosed = enclosed;
+  if (disc == Discretization::SV) {
+    auto [mb, bmap] = barycentric_refine(base);
+    c.mesh = std::move(mb);
+    c.sys0 = assemble_scott_vogelius(dev, c.mesh, prob);
+    auto [mf, qmap] = quadrisect(c.mesh);
+    c.sys1 = assemble_iso(dev, c.mesh, mf, qmap, prob);
+    c.transfer = build_sv_transfer(c.sys0, c.sys1);
+  } else {
+    c.mesh = base;
+    c.sys0 = assemble_taylor_hood(dev, c.mesh, prob);
+    auto [mf, qmap] = quadrisect(c.mesh);
+    c.sys1 = assemble_iso(dev, c.mesh, mf, qmap, prob);
+    c.transfer = build_th_transfer(c.sys0, c.sys1);
+  }
+  return c;
+}
+
 }  // namespace stokesamg::gpu
 
 // ======================================================================
@@ -576,6 +952,7 @@ thread_local std::string g_err;
 
 struct HostCase {
   AssembledCase c;
+  ProblemData prob;  // the case's problem data (device assembly input)
   SparseMatrix k0;
   AmgConfig amg;
   MonolithicHierarchy h;
@@ -625,13 +1002,75 @@ const SparseMatrix* pick(const HostCase& hc, int which) {
   return s + 1 < hc.sh.levels() ? &hc.sh.prolongators[s] : nullptr;
 }
 
+// problem_data_for (experiments.cpp:56-84): the problem data build_case uses
+ProblemData problem_for(const std::string& problem) {
+  if (problem == "bfs") return bfs_problem();
+  if (problem == "channel") return channel_problem();
+  if (problem == "manufactured") return manufactured_unit_square().problem;
+  if (problem == "cavity") {
+    ProblemData p = zero_problem();
+    p.dirichlet = [](BoundaryTag, double, double y) {
+      return std::array<double, 2>{y > 1 - 1e-12 ? 1.0 : 0.0, 0.0};
+    };
+    p.check_compatibility = false;
+    return p;
+  }
+  if (problem == "forced") {
+    ProblemData p = zero_problem();
+    p.force = [](double x, double y) {
+      return std::array<double, 2>{std::sin(3.0 * y) + 1.0, std::cos(2.0 * x)};
+    };
+    return p;
+  }
+  throw ConfigError("experiment spec: unknown problem: " + problem);
+}
+
 // f = (sin(k1 x), cos(k2 y)) body force, all-Dirichlet zero (BASELINE config 4)
-AssembledCase mesh_case(const char* path, double k1, double k2) {
+ProblemData forced_problem(double k1, double k2) {
   ProblemData prob = zero_problem();
   prob.force = [k1, k2](double x, double y) {
     return std::array<double, 2>{std::sin(k1 * x), std::cos(k2 * y)};
   };
   prob.check_compatibility = false;
+  return prob;
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+bool same(const SparseMatrix& a, const SparseMatrix& b) {
+  return a.nrows == b.nrows && a.ncols == b.ncols && a.row_offsets == b.row_offsets &&
+         a.col_indices == b.col_indices &&
+         a.values.size() == b.values.size() &&
+         (a.values.empty() ||
+          std::memcmp(a.values.data(), b.values.data(), 8 * a.values.size()) == 0);
+}
+bool same(const std::vector<double>& a, const std::vector<double>& b) {
+  return a.size() == b.size() && (a.empty() || std::memcmp(a.data(), b.data(), 8 * a.size()) == 0);
+}
+// every field of two saddle systems, bitwise; bit i set = field i differs
+int system_diff(const SaddleSystem& a, const SaddleSystem& b) {
+  int d = 0;
+  if (!same(a.A, b.A)) d |= 1;
+  if (!same(a.B, b.B)) d |= 2;
+  if (!same(a.Ap, b.Ap)) d |= 4;
+  if (!same(a.Mp, b.Mp)) d |= 8;
+  if (!same(a.rhs, b.rhs)) d |= 16;
+  if (a.n_x != b.n_x || a.n_y != b.n_y || a.n_p != b.n_p || a.disc != b.disc) d |= 32;
+  if (a.velocity_coords != b.velocity_coords || a.pressure_coords != b.pressure_coords) d |= 64;
+  if (a.bc.constrained != b.bc.constrained || !same(a.bc.values_x, b.bc.values_x) ||
+      !same(a.bc.values_y, b.bc.values_y))
+    d |= 128;
+  if (!same(a.Mp_cg, b.Mp_cg) || !same(a.M_mix, b.M_mix) ||
+      !same(a.sv_element_areas, b.sv_element_areas) ||
+      a.sv_pressure_vertices != b.sv_pressure_vertices)
+    d |= 256;
+  return d;
+}
+
+AssembledCase mesh_case(const char* path, double k1, double k2) {
+  ProblemData prob = forced_problem(k1, k2);
   AssembledCase c;
   c.enclosed = true;
   c.mesh = read_mesh(path);
@@ -662,7 +1101,9 @@ void* sagh_case_build(const char* problem, int sv, const char* mesh_kind, int n,
     auto hc = std::make_unique<HostCase>();
     if (std::string(mesh_kind) == "file_forced") {
       hc->c = mesh_case(mesh_path, k1, k2);
+      hc->prob = forced_problem(k1, k2);
     } else {
+      hc->prob = problem_for(problem);
       ExperimentSpec s;
       s.problem = problem;
       s.disc = sv ? Discretization::SV : Discretization::TH;
@@ -684,6 +1125,58 @@ void* sagh_case_build(const char* problem, int sv, const char* mesh_kind, int n,
 }
 
 void sagh_case_free(void* h) { delete static_cast<HostCase*>(h); }
+
+// The case's systems assembled again on the device (gpu::assemble_*, from the
+// same high-order mesh and problem data) and compared with the reference's
+// bitwise. out = [sys0 diff bits, sys1 diff bits, K0 equal, device
+// assembly s (sys0 + quadrisect + sys1 + K0), reference assembly s (the same
+// calls, only when time_reference), sys0 s, sys1 s, K0 s]
+int sagh_case_assembly_gpu(void* h, int device, int time_reference, double* out) {
+  return guarded([&] {
+    auto& hc = *static_cast<HostCase*>(h);
+    gpu::Device dev(device);
+    const bool sv = hc.c.sys0.disc == Discretization::SV;
+    auto t0 = std::chrono::steady_clock::now();
+    SaddleSystem s0 = sv ? gpu::assemble_scott_vogelius(dev, hc.c.mesh, hc.prob)
+                         : gpu::assemble_taylor_hood(dev, hc.c.mesh, hc.prob);
+    const double t_s0 = seconds_since(t0);
+    auto t1 = std::chrono::steady_clock::now();
+    auto [mf, qmap] = quadrisect(hc.c.mesh);
+    SaddleSystem s1 = gpu::assemble_iso(dev, hc.c.mesh, mf, qmap, hc.prob);
+    const double t_s1 = seconds_since(t1);
+    auto t2 = std::chrono::steady_clock::now();
+    SparseMatrix k0 = gpu::assemble_saddle_matrix(dev, s0);
+    const double t_k0 = seconds_since(t2);
+    const double t_dev = seconds_since(t0);
+    double t_ref = -1.0;
+    if (time_reference) {
+      auto r0 = std::chrono::steady_clock::now();
+      SaddleSystem a = sv ? assemble_scott_vogelius(hc.c.mesh, hc.prob)
+                          : assemble_taylor_hood(hc.c.mesh, hc.prob);
+      auto [mf2, qmap2] = quadrisect(hc.c.mesh);
+      SaddleSystem b = assemble_iso(hc.c.mesh, mf2, qmap2, hc.prob);
+      SparseMatrix k = assemble_saddle_matrix(a);
+      t_ref = seconds_since(r0);
+    }
+    out[0] = system_diff(s0, hc.c.sys0);
+    out[1] = system_diff(s1, hc.c.sys1);
+    out[2] = same(k0, hc.k0) ? 1.0 : 0.0;
+    out[3] = t_dev;
+    out[4] = t_ref;
+    out[5] = t_s0;
+    out[6] = t_s1;
+    out[7] = t_k0;
+  });
+}
+
+// std::sort's permutation of n keys on the device (sag_sort_permutation)
+int sagh_sort_permutation(int device, long long n, const unsigned long long* keys, int* perm,
+                          int* heap_ranges) {
+  return guarded([&] {
+    gpu::Device dev(device);
+    gpu::check(sag_sort_permutation(dev.handle(), n, keys, perm, heap_ranges));
+  });
+}
 
 // build_scalar_hierarchy by the reference and on the device for the case's
 // scalar operators -- A_x of the high-order system (Uzawa) and the pressure

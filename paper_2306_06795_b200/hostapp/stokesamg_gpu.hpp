@@ -16,7 +16,11 @@
 
 #include "sag.h"
 #include "stokesamg/errors.hpp"
+#include "stokesamg/experiments.hpp"
+#include "stokesamg/fem.hpp"
+#include "stokesamg/mesh.hpp"
 #include "stokesamg/preconditioner.hpp"
+#include "stokesamg/transfer.hpp"
 
 namespace stokesamg::gpu {
 
@@ -172,5 +176,22 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
 // hierarchies of the Uzawa preconditioner and the SV mass projection.
 ScalarHierarchy build_scalar_hierarchy(Device& dev, const SparseMatrix& a, const AmgConfig& cfg,
                                        double* times = nullptr);
+
+// FEM assembly with the element loops, every from_triplets (sparse.cpp:43-66)
+// and the Dirichlet elimination (fem.cpp:207-266) on the device, bitwise the
+// reference's systems (same signatures as fem.hpp:70-78 plus the device):
+// the host keeps the mesh, the user's callbacks and the boundary bookkeeping.
+SaddleSystem assemble_taylor_hood(Device& dev, const SimplicialMesh2D& m, const ProblemData& prob);
+SaddleSystem assemble_scott_vogelius(Device& dev, const SimplicialMesh2D& m_bary,
+                                     const ProblemData& prob, bool force_unrefined = false);
+SaddleSystem assemble_iso(Device& dev, const SimplicialMesh2D& m, const SimplicialMesh2D& m_fine,
+                          const RefinementMap& map, const ProblemData& prob);
+// assemble_saddle_matrix (fem.hpp:70; fem.cpp:290-306) on the device.
+SparseMatrix assemble_saddle_matrix(Device& dev, const SaddleSystem& sys);
+// build_case (experiments.cpp:215-235) from the base mesh and problem data
+// the caller built with the reference (base_mesh, problem_data_for), with
+// the assembly above.
+AssembledCase build_case(Device& dev, const SimplicialMesh2D& base, const ProblemData& prob,
+                         Discretization disc, bool enclosed);
 
 }  // namespace stokesamg::gpu

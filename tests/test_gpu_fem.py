@@ -1,0 +1,145 @@
+"""FEM assembly on the device against the reference, bitwise:
+
+* std::sort's permutation (the order from_triplets sums duplicates in,
+  sparse.cpp:43-66) reproduced on the device for random, structured,
+  organ-pipe and adversarial (McIlroy antiqsort: introsort's heap-sort
+  fallback) key sequences, compared with the reference's own std::sort on
+  its Triplet type (oracle/_ref ref_sort_permutation);
+* from_triplets with duplicates, cancellations to exact zero and empty rows;
+* whole systems (A, B, Ap, Mp, rhs, coordinates, Dirichlet data, SV extras)
+  and K0 assembled by gpu::assemble_taylor_hood / assemble_scott_vogelius /
+  assemble_iso identical to the reference's build_case for the cavity (lid
+  Dirichlet data), BFS (inflow + Neumann outflow), forced (body force +
+  Neumann), manufactured problems, SV, and a jittered Delaunay mesh with the
+  config-4 body force; full size for configs 2-4 (slow).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import paper_2306_06795_b200 as S
+    return S
+
+
+def _keys(kind, rng):
+    if kind == "dup5":
+        return rng.integers(0, 5, 1000)
+    if kind == "dup100":
+        return rng.integers(0, 100, 50_000)
+    if kind == "sorted":
+        return np.arange(3000)
+    if kind == "reversed":
+        return np.arange(3000)[::-1]
+    if kind == "equal":
+        return np.zeros(500)
+    if kind == "organ_pipe":
+        return np.concatenate([np.arange(1000), np.arange(1000)[::-1]])
+    if kind == "tiny":
+        return rng.integers(0, 3, 17)
+    if kind == "sawtooth":
+        return np.arange(20_000) % 37
+    if kind == "binary":
+        return rng.integers(0, 2, 50_000)
+    if kind == "random2M":
+        return rng.integers(0, 1 << 40, 2_000_000)
+    if kind == "rowcol":  # (row, col) keys of a banded matrix, many duplicates
+        r = rng.integers(0, 5000, 300_000)
+        c = np.clip(r + rng.integers(-20, 21, r.size), 0, 4999)
+        return (r.astype(np.uint64) << np.uint64(32)) | c.astype(np.uint64)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["dup5", "dup100", "sorted", "reversed", "equal", "organ_pipe",
+                                  "tiny", "sawtooth", "binary", "random2M", "rowcol"])
+def test_sort_permutation_is_std_sort(S, kind):
+    keys = np.asarray(_keys(kind, np.random.default_rng(7)), dtype=np.uint64)
+    perm, heap = S.sort_permutation(keys)
+    assert np.array_equal(perm, O.ref_sort_permutation(keys))
+    if kind == "organ_pipe":
+        assert heap > 0  # introsort's depth limit reached: the heap-sort path ran
+
+
+@pytest.mark.parametrize("n", [100, 2000, 30_000])
+def test_sort_permutation_adversary(S, n):
+    keys = O.ref_antiqsort_keys(n)
+    perm, heap = S.sort_permutation(keys)
+    assert heap > 0
+    assert np.array_equal(perm, O.ref_sort_permutation(keys))
+
+
+def test_sort_permutation_degenerate(S):
+    for n in (0, 1, 2, 16):
+        keys = np.arange(n, dtype=np.uint64)[::-1].copy()
+        perm, _ = S.sort_permutation(keys)
+        assert np.array_equal(perm, O.ref_sort_permutation(keys))
+
+
+def _csr_equal(a, b):
+    return (a.nrows == b.nrows and a.ncols == b.ncols and np.array_equal(a.rp, b.rp)
+            and np.array_equal(a.ci, b.ci) and a.v.tobytes() == b.v.tobytes())
+
+
+def test_from_triplets_bitwise(S):
+    rng = np.random.default_rng(3)
+    nr, nc, m = 700, 500, 200_000
+    r = rng.integers(0, nr - 50, m)      # the last 50 rows stay empty
+    c = rng.integers(0, nc, m)
+    v = rng.standard_normal(m) * 10.0 ** rng.integers(-8, 8, m)
+    # exact cancellations: some (row, col) pairs get +x and -x only
+    r = np.concatenate([r, [5, 5, 9, 9, 9]])
+    c = np.concatenate([c, [499, 499, 0, 0, 0]])
+    v = np.concatenate([v, [0.3, -0.3, 1e-300, -1e-300, 0.0]])
+    got = S.from_triplets(nr, nc, r, c, v).to_csr()
+    ref = O.RefMat.from_triplets(nr, nc, r, c, v).csr()
+    assert _csr_equal(got, ref)
+    empty = S.from_triplets(3, 4, [], [], []).to_csr()
+    assert np.array_equal(empty.rp, [0, 0, 0, 0])
+    with pytest.raises(S.DimensionMismatch):
+        S.from_triplets(3, 3, [0, 3], [0, 0], [1.0, 1.0])
+
+
+CASES = [("cavity", False, "structured", 8), ("cavity", False, "structured", 64),
+         ("cavity", True, "structured", 8), ("cavity", True, "structured", 32),
+         ("bfs", False, "bfs", 4), ("forced", False, "structured", 16),
+         ("manufactured", False, "structured", 16), ("channel", False, "structured", 8)]
+
+
+@pytest.mark.parametrize("problem,sv,kind,n", CASES)
+def test_assembly_bitwise(problem, sv, kind, n):
+    from paper_2306_06795_b200.cases import HostCase
+    h = HostCase(problem, sv, kind, n)
+    r = h.assembly_gpu(time_reference=True)
+    assert r["sys0_diff"] == 0, r
+    assert r["sys1_diff"] == 0, r
+    assert r["k0_equal"], r
+
+
+def test_assembly_bitwise_jittered_forced(tmp_path):
+    # config 4's recipe at 24 x 24: jittered Delaunay, all-Dirichlet zero,
+    # f = (sin k1 x, cos k2 y)
+    from paper_2306_06795_b200 import meshgen
+    from paper_2306_06795_b200.cases import HostCase
+    path = meshgen.write_mesh(str(tmp_path / "m.json"), 24, seed=7, jitter=0.3)
+    k1, k2 = meshgen.force_wavenumbers()
+    h = HostCase("cavity", False, "file_forced", 0, mesh_path=path, k1=k1, k2=k2)
+    r = h.assembly_gpu(time_reference=True)
+    assert r["sys0_diff"] == 0 and r["sys1_diff"] == 0 and r["k0_equal"], r
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("config", [2, 3, 4])
+def test_assembly_bitwise_fullsize(config):
+    import bench
+    h = bench.host_case(bench.CONFIGS[config])
+    r = h.assembly_gpu()
+    assert r["sys0_diff"] == 0 and r["sys1_diff"] == 0 and r["k0_equal"], r
+    if config == 2:
+        assert r["device_s"] < 5.0, r  # reference: ~35 s of assembly on one core
