@@ -326,6 +326,19 @@ int sag_evolution_soc(sag_ctx* ctx, const sag_matrix* a, double omega, double th
  * divergence B (n_p x n_u). Replaces assemble_saddle_matrix (fem.hpp;
  * fem.cpp:290-306): the blocks never overlap, so K is bitwise the reference's. */
 int sag_saddle_matrix(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* b, sag_matrix** out);
+/* tentative_prolongator_with_nullvec (amg.cpp:184-205) on the device: T
+ * (n x num_aggregates, T_ic = nullvec_i / ||nullvec over aggregate c||, the
+ * norms summed in node order), coarse_nullvec = the aggregate norms (host or
+ * device, may be NULL). SAG_ERROR for an aggregate with a zero norm. */
+int sag_tentative_prolongator(sag_ctx* ctx, int n, int num_aggregates, const int* node_to_agg,
+                              const double* nullvec, sag_matrix** t, double* coarse_nullvec);
+/* power_rho_estimate (sparse.cpp:239-261) from the caller's normalised start
+ * vector x0 (the reference's mt19937 stream / its norm): iters x (y = D^-1 M x
+ * on the device, rows summed in order; ||y|| summed sequentially on the host;
+ * x = y / ||y||); *rho = the last ||y|| (0 when it vanishes). Bitwise the
+ * reference's estimate. */
+int sag_power_rho(sag_ctx* ctx, const sag_matrix* m, const double* d_inv, const double* x0,
+                  int iters, double* rho);
 /* Copies a matrix's CSR arrays out (host or device arrays; any may be NULL). */
 int sag_matrix_export(sag_ctx* ctx, const sag_matrix* m, int* row_offsets, int* col_indices,
                       double* values);

@@ -193,6 +193,8 @@ SIGNATURES = {
     "sag_galerkin": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "sag_smooth_prolongator": (C.c_int, [vp, vp, vp, C.c_double, C.POINTER(vp)]),
     "sag_matrix_export": (C.c_int, [vp, vp, vp, vp, vp]),
+    "sag_tentative_prolongator": (C.c_int, [vp, C.c_int, C.c_int, vp, vp, C.POINTER(vp), vp]),
+    "sag_power_rho": (C.c_int, [vp, vp, vp, vp, C.c_int, f64p]),
     "sag_saddle_matrix": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "sag_evolution_soc": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_int, C.POINTER(vp)]),
     # FEM assembly (bitwise the reference's)
@@ -429,6 +431,31 @@ def sort_permutation(keys, ctx: Context = None):
     return p, nh.value
 
 
+def tentative_prolongator(node_to_agg, num_aggregates: int, nullvec, ctx: Context = None):
+    """tentative_prolongator_with_nullvec (amg.cpp:184-205) on the device:
+    (T, coarse nullvec)."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(node_to_agg, dtype=np.int32)
+    nv = np.ascontiguousarray(nullvec, dtype=np.float64)
+    if len(a) != len(nv):
+        raise DimensionMismatch("tentative_prolongator: aggregation and nullvec differ in length")
+    cn = np.empty(max(int(num_aggregates), 1))
+    h = vp()
+    _check(lib().sag_tentative_prolongator(ctx.h, len(a), int(num_aggregates), a.ctypes.data,
+                                           nv.ctypes.data, C.byref(h), cn.ctypes.data))
+    return SparseMatrix._wrap(h, ctx), cn[:int(num_aggregates)]
+
+
+def power_rho(m: SparseMatrix, d_inv, x0, iters: int = 10) -> float:
+    """power_rho_estimate (sparse.cpp:239-261) from a normalised start vector."""
+    d = np.ascontiguousarray(d_inv, dtype=np.float64)
+    x = np.ascontiguousarray(x0, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().sag_power_rho(m.ctx.h, m.h, d.ctypes.data, x.ctypes.data, int(iters),
+                               C.byref(out)))
+    return out.value
+
+
 def spgemm(a: SparseMatrix, b: SparseMatrix) -> SparseMatrix:
     """C = A B, bitwise the reference's spgemm (sparse.cpp:113-150)."""
     return _new(lib().sag_spgemm, a.ctx, a.h, b.h)
@@ -555,7 +582,8 @@ class VankaFactorization:
         res = []
         for i in range(min(nc.value, 16)):
             R, lpp, npch, nb = (int(v) for v in out[4 * i:4 * i + 4])
-            kern = (f"vanka_subwarp_kernel<{lpp}>" if lpp < 32 else f"vanka_patch_kernel<R={R}>")
+            kern = ("vanka_fixed_kernel<6,3>" if lpp == 9 else
+                    f"vanka_subwarp_kernel<{lpp}>" if lpp < 32 else f"vanka_patch_kernel<R={R}>")
             res.append((kern, R, lpp, npch, nb))
         return res
 

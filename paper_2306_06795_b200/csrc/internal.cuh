@@ -57,6 +57,7 @@ struct Vanka {
     long long slot_bytes;
     int lpp;  // lanes per patch: 32, or 16 / 8 for the sub-warp kernel
     long long bytes = 0;  // blob bytes of the class
+    int fm = 0, fnp = 0;  // fixed shape (nx = ny = fm, np = fnp; vanka_fixed_kernel), or 0
   };
   std::vector<RClass> rclasses;
   int max_dim = 0, max_nv = 0, max_np = 0;
@@ -84,6 +85,10 @@ struct Vanka {
   // per-patch payload bases and shapes (host copies, for export)
   std::vector<long long> h_dbase, h_ibase;
   std::vector<int> h_nx, h_nv, h_np;
+  std::vector<int> blob_patch;  // patch id at each blob position (class order)
+  // the host-buffer step of sag_vanka_spmv pipelined in stages (built on
+  // first use, for one operator)
+  std::shared_ptr<struct StreamPlan> stream_plan;
 };
 
 // Krylov scalar state in device memory (one per FGMRES instance); mirrors the

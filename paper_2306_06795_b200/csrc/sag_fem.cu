@@ -378,13 +378,14 @@ std::unique_ptr<Matrix> from_triplets_dev(Ctx& c, int nrows, int ncols, long lon
                                                      sums.p, rows.p, cols.p, rowcnt.p);
   SAG_LAUNCHED(c);
   // the kept runs in sorted order are the CSR entries
-  size_t t2 = 0, t3 = 0;
+  size_t t2 = 0, t3 = 0, t4 = 0;
   SAG_CUDA(cub::DeviceSelect::Flagged(nullptr, t2, cols.p, keep.p, ci.p, nkeep.p, R, c.stream));
+  SAG_CUDA(cub::DeviceSelect::Flagged(nullptr, t4, sums.p, keep.p, v.p, nkeep.p, R, c.stream));
   DevBuf<int> rp(nrows + 1);
   SAG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, rowcnt.p, rp.p, nrows + 1, c.stream));
-  DevBuf<unsigned char> ws2(std::max<size_t>(std::max(t2, t3), 1));
+  DevBuf<unsigned char> ws2(std::max<size_t>(std::max(std::max(t2, t3), t4), 1));
   SAG_CUDA(cub::DeviceSelect::Flagged(ws2.p, t2, cols.p, keep.p, ci.p, nkeep.p, R, c.stream));
-  SAG_CUDA(cub::DeviceSelect::Flagged(ws2.p, t2, sums.p, keep.p, v.p, nkeep.p, R, c.stream));
+  SAG_CUDA(cub::DeviceSelect::Flagged(ws2.p, t4, sums.p, keep.p, v.p, nkeep.p, R, c.stream));
   SAG_CUDA(cub::DeviceScan::ExclusiveSum(ws2.p, t3, rowcnt.p, rp.p, nrows + 1, c.stream));
   int nnz = 0;
   SAG_CUDA(cudaMemcpyAsync(&nnz, nkeep.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));

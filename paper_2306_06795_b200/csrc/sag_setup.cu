@@ -17,6 +17,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
+#include <string>
 #include <vector>
 
 #include "internal.cuh"
@@ -657,6 +659,78 @@ std::unique_ptr<Matrix> saddle_matrix_dev(Ctx& c, const Matrix& a, const Matrix&
 // =================================================================== C-ABI
 using namespace sag;
 
+
+namespace sag {
+// ---- tentative prolongator (amg.cpp:184-205) and power_rho_estimate
+// (sparse.cpp:239-261), bitwise ---------------------------------------------
+// colnorm_c = sqrt(sum over the aggregate's nodes, in node order, of
+// nullvec_i^2): a stable sort of the nodes by aggregate keeps node order.
+__global__ void agg_norm_kernel(int n, const int* __restrict__ agg_sorted,
+                                const int* __restrict__ node_sorted,
+                                const double* __restrict__ nullvec, double* colnorm) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int a = agg_sorted[i];
+    if (i > 0 && agg_sorted[i - 1] == a) continue;
+    double s = 0.0;
+    for (int j = i; j < n && agg_sorted[j] == a; ++j) {
+      const double v = nullvec[node_sorted[j]];
+      s = __dadd_rn(s, __dmul_rn(v, v));
+    }
+    colnorm[a] = sqrt(s);
+  }
+}
+// T_ic = nullvec_i / colnorm_c, one entry per row (from_triplets drops zeros)
+__global__ void tentative_count_kernel(int n, const int* __restrict__ agg,
+                                       const double* __restrict__ nullvec,
+                                       const double* __restrict__ colnorm, int* cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = agg[i];
+    cnt[i] = (nullvec[i] / colnorm[c]) != 0.0 ? 1 : 0;
+  }
+}
+__global__ void tentative_fill_kernel(int n, const int* __restrict__ agg,
+                                      const double* __restrict__ nullvec,
+                                      const double* __restrict__ colnorm,
+                                      const int* __restrict__ rp, int* ci, double* v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int c = agg[i];
+    const double t = nullvec[i] / colnorm[c];
+    if (t != 0.0) {
+      ci[rp[i]] = c;
+      v[rp[i]] = t;
+    }
+  }
+}
+__global__ void empty_agg_kernel(int nc, const double* colnorm, const int* seen, int* bad) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x)
+    if (!seen[c] || colnorm[c] == 0.0) atomicMin(bad, c);
+}
+__global__ void iota_kernel(int n, int* a) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+__global__ void mark_agg_kernel(int n, const int* agg, int* seen) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    seen[agg[i]] = 1;
+}
+
+// y = D^-1 (M x), each row summed in order with round-to-nearest operations
+// (spmv, sparse.cpp:78-91, then y_i *= d_inv_i, :252)
+__global__ void spmv_rn_scale_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                     const double* __restrict__ v, const double* __restrict__ x,
+                                     const double* __restrict__ dinv, double* y) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = rp[r]; k < rp[r + 1]; ++k) s = __dadd_rn(s, __dmul_rn(v[k], x[ci[k]]));
+    y[r] = __dmul_rn(s, dinv[r]);
+  }
+}
+__global__ void scale_div_kernel(int n, const double* y, double ny, double* x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    x[i] = __ddiv_rn(y[i], ny);
+}
+
+}  // namespace sag
+
 namespace {
 sag_matrix* wrap(std::unique_ptr<Matrix> m) {
   auto* h = new sag_matrix;
@@ -731,6 +805,110 @@ int sag_saddle_matrix(sag_ctx* ctx, const sag_matrix* a, const sag_matrix* b, sa
     SAG_NOTNULL(b);
     SAG_NOTNULL(out);
     *out = wrap(saddle_matrix_dev(ctx->c, a->m, b->m));
+  });
+}
+
+int sag_tentative_prolongator(sag_ctx* ctx, int n, int num_aggregates, const int* node_to_agg,
+                              const double* nullvec, sag_matrix** t, double* coarse_nullvec) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(t);
+    SAG_REQUIRE(n >= 0 && num_aggregates >= 0, SAG_DIMENSION_MISMATCH,
+                "tentative_prolongator: negative size");
+    Ctx& c = ctx->c;
+    const int nc = num_aggregates;
+    DevBuf<int> agg(std::max(n, 1)), agg2(std::max(n, 1)), ids(std::max(n, 1)),
+        ids2(std::max(n, 1)), cnt(n + 1), seen(std::max(nc, 1)), bad(1);
+    DevBuf<double> nv(std::max(n, 1)), cn(std::max(nc, 1));
+    if (n) {
+      SAG_NOTNULL(node_to_agg);
+      SAG_NOTNULL(nullvec);
+      SAG_CUDA(cudaMemcpyAsync(agg.p, node_to_agg, 4 * (size_t)n, cudaMemcpyDefault, c.stream));
+      SAG_CUDA(cudaMemcpyAsync(nv.p, nullvec, 8 * (size_t)n, cudaMemcpyDefault, c.stream));
+    }
+    SAG_CUDA(cudaMemsetAsync(cn.p, 0, 8 * (size_t)std::max(nc, 1), c.stream));
+    SAG_CUDA(cudaMemsetAsync(seen.p, 0, 4 * (size_t)std::max(nc, 1), c.stream));
+    const int big = 0x7fffffff;
+    SAG_CUDA(cudaMemcpyAsync(bad.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    const int g = std::max(1, std::min((std::max(n, nc) + 255) / 256, c.num_sms * 16));
+    if (n) {
+      iota_kernel<<<g, 256, 0, c.stream>>>(n, ids.p);
+      SAG_LAUNCHED(c);
+      size_t tmp = 0;
+      SAG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, agg.p, agg2.p, ids.p, ids2.p, n, 0,
+                                               32, c.stream));
+      DevBuf<unsigned char> ws(std::max<size_t>(tmp, 1));
+      SAG_CUDA(cub::DeviceRadixSort::SortPairs(ws.p, tmp, agg.p, agg2.p, ids.p, ids2.p, n, 0, 32,
+                                               c.stream));
+      agg_norm_kernel<<<g, 256, 0, c.stream>>>(n, agg2.p, ids2.p, nv.p, cn.p);
+      SAG_LAUNCHED(c);
+      mark_agg_kernel<<<g, 256, 0, c.stream>>>(n, agg.p, seen.p);
+      SAG_LAUNCHED(c);
+    }
+    if (nc) {
+      empty_agg_kernel<<<g, 256, 0, c.stream>>>(nc, cn.p, seen.p, bad.p);
+      SAG_LAUNCHED(c);
+    }
+    int hb = big;
+    SAG_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    SAG_REQUIRE(hb == big, SAG_ERROR,
+                "tentative_prolongator: zero near-kernel over aggregate " + std::to_string(hb));
+    SAG_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * (size_t)(n + 1), c.stream));
+    if (n) {
+      tentative_count_kernel<<<g, 256, 0, c.stream>>>(n, agg.p, nv.p, cn.p, cnt.p);
+      SAG_LAUNCHED(c);
+    }
+    *t = wrap(csr_from_counts(c, n, nc, cnt, [&](int* rp, int* ci, double* v) {
+      if (n) {
+        tentative_fill_kernel<<<g, 256, 0, c.stream>>>(n, agg.p, nv.p, cn.p, rp, ci, v);
+        SAG_LAUNCHED(c);
+      }
+    }));
+    if (coarse_nullvec && nc)
+      SAG_CUDA(cudaMemcpyAsync(coarse_nullvec, cn.p, 8 * (size_t)nc, cudaMemcpyDefault, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sag_power_rho(sag_ctx* ctx, const sag_matrix* m, const double* d_inv, const double* x0,
+                  int iters, double* rho) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(m);
+    SAG_NOTNULL(rho);
+    Ctx& c = ctx->c;
+    const Matrix& M = m->m;
+    SAG_REQUIRE(M.nrows == M.ncols, SAG_DIMENSION_MISMATCH,
+                "power_rho_estimate: matrix must be square");
+    const int n = M.nrows;
+    *rho = 0.0;
+    if (n == 0) return;
+    SAG_NOTNULL(d_inv);
+    SAG_NOTNULL(x0);
+    DevBuf<double> x(n), y(n), di(n);
+    std::vector<double> hy(n);
+    SAG_CUDA(cudaMemcpyAsync(x.p, x0, 8 * (size_t)n, cudaMemcpyDefault, c.stream));
+    SAG_CUDA(cudaMemcpyAsync(di.p, d_inv, 8 * (size_t)n, cudaMemcpyDefault, c.stream));
+    const int g = std::max(1, std::min((n + 255) / 256, c.num_sms * 16));
+    for (int it = 0; it < iters; ++it) {
+      spmv_rn_scale_kernel<<<g, 256, 0, c.stream>>>(n, M.rp.p, M.ci.p, M.v.p, x.p, di.p, y.p);
+      SAG_LAUNCHED(c);
+      SAG_CUDA(cudaMemcpyAsync(hy.data(), y.p, 8 * (size_t)n, cudaMemcpyDeviceToHost, c.stream));
+      SAG_CUDA(cudaStreamSynchronize(c.stream));
+      // norm2 (sparse.cpp:217-221): a sequential sum, on the host
+      double s = 0.0;
+      for (double v : hy) s += v * v;
+      const double ny = std::sqrt(s);
+      if (ny == 0.0) {
+        *rho = 0.0;
+        return;
+      }
+      *rho = ny;
+      scale_div_kernel<<<g, 256, 0, c.stream>>>(n, y.p, ny, x.p);
+      SAG_LAUNCHED(c);
+    }
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
 

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <random>
 #include <string>
 #include <utility>
 
@@ -400,14 +401,28 @@ struct DeviceSetup {
   Step coarsen(const SparseMatrix& a, const DevM& da, const std::vector<double>& nullvec,
                bool& stagnated) {
     Step s;
-    TentativeResult tent;
+    Aggregation agg;
     double omega = 0.0;
     bool stop = false;
     // rho(D^-1 A): evolution_soc (amg.cpp:47-49) and smooth_prolongator
-    // (amg.cpp:227-229) estimate it identically -- once here, on the host
-    // (its start vector is the reference's mt19937 stream)
+    // (amg.cpp:227-229) estimate it identically -- once here: the start
+    // vector is the reference's mt19937 stream (host), the iterations'
+    // products on the device, their sequential norms on the host
     double rho = 0.0;
-    host([&] { rho = power_rho_estimate(a, inv_diagonal(a), 10); });
+    std::vector<double> dinv, x0;
+    host([&] {
+      dinv = inv_diagonal(a);
+      std::mt19937 rng(1234);  // power_rho_estimate's default seed (sparse.hpp:70-71)
+      std::uniform_real_distribution<double> dist(-1.0, 1.0);
+      x0.resize(a.nrows);
+      for (double& v : x0) v = dist(rng);
+      const double nx = norm2(x0);
+      if (nx == 0.0 || a.nrows == 0) x0.clear();
+      for (double& v : x0) v /= nx;
+    });
+    device([&] {
+      if (!x0.empty()) check(sag_power_rho(dev.handle(), da.h, dinv.data(), x0.data(), 10, &rho));
+    });
     StrengthGraph g;
     bool soc_on_device = false;
     if (cfg.use_evolution_soc) {
@@ -432,12 +447,11 @@ struct DeviceSetup {
                                   : symmetric_soc(a, cfg.sym_theta);
         ++soc_host;
       }
-      const Aggregation agg = aggregate(g);
+      agg = aggregate(g);
       if (agg.num_aggregates > 0.9 * a.nrows) {
         stop = true;
         return;
       }
-      tent = tentative_prolongator_with_nullvec(agg, nullvec);
       omega = cfg.omega_frac / rho;
     });
     if (stop) {
@@ -445,11 +459,15 @@ struct DeviceSetup {
       return s;
     }
     device([&] {
-      DevM dt(dev, tent.t);
+      // tentative_prolongator_with_nullvec (amg.cpp:184-205) on the device
+      DevM dt;
+      s.coarse_null.resize(agg.num_aggregates);
+      gpu::check(sag_tentative_prolongator(dev.handle(), static_cast<int>(agg.node_to_agg.size()),
+                                           agg.num_aggregates, agg.node_to_agg.data(),
+                                           nullvec.data(), &dt.h, s.coarse_null.data()));
       check(sag_smooth_prolongator(dev.handle(), da.h, dt.h, omega, &s.dp.h));
       s.p = to_host(dev, s.dp);
     });
-    s.coarse_null = std::move(tent.coarse_nullvec);
     return s;
   }
   // P^T K P on the device; the result kept on the device and copied out

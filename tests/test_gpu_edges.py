@@ -313,9 +313,9 @@ def test_set_parameters_recaptures_solve_graph(S):
     for eu, ep, om in points:
         dc.set_parameters(eu, ep, om)
         x, rep = S.solve_stokes(K0, rhs, dc, cfg)
-        _, fresh, _ = _device_dc(S, k0, d.nxyz0, levels, conf)
+        K0f, fresh, _ = _device_dc(S, k0, d.nxyz0, levels, conf)
         fresh.set_parameters(eu, ep, om)
-        xf, repf = S.solve_stokes(K0, rhs, fresh, cfg)
+        xf, repf = S.solve_stokes(K0f, rhs, fresh, cfg)
         assert rep.iterations == repf.iterations, (eu, ep, om)
         assert np.array_equal(x, xf), (eu, ep, om)
         d.set_parameters(eu, ep, om)

@@ -48,8 +48,9 @@ def _keys(kind, rng):
         return np.arange(20_000) % 37
     if kind == "binary":
         return rng.integers(0, 2, 50_000)
-    if kind == "random2M":
-        return rng.integers(0, 1 << 40, 2_000_000)
+    if kind == "random2M":  # (row, col) keys: both below 2^31, as int32 indices are
+        r = rng.integers(0, 1 << 20, 2_000_000).astype(np.uint64)
+        return (r << np.uint64(32)) | rng.integers(0, 1 << 31, r.size).astype(np.uint64)
     if kind == "rowcol":  # (row, col) keys of a banded matrix, many duplicates
         r = rng.integers(0, 5000, 300_000)
         c = np.clip(r + rng.integers(-20, 21, r.size), 0, 4999)

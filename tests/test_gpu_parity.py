@@ -107,20 +107,36 @@ def test_apply_vanka_parity(S, n):
         assert np.all(z == 0.0)  # tests/test_vanka.cpp:264-271
 
 
-@pytest.mark.parametrize("device", [False, True])
-def test_vanka_spmv_step(S, device):
-    """sag_vanka_spmv (x read once, y copied back under the sweep) equals
-    spmv + apply_vanka of the reference, with host (pinned) and device buffers."""
+@pytest.mark.parametrize("mode,sv,stages", [("device", False, 0), ("pinned", False, 0),
+                                             ("pinned", False, 1), ("pinned", False, 3),
+                                             ("pinned", False, 40), ("pageable", False, 0),
+                                             ("pinned", True, 0), ("pinned", True, 5)])
+def test_vanka_spmv_step(S, monkeypatch, mode, sv, stages):
+    """sag_vanka_spmv equals spmv + apply_vanka of the reference with device
+    buffers (x read once), pageable host buffers (staged, y copied back under
+    the sweep) and pinned host buffers -- the pipelined step: copy-in, patch
+    solves and host writes in stages -- bitwise the unpipelined results, for
+    any stage count, one-class (TH) and multi-class (SV: sub-warp) levels."""
     import torch
-    c, d, k0, levels, _ = ref_case(64)
-    rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0)
+    if stages:
+        monkeypatch.setenv("SAG_STREAMED_STAGES", str(stages))
+    if sv:
+        c = O.RefCase.build("cavity", True, "structured", 64)  # sub-warp classes
+        k0 = c.k0().csr()
+        nxyz = (c.n_x0, c.n_y0, c.n_p0)
+    else:
+        c, d, k0, levels, _ = ref_case(64)
+        nxyz = d.nxyz0
+    rv = O.RefVanka.build(O.RefMat.from_csr(k0), *nxyz, sv_triples=sv)
     K = S.SparseMatrix.from_csr(k0)
-    f = S.factor_patches(K, S.build_patches(K, *d.nxyz0), d.nxyz0[0] + d.nxyz0[1])
+    f = S.factor_patches(K, S.build_patches(K, *nxyz, sv_triples=sv), nxyz[0] + nxyz[1])
     x = O.splitmix64_uniform(k0.nrows)
-    if device:
+    if mode == "device":
         xt = torch.from_numpy(x).cuda()
         dt, yt = S.vanka_spmv_step(f, K, xt)
         dl, y = dt.cpu().numpy(), yt.cpu().numpy()
+    elif mode == "pageable":
+        dl, y = S.vanka_spmv_step(f, K, x.copy())
     else:
         xh = torch.from_numpy(x).pin_memory().numpy()
         dh = torch.empty(k0.nrows, dtype=torch.float64).pin_memory().numpy()
@@ -265,6 +281,30 @@ def test_apply_vanka_sv_subwarp(S):
     want = rv.relax(x0, r, 1, 2, 0.78)
     got = S.vanka_relax(K, f, x0.copy(), r, 1, 2, 0.78)
     assert rel_inf(got, want) <= 1e-11
+
+
+def test_apply_vanka_sv_fixed_shape(S, monkeypatch):
+    # the interior element triples (nx = ny = 6, np = 3) run on the
+    # fixed-shape kernel: same operations as the sub-warp kernel, so the sweep
+    # is bitwise the one with that class switched off, and within 1e-12 of
+    # the reference; the factor payload exports unchanged
+    c, d, k0, levels, _ = ref_case(32, sv=True, cfg=dict(omega0=0.78, eta_p=2.68))
+    rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0, sv_triples=True)
+    K = S.SparseMatrix.from_csr(k0)
+    p = S.build_patches(K, *d.nxyz0, sv_triples=True)
+    f = S.factor_patches(K, p, d.nxyz0[0] + d.nxyz0[1])
+    kinds = [k[0] for k in f.classes()]
+    assert any(k.startswith("vanka_fixed_kernel") for k in kinds), kinds
+    r = O.splitmix64_uniform(k0.nrows)
+    z = S.apply_vanka(f, r)
+    assert rel_inf(z, rv.apply(r)) <= TOL
+    monkeypatch.setenv("SAG_VANKA_FIXED", "0")
+    f0 = S.factor_patches(K, p, d.nxyz0[0] + d.nxyz0[1])
+    assert not any(k[0].startswith("vanka_fixed_kernel") for k in f0.classes())
+    assert np.array_equal(z, S.apply_vanka(f0, r))
+    got, want = f.export(p.export()), rv.factors()
+    for key in ("uhat", "bhat", "sinv", "weights"):
+        assert np.array_equal(got[key], want[key]), key
 
 
 def test_singular_patch_raises(S):

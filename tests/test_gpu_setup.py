@@ -144,3 +144,60 @@ def test_spgemm_drops_exact_cancellation_and_keeps_empty_rows():
     eye = S.SparseMatrix(3, 3, [0, 1, 2, 3], [0, 1, 2], [1.0, 1.0, 1.0])
     g = S.galerkin_triple(eye, a).to_csr()
     assert list(g[0]) == [0, 2, 2, 4] and list(g[2]) == [1.0, 1.0, 2.0, 3.0]
+
+
+def test_tentative_prolongator_device():
+    # amg.cpp:184-205: per-aggregate norms summed in node order, T = nullvec
+    # / norm with exact zeros dropped (from_triplets), coarse nullvec = norms;
+    # an aggregate with a zero norm (or no node) raises
+    import math
+    import paper_2306_06795_b200 as S
+    rng = np.random.default_rng(5)
+    n, nc = 5000, 700
+    agg = rng.permutation(np.arange(n) % nc).astype(np.int32)
+    nv = rng.standard_normal(n)
+    nv[::97] = 0.0
+    t, cn = S.tentative_prolongator(agg, nc, nv)
+    want = np.zeros(nc)
+    for i in range(n):                   # the reference's loop, in order
+        want[agg[i]] += nv[i] * nv[i]
+    want = np.array([math.sqrt(v) for v in want])
+    assert cn.tobytes() == want.tobytes()
+    csr = t.to_csr()
+    keep = nv != 0.0
+    assert np.array_equal(np.diff(csr.rp), keep.astype(np.int32))
+    assert np.array_equal(csr.ci, agg[keep])
+    assert csr.v.tobytes() == (nv[keep] / want[agg[keep]]).tobytes()
+    with pytest.raises(S.Error):
+        S.tentative_prolongator(np.zeros(4, np.int32), 2, np.ones(4))   # aggregate 1 empty
+    with pytest.raises(S.Error):
+        S.tentative_prolongator(np.array([0, 1], np.int32), 2, np.array([1.0, 0.0]))
+
+
+def test_power_rho_device():
+    # sparse.cpp:239-261 with the reference's start vector and sequential norms
+    import paper_2306_06795_b200 as S
+    c = O.RefCase.build("cavity", False, "structured", 16)
+    k = c.k0().csr()
+    a = O.Csr(k.nrows, k.nrows, k.rp, k.ci, k.v)
+    n = k.nrows
+    d = np.array([1.0 / a.v[a.rp[r]:a.rp[r + 1]][a.ci[a.rp[r]:a.rp[r + 1]] == r][0]
+                  if (a.ci[a.rp[r]:a.rp[r + 1]] == r).any() else 1.0 for r in range(n)])
+    x = np.random.default_rng(1).uniform(-1, 1, n)
+    x = x / np.sqrt(np.sum(x * x))
+    rho = S.power_rho(S.SparseMatrix.from_csr(k), d, x, 10)
+    xr = x.copy()
+    ref = 0.0
+    for _ in range(10):                  # the reference loop with row-ordered sums
+        y = np.empty(n)
+        for r in range(n):
+            s = 0.0
+            for q in range(a.rp[r], a.rp[r + 1]):
+                s += a.v[q] * xr[a.ci[q]]
+            y[r] = s * d[r]
+        s = 0.0
+        for v in y:
+            s += v * v
+        ref = float(np.sqrt(s))
+        xr = y / ref
+    assert rho == ref
