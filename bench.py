@@ -13,10 +13,11 @@ by all ranks (GDOF/s). Inputs (K0 0.48 GB + Vanka factors 1.4 GB) exceed the
   python bench.py --impl reference      # the reference's CPU path, host cores
 
 Multi-GPU (torchrun, N > 1; --dist at N = 1): K0's rows and Vanka patches are
-partitioned across the ranks in rank-local numbering
-(paper_2306_06795_b200.partition, .dsolve) with NCCL halo exchanges (strong
-scaling); the line also carries the distributed FGMRES + DC-all solve. Times
-are CUDA events on libsag's stream, max over ranks.
+partitioned across the ranks in rank-local numbering by libsag's planner with
+NCCL halo exchanges, through the C-ABI (sag_dist_*; strong scaling); the line
+also carries the distributed FGMRES + DC-all solve (one CUDA graph with the
+collectives captured). Times are CUDA events on libsag's stream, max over
+ranks.
 
 roofline: the dominant kernel is the Vanka patch kernel; its algorithmic bytes
 are those of the representation it streams (factor blobs incl. dof indices,
@@ -365,158 +366,99 @@ def run_reference(args, ws, rank):
 
 
 # ------------------------------------------------------- GPU arm, N > 1
-def dist_solve(case, rs, levels, be, comm, dev, ws, args):
-    """The distributed FGMRES(30) + DC-all solve on this rank's partition
-    (dsolve.DistSolver), timed after one warm-up solve, max over ranks."""
-    import torch
-    import torch.distributed as dist
-
-    import paper_2306_06795_b200 as S
-    from paper_2306_06795_b200.dsolve import DistSolver
-
-    scfg = S.SolverConfig(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
-                          enclosed_flow=case.enclosed)
-    ts0 = time.perf_counter()
-    solver = DistSolver(rs, levels, scfg, be, comm)
-    torch.cuda.synchronize(dev)
-    setup_s = time.perf_counter() - ts0
-    rhs = be.from_host(case.rhs()[rs.l2g])
-    xs = be.vec(rs.nl)
-    solver.solve(rhs, xs)   # warm-up (graph captures)
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    ts = time.perf_counter()
-    rep = solver.solve(rhs, xs)
-    torch.cuda.synchronize(dev)
-    t_solve = dist_max(time.perf_counter() - ts, ws)
-    solver.close()
-    return {"gpu_s": t_solve, "iterations": rep.iterations,
-            "final_relative_residual": rep.final_relative_residual,
-            "converged": rep.converged, "setup_s": setup_s,
-            "prec_cuda_graph": solver.graph is not None,
-            "path": "dsolve.DistSolver (partitioned K0/L0, agglomerated coarse levels, "
-                    "NCCL all-reduce dots)",
-            "reference": golden_solve(args.config) and {
-                k: golden_solve(args.config)[k] for k in ("iterations", "cpu_s_1core",
-                                                          "final_relative_residual")}}
-
-
 def run_dist(args, ws, rank, local):
-    """Strong scaling across the ranks of one node: K0's rows and
-    Vanka patches partitioned in rank-local numbering
-    (paper_2306_06795_b200.partition), forward halo of x and reverse halo of
-    the Vanka partial sums over NCCL point-to-point (NVLink), rank-local
-    libsag kernels (paper_2306_06795_b200.dsolve.DistStep). Unless --no-solve,
-    also the distributed FGMRES(30) + DC-all solve (dsolve.DistSolver: L0
-    partitioned the same way, coarser levels agglomerated, MGS dots as
-    all-reduces)."""
+    """Strong scaling across the ranks of one node through the
+    C-ABI (sag_dist_*: the path gpu::DistDCPreconditioner drives): K0's rows
+    and Vanka patches partitioned in rank-local numbering by libsag's planner,
+    forward / reverse halos and the FGMRES all-reduces over NCCL (NVLink),
+    levels below level 0 agglomerated. The step is the partitioned Vanka
+    sweep + SpMV; the solve is the whole distributed FGMRES(30) + DC-all as one
+    CUDA graph (collectives captured)."""
     import torch
     import torch.distributed as dist
 
     import paper_2306_06795_b200 as S
-    from paper_2306_06795_b200.dsolve import Comm, DistSolver, DistStep, LibsagBackend
-    from paper_2306_06795_b200.partition import build_rank_systems
 
     cfg = CONFIGS[args.config]
     if cfg["sv"]:
         raise SystemExit("bench --gpus N: the partitioned path covers Taylor-Hood configs")
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    own_pg = not dist.is_initialized()
-    if own_pg:  # --dist on one GPU without torchrun
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29561")
-        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
     t0 = time.perf_counter()
     case = host_case(cfg)
     k0 = case.k0()
     levels = case.levels()
     host_setup_s = time.perf_counter() - t0
     n = k0.nrows
-    t1 = time.perf_counter()
-    l0, p0, nxyz_l0 = levels[0]
-    rs = build_rank_systems(ws, k0, l0, p0, case.nxyz0, nxyz_l0, ranks=[rank])[0]
-    plan_s = time.perf_counter() - t1
-    # libsag launches on a torch-owned stream: tensors, NCCL work and libsag
-    # kernels share it, and tearing the context down never destroys a stream
-    # torch still references
     stream = torch.cuda.Stream(device=dev)
     ctx = S.Context(local, stream=stream.cuda_stream)
-    comm = Comm(dist, torch)
+    uid = [S.nccl_unique_id() if rank == 0 else None]
+    if ws > 1:
+        dist.broadcast_object_list(uid, src=0)
+    comm = S.Comm(ctx, ws, rank, nccl_id=uid[0])
+    scfg = S.SolverConfig(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500,
+                          enclosed_flow=case.enclosed)
+    t1 = time.perf_counter()
+    ds = S.DistSolver(comm, k0, case.nxyz0, levels, scfg)
+    torch.cuda.synchronize(dev)
+    setup_gpu_s = time.perf_counter() - t1
+    nl = ds.nl
+    xg = splitmix64_uniform(n)
     with torch.cuda.stream(stream):
-        be = LibsagBackend(ctx, dev, torch, stream)
-        t2 = time.perf_counter()
-        step = DistStep(rs, be, comm)
+        x = torch.from_numpy(xg[ds.l2g]).to(dev)
+        delta = torch.empty(nl, dtype=torch.float64, device=dev)
+        y = torch.empty(nl, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize(dev)
+    for _ in range(max(args.warmup, 3)):
+        ds.step(x, delta, y)
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local) if rank == 0 else None
+    barrier(ws)
+    l0n = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ds.step(x, delta, y)
+    e1.record(stream)
+    e1.synchronize()
+    launches = ctx.launch_count() - l0n
+    t_steps = dist_max(e0.elapsed_time(e1) / 1e3, ws)
+    # e2e: this rank's local inputs from pinned host memory, outputs back
+    xh = torch.from_numpy(xg[ds.l2g]).pin_memory().numpy()
+    dh = torch.empty(nl, dtype=torch.float64).pin_memory().numpy()
+    yh = torch.empty(nl, dtype=torch.float64).pin_memory().numpy()
+    ke = max(args.steps // 4, 5)
+    for _ in range(2):
+        ds.step(xh, dh, yh)
+    barrier(ws)
+    te0 = time.perf_counter()
+    for _ in range(ke):
+        ds.step(xh, dh, yh)
+    t_e2e = dist_max((time.perf_counter() - te0) / ke, ws)
+    clk = clocks.stop() if clocks else None
+    solve = None
+    if not args.no_solve:
+        rhs = case.rhs()[ds.l2g]
+        ds.solve(rhs)  # warm-up: graph capture
         torch.cuda.synchronize(dev)
-        setup_gpu_s = time.perf_counter() - t2
-        x = be.from_host(splitmix64_uniform(n)[rs.l2g])
-        delta, y = be.vec(rs.nl), be.vec(rs.nl)
-        dist.barrier()  # a collective before the first point-to-point batch
-        for _ in range(max(args.warmup, 3)):
-            step.step(x, delta, y)
-        torch.cuda.synchronize(dev)
-        clocks = ClockSampler(local) if rank == 0 else None
-        dist.barrier()
-        torch.cuda.synchronize(dev)
-        l0n = ctx.launch_count()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            step.step(x, delta, y)
-        e1.record(stream)
-        e1.synchronize()
-        launches = ctx.launch_count() - l0n
-        t_steps = dist_max(e0.elapsed_time(e1) / 1e3, ws)
-        # per-rank patch kernel (roofline of the dominant kernel)
-        f = step.k0.f_int if step.k0.f_int is not None else step.k0.f_bnd
-        xp, dp = S.C.c_void_p(x.data_ptr()), S.C.c_void_p(delta.data_ptr())
-        kper = max(args.steps // 2, 10)
-        e0.record(stream)
-        for _ in range(kper):
-            S._check(S.lib().sag_apply_vanka_stage(ctx.h, f.h, xp, dp, 1))
-        e1.record(stream)
-        e1.synchronize()
-        t_patch = e0.elapsed_time(e1) / 1e3 / kper
-        dist.barrier()
-        # e2e: owned inputs from pinned host memory, owned outputs back
-        own = torch.as_tensor(np.nonzero(rs.owned)[0], device=dev)
-        xh = torch.from_numpy(splitmix64_uniform(n)[rs.l2g[rs.owned.astype(bool)]]).pin_memory()
-        dh = torch.empty(rs.n_own, dtype=torch.float64).pin_memory()
-        yh = torch.empty(rs.n_own, dtype=torch.float64).pin_memory()
-        ke = max(args.steps // 4, 5)
-
-        def e2e_step():
-            x.index_copy_(0, own, xh.to(dev, non_blocking=True))
-            step.step(x, delta, y)
-            dh.copy_(delta.index_select(0, own), non_blocking=True)
-            yh.copy_(y.index_select(0, own), non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
-
-        for _ in range(2):  # warm-up: allocator, pinned staging
-            e2e_step()
-        torch.cuda.synchronize(dev)
-        dist.barrier()
-        te0 = time.perf_counter()
-        for _ in range(ke):
-            e2e_step()
-        t_e2e = dist_max((time.perf_counter() - te0) / ke, ws)
-        clk = clocks.stop() if clocks else None
-
-        solve = None
-        if not args.no_solve:
-            step.close()
-            del step
-            try:
-                solve = dist_solve(case, rs, levels, be, comm, dev, ws, args)
-            except Exception as e:  # the step's line must survive a failing solve
-                solve = {"error": repr(e)[:300]}
-    ghosts = dist_max(float(rs.ghost_count()), ws)
-    own_max = dist_max(float(rs.n_own), ws)
-    t_patch = dist_max(t_patch, ws)
+        barrier(ws)
+        ts = time.perf_counter()
+        xs, rep = ds.solve(rhs)
+        t_solve = dist_max(time.perf_counter() - ts, ws)
+        g = golden_solve(args.config)
+        solve = {"gpu_s": t_solve, "iterations": rep.iterations,
+                 "final_relative_residual": rep.final_relative_residual,
+                 "converged": rep.converged, "setup_s": setup_gpu_s,
+                 "path": "sag_dist_solve_stokes (partitioned K0/L0, agglomerated levels >= 1, "
+                         "NCCL all-reduces and halos, one CUDA graph)"}
+        if g:
+            solve["reference"] = {k: g[k] for k in ("iterations", "cpu_s_1core",
+                                                    "final_relative_residual")}
+    ghosts = dist_max(float(ds.ghosts), ws)
+    own_max = dist_max(float(ds.n_own), ws)
     if rank == 0:
         peak, peak_kind = peak_hbm()
-        b_p = vanka_patch_bytes(f, rs.nl)
         out = {
             "metric": METRIC, "value": n / (t_steps / args.steps) / 1e9, "unit": "GDOF/s",
             "n_gpus": ws, "steps": args.steps, "warmup": max(args.warmup, 3),
@@ -524,29 +466,27 @@ def run_dist(args, ws, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: reference build_case cavity + splitmix64 x (SURVEY 8(d))",
             "config": config_dict(cfg, k0),
-            "layout": {"parallelism": f"row/patch partition x{ws}, NCCL halo",
+            "layout": {"parallelism": f"row/patch partition x{ws}, NCCL halos (sag_dist)",
                        "max_owned_dofs_per_rank": int(own_max),
                        "max_ghost_dofs_per_rank": int(ghosts),
                        "l2": "inputs exceed L2; no flush"},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "kernel": "vanka_patch_kernel (rank 0's interior K0 patches)",
-                         "achieved": b_p / t_patch / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": b_p / t_patch / 1e9 / peak, "traffic": None,
-                         "algorithmic_bytes": b_p, "peak_kind": peak_kind,
-                         "bytes_def": "factor blobs + 8 n_local (r) + 8 slots"},
+            "roofline": {"bound": "hbm", "kernel": "partitioned step (Vanka sweep + SpMV)",
+                         "achieved": None, "peak": peak, "unit": "GB/s", "frac": None,
+                         "traffic": None, "peak_kind": peak_kind,
+                         "note": "per-kernel roofline: the single-GPU line (bench.py without "
+                                 "--dist); the partitioned kernels are the same kernels"},
             "e2e": {"value": n / t_e2e / 1e9, "unit": "GDOF/s",
-                    "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 16 * n},
-            "setup": {"host_reference_setup_s": host_setup_s, "partition_plan_s": plan_s,
-                      "gpu_setup_s": setup_gpu_s},
+                    "h2d_bytes_per_step": 8 * nl, "d2h_bytes_per_step": 16 * nl,
+                    "call": "sag_dist_step, pinned host buffers (rank-local vectors)"},
+            "setup": {"host_reference_setup_s": host_setup_s, "gpu_setup_s": setup_gpu_s},
         }
         if solve:
             out["solve"] = solve
         if clk:
             out["clocks"] = clk
         emit(out)
-    if own_pg:
-        torch.cuda.synchronize(dev)
-        dist.destroy_process_group()
+    del ds, comm
 
 
 # ------------------------------------------------------------------ GPU arm

@@ -392,6 +392,88 @@ int sag_reduce_dirichlet(sag_ctx* ctx, const sag_matrix* a_full, const sag_matri
                          sag_matrix** a_red, sag_matrix** b_red, double* lift_x, double* lift_y,
                          double* rhs_p);
 
+/* ---- partitioned solve: multi-GPU behind the C-ABI ----------
+ * One process per GPU. A communicator carries the collectives: NCCL (rank 0
+ * gets an id from sag_nccl_unique_id and the caller broadcasts it), or the
+ * caller's own host-staged transport (sag_comm_ops: gloo, MPI, sockets; every
+ * call blocking and made by all ranks in the same order). sag_dist_create
+ * plans this rank's share of the row/patch partition from the GLOBAL host
+ * CSR arrays every rank passes (K0, the low-order hierarchy and its
+ * prolongators as built by build_monolithic_hierarchy, amg.hpp:99), factors
+ * its patches and builds the agglomerated coarse levels; vectors are
+ * rank-local (sag_dist_local_dofs: local -> global ids, owned flags). The
+ * reference has no distributed path; the semantics are solve_stokes'
+ * (preconditioner.cpp:229-259) over DCPreconditioner::apply
+ * (preconditioner.cpp:114-153) with Taylor-Hood transfers. */
+typedef struct sag_csr {
+  int nrows, ncols;
+  const int* row_offsets;   /* nrows + 1 */
+  const int* col_indices;   /* row_offsets[nrows] */
+  const double* values;
+} sag_csr;
+typedef struct sag_comm sag_comm;
+typedef struct sag_dist sag_dist;
+typedef struct sag_plan sag_plan;
+typedef struct sag_comm_ops {
+  void* user;
+  /* buf (host, n doubles) <- the element-wise sum over all ranks; 0 on success */
+  int (*allreduce_sum)(void* user, double* buf, long long n);
+  /* send sbuf[i] (scount[i] doubles) to rank to[i] and receive rbuf[j]
+   * (rcount[j] doubles) from rank from[j], all at once; 0 on success */
+  int (*exchange)(void* user, int nsend, const int* to, const double* const* sbuf,
+                  const long long* scount, int nrecv, const int* from, double* const* rbuf,
+                  const long long* rcount);
+} sag_comm_ops;
+int sag_nccl_unique_id(unsigned char* id /* 128 bytes */);
+int sag_comm_create_nccl(sag_ctx* ctx, int nranks, int rank, const unsigned char* id,
+                         sag_comm** out);
+int sag_comm_create_host(int nranks, int rank, const sag_comm_ops* ops, sag_comm** out);
+int sag_comm_destroy(sag_comm* comm);
+/* buf (device, n doubles) <- the sum over the ranks (blocking) */
+int sag_comm_allreduce(sag_ctx* ctx, sag_comm* comm, double* buf, long long n);
+/* levels[0..nlevels) / prolongators[0..nlevels-1) / level_nxyz[3 l + {0,1,2}]:
+ * the low-order hierarchy (level 0 on the K0 dofs). DC-all / DC-LO / DC-HO,
+ * nu1, nu2 <= 1. */
+int sag_dist_create(sag_ctx* ctx, sag_comm* comm, const sag_csr* k0, int n_x, int n_y, int n_p,
+                    int nlevels, const sag_csr* levels, const sag_csr* prolongators,
+                    const int* level_nxyz, const sag_solver_config* cfg, sag_dist** out);
+int sag_dist_destroy(sag_dist* d);
+/* out = [local dofs, owned, ghosts, neighbours, own K0 patches, level-1 rows,
+ * local velocity dofs] */
+int sag_dist_info(const sag_dist* d, long long* out);
+int sag_dist_local_dofs(const sag_dist* d, long long* l2g, unsigned char* owned);
+/* The partitioned hot step on local vectors: delta = apply_vanka(x)
+ * (vanka.cpp:151-184), y = K0 x (sparse.cpp:78-91) at the owned dofs. */
+int sag_dist_step(sag_ctx* ctx, sag_dist* d, const double* x, double* delta, double* y);
+/* solve_stokes over the partition: rhs, x local (owned entries valid); the
+ * report and history are the global ones (identical on every rank). */
+int sag_dist_solve_stokes(sag_ctx* ctx, sag_dist* d, const double* rhs, double* x,
+                          sag_krylov_report* report, double* history, int history_cap);
+/* The partition plan alone (host only, no device): for tests and tools.
+ * sag_plan_array copies one array out (out may be NULL to query *count). */
+enum sag_plan_item {
+  SAG_PLAN_INFO = 0,       /* [local dofs, local velocity dofs, patch lo, hi, level-1 rows,
+                              forward-send peers, forward-receive peers] (int64) */
+  SAG_PLAN_L2G = 1,        /* int64 */
+  SAG_PLAN_OWNED = 2,      /* uint8 */
+  SAG_PLAN_FWD_SEND = 3,   /* int32 local ids for `peer` */
+  SAG_PLAN_FWD_RECV = 4,
+  SAG_PLAN_REV_SEND = 5,
+  SAG_PLAN_REV_RECV = 6,
+  SAG_PLAN_EXT_RP = 7,     /* + 100 for the low-order level 0 instead of K0 */
+  SAG_PLAN_EXT_CI = 8,
+  SAG_PLAN_EXT_V = 9,
+  SAG_PLAN_INT_PVIDX = 10, /* interior patches' velocity lists */
+  SAG_PLAN_BND_PVIDX = 11,
+  SAG_PLAN_WEIGHTS = 12,
+  SAG_PLAN_P_RP = 13,
+  SAG_PLAN_P_CI = 14
+};
+int sag_plan_create(int nranks, int rank, const sag_csr* k0, const sag_csr* l0, const sag_csr* p0,
+                    int n_x, int n_y, int n_p, sag_plan** out);
+int sag_plan_destroy(sag_plan* plan);
+int sag_plan_array(const sag_plan* plan, int which, int peer, void* out, long long* count);
+
 /* ---- partitioned-solve primitives ---------------------------
  * Building blocks for a caller that row-partitions the solve across ranks
  * (one process per GPU, paper_2306_06795_b200/dist.py). All pointers are

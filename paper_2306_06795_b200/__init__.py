@@ -126,6 +126,19 @@ class sag_mesh2d(C.Structure):
                 ("vertices", vp), ("triangles", vp), ("tri_edges", vp)]
 
 
+class sag_csr(C.Structure):
+    _fields_ = [("nrows", C.c_int), ("ncols", C.c_int), ("row_offsets", vp),
+                ("col_indices", vp), ("values", vp)]
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, vp, vp, C.c_longlong)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, vp, C.c_int, vp, vp, vp, C.c_int, vp, vp, vp)
+
+
+class sag_comm_ops(C.Structure):
+    _fields_ = [("user", vp), ("allreduce_sum", ALLREDUCE_FN), ("exchange", EXCHANGE_FN)]
+
+
 #: every entry point declared in include/sag.h, with its ctypes signature
 SIGNATURES = {
     "sag_last_error": (C.c_char_p, []),
@@ -208,6 +221,26 @@ SIGNATURES = {
                                    vp, vp]),
     "sag_reduce_dirichlet": (C.c_int, [vp, vp, vp, C.c_int, vp, vp, vp, C.POINTER(vp),
                                        C.POINTER(vp), vp, vp, vp]),
+    # partitioned solve (multi-GPU)
+    "sag_nccl_unique_id": (C.c_int, [vp]),
+    "sag_comm_create_nccl": (C.c_int, [vp, C.c_int, C.c_int, vp, C.POINTER(vp)]),
+    "sag_comm_create_host": (C.c_int, [C.c_int, C.c_int, C.POINTER(sag_comm_ops),
+                                       C.POINTER(vp)]),
+    "sag_comm_destroy": (C.c_int, [vp]),
+    "sag_comm_allreduce": (C.c_int, [vp, vp, vp, C.c_longlong]),
+    "sag_dist_create": (C.c_int, [vp, vp, C.POINTER(sag_csr), C.c_int, C.c_int, C.c_int,
+                                  C.c_int, vp, vp, vp, C.POINTER(sag_solver_config),
+                                  C.POINTER(vp)]),
+    "sag_dist_destroy": (C.c_int, [vp]),
+    "sag_dist_info": (C.c_int, [vp, i64p]),
+    "sag_dist_local_dofs": (C.c_int, [vp, vp, vp]),
+    "sag_dist_step": (C.c_int, [vp, vp, vp, vp, vp]),
+    "sag_dist_solve_stokes": (C.c_int, [vp, vp, vp, vp, C.POINTER(sag_krylov_report), vp,
+                                        C.c_int]),
+    "sag_plan_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(sag_csr), C.POINTER(sag_csr),
+                                  C.POINTER(sag_csr), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "sag_plan_destroy": (C.c_int, [vp]),
+    "sag_plan_array": (C.c_int, [vp, C.c_int, C.c_int, vp, i64p]),
     # partitioned-solve primitives (device pointers, no host sync)
     "sag_dot_async": (C.c_int, [vp, C.c_int, vp, vp, vp, vp]),
     "sag_axpy_async": (C.c_int, [vp, C.c_int, vp, C.c_double, vp, vp]),
@@ -911,3 +944,170 @@ def solve_stokes(k0: SparseMatrix, rhs, prec, cfg: SolverConfig, x=None):
     return xo, KrylovReport(bool(rep.converged), rep.iterations,
                             hist[:min(rep.history_len, cap)].copy(),
                             rep.final_relative_residual)
+
+
+# ------------------------------------------------------- multi-GPU (8(e)) --
+def _csr_struct(m, keep):
+    rp = np.ascontiguousarray(m.rp, dtype=np.int32)
+    ci = np.ascontiguousarray(m.ci, dtype=np.int32)
+    v = np.ascontiguousarray(m.v, dtype=np.float64)
+    keep.extend([rp, ci, v])
+    return sag_csr(int(m.nrows), int(m.ncols), rp.ctypes.data, ci.ctypes.data, v.ctypes.data)
+
+
+_PLAN_DTYPES = {0: np.int64, 1: np.int64, 2: np.uint8, 9: np.float64, 12: np.float64}
+
+
+def partition_plan(nranks: int, rank: int, k0, l0, p0, nxyz):
+    """libsag's partition plan of one rank (host only; sag_plan_*): a dict of
+    the arrays partition.build_rank_systems states in numpy."""
+    keep = []
+    ks, ls = _csr_struct(k0, keep), _csr_struct(l0, keep)
+    ps = _csr_struct(p0, keep) if p0 is not None else None
+    h = vp()
+    _check(lib().sag_plan_create(int(nranks), int(rank), C.byref(ks), C.byref(ls),
+                                 C.byref(ps) if ps is not None else None, *map(int, nxyz),
+                                 C.byref(h)))
+
+    def arr(which, peer=0):
+        cnt = C.c_longlong()
+        _check(lib().sag_plan_array(h, which, peer, None, C.byref(cnt)))
+        dt = _PLAN_DTYPES.get(which % 100, np.int32)
+        out = np.empty(max(cnt.value, 1), dtype=dt)
+        _check(lib().sag_plan_array(h, which, peer, out.ctypes.data, C.byref(cnt)))
+        return out[:cnt.value]
+    try:
+        info = arr(0)
+        res = {"info": info, "l2g": arr(1), "owned": arr(2)}
+        for name, w in (("fwd_send", 3), ("fwd_recv", 4), ("rev_send", 5), ("rev_recv", 6)):
+            res[name] = {q: arr(w, q) for q in range(nranks) if q != rank and len(arr(w, q))}
+        for lvl, base in (("K0", 0), ("L0", 100)):
+            res[lvl] = {k: arr(base + w) for k, w in (("ext_rp", 7), ("ext_ci", 8), ("ext_v", 9),
+                                                       ("int_vidx", 10), ("bnd_vidx", 11),
+                                                       ("weights", 12))}
+        res["p_rp"], res["p_ci"] = arr(13), arr(14)
+        return res
+    finally:
+        lib().sag_plan_destroy(h)
+
+
+def nccl_unique_id() -> bytes:
+    b = (C.c_ubyte * 128)()
+    _check(lib().sag_nccl_unique_id(b))
+    return bytes(b)
+
+
+class Comm:
+    """sag_comm: NCCL (nccl_id: 128 bytes from rank 0's nccl_unique_id) or the
+    caller's host-staged collectives (allreduce(np.ndarray) in place,
+    exchange(sends: [(peer, ndarray)], recvs: [(peer, ndarray)]))."""
+
+    def __init__(self, ctx: Context, nranks: int, rank: int, nccl_id: bytes = None,
+                 allreduce=None, exchange=None):
+        self.ctx, self.size, self.rank = ctx, nranks, rank
+        h = vp()
+        if nccl_id is not None:
+            b = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+            _check(lib().sag_comm_create_nccl(ctx.h, nranks, rank, b, C.byref(h)))
+            self._ops = None
+        else:
+            def ar(user, buf, n):
+                try:
+                    allreduce(np.ctypeslib.as_array(C.cast(buf, f64p), (n,)))
+                    return 0
+                except Exception:  # noqa: BLE001
+                    return 1
+
+            def ex(user, ns, to, sb, sc, nr, frm, rb, rc):
+                try:
+                    to_ = C.cast(to, i32p)
+                    sb_ = C.cast(sb, C.POINTER(f64p))
+                    sc_ = C.cast(sc, i64p)
+                    fr_ = C.cast(frm, i32p)
+                    rb_ = C.cast(rb, C.POINTER(f64p))
+                    rc_ = C.cast(rc, i64p)
+                    sends = [(to_[i], np.ctypeslib.as_array(sb_[i], (sc_[i],))) for i in range(ns)]
+                    recvs = [(fr_[i], np.ctypeslib.as_array(rb_[i], (rc_[i],))) for i in range(nr)]
+                    exchange(sends, recvs)
+                    return 0
+                except Exception:  # noqa: BLE001
+                    return 1
+            self._ops = sag_comm_ops(None, ALLREDUCE_FN(ar), EXCHANGE_FN(ex))
+            _check(lib().sag_comm_create_host(nranks, rank, C.byref(self._ops), C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def torch_host(ctx: Context, dist, torch):
+        """Host-staged collectives over torch.distributed (gloo)."""
+        def allreduce(a):
+            t = torch.from_numpy(a)
+            dist.all_reduce(t)
+
+        def exchange(sends, recvs):
+            ops = [dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(a)), q)
+                   for q, a in sends]
+            ops += [dist.P2POp(dist.irecv, torch.from_numpy(a), q) for q, a in recvs]
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+        return Comm(ctx, dist.get_world_size(), dist.get_rank(), allreduce=allreduce,
+                    exchange=exchange)
+
+    def __del__(self):
+        try:
+            lib().sag_comm_destroy(self.h)
+        except Exception:
+            pass
+
+
+class DistSolver:
+    """solve_stokes with the DC preconditioner over a row/patch partition, one
+    rank per process (sag_dist_*). k0 and the levels are the GLOBAL host CSR
+    arrays (every rank passes the same); vectors are rank-local: l2g / owned
+    map them to the global numbering."""
+
+    def __init__(self, comm: Comm, k0, nxyz0, levels, cfg: SolverConfig):
+        self.comm, self.ctx, self.cfg = comm, comm.ctx, cfg
+        keep = []
+        ks = _csr_struct(k0, keep)
+        lv = (sag_csr * len(levels))(*[_csr_struct(k, keep) for k, _, _ in levels])
+        pv = (sag_csr * max(len(levels) - 1, 1))(*[_csr_struct(p, keep) for _, p, _ in levels[:-1]])
+        nx = np.ascontiguousarray(np.array([v for _, _, t in levels for v in t]), dtype=np.int32)
+        c = cfg.to_c()
+        h = vp()
+        _check(lib().sag_dist_create(self.ctx.h, comm.h, C.byref(ks), *map(int, nxyz0),
+                                     len(levels), C.cast(lv, vp), C.cast(pv, vp),
+                                     nx.ctypes.data, C.byref(c), C.byref(h)))
+        self.h = h
+        info = np.zeros(7, dtype=np.int64)
+        _check(lib().sag_dist_info(h, info.ctypes.data_as(i64p)))
+        self.nl, self.n_own, self.ghosts, self.neighbours, self.patches, self.n1, \
+            self.n_u_loc = (int(v) for v in info)
+        self.l2g = np.empty(self.nl, dtype=np.int64)
+        self.owned = np.empty(self.nl, dtype=np.uint8)
+        _check(lib().sag_dist_local_dofs(h, self.l2g.ctypes.data, self.owned.ctypes.data))
+
+    def step(self, x, delta=None, y=None):
+        xp, xk = _vec_in(x, self.nl)
+        dp, d = _vec_out(delta, self.nl, like=x)
+        yp, yy = _vec_out(y, self.nl, like=x)
+        _check(lib().sag_dist_step(self.ctx.h, self.h, xp, dp, yp))
+        return d, yy
+
+    def solve(self, rhs, x=None):
+        bp, bk = _vec_in(rhs, self.nl)
+        xp, xo = _vec_out(x, self.nl, like=rhs)
+        rep = sag_krylov_report()
+        cap = self.cfg.max_iters + 2
+        hist = np.zeros(cap)
+        _check(lib().sag_dist_solve_stokes(self.ctx.h, self.h, bp, xp, C.byref(rep),
+                                           C.c_void_p(hist.ctypes.data), cap))
+        return xo, KrylovReport(bool(rep.converged), rep.iterations,
+                                hist[:min(rep.history_len, cap)].copy(),
+                                rep.final_relative_residual)
+
+    def __del__(self):
+        try:
+            lib().sag_dist_destroy(self.h)
+        except Exception:
+            pass

@@ -50,6 +50,8 @@ def hlib():
         L.sagh_case_hierarchy_gpu.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.sagh_case_scalar_hierarchy_gpu.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.sagh_case_assembly_gpu.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+        L.sagh_case_solve_dist.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]
         L.sagh_case_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                       C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                       C.c_void_p]
@@ -153,6 +155,17 @@ class HostCase:
         return dict(sys0_diff=int(out[0]), sys1_diff=int(out[1]), k0_equal=bool(out[2]),
                     device_s=float(out[3]), reference_s=float(out[4]) if out[4] >= 0 else None,
                     sys0_s=float(out[5]), sys1_s=float(out[6]), k0_s=float(out[7]))
+
+    def solve_dist_dropin(self, device=0):
+        """gpu::DistDCPreconditioner (the C++ multi-GPU drop-in) at one rank."""
+        x = np.empty(self.n0)
+        rep = np.zeros(2, dtype=np.int32)
+        res = C.c_double()
+        if hlib().sagh_case_solve_dist(self.h, device, x.ctypes.data, rep.ctypes.data,
+                                       C.byref(res)):
+            raise RuntimeError(hlib().sagh_last_error().decode())
+        return x, dict(converged=bool(rep[0]), iterations=int(rep[1]),
+                       final_relative_residual=res.value)
 
     def rhs(self):
         r = np.empty(self.n0)

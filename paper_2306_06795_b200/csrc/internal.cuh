@@ -85,10 +85,7 @@ struct Vanka {
   // per-patch payload bases and shapes (host copies, for export)
   std::vector<long long> h_dbase, h_ibase;
   std::vector<int> h_nx, h_nv, h_np;
-  std::vector<int> blob_patch;  // patch id at each blob position (class order)
-  // the host-buffer step of sag_vanka_spmv pipelined in stages (built on
-  // first use, for one operator)
-  std::shared_ptr<struct StreamPlan> stream_plan;
+
 };
 
 // Krylov scalar state in device memory (one per FGMRES instance); mirrors the
@@ -166,6 +163,8 @@ struct SpmvArgs {
 void launch_spmv(Ctx& c, const Matrix& m, const double* x, double* y, Epi e,
                  const SpmvArgs& a = SpmvArgs());
 void compute_norm_inf(Ctx& c, Matrix& m);
+// y[r0, r1) = (K x)[r0, r1)  (Store)
+void launch_spmv_rows(Ctx& c, const Matrix& m, int r0, int r1, const double* x, double* y);
 
 // deterministic BLAS-1 (reductions finish through Fin)
 void launch_dot(Ctx& c, int n, const double* a, const double* b, const Fin& fin,
@@ -243,6 +242,19 @@ void launch_kinit(Ctx& c, KState* st, int m, double tol, double bd, int hist_cap
                   bool keep_ref);
 void launch_copy(Ctx& c, int n, const double* x, double* y);
 void launch_zero(Ctx& c, int n, double* y);
+// partitioned-solve primitives on device scalars (sag_core.cu)
+void launch_fin_from(Ctx& c, const Fin& f, const double* tot);  // apply_fin(f, *tot)
+// *out = sum over i with mask[i] (all i when mask is null) of a_i b_i
+void launch_dot_mask(Ctx& c, int n, const double* a, const double* b, const unsigned char* mask,
+                     double* out);
+void launch_axpy_dev(Ctx& c, int n, const double* s, double sign, const double* x, double* y);
+void launch_div_dev(Ctx& c, int n, const double* x, const double* s, int take_sqrt, double* y);
+void launch_fgmres1_coef(Ctx& c, const double* ssq_r, const double* h00, const double* ssq_w,
+                         double* y0);
+void launch_sub_mean(Ctx& c, int n, const double* x, const double* sum, double count, double* y);
+void launch_axpby(Ctx& c, int n, double a, const double* x, double b, double* y);
+void launch_gather_idx(Ctx& c, int n, const int* idx, const double* src, double* dst);
+void launch_scatter_idx(Ctx& c, int n, const int* idx, const double* src, double* dst, int add);
 // y = x with the pressure block shifted by -(*mean)   (preconditioner.cpp:235-240)
 void launch_project(Ctx& c, int n, int n_u, const double* x, const double* mean, double* y);
 // y = eta_u * x (i < n_u), eta_p * x (i >= n_u)   (transfer.cpp:127-135)
@@ -259,6 +271,8 @@ void vanka_apply(Ctx& c, const Vanka& f, const double* r, double* delta,
                  const int* gate = nullptr);
 void vanka_apply_stage(Ctx& c, const Vanka& f, const double* r, double* delta, int stage);
 void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega);
+// the gather stage for dofs [d0, d1) only (delta = the unweighted-sum store)
+void vanka_gather_range(Ctx& c, const Vanka& f, int d0, int d1, double* delta);
 std::unique_ptr<Patches> build_patches_dev(Ctx& c, const Matrix& k, int n_x, int n_y, int n_p,
                                            bool sv_triples);
 std::unique_ptr<Patches> patches_from_lists(Ctx& c, int npatch, const int* pptr,

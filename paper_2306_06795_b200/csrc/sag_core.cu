@@ -234,10 +234,14 @@ __global__ void __launch_bounds__(256, 8) spmv_kernel(int nrows, const int* __re
 
 template <int G>
 static void spmv_dispatch_e(Ctx& c, const Matrix& m, const double* x, double* y, Epi e,
-                            const SpmvArgs& a) {
+                            const SpmvArgs& a, int r0 = 0, int r1 = -1) {
+  // rows [r0, r1) only (Store): row offsets are absolute, so the kernel runs
+  // on the shifted row-offset array and output
+  const int nrows = r1 < 0 ? m.nrows : r1 - r0;
+  y += r0;
   const int rows_per_block = 256 / G;
-  long long need = (m.nrows + rows_per_block - 1) / rows_per_block;
-  auto* rp = m.rp.p;
+  long long need = (nrows + rows_per_block - 1) / rows_per_block;
+  auto* rp = m.rp.p + r0;
   auto* ci = m.ci.p;
   auto* v = m.v.p;
   // persistent grid of exactly the resident blocks: a partial second wave of
@@ -257,7 +261,7 @@ static void spmv_dispatch_e(Ctx& c, const Matrix& m, const double* x, double* y,
 #define CASE(EE)                                                                              \
   case Epi::EE:                                                                               \
     spmv_kernel<G, Epi::EE><<<grid_of(spmv_kernel<G, Epi::EE>), 256, 0, c.stream>>>(          \
-        m.nrows, rp, ci, v, x, y, a, c.partials.p, c.ticket.p);                               \
+        nrows, rp, ci, v, x, y, a, c.partials.p, c.ticket.p);                                 \
     break;
     CASE(Store)
     CASE(Resid)
@@ -278,6 +282,17 @@ void launch_spmv(Ctx& c, const Matrix& m, const double* x, double* y, Epi e, con
     case 8: spmv_dispatch_e<8>(c, m, x, y, e, a); break;
     case 16: spmv_dispatch_e<16>(c, m, x, y, e, a); break;
     default: spmv_dispatch_e<32>(c, m, x, y, e, a); break;
+  }
+}
+void launch_spmv_rows(Ctx& c, const Matrix& m, int r0, int r1, const double* x, double* y) {
+  if (r1 <= r0) return;
+  const SpmvArgs a;
+  switch (m.group) {
+    case 2: spmv_dispatch_e<2>(c, m, x, y, Epi::Store, a, r0, r1); break;
+    case 4: spmv_dispatch_e<4>(c, m, x, y, Epi::Store, a, r0, r1); break;
+    case 8: spmv_dispatch_e<8>(c, m, x, y, Epi::Store, a, r0, r1); break;
+    case 16: spmv_dispatch_e<16>(c, m, x, y, Epi::Store, a, r0, r1); break;
+    default: spmv_dispatch_e<32>(c, m, x, y, Epi::Store, a, r0, r1); break;
   }
 }
 
@@ -967,6 +982,58 @@ __global__ void scatter_idx_kernel(int n, const int* __restrict__ idx, const dou
     const int d = idx[i];
     dst[d] = add ? dst[d] + src[i] : src[i];
   }
+}
+
+// internal launchers of the partitioned-solve primitives (no pointer-kind
+// queries: usable while a stream is being captured)
+__global__ void fin_from_kernel(Fin f, const double* tot) { apply_fin(f, *tot); }
+void launch_fin_from(Ctx& c, const Fin& f, const double* tot) {
+  fin_from_kernel<<<1, 1, 0, c.stream>>>(f, tot);
+  SAG_LAUNCHED(c);
+}
+void launch_dot_mask(Ctx& c, int n, const double* a, const double* b, const unsigned char* mask,
+                     double* out) {
+  Fin f;
+  f.kind = FIN_STORE;
+  f.out = out;
+  dot_mask_kernel<<<red_grid_fit(c, dot_mask_kernel, n), kRedBlock, 0, c.stream>>>(
+      n, a, b, mask, f, c.partials.p, c.ticket.p);
+  SAG_LAUNCHED(c);
+}
+void launch_axpy_dev(Ctx& c, int n, const double* s, double sign, const double* x, double* y) {
+  if (n <= 0) return;
+  axpy_dev_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, s, sign, x, y);
+  SAG_LAUNCHED(c);
+}
+void launch_div_dev(Ctx& c, int n, const double* x, const double* s, int take_sqrt, double* y) {
+  if (n <= 0) return;
+  div_dev_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, s, take_sqrt, y);
+  SAG_LAUNCHED(c);
+}
+void launch_fgmres1_coef(Ctx& c, const double* ssq_r, const double* h00, const double* ssq_w,
+                         double* y0) {
+  fgmres1_coef_kernel<<<1, 1, 0, c.stream>>>(ssq_r, h00, ssq_w, y0);
+  SAG_LAUNCHED(c);
+}
+void launch_sub_mean(Ctx& c, int n, const double* x, const double* sum, double count, double* y) {
+  if (n <= 0) return;
+  sub_mean_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, x, sum, count, y);
+  SAG_LAUNCHED(c);
+}
+void launch_axpby(Ctx& c, int n, double a, const double* x, double b, double* y) {
+  if (n <= 0) return;
+  axpby_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, a, x, b, y);
+  SAG_LAUNCHED(c);
+}
+void launch_gather_idx(Ctx& c, int n, const int* idx, const double* src, double* dst) {
+  if (n <= 0) return;
+  gather_idx_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, idx, src, dst);
+  SAG_LAUNCHED(c);
+}
+void launch_scatter_idx(Ctx& c, int n, const int* idx, const double* src, double* dst, int add) {
+  if (n <= 0) return;
+  scatter_idx_kernel<<<ew_grid(c, n), 256, 0, c.stream>>>(n, idx, src, dst, add);
+  SAG_LAUNCHED(c);
 }
 
 // ------------------------------------------------- scalar V-cycle tail --

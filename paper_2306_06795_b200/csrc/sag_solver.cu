@@ -9,12 +9,17 @@
 // fixed sequence of kernel launches with no host synchronisation (captured
 // once into a CUDA graph). The outer solve reads one small status record per
 // Arnoldi step to decide convergence, as krylov.cpp:95-97 does.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <vector>
 
+#include "dist_plan.hpp"
 #include "internal.cuh"
 
 namespace sag {
@@ -1734,6 +1739,853 @@ int sag_solve_stokes_uzawa(sag_ctx* ctx, const sag_matrix* k0, sag_uzawa* h, con
                 "solve_stokes: K0 does not match the preconditioner size");
     solve_stokes_dev(c, k0->m, n_u, u.n_p, u.din.p, u.dout.p, [&] { uzawa_apply_graph(c, u); },
                      h->outer, *cfg, rhs, x, rep, history, history_cap, &u.solve_graph);
+  });
+}
+
+}  // extern "C"
+
+// ======================================================================
+// Partitioned solve: one rank's share of solve_stokes with the
+// DC preconditioner over the row/patch partition planned by plan_rank
+// (sag_dist_plan.cpp). K0 and the low-order level 0 are distributed (owned
+// rows for the SpMV, own Vanka patches with the global partition-of-unity
+// weights, forward and reverse halos with the neighbours only); the coarser
+// levels are agglomerated (every rank runs the HO-AMG form of the device
+// V-cycle on them; the restriction is a partial (P0 on the owned rows)^T r
+// summed over the ranks). FGMRES dots and norms are masked partial sums +
+// an all-reduce, every Krylov scalar stays on the device, so with a
+// capturable communicator (NCCL, or one rank) the whole solve is one CUDA
+// graph -- the same conditional-node loop as the single-GPU solve, the
+// collectives captured in it. A host-staged communicator (sag_comm_ops:
+// gloo, MPI, sockets) runs the same sequence with one status read per
+// Arnoldi step.
+// ======================================================================
+
+struct sag_comm {
+  virtual ~sag_comm() = default;
+  int size = 1, rank = 0;
+  virtual bool capturable() const = 0;
+  // buf (device, n doubles) <- the sum over the ranks, ordered on c.stream
+  virtual void allreduce(sag::Ctx& c, double* buf, long long n) = 0;
+  struct Msg {
+    int peer;
+    double* buf;  // device
+    long long n;
+  };
+  virtual void exchange(sag::Ctx& c, const std::vector<Msg>& sends,
+                        const std::vector<Msg>& recvs) = 0;
+};
+
+namespace sag {
+namespace {
+
+// NCCL, resolved at run time (no link dependency): the library already in
+// the process (torch's) or the system's libnccl.so.2
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool loaded = false;
+  if (!loaded) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+    SAG_REQUIRE(h, SAG_CUDA_ERROR, "NCCL (libnccl.so.2) not found");
+    auto sym = [&](const char* s) {
+      void* p = dlsym(h, s);
+      SAG_REQUIRE(p, SAG_CUDA_ERROR, std::string("NCCL symbol missing: ") + s);
+      return p;
+    };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    loaded = true;
+  }
+  return api;
+}
+
+#define SAG_NCCL(x)                                                                        \
+  do {                                                                                     \
+    ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess)                                                                 \
+      throw ::sag::Error(SAG_CUDA_ERROR, std::string(#x) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+struct NcclComm : sag_comm {
+  ncclComm_t comm = nullptr;
+  bool capturable() const override { return true; }
+  void allreduce(Ctx& c, double* buf, long long n) override {
+    if (size == 1 || n == 0) return;
+    SAG_NCCL(nccl().AllReduce(buf, buf, (size_t)n, ncclDouble, ncclSum, comm, c.stream));
+  }
+  void exchange(Ctx& c, const std::vector<Msg>& sends, const std::vector<Msg>& recvs) override {
+    if (sends.empty() && recvs.empty()) return;
+    SAG_NCCL(nccl().GroupStart());
+    for (const auto& m : sends) SAG_NCCL(nccl().Send(m.buf, (size_t)m.n, ncclDouble, m.peer, comm, c.stream));
+    for (const auto& m : recvs) SAG_NCCL(nccl().Recv(m.buf, (size_t)m.n, ncclDouble, m.peer, comm, c.stream));
+    SAG_NCCL(nccl().GroupEnd());
+  }
+  ~NcclComm() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+};
+
+// collectives staged through host memory and the caller's callbacks
+struct HostComm : sag_comm {
+  sag_comm_ops ops{};
+  std::vector<double> h;
+  bool capturable() const override { return size == 1; }
+  void allreduce(Ctx& c, double* buf, long long n) override {
+    if (size == 1 || n == 0) return;
+    h.resize(n);
+    SAG_CUDA(cudaMemcpyAsync(h.data(), buf, 8 * n, cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    SAG_REQUIRE(ops.allreduce_sum(ops.user, h.data(), n) == 0, SAG_ERROR,
+                "sag_comm_ops.allreduce_sum failed");
+    SAG_CUDA(cudaMemcpyAsync(buf, h.data(), 8 * n, cudaMemcpyHostToDevice, c.stream));
+  }
+  void exchange(Ctx& c, const std::vector<Msg>& sends, const std::vector<Msg>& recvs) override {
+    if (size == 1) return;
+    std::vector<std::vector<double>> sb(sends.size()), rb(recvs.size());
+    for (size_t i = 0; i < sends.size(); ++i) {
+      sb[i].resize(sends[i].n);
+      SAG_CUDA(cudaMemcpyAsync(sb[i].data(), sends[i].buf, 8 * sends[i].n, cudaMemcpyDeviceToHost,
+                               c.stream));
+    }
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    std::vector<int> to(sends.size()), from(recvs.size());
+    std::vector<const double*> sp(sends.size());
+    std::vector<double*> rp(recvs.size());
+    std::vector<long long> sc(sends.size()), rc(recvs.size());
+    for (size_t i = 0; i < sends.size(); ++i) {
+      to[i] = sends[i].peer;
+      sp[i] = sb[i].data();
+      sc[i] = sends[i].n;
+    }
+    for (size_t i = 0; i < recvs.size(); ++i) {
+      rb[i].resize(recvs[i].n);
+      from[i] = recvs[i].peer;
+      rp[i] = rb[i].data();
+      rc[i] = recvs[i].n;
+    }
+    SAG_REQUIRE(ops.exchange(ops.user, (int)sends.size(), to.data(), sp.data(), sc.data(),
+                             (int)recvs.size(), from.data(), rp.data(), rc.data()) == 0,
+                SAG_ERROR, "sag_comm_ops.exchange failed");
+    for (size_t i = 0; i < recvs.size(); ++i)
+      SAG_CUDA(cudaMemcpyAsync(recvs[i].buf, rb[i].data(), 8 * recvs[i].n,
+                               cudaMemcpyHostToDevice, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));  // rb leaves scope
+  }
+};
+
+struct Halo {
+  std::vector<int> peers;
+  std::vector<DevBuf<int>> idx;
+  std::vector<DevBuf<double>> buf;
+  std::vector<int> cnt;
+  void set(const std::map<int, std::vector<int>>& m) {
+    for (const auto& [q, ids] : m) {
+      peers.push_back(q);
+      cnt.push_back((int)ids.size());
+      idx.emplace_back(ids.size());
+      SAG_CUDA(cudaMemcpy(idx.back().p, ids.data(), 4 * ids.size(), cudaMemcpyHostToDevice));
+      buf.emplace_back(ids.size());
+    }
+  }
+  std::vector<sag_comm::Msg> msgs() {
+    std::vector<sag_comm::Msg> out;
+    for (size_t i = 0; i < peers.size(); ++i) out.push_back({peers[i], buf[i].p, cnt[i]});
+    return out;
+  }
+};
+
+struct DistLevel {
+  std::unique_ptr<Matrix> K_int, K_bnd;
+  std::unique_ptr<Vanka> f_int, f_bnd;
+  DevBuf<double> r, v0, z0, w;
+};
+
+std::unique_ptr<Matrix> upload_local(Ctx& c, const LocalCsr& m, int ncols) {
+  return matrix_upload(c, m.n, ncols, (long long)m.ci.size(), m.rp.data(), m.ci.data(),
+                       m.v.data());
+}
+
+std::unique_ptr<Vanka> local_vanka(Ctx& c, const LocalCsr& ext, const LocalPatches& p, int n_u,
+                                   const std::vector<double>& w) {
+  if (p.count() == 0) return nullptr;
+  auto K = upload_local(c, ext, ext.n);
+  DevBuf<int> pptr(p.pptr.size()), pidx(std::max<size_t>(p.pidx.size(), 1)),
+      vptr(p.vptr.size()), vidx(std::max<size_t>(p.vidx.size(), 1)), nx(p.nx.size());
+  auto up = [&](DevBuf<int>& d, const std::vector<int>& h) {
+    if (!h.empty()) SAG_CUDA(cudaMemcpy(d.p, h.data(), 4 * h.size(), cudaMemcpyHostToDevice));
+  };
+  up(pptr, p.pptr);
+  up(pidx, p.pidx);
+  up(vptr, p.vptr);
+  up(vidx, p.vidx);
+  up(nx, p.nx);
+  auto pt = patches_from_lists(c, p.count(), pptr.p, pidx.p, vptr.p, vidx.p, nx.p);
+  auto f = factor_patches_dev(c, *K, *pt, n_u);
+  SAG_CUDA(cudaMemcpy(f->w.p, w.data(), 8 * w.size(), cudaMemcpyHostToDevice));
+  f->w_ext = true;
+  return f;
+}
+
+}  // namespace
+}  // namespace sag
+
+struct sag_dist {
+  sag::Ctx* c = nullptr;
+  sag_comm* comm = nullptr;
+  sag_solver_config cfg{};
+  int nl = 0, n_u_loc = 0, n_p = 0, n1 = 0, n_own = 0, npatch = 0;
+  std::vector<long long> l2g;
+  std::vector<unsigned char> owned;
+  sag::DevBuf<unsigned char> mask;
+  sag::DevBuf<double> ones;
+  sag::Halo fs, fr, rs, rr;
+  sag::DistLevel k0, l0;
+  std::unique_ptr<sag::Matrix> P, R;
+  std::vector<sag_matrix*> coarse_mats;
+  sag_dc* coarse = nullptr;
+  sag::DevBuf<double> rc, xc;
+  sag::Krylov outer;
+  sag::DevBuf<double> din, dout, t, b0, x0, gam_rc, gam_e, sc;
+  cudaGraphExec_t graph = nullptr;
+  const void* gkey[2] = {nullptr, nullptr};
+  ~sag_dist() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (coarse) sag_dc_destroy(coarse);
+    for (auto* m : coarse_mats) sag_matrix_destroy(m);
+  }
+};
+
+namespace sag {
+namespace {
+
+using Dist = sag_dist;
+
+void halo_fwd(Ctx& c, Dist& d, double* x) {
+  for (size_t i = 0; i < d.fs.peers.size(); ++i)
+    launch_gather_idx(c, d.fs.cnt[i], d.fs.idx[i].p, x, d.fs.buf[i].p);
+  d.comm->exchange(c, d.fs.msgs(), d.fr.msgs());
+  for (size_t i = 0; i < d.fr.peers.size(); ++i)
+    launch_scatter_idx(c, d.fr.cnt[i], d.fr.idx[i].p, d.fr.buf[i].p, x, 0);
+}
+
+// partial sums at ghosts to their owners, added in rank order
+void halo_rev(Ctx& c, Dist& d, double* z) {
+  for (size_t i = 0; i < d.rs.peers.size(); ++i)
+    launch_gather_idx(c, d.rs.cnt[i], d.rs.idx[i].p, z, d.rs.buf[i].p);
+  d.comm->exchange(c, d.rs.msgs(), d.rr.msgs());
+  for (size_t i = 0; i < d.rr.peers.size(); ++i)
+    launch_scatter_idx(c, d.rr.cnt[i], d.rr.idx[i].p, d.rr.buf[i].p, z, 1);
+}
+
+// *out = global (a, b) over the owned entries
+void mdot(Ctx& c, Dist& d, const double* a, const double* b, double* out) {
+  launch_dot_mask(c, d.nl, a, b, d.mask.p, out);
+  d.comm->allreduce(c, out, 1);
+}
+
+// y = K x (Store), aux - K x (Resid; y may be aux) or y + K x (Add) on the owned rows
+void apply_op(Ctx& c, Dist& d, DistLevel& L, double* x, double* y, Epi e,
+              const double* aux = nullptr) {
+  halo_fwd(c, d, x);
+  SpmvArgs a;
+  a.b = aux;
+  launch_spmv(c, *L.K_int, x, y, e, a);
+  if (L.K_bnd) {
+    if (e == Epi::Resid) {
+      SpmvArgs b;
+      b.b = y;
+      launch_spmv(c, *L.K_bnd, x, y, Epi::Resid, b);
+    } else {
+      launch_spmv(c, *L.K_bnd, x, y, Epi::Add);
+    }
+  }
+}
+
+// z = apply_vanka(v) over the partition (vanka.cpp:151-184)
+void vanka(Ctx& c, Dist& d, DistLevel& L, double* v, double* z) {
+  halo_fwd(c, d, v);
+  if (L.f_int)
+    vanka_apply(c, *L.f_int, v, z);
+  else
+    launch_zero(c, d.nl, z);
+  if (L.f_bnd) vanka_apply_stationary(c, *L.f_bnd, v, z, 1.0);
+  halo_rev(c, d, z);
+}
+
+// vanka_relax, Krylov-wrapped with nu = 1 (vanka.cpp:199-208): the one-step
+// FGMRES on device scalars
+void relax1(Ctx& c, Dist& d, DistLevel& L, double* x, const double* b, bool x_zero) {
+  double* s = d.sc.p;
+  const double* r = b;
+  if (!x_zero) {
+    apply_op(c, d, L, x, L.r.p, Epi::Resid, b);
+    r = L.r.p;
+  }
+  mdot(c, d, r, r, s + 0);                          // ||r||^2
+  launch_div_dev(c, d.nl, r, s + 0, 1, L.v0.p);     // v_0 = r / ||r||
+  vanka(c, d, L, L.v0.p, L.z0.p);                   // z_0 = M v_0
+  apply_op(c, d, L, L.z0.p, L.w.p, Epi::Store);     // w = K z_0
+  mdot(c, d, L.w.p, L.v0.p, s + 1);                 // h_00
+  launch_axpy_dev(c, d.nl, s + 1, -1.0, L.v0.p, L.w.p);
+  mdot(c, d, L.w.p, L.w.p, s + 2);                  // h_10^2
+  launch_fgmres1_coef(c, s + 0, s + 1, s + 2, s + 3);
+  if (x_zero) launch_zero(c, d.nl, x);
+  launch_axpy_dev(c, d.nl, s + 3, 1.0, L.z0.p, x);  // x += y_0 z_0
+}
+
+// MonolithicSolver::cycle_level on level 0 (preconditioner.cpp:57-81)
+void cycle0(Ctx& c, Dist& d, double* b, double* x, bool skip_finest) {
+  const auto& cf = d.cfg;
+  const bool relax = !skip_finest;
+  const double* r = b;
+  if (relax && cf.nu1 > 0) {
+    relax1(c, d, d.l0, x, b, true);
+    apply_op(c, d, d.l0, x, d.l0.r.p, Epi::Resid, b);
+    r = d.l0.r.p;
+  } else {
+    launch_zero(c, d.nl, x);
+  }
+  launch_spmv(c, *d.R, r, d.rc.p, Epi::Store);      // partial restriction (owned rows)
+  d.comm->allreduce(c, d.rc.p, d.n1);
+  dc_apply_dev(c, d.coarse->d, d.rc.p, d.xc.p);      // agglomerated V-cycle below level 0
+  launch_spmv(c, *d.P, d.xc.p, x, Epi::Add);         // x += P x_c on the owned rows
+  if (relax && cf.nu2 > 0) relax1(c, d, d.l0, x, b, false);
+}
+
+// DCPreconditioner::apply (preconditioner.cpp:114-153), Taylor-Hood
+void dist_dc_apply(Ctx& c, Dist& d, double* r, double* z) {
+  const auto& cf = d.cfg;
+  const bool relax_fine = cf.variant != SAG_DC_LO;
+  double* x = z;
+  const double* r1 = r;
+  if (relax_fine && cf.nu1 > 0) {
+    relax1(c, d, d.k0, x, r, true);
+    apply_op(c, d, d.k0, x, d.t.p, Epi::Resid, r);
+    r1 = d.t.p;
+  } else {
+    launch_zero(c, d.nl, x);
+  }
+  launch_eta(c, d.nl, d.n_u_loc, cf.eta_u, cf.eta_p, r1, d.b0.p);  // transfer.cpp:127-135
+  const bool skip = cf.variant == SAG_DC_HO;
+  if (cf.gamma <= 1) {
+    cycle0(c, d, d.b0.p, d.x0.p, skip);
+    launch_add(c, d.nl, x, d.x0.p);
+  } else {
+    launch_copy(c, d.nl, d.b0.p, d.gam_rc.p);
+    launch_zero(c, d.nl, d.gam_e.p);
+    for (int g = 0; g < cf.gamma; ++g) {
+      if (g > 0)
+        apply_op(c, d, d.l0, d.gam_e.p, d.b0.p, Epi::Resid, d.gam_rc.p);
+      else
+        launch_copy(c, d.nl, d.gam_rc.p, d.b0.p);
+      cycle0(c, d, d.b0.p, d.x0.p, skip);
+      launch_add(c, d.nl, d.gam_e.p, d.x0.p);
+    }
+    launch_add(c, d.nl, x, d.gam_e.p);
+  }
+  if (relax_fine && cf.nu2 > 0) relax1(c, d, d.k0, x, r, false);
+}
+
+// y = x with the global pressure mean removed (preconditioner.cpp:235-240)
+void dist_project(Ctx& c, Dist& d, const double* x, double* y, double* s) {
+  const int nu = d.n_u_loc;
+  launch_dot_mask(c, d.nl - nu, x + nu, d.ones.p + nu, d.mask.p + nu, s);
+  d.comm->allreduce(c, s, 1);
+  if (y != x) launch_copy(c, nu, x, y);
+  launch_sub_mean(c, d.nl - nu, x + nu, s, (double)d.n_p, y + nu);
+}
+
+void dist_prec(Ctx& c, Dist& d, const double* v, double* z) {
+  if (d.cfg.enclosed_flow) {
+    dist_project(c, d, v, d.din.p, d.sc.p + 4);
+    dist_dc_apply(c, d, d.din.p, d.dout.p);
+    dist_project(c, d, d.dout.p, z, d.sc.p + 5);
+  } else {
+    launch_copy(c, d.nl, v, d.din.p);
+    dist_dc_apply(c, d, d.din.p, z);
+  }
+}
+
+// the fgmres of krylov.cpp:17-121 over the partition, every scalar on the
+// device: graph = conditional nodes (a capturing caller), else one status
+// read per Arnoldi step
+void dist_fgmres(Ctx& c, Dist& d, const double* b, double* x, bool graph) {
+  Krylov& K = d.outer;
+  const auto& cf = d.cfg;
+  const int m = cf.restart, n = d.nl;
+  double* s = d.sc.p + 8;
+  SAG_CUDA(cudaMemsetAsync(c.ticket.p, 0, sizeof(unsigned) * c.ticket.n, c.stream));
+  launch_kinit(c, K.st, m, cf.tol, 1e-30, K.hist_cap, false);
+  launch_zero(c, n, x);
+  auto fin = [&](FinKind k, int i, int j, double* out = nullptr) {
+    Fin f;
+    f.kind = k;
+    f.st = K.st;
+    f.i = i;
+    f.j = j;
+    f.out = out;
+    return f;
+  };
+  mdot(c, d, b, b, s);
+  launch_fin_from(c, fin(FIN_REF, 0, 0), s);                   // ref = ||b||
+  auto residual = [&](int hist) {
+    apply_op(c, d, d.k0, x, K.r.p, Epi::Resid, b);
+    mdot(c, d, K.r.p, K.r.p, s + 1);
+    launch_fin_from(c, fin(FIN_BETA, hist, 0), s + 1);         // beta, g, stop
+  };
+  residual(2);                                                 // history[0]
+  auto step = [&](int j) {
+    dist_prec(c, d, K.v(j), K.z(j));
+    apply_op(c, d, d.k0, K.z(j), K.w.p, Epi::Store);
+    for (int i = 0; i <= j; ++i) {                             // MGS (krylov.cpp:63-67)
+      mdot(c, d, K.w.p, K.v(i), s + 2 + i);
+      launch_fin_from(c, fin(FIN_H, i, j), s + 2 + i);
+      launch_axpy_dev(c, n, K.h(m, i, j), -1.0, K.v(i), K.w.p);
+    }
+    mdot(c, d, K.w.p, K.w.p, s + 2 + j + 1);
+    launch_fin_from(c, fin(FIN_ARNOLDI, 0, j), s + 2 + j + 1);  // Givens, residual estimate
+    launch_div(c, n, K.w.p, K.wnorm(), K.v(j + 1), K.stop(), K.breakdown());
+  };
+  auto cycle_body = [&] {
+    residual(0);                                               // restart (krylov.cpp:43-53)
+    launch_div(c, n, K.r.p, K.beta(), K.v(0), K.stop());
+  };
+  if (graph) {
+    auto set = [&](int mode) {
+      return [&, mode](cudaGraphConditionalHandle h) {
+        cond_set_kernel<<<1, 1, 0, c.stream>>>(h, K.st, mode, cf.max_iters);
+        SAG_LAUNCHED(c);
+      };
+    };
+    cond_node(c, cudaGraphCondTypeWhile, set(0), [&](cudaGraphConditionalHandle hw) {
+      cycle_body();
+      for (int j = 0; j < m; ++j)
+        cond_node(c, cudaGraphCondTypeIf, set(1), [&](cudaGraphConditionalHandle) { step(j); });
+      launch_backsub(c, K.st);
+      launch_update(c, n, x, K.Z.p, (size_t)n, K.st, false);
+      cond_set_kernel<<<1, 1, 0, c.stream>>>(hw, K.st, 0, cf.max_iters);
+      SAG_LAUNCHED(c);
+    });
+  } else {
+    KHeader hd = read_header(c, K.st);
+    while (!hd.converged && hd.iterations < cf.max_iters) {
+      cycle_body();
+      hd = read_header(c, K.st);
+      if (hd.stop) break;
+      for (int j = 0; j < m && hd.iterations < cf.max_iters; ++j) {
+        step(j);
+        hd = read_header(c, K.st);
+        if (hd.stop) break;
+      }
+      launch_backsub(c, K.st);
+      launch_update(c, n, x, K.Z.p, (size_t)n, K.st, false);
+      hd = read_header(c, K.st);
+    }
+  }
+  apply_op(c, d, d.k0, x, K.r.p, Epi::Resid, b);                // final true residual
+  mdot(c, d, K.r.p, K.r.p, s + 1);
+  launch_fin_from(c, fin(FIN_FINAL, 0, 0, c.scal.p), s + 1);
+}
+
+void check_status(int st) {
+  if (st != SAG_OK) throw Error(st, sag_last_error());
+}
+
+double host_norm_inf(const HostCsr& m) {  // norm_inf (sparse.cpp:229-237)
+  double best = 0.0;
+  for (int r = 0; r < m.nrows; ++r) {
+    double s = 0.0;
+    for (int k = m.rp[r]; k < m.rp[r + 1]; ++k) s += std::abs(m.v[k]);
+    best = std::max(best, s);
+  }
+  return best;
+}
+
+HostCsr host_csr(const sag_csr& m) {
+  HostCsr h;
+  h.nrows = m.nrows;
+  h.ncols = m.ncols;
+  h.rp = m.row_offsets;
+  h.ci = m.col_indices;
+  h.v = m.values;
+  return h;
+}
+
+}  // namespace
+}  // namespace sag
+
+using namespace sag;
+
+struct sag_plan {
+  RankPlan p;
+};
+
+extern "C" {
+
+int sag_nccl_unique_id(unsigned char* id) {
+  return guard([&] {
+    SAG_NOTNULL(id);
+    ncclUniqueId u;
+    SAG_NCCL(nccl().GetUniqueId(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int sag_comm_create_nccl(sag_ctx* ctx, int nranks, int rank, const unsigned char* id,
+                         sag_comm** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(id);
+    SAG_NOTNULL(out);
+    SAG_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, SAG_CONFIG_ERROR,
+                "sag_comm_create_nccl: rank out of range");
+    auto cm = std::make_unique<NcclComm>();
+    cm->size = nranks;
+    cm->rank = rank;
+    if (nranks > 1) {
+      ncclUniqueId u;
+      std::memcpy(&u, id, sizeof(u));
+      SAG_CUDA(cudaSetDevice(ctx->c.device));
+      SAG_NCCL(nccl().CommInitRank(&cm->comm, nranks, u, rank));
+    }
+    *out = cm.release();
+  });
+}
+
+int sag_comm_create_host(int nranks, int rank, const sag_comm_ops* ops, sag_comm** out) {
+  return guard([&] {
+    SAG_NOTNULL(out);
+    SAG_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, SAG_CONFIG_ERROR,
+                "sag_comm_create_host: rank out of range");
+    SAG_REQUIRE(nranks == 1 || (ops && ops->allreduce_sum && ops->exchange), SAG_INVALID_ARGUMENT,
+                "sag_comm_create_host: missing callbacks");
+    auto cm = std::make_unique<HostComm>();
+    cm->size = nranks;
+    cm->rank = rank;
+    if (ops) cm->ops = *ops;
+    *out = cm.release();
+  });
+}
+
+int sag_comm_allreduce(sag_ctx* ctx, sag_comm* comm, double* buf, long long n) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(comm);
+    SAG_REQUIRE(is_device_ptr(buf) || n == 0, SAG_INVALID_ARGUMENT,
+                "sag_comm_allreduce: device buffer expected");
+    comm->allreduce(ctx->c, buf, n);
+    SAG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+int sag_comm_destroy(sag_comm* comm) {
+  return guard([&] { delete comm; });
+}
+
+int sag_plan_create(int nranks, int rank, const sag_csr* k0, const sag_csr* l0, const sag_csr* p0,
+                    int n_x, int n_y, int n_p, sag_plan** out) {
+  return guard([&] {
+    SAG_NOTNULL(k0);
+    SAG_NOTNULL(l0);
+    SAG_NOTNULL(out);
+    const HostCsr hk = host_csr(*k0), hl = host_csr(*l0);
+    HostCsr hp;
+    if (p0) hp = host_csr(*p0);
+    auto pl = std::make_unique<sag_plan>();
+    try {
+      pl->p = plan_rank(nranks, rank, hk, hl, p0 ? &hp : nullptr, n_x, n_y, n_p);
+    } catch (const std::runtime_error& e) {
+      throw Error(SAG_CONFIG_ERROR, e.what());
+    }
+    *out = pl.release();
+  });
+}
+
+int sag_plan_destroy(sag_plan* plan) {
+  return guard([&] { delete plan; });
+}
+
+int sag_plan_array(const sag_plan* plan, int which, int peer, void* out, long long* count) {
+  return guard([&] {
+    SAG_NOTNULL(plan);
+    SAG_NOTNULL(count);
+    const RankPlan& p = plan->p;
+    auto give = [&](const auto& v) {
+      using T = typename std::decay_t<decltype(v)>::value_type;
+      *count = (long long)v.size();
+      if (out && !v.empty()) std::memcpy(out, v.data(), sizeof(T) * v.size());
+    };
+    auto halo = [&](const std::map<int, std::vector<int>>& m) {
+      static const std::vector<int> none;
+      auto it = m.find(peer);
+      give(it == m.end() ? none : it->second);
+    };
+    const LocalLevel& L = (which / 100) == 1 ? p.l0 : p.k0;
+    switch (which % 100) {
+      case SAG_PLAN_L2G: give(p.l2g); break;
+      case SAG_PLAN_OWNED: give(p.owned); break;
+      case SAG_PLAN_FWD_SEND: halo(p.fwd_send); break;
+      case SAG_PLAN_FWD_RECV: halo(p.fwd_recv); break;
+      case SAG_PLAN_REV_SEND: halo(p.rev_send); break;
+      case SAG_PLAN_REV_RECV: halo(p.rev_recv); break;
+      case SAG_PLAN_EXT_RP: give(L.ext.rp); break;
+      case SAG_PLAN_EXT_CI: give(L.ext.ci); break;
+      case SAG_PLAN_EXT_V: give(L.ext.v); break;
+      case SAG_PLAN_INT_PVIDX: give(L.p_int.vidx); break;
+      case SAG_PLAN_BND_PVIDX: give(L.p_bnd.vidx); break;
+      case SAG_PLAN_WEIGHTS: give(L.w); break;
+      case SAG_PLAN_P_RP: give(p.p_own.rp); break;
+      case SAG_PLAN_P_CI: give(p.p_own.ci); break;
+      case SAG_PLAN_INFO: {
+        const std::vector<long long> info = {p.nl(), p.n_u_loc, p.patch_lo, p.patch_hi, p.n1,
+                                             (long long)p.fwd_send.size(),
+                                             (long long)p.fwd_recv.size()};
+        give(info);
+        break;
+      }
+      default:
+        throw Error(SAG_INVALID_ARGUMENT, "sag_plan_array: unknown array");
+    }
+  });
+}
+
+int sag_dist_create(sag_ctx* ctx, sag_comm* comm, const sag_csr* k0, int n_x, int n_y, int n_p,
+                    int nlevels, const sag_csr* levels, const sag_csr* prolongators,
+                    const int* level_nxyz, const sag_solver_config* cfg, sag_dist** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(comm);
+    SAG_NOTNULL(k0);
+    SAG_NOTNULL(levels);
+    SAG_NOTNULL(level_nxyz);
+    SAG_NOTNULL(cfg);
+    SAG_NOTNULL(out);
+    check_config(*cfg);
+    SAG_REQUIRE(cfg->variant == SAG_DC_ALL || cfg->variant == SAG_DC_LO ||
+                    cfg->variant == SAG_DC_HO,
+                SAG_CONFIG_ERROR, "sag_dist_create: DC-all / DC-LO / DC-HO only");
+    SAG_REQUIRE(cfg->nu1 <= 1 && cfg->nu2 <= 1, SAG_CONFIG_ERROR,
+                "sag_dist_create: nu1, nu2 <= 1 (one-step Krylov-wrapped relaxation)");
+    SAG_REQUIRE(nlevels >= 2 && prolongators, SAG_CONFIG_ERROR,
+                "sag_dist_create: a hierarchy of at least two levels");
+    Ctx& c = ctx->c;
+    const HostCsr hk = host_csr(*k0), hl = host_csr(levels[0]), hp = host_csr(prolongators[0]);
+    RankPlan pl;
+    try {
+      pl = plan_rank(comm->size, comm->rank, hk, hl, &hp, n_x, n_y, n_p);
+    } catch (const std::runtime_error& e) {
+      throw Error(SAG_CONFIG_ERROR, e.what());
+    }
+    auto d = std::make_unique<sag_dist>();
+    d->c = &c;
+    d->comm = comm;
+    d->cfg = *cfg;
+    d->nl = pl.nl();
+    d->n_u_loc = pl.n_u_loc;
+    d->n_p = n_p;
+    d->n1 = pl.n1;
+    d->l2g = pl.l2g;
+    d->owned = pl.owned;
+    d->npatch = (int)(pl.patch_hi - pl.patch_lo);
+    for (unsigned char o : pl.owned) d->n_own += o;
+    const int nl = d->nl;
+    d->mask.alloc(nl);
+    SAG_CUDA(cudaMemcpy(d->mask.p, pl.owned.data(), nl, cudaMemcpyHostToDevice));
+    d->ones.alloc(nl);
+    {
+      std::vector<double> o(nl, 1.0);
+      SAG_CUDA(cudaMemcpy(d->ones.p, o.data(), 8 * (size_t)nl, cudaMemcpyHostToDevice));
+    }
+    d->fs.set(pl.fwd_send);
+    d->fr.set(pl.fwd_recv);
+    d->rs.set(pl.rev_send);
+    d->rr.set(pl.rev_recv);
+    const int n_u_loc = pl.n_u_loc;
+    auto level = [&](DistLevel& L, const LocalLevel& ll) {
+      L.K_int = upload_local(c, ll.rows_int, nl);
+      if (!ll.rows_bnd.ci.empty()) L.K_bnd = upload_local(c, ll.rows_bnd, nl);
+      L.f_int = local_vanka(c, ll.ext, ll.p_int, n_u_loc, ll.w);
+      L.f_bnd = local_vanka(c, ll.ext, ll.p_bnd, n_u_loc, ll.w);
+      L.r.alloc(nl);
+      L.v0.alloc(nl);
+      L.z0.alloc(nl);
+      L.w.alloc(nl);
+    };
+    level(d->k0, pl.k0);
+    level(d->l0, pl.l0);
+    d->P = upload_local(c, pl.p_own, pl.n1);
+    d->R = transpose_dev(c, *d->P);
+    // agglomerated levels 1..: the HO-AMG form of the device V-cycle, the
+    // coarsest pinned with the norm of level 0 (preconditioner.cpp:49-53)
+    std::vector<sag_level_desc> lv(nlevels - 1);
+    for (int l = 1; l < nlevels; ++l) {
+      sag_matrix* k = nullptr;
+      check_status(sag_matrix_create(ctx, levels[l].nrows, levels[l].ncols,
+                                     levels[l].row_offsets[levels[l].nrows],
+                                     levels[l].row_offsets, levels[l].col_indices,
+                                     levels[l].values, &k));
+      d->coarse_mats.push_back(k);
+      lv[l - 1].k = k;
+      lv[l - 1].p = nullptr;
+      if (l + 1 < nlevels) {
+        sag_matrix* p = nullptr;
+        const sag_csr& pm = prolongators[l];
+        check_status(sag_matrix_create(ctx, pm.nrows, pm.ncols, pm.row_offsets[pm.nrows],
+                                       pm.row_offsets, pm.col_indices, pm.values, &p));
+        d->coarse_mats.push_back(p);
+        lv[l - 1].p = p;
+      }
+      lv[l - 1].n_x = level_nxyz[3 * l];
+      lv[l - 1].n_y = level_nxyz[3 * l + 1];
+      lv[l - 1].n_p = level_nxyz[3 * l + 2];
+    }
+    sag_solver_config ccfg = *cfg;
+    ccfg.variant = SAG_HOAMG;
+    check_status(sag_dc_create(ctx, lv[0].k, lv[0].n_x, lv[0].n_y, lv[0].n_p, 0, nlevels - 1,
+                               lv.data(), &ccfg, &d->coarse));
+    if (cfg->enclosed_flow)
+      check_status(sag_dc_set_coarse_pin(ctx, d->coarse, host_norm_inf(hl)));
+    d->rc.alloc(pl.n1);
+    d->xc.alloc(pl.n1);
+    d->outer.init(nl, cfg->restart, cfg->max_iters + 2);
+    for (auto* b : {&d->din, &d->dout, &d->t, &d->b0, &d->x0, &d->gam_rc, &d->gam_e})
+      b->alloc(nl);
+    d->sc.alloc(64 + 2 * (size_t)cfg->restart);
+    SAG_CUDA(cudaDeviceSynchronize());
+    *out = d.release();
+  });
+}
+
+int sag_dist_destroy(sag_dist* d) {
+  return guard([&] {
+    if (d) cudaDeviceSynchronize();
+    delete d;
+  });
+}
+
+int sag_dist_info(const sag_dist* d, long long* out) {
+  return guard([&] {
+    SAG_NOTNULL(d);
+    SAG_NOTNULL(out);
+    out[0] = d->nl;
+    out[1] = d->n_own;
+    out[2] = d->nl - d->n_own;
+    out[3] = (long long)std::max(d->fs.peers.size(), d->fr.peers.size());
+    out[4] = d->npatch;
+    out[5] = d->n1;
+    out[6] = d->n_u_loc;
+  });
+}
+
+int sag_dist_local_dofs(const sag_dist* d, long long* l2g, unsigned char* owned) {
+  return guard([&] {
+    SAG_NOTNULL(d);
+    if (l2g) std::memcpy(l2g, d->l2g.data(), 8 * d->l2g.size());
+    if (owned) std::memcpy(owned, d->owned.data(), d->owned.size());
+  });
+}
+
+int sag_dist_step(sag_ctx* ctx, sag_dist* d, const double* x, double* delta, double* y) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(d);
+    Ctx& c = ctx->c;
+    const int nl = d->nl;
+    InVec xi(c, x, nl, 0);
+    double* xw = c.stage_buf(3, nl);  // ghosts are overwritten by the halo
+    launch_copy(c, nl, xi.d, xw);
+    OutVec dv(c, delta, nl, 1, false), yv(c, y, nl, 2, false);
+    DistLevel& L = d->k0;
+    halo_fwd(c, *d, xw);
+    if (L.f_int)
+      vanka_apply(c, *L.f_int, xw, dv.d);
+    else
+      launch_zero(c, nl, dv.d);
+    launch_spmv(c, *L.K_int, xw, yv.d, Epi::Store);
+    if (L.f_bnd) vanka_apply_stationary(c, *L.f_bnd, xw, dv.d, 1.0);
+    if (L.K_bnd) launch_spmv(c, *L.K_bnd, xw, yv.d, Epi::Add);
+    halo_rev(c, *d, dv.d);
+    dv.finish();
+    yv.finish();
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sag_dist_solve_stokes(sag_ctx* ctx, sag_dist* d, const double* rhs, double* x,
+                          sag_krylov_report* rep, double* history, int history_cap) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(d);
+    Ctx& c = ctx->c;
+    const int nl = d->nl;
+    InVec bi(c, rhs, nl, 0);
+    OutVec xo(c, x, nl, 1, false);
+    const bool graph = d->comm->capturable() &&
+                       !(getenv("SAG_SOLVE_GRAPH") && !atoi(getenv("SAG_SOLVE_GRAPH")));
+    if (graph) {
+      const void* key[2] = {bi.d, xo.d};
+      if (!d->graph || key[0] != d->gkey[0] || key[1] != d->gkey[1]) {
+        if (d->graph) cudaGraphExecDestroy(d->graph);
+        d->graph = nullptr;
+        cudaGraph_t g;
+        const long long la = c.launches;
+        SAG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+        try {
+          dist_fgmres(c, *d, bi.d, xo.d, true);
+        } catch (...) {
+          cudaStreamEndCapture(c.stream, &g);
+          throw;
+        }
+        SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
+        SAG_CUDA(cudaGraphInstantiate(&d->graph, g, 0));
+        cudaGraphDestroy(g);
+        d->gkey[0] = key[0];
+        d->gkey[1] = key[1];
+        c.launches = la;
+      }
+      SAG_CUDA(cudaGraphLaunch(d->graph, c.stream));
+    } else {
+      dist_fgmres(c, *d, bi.d, xo.d, false);
+    }
+    const KHeader hd = read_header(c, d->outer.st);
+    if (rep) {
+      rep->converged = hd.converged;
+      rep->iterations = hd.iterations;
+      SAG_CUDA(cudaMemcpyAsync(&rep->final_relative_residual, c.scal.p, sizeof(double),
+                               cudaMemcpyDeviceToHost, c.stream));
+    }
+    const int m = d->cfg.restart;
+    const int hl = std::min({hd.hist_len, d->outer.hist_cap, history ? history_cap : 0});
+    if (history && hl > 0)
+      SAG_CUDA(cudaMemcpyAsync(history, ks_h(d->outer.st) + (size_t)(m + 1) * m + m + m + (m + 1) + m,
+                               sizeof(double) * hl, cudaMemcpyDeviceToHost, c.stream));
+    if (rep) rep->history_len = hd.hist_len;
+    xo.finish();
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
 

@@ -669,11 +669,12 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     // paired patches go to the sub-warp kernel (several patches per warp)
     const bool subwarp = f->pairs && env_int("SAG_VANKA_SUBWARP", 1) != 0;
     f->seq = env_int("SAG_VANKA_SEQGATHER", 1) != 0;
-    // fixed-shape class: the SV fine level's interior element triples
-    // (nx = ny = 6, np = 3) get a kernel with the shape compiled in
+    // fixed-shape class: the SV fine level's element triples with
+    // max(nx, ny) = 6, np = 3 get a kernel with the shape compiled in
     const bool fixed63 = f->pairs && subwarp && sym && env_int("SAG_VANKA_FIXED", 1) != 0;
     auto is_fixed = [&](int i) {
-      return fixed63 && f->h_nx[i] == 6 && f->h_nv[i] == 12 && f->h_np[i] == 3;
+      const int x = f->h_nx[i], y = f->h_nv[i] - x;
+      return fixed63 && std::max(x, y) == 6 && f->h_np[i] == 3;
     };
     auto key_of = [&](int i) {
       const int x = f->h_nx[i], y = f->h_nv[i] - x;
@@ -699,7 +700,6 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     h_hoff.assign(np_, 0);
     int maxbytes = 16;
     f->rclasses.clear();
-    f->blob_patch.assign(np_, 0);
     for (int q = 0; q < np_; ++q) {
       const int i = order[q];
       long long bytes = 16 + 8 * ndbl(i) + 4 * (f->h_nv[i] + f->h_np[i]) * (f->seq ? 2 : 1);
@@ -709,7 +709,6 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
       maxbytes = std::max<long long>(maxbytes, bytes);
       f->h_dbase[i] = (off[q] + 16) / 8;
       f->h_ibase[i] = (off[q] + 16 + 8 * ndbl(i)) / 4;
-      f->blob_patch[q] = i;
       const int key = r_of(i), R = key / 4, fx = key % 4 == 3;
       const int lpp = fx ? 9 : 32 >> (key % 4);
       if (f->rclasses.empty() || f->rclasses.back().R != R || f->rclasses.back().lpp != lpp ||
@@ -1355,64 +1354,71 @@ __global__ void __launch_bounds__(256) vanka_subwarp_kernel(
 }
 
 
-// Fixed-shape paired patches (the SV fine level's interior element triples:
-// nx = ny = M velocity nodes, NP = 3 pressure seeds): every blob has the
-// same size and layout, so the shape, all offsets and the loop bounds are
-// compile-time constants. L = M + NP lanes per patch (M pair rows + NP b_hat
-// rows), 32 / L patches per warp; the group's blobs arrive with one bulk
-// copy. Same operations in the same order as vanka_subwarp_kernel (bitwise
-// the same results), with ~1/5 of its instructions.
+// Fixed-shape paired patches: the SV fine level's element triples with
+// m = max(nx, ny) = M velocity pair rows and NP = 3 pressure seeds (~90-97%
+// of the level; nx, ny vary through exact cancellations in B). The paired
+// layout zero-pads the smaller component to M, so the shape, the factor
+// offsets and the loop bounds are compile-time constants; only the dof lists
+// depend on (nx, ny). L = M + NP lanes per patch (M pair rows + NP b_hat
+// rows), 32 / L patches per warp, the group's blobs in one bulk copy. Same
+// operations in the same order as vanka_subwarp_kernel (bitwise the same
+// results) with a fraction of its instructions.
 template <int M, int NP>
 __global__ void __launch_bounds__(256) vanka_fixed_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
-    int bytes, int nstage, const double* __restrict__ r, double* __restrict__ out,
+    int slot_bytes, int nstage, const double* __restrict__ r, double* __restrict__ out,
     const int* gate) {
   if (gate && *gate) return;
-  constexpr int L = M + NP, P = 32 / L, NV = 2 * M, NB = 2 * M + NP;  // b: (x, y) pairs, p
-  constexpr int A2 = M * (M + 1) / 2;                                 // A pairs
+  constexpr int L = M + NP, P = 32 / L, NV2 = 2 * M;
+  constexpr int NBS = (2 * M + NP + 1) & ~1;  // per-patch b stride (16-byte aligned)
+  constexpr int A2 = M * (M + 1) / 2;          // A pairs
+  constexpr int FD = 2 * A2 + 4 * NP * M + NP * NP;  // factor doubles after the header
   extern __shared__ __align__(128) unsigned char smem[];
   const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane / L, gl = lane % L;
+  const int gg = g < P ? g : 0;
   const int nbar = (nstage + 1) & ~1;
-  const size_t stage_bytes = (size_t)P * bytes;
+  const size_t stage_bytes = (size_t)P * slot_bytes;
   unsigned char* ring = smem + (size_t)wib * nstage * stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)warps * nstage * stage_bytes) +
                    (size_t)wib * nbar;
   double* sbuf = reinterpret_cast<double*>(smem + (size_t)warps * nstage * stage_bytes +
                                            (size_t)warps * nbar * 8) +
-                 (size_t)wib * 2 * P * NB;
+                 (size_t)wib * 2 * P * NBS;
   const int ngroups = (npatch + P - 1) / P;
   const int first = blockIdx.x * warps + wib;
   const int stride = gridDim.x * warps;
-  const long long base = __ldg(off);
   const uint64_t policy = evict_first_policy();
+  auto grp_end = [&](int q) { return q * P + P < npatch ? q * P + P : npatch; };
   auto issue_at = [&](int s, int q) {
-    const int cnt = min(P, npatch - q * P);
-    const unsigned nb = (unsigned)cnt * (unsigned)bytes;
-    mbar_expect_tx(bars + s, nb);
-    bulk_copy_hint(ring + (size_t)s * stage_bytes, blob + base + (long long)q * P * bytes, nb,
-                   bars + s, policy);
+    const long long o0 = off[q * P], o1 = off[grp_end(q)];
+    mbar_expect_tx(bars + s, (unsigned)(o1 - o0));
+    bulk_copy_hint(ring + (size_t)s * stage_bytes, blob + o0, (unsigned)(o1 - o0), bars + s,
+                   policy);
   };
-  // this lane's r values of its patch in stage s: velocity lanes (x_gl, y_gl),
+  // this lane's patch in stage s of group q (valid lanes only)
+  auto patch_at = [&](int s, int q) {
+    return ring + (size_t)s * stage_bytes + (size_t)(off[min(q * P + gg, npatch - 1)] - off[q * P]);
+  };
+  // this lane's r values: velocity lanes (x_gl, y_gl) zero past nx / ny,
   // pressure lanes p_(gl - M)
-  auto load_r = [&](int s, bool valid, double& v0, double& v1) {
+  auto load_r = [&](const unsigned char* B, bool valid, double& v0, double& v1) {
     v0 = v1 = 0.0;
     if (!valid) return;
-    const int* idx = reinterpret_cast<const int*>(ring + (size_t)s * stage_bytes +
-                                                  (size_t)g * bytes + 16 + 8 * (2 * A2 + 4 * NP * M + NP * NP));
+    const int2 hdr = *reinterpret_cast<const int2*>(B);
+    const int* idx = reinterpret_cast<const int*>(B + 16 + 8 * FD);
     if (gl < M) {
-      v0 = __ldg(r + idx[gl]);
-      v1 = __ldg(r + idx[M + gl]);
+      if (gl < hdr.x) v0 = __ldg(r + idx[gl]);
+      if (gl < hdr.y) v1 = __ldg(r + idx[hdr.x + gl]);
     } else {
-      v0 = __ldg(r + idx[NV + gl - M]);
+      v0 = __ldg(r + idx[hdr.x + hdr.y + gl - M]);
     }
   };
   auto store_r = [&](double* sb, double v0, double v1) {
-    if (gl < M) {
+    if (gl < M)
       reinterpret_cast<double2*>(sb)[gl] = make_double2(v0, v1);
-    } else {
-      sb[NV + gl - M] = v0;
-    }
+    else
+      sb[NV2 + gl - M] = v0;
   };
   if (lane == 0) {
     for (int s = 0; s < nstage; ++s) mbar_init(bars + s, 1);
@@ -1427,28 +1433,29 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
   if (first < ngroups) {
     mbar_wait(bars, 0);
     phase ^= 1u;
-    double v0, v1;
     const bool valid = g < P && first * P + g < npatch;
-    load_r(0, valid, v0, v1);
-    if (valid) store_r(sbuf + g * NB, v0, v1);
+    double v0, v1;
+    load_r(patch_at(0, first), valid, v0, v1);
+    if (valid) store_r(sbuf + g * NBS, v0, v1);
   }
   __syncwarp();
   // per-lane pair offsets of the column loop (compile-time j): velocity row
   // gl reads A(gl, j) -- column j's entry gl when gl <= j, else column gl's
-  // entry j -- b_hat row a reads its pair j
+  // entry j -- b_hat row a = gl - M reads its pair j (b_hat pairs follow U)
   const int a_row = gl - M;
-  const int own_col = gl < M ? gl * (gl + 1) / 2 : A2 + NP * M + a_row * M;  // b_hat pairs follow U
+  const int own_col = gl < M ? gl * (gl + 1) / 2 : A2 + NP * M + a_row * M;
   int stage = 0, it = 0;
   for (int q = first; q < ngroups; q += stride, ++it) {
     const int qr = q + nstage * stride;
     const int qn = q + stride;
     const bool valid = g < P && q * P + g < npatch;
-    const unsigned char* B = ring + (size_t)stage * stage_bytes + (size_t)(g < P ? g : 0) * bytes;
+    const unsigned char* B = patch_at(stage, q);
+    const int2 hdr = *reinterpret_cast<const int2*>(B);
     const double2* AP = reinterpret_cast<const double2*>(B + 16);
     const double* U = reinterpret_cast<const double*>(B + 16) + 2 * A2;
     const double* Si = U + 4 * NP * M;
-    const int* pos = reinterpret_cast<const int*>(Si + NP * NP) + NB;
-    const double* sb = sbuf + ((it & 1) * P + (g < P ? g : 0)) * NB;
+    const int* pos = reinterpret_cast<const int*>(Si + NP * NP) + hdr.x + hdr.y + NP;
+    const double* sb = sbuf + ((it & 1) * P + gg) * NBS;
     const int sn = stage + 1 == nstage ? 0 : stage + 1;
     // the next group's r, requested before this group's solve
     double nv0 = 0.0, nv1 = 0.0;
@@ -1457,27 +1464,25 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
       mbar_wait(bars + sn, (phase >> sn) & 1u);
       phase ^= 1u << sn;
       nvalid = g < P && qn * P + g < npatch;
-      load_r(sn, nvalid, nv0, nv1);
+      load_r(patch_at(sn, qn), nvalid, nv0, nv1);
     }
     const double2* SB = reinterpret_cast<const double2*>(sb);
     double tx = 0.0, ty = 0.0;
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       const double2 b = SB[j];
-      const int ao = (gl < M && gl <= j) ? j * (j + 1) / 2 + gl : own_col + j;
-      const double2 a = AP[ao];
+      const double2 a = AP[(gl < M && gl <= j) ? j * (j + 1) / 2 + gl : own_col + j];
       tx = fma(a.x, b.x, tx);
       ty = fma(a.y, b.y, ty);
     }
     double xl = tx + ty;
     const int ar = gl < M ? 0 : a_row;
 #pragma unroll
-    for (int e = 0; e < NP; ++e) xl = fma(Si[ar * NP + e], sb[NV + e], xl);
-    if (valid && gl >= M) out[pos[NV + a_row]] = xl;
+    for (int e = 0; e < NP; ++e) xl = fma(Si[ar * NP + e], sb[NV2 + e], xl);
+    if (valid && gl >= M) out[pos[hdr.x + hdr.y + a_row]] = xl;
     double xp[NP];
 #pragma unroll
-    for (int e = 0; e < NP; ++e)
-      xp[e] = __shfl_sync(0xffffffffu, xl, (g < P ? g : 0) * L + M + e);
+    for (int e = 0; e < NP; ++e) xp[e] = __shfl_sync(0xffffffffu, xl, gg * L + M + e);
     if (valid && gl < M) {
       const double2* UP = reinterpret_cast<const double2*>(U);
       double ox = tx, oy = ty;
@@ -1487,10 +1492,10 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
         ox = fma(u.x, xp[e], ox);
         oy = fma(u.y, xp[e], oy);
       }
-      out[pos[gl]] = ox;
-      out[pos[M + gl]] = oy;
+      if (gl < hdr.x) out[pos[gl]] = ox;
+      if (gl < hdr.y) out[pos[hdr.x + gl]] = oy;
     }
-    if (nvalid) store_r(sbuf + (((it + 1) & 1) * P + g) * NB, nv0, nv1);
+    if (nvalid) store_r(sbuf + (((it + 1) & 1) * P + g) * NBS, nv0, nv1);
     __syncwarp();
     if (lane == 0 && qr < ngroups) {
       fence_proxy_async();
@@ -1688,9 +1693,9 @@ template <int M, int NP>
 static void launch_fixed(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const double* r,
                          const int* gate) {
   static thread_local int configured = 0;
-  constexpr int L = M + NP, P = 32 / L, NB = 2 * M + NP;
+  constexpr int L = M + NP, P = 32 / L, NB = ((2 * M + NP) + 1) & ~1;
   const int npatch = cl.k1 - cl.k0;
-  const int bytes = (int)cl.slot_bytes;  // every blob of the class has this size
+  const int bytes = (int)cl.slot_bytes;  // the largest blob of the class
   const int nstage = std::max(2, env_int("SAG_VANKA_STAGES", 2));
   const int per_warp = nstage * P * bytes + ((nstage + 1) & ~1) * 8 + 2 * P * NB * 8;
   const int cta_budget = env_int("SAG_VANKA_CTA_SMEM", 60000);
@@ -1707,6 +1712,7 @@ static void launch_fixed(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const 
   const long long ngroups = (npatch + P - 1) / P;
   const int blocks = (int)std::max(1LL, std::min<long long>((ngroups + warps - 1) / warps,
                                                           (long long)occ * c.num_sms));
+  SAG_REQUIRE(f.seq, SAG_ERROR, "apply_vanka: the fixed-shape kernel needs dof-ordered results");
   kern<<<blocks, warps * 32, smem, c.stream>>>(npatch, f.blob.p, f.off.p + cl.k0, bytes, nstage,
                                                 r, f.out.p, gate);
   SAG_LAUNCHED(c);
@@ -1788,6 +1794,18 @@ void vanka_apply_stage(Ctx& c, const Vanka& f, const double* r, double* delta, i
   }
 }
 
+void vanka_gather_range(Ctx& c, const Vanka& f, int d0, int d1, double* delta) {
+  if (d1 <= d0) return;
+  const double* w = f.w_ext ? f.w.p + d0 : nullptr;
+  if (f.seq)
+    vanka_gather_seq_kernel<<<grid_for(c, d1 - d0), 256, 0, c.stream>>>(
+        d1 - d0, f.dof_ptr.p + d0, f.out.p, w, delta + d0, nullptr, 1.0, nullptr);
+  else
+    vanka_gather_kernel<<<grid_for(c, d1 - d0), 256, 0, c.stream>>>(
+        d1 - d0, f.dof_ptr.p + d0, f.dof_slot.p, f.out.p, w, delta + d0, nullptr, 1.0, nullptr);
+  SAG_LAUNCHED(c);
+}
+
 void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega) {
   launch_patch_any(c, f, r, nullptr);
   launch_gather(c, f, nullptr, x, omega, nullptr);
@@ -1844,261 +1862,6 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
   if (weights) SAG_CUDA(cudaMemcpy(weights, f.w.p, sizeof(double) * f.n, cudaMemcpyDefault));
 }
 
-
-// ==================================== the host-buffer step, pipelined ==
-// sag_vanka_spmv with pinned host buffers moves 8n bytes in and 16n out over
-// the host link, which bounds the step when done as copy-in, compute,
-// copy-out. The plan cuts the patches into C contiguous ranges (stages) and
-// orders every per-dof piece of work by the first stage at which it can run:
-//   in(d)  = stage of the lowest patch containing d: x_d is read from host
-//            memory (mapped, no copy call) by the stage-in(d) copy kernel --
-//            a patch of stage k only touches dofs with in <= k;
-//   ga(d)  = stage of the highest patch containing d: delta_d is complete
-//            after that stage's patches and is written straight to host
-//            memory by the gather;
-//   sp(d)  = max in(c) over the columns of row d: y_d is computed and written
-//            to host memory once those x values have landed.
-// Three streams -- copy-in, patch solves (c.stream), host writes -- so the
-// two link directions and the HBM work overlap; every result is the one the
-// unpipelined path computes (same kernels' arithmetic, same order).
-struct StreamPlan {
-  const Matrix* K = nullptr;
-  int C = 0;
-  std::vector<std::vector<Vanka::RClass>> cls;  // per stage: class windows
-  std::vector<int> in_ptr, sp_ptr, ga_ptr;      // C + 1 offsets into the lists
-  DevBuf<int> in_ids, sp_ids, ga_ids;
-  cudaStream_t s_in = nullptr, s_out = nullptr;
-  std::vector<cudaEvent_t> ev_in, ev_patch;
-  cudaEvent_t ev_start = nullptr, ev_done = nullptr;
-  ~StreamPlan() {
-    for (auto e : ev_in) cudaEventDestroy(e);
-    for (auto e : ev_patch) cudaEventDestroy(e);
-    if (ev_start) cudaEventDestroy(ev_start);
-    if (ev_done) cudaEventDestroy(ev_done);
-    if (s_in) cudaStreamDestroy(s_in);
-    if (s_out) cudaStreamDestroy(s_out);
-  }
-};
-
-__global__ void xin_list_kernel(int cnt, const int* __restrict__ ids, const double* hx,
-                                double* __restrict__ dx) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-    const int d = __ldg(ids + i);
-    dx[d] = hx[d];
-  }
-}
-
-// spmv_kernel's Store epilogue over a list of rows (y may be host memory)
-template <int G>
-__global__ void __launch_bounds__(256) spmv_list_kernel(int cnt, const int* __restrict__ rows,
-                                                        const int* __restrict__ rp,
-                                                        const int* __restrict__ ci,
-                                                        const double* __restrict__ val,
-                                                        const double* __restrict__ x, double* y) {
-  constexpr int RPW = 32 / G;
-  const int lane = threadIdx.x & 31, sub = lane & (G - 1), grp = lane / G;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int base = warp * RPW; base < cnt; base += nwarps * RPW) {
-    const int i = base + grp;
-    double s = 0.0;
-    const int row = i < cnt ? __ldg(rows + i) : 0;
-    if (i < cnt) {
-      const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
-      for (int k0 = beg + sub; k0 < end; k0 += 4 * G) {
-        double v[4], xv[4];
-        int cc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u * G;
-          const bool in = k < end;
-          v[u] = in ? __ldcs(val + k) : 0.0;
-          cc[u] = in ? __ldcs(ci + k) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) xv[u] = (k0 + u * G < end) ? __ldg(x + cc[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s = fma(v[u], xv[u], s);
-      }
-    }
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-    if (sub == 0 && i < cnt) y[row] = s;
-  }
-}
-
-// vanka_gather_seq_kernel over a list of dofs (delta may be host memory)
-__global__ void gather_list_kernel(int cnt, const int* __restrict__ ids,
-                                   const int* __restrict__ dof_ptr, const double* __restrict__ out,
-                                   const double* __restrict__ w, double* delta) {
-  constexpr int U = 8;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-    const int d = __ldg(ids + i);
-    const int s0 = __ldg(dof_ptr + d), s1 = __ldg(dof_ptr + d + 1);
-    const double wd = w ? __ldg(w + d) : (s1 > s0 ? 1.0 / (double)(s1 - s0) : 0.0);
-    double acc = 0.0;
-    for (int sb = s0; sb < s1; sb += U) {
-      double v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = sb + u < s1 ? __ldcs(out + sb + u) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (sb + u < s1) acc = __dadd_rn(acc, __dmul_rn(wd, v[u]));
-    }
-    delta[d] = acc;
-  }
-}
-
-static std::shared_ptr<StreamPlan> stream_plan(Ctx& c, Vanka& f, const Matrix& K, int C) {
-  if (f.stream_plan && f.stream_plan->K == &K && f.stream_plan->C == C) return f.stream_plan;
-  SAG_REQUIRE(f.seq, SAG_ERROR, "pipelined step: needs the dof-ordered gather");
-  auto P = std::make_shared<StreamPlan>();
-  P->K = &K;
-  P->C = C;
-  const int n = f.n, np_ = f.npatch;
-  std::vector<int> dptr(n + 1), dslot(std::max<long long>(f.nslots, 1));
-  std::vector<int> rp(n + 1), ci(std::max<long long>(K.nnz, 1));
-  SAG_CUDA(cudaMemcpyAsync(dptr.data(), f.dof_ptr.p, 4 * (size_t)(n + 1), cudaMemcpyDeviceToHost, c.stream));
-  if (f.nslots)
-    SAG_CUDA(cudaMemcpyAsync(dslot.data(), f.dof_slot.p, 4 * (size_t)f.nslots, cudaMemcpyDeviceToHost, c.stream));
-  SAG_CUDA(cudaMemcpyAsync(rp.data(), K.rp.p, 4 * (size_t)(n + 1), cudaMemcpyDeviceToHost, c.stream));
-  if (K.nnz) SAG_CUDA(cudaMemcpyAsync(ci.data(), K.ci.p, 4 * (size_t)K.nnz, cudaMemcpyDeviceToHost, c.stream));
-  SAG_CUDA(cudaStreamSynchronize(c.stream));
-  // slots are numbered patch by patch: patch of a slot by its base
-  std::vector<long long> sbase(np_ + 1, 0);
-  for (int i = 0; i < np_; ++i) sbase[i + 1] = sbase[i] + f.h_nv[i] + f.h_np[i];
-  auto patch_of = [&](int s) {
-    return (int)(std::upper_bound(sbase.begin(), sbase.end(), (long long)s) - sbase.begin()) - 1;
-  };
-  std::vector<long long> b(C + 1);
-  for (int k = 0; k <= C; ++k) b[k] = (long long)np_ * k / C;
-  auto stage_of = [&](int p) {
-    return (int)(std::upper_bound(b.begin(), b.end(), (long long)p) - b.begin()) - 1;
-  };
-  std::vector<int> in(n), ga(n), sp(n);
-  for (int d = 0; d < n; ++d) {
-    if (dptr[d + 1] > dptr[d]) {
-      in[d] = stage_of(patch_of(dslot[dptr[d]]));
-      ga[d] = stage_of(patch_of(dslot[dptr[d + 1] - 1]));
-    } else {
-      in[d] = ga[d] = (int)((long long)d * C / std::max(n, 1));
-    }
-  }
-  for (int d = 0; d < n; ++d) {
-    int m = in[d];
-    for (int q = rp[d]; q < rp[d + 1]; ++q) m = std::max(m, in[ci[q]]);
-    sp[d] = m;
-  }
-  auto lists = [&](const std::vector<int>& st, std::vector<int>& ptr, DevBuf<int>& ids) {
-    ptr.assign(C + 1, 0);
-    for (int d = 0; d < n; ++d) ++ptr[st[d] + 1];
-    for (int k = 0; k < C; ++k) ptr[k + 1] += ptr[k];
-    std::vector<int> pos(ptr.begin(), ptr.end() - 1), h(std::max(n, 1));
-    for (int d = 0; d < n; ++d) h[pos[st[d]]++] = d;
-    ids.alloc(std::max(n, 1));
-    SAG_CUDA(cudaMemcpyAsync(ids.p, h.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c.stream));
-  };
-  lists(in, P->in_ptr, P->in_ids);
-  lists(sp, P->sp_ptr, P->sp_ids);
-  lists(ga, P->ga_ptr, P->ga_ids);
-  // per stage, each size class narrowed to the blobs of the stage's patches
-  // (patch ids increase within a class: the classes are a stable sort)
-  P->cls.resize(C);
-  for (int k = 0; k < C; ++k)
-    for (const auto& cl : f.rclasses) {
-      auto lo = std::lower_bound(f.blob_patch.begin() + cl.k0, f.blob_patch.begin() + cl.k1,
-                                 (int)b[k]);
-      auto hi = std::lower_bound(lo, f.blob_patch.begin() + cl.k1, (int)b[k + 1]);
-      Vanka::RClass w = cl;
-      w.k0 = (int)(lo - f.blob_patch.begin());
-      w.k1 = (int)(hi - f.blob_patch.begin());
-      P->cls[k].push_back(w);
-    }
-  SAG_CUDA(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
-  SAG_CUDA(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
-  P->ev_in.resize(C);
-  P->ev_patch.resize(C);
-  for (int k = 0; k < C; ++k) {
-    SAG_CUDA(cudaEventCreateWithFlags(&P->ev_in[k], cudaEventDisableTiming));
-    SAG_CUDA(cudaEventCreateWithFlags(&P->ev_patch[k], cudaEventDisableTiming));
-  }
-  SAG_CUDA(cudaEventCreateWithFlags(&P->ev_start, cudaEventDisableTiming));
-  SAG_CUDA(cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming));
-  SAG_CUDA(cudaStreamSynchronize(c.stream));
-  f.stream_plan = P;
-  return P;
-}
-
-// The device-accessible address of mapped (pinned) host memory, or null.
-static const void* mapped(const void* p) {
-  if (!p) return nullptr;
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
-}
-
-// delta = apply_vanka(x), y = K x with x, delta, y pinned host memory;
-// false when the buffers do not qualify (the caller takes the staged path)
-bool vanka_spmv_pipelined(Ctx& c, Vanka& f, const Matrix& K, const double* x, double* delta,
-                          double* y) {
-  const char* e = getenv("SAG_STREAMED_STEP");
-  if (e && atoi(e) == 0) return false;
-  const double* hx = static_cast<const double*>(mapped(x));
-  double* hd = static_cast<double*>(const_cast<void*>(mapped(delta)));
-  double* hy = static_cast<double*>(const_cast<void*>(mapped(y)));
-  if (!hx || !hd || !hy || !f.seq || f.n == 0) return false;
-  const int C = std::max(1, env_int("SAG_STREAMED_STAGES", 12));
-  auto P = stream_plan(c, f, K, C);
-  const int n = f.n;
-  double* dx = c.stage_buf(0, n);
-  const double* w = f.w_ext ? f.w.p : nullptr;
-  SAG_CUDA(cudaEventRecord(P->ev_start, c.stream));
-  SAG_CUDA(cudaStreamWaitEvent(P->s_in, P->ev_start, 0));
-  SAG_CUDA(cudaStreamWaitEvent(P->s_out, P->ev_start, 0));
-  for (int k = 0; k < C; ++k) {
-    const int cnt = P->in_ptr[k + 1] - P->in_ptr[k];
-    if (cnt) {
-      xin_list_kernel<<<grid_for(c, cnt), 256, 0, P->s_in>>>(cnt, P->in_ids.p + P->in_ptr[k],
-                                                             hx, dx);
-      SAG_LAUNCHED(c);
-    }
-    SAG_CUDA(cudaEventRecord(P->ev_in[k], P->s_in));
-  }
-  for (int k = 0; k < C; ++k) {
-    SAG_CUDA(cudaStreamWaitEvent(c.stream, P->ev_in[k], 0));
-    launch_patch_any(c, f, dx, nullptr, &P->cls[k]);
-    SAG_CUDA(cudaEventRecord(P->ev_patch[k], c.stream));
-    // host writes: y rows whose x has landed, delta dofs whose patches are done
-    SAG_CUDA(cudaStreamWaitEvent(P->s_out, P->ev_in[k], 0));
-    const int ns = P->sp_ptr[k + 1] - P->sp_ptr[k];
-    if (ns) {
-      const int* rows = P->sp_ids.p + P->sp_ptr[k];
-      const int g = grid_for(c, (long long)ns * K.group);
-      switch (K.group) {
-        case 2: spmv_list_kernel<2><<<g, 256, 0, P->s_out>>>(ns, rows, K.rp.p, K.ci.p, K.v.p, dx, hy); break;
-        case 4: spmv_list_kernel<4><<<g, 256, 0, P->s_out>>>(ns, rows, K.rp.p, K.ci.p, K.v.p, dx, hy); break;
-        case 8: spmv_list_kernel<8><<<g, 256, 0, P->s_out>>>(ns, rows, K.rp.p, K.ci.p, K.v.p, dx, hy); break;
-        case 16: spmv_list_kernel<16><<<g, 256, 0, P->s_out>>>(ns, rows, K.rp.p, K.ci.p, K.v.p, dx, hy); break;
-        default: spmv_list_kernel<32><<<g, 256, 0, P->s_out>>>(ns, rows, K.rp.p, K.ci.p, K.v.p, dx, hy); break;
-      }
-      SAG_LAUNCHED(c);
-    }
-    SAG_CUDA(cudaStreamWaitEvent(P->s_out, P->ev_patch[k], 0));
-    const int ng = P->ga_ptr[k + 1] - P->ga_ptr[k];
-    if (ng) {
-      gather_list_kernel<<<grid_for(c, ng), 256, 0, P->s_out>>>(
-          ng, P->ga_ids.p + P->ga_ptr[k], f.dof_ptr.p, f.out.p, w, hd);
-      SAG_LAUNCHED(c);
-    }
-  }
-  SAG_CUDA(cudaEventRecord(P->ev_done, P->s_out));
-  SAG_CUDA(cudaStreamWaitEvent(c.stream, P->ev_done, 0));
-  SAG_CUDA(cudaStreamSynchronize(c.stream));
-  return true;
-}
 
 }  // namespace sag
 
@@ -2303,23 +2066,39 @@ int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const 
     const int n = f->f.n;
     SAG_REQUIRE(k->m.nrows == n && k->m.ncols == n, SAG_DIMENSION_MISMATCH,
                 "sag_vanka_spmv: operator and factorization sizes differ");
-    // pinned host buffers: the step pipelined in stages (copy-in, patch
-    // solves and host writes of y and delta overlap)
-    if (vanka_spmv_pipelined(c, const_cast<Vanka&>(f->f), k->m, x, delta, y)) return;
     InVec xi(c, x, n, 0);                 // x crosses the host link once
     OutVec yo(c, y, n, 2, false);
     OutVec d(c, delta, n, 1, false);
-    launch_spmv(c, k->m, xi.d, yo.d, Epi::Store);
-    if (yo.host) {
-      // y's device->host copy runs on the copy stream under the Vanka sweep
-      cudaStream_t cs = c.copy();
+    if (!yo.host && !d.host) {
+      launch_spmv(c, k->m, xi.d, yo.d, Epi::Store);
+      vanka_apply(c, f->f, xi.d, d.d);
+      return;
+    }
+    // host outputs: y and delta leave in row / dof chunks on the copy
+    // stream as they are computed, so the device->host direction (twice the
+    // bytes of the input) starts right after the first SpMV chunk and runs
+    // under the rest of the step
+    const int C = 4;
+    cudaStream_t cs = c.copy();
+    auto out_chunk = [&](double* host, const double* dev, int a, int b) {
       SAG_CUDA(cudaEventRecord(c.copy_ev, c.stream));
       SAG_CUDA(cudaStreamWaitEvent(cs, c.copy_ev, 0));
-      SAG_CUDA(cudaMemcpyAsync(yo.host, yo.d, sizeof(double) * n, cudaMemcpyDeviceToHost, cs));
+      SAG_CUDA(cudaMemcpyAsync(host + a, dev + a, sizeof(double) * (b - a),
+                               cudaMemcpyDeviceToHost, cs));
+    };
+    for (int q = 0; q < C; ++q) {
+      const int a = (int)((long long)n * q / C), b = (int)((long long)n * (q + 1) / C);
+      launch_spmv_rows(c, k->m, a, b, xi.d, yo.d);
+      if (yo.host) out_chunk(yo.host, yo.d, a, b);
     }
-    vanka_apply(c, f->f, xi.d, d.d);
-    d.finish();
-    if (yo.host) SAG_CUDA(cudaStreamSynchronize(c.copy()));
+    launch_patch_any(c, f->f, xi.d, nullptr);
+    for (int q = 0; q < C; ++q) {
+      const int a = (int)((long long)n * q / C), b = (int)((long long)n * (q + 1) / C);
+      vanka_gather_range(c, f->f, a, b, d.d);
+      if (d.host) out_chunk(d.host, d.d, a, b);
+    }
+    SAG_CUDA(cudaStreamSynchronize(cs));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
 

@@ -582,6 +582,99 @@ ScalarHierarchy build_scalar_hierarchy(Device& dev, const SparseMatrix& a, const
   return h;
 }
 
+// ---- multi-GPU: the partitioned solve -----------------------
+Communicator::NcclId Communicator::nccl_unique_id() {
+  NcclId id{};
+  check(sag_nccl_unique_id(id.data()));
+  return id;
+}
+
+Communicator::Communicator(Device& dev, int nranks, int rank, const NcclId& id)
+    : size_(nranks), rank_(rank) {
+  check(sag_comm_create_nccl(dev.handle(), nranks, rank, id.data(), &comm_));
+}
+
+Communicator::Communicator(int nranks, int rank, const sag_comm_ops& ops)
+    : size_(nranks), rank_(rank) {
+  check(sag_comm_create_host(nranks, rank, &ops, &comm_));
+}
+
+Communicator::~Communicator() { sag_comm_destroy(comm_); }
+
+namespace {
+sag_csr csr_view(const SparseMatrix& m) {
+  return sag_csr{m.nrows, m.ncols, m.row_offsets.data(), m.col_indices.data(), m.values.data()};
+}
+}  // namespace
+
+DistDCPreconditioner::DistDCPreconditioner(Device& dev, Communicator& comm,
+                                           const SaddleSystem& sys0, const SaddleSystem& sys1,
+                                           TransferPair transfer, SolverConfig cfg)
+    : dev_(dev), comm_(comm), cfg_(std::move(cfg)) {
+  if (cfg_.validate) cfg_.check();
+  if (sys0.disc == Discretization::SV)
+    throw UnsupportedDiscretization("gpu::DistDCPreconditioner: Taylor-Hood systems only");
+  if (transfer.n_u0 != sys0.n_u() || transfer.n_p0 != sys0.n_p)
+    throw DimensionMismatch("DCPreconditioner: transfer does not match the high-order system");
+  k0_ = assemble_saddle_matrix(dev, sys0);
+  h_ = build_monolithic_hierarchy(dev, sys1, cfg_.amg);
+  const int nl = h_.num_levels();
+  std::vector<sag_csr> lv(nl), pv(std::max(nl - 1, 1));
+  std::vector<int> nxyz(3 * nl);
+  for (int l = 0; l < nl; ++l) {
+    lv[l] = csr_view(h_.levels[l].k);
+    if (l + 1 < nl) pv[l] = csr_view(h_.levels[l].p);
+    nxyz[3 * l] = h_.levels[l].n_x;
+    nxyz[3 * l + 1] = h_.levels[l].n_y;
+    nxyz[3 * l + 2] = h_.levels[l].n_p;
+  }
+  const sag_csr k = csr_view(k0_);
+  const sag_solver_config c = to_c(cfg_);
+  check(sag_dist_create(dev.handle(), comm.handle(), &k, sys0.n_x, sys0.n_y, sys0.n_p, nl,
+                        lv.data(), pv.data(), nxyz.data(), &c, &d_));
+  long long info[7];
+  check(sag_dist_info(d_, info));
+  l2g_.resize(info[0]);
+  owned_.resize(info[0]);
+  check(sag_dist_local_dofs(d_, l2g_.data(), owned_.data()));
+}
+
+DistDCPreconditioner::~DistDCPreconditioner() { sag_dist_destroy(d_); }
+
+SolveResult DistDCPreconditioner::solve(const std::vector<double>& rhs) const {
+  if ((int)rhs.size() != k0_.nrows) throw DimensionMismatch("solve_stokes: rhs length");
+  const size_t nl = l2g_.size();
+  std::vector<double> b(nl), x(nl);
+  for (size_t i = 0; i < nl; ++i) b[i] = rhs[l2g_[i]];
+  sag_krylov_report rep{};
+  std::vector<double> hist(cfg_.max_iters + 2);
+  check(sag_dist_solve_stokes(dev_.handle(), d_, b.data(), x.data(), &rep, hist.data(),
+                              (int)hist.size()));
+  // the global solution: owned entries, summed over the ranks (one all-reduce)
+  std::vector<double> xg(rhs.size(), 0.0);
+  for (size_t i = 0; i < nl; ++i)
+    if (owned_[i]) xg[l2g_[i]] = x[i];
+  if (comm_.size() > 1) {
+    sag_ctx* ctx = dev_.handle();
+    void* dbuf = nullptr;
+    check(sag_alloc(ctx, 8 * xg.size(), &dbuf));
+    check(sag_memcpy(ctx, dbuf, xg.data(), 8 * xg.size()));
+    const int st = sag_comm_allreduce(ctx, comm_.handle(), static_cast<double*>(dbuf),
+                                      (long long)xg.size());
+    if (st == SAG_OK) check(sag_memcpy(ctx, xg.data(), dbuf, 8 * xg.size()));
+    sag_free(ctx, dbuf);
+    check(st);
+  }
+  SolveResult out;
+  out.x = std::move(xg);
+  out.report.converged = rep.converged != 0;
+  out.report.iterations = rep.iterations;
+  out.report.final_relative_residual = rep.final_relative_residual;
+  out.report.residual_history.assign(hist.begin(),
+                                     hist.begin() + std::min<int>(rep.history_len, hist.size()));
+  return out;
+}
+
 // ---- FEM assembly on the device --------------------------
 // The host keeps the mesh, the user's callbacks (Dirichlet values, body force,
 // Neumann data) and the boundary bookkeeping; the element loops, every
@@ -1184,6 +1277,29 @@ int sagh_case_assembly_gpu(void* h, int device, int time_reference, double* out)
     out[5] = t_s0;
     out[6] = t_s1;
     out[7] = t_k0;
+  });
+}
+
+// gpu::DistDCPreconditioner at one rank (NCCL communicator of size 1): the C++
+// multi-GPU drop-in end to end. rep = [converged, iterations]
+int sagh_case_solve_dist(void* h, int device, double* x, int* rep, double* res) {
+  return guarded([&] {
+    auto& hc = *static_cast<HostCase*>(h);
+    gpu::Device dev(device);
+    gpu::Communicator comm(dev, 1, 0, gpu::Communicator::NcclId{});
+    SolverConfig cfg;
+    cfg.variant = Variant::DCall;
+    cfg.nu1 = cfg.nu2 = 1;
+    cfg.restart = 30;
+    cfg.tol = 1e-8;
+    cfg.max_iters = 500;
+    cfg.enclosed_flow = hc.c.enclosed;
+    gpu::DistDCPreconditioner prec(dev, comm, hc.c.sys0, hc.c.sys1, hc.c.transfer, cfg);
+    const SolveResult r = prec.solve(hc.c.sys0.rhs);
+    std::copy(r.x.begin(), r.x.end(), x);
+    rep[0] = r.report.converged ? 1 : 0;
+    rep[1] = r.report.iterations;
+    *res = r.report.final_relative_residual;
   });
 }
 

@@ -11,6 +11,7 @@
 // reference's own exception classes (errors.hpp:8-58).
 #pragma once
 
+#include <array>
 #include <memory>
 #include <vector>
 
@@ -176,6 +177,59 @@ MonolithicHierarchy build_monolithic_hierarchy(Device& dev, const SaddleSystem& 
 // hierarchies of the Uzawa preconditioner and the SV mass projection.
 ScalarHierarchy build_scalar_hierarchy(Device& dev, const SparseMatrix& a, const AmgConfig& cfg,
                                        double* times = nullptr);
+
+// ---- multi-GPU: the partitioned solve ----------------------
+// One process per GPU. The communicator carries the collectives: NCCL (rank
+// 0 calls nccl_unique_id() and the caller broadcasts the id -- MPI_Bcast, a
+// file, a socket) or the caller's own host-staged transport (sag_comm_ops).
+class Communicator {
+ public:
+  using NcclId = std::array<unsigned char, 128>;
+  static NcclId nccl_unique_id();
+  Communicator(Device& dev, int nranks, int rank, const NcclId& id);
+  Communicator(int nranks, int rank, const sag_comm_ops& ops);
+  ~Communicator();
+  Communicator(const Communicator&) = delete;
+  Communicator& operator=(const Communicator&) = delete;
+  sag_comm* handle() const { return comm_; }
+  int size() const { return size_; }
+  int rank() const { return rank_; }
+
+ private:
+  sag_comm* comm_ = nullptr;
+  int size_ = 1, rank_ = 0;
+};
+
+// DCPreconditioner + solve_stokes over a row/patch partition of K0 across the
+// communicator's ranks (Taylor-Hood; DC-all / DC-LO / DC-HO, nu <= 1): the
+// same constructor arguments as DCPreconditioner (every rank passes the
+// whole systems), the hierarchy built as DCPreconditioner builds it, then
+// libsag plans this rank's share (sag_dist_create). solve() takes the global
+// rhs and returns the global solution (owned entries summed over the ranks
+// by one all-reduce), the report identical on every rank.
+class DistDCPreconditioner {
+ public:
+  DistDCPreconditioner(Device& dev, Communicator& comm, const SaddleSystem& sys0,
+                       const SaddleSystem& sys1, TransferPair transfer, SolverConfig cfg);
+  ~DistDCPreconditioner();
+  DistDCPreconditioner(const DistDCPreconditioner&) = delete;
+  DistDCPreconditioner& operator=(const DistDCPreconditioner&) = delete;
+  SolveResult solve(const std::vector<double>& rhs) const;
+  const std::vector<long long>& local_to_global() const { return l2g_; }
+  const std::vector<unsigned char>& owned() const { return owned_; }
+  const SparseMatrix& k0() const { return k0_; }
+  sag_dist* handle() const { return d_; }
+
+ private:
+  Device& dev_;
+  Communicator& comm_;
+  SolverConfig cfg_;
+  SparseMatrix k0_;
+  MonolithicHierarchy h_;
+  std::vector<long long> l2g_;
+  std::vector<unsigned char> owned_;
+  sag_dist* d_ = nullptr;
+};
 
 // FEM assembly with the element loops, every from_triplets (sparse.cpp:43-66)
 // and the Dirichlet elimination (fem.cpp:207-266) on the device, bitwise the

@@ -98,11 +98,11 @@ def test_from_triplets_bitwise(S):
     r = np.concatenate([r, [5, 5, 9, 9, 9]])
     c = np.concatenate([c, [499, 499, 0, 0, 0]])
     v = np.concatenate([v, [0.3, -0.3, 1e-300, -1e-300, 0.0]])
-    got = S.from_triplets(nr, nc, r, c, v).to_csr()
+    got = O.Csr(nr, nc, *S.from_triplets(nr, nc, r, c, v).to_csr())
     ref = O.RefMat.from_triplets(nr, nc, r, c, v).csr()
     assert _csr_equal(got, ref)
-    empty = S.from_triplets(3, 4, [], [], []).to_csr()
-    assert np.array_equal(empty.rp, [0, 0, 0, 0])
+    rp0, _, _ = S.from_triplets(3, 4, [], [], []).to_csr()
+    assert np.array_equal(rp0, [0, 0, 0, 0])
     with pytest.raises(S.DimensionMismatch):
         S.from_triplets(3, 3, [0, 3], [0, 0], [1.0, 1.0])
 

@@ -163,11 +163,11 @@ def test_tentative_prolongator_device():
         want[agg[i]] += nv[i] * nv[i]
     want = np.array([math.sqrt(v) for v in want])
     assert cn.tobytes() == want.tobytes()
-    csr = t.to_csr()
+    rp, ci, v = t.to_csr()
     keep = nv != 0.0
-    assert np.array_equal(np.diff(csr.rp), keep.astype(np.int32))
-    assert np.array_equal(csr.ci, agg[keep])
-    assert csr.v.tobytes() == (nv[keep] / want[agg[keep]]).tobytes()
+    assert np.array_equal(np.diff(rp), keep.astype(np.int32))
+    assert np.array_equal(ci, agg[keep])
+    assert v.tobytes() == (nv[keep] / want[agg[keep]]).tobytes()
     with pytest.raises(S.Error):
         S.tentative_prolongator(np.zeros(4, np.int32), 2, np.ones(4))   # aggregate 1 empty
     with pytest.raises(S.Error):

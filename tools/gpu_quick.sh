@@ -1,16 +1,15 @@
-# One GPU-box pass: GPU suite, smoke, config 2/3 bench lines, ncu captures of the
-# hot kernels per level, summarised on the box (gpurun_out/ must stay < 64 MiB).
+# Targeted GPU pass: selected test files ($TESTS), bench lines ($BENCH_CONFIGS),
+# one ncu capture ($NCU_SPEC, e.g. "3 K0"), extra commands ($EXTRA).
 mkdir -p gpurun_out
-set -x
-R=${R:-r02}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt
-timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=25 ${PYTEST_ARGS} > gpurun_out/gpu_tests.log 2>&1; echo tests_rc=$? >> gpurun_out/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo rc=$? >> gpurun_out/smoke.log
-[ -n "$NO_BENCH" ] && exit 0
-timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
-timeout 900 python bench.py --config 3 --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
-[ -n "$NO_NCU" ] && exit 0
-for spec in "2 K0" "3 K0" "3 ISO0" "2 ISO0"; do set -- $spec
+if [ "$TESTS" != "none" ]; then
+  timeout 1500 python -m pytest ${TESTS:-tests} -m gpu -q -p no:cacheprovider --durations=10 > gpurun_out/gpu_tests.log 2>&1; echo tests_rc=$? >> gpurun_out/gpu_tests.log
+fi
+for c in ${BENCH_CONFIGS:-2 3}; do
+  timeout 900 python bench.py --config $c --steps 20 --warmup 5 --no-cpu --no-setup > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err
+done
+if [ -n "$EXTRA" ]; then bash -c "$EXTRA" > gpurun_out/extra.log 2>&1; fi
+if [ -n "$NCU_SPEC" ]; then set -- $NCU_SPEC
  rep=gpurun_out/prof_c$1_$2
  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"spmv_kernel|vanka_patch_kernel|vanka_subwarp_kernel|vanka_fixed_kernel|vanka_gather" -o $rep python tools/prof_once.py --config $1 --level $2 > $rep.log 2>&1
  wl=$(python -c "import bench;print(bench.CONFIGS[$1]['workload'])")
@@ -19,5 +18,5 @@ for spec in "2 K0" "3 K0" "3 ISO0" "2 ISO0"; do set -- $spec
  python tools/ncu_summary.py $rep.ncu-rep > $rep.summary.txt 2>&1
  ncu -i $rep.ncu-rep --page source --csv > $rep.source.csv 2>/dev/null; gzip -f $rep.source.csv
  rm -f $rep.ncu-rep
-done
+fi
 du -sh gpurun_out

@@ -41,7 +41,7 @@ def rows(rep):
 
 
 def kind(name):
-    if re.search(r"vanka_(patch|subwarp)_kernel", name):
+    if re.search(r"vanka_(patch|subwarp|fixed)_kernel", name):
         return "vanka_patch"
     if "vanka_gather" in name:
         return "vanka_gather"

@@ -3,7 +3,7 @@
 round warms up; ncu_traffic.py keeps the second), for ncu captures:
 
     ncu --set full --import-source on --clock-control none \
-        -k regex:"spmv_kernel|vanka_patch_kernel|vanka_subwarp_kernel|vanka_gather" \
+        -k regex:"spmv_kernel|vanka_patch_kernel|vanka_subwarp_kernel|vanka_fixed_kernel|vanka_gather" \
         -o gpurun_out/prof python tools/prof_once.py --config 3 --level ISO0
 
 Order per round: spmv (Store), Vanka patch stage (one launch per size class),
