@@ -255,8 +255,52 @@ static FgmresOut fgmres_dev(Ctx& c, const Matrix& A, const double* b, double* x,
 // not stopped and iterations < max_iters, krylov.cpp:58); the conditions are
 // set on the device from KState. Same operations, same order, no host sync.
 
+// Programmatic dependent launch inside captured graphs: every edge of a
+// kernel -> kernel chain (the source's only successor, the target's only
+// predecessor) becomes a programmatic edge, so the target is launched while
+// the source drains and waits in SAG_PDL_WAIT (griddepcontrol.wait) for its
+// writes -- the launch gap of a dependent small kernel overlaps the previous
+// kernel's tail. SAG_PDL=0 keeps plain edges.
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SAG_PDL");
+    on = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return on == 1;
+}
+
+static void graph_programmatic_edges(cudaGraph_t g) {
+  if (!pdl_enabled()) return;
+  size_t ne = 0;
+  SAG_CUDA(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
+  if (ne == 0) return;
+  std::vector<cudaGraphNode_t> from(ne), to(ne);
+  std::vector<cudaGraphEdgeData> ed(ne);
+  SAG_CUDA(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne));
+  std::map<cudaGraphNode_t, int> outdeg, indeg;
+  for (size_t i = 0; i < ne; ++i) {
+    ++outdeg[from[i]];
+    ++indeg[to[i]];
+  }
+  for (size_t i = 0; i < ne; ++i) {
+    cudaGraphNodeType tf, tt;
+    SAG_CUDA(cudaGraphNodeGetType(from[i], &tf));
+    SAG_CUDA(cudaGraphNodeGetType(to[i], &tt));
+    if (tf != cudaGraphNodeTypeKernel || tt != cudaGraphNodeTypeKernel) continue;
+    if (outdeg[from[i]] != 1 || indeg[to[i]] != 1) continue;
+    if (ed[i].type != cudaGraphDependencyTypeDefault) continue;
+    SAG_CUDA(cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &ed[i], 1));
+    cudaGraphEdgeData e{};
+    e.from_port = cudaGraphKernelNodePortProgrammatic;
+    e.type = cudaGraphDependencyTypeProgrammatic;
+    SAG_CUDA(cudaGraphAddDependencies_v2(g, &from[i], &to[i], &e, 1));
+  }
+}
+
 __global__ void cond_set_kernel(cudaGraphConditionalHandle h, const KState* st, int mode,
                                 int max_iters) {
+  SAG_PDL_WAIT();
   const unsigned v = mode == 0 ? (!st->converged && st->iterations < max_iters)
                                : (!st->stop && st->iterations < max_iters);
   cudaGraphSetConditional(h, v);
@@ -308,6 +352,7 @@ static void cond_node(Ctx& c, cudaGraphConditionalNodeType type, Set set, Body b
   c.stream = outer;
   c.body_depth = d;
   SAG_CUDA(cudaStreamEndCapture(bs, &done));
+  graph_programmatic_edges(p.conditional.phGraph_out[0]);
 }
 
 static bool stream_capturing(Ctx& c);
@@ -378,16 +423,19 @@ static void fgmres_graph(Ctx& c, const Matrix& A, const double* b, double* x, co
 
 __global__ void dense_scatter_kernel(int n, const int* rp, const int* ci, const double* v,
                                      double* A) {
+  SAG_PDL_WAIT();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     for (int k = rp[r]; k < rp[r + 1]; ++k) A[(size_t)r * n + ci[k]] += v[k];
 }
 
 __global__ void pin_kernel(double* A, int n, int row, double pin) {
+  SAG_PDL_WAIT();
   A[(size_t)row * n + row] += pin;
 }
 
 // sparse.cpp:310-341 by one CTA on a row-major matrix in global memory.
 __global__ void __launch_bounds__(1024) dense_lu_kernel(int n, double* A, int* piv, int* err) {
+  SAG_PDL_WAIT();
   __shared__ double sv[32];
   __shared__ int si[32];
   __shared__ int sp;
@@ -466,6 +514,7 @@ __global__ void __launch_bounds__(1024) dense_lu_kernel(int n, double* A, int* p
 // inverse columns: thread c solves e_c with the reference's substitution order
 __global__ void dense_inv_kernel(int n, const double* LU, const int* piv, double* X,
                                  double* Ainv) {
+  SAG_PDL_WAIT();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   double* x = X + (size_t)c * n;
@@ -486,6 +535,7 @@ __global__ void dense_inv_kernel(int n, const double* LU, const int* piv, double
 // x = Ainv b, one warp per row
 __global__ void dense_matvec_kernel(int n, const double* __restrict__ A,
                                     const double* __restrict__ b, double* __restrict__ x) {
+  SAG_PDL_WAIT();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
   const double* row = A + (size_t)warp * n;
@@ -500,6 +550,7 @@ __global__ void dense_matvec_kernel(int n, const double* __restrict__ A,
 __global__ void dense_lu_solve_kernel(int n, const double* __restrict__ LU,
                                       const int* __restrict__ piv, const double* __restrict__ b,
                                       double* __restrict__ x) {
+  SAG_PDL_WAIT();
   const int lane = threadIdx.x;
   for (int i = lane; i < n; i += 32) x[i] = b[piv[i]];
   __syncwarp();
@@ -618,6 +669,7 @@ struct SvTransfer {
 };
 
 __global__ void proj_check_kernel(const KState* st, int* fail) {
+  SAG_PDL_WAIT();
   if (!st->converged) *fail = 1;
 }
 
@@ -939,6 +991,7 @@ static void dc_apply_graph(Ctx& c, Dc& d) {
     }
     SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
     if (d.graph) cudaGraphExecDestroy(d.graph);
+    graph_programmatic_edges(g);
     SAG_CUDA(cudaGraphInstantiate(&d.graph, g, 0));
     cudaGraphDestroy(g);
     d.graph_ok = true;
@@ -960,6 +1013,7 @@ static void dc_apply_graph(Ctx& c, Dc& d) {
 }
 
 __global__ void neg_copy_kernel(int n, const double* __restrict__ in, double* __restrict__ out) {
+  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = -in[i];
 }
@@ -969,6 +1023,7 @@ __global__ void neg_copy_kernel(int n, const double* __restrict__ in, double* __
 // reference's operation order (negation is exact).
 __global__ void sv_mass_inv_kernel(int ne, const double* __restrict__ areas,
                                    const double* __restrict__ s, double* __restrict__ dp) {
+  SAG_PDL_WAIT();
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
     const double cc = __ddiv_rn(3.0, areas[e]);
     const double t0 = -s[3 * e], t1 = -s[3 * e + 1], t2 = -s[3 * e + 2];
@@ -1020,6 +1075,7 @@ static void uzawa_apply_graph(Ctx& c, Uzawa& u) {
     }
     SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
     if (u.graph) cudaGraphExecDestroy(u.graph);
+    graph_programmatic_edges(g);
     SAG_CUDA(cudaGraphInstantiate(&u.graph, g, 0));
     cudaGraphDestroy(g);
     u.graph_ok = true;
@@ -1295,6 +1351,7 @@ void solve_stokes_dev(Ctx& c, const Matrix& K0, int n_u, int n_p, double* din, d
       SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
       if (sg->exec) cudaGraphExecDestroy(sg->exec);
       sg->exec = nullptr;
+      graph_programmatic_edges(g);
       SAG_CUDA(cudaGraphInstantiate(&sg->exec, g, 0));
       cudaGraphDestroy(g);
       std::copy(key, key + 6, sg->key);
@@ -1921,6 +1978,7 @@ struct DistLevel {
   std::unique_ptr<Matrix> K_int, K_bnd;
   std::unique_ptr<Vanka> f_int, f_bnd;
   DevBuf<double> r, v0, z0, w;
+  Krylov kr;  // one rank: the single-GPU fused relaxation
 };
 
 std::unique_ptr<Matrix> upload_local(Ctx& c, const LocalCsr& m, int ncols) {
@@ -2038,6 +2096,11 @@ void vanka(Ctx& c, Dist& d, DistLevel& L, double* v, double* z) {
 // vanka_relax, Krylov-wrapped with nu = 1 (vanka.cpp:199-208): the one-step
 // FGMRES on device scalars
 void relax1(Ctx& c, Dist& d, DistLevel& L, double* x, const double* b, bool x_zero) {
+  if (d.comm->size == 1 && L.f_int && !L.f_bnd && !L.K_bnd) {
+    // one rank (no ghosts): the single-GPU fused kernels, same operations
+    relax_kw(c, *L.K_int, *L.f_int, L.kr, x, b, 1, x_zero);
+    return;
+  }
   double* s = d.sc.p;
   const double* r = b;
   if (!x_zero) {
@@ -2063,7 +2126,10 @@ void cycle0(Ctx& c, Dist& d, double* b, double* x, bool skip_finest) {
   const double* r = b;
   if (relax && cf.nu1 > 0) {
     relax1(c, d, d.l0, x, b, true);
-    apply_op(c, d, d.l0, x, d.l0.r.p, Epi::Resid, b);
+    if (d.l0.kr.st)  // one rank: r = b - y_0 w (= b - K x by linearity, as cycle_level)
+      launch_lin_resid(c, d.nl, d.nl, 1.0, 1.0, b, d.l0.kr.w.p, d.l0.kr.st, d.l0.r.p);
+    else
+      apply_op(c, d, d.l0, x, d.l0.r.p, Epi::Resid, b);
     r = d.l0.r.p;
   } else {
     launch_zero(c, d.nl, x);
@@ -2081,14 +2147,22 @@ void dist_dc_apply(Ctx& c, Dist& d, double* r, double* z) {
   const bool relax_fine = cf.variant != SAG_DC_LO;
   double* x = z;
   const double* r1 = r;
-  if (relax_fine && cf.nu1 > 0) {
+  if (relax_fine && cf.nu1 > 0 && d.k0.kr.st) {
+    // one rank: the residual by linearity fused with the eta weighting, as
+    // dc_apply_dev
     relax1(c, d, d.k0, x, r, true);
-    apply_op(c, d, d.k0, x, d.t.p, Epi::Resid, r);
-    r1 = d.t.p;
+    launch_lin_resid(c, d.nl, d.n_u_loc, cf.eta_u, cf.eta_p, r, d.k0.kr.w.p, d.k0.kr.st,
+                     d.b0.p);
   } else {
-    launch_zero(c, d.nl, x);
+    if (relax_fine && cf.nu1 > 0) {
+      relax1(c, d, d.k0, x, r, true);
+      apply_op(c, d, d.k0, x, d.t.p, Epi::Resid, r);
+      r1 = d.t.p;
+    } else {
+      launch_zero(c, d.nl, x);
+    }
+    launch_eta(c, d.nl, d.n_u_loc, cf.eta_u, cf.eta_p, r1, d.b0.p);  // transfer.cpp:127-135
   }
-  launch_eta(c, d.nl, d.n_u_loc, cf.eta_u, cf.eta_p, r1, d.b0.p);  // transfer.cpp:127-135
   const bool skip = cf.variant == SAG_DC_HO;
   if (cf.gamma <= 1) {
     cycle0(c, d, d.b0.p, d.x0.p, skip);
@@ -2112,6 +2186,15 @@ void dist_dc_apply(Ctx& c, Dist& d, double* r, double* z) {
 // y = x with the global pressure mean removed (preconditioner.cpp:235-240)
 void dist_project(Ctx& c, Dist& d, const double* x, double* y, double* s) {
   const int nu = d.n_u_loc;
+  if (d.comm->size == 1) {  // preconditioner.cpp:235-240 as the single-GPU path
+    Fin f;
+    f.kind = FIN_MEAN;
+    f.i = d.nl - nu;
+    f.out = s;
+    launch_sum(c, d.nl - nu, x + nu, f);
+    launch_project(c, d.nl, nu, x, s, y);
+    return;
+  }
   launch_dot_mask(c, d.nl - nu, x + nu, d.ones.p + nu, d.mask.p + nu, s);
   d.comm->allreduce(c, s, 1);
   if (y != x) launch_copy(c, nu, x, y);
@@ -2149,9 +2232,22 @@ void dist_fgmres(Ctx& c, Dist& d, const double* b, double* x, bool graph) {
     f.out = out;
     return f;
   };
-  mdot(c, d, b, b, s);
-  launch_fin_from(c, fin(FIN_REF, 0, 0), s);                   // ref = ||b||
+  // one rank (no ghosts): the single-GPU fused reductions, same operations
+  const bool one = d.comm->size == 1 && !d.k0.K_bnd;
+  if (one) {
+    launch_ssq(c, n, b, fin(FIN_REF, 0, 0));
+  } else {
+    mdot(c, d, b, b, s);
+    launch_fin_from(c, fin(FIN_REF, 0, 0), s);                 // ref = ||b||
+  }
   auto residual = [&](int hist) {
+    if (one) {
+      SpmvArgs a;
+      a.b = b;
+      a.fin = fin(FIN_BETA, hist, 0);
+      launch_spmv(c, *d.k0.K_int, x, K.r.p, Epi::ResidSsq, a);
+      return;
+    }
     apply_op(c, d, d.k0, x, K.r.p, Epi::Resid, b);
     mdot(c, d, K.r.p, K.r.p, s + 1);
     launch_fin_from(c, fin(FIN_BETA, hist, 0), s + 1);         // beta, g, stop
@@ -2159,6 +2255,10 @@ void dist_fgmres(Ctx& c, Dist& d, const double* b, double* x, bool graph) {
   residual(2);                                                 // history[0]
   auto step = [&](int j) {
     dist_prec(c, d, K.v(j), K.z(j));
+    if (one) {
+      arnoldi_step(c, *d.k0.K_int, K, m, j, K.stop());
+      return;
+    }
     apply_op(c, d, d.k0, K.z(j), K.w.p, Epi::Store);
     for (int i = 0; i <= j; ++i) {                             // MGS (krylov.cpp:63-67)
       mdot(c, d, K.w.p, K.v(i), s + 2 + i);
@@ -2205,7 +2305,14 @@ void dist_fgmres(Ctx& c, Dist& d, const double* b, double* x, bool graph) {
       hd = read_header(c, K.st);
     }
   }
-  apply_op(c, d, d.k0, x, K.r.p, Epi::Resid, b);                // final true residual
+  if (one) {                                                   // final true residual
+    SpmvArgs a;
+    a.b = b;
+    a.fin = fin(FIN_FINAL, 0, 0, c.scal.p);
+    launch_spmv(c, *d.k0.K_int, x, K.r.p, Epi::ResidSsq, a);
+    return;
+  }
+  apply_op(c, d, d.k0, x, K.r.p, Epi::Resid, b);
   mdot(c, d, K.r.p, K.r.p, s + 1);
   launch_fin_from(c, fin(FIN_FINAL, 0, 0, c.scal.p), s + 1);
 }
@@ -2434,6 +2541,7 @@ int sag_dist_create(sag_ctx* ctx, sag_comm* comm, const sag_csr* k0, int n_x, in
       L.v0.alloc(nl);
       L.z0.alloc(nl);
       L.w.alloc(nl);
+      if (comm->size == 1) L.kr.init(nl, 1, 4);
     };
     level(d->k0, pl.k0);
     level(d->l0, pl.l0);
@@ -2561,6 +2669,7 @@ int sag_dist_solve_stokes(sag_ctx* ctx, sag_dist* d, const double* rhs, double* 
           throw;
         }
         SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
+        graph_programmatic_edges(g);
         SAG_CUDA(cudaGraphInstantiate(&d->graph, g, 0));
         cudaGraphDestroy(g);
         d->gkey[0] = key[0];
