@@ -697,6 +697,10 @@ def run_ours(args, ws, rank, local):
         # setup's strength graphs and sparse products on the device
         # (gpu::build_monolithic_hierarchy), compared bitwise
         out["setup"]["hierarchy"] = case.hierarchy_gpu(local)
+    if rank == 0 and ws == 1 and not args.no_setup:
+        # FEM assembly (sys0, quadrisect + sys1, K0) again on the device,
+        # compared with the reference-built systems field by field
+        out["setup"]["fem_assembly"] = case.assembly_gpu(local)
 
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1

@@ -44,12 +44,6 @@ struct Error : std::runtime_error {
     (ctx).launches++;                                       \
   } while (0)
 
-// Programmatic dependent launch: a kernel may be launched before its
-// predecessor in a CUDA graph has finished (programmatic edges, see
-// graph_programmatic_edges); it waits here, before touching any memory, until
-// the predecessor's writes are visible. A no-op for ordinary launches.
-#define SAG_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
-
 template <class T>
 struct DevBuf {
   T* p = nullptr;

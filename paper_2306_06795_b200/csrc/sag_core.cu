@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(256, 8) spmv_kernel(int nrows, const int* __re
                                                    const double* __restrict__ x,
                                                    double* __restrict__ y, SpmvArgs a,
                                                    double* partials, unsigned* ticket) {
-  SAG_PDL_WAIT();
   if (a.gate && *a.gate) return;
   constexpr bool kRed = (E == Epi::StoreDot || E == Epi::ResidSsq);
   constexpr int RPW = 32 / G;  // rows per warp per step
@@ -303,7 +302,6 @@ __global__ void __launch_bounds__(kRedBlock) dot_kernel(int n, const double* __r
                                                         const double* __restrict__ b, Fin fin,
                                                         const int* gate, double* partials,
                                                         unsigned* ticket) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   // four grid strides per pass: eight independent loads in flight per thread
   // (these vectors are streamed once; one load per trip leaves HBM idle)
@@ -327,7 +325,6 @@ __global__ void __launch_bounds__(kRedBlock) dot_kernel(int n, const double* __r
 __global__ void __launch_bounds__(kRedBlock) ssq2_kernel(int n, const double* __restrict__ a,
                                                          Fin f1, Fin f2, double* partials,
                                                          unsigned* ticket) {
-  SAG_PDL_WAIT();
   const int st = gridDim.x * blockDim.x;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
@@ -355,7 +352,6 @@ __global__ void __launch_bounds__(kRedBlock) ssq2_kernel(int n, const double* __
 __global__ void __launch_bounds__(kRedBlock) sum_kernel(int n, const double* __restrict__ a,
                                                         Fin fin, double* partials,
                                                         unsigned* ticket) {
-  SAG_PDL_WAIT();
   double s = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     s += a[i];
@@ -381,7 +377,6 @@ __device__ __forceinline__ void ew4(int n, Load load, Store store) {
 
 __global__ void div_kernel(int n, const double* __restrict__ x, const double* s,
                            double* __restrict__ y, const int* gate, const int* gate2) {
-  SAG_PDL_WAIT();
   if ((gate && *gate) || (gate2 && *gate2)) return;
   const double d = *s;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -394,7 +389,6 @@ __global__ void __launch_bounds__(kRedBlock) mgs_kernel(int n, double* __restric
                                                         const double* __restrict__ vnext,
                                                         Fin fin, const int* gate,
                                                         double* partials, unsigned* ticket) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   const double hh = vprev ? *h : 0.0;
   const int st = gridDim.x * blockDim.x;
@@ -436,7 +430,6 @@ __global__ void __launch_bounds__(kRedBlock) mgs_last_kernel(int n, double* __re
                                                              const double* h, Fin fin,
                                                              const int* gate, int write_w,
                                                              double* partials, unsigned* ticket) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   const double hh = *h;
   const int st = gridDim.x * blockDim.x;
@@ -470,7 +463,6 @@ __global__ void __launch_bounds__(kRedBlock) mgs_last_kernel(int n, double* __re
 __global__ void lin_resid_kernel(int n, int n_u, double eu, double ep,
                                  const double* __restrict__ b, const double* __restrict__ w,
                                  const KState* st, double* __restrict__ r) {
-  SAG_PDL_WAIT();
   const bool step = st->jeff > 0;
   const double y0 = step ? ks_y(const_cast<KState*>(st))[0] : 0.0;
   ew4(n, [&](int i) { return make_double2(b[i], step ? w[i] : 0.0); },
@@ -482,7 +474,6 @@ __global__ void lin_resid_kernel(int n, int n_u, double eu, double ep,
 
 // krylov.cpp:102-107, one thread (j <= restart)
 __global__ void backsub_kernel(KState* st) {
-  SAG_PDL_WAIT();
   const int j = st->jeff, m = st->m;
   const double* h = ks_h(st);
   const double* g = ks_g(st);
@@ -497,7 +488,6 @@ __global__ void backsub_kernel(KState* st) {
 // krylov.cpp:108-110 (+ vanka.cpp:208 for relaxation): x += sum_i y_i Z_i
 __global__ void update_kernel(int n, double* __restrict__ x, const double* __restrict__ Z,
                               size_t zs, const KState* st, int store) {
-  SAG_PDL_WAIT();
   const int j = st->jeff;
   if (j == 0 && !store) return;
   const double* y = ks_y(const_cast<KState*>(st));
@@ -514,7 +504,6 @@ __global__ void update_kernel(int n, double* __restrict__ x, const double* __res
 __global__ void div_mul_kernel(int n, const double* __restrict__ x, const double* s,
                                double* __restrict__ y, const double* __restrict__ d,
                                double* __restrict__ z, const int* gate) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   const double q = *s;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -529,7 +518,6 @@ __global__ void div_mul_kernel(int n, const double* __restrict__ x, const double
 // system itself (the same operations as backsub_kernel), block 0 stores y
 __global__ void update_bs_kernel(int n, double* __restrict__ x, const double* __restrict__ Z,
                                  size_t zs, KState* st, int store) {
-  SAG_PDL_WAIT();
   __shared__ double ys[kUpdBsMax];
   const int j = st->jeff, m = st->m;
   if (threadIdx.x == 0) {
@@ -558,7 +546,6 @@ __global__ void update_bs_kernel(int n, double* __restrict__ x, const double* __
 
 __global__ void mul_kernel(int n, const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ y) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     y[i] = a[i] * b[i];
 }
@@ -566,7 +553,6 @@ __global__ void mul_kernel(int n, const double* __restrict__ a, const double* __
 // inv_diagonal (sparse.cpp:208-215)
 __global__ void inv_diag_kernel(int n, const int* rp, const int* ci, const double* v,
                                 double* dinv, int* bad) {
-  SAG_PDL_WAIT();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     double d = 0.0;
     for (int k = rp[r]; k < rp[r + 1]; ++k)
@@ -578,7 +564,6 @@ __global__ void inv_diag_kernel(int n, const int* rp, const int* ci, const doubl
 
 __global__ void kinit_kernel(KState* st, int m, double tol, double bd, int hist_cap,
                              int keep_ref) {
-  SAG_PDL_WAIT();
   if (!keep_ref) st->ref = 1.0;
   st->tol = tol;
   st->bd = bd;
@@ -595,33 +580,27 @@ __global__ void kinit_kernel(KState* st, int m, double tol, double bd, int hist_
 }
 
 __global__ void copy_kernel(int n, const double* __restrict__ x, double* __restrict__ y) {
-  SAG_PDL_WAIT();
   ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = v; });
 }
 __global__ void zero_kernel(int n, double* __restrict__ y) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     y[i] = 0.0;
 }
 __global__ void project_kernel(int n, int n_u, const double* __restrict__ x, const double* mean,
                                double* __restrict__ y) {
-  SAG_PDL_WAIT();
   const double mu = *mean;
   ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = i < n_u ? v : v - mu; });
 }
 __global__ void eta_kernel(int n, int n_u, double eu, double ep, const double* __restrict__ x,
                            double* __restrict__ y) {
-  SAG_PDL_WAIT();
   ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = (i < n_u ? eu : ep) * v; });
 }
 __global__ void add_kernel(int n, double* __restrict__ x, const double* __restrict__ y) {
-  SAG_PDL_WAIT();
   ew4(n, [&](int i) { return make_double2(x[i], y[i]); },
       [&](int i, double2 v) { x[i] = v.x + v.y; });
 }
 __global__ void axpy_kernel(int n, double* __restrict__ x, double omega,
                             const double* __restrict__ d) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     x[i] = x[i] + omega * d[i];
 }
@@ -753,7 +732,6 @@ void launch_axpy(Ctx& c, int n, double* x, double omega, const double* d) {
 
 __global__ void validate_csr_kernel(int nrows, int ncols, long long nnz, const int* rp,
                                     const int* ci, int* bad) {
-  SAG_PDL_WAIT();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
     const int b = rp[r], e = rp[r + 1];
     if (b > e || b < 0 || (long long)e > nnz) {
@@ -769,7 +747,6 @@ __global__ void validate_csr_kernel(int nrows, int ncols, long long nnz, const i
 }
 
 __global__ void norm_inf_kernel(int nrows, const int* rp, const double* v, double* out) {
-  SAG_PDL_WAIT();
   __shared__ double sh[32];
   double best = 0.0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
@@ -800,25 +777,21 @@ void compute_norm_inf(Ctx& c, Matrix& m) {
 // ------------------------------------------------------------ transpose --
 
 __global__ void row_of_kernel(int nrows, const int* rp, int* row_of) {
-  SAG_PDL_WAIT();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x)
     for (int k = rp[r]; k < rp[r + 1]; ++k) row_of[k] = r;
 }
 __global__ void iota_kernel(long long n, int* a) {
-  SAG_PDL_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     a[i] = (int)i;
 }
 __global__ void count_kernel(long long n, const int* key, int* cnt) {
-  SAG_PDL_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     atomicAdd(cnt + key[i], 1);
 }
 __global__ void permute_kernel(long long n, const int* perm, const int* row_of, const double* v,
                                int* ciT, double* vT) {
-  SAG_PDL_WAIT();
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x) {
     const int o = perm[q];
@@ -925,7 +898,6 @@ __global__ void __launch_bounds__(kRedBlock) dot_mask_kernel(int n, const double
                                                              const unsigned char* __restrict__ mask,
                                                              Fin fin, double* partials,
                                                              unsigned* ticket) {
-  SAG_PDL_WAIT();
   const int st = gridDim.x * blockDim.x;
   double s = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
@@ -935,7 +907,6 @@ __global__ void __launch_bounds__(kRedBlock) dot_mask_kernel(int n, const double
 // y = y + sign * (*s) x   (MGS: w[k] -= h_ij v_i[k], krylov.cpp:66)
 __global__ void axpy_dev_kernel(int n, const double* s, double sign, const double* __restrict__ x,
                                 double* __restrict__ y) {
-  SAG_PDL_WAIT();
   const double h = *s;
   ew4(n, [&](int i) { return make_double2(y[i], x[i]); },
       [&](int i, double2 v) { y[i] = sign < 0.0 ? v.x - h * v.y : v.x + h * v.y; });
@@ -944,7 +915,6 @@ __global__ void axpy_dev_kernel(int n, const double* s, double sign, const doubl
 // when d == 0 (a zero residual, whose Krylov step the reference skips)
 __global__ void div_dev_kernel(int n, const double* __restrict__ x, const double* s, int take_sqrt,
                                double* __restrict__ y) {
-  SAG_PDL_WAIT();
   const double d = take_sqrt ? sqrt(*s) : *s;
   ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = d != 0.0 ? v / d : 0.0; });
 }
@@ -954,7 +924,6 @@ __global__ void div_dev_kernel(int n, const double* __restrict__ x, const double
 // 0 when r = 0 (the reference returns before the step).
 __global__ void fgmres1_coef_kernel(const double* ssq_r, const double* h00p, const double* ssq_w,
                                     double* y0) {
-  SAG_PDL_WAIT();
   const double beta = sqrt(*ssq_r), h00 = *h00p, h10 = sqrt(*ssq_w);
   if (beta == 0.0) {
     *y0 = 0.0;
@@ -973,7 +942,6 @@ __global__ void fgmres1_coef_kernel(const double* ssq_r, const double* h00p, con
 // y = x - (*sum) / count   (project_pressure, preconditioner.cpp:235-240)
 __global__ void sub_mean_kernel(int n, const double* __restrict__ x, const double* sum,
                                 double count, double* __restrict__ y) {
-  SAG_PDL_WAIT();
   const double mean = *sum / count;
   ew4(n, [&](int i) { return x[i]; }, [&](int i, double v) { y[i] = v - mean; });
 }
@@ -981,7 +949,6 @@ __global__ void sub_mean_kernel(int n, const double* __restrict__ x, const doubl
 // (x += y_i z_i, krylov.cpp:108-110)
 __global__ void axpby_kernel(int n, double a, const double* __restrict__ x, double b,
                              double* __restrict__ y) {
-  SAG_PDL_WAIT();
   if (a == 0.0 && b == 0.0) {
     ew4(n, [&](int i) { return 0.0; }, [&](int i, double v) { y[i] = v; });
   } else if (b == 0.0) {
@@ -997,7 +964,6 @@ __global__ void axpby_kernel(int n, double a, const double* __restrict__ x, doub
 // halo pack / unpack: dst[i] = src[idx[i]]; dst[idx[i]] (+)= src[i] (idx unique)
 __global__ void gather_idx_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
                                   double* __restrict__ dst) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     dst[i] = src[idx[i]];
 }
@@ -1006,14 +972,12 @@ __global__ void gather_idx_kernel(int n, const int* __restrict__ idx, const doub
 // them before the kernel's completion is observed by the neighbour
 __global__ void push_idx_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
                                 double* __restrict__ dst) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     dst[i] = src[idx[i]];
   __threadfence_system();
 }
 __global__ void scatter_idx_kernel(int n, const int* __restrict__ idx, const double* __restrict__ src,
                                    double* __restrict__ dst, int add) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int d = idx[i];
     dst[d] = add ? dst[d] + src[i] : src[i];
@@ -1022,8 +986,7 @@ __global__ void scatter_idx_kernel(int n, const int* __restrict__ idx, const dou
 
 // internal launchers of the partitioned-solve primitives (no pointer-kind
 // queries: usable while a stream is being captured)
-__global__ void fin_from_kernel(Fin f, const double* tot) {
-  SAG_PDL_WAIT(); apply_fin(f, *tot); }
+__global__ void fin_from_kernel(Fin f, const double* tot) { apply_fin(f, *tot); }
 void launch_fin_from(Ctx& c, const Fin& f, const double* tot) {
   fin_from_kernel<<<1, 1, 0, c.stream>>>(f, tot);
   SAG_LAUNCHED(c);
@@ -1358,7 +1321,6 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, double* sm, int& s
 }
 
 __global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams p) {
-  SAG_PDL_WAIT();
   __shared__ TailSh s;
   extern __shared__ double sm[];
   cg::cluster_group cl = cg::this_cluster();

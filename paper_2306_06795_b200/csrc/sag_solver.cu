@@ -255,52 +255,8 @@ static FgmresOut fgmres_dev(Ctx& c, const Matrix& A, const double* b, double* x,
 // not stopped and iterations < max_iters, krylov.cpp:58); the conditions are
 // set on the device from KState. Same operations, same order, no host sync.
 
-// Programmatic dependent launch inside captured graphs: every edge of a
-// kernel -> kernel chain (the source's only successor, the target's only
-// predecessor) becomes a programmatic edge, so the target is launched while
-// the source drains and waits in SAG_PDL_WAIT (griddepcontrol.wait) for its
-// writes -- the launch gap of a dependent small kernel overlaps the previous
-// kernel's tail. SAG_PDL=0 keeps plain edges.
-static bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SAG_PDL");
-    on = (e && atoi(e) == 0) ? 0 : 1;
-  }
-  return on == 1;
-}
-
-static void graph_programmatic_edges(cudaGraph_t g) {
-  if (!pdl_enabled()) return;
-  size_t ne = 0;
-  SAG_CUDA(cudaGraphGetEdges_v2(g, nullptr, nullptr, nullptr, &ne));
-  if (ne == 0) return;
-  std::vector<cudaGraphNode_t> from(ne), to(ne);
-  std::vector<cudaGraphEdgeData> ed(ne);
-  SAG_CUDA(cudaGraphGetEdges_v2(g, from.data(), to.data(), ed.data(), &ne));
-  std::map<cudaGraphNode_t, int> outdeg, indeg;
-  for (size_t i = 0; i < ne; ++i) {
-    ++outdeg[from[i]];
-    ++indeg[to[i]];
-  }
-  for (size_t i = 0; i < ne; ++i) {
-    cudaGraphNodeType tf, tt;
-    SAG_CUDA(cudaGraphNodeGetType(from[i], &tf));
-    SAG_CUDA(cudaGraphNodeGetType(to[i], &tt));
-    if (tf != cudaGraphNodeTypeKernel || tt != cudaGraphNodeTypeKernel) continue;
-    if (outdeg[from[i]] != 1 || indeg[to[i]] != 1) continue;
-    if (ed[i].type != cudaGraphDependencyTypeDefault) continue;
-    SAG_CUDA(cudaGraphRemoveDependencies_v2(g, &from[i], &to[i], &ed[i], 1));
-    cudaGraphEdgeData e{};
-    e.from_port = cudaGraphKernelNodePortProgrammatic;
-    e.type = cudaGraphDependencyTypeProgrammatic;
-    SAG_CUDA(cudaGraphAddDependencies_v2(g, &from[i], &to[i], &e, 1));
-  }
-}
-
 __global__ void cond_set_kernel(cudaGraphConditionalHandle h, const KState* st, int mode,
                                 int max_iters) {
-  SAG_PDL_WAIT();
   const unsigned v = mode == 0 ? (!st->converged && st->iterations < max_iters)
                                : (!st->stop && st->iterations < max_iters);
   cudaGraphSetConditional(h, v);
@@ -352,7 +308,6 @@ static void cond_node(Ctx& c, cudaGraphConditionalNodeType type, Set set, Body b
   c.stream = outer;
   c.body_depth = d;
   SAG_CUDA(cudaStreamEndCapture(bs, &done));
-  graph_programmatic_edges(p.conditional.phGraph_out[0]);
 }
 
 static bool stream_capturing(Ctx& c);
@@ -423,19 +378,16 @@ static void fgmres_graph(Ctx& c, const Matrix& A, const double* b, double* x, co
 
 __global__ void dense_scatter_kernel(int n, const int* rp, const int* ci, const double* v,
                                      double* A) {
-  SAG_PDL_WAIT();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     for (int k = rp[r]; k < rp[r + 1]; ++k) A[(size_t)r * n + ci[k]] += v[k];
 }
 
 __global__ void pin_kernel(double* A, int n, int row, double pin) {
-  SAG_PDL_WAIT();
   A[(size_t)row * n + row] += pin;
 }
 
 // sparse.cpp:310-341 by one CTA on a row-major matrix in global memory.
 __global__ void __launch_bounds__(1024) dense_lu_kernel(int n, double* A, int* piv, int* err) {
-  SAG_PDL_WAIT();
   __shared__ double sv[32];
   __shared__ int si[32];
   __shared__ int sp;
@@ -514,7 +466,6 @@ __global__ void __launch_bounds__(1024) dense_lu_kernel(int n, double* A, int* p
 // inverse columns: thread c solves e_c with the reference's substitution order
 __global__ void dense_inv_kernel(int n, const double* LU, const int* piv, double* X,
                                  double* Ainv) {
-  SAG_PDL_WAIT();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   double* x = X + (size_t)c * n;
@@ -535,7 +486,6 @@ __global__ void dense_inv_kernel(int n, const double* LU, const int* piv, double
 // x = Ainv b, one warp per row
 __global__ void dense_matvec_kernel(int n, const double* __restrict__ A,
                                     const double* __restrict__ b, double* __restrict__ x) {
-  SAG_PDL_WAIT();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
   const double* row = A + (size_t)warp * n;
@@ -550,7 +500,6 @@ __global__ void dense_matvec_kernel(int n, const double* __restrict__ A,
 __global__ void dense_lu_solve_kernel(int n, const double* __restrict__ LU,
                                       const int* __restrict__ piv, const double* __restrict__ b,
                                       double* __restrict__ x) {
-  SAG_PDL_WAIT();
   const int lane = threadIdx.x;
   for (int i = lane; i < n; i += 32) x[i] = b[piv[i]];
   __syncwarp();
@@ -669,7 +618,6 @@ struct SvTransfer {
 };
 
 __global__ void proj_check_kernel(const KState* st, int* fail) {
-  SAG_PDL_WAIT();
   if (!st->converged) *fail = 1;
 }
 
@@ -846,7 +794,11 @@ static void sv_restrict(Ctx& c, Dc& d, const double* p_dg, double* p_cg) {
   if (stream_capturing(c)) {
     // inside the DC apply's CUDA graph: the device-side convergence loop; a
     // failure is flagged on the device and raised at the next host check
-    fgmres_graph(c, *t.sh.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, 20, 1e-30, t.outer,
+    // SAG_PROJ_RESTART (diagnostic only; default 20 = transfer.cpp:27) caps the
+    // number of IF nodes per restart cycle of the graph
+    const char* pr = getenv("SAG_PROJ_RESTART");
+    const int rst = pr ? std::max(1, std::min(20, atoi(pr))) : 20;
+    fgmres_graph(c, *t.sh.A[0], t.rhs.p, p_cg, prec, 1e-12, 200, rst, 1e-30, t.outer,
                  c.scal.p + 8);
     proj_check_kernel<<<1, 1, 0, c.stream>>>(t.outer.st, t.fail.p);
     SAG_LAUNCHED(c);
@@ -991,7 +943,6 @@ static void dc_apply_graph(Ctx& c, Dc& d) {
     }
     SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
     if (d.graph) cudaGraphExecDestroy(d.graph);
-    graph_programmatic_edges(g);
     SAG_CUDA(cudaGraphInstantiate(&d.graph, g, 0));
     cudaGraphDestroy(g);
     d.graph_ok = true;
@@ -1013,7 +964,6 @@ static void dc_apply_graph(Ctx& c, Dc& d) {
 }
 
 __global__ void neg_copy_kernel(int n, const double* __restrict__ in, double* __restrict__ out) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = -in[i];
 }
@@ -1023,7 +973,6 @@ __global__ void neg_copy_kernel(int n, const double* __restrict__ in, double* __
 // reference's operation order (negation is exact).
 __global__ void sv_mass_inv_kernel(int ne, const double* __restrict__ areas,
                                    const double* __restrict__ s, double* __restrict__ dp) {
-  SAG_PDL_WAIT();
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x) {
     const double cc = __ddiv_rn(3.0, areas[e]);
     const double t0 = -s[3 * e], t1 = -s[3 * e + 1], t2 = -s[3 * e + 2];
@@ -1075,7 +1024,6 @@ static void uzawa_apply_graph(Ctx& c, Uzawa& u) {
     }
     SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
     if (u.graph) cudaGraphExecDestroy(u.graph);
-    graph_programmatic_edges(g);
     SAG_CUDA(cudaGraphInstantiate(&u.graph, g, 0));
     cudaGraphDestroy(g);
     u.graph_ok = true;
@@ -1351,7 +1299,6 @@ void solve_stokes_dev(Ctx& c, const Matrix& K0, int n_u, int n_p, double* din, d
       SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
       if (sg->exec) cudaGraphExecDestroy(sg->exec);
       sg->exec = nullptr;
-      graph_programmatic_edges(g);
       SAG_CUDA(cudaGraphInstantiate(&sg->exec, g, 0));
       cudaGraphDestroy(g);
       std::copy(key, key + 6, sg->key);
@@ -2669,7 +2616,6 @@ int sag_dist_solve_stokes(sag_ctx* ctx, sag_dist* d, const double* rhs, double* 
           throw;
         }
         SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
-        graph_programmatic_edges(g);
         SAG_CUDA(cudaGraphInstantiate(&d->graph, g, 0));
         cudaGraphDestroy(g);
         d->gkey[0] = key[0];

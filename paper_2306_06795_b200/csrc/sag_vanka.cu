@@ -56,7 +56,6 @@ __device__ __forceinline__ int merge_unique(const int* rp, const int* ci, int ro
 
 __global__ void patch_count_kernel(int npatch, int group, int n_u, int n_x, const int* rp,
                                    const int* ci, int* cnt_v, int* cnt_x) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npatch; i += gridDim.x * blockDim.x) {
     const int row0 = n_u + i * group;
     int nv, nx = 0;
@@ -78,7 +77,6 @@ __global__ void patch_count_kernel(int npatch, int group, int n_u, int n_x, cons
 __global__ void patch_fill_kernel(int npatch, int group, int n_u, int n_x, const int* rp,
                                   const int* ci, const int* vptr, int* vidx, int* pptr,
                                   int* pidx, int* nx_out) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npatch; i += gridDim.x * blockDim.x) {
     const int row0 = n_u + i * group;
     int* dst = vidx + vptr[i];
@@ -326,7 +324,6 @@ __global__ void __launch_bounds__(256) factor_kernel(
     const int* __restrict__ ci, const double* __restrict__ kv, const int* __restrict__ pptr,
     const int* __restrict__ pidx, const int* __restrict__ vptr, const int* __restrict__ vidx,
     const int* __restrict__ nxs, FactorOut fo, int* err) {
-  SAG_PDL_WAIT();
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned char* base = smem + (size_t)wib * wbytes;
@@ -513,7 +510,6 @@ __global__ void __launch_bounds__(256) factor_kernel(
 // (velocity entries first, then pressure, as the apply writes them)
 __global__ void slot_keys_kernel(int npatch, const int* pptr, const int* pidx, const int* vptr,
                                  const int* vidx, const int* sbase, int es, int* keys) {
-  SAG_PDL_WAIT();
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < npatch; k += gridDim.x * blockDim.x) {
     int s = sbase[k];
     for (int q = vptr[k]; q < vptr[k + 1]; ++q, s += es) keys[s] = vidx[q];
@@ -522,21 +518,18 @@ __global__ void slot_keys_kernel(int npatch, const int* pptr, const int* pidx, c
 }
 
 __global__ void fill_int_kernel(long long n, int v, int* a) {
-  SAG_PDL_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     a[i] = v;
 }
 
 __global__ void count_int_kernel(long long n, const int* key, int* cnt) {
-  SAG_PDL_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     atomicAdd(cnt + key[i], 1);
 }
 
 __global__ void iota_int_kernel(long long n, int* a) {
-  SAG_PDL_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     a[i] = (int)i;
@@ -544,7 +537,6 @@ __global__ void iota_int_kernel(long long n, int* a) {
 
 // vanka.cpp:67-73: w_d = 1 / #patches containing d (0 if none)
 __global__ void weights_kernel(int n, const int* dof_ptr, double* w) {
-  SAG_PDL_WAIT();
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
     const int m = dof_ptr[d + 1] - dof_ptr[d];
     w[d] = m > 0 ? 1.0 / (double)m : 0.0;
@@ -559,7 +551,6 @@ static int grid_for(Ctx& c, long long n) {
 // and max |a_ij| (as ordered uint64 bit patterns of non-negative doubles).
 __global__ void asym_kernel(int n_u, const int* rp, const int* ci, const double* v,
                             unsigned long long* out) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_u; i += gridDim.x * blockDim.x) {
     double dmax = 0.0, amax = 0.0;
     for (int q = rp[i]; q < rp[i + 1]; ++q) {
@@ -600,7 +591,6 @@ static bool velocity_block_symmetric(Ctx& c, const Matrix& k, int n_u) {
 }
 
 __global__ void inverse_perm_kernel(long long n, const int* __restrict__ perm, int* __restrict__ inv) {
-  SAG_PDL_WAIT();
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
        t += (long long)gridDim.x * blockDim.x)
     inv[perm[t]] = (int)t;
@@ -610,7 +600,6 @@ __global__ void blob_pos_kernel(int npatch, const int* __restrict__ vptr,
                                 const int* __restrict__ pptr, const long long* __restrict__ ibase,
                                 const int* __restrict__ sbase, const int* __restrict__ pos,
                                 int* __restrict__ I) {
-  SAG_PDL_WAIT();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < npatch; i += gridDim.x * blockDim.x) {
     const int cnt = (vptr[i + 1] - vptr[i]) + (pptr[i + 1] - pptr[i]);
     int* dst = I + ibase[i] + cnt;
@@ -920,7 +909,6 @@ __global__ void __launch_bounds__(256) vanka_patch_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, int sb_len, int pairs, const double* __restrict__ r,
     double* __restrict__ out, int seq, const int* gate) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   constexpr int G = 2 * R + 1;  // gathered values per lane (nv + np <= 32 G)
   // paired blobs (vanka_paired) exist only on symmetric levels, R <= 2
@@ -1203,7 +1191,6 @@ __global__ void __launch_bounds__(256) vanka_subwarp_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, int sb_len, const double* __restrict__ r,
     double* __restrict__ out, int seq, const int* gate) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   constexpr int P = 32 / LPP;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1381,7 +1368,6 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, const double* __restrict__ r, double* __restrict__ out,
     const int* gate) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   constexpr int L = M + NP, P = 32 / L, NV2 = 2 * M;
   constexpr int NBS = (2 * M + NP + 1) & ~1;  // per-patch b stride (16-byte aligned)
@@ -1530,7 +1516,6 @@ __global__ void vanka_gather_kernel(int n, const int* __restrict__ dof_ptr,
                                     const double* __restrict__ out, const double* __restrict__ w,
                                     double* __restrict__ delta, double* __restrict__ xadd,
                                     double omega, const int* gate) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   constexpr int U = 8;  // multiplicities up to U in one pass (K0/ISO0: <= 7)
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
@@ -1566,7 +1551,6 @@ __global__ void vanka_gather_seq_kernel(int n, const int* __restrict__ dof_ptr,
                                         const double* __restrict__ out,
                                         const double* __restrict__ w, double* __restrict__ delta,
                                         double* __restrict__ xadd, double omega, const int* gate) {
-  SAG_PDL_WAIT();
   if (gate && *gate) return;
   constexpr int U = 8;
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
@@ -1602,7 +1586,6 @@ __global__ void vanka_gather_push_kernel(int n, const int* __restrict__ dof_ptr,
                                          const double* __restrict__ w, double* __restrict__ x,
                                          double omega, const int* __restrict__ slot,
                                          const unsigned char* __restrict__ nbr, PeerMap pm) {
-  SAG_PDL_WAIT();
   constexpr int U = 8;
   for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
     const double xo = x[d];
