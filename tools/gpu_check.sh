@@ -9,6 +9,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 [ -n "$NO_BENCH" ] && exit 0
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
 timeout 900 python bench.py --config 3 --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 900 python bench.py --config 4 --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
+timeout 900 python bench.py --dist --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_dist1.json 2> gpurun_out/bench_dist1.err
 [ -n "$NO_NCU" ] && exit 0
 for spec in "2 K0" "3 K0" "3 ISO0" "2 ISO0"; do set -- $spec
  rep=gpurun_out/prof_c$1_$2
