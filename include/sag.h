@@ -343,6 +343,21 @@ int sag_power_rho(sag_ctx* ctx, const sag_matrix* m, const double* d_inv, const 
 int sag_matrix_export(sag_ctx* ctx, const sag_matrix* m, int* row_offsets, int* col_indices,
                       double* values);
 
+/* ---- 3 velocity components (BASELINE config 5) -----------
+ * The reference is 2D only. factor_patches / apply_vanka
+ * (vanka.cpp:11-184) generalised to K rows [x | y | z | p]: one pressure seed
+ * per patch, one LU per velocity component, CTA-per-patch kernels for the
+ * 100-250-dof patches of 3D Taylor-Hood. Parity is against oracle.c's
+ * 3-component restatement (or_*3). */
+typedef struct sag_vanka3 sag_vanka3;
+int sag_factor_patches3(sag_ctx* ctx, const sag_matrix* k, int n_x, int n_y, int n_z, int n_p,
+                        sag_vanka3** out);
+int sag_vanka3_destroy(sag_vanka3* f);
+/* stats = [npatch, n, blob bytes, max patch velocity dofs, slots,
+ *          a_factor_bytes, aux_bytes] */
+int sag_vanka3_stats(const sag_vanka3* f, long long* stats);
+int sag_apply_vanka3(sag_ctx* ctx, const sag_vanka3* f, const double* r, double* delta);
+
 /* ---- FEM assembly on the device, bitwise the reference ---
  * A 2D triangle mesh (mesh.hpp:24-43) as plain arrays: vertices (x, y) pairs,
  * triangles (3 vertex ids each, positively oriented), tri_edges[t][k] = edge

@@ -106,6 +106,17 @@ class or_vanka(C.Structure):
                 ("dense_inverse_bytes", C.c_int64)]
 
 
+class or_patches3(C.Structure):
+    _fields_ = [("npatch", C.c_int), ("pptr", i32p), ("pidx", i32p), ("vptr", i32p),
+                ("vidx", i32p), ("cnt", i32p)]
+
+
+class or_vanka3(C.Structure):
+    _fields_ = [("pat", or_patches3), ("n", C.c_int), ("lu_off", i64p), ("piv_off", i64p),
+                ("aux_off", i64p), ("s_off", i64p), ("lu", f64p), ("piv", i32p),
+                ("uhat", f64p), ("bhat", f64p), ("sinv", f64p), ("weights", f64p)]
+
+
 class or_fgmres_opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iters", C.c_int), ("restart", C.c_int),
                 ("breakdown", C.c_double)]
@@ -268,6 +279,44 @@ class OracleVanka:
             weights=np.ctypeslib.as_array(f.weights, (self.n,)).copy(),
             a_factor_bytes=f.a_factor_bytes, aux_bytes=f.aux_bytes,
             dense_inverse_bytes=f.dense_inverse_bytes)
+
+
+class OracleVanka3:
+    """The 3-component generalisation of build_patches / factor_patches /
+    apply_vanka (vanka.cpp:11-184 with x, y, z blocks) for BASELINE config 5,
+    which the reference does not support: parity of the 3D
+    kernels is pinned to this restatement and to a dense check of it, not to
+    the reference."""
+
+    def __init__(self, k: Csr, n_x, n_y, n_z, n_p):
+        self._k = k
+        p = or_patches3()
+        _ocheck(olib().or_build_patches3(C.byref(_ocsr(k)), int(n_x), int(n_y), int(n_z),
+                                         int(n_p), C.byref(p)))
+        self.f = or_vanka3()
+        rc = olib().or_factor_patches3(C.byref(_ocsr(k)), C.byref(p), C.byref(self.f))
+        n = p.npatch
+        self.pptr = np.ctypeslib.as_array(p.pptr, (n + 1,)).copy()
+        self.vptr = np.ctypeslib.as_array(p.vptr, (n + 1,)).copy()
+        self.pidx = np.ctypeslib.as_array(p.pidx, (max(n, 1),))[:n].copy()
+        self.vidx = np.ctypeslib.as_array(p.vidx, (max(int(self.vptr[-1]), 1),))[
+            :self.vptr[-1]].copy()
+        self.cnt = np.ctypeslib.as_array(p.cnt, (max(3 * n, 1),))[:3 * n].reshape(n, 3).copy()
+        olib().or_patches3_free(C.byref(p))
+        _ocheck(rc)
+        self.n = k.nrows
+
+    def __del__(self):
+        try:
+            olib().or_vanka3_free(C.byref(self.f))
+        except Exception:
+            pass
+
+    def apply(self, r):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        d = np.empty(self.n)
+        olib().or_apply_vanka3(C.byref(self.f), dp(r), dp(d))
+        return d
 
 
 class OracleDC:

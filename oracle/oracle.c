@@ -396,6 +396,234 @@ void or_apply_vanka(const or_vanka* f, const double* r, double* delta) {
   free(xp);
 }
 
+/* ------------------------------------------ 3 components (config 5) --- */
+/* vanka.cpp:11-42 with one seed and three velocity blocks */
+int or_build_patches3(const or_csr* k, int n_x, int n_y, int n_z, int n_p, or_patches3* out) {
+  const int n_u = n_x + n_y + n_z;
+  memset(out, 0, sizeof *out);
+  if (n_p < 0 || k->nrows != n_u + n_p)
+    return fail(OR_DIM, "build_patches3: block sizes do not match K");
+  out->npatch = n_p;
+  out->pptr = XMALLOC(int, n_p + 1);
+  out->pidx = XMALLOC(int, n_p);
+  out->vptr = XMALLOC(int, n_p + 1);
+  out->cnt = XMALLOC(int, 3 * (int64_t)n_p);
+  int64_t cap = 0;
+  for (int p0 = 0; p0 < n_p; ++p0) cap += k->rp[n_u + p0 + 1] - k->rp[n_u + p0];
+  out->vidx = XMALLOC(int, cap > 0 ? cap : 1);
+  int vv = 0;
+  for (int i = 0; i < n_p; ++i) {
+    const int row = n_u + i, start = vv;
+    out->pptr[i] = i;
+    out->pidx[i] = row;
+    for (int q = k->rp[row]; q < k->rp[row + 1]; ++q)  /* canonical row: sorted, unique */
+      if (k->ci[q] < n_u) out->vidx[vv++] = k->ci[q];
+    if (vv == start) {
+      or_patches3_free(out);
+      return fail(OR_SINGULAR_PATCH, "build_patches3: pressure row couples to no velocity DoFs");
+    }
+    int cx = 0, cy = 0;
+    while (start + cx < vv && out->vidx[start + cx] < n_x) ++cx;
+    while (start + cx + cy < vv && out->vidx[start + cx + cy] < n_x + n_y) ++cy;
+    out->cnt[3 * i] = cx;
+    out->cnt[3 * i + 1] = cy;
+    out->cnt[3 * i + 2] = vv - start - cx - cy;
+    out->vptr[i + 1] = vv;
+  }
+  out->pptr[n_p] = n_p;
+  return OR_OK;
+}
+
+void or_patches3_free(or_patches3* p) {
+  free(p->pptr);
+  free(p->pidx);
+  free(p->vptr);
+  free(p->vidx);
+  free(p->cnt);
+  memset(p, 0, sizeof *p);
+}
+
+/* vanka.cpp:64-149 with three velocity blocks */
+int or_factor_patches3(const or_csr* k, const or_patches3* p, or_vanka3* f) {
+  memset(f, 0, sizeof *f);
+  const int np_ = p->npatch, n = k->nrows;
+  f->n = n;
+  f->pat.npatch = np_;
+  f->pat.pptr = XMALLOC(int, np_ + 1);
+  f->pat.pidx = XMALLOC(int, np_ > 0 ? np_ : 1);
+  f->pat.vptr = XMALLOC(int, np_ + 1);
+  f->pat.vidx = XMALLOC(int, p->vptr[np_] > 0 ? p->vptr[np_] : 1);
+  f->pat.cnt = XMALLOC(int, 3 * (size_t)(np_ > 0 ? np_ : 1));
+  memcpy(f->pat.pptr, p->pptr, sizeof(int) * (np_ + 1));
+  memcpy(f->pat.pidx, p->pidx, sizeof(int) * np_);
+  memcpy(f->pat.vptr, p->vptr, sizeof(int) * (np_ + 1));
+  memcpy(f->pat.vidx, p->vidx, sizeof(int) * p->vptr[np_]);
+  memcpy(f->pat.cnt, p->cnt, sizeof(int) * 3 * np_);
+  f->weights = XMALLOC(double, n);
+  for (int i = 0; i < np_; ++i) {
+    for (int q = p->vptr[i]; q < p->vptr[i + 1]; ++q) f->weights[p->vidx[q]] += 1.0;
+    for (int q = p->pptr[i]; q < p->pptr[i + 1]; ++q) f->weights[p->pidx[q]] += 1.0;
+  }
+  for (int d = 0; d < n; ++d)
+    if (f->weights[d] > 0.0) f->weights[d] = 1.0 / f->weights[d];
+  f->lu_off = XMALLOC(int64_t, np_ + 1);
+  f->piv_off = XMALLOC(int64_t, np_ + 1);
+  f->aux_off = XMALLOC(int64_t, np_ + 1);
+  f->s_off = XMALLOC(int64_t, np_ + 1);
+  int maxv = 1, maxp = 1;
+  for (int i = 0; i < np_; ++i) {
+    const int nv = p->vptr[i + 1] - p->vptr[i], npp = p->pptr[i + 1] - p->pptr[i];
+    int64_t sq = 0;
+    for (int c = 0; c < 3; ++c) sq += (int64_t)p->cnt[3 * i + c] * p->cnt[3 * i + c];
+    f->lu_off[i + 1] = f->lu_off[i] + sq;
+    f->piv_off[i + 1] = f->piv_off[i] + nv;
+    f->aux_off[i + 1] = f->aux_off[i] + (int64_t)nv * npp;
+    f->s_off[i + 1] = f->s_off[i] + (int64_t)npp * npp;
+    if (nv > maxv) maxv = nv;
+    if (npp > maxp) maxp = npp;
+  }
+  f->lu = XMALLOC(double, f->lu_off[np_] > 0 ? f->lu_off[np_] : 1);
+  f->piv = XMALLOC(int, f->piv_off[np_] > 0 ? f->piv_off[np_] : 1);
+  f->uhat = XMALLOC(double, f->aux_off[np_] > 0 ? f->aux_off[np_] : 1);
+  f->bhat = XMALLOC(double, f->aux_off[np_] > 0 ? f->aux_off[np_] : 1);
+  f->sinv = XMALLOC(double, f->s_off[np_] > 0 ? f->s_off[np_] : 1);
+  int* scatter = XMALLOC(int, n);
+  for (int d = 0; d < n; ++d) scatter[d] = -1;
+  double* b = XMALLOC(double, (size_t)maxp * maxv);
+  double* col = XMALLOC(double, maxv > maxp ? maxv : maxp);
+  double* s = XMALLOC(double, (size_t)maxp * maxp);
+  int* spiv = XMALLOC(int, maxp);
+  int rc = OR_OK;
+  for (int i = 0; i < np_ && rc == OR_OK; ++i) {
+    const int* vel = p->vidx + p->vptr[i];
+    const int* pres = p->pidx + p->pptr[i];
+    const int nv = p->vptr[i + 1] - p->vptr[i], npp = p->pptr[i + 1] - p->pptr[i];
+    const int* cnt = p->cnt + 3 * i;
+    double* lu[3];
+    int* piv[3];
+    int off[3] = {0, cnt[0], cnt[0] + cnt[1]};
+    lu[0] = f->lu + f->lu_off[i];
+    lu[1] = lu[0] + (size_t)cnt[0] * cnt[0];
+    lu[2] = lu[1] + (size_t)cnt[1] * cnt[1];
+    piv[0] = f->piv + f->piv_off[i];
+    piv[1] = piv[0] + cnt[0];
+    piv[2] = piv[1] + cnt[1];
+    for (int c = 0; c < 3 && rc == OR_OK; ++c) {
+      if (cnt[c] == 0) continue;
+      gather_dense(k, vel + off[c], cnt[c], vel + off[c], cnt[c], scatter, lu[c]);
+      if (or_lu_factor(cnt[c], lu[c], piv[c]) != OR_OK)
+        rc = fail(OR_SINGULAR_PATCH, "factor_patches3: singular velocity block");
+    }
+    if (rc != OR_OK) break;
+    gather_dense(k, pres, npp, vel, nv, scatter, b);
+    double* uhat = f->uhat + f->aux_off[i];
+    double* bhat = f->bhat + f->aux_off[i];
+    double* sinv = f->sinv + f->s_off[i];
+    for (int j = 0; j < npp; ++j)
+      for (int c = 0; c < 3; ++c) {
+        for (int q = 0; q < cnt[c]; ++q) col[q] = -b[(size_t)j * nv + off[c] + q];
+        if (cnt[c] > 0) or_lu_solve(cnt[c], lu[c], piv[c], col);
+        for (int q = 0; q < cnt[c]; ++q) uhat[(size_t)(off[c] + q) * npp + j] = col[q];
+      }
+    for (int a = 0; a < npp; ++a)
+      for (int c = 0; c < npp; ++c) {
+        double acc = 0.0;
+        for (int m = 0; m < nv; ++m) acc += b[(size_t)a * nv + m] * uhat[(size_t)m * npp + c];
+        s[a * npp + c] = acc;
+      }
+    if (or_lu_factor(npp, s, spiv) != OR_OK) {
+      rc = fail(OR_SINGULAR_PATCH, "factor_patches3: singular Schur block");
+      break;
+    }
+    for (int j = 0; j < npp; ++j) {
+      for (int q = 0; q < npp; ++q) col[q] = 0.0;
+      col[j] = 1.0;
+      or_lu_solve(npp, s, spiv, col);
+      for (int q = 0; q < npp; ++q) sinv[q * npp + j] = col[q];
+    }
+    for (int a = 0; a < npp; ++a)
+      for (int c = 0; c < nv; ++c) {
+        double acc = 0.0;
+        for (int m = 0; m < npp; ++m) acc += sinv[a * npp + m] * uhat[(size_t)c * npp + m];
+        bhat[(size_t)a * nv + c] = acc;
+      }
+  }
+  free(scatter);
+  free(b);
+  free(col);
+  free(s);
+  free(spiv);
+  if (rc != OR_OK) or_vanka3_free(f);
+  return rc;
+}
+
+void or_vanka3_free(or_vanka3* f) {
+  or_patches3_free(&f->pat);
+  free(f->lu_off);
+  free(f->piv_off);
+  free(f->aux_off);
+  free(f->s_off);
+  free(f->lu);
+  free(f->piv);
+  free(f->uhat);
+  free(f->bhat);
+  free(f->sinv);
+  free(f->weights);
+  memset(f, 0, sizeof *f);
+}
+
+/* vanka.cpp:151-184 with three blocks, patch order, delta += w x */
+void or_apply_vanka3(const or_vanka3* f, const double* r, double* delta) {
+  const or_patches3* p = &f->pat;
+  memset(delta, 0, sizeof(double) * (size_t)f->n);
+  int maxv = 1, maxp = 1;
+  for (int i = 0; i < p->npatch; ++i) {
+    if (p->vptr[i + 1] - p->vptr[i] > maxv) maxv = p->vptr[i + 1] - p->vptr[i];
+    if (p->pptr[i + 1] - p->pptr[i] > maxp) maxp = p->pptr[i + 1] - p->pptr[i];
+  }
+  double* bu = XMALLOC(double, maxv);
+  double* xu = XMALLOC(double, maxv);
+  double* bp = XMALLOC(double, maxp);
+  double* xp = XMALLOC(double, maxp);
+  for (int i = 0; i < p->npatch; ++i) {
+    const int* vel = p->vidx + p->vptr[i];
+    const int* pres = p->pidx + p->pptr[i];
+    const int nv = p->vptr[i + 1] - p->vptr[i], npp = p->pptr[i + 1] - p->pptr[i];
+    const int* cnt = p->cnt + 3 * i;
+    const double* lu = f->lu + f->lu_off[i];
+    const int* piv = f->piv + f->piv_off[i];
+    const double* uhat = f->uhat + f->aux_off[i];
+    const double* bhat = f->bhat + f->aux_off[i];
+    const double* sinv = f->sinv + f->s_off[i];
+    for (int q = 0; q < nv; ++q) bu[q] = r[vel[q]];
+    for (int q = 0; q < npp; ++q) bp[q] = r[pres[q]];
+    for (int q = 0; q < nv; ++q) xu[q] = bu[q];
+    int off = 0;
+    for (int c = 0; c < 3; ++c) {
+      if (cnt[c] > 0) or_lu_solve(cnt[c], lu, piv, xu + off);
+      lu += (size_t)cnt[c] * cnt[c];
+      piv += cnt[c];
+      off += cnt[c];
+    }
+    for (int a = 0; a < npp; ++a) {
+      double acc = 0.0;
+      for (int j = 0; j < npp; ++j) acc += sinv[a * npp + j] * bp[j];
+      for (int j = 0; j < nv; ++j) acc += bhat[(size_t)a * nv + j] * bu[j];
+      xp[a] = acc;
+    }
+    for (int q = 0; q < nv; ++q) {
+      double acc = xu[q];
+      for (int j = 0; j < npp; ++j) acc += uhat[(size_t)q * npp + j] * xp[j];
+      delta[vel[q]] += f->weights[vel[q]] * acc;
+    }
+    for (int a = 0; a < npp; ++a) delta[pres[a]] += f->weights[pres[a]] * xp[a];
+  }
+  free(bu);
+  free(xu);
+  free(bp);
+  free(xp);
+}
+
 /* ------------------------------------------------------------ krylov.cpp */
 
 /* krylov.cpp:17-121 -- right-preconditioned FGMRES, MGS + Givens */

@@ -80,6 +80,29 @@ void or_vanka_free(or_vanka* f);
 /* vanka.cpp:151-184 */
 void or_apply_vanka(const or_vanka* f, const double* r, double* delta);
 
+/* The 3-component generalisation (BASELINE config 5, which the reference does
+ * not support): K rows [x | y | z | p], one pressure seed per patch,
+ * the velocity set split into its x, y, z parts by the block sizes, one LU per
+ * component, then vanka.cpp:99-184 with three blocks instead of two. */
+typedef struct {
+  int npatch;
+  int *pptr, *pidx, *vptr, *vidx;
+  int* cnt; /* 3 per patch: x, y, z counts */
+} or_patches3;
+typedef struct {
+  or_patches3 pat;
+  int n;
+  int64_t *lu_off, *piv_off, *aux_off, *s_off;
+  double* lu; /* lu_x | lu_y | lu_z, row-major */
+  int* piv;
+  double *uhat, *bhat, *sinv, *weights;
+} or_vanka3;
+int or_build_patches3(const or_csr* k, int n_x, int n_y, int n_z, int n_p, or_patches3* out);
+void or_patches3_free(or_patches3* p);
+int or_factor_patches3(const or_csr* k, const or_patches3* p, or_vanka3* out);
+void or_vanka3_free(or_vanka3* f);
+void or_apply_vanka3(const or_vanka3* f, const double* r, double* delta);
+
 /* krylov.hpp:12, :17-35 */
 typedef void (*or_op)(void* ctx, const double* x, double* y);
 typedef struct {

@@ -210,6 +210,12 @@ SIGNATURES = {
     "sag_power_rho": (C.c_int, [vp, vp, vp, vp, C.c_int, f64p]),
     "sag_saddle_matrix": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "sag_evolution_soc": (C.c_int, [vp, vp, C.c_double, C.c_double, C.c_int, C.POINTER(vp)]),
+    # 3 velocity components (config 5)
+    "sag_factor_patches3": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(vp)]),
+    "sag_vanka3_destroy": (C.c_int, [vp]),
+    "sag_vanka3_stats": (C.c_int, [vp, i64p]),
+    "sag_apply_vanka3": (C.c_int, [vp, vp, vp, vp]),
     # FEM assembly (bitwise the reference's)
     "sag_from_triplets": (C.c_int, [vp, C.c_int, C.c_int, C.c_longlong, vp, vp, vp,
                                     C.POINTER(vp)]),
@@ -1109,5 +1115,35 @@ class DistSolver:
     def __del__(self):
         try:
             lib().sag_dist_destroy(self.h)
+        except Exception:
+            pass
+
+
+# ---------------------------------------------- 3 components (config 5) --
+class VankaFactorization3:
+    """factor_patches generalised to [x | y | z | p] (BASELINE config 5; the
+    reference is 2D only): one pressure seed per patch, one LU per velocity
+    component, CTA-per-patch kernels (sag_factor_patches3 / sag_apply_vanka3)."""
+
+    def __init__(self, k: SparseMatrix, n_x: int, n_y: int, n_z: int, n_p: int):
+        self.ctx, self.k = k.ctx, k
+        h = vp()
+        _check(lib().sag_factor_patches3(k.ctx.h, k.h, int(n_x), int(n_y), int(n_z), int(n_p),
+                                         C.byref(h)))
+        self.h = h
+        st = np.zeros(7, dtype=np.int64)
+        _check(lib().sag_vanka3_stats(h, st.ctypes.data_as(i64p)))
+        (self.npatch, self.n, self.device_bytes, self.max_nv, self.nslots, self.a_factor_bytes,
+         self.aux_bytes) = (int(v) for v in st)
+
+    def apply(self, r, out=None):
+        rp, rk = _vec_in(r, self.n)
+        dp, d = _vec_out(out, self.n, like=r)
+        _check(lib().sag_apply_vanka3(self.ctx.h, self.h, rp, dp))
+        return d
+
+    def __del__(self):
+        try:
+            lib().sag_vanka3_destroy(self.h)
         except Exception:
             pass

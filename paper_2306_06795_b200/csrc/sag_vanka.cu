@@ -1863,6 +1863,444 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
 }
 
 
+
+// ================================ 3 velocity components (BASELINE config 5) ==
+// The reference is 2D only; this is the 3-component
+// generalisation of factor_patches / apply_vanka (vanka.cpp:64-184 with x, y,
+// z blocks; oracle.c or_*3 is its CPU restatement). 3D Taylor-Hood patches
+// hold ~100-250 dofs (m up to ~60 per component), too large for a warp, so
+// both kernels run one CTA per patch.
+//
+// Blob per patch (16-byte aligned, int64 offset table, patch order):
+//   header {cnt_x, cnt_y, cnt_z, np, nv, slot_base, 0, 0}
+//   A_c^-1 (c = x, y, z), m_c x m_c column-major (the explicit inverse,
+//          columns = the LU solves of the unit vectors, sparse.cpp:343-361)
+//   U_hat (nv x np, [i np + a]) | B_hat (np x nv) | S^-1 (np x np)
+//   velocity dofs (nv) | pressure dofs (np)
+struct Vanka3 {
+  int n = 0, npatch = 0, max_nv = 0, max_m = 0, max_np = 0;
+  DevBuf<unsigned char> blob;
+  DevBuf<long long> off;
+  long long blob_bytes = 0, nslots = 0, a_factor_bytes = 0, aux_bytes = 0;
+  DevBuf<double> out;
+  DevBuf<int> dof_ptr, dof_slot;
+};
+
+__host__ __device__ inline long long v3_doubles(int mx, int my, int mz, int np) {
+  const long long nv = mx + my + mz;
+  return (long long)mx * mx + (long long)my * my + (long long)mz * mz + 2 * nv * np +
+         (long long)np * np;
+}
+
+// CTA per patch: A_c gathered into shared memory, LU with partial pivoting
+// (sparse.cpp:310-341: first max |a_ik|, whole-row swaps, multiplier
+// a_ik (1 / a_kk)), the inverse's columns by thread-per-column substitution,
+// then U_hat = -A^-1 B^T, S = B U_hat, S^-1, B_hat = S^-1 U_hat^T
+// (vanka.cpp:99-140, the symmetric-A b_hat formula)
+__global__ void __launch_bounds__(256) factor3_kernel(
+    int npatch, int n_u1, int n_u2, const int* __restrict__ rp, const int* __restrict__ ci,
+    const double* __restrict__ kv, const int* __restrict__ vptr, const int* __restrict__ vidx,
+    const int* __restrict__ pidx, const int* __restrict__ pptr, const long long* __restrict__ off,
+    unsigned char* blob, int MM, int* err) {
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int k = blockIdx.x; k < npatch; k += gridDim.x) {
+    const int v0 = vptr[k], nv = vptr[k + 1] - v0;
+    const int p0 = pptr[k], np = pptr[k + 1] - p0;
+    const int* vel = vidx + v0;
+    int cnt[3] = {0, 0, 0};
+    for (int i = 0; i < nv; ++i) cnt[vel[i] < n_u1 ? 0 : vel[i] < n_u2 ? 1 : 2]++;
+    unsigned char* B = blob + off[k];
+    int* hdr = reinterpret_cast<int*>(B);
+    double* D = reinterpret_cast<double*>(B + 32);
+    if (tid == 0) {
+      hdr[0] = cnt[0];
+      hdr[1] = cnt[1];
+      hdr[2] = cnt[2];
+      hdr[3] = np;
+      hdr[4] = nv;
+      hdr[6] = hdr[7] = 0;
+    }
+    const long long nA = (long long)cnt[0] * cnt[0] + (long long)cnt[1] * cnt[1] +
+                         (long long)cnt[2] * cnt[2];
+    double* gU = D + nA;
+    double* gB = gU + (long long)nv * np;
+    double* gS = gB + (long long)np * nv;
+    int* gI = reinterpret_cast<int*>(gS + np * np);
+    for (int i = tid; i < nv; i += nt) gI[i] = vel[i];
+    for (int a = tid; a < np; a += nt) gI[nv + a] = pidx[p0 + a];
+    // shared: A (MM x MM) | W (MM x MM) | Bm (np x nv) | piv (MM) | scratch
+    double* A = sm;
+    double* W = A + (size_t)MM * MM;
+    double* Bm = W + (size_t)MM * MM;
+    int* piv = reinterpret_cast<int*>(Bm + (size_t)4 * 512);  // Bm: np <= 4 rows of nv <= 511
+    __shared__ int s_p;
+    __shared__ int s_bad;
+    // B rows of the patch (np x nv), missing entries 0 (vanka.cpp:47-60)
+    for (int e = tid; e < np * nv; e += nt) Bm[e] = 0.0;
+    __syncthreads();
+    for (int a = 0; a < np; ++a) {
+      const int row = pidx[p0 + a];
+      for (int q = rp[row] + tid; q < rp[row + 1]; q += nt) {
+        const int pos = bsearch_idx(vel, nv, ci[q]);
+        if (pos >= 0) Bm[a * nv + pos] = kv[q];
+      }
+    }
+    __syncthreads();
+    int off_c = 0;
+    double* gA = D;
+    for (int c = 0; c < 3; ++c) {
+      const int m = cnt[c];
+      const int* vc = vel + off_c;
+      for (int e = tid; e < m * m; e += nt) A[e] = 0.0;
+      __syncthreads();
+      for (int r = tid; r < m; r += nt) {
+        const int row = vc[r];
+        for (int q = rp[row]; q < rp[row + 1]; ++q) {
+          const int pos = bsearch_idx(vc, m, ci[q]);
+          if (pos >= 0) A[r * m + pos] = kv[q];
+        }
+      }
+      for (int i = tid; i < m; i += nt) piv[i] = i;
+      if (tid == 0) s_bad = 0;
+      __syncthreads();
+      for (int kk = 0; kk < m; ++kk) {
+        if (tid == 0) {
+          int p = kk;
+          double best = fabs(A[kk * m + kk]);
+          for (int i = kk + 1; i < m; ++i) {
+            const double v = fabs(A[i * m + kk]);
+            if (v > best) {
+              best = v;
+              p = i;
+            }
+          }
+          if (best == 0.0) s_bad = 1;
+          s_p = p;
+          if (p != kk) {
+            const int t = piv[kk];
+            piv[kk] = piv[p];
+            piv[p] = t;
+          }
+        }
+        __syncthreads();
+        if (s_bad) break;
+        const int p = s_p;
+        if (p != kk)
+          for (int j = tid; j < m; j += nt) {
+            const double t = A[kk * m + j];
+            A[kk * m + j] = A[p * m + j];
+            A[p * m + j] = t;
+          }
+        __syncthreads();
+        const double inv_piv = 1.0 / A[kk * m + kk];
+        for (int i = kk + 1 + tid; i < m; i += nt) A[i * m + kk] *= inv_piv;
+        __syncthreads();
+        for (int e = tid; e < (m - kk - 1) * (m - kk - 1); e += nt) {
+          const int i = kk + 1 + e / (m - kk - 1), j = kk + 1 + e % (m - kk - 1);
+          const double mult = A[i * m + kk];
+          if (mult != 0.0) A[i * m + j] -= mult * A[kk * m + j];
+        }
+        __syncthreads();
+      }
+      if (s_bad) {
+        if (tid == 0) atomicMin(err, k);
+        break;
+      }
+      // inverse columns: thread j solves L U x = P e_j (sparse.cpp:343-361)
+      for (int j = tid; j < m; j += nt) {
+        double* x = W + (size_t)j * m;  // column j, contiguous
+        for (int i = 0; i < m; ++i) x[i] = piv[i] == j ? 1.0 : 0.0;
+        for (int i = 1; i < m; ++i) {
+          double acc = x[i];
+          for (int q = 0; q < i; ++q) acc -= A[i * m + q] * x[q];
+          x[i] = acc;
+        }
+        for (int i = m - 1; i >= 0; --i) {
+          double acc = x[i];
+          for (int q = i + 1; q < m; ++q) acc -= A[i * m + q] * x[q];
+          x[i] = acc / A[i * m + i];
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < m * m; e += nt) gA[e] = W[e];  // column-major
+      // U_hat rows of this component: u(i, a) = -sum_j W(i, j) B(a, off_c + j)
+      for (int e = tid; e < m * np; e += nt) {
+        const int i = e / np, a = e % np;
+        double acc = 0.0;
+        for (int j = 0; j < m; ++j) acc -= W[(size_t)j * m + i] * Bm[a * nv + off_c + j];
+        gU[(size_t)(off_c + i) * np + a] = acc;
+      }
+      __syncthreads();
+      gA += (long long)m * m;
+      off_c += m;
+    }
+    if (s_bad) continue;
+    __syncthreads();
+    // S = B U_hat (np x np), its inverse (np <= 4: one thread), B_hat
+    if (tid == 0) {
+      double S[16], L[16];
+      int pv[4];
+      for (int a = 0; a < np; ++a)
+        for (int b = 0; b < np; ++b) {
+          double acc = 0.0;
+          for (int q = 0; q < nv; ++q) acc += Bm[a * nv + q] * gU[(size_t)q * np + b];
+          S[a * np + b] = acc;
+        }
+      for (int i = 0; i < np * np; ++i) L[i] = S[i];
+      for (int i = 0; i < np; ++i) pv[i] = i;
+      bool ok = true;
+      for (int kk = 0; kk < np && ok; ++kk) {
+        int p = kk;
+        double best = fabs(L[kk * np + kk]);
+        for (int i = kk + 1; i < np; ++i)
+          if (fabs(L[i * np + kk]) > best) {
+            best = fabs(L[i * np + kk]);
+            p = i;
+          }
+        if (best == 0.0) {
+          ok = false;
+          break;
+        }
+        if (p != kk) {
+          for (int j = 0; j < np; ++j) {
+            const double t = L[kk * np + j];
+            L[kk * np + j] = L[p * np + j];
+            L[p * np + j] = t;
+          }
+          const int t = pv[kk];
+          pv[kk] = pv[p];
+          pv[p] = t;
+        }
+        const double ip = 1.0 / L[kk * np + kk];
+        for (int i = kk + 1; i < np; ++i) {
+          const double mult = L[i * np + kk] * ip;
+          L[i * np + kk] = mult;
+          for (int j = kk + 1; j < np; ++j) L[i * np + j] -= mult * L[kk * np + j];
+        }
+      }
+      if (!ok) {
+        atomicMin(err, k);
+      } else {
+        for (int j = 0; j < np; ++j) {
+          double x[4];
+          for (int i = 0; i < np; ++i) x[i] = pv[i] == j ? 1.0 : 0.0;
+          for (int i = 1; i < np; ++i)
+            for (int q = 0; q < i; ++q) x[i] -= L[i * np + q] * x[q];
+          for (int i = np - 1; i >= 0; --i) {
+            for (int q = i + 1; q < np; ++q) x[i] -= L[i * np + q] * x[q];
+            x[i] /= L[i * np + i];
+          }
+          for (int i = 0; i < np; ++i) gS[i * np + j] = x[i];
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < np * nv; e += nt) {
+      const int a = e / nv, c = e % nv;
+      double acc = 0.0;
+      for (int q = 0; q < np; ++q) acc += gS[a * np + q] * gU[(size_t)c * np + q];
+      gB[(size_t)a * nv + c] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// CTA per patch: b gathered to shared memory, t_c = A_c^-1 b_c (column-major
+// inverse, thread = row: coalesced), x_p = S^-1 b_p + B_hat b_u (block sum),
+// x_u = t + U_hat x_p, unweighted local results to the patch's slots
+// (vanka.cpp:154-181; the weighted, ordered scatter is the gather kernel).
+__global__ void __launch_bounds__(256) apply3_kernel(int npatch,
+                                                     const unsigned char* __restrict__ blob,
+                                                     const long long* __restrict__ off,
+                                                     const double* __restrict__ r,
+                                                     double* __restrict__ out) {
+  __shared__ double sb[512];
+  __shared__ double red[8][4];
+  __shared__ double xp[4];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  for (int k = blockIdx.x; k < npatch; k += gridDim.x) {
+    const unsigned char* B = blob + off[k];
+    const int4 h0 = *reinterpret_cast<const int4*>(B);
+    const int4 h1 = *reinterpret_cast<const int4*>(B + 16);
+    const int cnt[3] = {h0.x, h0.y, h0.z};
+    const int np = h0.w, nv = h1.x, sbase = h1.y;
+    const double* D = reinterpret_cast<const double*>(B + 32);
+    const long long nA = (long long)cnt[0] * cnt[0] + (long long)cnt[1] * cnt[1] +
+                         (long long)cnt[2] * cnt[2];
+    const double* U = D + nA;
+    const double* Bh = U + (long long)nv * np;
+    const double* Si = Bh + (long long)np * nv;
+    const int* idx = reinterpret_cast<const int*>(Si + np * np);
+    for (int i = tid; i < nv + np; i += nt) sb[i] = __ldg(r + idx[i]);
+    __syncthreads();
+    // x_p partial sums: b_hat . b_u
+    double part[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = tid; j < nv; j += nt)
+      for (int a = 0; a < np; ++a) part[a] = fma(Bh[(size_t)a * nv + j], sb[j], part[a]);
+    for (int a = 0; a < np; ++a) {
+      double v = part[a];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[wid][a] = v;
+    }
+    // t = A^-1 b_u, row i of component c
+    double t[2] = {0.0, 0.0};
+    int rowc[2] = {-1, -1}, rowi[2] = {0, 0};
+    {
+      int q = 0;
+      for (int i = tid; i < nv && q < 2; i += nt, ++q) {
+        int c = 0, base = 0;
+        while (i - base >= cnt[c]) base += cnt[c++];
+        rowc[q] = c;
+        rowi[q] = i;
+        const int m = cnt[c], li = i - base;
+        const double* Ac = D;
+        for (int cc = 0; cc < c; ++cc) Ac += (long long)cnt[cc] * cnt[cc];
+        double acc = 0.0;
+        for (int j = 0; j < m; ++j) acc = fma(Ac[(size_t)j * m + li], sb[base + j], acc);
+        t[q] = acc;
+      }
+    }
+    __syncthreads();
+    if (tid < np) {
+      double acc = 0.0;
+      for (int w = 0; w < (nt >> 5); ++w) acc += red[w][tid];
+      for (int j = 0; j < np; ++j) acc = fma(Si[tid * np + j], sb[nv + j], acc);
+      xp[tid] = acc;
+      out[sbase + nv + tid] = acc;
+    }
+    __syncthreads();
+    for (int q = 0; q < 2; ++q) {
+      if (rowc[q] < 0) continue;
+      const int i = rowi[q];
+      double acc = t[q];
+      for (int a = 0; a < np; ++a) acc = fma(U[(size_t)i * np + a], xp[a], acc);
+      out[sbase + i] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void slot_base3_kernel(int npatch, const long long* off, const int* sbase,
+                                  unsigned char* blob) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < npatch; k += gridDim.x * blockDim.x)
+    reinterpret_cast<int*>(blob + off[k])[5] = sbase[k];
+}
+
+std::unique_ptr<Vanka3> factor3_dev(Ctx& c, const Matrix& k, int n_x, int n_y, int n_z,
+                                    int n_p) {
+  const int n = k.nrows, n_u = n_x + n_y + n_z;
+  SAG_REQUIRE(n == n_u + n_p && k.ncols == n, SAG_DIMENSION_MISMATCH,
+              "factor_patches3: block sizes do not match K");
+  std::vector<int> rp(n + 1), ci(std::max<long long>(k.nnz, 1));
+  SAG_CUDA(cudaMemcpy(rp.data(), k.rp.p, 4 * (size_t)(n + 1), cudaMemcpyDeviceToHost));
+  if (k.nnz) SAG_CUDA(cudaMemcpy(ci.data(), k.ci.p, 4 * (size_t)k.nnz, cudaMemcpyDeviceToHost));
+  auto f = std::make_unique<Vanka3>();
+  f->n = n;
+  f->npatch = n_p;
+  // patches (vanka.cpp:11-42, one seed): the seed row's velocity columns
+  std::vector<int> vptr(n_p + 1, 0), vidx, pptr(n_p + 1), pidx(n_p);
+  std::vector<long long> offh(n_p + 1, 0);
+  std::vector<int> sbase(std::max(n_p, 1));
+  long long slots = 0;
+  for (int i = 0; i < n_p; ++i) {
+    const int row = n_u + i;
+    int cnt[3] = {0, 0, 0};
+    for (int q = rp[row]; q < rp[row + 1]; ++q)
+      if (ci[q] < n_u) {
+        vidx.push_back(ci[q]);
+        cnt[ci[q] < n_x ? 0 : ci[q] < n_x + n_y ? 1 : 2]++;
+      }
+    vptr[i + 1] = (int)vidx.size();
+    pptr[i] = i;
+    pidx[i] = row;
+    const int nv = vptr[i + 1] - vptr[i];
+    SAG_REQUIRE(nv > 0, SAG_SINGULAR_PATCH, "build_patches3: pressure row couples to no velocity DoFs");
+    f->max_nv = std::max(f->max_nv, nv);
+    f->max_m = std::max({f->max_m, cnt[0], cnt[1], cnt[2]});
+    long long bytes = 32 + 8 * v3_doubles(cnt[0], cnt[1], cnt[2], 1) + 4LL * (nv + 1);
+    bytes = (bytes + 15) / 16 * 16;
+    offh[i + 1] = offh[i] + bytes;
+    sbase[i] = (int)slots;
+    slots += nv + 1;
+    f->a_factor_bytes += 8LL * (cnt[0] * cnt[0] + cnt[1] * cnt[1] + cnt[2] * cnt[2]);
+    f->aux_bytes += 8LL * (2 * nv + 1);
+  }
+  pptr[n_p] = n_p;
+  f->max_np = 1;
+  SAG_REQUIRE(f->max_nv + f->max_np <= 512, SAG_DIMENSION_MISMATCH,
+              "factor_patches3: patch larger than 512 dofs");
+  SAG_REQUIRE(slots < (1LL << 31), SAG_DIMENSION_MISMATCH, "factor_patches3: too many slots");
+  f->blob_bytes = offh[n_p];
+  f->nslots = slots;
+  f->blob.alloc(std::max<long long>(offh[n_p], 16));
+  f->off.alloc(n_p + 1);
+  SAG_CUDA(cudaMemcpy(f->off.p, offh.data(), 8 * (size_t)(n_p + 1), cudaMemcpyHostToDevice));
+  DevBuf<int> dvptr(n_p + 1), dvidx(std::max<size_t>(vidx.size(), 1)), dpptr(n_p + 1),
+      dpidx(std::max(n_p, 1)), dsb(std::max(n_p, 1)), err(1);
+  SAG_CUDA(cudaMemcpy(dvptr.p, vptr.data(), 4 * (size_t)(n_p + 1), cudaMemcpyHostToDevice));
+  if (!vidx.empty())
+    SAG_CUDA(cudaMemcpy(dvidx.p, vidx.data(), 4 * vidx.size(), cudaMemcpyHostToDevice));
+  SAG_CUDA(cudaMemcpy(dpptr.p, pptr.data(), 4 * (size_t)(n_p + 1), cudaMemcpyHostToDevice));
+  if (n_p) {
+    SAG_CUDA(cudaMemcpy(dpidx.p, pidx.data(), 4 * (size_t)n_p, cudaMemcpyHostToDevice));
+    SAG_CUDA(cudaMemcpy(dsb.p, sbase.data(), 4 * (size_t)n_p, cudaMemcpyHostToDevice));
+  }
+  const int big = 0x7fffffff;
+  SAG_CUDA(cudaMemcpy(err.p, &big, sizeof(int), cudaMemcpyHostToDevice));
+  if (n_p > 0) {
+    const int MM = std::max(f->max_m, 1);
+    const size_t smem = (size_t)2 * MM * MM * 8 + 4 * 512 * 8 + 4 * MM + 16;
+    SAG_REQUIRE(smem <= 227 * 1024, SAG_DIMENSION_MISMATCH,
+                "factor_patches3: velocity block too large for shared memory");
+    SAG_CUDA(cudaFuncSetAttribute(factor3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    const int blocks = std::min(n_p, c.num_sms * 8);
+    factor3_kernel<<<blocks, 256, smem, c.stream>>>(n_p, n_x, n_x + n_y, k.rp.p, k.ci.p, k.v.p,
+                                                    dvptr.p, dvidx.p, dpidx.p, dpptr.p,
+                                                    f->off.p, f->blob.p, MM, err.p);
+    SAG_LAUNCHED(c);
+    slot_base3_kernel<<<grid_for(c, n_p), 256, 0, c.stream>>>(n_p, f->off.p, dsb.p, f->blob.p);
+    SAG_LAUNCHED(c);
+  }
+  int herr = big;
+  SAG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  SAG_REQUIRE(herr == big, SAG_SINGULAR_PATCH,
+              "factor_patches3: singular block in patch " + std::to_string(herr));
+  // dof -> slot map (slots in patch order: ascending patch order per dof)
+  std::vector<int> cnt(n + 1, 0), dslot(std::max<long long>(slots, 1));
+  for (int i = 0; i < n_p; ++i) {
+    for (int q = vptr[i]; q < vptr[i + 1]; ++q) ++cnt[vidx[q] + 1];
+    ++cnt[pidx[i] + 1];
+  }
+  for (int d = 0; d < n; ++d) cnt[d + 1] += cnt[d];
+  std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+  for (int i = 0; i < n_p; ++i) {
+    int sl = sbase[i];
+    for (int q = vptr[i]; q < vptr[i + 1]; ++q) dslot[pos[vidx[q]]++] = sl++;
+    dslot[pos[pidx[i]]++] = sl;
+  }
+  f->dof_ptr.alloc(n + 1);
+  f->dof_slot.alloc(std::max<long long>(slots, 1));
+  f->out.alloc(std::max<long long>(slots, 1));
+  SAG_CUDA(cudaMemcpy(f->dof_ptr.p, cnt.data(), 4 * (size_t)(n + 1), cudaMemcpyHostToDevice));
+  if (slots)
+    SAG_CUDA(cudaMemcpy(f->dof_slot.p, dslot.data(), 4 * (size_t)slots, cudaMemcpyHostToDevice));
+  return f;
+}
+
+void apply3_dev(Ctx& c, const Vanka3& f, const double* r, double* delta) {
+  if (f.npatch > 0) {
+    const int blocks = std::min(f.npatch, c.num_sms * 16);
+    apply3_kernel<<<blocks, 256, 0, c.stream>>>(f.npatch, f.blob.p, f.off.p, r, f.out.p);
+    SAG_LAUNCHED(c);
+  }
+  vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(
+      f.n, f.dof_ptr.p, f.dof_slot.p, f.out.p, nullptr, delta, nullptr, 1.0, nullptr);
+  SAG_LAUNCHED(c);
+}
+
 }  // namespace sag
 
 // =================================================================== C-ABI
@@ -2114,4 +2552,56 @@ int sag_apply_vanka_stage(sag_ctx* ctx, const sag_vanka* f, const double* r, dou
   });
 }
 
+
+struct sag_vanka3 {
+  sag::Vanka3 f;
+  sag::Ctx* c = nullptr;
+};
+
+int sag_factor_patches3(sag_ctx* ctx, const sag_matrix* k, int n_x, int n_y, int n_z, int n_p,
+                        sag_vanka3** out) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(k);
+    SAG_NOTNULL(out);
+    auto f = factor3_dev(ctx->c, k->m, n_x, n_y, n_z, n_p);
+    auto* h = new sag_vanka3;
+    h->f = std::move(*f);
+    h->c = &ctx->c;
+    *out = h;
+  });
+}
+
+int sag_vanka3_destroy(sag_vanka3* f) {
+  return guard([&] {
+    if (f && f->c) cudaStreamSynchronize(f->c->stream);
+    delete f;
+  });
+}
+
+int sag_vanka3_stats(const sag_vanka3* f, long long* s) {
+  return guard([&] {
+    SAG_NOTNULL(f);
+    SAG_NOTNULL(s);
+    s[0] = f->f.npatch;
+    s[1] = f->f.n;
+    s[2] = f->f.blob_bytes;
+    s[3] = f->f.max_nv;
+    s[4] = f->f.nslots;
+    s[5] = f->f.a_factor_bytes;
+    s[6] = f->f.aux_bytes;
+  });
+}
+
+int sag_apply_vanka3(sag_ctx* ctx, const sag_vanka3* f, const double* r, double* delta) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    auto& c = ctx->c;
+    InVec ri(c, r, f->f.n, 0);
+    OutVec d(c, delta, f->f.n, 1, false);
+    apply3_dev(c, f->f, ri.d, d.d);
+    d.finish();
+  });
+}
 }  // extern "C"
