@@ -2156,8 +2156,17 @@ __global__ void __launch_bounds__(256) apply3_kernel(int npatch,
         const int m = cnt[c], li = i - base;
         const double* Ac = D;
         for (int cc = 0; cc < c; ++cc) Ac += (long long)cnt[cc] * cnt[cc];
+        // eight independent column loads in flight per step (same fma order)
         double acc = 0.0;
-        for (int j = 0; j < m; ++j) acc = fma(Ac[(size_t)j * m + li], sb[base + j], acc);
+        int j = 0;
+        for (; j + 8 <= m; j += 8) {
+          double a[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[u] = __ldg(Ac + (size_t)(j + u) * m + li);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = fma(a[u], sb[base + j + u], acc);
+        }
+        for (; j < m; ++j) acc = fma(__ldg(Ac + (size_t)j * m + li), sb[base + j], acc);
         t[q] = acc;
       }
     }
