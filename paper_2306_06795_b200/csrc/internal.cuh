@@ -85,6 +85,7 @@ struct Vanka {
   // per-patch payload bases and shapes (host copies, for export)
   std::vector<long long> h_dbase, h_ibase;
   std::vector<int> h_nx, h_nv, h_np;
+  std::vector<unsigned char> h_nob;  // per patch: blob without b_hat (fixed-shape class)
 
 };
 

@@ -317,6 +317,7 @@ struct FactorOut {
   const long long* hoff = nullptr;
   const int* sbase = nullptr;
   int pairs = 0;  // paired blob layout for qualifying patches (vanka_paired)
+  const unsigned char* nob = nullptr;  // per patch: no stored b_hat (fixed-shape class)
 };
 
 __global__ void __launch_bounds__(256) factor_kernel(
@@ -402,11 +403,14 @@ __global__ void __launch_bounds__(256) factor_kernel(
       gUx = gAx + 2 * ainv_len(m, true);
       gUy = gUx + 1;
       gB = gUx + 2LL * np * m;
-      gS = gB + 2LL * np * m;
+      gS = gB + ((fo.nob && fo.nob[k]) ? 0 : 2LL * np * m);
       urx = ury = m;  // pair rows of U: [a * m + i]
       // zero padding of the smaller component
       if (nx != ny)
-        for (long long e = lane; e < vanka_paired_doubles(m, np) - (long long)np * np; e += 32)
+        for (long long e = lane;
+             e < vanka_paired_doubles(m, np) - (long long)np * np -
+                     ((fo.nob && fo.nob[k]) ? 2LL * np * m : 0);
+             e += 32)
           gAx[e] = 0.0;
       __syncwarp();
     } else {
@@ -480,6 +484,7 @@ __global__ void __launch_bounds__(256) factor_kernel(
       const int a = e / nv, j = e % nv;
       double acc = 0.0;
       for (int m = 0; m < np; ++m) acc = __dadd_rn(acc, __dmul_rn(Sinv[a * np + m], Um[j * NP + m]));
+      if (pr && fo.nob && fo.nob[k]) continue;
       if (pr)
         gB[2LL * a * (nx > ny ? nx : ny) + (j < nx ? 2 * j : 2 * (j - nx) + 1)] = acc;
       else
@@ -642,10 +647,15 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     f->aux_bytes += 8 * (2 * nv * npp + npp * npp);
     f->dense_inverse_bytes += 8 * (nv + npp) * (nv + npp);
   }
+  // nob[i]: the patch's blob stores no b_hat (the fixed-shape class recomputes
+  // it from S^-1 and U_hat, vanka.cpp:133-140, bitwise)
+  std::vector<unsigned char>& nob = f->h_nob;
+  nob.assign(np_, 0);
   auto ndbl = [&](int i) {
     const long long nv = f->h_nv[i], npp = f->h_np[i], x = f->h_nx[i], y = nv - x;
     if (vanka_paired(f->pairs, (int)x, (int)y, (int)npp))
-      return vanka_paired_doubles((int)std::max(x, y), (int)npp);
+      return vanka_paired_doubles((int)std::max(x, y), (int)npp) -
+             (nob[i] ? 2 * npp * std::max(x, y) : 0);
     return ainv_len(x, sym) + ainv_len(y, sym) + 2 * nv * npp + npp * npp;
   };
   f->h_dbase.assign(np_, 0);
@@ -694,7 +704,10 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
       return (k % 4 != 0 && nkey[std::min(k, 15)] < min_sub) ? 4 * (k / 4) : k;
     };
     std::vector<int> order(np_);
-    for (int i = 0; i < np_; ++i) order[i] = i;
+    for (int i = 0; i < np_; ++i) {
+      order[i] = i;
+      nob[i] = r_of(i) % 4 == 3 ? 1 : 0;
+    }
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return r_of(a) < r_of(b); });
     std::vector<long long> off(np_ + 1, 0);
     h_hoff.assign(np_, 0);
@@ -795,6 +808,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
     const int blocks = std::max(1, std::min((np_ + warps - 1) / warps, c.num_sms * 8));
     FactorOut fo;
     DevBuf<long long> dhoff;
+    DevBuf<unsigned char> dnob;
     fo.es = es;
     fo.dbase = ddbase.p;
     fo.ibase = dibase.p;
@@ -809,6 +823,11 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
                                  cudaMemcpyHostToDevice, c.stream));
       fo.hoff = dhoff.p;
       fo.pairs = f->pairs ? 1 : 0;
+      if (np_) {
+        dnob.alloc(np_);
+        SAG_CUDA(cudaMemcpyAsync(dnob.p, f->h_nob.data(), np_, cudaMemcpyHostToDevice, c.stream));
+        fo.nob = dnob.p;
+      }
     }
     factor_kernel<<<blocks, warps * 32, smem, c.stream>>>(
         np_, L.D, L.NV, L.NP, L.bytes, sym ? 1 : 0, k.rp.p, k.ci.p, k.v.p, p.pptr.p, p.pidx.p,
@@ -1372,7 +1391,7 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
   constexpr int L = M + NP, P = 32 / L, NV2 = 2 * M;
   constexpr int NBS = (2 * M + NP + 1) & ~1;  // per-patch b stride (16-byte aligned)
   constexpr int A2 = M * (M + 1) / 2;          // A pairs
-  constexpr int FD = 2 * A2 + 4 * NP * M + NP * NP;  // factor doubles after the header
+  constexpr int FD = 2 * A2 + 2 * NP * M + NP * NP;  // A | U pairs | S^-1 (no b_hat)
   extern __shared__ __align__(128) unsigned char smem[];
   const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane / L, gl = lane % L;
@@ -1390,15 +1409,25 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
   const int stride = gridDim.x * warps;
   const uint64_t policy = evict_first_policy();
   auto grp_end = [&](int q) { return q * P + P < npatch ? q * P + P : npatch; };
-  auto issue_at = [&](int s, int q) {
-    const long long o0 = off[q * P], o1 = off[grp_end(q)];
+  auto issue_bytes = [&](int s, long long o0, long long o1) {
     mbar_expect_tx(bars + s, (unsigned)(o1 - o0));
     bulk_copy_hint(ring + (size_t)s * stage_bytes, blob + o0, (unsigned)(o1 - o0), bars + s,
                    policy);
   };
-  // this lane's patch in stage s of group q (valid lanes only)
-  auto patch_at = [&](int s, int q) {
-    return ring + (size_t)s * stage_bytes + (size_t)(off[min(q * P + gg, npatch - 1)] - off[q * P]);
+  auto issue_at = [&](int s, int q) { issue_bytes(s, off[q * P], off[grp_end(q)]); };
+  // this lane's patch in stage s: the group's blobs are contiguous and a
+  // blob's size follows from its header (nx, ny), so the position is a walk
+  // over the earlier headers in shared memory -- no offset-table load on the
+  // critical path
+  auto patch_at = [&](int s) {
+    const unsigned char* B = ring + (size_t)s * stage_bytes;
+#pragma unroll
+    for (int h = 0; h < P - 1; ++h)
+      if (h < gg) {
+        const int2 hd = *reinterpret_cast<const int2*>(B);
+        B += ((16 + 8 * FD + 8 * (hd.x + hd.y + NP)) + 15) & ~15;
+      }
+    return B;
   };
   // this lane's r values: velocity lanes (x_gl, y_gl) zero past nx / ny,
   // pressure lanes p_(gl - M)
@@ -1435,7 +1464,7 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
     phase ^= 1u;
     const bool valid = g < P && first * P + g < npatch;
     double v0, v1;
-    load_r(patch_at(0, first), valid, v0, v1);
+    load_r(patch_at(0), valid, v0, v1);
     if (valid) store_r(sbuf + g * NBS, v0, v1);
   }
   __syncwarp();
@@ -1443,17 +1472,24 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
   // gl reads A(gl, j) -- column j's entry gl when gl <= j, else column gl's
   // entry j -- b_hat row a = gl - M reads its pair j (b_hat pairs follow U)
   const int a_row = gl - M;
-  const int own_col = gl < M ? gl * (gl + 1) / 2 : A2 + NP * M + a_row * M;
+  const int own_col = gl < M ? gl * (gl + 1) / 2 : 0;
   int stage = 0, it = 0;
   for (int q = first; q < ngroups; q += stride, ++it) {
     const int qr = q + nstage * stride;
     const int qn = q + stride;
+    // offsets of the group that refills this stage, loaded now so the
+    // refill at the end of the iteration does not wait on them
+    long long ro0 = 0, ro1 = 0;
+    if (lane == 0 && qr < ngroups) {
+      ro0 = __ldg(off + qr * P);
+      ro1 = __ldg(off + grp_end(qr));
+    }
     const bool valid = g < P && q * P + g < npatch;
-    const unsigned char* B = patch_at(stage, q);
+    const unsigned char* B = patch_at(stage);
     const int2 hdr = *reinterpret_cast<const int2*>(B);
     const double2* AP = reinterpret_cast<const double2*>(B + 16);
     const double* U = reinterpret_cast<const double*>(B + 16) + 2 * A2;
-    const double* Si = U + 4 * NP * M;
+    const double* Si = U + 2 * NP * M;
     const int* pos = reinterpret_cast<const int*>(Si + NP * NP) + hdr.x + hdr.y + NP;
     const double* sb = sbuf + ((it & 1) * P + gg) * NBS;
     const int sn = stage + 1 == nstage ? 0 : stage + 1;
@@ -1464,14 +1500,35 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
       mbar_wait(bars + sn, (phase >> sn) & 1u);
       phase ^= 1u << sn;
       nvalid = g < P && qn * P + g < npatch;
-      load_r(patch_at(sn, qn), nvalid, nv0, nv1);
+      load_r(patch_at(sn), nvalid, nv0, nv1);
     }
     const double2* SB = reinterpret_cast<const double2*>(sb);
+    // b_hat row a = gl - M recomputed from S^-1 and U_hat (vanka.cpp:133-140:
+    // b_hat(a, j) = sum_m S^-1(a, m) u_hat(j, m) from 0.0, the factor
+    // kernel's operations, so bitwise the value other classes store)
+    double2 bh[M];
+    if (gl >= M) {
+      const double2* UP = reinterpret_cast<const double2*>(U);
+      double srow[NP];
+#pragma unroll
+      for (int e = 0; e < NP; ++e) srow[e] = Si[a_row * NP + e];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        double bx = 0.0, by = 0.0;
+#pragma unroll
+        for (int e = 0; e < NP; ++e) {
+          const double2 u = UP[e * M + j];
+          bx = __dadd_rn(bx, __dmul_rn(srow[e], u.x));
+          by = __dadd_rn(by, __dmul_rn(srow[e], u.y));
+        }
+        bh[j] = make_double2(bx, by);
+      }
+    }
     double tx = 0.0, ty = 0.0;
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       const double2 b = SB[j];
-      const double2 a = AP[(gl < M && gl <= j) ? j * (j + 1) / 2 + gl : own_col + j];
+      const double2 a = gl < M ? AP[gl <= j ? j * (j + 1) / 2 + gl : own_col + j] : bh[j];
       tx = fma(a.x, b.x, tx);
       ty = fma(a.y, b.y, ty);
     }
@@ -1499,7 +1556,7 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
     __syncwarp();
     if (lane == 0 && qr < ngroups) {
       fence_proxy_async();
-      issue_at(stage, qr);
+      issue_bytes(stage, ro0, ro1);
     }
     stage = sn;
   }
@@ -1827,14 +1884,21 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
     long long urx, ury;
     if (vanka_paired(f.pairs, nx, ny, np)) {  // (A) | (U) | (B) pairs | S^-1
       const int m = std::max(nx, ny);
+      const bool nob = !f.h_nob.empty() && f.h_nob[k];
       const double* U2 = base + 2 * ainv_len(m, true);
       const double* B2 = U2 + 2LL * np * m;
-      const double* S2 = B2 + 2LL * np * m;
+      const double* S2 = B2 + (nob ? 0 : 2LL * np * m);
       for (int i = 0; i < nv; ++i)
         for (int a = 0; a < np; ++a) {
           const long long e = 2LL * a * m + (i < nx ? 2 * i : 2 * (i - nx) + 1);
           if (uhat) uhat[ou + (size_t)i * np + a] = U2[e];
-          if (bhat) bhat[ou + (size_t)a * nv + i] = B2[e];
+          if (bhat && !nob) bhat[ou + (size_t)a * nv + i] = B2[e];
+          if (bhat && nob) {  // b_hat = S^-1 u_hat^T (vanka.cpp:133-140), as the kernels do
+            double acc = 0.0;
+            for (int q = 0; q < np; ++q)
+              acc += S2[a * np + q] * U2[2LL * q * m + (i < nx ? 2 * i : 2 * (i - nx) + 1)];
+            bhat[ou + (size_t)a * nv + i] = acc;
+          }
         }
       if (sinv)
         for (int e = 0; e < np * np; ++e) sinv[os + e] = S2[e];
