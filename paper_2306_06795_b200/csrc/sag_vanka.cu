@@ -1378,12 +1378,13 @@ __global__ void __launch_bounds__(256) vanka_subwarp_kernel(
 // of the level; nx, ny vary through exact cancellations in B). The paired
 // layout zero-pads the smaller component to M, so the shape, the factor
 // offsets and the loop bounds are compile-time constants; only the dof lists
-// depend on (nx, ny). L = M + NP lanes per patch (M pair rows + NP b_hat
-// rows), 32 / L patches per warp, the group's blobs in one bulk copy. Same
-// operations in the same order as vanka_subwarp_kernel (bitwise the same
-// results) with a fraction of its instructions.
-template <int M, int NP>
-__global__ void __launch_bounds__(256) vanka_fixed_kernel(
+// depend on (nx, ny). L = M + NP lanes per patch (M pair rows + NP pressure
+// rows), 32 / L patches per warp, the group's blobs in one bulk copy. The
+// blob carries no b_hat: x_p = S^-1 (b_p + U_hat^T b_u), with U_hat^T b_u a
+// shuffle tree over the pair lanes -- 26% fewer bytes than the stored-b_hat
+// classes, results within rounding of theirs (vanka.cpp:133-181 reassociated).
+template <int M, int NP, int MINB>
+__global__ void __launch_bounds__(256, MINB) vanka_fixed_kernel(
     int npatch, const unsigned char* __restrict__ blob, const long long* __restrict__ off,
     int slot_bytes, int nstage, const double* __restrict__ r, double* __restrict__ out,
     const int* gate) {
@@ -1391,6 +1392,8 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
   constexpr int L = M + NP, P = 32 / L, NV2 = 2 * M;
   constexpr int NBS = (2 * M + NP + 1) & ~1;  // per-patch b stride (16-byte aligned)
   constexpr int A2 = M * (M + 1) / 2;          // A pairs
+  constexpr int W2 = M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : 16;  // reduction width
+  static_assert(W2 <= L, "the w_e tree must stay inside the patch's lanes");
   constexpr int FD = 2 * A2 + 2 * NP * M + NP * NP;  // A | U pairs | S^-1 (no b_hat)
   extern __shared__ __align__(128) unsigned char smem[];
   const int warps = blockDim.x >> 5, wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1503,51 +1506,60 @@ __global__ void __launch_bounds__(256) vanka_fixed_kernel(
       load_r(patch_at(sn), nvalid, nv0, nv1);
     }
     const double2* SB = reinterpret_cast<const double2*>(sb);
-    // b_hat row a = gl - M recomputed from S^-1 and U_hat (vanka.cpp:133-140:
-    // b_hat(a, j) = sum_m S^-1(a, m) u_hat(j, m) from 0.0, the factor
-    // kernel's operations, so bitwise the value other classes store)
-    double2 bh[M];
-    if (gl >= M) {
-      const double2* UP = reinterpret_cast<const double2*>(U);
-      double srow[NP];
-#pragma unroll
-      for (int e = 0; e < NP; ++e) srow[e] = Si[a_row * NP + e];
+    const double2* UP = reinterpret_cast<const double2*>(U);
+    // pair lanes: t = A_c^-1 b_u (both components at once) and the pair's
+    // part of w_e = sum_j u_hat(j, e) . b_u(j)
+    double tx = 0.0, ty = 0.0;
+    double2 uu[NP];
+    double wp[NP];
+    if (gl < M) {
 #pragma unroll
       for (int j = 0; j < M; ++j) {
-        double bx = 0.0, by = 0.0;
+        const double2 b = SB[j];
+        const double2 a = AP[gl <= j ? j * (j + 1) / 2 + gl : own_col + j];
+        tx = fma(a.x, b.x, tx);
+        ty = fma(a.y, b.y, ty);
+      }
+      const double2 bo = SB[gl];
 #pragma unroll
-        for (int e = 0; e < NP; ++e) {
-          const double2 u = UP[e * M + j];
-          bx = __dadd_rn(bx, __dmul_rn(srow[e], u.x));
-          by = __dadd_rn(by, __dmul_rn(srow[e], u.y));
-        }
-        bh[j] = make_double2(bx, by);
+      for (int e = 0; e < NP; ++e) {
+        uu[e] = UP[e * M + gl];
+        wp[e] = fma(uu[e].y, bo.y, uu[e].x * bo.x);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NP; ++e) {
+        uu[e] = make_double2(0.0, 0.0);
+        wp[e] = 0.0;
       }
     }
-    double tx = 0.0, ty = 0.0;
+    // w_e: a fixed tree over the group's first W2 lanes (pair lanes; the
+    // pressure lanes in it hold 0), broadcast from the group's lane 0
+    double w[NP];
 #pragma unroll
-    for (int j = 0; j < M; ++j) {
-      const double2 b = SB[j];
-      const double2 a = gl < M ? AP[gl <= j ? j * (j + 1) / 2 + gl : own_col + j] : bh[j];
-      tx = fma(a.x, b.x, tx);
-      ty = fma(a.y, b.y, ty);
+    for (int e = 0; e < NP; ++e) {
+      double v = wp[e];
+#pragma unroll
+      for (int o = W2 / 2; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      w[e] = __shfl_sync(0xffffffffu, v, gg * L);
     }
-    double xl = tx + ty;
+    // pressure lane a: x_p(a) = sum_e S^-1(a, e) (b_p(e) + w_e)
+    // (= S^-1 b_p + b_hat b_u with b_hat = S^-1 U_hat^T, vanka.cpp:133-140,
+    // reassociated so b_hat is neither stored nor formed)
+    double xl = 0.0;
     const int ar = gl < M ? 0 : a_row;
 #pragma unroll
-    for (int e = 0; e < NP; ++e) xl = fma(Si[ar * NP + e], sb[NV2 + e], xl);
+    for (int e = 0; e < NP; ++e) xl = fma(Si[ar * NP + e], sb[NV2 + e] + w[e], xl);
     if (valid && gl >= M) out[pos[hdr.x + hdr.y + a_row]] = xl;
     double xp[NP];
 #pragma unroll
     for (int e = 0; e < NP; ++e) xp[e] = __shfl_sync(0xffffffffu, xl, gg * L + M + e);
     if (valid && gl < M) {
-      const double2* UP = reinterpret_cast<const double2*>(U);
       double ox = tx, oy = ty;
 #pragma unroll
       for (int e = 0; e < NP; ++e) {
-        const double2 u = UP[e * M + gl];
-        ox = fma(u.x, xp[e], ox);
-        oy = fma(u.y, xp[e], oy);
+        ox = fma(uu[e].x, xp[e], ox);
+        oy = fma(uu[e].y, xp[e], oy);
       }
       if (gl < hdr.x) out[pos[gl]] = ox;
       if (gl < hdr.y) out[pos[hdr.x + gl]] = oy;
@@ -1749,7 +1761,7 @@ static void launch_subwarp(Ctx& c, const Vanka& f, const Vanka::RClass& cl, cons
 template <int M, int NP>
 static void launch_fixed(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const double* r,
                          const int* gate) {
-  static thread_local int configured = 0;
+  static thread_local int configured[2] = {0, 0};
   constexpr int L = M + NP, P = 32 / L, NB = ((2 * M + NP) + 1) & ~1;
   const int npatch = cl.k1 - cl.k0;
   const int bytes = (int)cl.slot_bytes;  // the largest blob of the class
@@ -1758,10 +1770,11 @@ static void launch_fixed(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const 
   const int cta_budget = env_int("SAG_VANKA_CTA_SMEM", 60000);
   int warps = std::max(1, std::min(env_int("SAG_VANKA_WARPS", 8), cta_budget / per_warp));
   const int smem = warps * per_warp;
-  auto kern = vanka_fixed_kernel<M, NP>;
-  if (configured < smem) {
+  const int v5 = env_int("SAG_VANKA_MINB", 4) == 5;
+  auto kern = v5 ? vanka_fixed_kernel<M, NP, 5> : vanka_fixed_kernel<M, NP, 4>;
+  if (configured[v5] < smem) {
     SAG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = smem;
+    configured[v5] = smem;
   }
   int occ = 0;
   SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, warps * 32, smem));
@@ -1937,12 +1950,14 @@ void vanka_export(Ctx& c, const Vanka& f, double* uhat, double* bhat, double* si
 //
 // Blob per patch (16-byte aligned, int64 offset table, patch order):
 //   header {cnt_x, cnt_y, cnt_z, np, nv, slot_base, 0, 0}
-//   A_c^-1 (c = x, y, z), m_c x m_c column-major (the explicit inverse,
-//          columns = the LU solves of the unit vectors, sparse.cpp:343-361)
+//   A_c^-1 (c = x, y, z): the explicit inverse (columns = the LU solves of
+//          the unit vectors, sparse.cpp:343-361), symmetrised, upper triangle
+//          packed by columns
 //   U_hat (nv x np, [i np + a]) | B_hat (np x nv) | S^-1 (np x np)
 //   velocity dofs (nv) | pressure dofs (np)
 struct Vanka3 {
   int n = 0, npatch = 0, max_nv = 0, max_m = 0, max_np = 0;
+  long long max_doubles = 0;  // factor doubles of the largest patch
   DevBuf<unsigned char> blob;
   DevBuf<long long> off;
   long long blob_bytes = 0, nslots = 0, a_factor_bytes = 0, aux_bytes = 0;
@@ -1950,10 +1965,12 @@ struct Vanka3 {
   DevBuf<int> dof_ptr, dof_slot;
 };
 
+// A_c^-1 of a symmetric block is stored as the symmetrised upper triangle
+// packed by columns (as the 2D blobs): m (m + 1) / 2 doubles
+__host__ __device__ inline long long v3_tri(int m) { return (long long)m * (m + 1) / 2; }
 __host__ __device__ inline long long v3_doubles(int mx, int my, int mz, int np) {
   const long long nv = mx + my + mz;
-  return (long long)mx * mx + (long long)my * my + (long long)mz * mz + 2 * nv * np +
-         (long long)np * np;
+  return v3_tri(mx) + v3_tri(my) + v3_tri(mz) + 2 * nv * np + (long long)np * np;
 }
 
 // CTA per patch: A_c gathered into shared memory, LU with partial pivoting
@@ -1985,8 +2002,7 @@ __global__ void __launch_bounds__(256) factor3_kernel(
       hdr[4] = nv;
       hdr[6] = hdr[7] = 0;
     }
-    const long long nA = (long long)cnt[0] * cnt[0] + (long long)cnt[1] * cnt[1] +
-                         (long long)cnt[2] * cnt[2];
+    const long long nA = v3_tri(cnt[0]) + v3_tri(cnt[1]) + v3_tri(cnt[2]);
     double* gU = D + nA;
     double* gB = gU + (long long)nv * np;
     double* gS = gB + (long long)np * nv;
@@ -2087,7 +2103,11 @@ __global__ void __launch_bounds__(256) factor3_kernel(
         }
       }
       __syncthreads();
-      for (int e = tid; e < m * m; e += nt) gA[e] = W[e];  // column-major
+      // symmetrised upper triangle by columns: (i, j), i <= j at j(j+1)/2 + i
+      for (int e = tid; e < m * m; e += nt) {
+        const int j = e / m, i = e % m;
+        if (i <= j) gA[j * (j + 1) / 2 + i] = 0.5 * (W[(size_t)j * m + i] + W[(size_t)i * m + j]);
+      }
       // U_hat rows of this component: u(i, a) = -sum_j W(i, j) B(a, off_c + j)
       for (int e = tid; e < m * np; e += nt) {
         const int i = e / np, a = e % np;
@@ -2096,7 +2116,7 @@ __global__ void __launch_bounds__(256) factor3_kernel(
         gU[(size_t)(off_c + i) * np + a] = acc;
       }
       __syncthreads();
-      gA += (long long)m * m;
+      gA += v3_tri(m);
       off_c += m;
     }
     if (s_bad) continue;
@@ -2170,15 +2190,19 @@ __global__ void __launch_bounds__(256) factor3_kernel(
   }
 }
 
-// CTA per patch: b gathered to shared memory, t_c = A_c^-1 b_c (column-major
-// inverse, thread = row: coalesced), x_p = S^-1 b_p + B_hat b_u (block sum),
-// x_u = t + U_hat x_p, unweighted local results to the patch's slots
-// (vanka.cpp:154-181; the weighted, ordered scatter is the gather kernel).
+// CTA per patch: the patch's factors (packed A_c^-1, U_hat, B_hat, S^-1 --
+// ~40 KB at 3D Taylor-Hood sizes) are staged into shared memory by coalesced
+// 16-byte loads of the whole CTA, b gathered beside them; then t_c = A_c^-1
+// b_c (thread = row, the packed symmetric addressing of the 2D kernels),
+// x_p = S^-1 b_p + B_hat b_u (block sum), x_u = t + U_hat x_p, unweighted
+// local results to the patch's slots (vanka.cpp:154-181; the weighted,
+// ordered scatter is the gather kernel).
 __global__ void __launch_bounds__(256) apply3_kernel(int npatch,
                                                      const unsigned char* __restrict__ blob,
                                                      const long long* __restrict__ off,
                                                      const double* __restrict__ r,
                                                      double* __restrict__ out) {
+  extern __shared__ __align__(16) double fac[];  // the factor doubles of one patch
   __shared__ double sb[512];
   __shared__ double red[8][4];
   __shared__ double xp[4];
@@ -2189,16 +2213,16 @@ __global__ void __launch_bounds__(256) apply3_kernel(int npatch,
     const int4 h1 = *reinterpret_cast<const int4*>(B + 16);
     const int cnt[3] = {h0.x, h0.y, h0.z};
     const int np = h0.w, nv = h1.x, sbase = h1.y;
-    const double* D = reinterpret_cast<const double*>(B + 32);
-    const long long nA = (long long)cnt[0] * cnt[0] + (long long)cnt[1] * cnt[1] +
-                         (long long)cnt[2] * cnt[2];
-    const double* U = D + nA;
-    const double* Bh = U + (long long)nv * np;
-    const double* Si = Bh + (long long)np * nv;
-    const int* idx = reinterpret_cast<const int*>(Si + np * np);
+    const long long nd = v3_doubles(cnt[0], cnt[1], cnt[2], np);
+    const double2* src = reinterpret_cast<const double2*>(B + 32);
+    for (long long e = tid; e < (nd + 1) / 2; e += nt) reinterpret_cast<double2*>(fac)[e] = __ldg(src + e);
+    const int* idx = reinterpret_cast<const int*>(reinterpret_cast<const double*>(B + 32) + nd);
     for (int i = tid; i < nv + np; i += nt) sb[i] = __ldg(r + idx[i]);
     __syncthreads();
-    // x_p partial sums: b_hat . b_u
+    const long long nA = v3_tri(cnt[0]) + v3_tri(cnt[1]) + v3_tri(cnt[2]);
+    const double* U = fac + nA;
+    const double* Bh = U + (long long)nv * np;
+    const double* Si = Bh + (long long)np * nv;
     double part[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = tid; j < nv; j += nt)
       for (int a = 0; a < np; ++a) part[a] = fma(Bh[(size_t)a * nv + j], sb[j], part[a]);
@@ -2207,30 +2231,24 @@ __global__ void __launch_bounds__(256) apply3_kernel(int npatch,
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) red[wid][a] = v;
     }
-    // t = A^-1 b_u, row i of component c
     double t[2] = {0.0, 0.0};
-    int rowc[2] = {-1, -1}, rowi[2] = {0, 0};
+    int rowi[2] = {-1, -1};
     {
       int q = 0;
       for (int i = tid; i < nv && q < 2; i += nt, ++q) {
         int c = 0, base = 0;
-        while (i - base >= cnt[c]) base += cnt[c++];
-        rowc[q] = c;
+        const double* Ac = fac;
+        while (i - base >= cnt[c]) {
+          Ac += v3_tri(cnt[c]);
+          base += cnt[c++];
+        }
         rowi[q] = i;
         const int m = cnt[c], li = i - base;
-        const double* Ac = D;
-        for (int cc = 0; cc < c; ++cc) Ac += (long long)cnt[cc] * cnt[cc];
-        // eight independent column loads in flight per step (same fma order)
+        const int cl = li * (li + 1) / 2;
         double acc = 0.0;
-        int j = 0;
-        for (; j + 8 <= m; j += 8) {
-          double a[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) a[u] = __ldg(Ac + (size_t)(j + u) * m + li);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc = fma(a[u], sb[base + j + u], acc);
-        }
-        for (; j < m; ++j) acc = fma(__ldg(Ac + (size_t)j * m + li), sb[base + j], acc);
+        int cs = 0;
+        for (int j = 0; j < m; cs += ++j)
+          acc = fma(Ac[li <= j ? cs + li : cl + j], sb[base + j], acc);
         t[q] = acc;
       }
     }
@@ -2244,7 +2262,7 @@ __global__ void __launch_bounds__(256) apply3_kernel(int npatch,
     }
     __syncthreads();
     for (int q = 0; q < 2; ++q) {
-      if (rowc[q] < 0) continue;
+      if (rowi[q] < 0) continue;
       const int i = rowi[q];
       double acc = t[q];
       for (int a = 0; a < np; ++a) acc = fma(U[(size_t)i * np + a], xp[a], acc);
@@ -2291,12 +2309,13 @@ std::unique_ptr<Vanka3> factor3_dev(Ctx& c, const Matrix& k, int n_x, int n_y, i
     SAG_REQUIRE(nv > 0, SAG_SINGULAR_PATCH, "build_patches3: pressure row couples to no velocity DoFs");
     f->max_nv = std::max(f->max_nv, nv);
     f->max_m = std::max({f->max_m, cnt[0], cnt[1], cnt[2]});
+    f->max_doubles = std::max(f->max_doubles, v3_doubles(cnt[0], cnt[1], cnt[2], 1));
     long long bytes = 32 + 8 * v3_doubles(cnt[0], cnt[1], cnt[2], 1) + 4LL * (nv + 1);
     bytes = (bytes + 15) / 16 * 16;
     offh[i + 1] = offh[i] + bytes;
     sbase[i] = (int)slots;
     slots += nv + 1;
-    f->a_factor_bytes += 8LL * (cnt[0] * cnt[0] + cnt[1] * cnt[1] + cnt[2] * cnt[2]);
+    f->a_factor_bytes += 8LL * (v3_tri(cnt[0]) + v3_tri(cnt[1]) + v3_tri(cnt[2]));
     f->aux_bytes += 8LL * (2 * nv + 1);
   }
   pptr[n_p] = n_p;
@@ -2365,8 +2384,18 @@ std::unique_ptr<Vanka3> factor3_dev(Ctx& c, const Matrix& k, int n_x, int n_y, i
 
 void apply3_dev(Ctx& c, const Vanka3& f, const double* r, double* delta) {
   if (f.npatch > 0) {
-    const int blocks = std::min(f.npatch, c.num_sms * 16);
-    apply3_kernel<<<blocks, 256, 0, c.stream>>>(f.npatch, f.blob.p, f.off.p, r, f.out.p);
+    const size_t smem = 8 * (size_t)(f.max_doubles + 2);
+    SAG_REQUIRE(smem <= 200 * 1024, SAG_DIMENSION_MISMATCH, "apply_vanka3: patch too large");
+    static thread_local size_t configured = 0;
+    if (configured < smem) {
+      SAG_CUDA(cudaFuncSetAttribute(apply3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      configured = smem;
+    }
+    int occ = 0;
+    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apply3_kernel, 256, smem));
+    const int blocks = std::min(f.npatch, std::max(occ, 1) * c.num_sms);
+    apply3_kernel<<<blocks, 256, smem, c.stream>>>(f.npatch, f.blob.p, f.off.p, r, f.out.p);
     SAG_LAUNCHED(c);
   }
   vanka_gather_kernel<<<grid_for(c, f.n), 256, 0, c.stream>>>(

@@ -285,9 +285,10 @@ def test_apply_vanka_sv_subwarp(S):
 
 def test_apply_vanka_sv_fixed_shape(S, monkeypatch):
     # the interior element triples (nx = ny = 6, np = 3) run on the
-    # fixed-shape kernel: same operations as the sub-warp kernel, so the sweep
-    # is bitwise the one with that class switched off, and within 1e-12 of
-    # the reference; the factor payload exports unchanged
+    # fixed-shape kernel: x_p = S^-1 (b_p + U_hat^T b_u) instead of the
+    # stored b_hat, so the sweep is within rounding (1e-14) of the one with
+    # that class switched off and within 1e-12 of the reference; the factor
+    # payload (b_hat rebuilt by the export) is bitwise the reference's
     c, d, k0, levels, _ = ref_case(32, sv=True, cfg=dict(omega0=0.78, eta_p=2.68))
     rv = O.RefVanka.build(O.RefMat.from_csr(k0), *d.nxyz0, sv_triples=True)
     K = S.SparseMatrix.from_csr(k0)
@@ -301,7 +302,7 @@ def test_apply_vanka_sv_fixed_shape(S, monkeypatch):
     monkeypatch.setenv("SAG_VANKA_FIXED", "0")
     f0 = S.factor_patches(K, p, d.nxyz0[0] + d.nxyz0[1])
     assert not any(k[0].startswith("vanka_fixed_kernel") for k in f0.classes())
-    assert np.array_equal(z, S.apply_vanka(f0, r))
+    assert rel_inf(z, S.apply_vanka(f0, r)) <= 1e-14
     got, want = f.export(p.export()), rv.factors()
     for key in ("uhat", "bhat", "sinv", "weights"):
         assert np.array_equal(got[key], want[key]), key
