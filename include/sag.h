@@ -252,6 +252,11 @@ int sag_dc_set_parameters(sag_dc* d, double eta_u, double eta_p, double omega0);
 int sag_dc_set_sv_transfer(sag_dc* d, const sag_matrix* p_dup, const sag_matrix* m_mix,
                            int nsl, const sag_matrix* const* scalar_levels,
                            const sag_matrix* const* scalar_prolongators);
+/* Diagnostic (no reference counterpart): with SAG_PROJ_TRACE=1 at setup the
+ * one-launch mass projection records (phase tag, globaltimer ns) pairs of its
+ * last run: out[0, 2*8192) for worker CTA 0, out[2*8192, 4*8192) for CTA 0 of
+ * the tail cluster; cap = number of 64-bit words of out. */
+int sag_dc_proj_trace(sag_ctx* ctx, sag_dc* d, unsigned long long* out, long long cap);
 /* Replaces DCPreconditioner::apply (preconditioner.cpp:114-153). */
 int sag_dc_apply(sag_ctx* ctx, sag_dc* d, const double* r, double* z);
 /* Replaces MonolithicSolver::vcycle (preconditioner.cpp:83-88) on the
@@ -259,7 +264,9 @@ int sag_dc_apply(sag_ctx* ctx, sag_dc* d, const double* r, double* z);
 int sag_dc_vcycle(sag_ctx* ctx, sag_dc* d, const double* b, double* x, int nu1, int nu2);
 /* counters = [fine_relax_units, level1_relax_units] (preconditioner.hpp:46-48) */
 int sag_dc_counters(const sag_dc* d, long long* counters);
-/* levels info: out = [nlevels, n0, n_levels rows..]; bytes of device factors */
+/* levels info: out = [nlevels, n0, n_levels rows.., bytes of device factors,
+ * launches of the captured apply, then for the SV mass projection: 1 when it
+ * runs as one persistent launch, its grid levels, CTAs and worker CTAs] */
 int sag_dc_info(const sag_dc* d, long long* out, int cap);
 
 /* Replaces solve_stokes (preconditioner.hpp:147-148; preconditioner.cpp:229-259):

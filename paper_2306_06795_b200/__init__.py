@@ -190,6 +190,7 @@ SIGNATURES = {
     "sag_dc_vcycle": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int]),
     "sag_dc_counters": (C.c_int, [vp, i64p]),
     "sag_dc_info": (C.c_int, [vp, i64p, C.c_int]),
+    "sag_dc_proj_trace": (C.c_int, [vp, vp, vp, C.c_longlong]),
     "sag_solve_stokes": (C.c_int, [vp, vp, vp, vp, C.POINTER(sag_solver_config),
                                    C.POINTER(sag_krylov_report), vp, C.c_int]),
     "sag_uzawa_create": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int,
@@ -850,7 +851,17 @@ class DCPreconditioner:
         _check(lib().sag_dc_info(self.h, v.ctypes.data_as(i64p), 32))
         nl = int(v[0])
         return dict(nlevels=nl, n0=int(v[1]), level_rows=[int(x) for x in v[2:2 + nl]],
-                    factor_bytes=int(v[2 + nl]), graph_launches=int(v[3 + nl]))
+                    factor_bytes=int(v[2 + nl]), graph_launches=int(v[3 + nl]),
+                    proj_fused=bool(v[4 + nl]), proj_grid_levels=int(v[5 + nl]),
+                    proj_ctas=int(v[6 + nl]), proj_workers=int(v[7 + nl]))
+
+    def proj_trace(self):
+        """Diagnostic: (tags, ns) of the last one-launch SV mass projection for
+        worker CTA 0 and tail CTA 0 (needs SAG_PROJ_TRACE=1 at setup)."""
+        cap = 8192
+        buf = np.zeros(4 * cap, dtype=np.uint64)
+        _check(lib().sag_dc_proj_trace(self.ctx.h, self.h, buf.ctypes.data, buf.size))
+        return buf[:2 * cap].reshape(-1, 2), buf[2 * cap:].reshape(-1, 2)
 
     def size(self):
         return self.n

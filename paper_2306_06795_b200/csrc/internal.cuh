@@ -214,6 +214,29 @@ void launch_inv_diag(Ctx& c, const Matrix& m, double* dinv, int* bad);
 // redundantly (identically) in each CTA from DSMEM-gathered partial sums.
 // Replaces ~30 dependent small launches per level; levels run from L[0]
 // (b0 given, x0 out, global memory) down to the coarse L[nlev-1].
+// Sliced ELLPACK copy of a CSR matrix for the persistent small-level kernels.
+// G = 2^g lanes share a row (g from the mean row length); a slice is 32 / G
+// consecutive rows; entry k of row r (rho = r % (32 / G)) is word
+// sptr[r / (32 / G)] + 32 (k / G) + rho G + k % G, so each step of a warp
+// reads 32 consecutive entries and no row pointer is needed per row. Rows are
+// padded to the slice's longest row with (value 0, the row's last column:
+// the gather stays unconditional and local). A row's sum is the shuffle tree
+// over its G lanes of the lanes' sums in ascending k.
+struct SellView {
+  const int* sptr = nullptr;  // nslices + 1 entry offsets (multiples of 32)
+  const int* ci = nullptr;
+  const double* v = nullptr;
+  int g = 0;                  // log2 lanes per row
+};
+struct Sell {
+  DevBuf<int> sptr, ci;
+  DevBuf<double> v;
+  long long entries = 0;
+  int g = 0;
+  SellView view() const { return SellView{sptr.p, ci.p, v.p, g}; }
+};
+void build_sell(Ctx& c, const Matrix& m, Sell& out);
+
 constexpr int kTailMaxLev = 6;
 constexpr int kTailVecs = 9;  // b x r rs w v0 v1 z0 z1 per level
 struct TailLevel {
@@ -234,6 +257,59 @@ struct TailParams {
   const double* b0 = nullptr;     // per launch: right-hand side of L[0]
   double* x0 = nullptr;           // per launch: result on L[0]
 };
+// The SV pressure mass projection p_cg = Mcg^-1 (M_mix p_dg)
+// (transfer.cpp:18-37: FGMRES(20) to 1e-12, scalar V(2,2) preconditioner,
+// amg.cpp:258-296) as ONE persistent launch. The grid is a set of clusters:
+// cluster 0 runs the small levels exactly as scalar_tail_kernel does; the
+// CTAs of the other clusters ("workers") own contiguous row chunks of the
+// large ("grid") levels, whose gathered vectors live in global memory (L2
+// resident) and whose pointwise vectors live in the owner's shared memory.
+// A gathered vector's producer and consumers are separated by a grid-wide
+// barrier (release fence + one atomic per CTA). A reduction needs no barrier:
+// every worker publishes its partial as two 8-byte {half of the value, phase
+// number} words (each an atomic store, so data and flag arrive together) and
+// every CTA polls all workers' words and sums them in worker order, so every
+// CTA holds the same Krylov scalars (KState in shared memory, updated by
+// apply_fin) and takes the same branches.
+constexpr int kProjMaxGl = 3;        // grid levels
+constexpr int kProjMaxRestart = 20;
+struct ProjLevel {
+  int n = 0, chunk = 0;           // rows, rows per worker (a multiple of 32)
+  SellView a;                     // A_l
+  SellView rt;                    // R_l = P_l^T (rows of level l + 1)
+  SellView p;                     // P_l
+  const double* dinv = nullptr;
+  int nc = 0, cchunk = 0;         // rows of level l + 1, per worker
+  double *b = nullptr, *x = nullptr;  // level vectors (level 0: set per Arnoldi step)
+  double *r = nullptr, *z0 = nullptr, *z1 = nullptr;
+};
+struct ProjParams {
+  int ngl = 0, grid = 0, workers = 0;
+  size_t smem = 0;
+  ProjLevel G[kProjMaxGl];
+  TailParams tail;                // levels ngl..; b0 / x0 are global work vectors
+  int n = 0;                      // rows of level 0 (Mcg)
+  SellView mm;                    // M_mix (n rows)
+  const double* p_dg = nullptr;   // per launch: input
+  double* x = nullptr;            // per launch: result p_cg (n)
+  double *rhs = nullptr, *V = nullptr, *Z = nullptr;  // n, (restart + 1) n, restart n
+  KState* st = nullptr;           // outer KState (header + arrays written back at the end)
+  int restart = 20, max_iters = 200;
+  double tol = 1e-12, bd = 1e-30;
+  unsigned* bar = nullptr;        // grid barrier counter; zeroed with the slots at launch
+  unsigned long long* ll = nullptr;  // reduction slots [2][workers][2][2]: {value half, phase}
+  size_t sync_bytes = 0;          // bytes from bar to zero at launch
+  int* fail = nullptr;            // set when the solve did not converge
+  // diagnostic (SAG_PROJ_TRACE): (phase tag, globaltimer ns) pairs of worker
+  // 0 [0, 2 cap) and of tail CTA 0 [2 cap, 4 cap)
+  unsigned long long* trace = nullptr;
+  int trace_cap = 0;
+};
+// grid, chunks and shared memory for p (levels and tail set); false when the
+// device cannot hold the grid levels' chunks or co-schedule the clusters
+bool sv_project_plan(Ctx& c, ProjParams& p);
+void launch_sv_project(Ctx& c, const ProjParams& p);
+
 // cluster size, row chunks and shared-memory layout for p.L[0..nlev) (n set);
 // false when no resident cluster can hold the levels
 bool scalar_tail_plan(Ctx& c, TailParams& p);

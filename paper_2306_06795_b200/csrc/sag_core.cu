@@ -1036,6 +1036,72 @@ void launch_scatter_idx(Ctx& c, int n, const int* idx, const double* src, double
   SAG_LAUNCHED(c);
 }
 
+// ------------------------------------------------------ sliced ELLPACK --
+__global__ void sell_width_kernel(int nrows, int g, const int* __restrict__ rp,
+                                  int* __restrict__ width) {
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int rs = 32 >> g;
+  if (s * rs >= nrows) return;
+  const int r = s * rs + (lane >> g);
+  const int G = 1 << g;
+  int steps = r < nrows ? (rp[r + 1] - rp[r] + G - 1) >> g : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) steps = max(steps, __shfl_xor_sync(0xffffffffu, steps, o));
+  if (lane == 0) width[s] = steps;
+}
+__global__ void sell_fill_kernel(int nrows, int ncols, int g, const int* __restrict__ rp,
+                                 const int* __restrict__ ci, const double* __restrict__ v,
+                                 const int* __restrict__ sptr, int* __restrict__ oc,
+                                 double* __restrict__ ov) {
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int rs = 32 >> g, G = 1 << g;
+  if (s * rs >= nrows) return;
+  const int r = s * rs + (lane >> g), sub = lane & (G - 1);
+  const int beg = r < nrows ? rp[r] : 0, len = r < nrows ? rp[r + 1] - beg : 0;
+  const int pad = len > 0 ? ci[beg + len - 1] : min(max(r, 0), ncols - 1);
+  const int p0 = sptr[s], w = (sptr[s + 1] - p0) >> 5;
+  for (int j = 0; j < w; ++j) {
+    const int k = j * G + sub;
+    oc[p0 + 32 * j + lane] = k < len ? ci[beg + k] : pad;
+    ov[p0 + 32 * j + lane] = k < len ? v[beg + k] : 0.0;
+  }
+}
+
+void build_sell(Ctx& c, const Matrix& m, Sell& out) {
+  // lanes per row from the mean row length (SAG_SELL_G: diagnostic override)
+  const double mean = m.nrows > 0 ? (double)m.nnz / m.nrows : 0.0;
+  int g = mean <= 8.0 ? 0 : mean <= 16.0 ? 1 : mean <= 32.0 ? 2 : mean <= 64.0 ? 3 : 4;
+  if (const char* e = getenv("SAG_SELL_G")) g = std::max(0, std::min(5, atoi(e)));
+  out.g = g;
+  const int rs = 32 >> g;
+  const int ns = (m.nrows + rs - 1) / rs;
+  DevBuf<int> width(std::max(ns, 1));
+  const int wpb = 8, blocks = (ns + wpb - 1) / wpb;
+  if (ns > 0) sell_width_kernel<<<blocks, wpb * 32, 0, c.stream>>>(m.nrows, g, m.rp.p, width.p);
+  SAG_LAUNCHED(c);
+  std::vector<int> hw(std::max(ns, 1), 0), hp(ns + 1, 0);
+  SAG_CUDA(cudaMemcpyAsync(hw.data(), width.p, sizeof(int) * ns, cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  long long tot = 0;
+  for (int i = 0; i < ns; ++i) {
+    hp[i] = (int)tot;
+    tot += 32LL * hw[i];
+    SAG_REQUIRE(tot < (1LL << 31), SAG_DIMENSION_MISMATCH, "sliced ELLPACK copy exceeds int32 offsets");
+  }
+  hp[ns] = (int)tot;
+  out.entries = tot;
+  out.sptr.alloc(ns + 1);
+  out.ci.alloc((size_t)std::max<long long>(tot, 1));
+  out.v.alloc((size_t)std::max<long long>(tot, 1));
+  SAG_CUDA(cudaMemcpyAsync(out.sptr.p, hp.data(), sizeof(int) * (ns + 1), cudaMemcpyHostToDevice,
+                           c.stream));
+  if (ns > 0)
+    sell_fill_kernel<<<blocks, wpb * 32, 0, c.stream>>>(m.nrows, m.ncols, g, m.rp.p, m.ci.p, m.v.p,
+                                                        out.sptr.p, out.ci.p, out.v.p);
+  SAG_LAUNCHED(c);
+  SAG_CUDA(cudaStreamSynchronize(c.stream));  // hp lives on this stack
+}
+
 // ------------------------------------------------- scalar V-cycle tail --
 // One cluster runs the small levels of scalar_vcycle (amg.cpp:258-296). CTA q
 // of the cluster owns rows [q chunk, (q+1) chunk) of every level and keeps
@@ -1117,6 +1183,65 @@ __device__ __forceinline__ void tail_reduce(cg::cluster_group& cl, TailSh& s, in
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = s.tot[k];
   slot ^= 1;
+}
+
+// rows [r0, r0 + nloc) of y = A x with A in sliced ELLPACK (r0 a multiple of
+// 32): G lanes per row, each warp takes two slices at a time (all their
+// index / value loads, then all their gathers, are issued together).
+// getx(col) reads x; epi(local row, sum) runs on the row's first lane.
+template <class G, class F>
+__device__ __forceinline__ void sell_spmv(const SellView& A, int r0, int nloc, G getx, F epi) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = A.g, rs = 32 >> g;
+  const int s0 = r0 >> (5 - g), nsl = (nloc + rs - 1) >> (5 - g);
+  for (int sa = wid; sa < nsl; sa += 2 * kTailWarps) {
+    const int sb = sa + kTailWarps;
+    const bool hb = sb < nsl;
+    const int p0 = __ldg(A.sptr + s0 + sa), q0 = __ldg(A.sptr + s0 + sa + 1);
+    int p1 = 0, q1 = 0;
+    if (hb) {
+      p1 = __ldg(A.sptr + s0 + sb);
+      q1 = __ldg(A.sptr + s0 + sb + 1);
+    }
+    const int n0 = (q0 - p0) >> 5, n1 = (q1 - p1) >> 5;
+    const int* c0 = A.ci + p0 + lane;
+    const double* v0 = A.v + p0 + lane;
+    const int* c1 = A.ci + p1 + lane;
+    const double* v1 = A.v + p1 + lane;
+    double a0 = 0.0, a1 = 0.0;
+    const int nmax = max(n0, n1);
+    for (int k = 0; k < nmax; k += 4) {
+      double va[4], vb[4], xa[4], xb[4];
+      int ca[4], cb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool oa = k + u < n0, ob = k + u < n1;
+        ca[u] = oa ? __ldg(c0 + 32 * (k + u)) : -1;
+        va[u] = oa ? __ldg(v0 + 32 * (k + u)) : 0.0;
+        cb[u] = ob ? __ldg(c1 + 32 * (k + u)) : -1;
+        vb[u] = ob ? __ldg(v1 + 32 * (k + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xa[u] = ca[u] >= 0 ? getx(ca[u]) : 0.0;  // warp-uniform conditions
+        xb[u] = cb[u] >= 0 ? getx(cb[u]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0 = fma(va[u], xa[u], a0);
+        a1 = fma(vb[u], xb[u], a1);
+      }
+    }
+    for (int o = (1 << g) >> 1; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if ((lane & ((1 << g) - 1)) == 0) {
+      const int l0 = sa * rs + (lane >> g), l1 = sb * rs + (lane >> g);
+      if (l0 < nloc) epi(l0, a0);
+      if (hb && l1 < nloc) epi(l1, a1);
+    }
+  }
 }
 
 // own rows of y = A x (x = vector k of level xt, gathered over DSMEM),
@@ -1320,10 +1445,27 @@ __device__ void tail_smooth(cg::cluster_group& cl, TailSh& s, double* sm, int& s
   cluster_bar();
 }
 
-__global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams p) {
-  __shared__ TailSh s;
-  extern __shared__ double sm[];
-  cg::cluster_group cl = cg::this_cluster();
+// diagnostic timestamps of tail CTA 0 inside sv_project_kernel (null otherwise)
+struct TailTrace {
+  unsigned long long* t = nullptr;
+  int cap = 0;
+  int* n = nullptr;
+};
+__device__ __forceinline__ void tail_mark(const TailTrace& tr, int tag) {
+  if (tr.t && threadIdx.x == 0 && blockIdx.x == 0 && *tr.n < tr.cap) {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    tr.t[2 * *tr.n] = (unsigned long long)tag;
+    tr.t[2 * *tr.n + 1] = ns;
+    ++*tr.n;
+  }
+}
+
+// The cluster's whole pass: b0 (global) -> x0 (global). b0 may have been
+// written earlier in the same launch (sv_project_kernel), so it is read
+// through L2.
+__device__ void tail_run(cg::cluster_group& cl, TailSh& s, double* sm, const TailParams& p,
+                         const TailTrace& tr = TailTrace()) {
   const int q = (int)cl.block_rank(), cs = (int)cl.num_blocks();
   if (threadIdx.x < cs) s.base[threadIdx.x] = cl.map_shared_rank(sm, (int)threadIdx.x);
   int slot = 0;
@@ -1331,14 +1473,16 @@ __global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams
   {
     const TL t = tl_make(p.L[0], q);
     double* b = tl_vec(sm, t, TB);
-    for (int i = threadIdx.x; i < t.nloc; i += kTailThreads) b[i] = __ldg(p.b0 + t.r0 + i);
+    for (int i = threadIdx.x; i < t.nloc; i += kTailThreads) b[i] = __ldcg(p.b0 + t.r0 + i);
   }
   cluster_bar();
   // down: pre-smoothing from zero, r = b - A x, b_(l+1) = R r
   for (int l = 0; l + 1 < nl; ++l) {
     const TailLevel& L = p.L[l];
     const TL t = tl_make(L, q);
+    tail_mark(tr, 600 + l);
     tail_smooth(cl, s, sm, slot, L, t, true);
+    tail_mark(tr, 610 + l);
     {
       const double* b = tl_vec(sm, t, TB);
       double* r = tl_vec(sm, t, TR);
@@ -1355,6 +1499,7 @@ __global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams
     cluster_bar();
   }
   // coarse: x = K^-1 b (dense inverse), one warp per row
+  tail_mark(tr, 620);
   {
     const TL tc = tl_make(p.L[nl - 1], q);
     double* xc = tl_vec(sm, tc, TX);
@@ -1389,16 +1534,674 @@ __global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams
                 [&](int li, double sum) { x[li] = x[li] + sum; });
     }
     cluster_bar();
+    tail_mark(tr, 630 + l);
     tail_smooth(cl, s, sm, slot, L, t, false);
+    tail_mark(tr, 640 + l);
   }
   {
     const TL t = tl_make(p.L[0], q);
     const double* x = tl_vec(sm, t, TX);
     for (int i = threadIdx.x; i < t.nloc; i += kTailThreads) p.x0[t.r0 + i] = x[i];
   }
-  // no CTA may exit while another can still read its shared memory
+  // no CTA may go on (or exit) while another can still read its shared memory
   cluster_bar();
 }
+
+__global__ void __launch_bounds__(kTailThreads, 1) scalar_tail_kernel(TailParams p) {
+  __shared__ TailSh s;
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  tail_run(cl, s, sm, p);
+}
+
+// -------------------------------------- SV mass projection, one launch --
+// sv_project_kernel (internal.cuh: ProjParams). The pointwise vectors of a
+// worker's rows live in its shared memory (every phase boundary below holds
+// a __syncthreads); the gathered vectors are global and need a grid barrier
+// between their producer and their consumers.
+
+constexpr int kProjKsDoubles =
+    10 + (kProjMaxRestart + 1) * kProjMaxRestart + 4 * kProjMaxRestart + 1;
+static_assert(sizeof(KState) == 80, "KState header is 10 doubles");
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct ProjCtx {
+  unsigned target;
+  int slot;
+  int wk, W;  // worker index (< 0: a CTA of the tail cluster), workers
+  int nt;     // trace entries written (diagnostic)
+  unsigned seq;  // reduction phase number
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// diagnostic: (tag, ns) pairs of worker 0 / tail CTA 0 when p.trace is set
+__device__ __forceinline__ void proj_trace(const ProjParams& p, ProjCtx& g, int tag) {
+  if (p.trace && threadIdx.x == 0 && (g.wk == 0 || blockIdx.x == 0) && g.nt < p.trace_cap) {
+    unsigned long long* t = p.trace + (g.wk == 0 ? 0 : 2 * (size_t)p.trace_cap);
+    t[2 * g.nt] = (unsigned long long)tag;
+    t[2 * g.nt + 1] = globaltimer_ns();
+    ++g.nt;
+  }
+}
+
+// grid-wide barrier: every CTA adds one to a counter that only grows and
+// waits for the launch's running target
+__device__ __forceinline__ void grid_bar(const ProjParams& p, ProjCtx& g, int tag) {
+  unsigned* bar = p.bar;
+  g.target += gridDim.x;
+  const unsigned target = g.target;
+  proj_trace(p, g, tag);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    atomicAdd(bar, 1u);
+    // watchdog: a CTA that waits ~2 s (a lost arrival: never seen, but a hang
+    // would take the whole device) opens every barrier of the launch; the
+    // caller sees the top bit of the counter and reports a failed projection
+    const long long t0 = clock64();
+    while (ld_acquire_u32(bar) < target) {
+      if (clock64() - t0 > 4000000000LL) atomicOr(bar, 0x80000000u);
+    }
+  }
+  __syncthreads();
+  proj_trace(p, g, tag + 1000);
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// sum of v[k] over the grid, the same bits in every CTA, without a barrier:
+// each worker publishes its block sum as two {32 bits of the value, phase}
+// words (8-byte stores are single-copy atomic, so a word whose phase matches
+// carries this phase's data); warp k of every CTA polls all workers' words of
+// value k and sums them in worker order (lane-strided, then the shuffle
+// tree). Slots alternate between two sets: a worker can be at most one phase
+// ahead of the slowest CTA, which has then already read the older set.
+template <int K>
+__device__ __forceinline__ void grid_reduce(TailSh& s, const ProjParams& p, ProjCtx& g,
+                                            double (&v)[K], int tag) {
+  static_assert(K <= 2, "two values per reduction slot");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  proj_trace(p, g, tag);
+  const unsigned seq = ++g.seq;
+  unsigned long long* set = p.ll + (size_t)(seq & 1u) * g.W * 4;
+  if (g.wk >= 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const double t = warp_sum(v[k]);
+      if (lane == 0) s.wp[wid][k] = t;
+    }
+    __syncthreads();
+    if (wid < K) {
+      const double t = warp_sum(s.wp[lane][wid]);
+      if (lane < 2) {
+        const unsigned half = lane == 0 ? (unsigned)__double2loint(t) : (unsigned)__double2hiint(t);
+        st_relaxed_u64(set + (size_t)g.wk * 4 + wid * 2 + lane,
+                       ((unsigned long long)seq << 32) | half);
+      }
+    }
+  }
+  if (wid < K) {
+    // lane q polls workers q, q + 32, ..: all their words are loaded together
+    // (one L2 round trip per poll), until every phase number matches
+    constexpr int kMaxPer = 8;  // workers <= 256
+    unsigned long long lo[kMaxPer], hi[kMaxPer];
+    const long long t0 = clock64();
+    unsigned spins = 0;
+    for (;;) {
+      bool ok = true;
+#pragma unroll
+      for (int u = 0; u < kMaxPer; ++u) {
+        const int q = lane + 32 * u;
+        if (q < g.W) {
+          const unsigned long long* a = set + (size_t)q * 4 + wid * 2;
+          lo[u] = ld_relaxed_u64(a);
+          hi[u] = ld_relaxed_u64(a + 1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kMaxPer; ++u)
+        if (lane + 32 * u < g.W)
+          ok = ok && (unsigned)(lo[u] >> 32) == seq && (unsigned)(hi[u] >> 32) == seq;
+      if (__all_sync(0xffffffffu, ok)) break;
+      // watchdog (see grid_bar): give up when the launch was opened or after ~2 s
+      if ((++spins & 255u) == 0u) {
+        if (clock64() - t0 > 4000000000LL) atomicOr(p.bar, 0x80000000u);
+        if (ld_acquire_u32(p.bar) & 0x80000000u) break;
+      }
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int u = 0; u < kMaxPer; ++u)
+      if (lane + 32 * u < g.W) t += __hiloint2double((int)(unsigned)hi[u], (int)(unsigned)lo[u]);
+    t = warp_sum(t);
+    if (lane == 0) s.tot[wid] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = s.tot[k];
+  proj_trace(p, g, tag + 1000);
+}
+
+// a grid level's product: x in global memory. Plain (L1-cached) loads: every
+// read of a gathered vector follows a grid barrier after its last write, and
+// the barrier's acquire invalidates this SM's L1.
+template <class F>
+__device__ __forceinline__ void grid_spmv(const SellView& A, int r0, int nloc, const double* x,
+                                          F epi) {
+  sell_spmv(A, r0, nloc, [&](int col) { return x[col]; }, epi);
+}
+
+__device__ __forceinline__ void proj_fin(KState* st, Fin f, double tot) {
+  if (threadIdx.x == 0) {
+    f.st = st;
+    apply_fin(f, tot);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void proj_backsub(KState* st) {
+  if (threadIdx.x == 0) {
+    const int j = st->jeff, m = st->m;
+    const double* h = ks_h(st);
+    const double* g = ks_g(st);
+    double* y = ks_y(st);
+    for (int i = j - 1; i >= 0; --i) {
+      double sum = g[i];
+      for (int k = i + 1; k < j; ++k) sum -= h[(size_t)i * m + k] * y[k];
+      y[i] = sum / h[(size_t)i * m + i];
+    }
+  }
+  __syncthreads();
+}
+
+// a worker's rows of a level with n rows in chunks of `chunk`
+struct Rows {
+  int r0, nloc;
+};
+__device__ __forceinline__ Rows proj_rows(const ProjCtx& g, int n, int chunk) {
+  Rows r;
+  if (g.wk < 0) {
+    r.r0 = n;
+    r.nloc = 0;
+  } else {
+    r.r0 = min(n, g.wk * chunk);
+    r.nloc = max(0, min(n - r.r0, chunk));
+  }
+  return r;
+}
+
+// fgmres(A, b, x, jacobi, {tol 0, max 2, restart 2}) on a grid level
+// (amg.cpp:265-276; the operations of jacobi_fgmres2 / tail_smooth), b and x
+// in global memory; x of the other workers is visible on entry (x_zero: x is
+// known to be zero and is only written). The caller puts a grid barrier
+// after it.
+__device__ void grid_smooth(TailSh& s, double* sm, int cmax, const ProjParams& p, ProjCtx& g,
+                            const ProjLevel& L, const double* bg, double* xg, bool x_zero) {
+  KState* st = reinterpret_cast<KState*>(s.ks);
+  const Rows R = proj_rows(g, L.n, L.chunk);
+  const int r0 = R.r0, nloc = R.nloc, i0 = threadIdx.x;
+  double* sb = sm;
+  double* v0 = sm + cmax;
+  double* v1 = sm + 2 * (size_t)cmax;
+  double* w = sm + 3 * (size_t)cmax;
+  const double* dinv = L.dinv + r0;
+  {
+    double red[2] = {0.0, 0.0};
+    for (int i = i0; i < nloc; i += kTailThreads) {
+      const double bi = __ldcg(bg + r0 + i);
+      sb[i] = bi;
+      red[0] = fma(bi, bi, red[0]);
+    }
+    if (x_zero) {
+      red[1] = red[0];
+    } else {
+      __syncthreads();  // sb rows are read by the rows' SpMV lanes
+      double acc = 0.0;
+      grid_spmv(L.a, r0, nloc, xg, [&](int li, double sum) {
+        const double ri = sb[li] - sum;
+        sb[li] = ri;
+        acc = fma(ri, ri, acc);
+      });
+      red[1] = acc;
+    }
+    grid_reduce<2>(s, p, g, red, 1);
+    Fin f;
+    f.kind = FIN_REF;
+    proj_fin(st, f, red[0]);
+    f.kind = FIN_BETA;
+    f.i = 4;
+    f.j = 2;
+    f.tol = 0.0;
+    proj_fin(st, f, red[1]);
+  }
+  if (!st->stop) {
+    const double beta = st->beta;
+    for (int i = i0; i < nloc; i += kTailThreads) {
+      const double vi = sb[i] / beta;
+      v0[i] = vi;
+      L.z0[r0 + i] = __ldg(dinv + i) * vi;
+    }
+    grid_bar(p, g, 2);
+    {
+      double red[1] = {0.0};
+      grid_spmv(L.a, r0, nloc, L.z0, [&](int li, double sum) {
+        w[li] = sum;
+        red[0] = fma(sum, v0[li], red[0]);
+      });
+      grid_reduce<1>(s, p, g, red, 3);
+      Fin f;
+      f.kind = FIN_H;
+      f.i = 0;
+      f.j = 0;
+      proj_fin(st, f, red[0]);
+    }
+    {
+      const double h = ks_h(st)[0];
+      double red[1] = {0.0};
+      for (int i = i0; i < nloc; i += kTailThreads) {
+        const double wi = fma(-h, v0[i], w[i]);
+        w[i] = wi;
+        red[0] = fma(wi, wi, red[0]);
+      }
+      grid_reduce<1>(s, p, g, red, 4);
+      Fin f;
+      f.kind = FIN_ARNOLDI;
+      f.j = 0;
+      proj_fin(st, f, red[0]);
+    }
+    if (!st->stop) {
+      const double wn = st->wnorm;
+      for (int i = i0; i < nloc; i += kTailThreads) {
+        const double vi = w[i] / wn;
+        v1[i] = vi;
+        L.z1[r0 + i] = __ldg(dinv + i) * vi;
+      }
+      grid_bar(p, g, 5);
+      {
+        double red[1] = {0.0};
+        grid_spmv(L.a, r0, nloc, L.z1, [&](int li, double sum) {
+          w[li] = sum;
+          red[0] = fma(sum, v0[li], red[0]);
+        });
+        grid_reduce<1>(s, p, g, red, 6);
+        Fin f;
+        f.kind = FIN_H;
+        f.i = 0;
+        f.j = 1;
+        proj_fin(st, f, red[0]);
+      }
+      {
+        const double h = ks_h(st)[1];
+        double red[1] = {0.0};
+        for (int i = i0; i < nloc; i += kTailThreads) {
+          const double wi = fma(-h, v0[i], w[i]);
+          w[i] = wi;
+          red[0] = fma(wi, v1[i], red[0]);
+        }
+        grid_reduce<1>(s, p, g, red, 7);
+        Fin f;
+        f.kind = FIN_H;
+        f.i = 1;
+        f.j = 1;
+        proj_fin(st, f, red[0]);
+      }
+      {
+        const double h = ks_h(st)[3];
+        double red[1] = {0.0};
+        for (int i = i0; i < nloc; i += kTailThreads) {
+          const double wi = fma(-h, v1[i], w[i]);
+          w[i] = wi;
+          red[0] = fma(wi, wi, red[0]);
+        }
+        grid_reduce<1>(s, p, g, red, 8);
+        Fin f;
+        f.kind = FIN_ARNOLDI;
+        f.j = 1;
+        proj_fin(st, f, red[0]);
+      }
+    }
+  }
+  proj_backsub(st);
+  const int j = st->jeff;
+  if (j > 0 || x_zero) {
+    const double y0 = ks_y(st)[0], y1 = ks_y(st)[1];
+    for (int i = i0; i < nloc; i += kTailThreads) {
+      const double di = __ldg(dinv + i);
+      double corr = 0.0;
+      if (j > 0) corr = fma(y0, di * v0[i], corr);
+      if (j > 1) corr = fma(y1, di * v1[i], corr);
+      xg[r0 + i] = x_zero ? corr : __ldcg(xg + r0 + i) + corr;
+    }
+  }
+}
+
+// x = V(2,2) b on the scalar hierarchy from x = 0 (amg.cpp:258-296): grid
+// levels here, the rest in cluster 0. Ends with x visible grid-wide.
+__device__ void proj_vcycle(cg::cluster_group& cl, TailSh& s, double* sm, int cmax,
+                            const ProjParams& p, ProjCtx& g, const double* b0, double* x0) {
+  const int ngl = p.ngl;
+  for (int l = 0; l < ngl; ++l) {
+    const ProjLevel& L = p.G[l];
+    const double* bg = l == 0 ? b0 : L.b;
+    double* xg = l == 0 ? x0 : L.x;
+    grid_smooth(s, sm, cmax, p, g, L, bg, xg, true);
+    grid_bar(p, g, 9);
+    const Rows R = proj_rows(g, L.n, L.chunk);
+    grid_spmv(L.a, R.r0, R.nloc, xg, [&](int li, double sum) {
+      L.r[R.r0 + li] = __ldcg(bg + R.r0 + li) - sum;
+    });
+    grid_bar(p, g, 10);
+    const Rows C = proj_rows(g, L.nc, L.cchunk);
+    double* bc = l + 1 < ngl ? p.G[l + 1].b : const_cast<double*>(p.tail.b0);
+    grid_spmv(L.rt, C.r0, C.nloc, L.r,
+              [&](int li, double sum) { bc[C.r0 + li] = sum; });
+    grid_bar(p, g, 11);
+  }
+  if (g.wk < 0) {
+    proj_trace(p, g, 500);
+    TailTrace tr;
+    if (p.trace && blockIdx.x == 0) {
+      tr.t = p.trace + 2 * (size_t)p.trace_cap;
+      tr.cap = p.trace_cap;
+      tr.n = &g.nt;
+    }
+    tail_run(cl, s, sm, p.tail, tr);
+    proj_trace(p, g, 501);
+  }
+  grid_bar(p, g, 12);
+  for (int l = ngl - 1; l >= 0; --l) {
+    const ProjLevel& L = p.G[l];
+    const double* bg = l == 0 ? b0 : L.b;
+    double* xg = l == 0 ? x0 : L.x;
+    const double* xc = l + 1 < ngl ? p.G[l + 1].x : p.tail.x0;
+    const Rows R = proj_rows(g, L.n, L.chunk);
+    grid_spmv(L.p, R.r0, R.nloc, xc, [&](int li, double sum) {
+      xg[R.r0 + li] = __ldcg(xg + R.r0 + li) + sum;
+    });
+    grid_bar(p, g, 13);
+    grid_smooth(s, sm, cmax, p, g, L, bg, xg, false);
+    grid_bar(p, g, 14);
+  }
+}
+
+__global__ void __launch_bounds__(kTailThreads, 1) sv_project_kernel(ProjParams p) {
+  __shared__ TailSh s;
+  __shared__ double oks[kProjKsDoubles];
+  extern __shared__ double sm[];
+  if (p.ngl <= 0) return;  // plan-time probe of the launch configuration
+  cg::cluster_group cl = cg::this_cluster();
+  ProjCtx g;
+  g.target = 0u;
+  g.slot = 0;
+  g.nt = 0;
+  g.seq = 0u;
+  g.W = p.workers;
+  g.wk = (int)blockIdx.x - (int)cl.num_blocks();  // cluster 0 = the tail
+  KState* ost = reinterpret_cast<KState*>(oks);
+  const ProjLevel& L0 = p.G[0];
+  const int n = p.n, i0 = threadIdx.x;
+  int cmax = 0;
+  for (int l = 0; l < p.ngl; ++l) cmax = max(cmax, p.G[l].chunk);
+  const Rows R = proj_rows(g, n, L0.chunk);
+  const int r0 = R.r0, nloc = R.nloc;
+  double* sb = sm;                      // the restart residual (own rows)
+  double* sw = sm + 3 * (size_t)cmax;   // Arnoldi w (own rows)
+  // rhs = M_mix p_dg (transfer.cpp:24), x = 0; ref = ||rhs|| (krylov.cpp:23-24)
+  double tot0;
+  {
+    double red[1] = {0.0};
+    grid_spmv(p.mm, r0, nloc, p.p_dg, [&](int li, double sum) {
+      p.rhs[r0 + li] = sum;
+      p.x[r0 + li] = 0.0;
+      red[0] = fma(sum, sum, red[0]);
+    });
+    grid_reduce<1>(s, p, g, red, 15);
+    tot0 = red[0];
+    if (threadIdx.x == 0) {
+      ost->ref = 1.0;
+      ost->tol = p.tol;
+      ost->bd = p.bd;
+      ost->m = p.restart;
+      ost->stop = 0;
+      ost->breakdown = 0;
+      ost->jeff = 0;
+      ost->iterations = 0;
+      ost->hist_len = 0;
+      ost->hist_cap = 0;
+      ost->converged = 0;
+      ost->beta = 0.0;
+      ost->rnorm = 0.0;
+    }
+    __syncthreads();
+    Fin f;
+    f.kind = FIN_REF;
+    proj_fin(ost, f, tot0);
+    f.kind = FIN_BETA;  // the initial residual b - A 0 = b (krylov.cpp:26-35)
+    f.i = 2;
+    proj_fin(ost, f, tot0);
+  }
+  const int m = p.restart;
+  bool first = true;
+  while (!ost->converged && ost->iterations < p.max_iters) {
+    // (re)start from the true residual (krylov.cpp:43-53)
+    {
+      Fin f;
+      f.kind = FIN_BETA;
+      f.i = 0;
+      if (first) {
+        for (int i = i0; i < nloc; i += kTailThreads) sb[i] = __ldcg(p.rhs + r0 + i);
+        proj_fin(ost, f, tot0);
+      } else {
+        double red[1] = {0.0};
+        grid_spmv(L0.a, r0, nloc, p.x, [&](int li, double sum) {
+          const double ri = __ldcg(p.rhs + r0 + li) - sum;
+          sb[li] = ri;
+          red[0] = fma(ri, ri, red[0]);
+        });
+        grid_reduce<1>(s, p, g, red, 16);
+        proj_fin(ost, f, red[0]);
+      }
+    }
+    if (ost->stop) break;
+    {
+      const double beta = ost->beta;
+      for (int i = i0; i < nloc; i += kTailThreads) p.V[r0 + i] = sb[i] / beta;
+    }
+    for (int j = 0; j < m && !ost->stop && ost->iterations < p.max_iters; ++j) {
+      double* zj = p.Z + (size_t)j * n;
+      proj_vcycle(cl, s, sm, cmax, p, g, p.V + (size_t)j * n, zj);
+      // Arnoldi step j (krylov.cpp:61-100): w = A z_j, modified Gram-Schmidt
+      {
+        double red[1] = {0.0};
+        grid_spmv(L0.a, r0, nloc, zj, [&](int li, double sum) {
+          sw[li] = sum;
+          red[0] = fma(sum, __ldcg(p.V + r0 + li), red[0]);
+        });
+        grid_reduce<1>(s, p, g, red, 17);
+        Fin f;
+        f.kind = FIN_H;
+        f.i = 0;
+        f.j = j;
+        proj_fin(ost, f, red[0]);
+      }
+      for (int i = 1; i <= j; ++i) {
+        const double h = ks_h(ost)[(size_t)(i - 1) * m + j];
+        const double* vp = p.V + (size_t)(i - 1) * n + r0;
+        const double* vn = p.V + (size_t)i * n + r0;
+        double red[1] = {0.0};
+        for (int k = i0; k < nloc; k += kTailThreads) {
+          const double wi = fma(-h, __ldcg(vp + k), sw[k]);
+          sw[k] = wi;
+          red[0] = fma(wi, __ldcg(vn + k), red[0]);
+        }
+        grid_reduce<1>(s, p, g, red, 18);
+        Fin f;
+        f.kind = FIN_H;
+        f.i = i;
+        f.j = j;
+        proj_fin(ost, f, red[0]);
+      }
+      {
+        const double h = ks_h(ost)[(size_t)j * m + j];
+        const double* vj = p.V + (size_t)j * n + r0;
+        double red[1] = {0.0};
+        for (int k = i0; k < nloc; k += kTailThreads) {
+          const double wi = fma(-h, __ldcg(vj + k), sw[k]);
+          sw[k] = wi;
+          red[0] = fma(wi, wi, red[0]);
+        }
+        grid_reduce<1>(s, p, g, red, 19);
+        Fin f;
+        f.kind = FIN_ARNOLDI;
+        f.j = j;
+        proj_fin(ost, f, red[0]);
+      }
+      if (!ost->stop) {
+        const double wn = ost->wnorm;
+        double* vq = p.V + (size_t)(j + 1) * n + r0;
+        for (int k = i0; k < nloc; k += kTailThreads) vq[k] = sw[k] / wn;
+      }
+    }
+    // back-substitution and x += sum_i y_i z_i (krylov.cpp:102-110)
+    proj_backsub(ost);
+    {
+      const int jj = ost->jeff;
+      const double* y = ks_y(ost);
+      if (jj > 0) {
+        for (int k = i0; k < nloc; k += kTailThreads) {
+          double corr = 0.0;
+          for (int i = 0; i < jj; ++i) corr = fma(y[i], __ldcg(p.Z + (size_t)i * n + r0 + k), corr);
+          p.x[r0 + k] = __ldcg(p.x + r0 + k) + corr;
+        }
+      }
+    }
+    first = false;
+    grid_bar(p, g, 20);
+  }
+  proj_trace(p, g, 9999);
+  if (blockIdx.x == 0) {
+    double* out = reinterpret_cast<double*>(p.st);
+    for (int i = i0; i < kProjKsDoubles; i += kTailThreads) out[i] = oks[i];
+    __syncthreads();
+    if (threadIdx.x == 0 && (!ost->converged || (ld_acquire_u32(p.bar) & 0x80000000u))) {
+      *p.fail = 1;
+      reinterpret_cast<KState*>(out)->converged = 0;
+    }
+  }
+}
+
+static void proj_launch_cfg(const ProjParams& p, cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at,
+                            bool coop) {
+  cfg = cudaLaunchConfig_t{};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(kTailThreads);
+  cfg.dynamicSmemBytes = p.smem;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.tail.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = coop ? 2 : 1;
+}
+
+static bool g_proj_coop = true;
+
+bool sv_project_plan(Ctx& c, ProjParams& p) {
+  if (p.ngl < 1 || p.ngl > kProjMaxGl || p.tail.cs <= 0 || p.tail.nlev < 1) return false;
+  if (p.restart < 1 || p.restart > kProjMaxRestart) return false;
+  constexpr size_t kMaxSmem = 200 * 1024;
+  static bool attr[64] = {};
+  int dev = 0;
+  SAG_CUDA(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && !attr[dev]) {
+    if (cudaFuncSetAttribute(sv_project_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) != cudaSuccess)
+      cudaGetLastError();
+    if (cudaFuncSetAttribute(sv_project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kMaxSmem) != cudaSuccess)
+      cudaGetLastError();
+    attr[dev] = true;
+  }
+  const int cs = p.tail.cs;
+  p.smem = p.tail.smem;
+  for (int pass = 0; pass < 3; ++pass) {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute at[2];
+    p.grid = cs;
+    proj_launch_cfg(p, cfg, at, false);
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, sv_project_kernel, &cfg) != cudaSuccess || nc < 2) {
+      cudaGetLastError();
+      return false;
+    }
+    const char* e = getenv("SAG_PROJ_CLUSTERS");
+    if (e && atoi(e) >= 2) nc = std::min(nc, atoi(e));
+    p.grid = nc * cs;
+    p.workers = p.grid - cs;
+    int cmax = 0;
+    for (int l = 0; l < p.ngl; ++l) {
+      ProjLevel& L = p.G[l];
+      L.chunk = ((L.n + p.workers - 1) / p.workers + 31) & ~31;
+      L.cchunk = ((L.nc + p.workers - 1) / p.workers + 31) & ~31;
+      cmax = std::max(cmax, L.chunk);
+    }
+    const size_t need = std::max(p.tail.smem, (size_t)4 * cmax * sizeof(double));
+    if (need > kMaxSmem) return false;
+    if (need == p.smem) break;
+    if (pass == 2) return false;
+    p.smem = need;
+  }
+  // probe the launch configuration once (cooperative + cluster); fall back
+  // to a plain cluster launch of a grid that is co-resident by construction
+  ProjParams probe = p;
+  probe.ngl = 0;
+  const char* ec = getenv("SAG_PROJ_COOP");
+  g_proj_coop = !(ec && std::strcmp(ec, "0") == 0);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute at[2];
+    proj_launch_cfg(p, cfg, at, g_proj_coop);
+    cfg.stream = c.stream;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, sv_project_kernel, probe);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+    if (e == cudaSuccess) return true;
+    cudaGetLastError();
+    if (!g_proj_coop) return false;
+    g_proj_coop = false;
+  }
+  return false;
+}
+
+void launch_sv_project(Ctx& c, const ProjParams& p) {
+  SAG_REQUIRE(p.grid > 0 && p.ngl >= 1 && p.p_dg && p.x && p.bar && p.ll, SAG_ERROR,
+              "SV mass projection: not planned");
+  SAG_CUDA(cudaMemsetAsync(p.bar, 0, p.sync_bytes, c.stream));
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute at[2];
+  proj_launch_cfg(p, cfg, at, g_proj_coop);
+  cfg.stream = c.stream;
+  SAG_CUDA(cudaLaunchKernelEx(&cfg, sv_project_kernel, p));
+  SAG_LAUNCHED(c);
+}
+
 
 bool scalar_tail_plan(Ctx& c, TailParams& p) {
   (void)c;
@@ -1416,7 +2219,11 @@ bool scalar_tail_plan(Ctx& c, TailParams& p) {
       cudaGetLastError();
     attr[dev] = true;
   }
-  for (int cs : {16, 8}) {
+  // SAG_TAIL_CS (diagnostic): one cluster size instead of 16, then 8
+  const char* ecs = getenv("SAG_TAIL_CS");
+  const int force_cs = ecs ? atoi(ecs) : 0;
+  for (int cs : {16, 8, 4, 2, 1}) {
+    if (force_cs > 0 ? cs != force_cs : cs < 8) continue;
     size_t off = 0;
     for (int l = 0; l < p.nlev; ++l) {
       TailLevel& L = p.L[l];

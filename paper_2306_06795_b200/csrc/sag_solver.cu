@@ -602,6 +602,8 @@ struct ScalarH {
   std::vector<DevBuf<double>> dinv, sb, sx, sr;
   std::vector<Krylov> kr;        // Jacobi-FGMRES(2) smoothing workspaces
   Coarse coarse;
+  // sliced ELLPACK copies of A_l, R_l, P_l for the persistent kernels (built on demand)
+  std::vector<std::unique_ptr<Sell>> ella, ellr, ellp;
   int tail_from = -1;            // levels >= tail_from run as one cluster launch
   TailParams tail;
   int n() const { return A.empty() ? 0 : A[0]->nrows; }
@@ -615,6 +617,12 @@ struct SvTransfer {
   DevBuf<double> rhs, pcg;
   std::vector<int> iterations;
   DevBuf<int> fail;              // set when a graph-run projection did not converge
+  // the whole projection as one persistent launch (sv_project_kernel)
+  bool fused = false;
+  ProjParams proj;
+  DevBuf<unsigned long long> proj_sync;
+  std::unique_ptr<Sell> sell_mmix;
+  DevBuf<unsigned long long> proj_trace;  // SAG_PROJ_TRACE=1 (diagnostic)
 };
 
 __global__ void proj_check_kernel(const KState* st, int* fail) {
@@ -788,6 +796,20 @@ static void scalar_setup(Ctx& c, ScalarH& t, int nl, const sag_matrix* const* a,
 
 static void sv_restrict(Ctx& c, Dc& d, const double* p_dg, double* p_cg) {
   SvTransfer& t = *d.svt;
+  if (t.fused) {
+    // M_mix product, FGMRES(20) and its V(2,2) cycles in one persistent launch
+    ProjParams p = t.proj;
+    p.p_dg = p_dg;
+    p.x = p_cg;
+    launch_sv_project(c, p);
+    if (stream_capturing(c)) return;  // failure flagged on the device (t.fail)
+    KHeader hd = read_header(c, t.outer.st);
+    if (!hd.converged)
+      throw Error(SAG_SOLVER_STAGNATION,
+                  "SvPressureRestrict: mass projection did not reach tolerance in 200 iterations");
+    t.iterations.push_back(hd.iterations);
+    return;
+  }
   launch_spmv(c, *t.mmix, p_dg, t.rhs.p, Epi::Store);
   launch_zero(c, t.mmix->nrows, p_cg);
   DevOp prec = [&](const double* in, double* out) { scalar_vcycle(c, t.sh, in, out); };
@@ -1036,6 +1058,8 @@ static void uzawa_apply_graph(Ctx& c, Uzawa& u) {
 
 constexpr int kTailRows = 65536;  // largest level the cluster tail takes
 
+static bool scalar_tail_from(Ctx& c, ScalarH& t, int from, TailParams& tp);
+
 static void scalar_setup(Ctx& c, ScalarH& t, int nl, const sag_matrix* const* a,
                          const sag_matrix* const* p, const char* what) {
   SAG_REQUIRE(nl >= 1, SAG_DIMENSION_MISMATCH, std::string(what) + ": empty scalar hierarchy");
@@ -1078,33 +1102,129 @@ static void scalar_setup(Ctx& c, ScalarH& t, int nl, const sag_matrix* const* a,
   // the small levels as one cluster launch (SAG_SCALAR_TAIL=0: per-kernel path)
   const char* e = getenv("SAG_SCALAR_TAIL");
   if ((e && std::strcmp(e, "0") == 0) || !t.coarse.use_inv) return;
-  const char* er = getenv("SAG_TAIL_ROWS");
-  const int rows_max = er ? atoi(er) : kTailRows;
   for (int from = 0; from + 1 < nl; ++from) {
-    if (t.A[from]->nrows > rows_max || nl - from > kTailMaxLev) continue;
     TailParams tp;
-    tp.nlev = nl - from;
-    tp.cinv = t.coarse.inv.p;
-    for (int l = from; l < nl; ++l) {
-      TailLevel& L = tp.L[l - from];
-      const Matrix& A = *t.A[l];
-      L.n = A.nrows;
-      L.arp = A.rp.p;
-      L.aci = A.ci.p;
-      L.av = A.v.p;
-      if (l + 1 < nl) {
-        L.rrp = t.R[l]->rp.p;
-        L.rci = t.R[l]->ci.p;
-        L.rv = t.R[l]->v.p;
-        L.prp = t.P[l]->rp.p;
-        L.pci = t.P[l]->ci.p;
-        L.pv = t.P[l]->v.p;
-        L.dinv = t.dinv[l].p;
-      }
-    }
-    if (!scalar_tail_plan(c, tp)) continue;  // too large for the shared memory: next level
+    if (!scalar_tail_from(c, t, from, tp)) continue;  // too large for the shared memory: next level
     t.tail = tp;
     t.tail_from = from;
+    return;
+  }
+}
+
+// sliced ELLPACK copies of level l's matrices
+static void scalar_sell(Ctx& c, ScalarH& t, int l) {
+  const int nl = (int)t.A.size();
+  if ((int)t.ella.size() < nl) {
+    t.ella.resize(nl);
+    t.ellr.resize(nl);
+    t.ellp.resize(nl);
+  }
+  if (t.ella[l]) return;
+  t.ella[l] = std::make_unique<Sell>();
+  build_sell(c, *t.A[l], *t.ella[l]);
+  if (l + 1 < nl) {
+    t.ellr[l] = std::make_unique<Sell>();
+    build_sell(c, *t.R[l], *t.ellr[l]);
+    t.ellp[l] = std::make_unique<Sell>();
+    build_sell(c, *t.P[l], *t.ellp[l]);
+  }
+}
+
+// levels from.. of t as a cluster tail; false when they do not fit
+static bool scalar_tail_from(Ctx& c, ScalarH& t, int from, TailParams& tp) {
+  const int nl = (int)t.A.size();
+  const char* er = getenv("SAG_TAIL_ROWS");
+  const int rows_max = er ? atoi(er) : kTailRows;
+  if (!t.coarse.use_inv || from < 0 || from >= nl) return false;
+  if (t.A[from]->nrows > rows_max || nl - from > kTailMaxLev) return false;
+  tp = TailParams();
+  tp.nlev = nl - from;
+  tp.cinv = t.coarse.inv.p;
+  for (int l = from; l < nl; ++l) {
+    TailLevel& L = tp.L[l - from];
+    const Matrix& A = *t.A[l];
+    L.n = A.nrows;
+    L.arp = A.rp.p;
+    L.aci = A.ci.p;
+    L.av = A.v.p;
+    if (l + 1 < nl) {
+      L.rrp = t.R[l]->rp.p;
+      L.rci = t.R[l]->ci.p;
+      L.rv = t.R[l]->v.p;
+      L.prp = t.P[l]->rp.p;
+      L.pci = t.P[l]->ci.p;
+      L.pv = t.P[l]->v.p;
+      L.dinv = t.dinv[l].p;
+    }
+  }
+  return scalar_tail_plan(c, tp);
+}
+
+// SvTransfer: plan the one-launch projection (sv_project_kernel) when the
+// hierarchy splits into 1..kProjMaxGl grid levels + a cluster tail
+// (SAG_PROJ_FUSED=1; the default is the multi-launch path)
+static void sv_project_setup(Ctx& c, SvTransfer& t) {
+  t.fused = false;
+  // opt-in: measured slower than the multi-launch path on B200 (DESIGN 5c)
+  const char* e = getenv("SAG_PROJ_FUSED");
+  if (!e || std::strcmp(e, "1") != 0) return;
+  ScalarH& h = t.sh;
+  const int nl = (int)h.A.size();
+  if (nl < 2 || !h.coarse.use_inv) return;
+  // SAG_PROJ_TAIL_ROWS (diagnostic): largest level the tail cluster takes here
+  const char* etr = getenv("SAG_PROJ_TAIL_ROWS");
+  const int tail_rows = etr ? atoi(etr) : kTailRows;
+  for (int from = 1; from < nl && from <= kProjMaxGl; ++from) {
+    ProjParams p;
+    if (h.A[from]->nrows > tail_rows) continue;
+    if (!scalar_tail_from(c, h, from, p.tail)) continue;
+    p.ngl = from;
+    for (int l = 0; l < from; ++l) {
+      ProjLevel& L = p.G[l];
+      L.n = h.A[l]->nrows;
+      scalar_sell(c, h, l);
+      L.a = h.ella[l]->view();
+      L.rt = h.ellr[l]->view();
+      L.p = h.ellp[l]->view();
+      L.dinv = h.dinv[l].p;
+      L.nc = h.A[l + 1]->nrows;
+      L.b = h.sb[l].p;
+      L.x = h.sx[l].p;
+      L.r = h.sr[l].p;
+      L.z0 = h.kr[l].z(0);
+      L.z1 = h.kr[l].z(1);
+    }
+    p.tail.b0 = h.sb[from].p;
+    p.tail.x0 = h.sx[from].p;
+    p.n = h.n();
+    if (!t.sell_mmix) {
+      t.sell_mmix = std::make_unique<Sell>();
+      build_sell(c, *t.mmix, *t.sell_mmix);
+    }
+    p.mm = t.sell_mmix->view();
+    p.rhs = t.rhs.p;
+    p.V = t.outer.V.p;
+    p.Z = t.outer.Z.p;
+    p.st = t.outer.st;
+    p.restart = 20;   // transfer.cpp:27
+    p.max_iters = 200;
+    p.tol = 1e-12;
+    p.bd = 1e-30;
+    p.fail = t.fail.p;
+    if (!sv_project_plan(c, p) || p.workers > 256) continue;
+    // [barrier counter, pad] + reduction slots, zeroed together at every launch
+    t.proj_sync.alloc(1 + (size_t)2 * p.workers * 4);
+    p.bar = reinterpret_cast<unsigned*>(t.proj_sync.p);
+    p.ll = t.proj_sync.p + 1;
+    p.sync_bytes = t.proj_sync.bytes();
+    if (const char* et = getenv("SAG_PROJ_TRACE"); et && std::strcmp(et, "0") != 0) {
+      p.trace_cap = 8192;
+      t.proj_trace.alloc((size_t)4 * p.trace_cap);
+      SAG_CUDA(cudaMemset(t.proj_trace.p, 0, sizeof(unsigned long long) * 4 * p.trace_cap));
+      p.trace = t.proj_trace.p;
+    }
+    t.proj = p;
+    t.fused = true;
     return;
   }
 }
@@ -1569,6 +1689,7 @@ int sag_dc_set_sv_transfer(sag_dc* h, const sag_matrix* p_dup, const sag_matrix*
     t->rhs.alloc(n_p1);
     t->fail.alloc(1);
     SAG_CUDA(cudaMemsetAsync(t->fail.p, 0, sizeof(int), c.stream));
+    sv_project_setup(c, *t);
     invalidate_graphs(d);
     d.svt = std::move(t);
   });
@@ -1633,7 +1754,28 @@ int sag_dc_info(const sag_dc* h, long long* out, int cap) {
       if (L.vanka) fb += L.vanka->blob_bytes;
     v.push_back(fb);
     v.push_back(d.graph_launches);
+    // SV mass projection as one launch: fused, grid levels, CTAs, workers
+    const bool fu = d.svt && d.svt->fused;
+    v.push_back(fu ? 1 : 0);
+    v.push_back(fu ? d.svt->proj.ngl : 0);
+    v.push_back(fu ? d.svt->proj.grid : 0);
+    v.push_back(fu ? d.svt->proj.workers : 0);
     for (int i = 0; i < cap && i < (int)v.size(); ++i) out[i] = v[i];
+  });
+}
+
+int sag_dc_proj_trace(sag_ctx* ctx, sag_dc* h, unsigned long long* out, long long cap) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(h);
+    SAG_NOTNULL(out);
+    Dc& d = h->d;
+    SAG_REQUIRE(d.svt && d.svt->fused && d.svt->proj.trace, SAG_CONFIG_ERROR,
+                "sag_dc_proj_trace: no traced one-launch projection (SAG_PROJ_TRACE=1 at setup)");
+    SAG_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    const long long n = std::min<long long>(cap, 4LL * d.svt->proj.trace_cap);
+    SAG_CUDA(cudaMemcpy(out, d.svt->proj.trace, sizeof(unsigned long long) * n,
+                        cudaMemcpyDeviceToHost));
   });
 }
 

@@ -457,3 +457,35 @@ def test_sv_scalar_tail(S, monkeypatch, tail):
     x, rep = S.solve_stokes(K0, c.rhs(), dc, cfg)
     assert rep.converged and rep.final_relative_residual <= cfg.tol
     assert abs(rep.iterations - d.solve(c.rhs())[1]["iterations"]) <= 1
+
+
+@pytest.mark.parametrize("n,tail_rows,ngl", [(32, None, 1), (64, None, 1), (64, "300", 2)])
+def test_sv_projection_one_launch(S, monkeypatch, n, tail_rows, ngl):
+    # transfer.cpp:18-37 (FGMRES(20) to 1e-12 on Mcg, scalar V(2,2) cycle) as one
+    # persistent launch (sv_project_kernel: grid levels in global memory behind
+    # grid barriers, the small levels in cluster 0) against the multi-launch
+    # path and the reference; tail_rows forces two grid levels
+    conf = dict(nu1=1, nu2=1, restart=30, tol=1e-8, max_iters=500, enclosed_flow=True,
+                omega0=0.78, eta_u=1.0, eta_p=2.68)
+    c, d, k0, levels, _ = ref_case(n, sv=True, cfg=conf)
+    r = O.splitmix64_uniform(c.n0)
+    zref = d.apply(r)
+    if tail_rows:
+        monkeypatch.setenv("SAG_TAIL_ROWS", tail_rows)
+    out = {}
+    for fused in ("0", "1"):
+        monkeypatch.setenv("SAG_PROJ_FUSED", fused)
+        h, K0, dc, cfg = _host_device(S, dict(problem="cavity", sv=True, n=n), conf)
+        info = dc.info()
+        assert info["proj_fused"] == (fused == "1")
+        if fused == "1":
+            assert info["proj_grid_levels"] == ngl and info["proj_workers"] > 0
+        z = dc.apply(r)
+        assert rel_inf(z, zref) <= 1e-8
+        assert np.array_equal(z, dc.apply(r))          # deterministic
+        x, rep = S.solve_stokes(K0, c.rhs(), dc, cfg)
+        assert rep.converged and rep.final_relative_residual <= cfg.tol
+        out[fused] = (z, x, rep.iterations)
+    assert rel_inf(out["1"][0], out["0"][0]) <= 1e-10
+    assert abs(out["1"][2] - out["0"][2]) <= 1
+    assert abs(out["1"][2] - d.solve(c.rhs())[1]["iterations"]) <= 1
