@@ -617,6 +617,11 @@ def run_ours(args, ws, rank, local):
         return dist_max((time.perf_counter() - te0) / ke, ws)
 
     t_e2e = e2e(lambda: S.vanka_spmv_step(f, K0, xh, dh, yh))
+    step_plan = S.vanka_step_plan(f)
+    # the same call with the stage pipeline off (x in, then compute + chunked copies out)
+    os.environ["SAG_STEP_STAGES"] = "1"
+    t_e2e1 = e2e(lambda: S.vanka_spmv_step(f, K0, xh, dh, yh))
+    del os.environ["SAG_STEP_STAGES"]
     t_e2e2 = e2e(lambda: (S.apply_vanka(f, xh, out=dh), S.spmv(K0, xh, out=yh)))
 
     peak, peak_kind = peak_hbm()
@@ -657,6 +662,8 @@ def run_ours(args, ws, rank, local):
         "e2e": {"value": ws * n / t_e2e / 1e9, "unit": "GDOF/s",
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 2 * 8 * n,
                 "call": "sag_vanka_spmv, pinned host buffers",
+                "pipeline": step_plan,
+                "unpipelined_value": ws * n / t_e2e1 / 1e9,
                 "two_calls_value": ws * n / t_e2e2 / 1e9,
                 "two_calls_note": "sag_apply_vanka + sag_spmv, x copied in twice"},
         "setup": {"host_reference_setup_s": host_setup_s, "gpu_patch_factor_s": factor_s},

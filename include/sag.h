@@ -158,6 +158,13 @@ int sag_apply_vanka_add_push(sag_ctx* ctx, const sag_vanka* f, const double* r, 
  * sag_spmv + sag_apply_vanka. */
 int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const double* x,
                    double* delta, double* y);
+/* Diagnostic (no reference counterpart): the plan of the last pipelined
+ * host-buffer step of f (sag_vanka_spmv with pinned host x, delta, y: x
+ * arrives in stages and every output range leaves as soon as its inputs
+ * arrived). out = [stages (0: not pipelined), ranges, host->device ranges,
+ * SpMV row ranges, gather ranges, patch windows]. SAG_STEP_STAGES sets the
+ * stage count (default 8; 1 disables the pipeline). */
+int sag_vanka_step_plan(const sag_vanka* f, long long* out, int cap);
 
 /* One stage of sag_apply_vanka, for per-kernel timing (device pointers):
  * stage 1 = patch kernel (local solves into the slot buffer),

@@ -191,6 +191,7 @@ SIGNATURES = {
     "sag_dc_counters": (C.c_int, [vp, i64p]),
     "sag_dc_info": (C.c_int, [vp, i64p, C.c_int]),
     "sag_dc_proj_trace": (C.c_int, [vp, vp, vp, C.c_longlong]),
+    "sag_vanka_step_plan": (C.c_int, [vp, i64p, C.c_int]),
     "sag_solve_stokes": (C.c_int, [vp, vp, vp, vp, C.POINTER(sag_solver_config),
                                    C.POINTER(sag_krylov_report), vp, C.c_int]),
     "sag_uzawa_create": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int,
@@ -665,6 +666,14 @@ def apply_vanka(f: VankaFactorization, r, out=None):
     dp, d = _vec_out(out, f.n, like=r)
     _check(lib().sag_apply_vanka(f.ctx.h, f.h, rp, dp))
     return d
+
+
+def vanka_step_plan(f: VankaFactorization):
+    """Plan of the last pipelined host-buffer step of f (sag_vanka_step_plan)."""
+    v = np.zeros(6, dtype=np.int64)
+    _check(lib().sag_vanka_step_plan(f.h, v.ctypes.data_as(i64p), 6))
+    return dict(stages=int(v[0]), ranges=int(v[1]), in_ranges=int(v[2]), row_ranges=int(v[3]),
+                gather_ranges=int(v[4]), patch_windows=int(v[5]))
 
 
 def vanka_spmv_step(f: VankaFactorization, k: SparseMatrix, x, delta=None, y=None):

@@ -86,6 +86,10 @@ struct Vanka {
   std::vector<long long> h_dbase, h_ibase;
   std::vector<int> h_nx, h_nv, h_np;
   std::vector<unsigned char> h_nob;  // per patch: blob without b_hat (fixed-shape class)
+  int n_u = 0;                       // velocity block size given to factor_patches
+  std::vector<int> h_order;          // blob position -> patch id
+  // pipelined host-buffer step (sag_vanka_spmv), planned per operator on first use
+  mutable std::shared_ptr<struct StepPlan> step_plan;
 
 };
 
@@ -214,6 +218,33 @@ void launch_inv_diag(Ctx& c, const Matrix& m, double* dinv, int* bad);
 // redundantly (identically) in each CTA from DSMEM-gathered partial sums.
 // Replaces ~30 dependent small launches per level; levels run from L[0]
 // (b0 given, x0 out, global memory) down to the coarse L[nlev-1].
+// A few row (or dof) ranges handled by one launch: virtual index v in
+// [vstart[k], vstart[k + 1]) is row row0[k] + v - vstart[k].
+constexpr int kMaxRowRanges = 12;
+struct RowRanges {
+  int n = 0;
+  int vstart[kMaxRowRanges + 1] = {0};
+  int row0[kMaxRowRanges] = {0};
+  __host__ __device__ int total() const { return vstart[n]; }
+  __device__ __forceinline__ int row(int v) const {
+    int k = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxRowRanges; ++i)
+      if (i < n && v >= vstart[i]) k = i;
+    return row0[k] + v - vstart[k];
+  }
+  bool push(int a, int b) {  // host: append rows [a, b); false when full
+    if (n >= kMaxRowRanges) return false;
+    row0[n] = a;
+    vstart[n + 1] = vstart[n] + (b - a);
+    ++n;
+    return true;
+  }
+};
+// y[rows] = (A x)[rows] for the rows of R, on stream st
+void launch_spmv_ranges(Ctx& c, const Matrix& m, const RowRanges& R, const double* x, double* y,
+                        cudaStream_t st);
+
 // Sliced ELLPACK copy of a CSR matrix for the persistent small-level kernels.
 // G = 2^g lanes share a row (g from the mean row length); a slice is 32 / G
 // consecutive rows; entry k of row r (rho = r % (32 / G)) is word

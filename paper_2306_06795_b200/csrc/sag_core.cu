@@ -284,6 +284,76 @@ void launch_spmv(Ctx& c, const Matrix& m, const double* x, double* y, Epi e, con
     default: spmv_dispatch_e<32>(c, m, x, y, e, a); break;
   }
 }
+// The Store product on a few row ranges in one launch (the pipelined
+// host-buffer step: one graph node per stage instead of one per range).
+template <int G>
+__global__ void __launch_bounds__(256, 8) spmv_ranges_kernel(RowRanges R, const int* __restrict__ rp,
+                                                          const int* __restrict__ ci,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y) {
+  constexpr int RPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (G - 1);
+  const int grp = lane / G;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int total = R.total();
+  for (int base = warp * RPW; base < total; base += nwarps * RPW) {
+    const int v = base + grp;
+    const bool ok = v < total;
+    const int row = ok ? R.row(v) : 0;
+    double s = 0.0;
+    if (ok) {
+      const int beg = __ldg(rp + row), end = __ldg(rp + row + 1);
+      for (int k0 = beg + sub; k0 < end; k0 += 4 * G) {
+        double vv[4], xv[4];
+        int cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * G;
+          const bool in = k < end;
+          vv[u] = in ? __ldcs(val + k) : 0.0;
+          cc[u] = in ? __ldcs(ci + k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) xv[u] = (k0 + u * G < end) ? __ldg(x + cc[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s = fma(vv[u], xv[u], s);
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+    if (ok && sub == 0) y[row] = s;
+  }
+}
+
+template <int G>
+static void spmv_ranges_g(Ctx& c, const Matrix& m, const RowRanges& R, const double* x, double* y,
+                          cudaStream_t st) {
+  static thread_local int occ = 0;
+  if (!occ) {
+    SAG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_ranges_kernel<G>, 256, 0));
+    occ = std::max(occ, 1);
+  }
+  const int rows_per_block = 256 / G;
+  const long long need = (R.total() + rows_per_block - 1) / rows_per_block;
+  const int grid = (int)std::max(1LL, std::min(need, (long long)occ * c.num_sms));
+  spmv_ranges_kernel<G><<<grid, 256, 0, st>>>(R, m.rp.p, m.ci.p, m.v.p, x, y);
+  SAG_LAUNCHED(c);
+}
+void launch_spmv_ranges(Ctx& c, const Matrix& m, const RowRanges& R, const double* x, double* y,
+                        cudaStream_t st) {
+  if (R.total() <= 0) return;
+  switch (m.group) {
+    case 2: spmv_ranges_g<2>(c, m, R, x, y, st); break;
+    case 4: spmv_ranges_g<4>(c, m, R, x, y, st); break;
+    case 8: spmv_ranges_g<8>(c, m, R, x, y, st); break;
+    case 16: spmv_ranges_g<16>(c, m, R, x, y, st); break;
+    default: spmv_ranges_g<32>(c, m, R, x, y, st); break;
+  }
+}
+
 void launch_spmv_rows(Ctx& c, const Matrix& m, int r0, int r1, const double* x, double* y) {
   if (r1 <= r0) return;
   const SpmvArgs a;

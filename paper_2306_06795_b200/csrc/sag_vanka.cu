@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
+#include <string>
 #include <vector>
 
 #include "internal.cuh"
@@ -620,6 +622,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
   auto f = std::make_unique<Vanka>();
   const int np_ = p.npatch;
   f->n = k.nrows;
+  f->n_u = std::min(std::max(n_u, 0), k.nrows);
   f->npatch = np_;
   f->max_dim = p.max_dim;
   f->max_nv = p.max_nv;
@@ -709,6 +712,7 @@ std::unique_ptr<Vanka> factor_patches_dev(Ctx& c, const Matrix& k, const Patches
       nob[i] = r_of(i) % 4 == 3 ? 1 : 0;
     }
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return r_of(a) < r_of(b); });
+    f->h_order = order;
     std::vector<long long> off(np_ + 1, 0);
     h_hoff.assign(np_, 0);
     int maxbytes = 16;
@@ -1876,6 +1880,552 @@ void vanka_gather_range(Ctx& c, const Vanka& f, int d0, int d1, double* delta) {
   SAG_LAUNCHED(c);
 }
 
+__global__ void vanka_gather_ranges_kernel(RowRanges R, const int* __restrict__ dof_ptr,
+                                           const double* __restrict__ out,
+                                           const double* __restrict__ w, double* __restrict__ delta);
+
+// ============================== pipelined host-buffer step (sag_vanka_spmv) ==
+// With pinned host buffers the step is bound by the host link: x in (8 n
+// bytes), delta and y out (16 n bytes). The two directions are independent
+// DMA engines, so x arrives in S stages and every output range leaves as soon
+// as the inputs it depends on have arrived: the device->host stream runs
+// under the rest of the host->device stream instead of after it.
+//
+// The plan is derived from the operator and the patches alone, correct for
+// any numbering: every input dof gets an arrival stage (the mesh strip of the
+// lowest pressure dof it couples to; pressure dofs by index), grouped into
+// contiguous ranges by taking the latest stage over blocks of 1024 dofs;
+// from the arrival stages: a row of K is ready when all its columns arrived,
+// a patch when all its dofs arrived, a dof of delta when all its patches ran;
+// each again rounded up to the latest stage over a block, which yields a few
+// contiguous ranges per stage for a strip-ordered numbering and degenerates to
+// "everything in the last stage" (the unpipelined step) for a hostile one.
+
+struct StepRange {
+  int a, b;
+};
+struct StepPlan {
+  const Matrix* k = nullptr;
+  int S = 0, want_S = 0, growth = 0;
+  std::vector<std::vector<StepRange>> in, rows, gat;  // per stage
+  std::vector<std::vector<Vanka::RClass>> pat;         // per stage: class windows
+  std::vector<cudaEvent_t> ev;                         // 3 S events
+  std::vector<std::vector<RowRanges>> rows_rr, gat_rr;  // the same ranges, <= 12 per launch
+  cudaStream_t sin = nullptr, sout = nullptr, ssp = nullptr;
+  long long ranges = 0;
+  // the whole step captured once per buffer set (the CPU cannot enqueue
+  // ~20 operations per stage as fast as the device retires them)
+  cudaGraphExec_t exec = nullptr;
+  long long graph_launches = 0;
+  DevBuf<unsigned long long> ktrace;  // SAG_STEP_TRACE=2: [3 S][start, end] of the copy kernels
+  const void* gkey[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  ~StepPlan() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    if (sin) cudaStreamDestroy(sin);
+    if (sout) cudaStreamDestroy(sout);
+    if (ssp) cudaStreamDestroy(ssp);
+  }
+};
+
+__global__ void step_minp_kernel(int n_u, const int* __restrict__ rp, const int* __restrict__ ci,
+                                 int* __restrict__ minp) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n_u; r += gridDim.x * blockDim.x) {
+    int m = 0x7fffffff;
+    for (int k = rp[r]; k < rp[r + 1]; ++k) {
+      const int c = ci[k];
+      if (c >= n_u) m = min(m, c);
+    }
+    minp[r] = m;
+  }
+}
+__global__ void step_rowq_kernel(int n, const int* __restrict__ rp, const int* __restrict__ ci,
+                                 const int* __restrict__ arr, int* __restrict__ q) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    int m = 0;
+    for (int k = rp[r]; k < rp[r + 1]; ++k) m = max(m, arr[ci[k]]);
+    q[r] = m;
+  }
+}
+// patch of slot t: slots are numbered patch by patch (sbase = prefix sums)
+__device__ __forceinline__ int step_slot_patch(const int* __restrict__ sbase, int np, int t) {
+  int lo = 0, hi = np;  // largest i with sbase[i] <= t
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (sbase[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+__global__ void step_patchq_kernel(int n, const int* __restrict__ dof_ptr,
+                                   const int* __restrict__ dof_slot, const int* __restrict__ sbase,
+                                   int np, const int* __restrict__ arr, int* qp) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x)
+    for (int s = dof_ptr[d]; s < dof_ptr[d + 1]; ++s)
+      atomicMax(qp + step_slot_patch(sbase, np, dof_slot[s]), arr[d]);
+}
+__global__ void step_dofq_kernel(int n, const int* __restrict__ dof_ptr,
+                                 const int* __restrict__ dof_slot, const int* __restrict__ sbase,
+                                 int np, const int* __restrict__ pd, int* __restrict__ og) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    int m = 0;
+    for (int s = dof_ptr[d]; s < dof_ptr[d + 1]; ++s)
+      m = max(m, pd[step_slot_patch(sbase, np, dof_slot[s])]);
+    og[d] = m;
+  }
+}
+
+// req[i] -> assigned stage >= req[i], constant over blocks of W (the block's
+// latest stage); appends the runs to out[stage] shifted by `base`
+static void step_runs(const int* req, int m, int W, int S, int base,
+                      std::vector<std::vector<StepRange>>& out, std::vector<int>* assigned,
+                      long long& nruns) {
+  int run_a = 0, run_s = -1;
+  for (int b0 = 0; b0 < m; b0 += W) {
+    const int b1 = std::min(m, b0 + W);
+    int s = 0;
+    for (int i = b0; i < b1; ++i) s = std::max(s, req[i]);
+    s = std::min(std::max(s, 0), S - 1);
+    if (assigned)
+      for (int i = b0; i < b1; ++i) (*assigned)[i] = s;
+    if (s != run_s) {
+      if (run_s >= 0) {
+        out[run_s].push_back({base + run_a, base + b0});
+        ++nruns;
+      }
+      run_a = b0;
+      run_s = s;
+    }
+  }
+  if (run_s >= 0 && m > 0) {
+    out[run_s].push_back({base + run_a, base + m});
+    ++nruns;
+  }
+}
+
+// SM-driven copies over the host link: one launch moves all ranges of a
+// stage between pinned (mapped) host memory and device memory. The DMA
+// engines cost ~7-16 us per range on top of the bytes (tools/smcopy_probe.cu),
+// a stage has ~5 ranges per vector; a few CTAs reach the same link bandwidth.
+constexpr int kStepMaxRanges = 12;
+struct CopyRanges {
+  int n = 0;
+  int a[kStepMaxRanges], b[kStepMaxRanges];
+};
+__global__ void __launch_bounds__(512) step_copy_kernel(const double* __restrict__ src,
+                                                        double* __restrict__ dst, CopyRanges R,
+                                                        unsigned long long* tr) {
+  if (tr && threadIdx.x == 0) {  // diagnostic: first start / last end of the launch
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(tr, t);
+  }
+  const int st = gridDim.x * blockDim.x;
+  for (int q = 0; q < R.n; ++q) {
+    const int b = R.b[q];
+    int i = R.a[q] + blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * st < b; i += 4 * st) {
+      const double v0 = src[i], v1 = src[i + st], v2 = src[i + 2 * st], v3 = src[i + 3 * st];
+      dst[i] = v0;
+      dst[i + st] = v1;
+      dst[i + 2 * st] = v2;
+      dst[i + 3 * st] = v3;
+    }
+    for (; i < b; i += st) dst[i] = src[i];
+  }
+  if (tr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(tr + 1, t);
+    }
+  }
+}
+static void step_copy(Ctx& c, cudaStream_t st, const double* src, double* dst,
+                      const std::vector<StepRange>& rs, int ctas, unsigned long long* tr = nullptr) {
+  for (size_t q0 = 0; q0 < rs.size(); q0 += kStepMaxRanges) {
+    CopyRanges R;
+    for (size_t q = q0; q < rs.size() && R.n < kStepMaxRanges; ++q) {
+      R.a[R.n] = rs[q].a;
+      R.b[R.n] = rs[q].b;
+      ++R.n;
+    }
+    step_copy_kernel<<<ctas, 512, 0, st>>>(src, dst, R, tr);
+    SAG_CUDA(cudaGetLastError());
+    ++c.launches;
+  }
+}
+// device-visible address of pinned host memory (null: not mapped)
+static double* host_mapped(const double* p) {
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, const_cast<double*>(p), 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return static_cast<double*>(d);
+}
+
+static std::shared_ptr<StepPlan> step_plan_build(Ctx& c, const Vanka& f, const Matrix& K, int S) {
+  auto P = std::make_shared<StepPlan>();
+  P->k = &K;
+  P->S = S;
+  P->want_S = S;
+  P->growth = env_int("SAG_STEP_GROWTH", 100);
+  const int n = f.n, n_u = std::min(std::max(f.n_u, 0), n), n_p = n - n_u, np_ = f.npatch;
+  P->in.assign(S, {});
+  P->rows.assign(S, {});
+  P->gat.assign(S, {});
+  P->pat.assign(S, {});
+  const int W = 1024;
+  // arrival stage of every dof
+  std::vector<int> h(n, 0), arr(n, 0);
+  {
+    DevBuf<int> minp(std::max(n_u, 1));
+    if (n_u > 0) {
+      step_minp_kernel<<<grid_for(c, n_u), 256, 0, c.stream>>>(n_u, K.rp.p, K.ci.p, minp.p);
+      SAG_LAUNCHED(c);
+      SAG_CUDA(cudaMemcpyAsync(h.data(), minp.p, sizeof(int) * n_u, cudaMemcpyDeviceToHost, c.stream));
+      SAG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    // stage q takes the pressure dofs up to the fraction cum[q]; SAG_STEP_GROWTH
+    // (percent, default 100 = equal stages) makes each stage that much larger
+    // than the one before, so the first outputs leave early
+    const double g = std::max(1.0, env_int("SAG_STEP_GROWTH", 100) / 100.0);
+    std::vector<double> cum(S);
+    {
+      double tot = 0.0, w = 1.0;
+      for (int q = 0; q < S; ++q, w *= g) tot += w;
+      double acc = 0.0;
+      w = 1.0;
+      for (int q = 0; q < S; ++q, w *= g) {
+        acc += w;
+        cum[q] = acc / tot;
+      }
+    }
+    auto pstage = [&](int col) {
+      if (n_p <= 0) return 0;
+      const double fr = (double)(col - n_u) / n_p;
+      int q = 0;
+      while (q < S - 1 && fr >= cum[q]) ++q;
+      return q;
+    };
+    for (int d = 0; d < n_u; ++d) h[d] = h[d] == 0x7fffffff ? 0 : pstage(h[d]);
+    for (int d = n_u; d < n; ++d) h[d] = pstage(d);
+  }
+  // the velocity and pressure blocks are grouped separately (a block of 1024
+  // never straddles them)
+  step_runs(h.data(), n_u, W, S, 0, P->in, &arr, P->ranges);
+  {
+    std::vector<int> ap(n_p, 0);
+    step_runs(h.data() + n_u, n_p, W, S, n_u, P->in, &ap, P->ranges);
+    std::copy(ap.begin(), ap.end(), arr.begin() + n_u);
+  }
+  DevBuf<int> darr(std::max(n, 1)), dq(std::max(n, 1));
+  SAG_CUDA(cudaMemcpyAsync(darr.p, arr.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c.stream));
+  // rows of y
+  step_rowq_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, K.rp.p, K.ci.p, darr.p, dq.p);
+  SAG_LAUNCHED(c);
+  SAG_CUDA(cudaMemcpyAsync(h.data(), dq.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c.stream));
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  step_runs(h.data(), n_u, W, S, 0, P->rows, nullptr, P->ranges);
+  step_runs(h.data() + n_u, n_p, W, S, n_u, P->rows, nullptr, P->ranges);
+  // patches (blob order, class by class)
+  std::vector<int> sbase(np_ + 1, 0);
+  for (int i = 0; i < np_; ++i) sbase[i + 1] = sbase[i] + f.h_nv[i] + f.h_np[i];
+  DevBuf<int> dsb(np_ + 1), dqp(std::max(np_, 1));
+  SAG_CUDA(cudaMemcpyAsync(dsb.p, sbase.data(), sizeof(int) * (np_ + 1), cudaMemcpyHostToDevice,
+                           c.stream));
+  SAG_CUDA(cudaMemsetAsync(dqp.p, 0, sizeof(int) * std::max(np_, 1), c.stream));
+  std::vector<int> qp(std::max(np_, 1), 0), pd(std::max(np_, 1), 0);
+  if (np_ > 0) {
+    step_patchq_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, f.dof_ptr.p, f.dof_slot.p, dsb.p,
+                                                             np_, darr.p, dqp.p);
+    SAG_LAUNCHED(c);
+    SAG_CUDA(cudaMemcpyAsync(qp.data(), dqp.p, sizeof(int) * np_, cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    SAG_REQUIRE((int)f.h_order.size() == np_, SAG_ERROR, "step plan: blob order missing");
+    for (const auto& cl : f.rclasses) {
+      const int m = cl.k1 - cl.k0;
+      if (m <= 0) continue;
+      std::vector<int> req(m), as(m);
+      for (int q = 0; q < m; ++q) req[q] = qp[f.h_order[cl.k0 + q]];
+      std::vector<std::vector<StepRange>> win(S);
+      step_runs(req.data(), m, 1536, S, cl.k0, win, &as, P->ranges);  // 1536: a multiple of every patches-per-warp count
+      for (int q = 0; q < m; ++q) pd[f.h_order[cl.k0 + q]] = as[q];
+      for (int st = 0; st < S; ++st)
+        for (const auto& r : win[st]) {
+          Vanka::RClass w = cl;
+          w.k0 = r.a;
+          w.k1 = r.b;
+          P->pat[st].push_back(w);
+        }
+    }
+    // dofs of delta
+    SAG_CUDA(cudaMemcpyAsync(dqp.p, pd.data(), sizeof(int) * np_, cudaMemcpyHostToDevice, c.stream));
+    step_dofq_kernel<<<grid_for(c, n), 256, 0, c.stream>>>(n, f.dof_ptr.p, f.dof_slot.p, dsb.p, np_,
+                                                           dqp.p, dq.p);
+    SAG_LAUNCHED(c);
+    SAG_CUDA(cudaMemcpyAsync(h.data(), dq.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c.stream));
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+  } else {
+    std::fill(h.begin(), h.end(), 0);
+  }
+  step_runs(h.data(), n_u, W, S, 0, P->gat, nullptr, P->ranges);
+  step_runs(h.data() + n_u, n_p, W, S, n_u, P->gat, nullptr, P->ranges);
+  // a fragmented numbering (many ranges) gains nothing from the pipeline
+  if (P->ranges > 64LL * S) {
+    P->S = 0;
+    return P;
+  }
+  // copy kernels go first when the block scheduler has a choice
+  int plo = 0, phi = 0;
+  SAG_CUDA(cudaDeviceGetStreamPriorityRange(&plo, &phi));
+  SAG_CUDA(cudaStreamCreateWithPriority(&P->sin, cudaStreamNonBlocking, phi));
+  SAG_CUDA(cudaStreamCreateWithPriority(&P->sout, cudaStreamNonBlocking, phi));
+  SAG_CUDA(cudaStreamCreateWithFlags(&P->ssp, cudaStreamNonBlocking));
+  auto pack = [&](const std::vector<std::vector<StepRange>>& src,
+                  std::vector<std::vector<RowRanges>>& dst) {
+    dst.assign(S, {});
+    for (int q = 0; q < S; ++q) {
+      RowRanges R;
+      for (const auto& r : src[q]) {
+        if (!R.push(r.a, r.b)) {
+          dst[q].push_back(R);
+          R = RowRanges();
+          R.push(r.a, r.b);
+        }
+      }
+      if (R.n) dst[q].push_back(R);
+    }
+  };
+  pack(P->rows, P->rows_rr);
+  pack(P->gat, P->gat_rr);
+  P->ev.assign(4 * (size_t)S + 4, nullptr);
+  for (auto& e : P->ev) SAG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return P;
+}
+
+static bool is_pinned_host(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// the pipelined step; false when it does not apply (caller takes the plain path)
+static bool vanka_spmv_pipelined(Ctx& c, const Vanka& f, const Matrix& K, const double* x,
+                                 double* delta, double* y) {
+  const int S = env_int("SAG_STEP_STAGES", 8);
+  if (S < 2 || S > 64 || f.n == 0 || !f.seq) return false;
+  if (!is_pinned_host(x) || !is_pinned_host(delta) || !is_pinned_host(y)) return false;
+  if (!f.step_plan || f.step_plan->k != &K || f.step_plan->want_S != S ||
+      f.step_plan->growth != env_int("SAG_STEP_GROWTH", 100))
+    f.step_plan = step_plan_build(c, f, K, S);
+  StepPlan& P = *f.step_plan;
+  if (P.S == 0) return false;
+  const int n = f.n;
+  double* dx = c.stage_buf(0, n);
+  double* dd = c.stage_buf(1, n);
+  double* dy = c.stage_buf(2, n);
+  // SAG_STEP_SMCOPY=0: the DMA engines (one cudaMemcpyAsync per range)
+  const int ctas = env_int("SAG_STEP_SMCOPY", 16);
+  const double* mx = ctas > 0 ? host_mapped(x) : nullptr;
+  double* md = ctas > 0 ? host_mapped(delta) : nullptr;
+  double* my = ctas > 0 ? host_mapped(y) : nullptr;
+  const bool sm = mx && md && my;
+  // per direction (diagnostic): SAG_STEP_SMIN / SAG_STEP_SMOUT = 0 keep that direction on DMA
+  const bool sm_in = sm && env_int("SAG_STEP_SMIN", 1) != 0;
+  const bool sm_out = sm && env_int("SAG_STEP_SMOUT", 1) != 0;
+  const bool trace = env_int("SAG_STEP_TRACE", 0) == 1;
+  const bool ktrace = env_int("SAG_STEP_TRACE", 0) == 2;
+  if (ktrace && P.ktrace.n < 6 * (size_t)S) {
+    P.ktrace.alloc(6 * (size_t)S);
+    if (P.exec) cudaGraphExecDestroy(P.exec);
+    P.exec = nullptr;
+  }
+  auto ktr = [&](int kind, int q) { return ktrace ? P.ktrace.p + 2 * ((size_t)kind * S + q) : nullptr; };
+  auto ktrace_reset = [&]() {
+    if (!ktrace) return;
+    std::vector<unsigned long long> h(6 * (size_t)S);
+    for (size_t i = 0; i < h.size(); i += 2) {
+      h[i] = ~0ull;
+      h[i + 1] = 0ull;
+    }
+    SAG_CUDA(cudaMemcpy(P.ktrace.p, h.data(), 8 * h.size(), cudaMemcpyHostToDevice));
+  };
+  auto ktrace_print = [&]() {
+    if (!ktrace) return;
+    std::vector<unsigned long long> h(6 * (size_t)S);
+    SAG_CUDA(cudaMemcpy(h.data(), P.ktrace.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull;
+    for (size_t i = 0; i < h.size(); i += 2) t0 = std::min(t0, h[i]);
+    const char* nm[3] = {"in", "yout", "dout"};
+    for (int k = 0; k < 3; ++k)
+      for (int q = 0; q < S; ++q) {
+        const unsigned long long a = h[2 * ((size_t)k * S + q)], b = h[2 * ((size_t)k * S + q) + 1];
+        if (b) fprintf(stderr, "step-ktrace %s%d %8.1f .. %8.1f us\n", nm[k], q, (a - t0) * 1e-3, (b - t0) * 1e-3);
+      }
+  };
+  ktrace_reset();
+  // SAG_STEP_GRAPH=0: enqueue operation by operation
+  const bool graph = !trace && env_int("SAG_STEP_GRAPH", 1) != 0;
+  const void* key[7] = {x, delta, y, dx, dd, dy,
+                        (const void*)(size_t)((sm ? ctas : 0) + (ktrace ? 1000 : 0) +
+                                              (sm_in ? 2000 : 0) + (sm_out ? 4000 : 0))};
+  if (graph && P.exec && std::memcmp(key, P.gkey, sizeof(key)) == 0) {
+    SAG_CUDA(cudaGraphLaunch(P.exec, c.stream));
+    c.launches += P.graph_launches;
+    SAG_CUDA(cudaStreamSynchronize(c.stream));
+    ktrace_print();
+    return true;
+  }
+  // an error while capturing must not leave the stream in capture mode
+  struct CaptureGuard {
+    cudaStream_t st = nullptr;
+    ~CaptureGuard() {
+      if (st) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+      }
+    }
+  } guard;
+  const long long launches0 = c.launches;
+  if (graph) {
+    if (P.exec) {
+      cudaGraphExecDestroy(P.exec);
+      P.exec = nullptr;
+    }
+    SAG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    guard.st = c.stream;
+  }
+  // the copy streams start after whatever the compute stream holds
+  cudaEvent_t e0 = P.ev[3 * (size_t)S];
+  SAG_CUDA(cudaEventRecord(e0, c.stream));
+  SAG_CUDA(cudaStreamWaitEvent(P.sin, e0, 0));
+  SAG_CUDA(cudaStreamWaitEvent(P.sout, e0, 0));
+  // SAG_STEP_TRACE=1 (diagnostic): timestamps of every stage on the three streams
+  std::vector<cudaEvent_t> te;
+  std::vector<std::string> tn;
+  auto mark = [&](cudaStream_t st, const std::string& name) {
+    if (!trace) return;
+    cudaEvent_t e;
+    SAG_CUDA(cudaEventCreate(&e));
+    SAG_CUDA(cudaEventRecord(e, st));
+    te.push_back(e);
+    tn.push_back(name);
+  };
+  mark(c.stream, "start");
+  for (int q = 0; q < S; ++q) {
+    if (sm_in) {
+      step_copy(c, P.sin, mx, dx, P.in[q], ctas, ktr(0, q));
+    } else {
+      for (const auto& r : P.in[q])
+        SAG_CUDA(cudaMemcpyAsync(dx + r.a, x + r.a, sizeof(double) * (r.b - r.a),
+                                 cudaMemcpyHostToDevice, P.sin));
+    }
+    SAG_CUDA(cudaEventRecord(P.ev[q], P.sin));
+    mark(P.sin, "in" + std::to_string(q));
+  }
+  // SpMV on its own stream (independent of the Vanka chain on c.stream)
+  SAG_CUDA(cudaStreamWaitEvent(P.ssp, e0, 0));
+  for (int q = 0; q < S; ++q) {
+    SAG_CUDA(cudaStreamWaitEvent(P.ssp, P.ev[q], 0));
+    for (const auto& R : P.rows_rr[q]) launch_spmv_ranges(c, K, R, dx, dy, P.ssp);
+    mark(P.ssp, "spmv" + std::to_string(q));
+    if (!P.rows[q].empty()) {
+      SAG_CUDA(cudaEventRecord(P.ev[S + q], P.ssp));
+      SAG_CUDA(cudaStreamWaitEvent(P.sout, P.ev[S + q], 0));
+      if (sm_out) {
+        step_copy(c, P.sout, dy, my, P.rows[q], ctas, ktr(1, q));
+      } else {
+        for (const auto& r : P.rows[q])
+          SAG_CUDA(cudaMemcpyAsync(y + r.a, dy + r.a, sizeof(double) * (r.b - r.a),
+                                   cudaMemcpyDeviceToHost, P.sout));
+      }
+      mark(P.sout, "yout" + std::to_string(q));
+    }
+    SAG_CUDA(cudaStreamWaitEvent(c.stream, P.ev[q], 0));
+    if (!P.pat[q].empty()) launch_patch_any(c, f, dx, nullptr, &P.pat[q]);
+    mark(c.stream, "patch" + std::to_string(q));
+    for (const auto& R : P.gat_rr[q]) {
+      vanka_gather_ranges_kernel<<<grid_for(c, R.total()), 256, 0, c.stream>>>(
+          R, f.dof_ptr.p, f.out.p, f.w_ext ? f.w.p : nullptr, dd);
+      SAG_LAUNCHED(c);
+    }
+    mark(c.stream, "gather" + std::to_string(q));
+    if (!P.gat[q].empty()) {
+      SAG_CUDA(cudaEventRecord(P.ev[2 * S + q], c.stream));
+      SAG_CUDA(cudaStreamWaitEvent(P.sout, P.ev[2 * S + q], 0));
+      if (sm_out) {
+        step_copy(c, P.sout, dd, md, P.gat[q], ctas, ktr(2, q));
+      } else {
+        for (const auto& r : P.gat[q])
+          SAG_CUDA(cudaMemcpyAsync(delta + r.a, dd + r.a, sizeof(double) * (r.b - r.a),
+                                   cudaMemcpyDeviceToHost, P.sout));
+      }
+      mark(P.sout, "dout" + std::to_string(q));
+    }
+  }
+  // join the side streams into the compute stream
+  SAG_CUDA(cudaEventRecord(P.ev[3 * (size_t)S + 1], P.sin));
+  SAG_CUDA(cudaStreamWaitEvent(c.stream, P.ev[3 * (size_t)S + 1], 0));
+  SAG_CUDA(cudaEventRecord(P.ev[3 * (size_t)S + 2], P.sout));
+  SAG_CUDA(cudaStreamWaitEvent(c.stream, P.ev[3 * (size_t)S + 2], 0));
+  SAG_CUDA(cudaEventRecord(P.ev[3 * (size_t)S + 3], P.ssp));
+  SAG_CUDA(cudaStreamWaitEvent(c.stream, P.ev[3 * (size_t)S + 3], 0));
+  if (graph) {
+    cudaGraph_t g = nullptr;
+    guard.st = nullptr;
+    SAG_CUDA(cudaStreamEndCapture(c.stream, &g));
+    P.graph_launches = c.launches - launches0;
+    cudaError_t e = cudaGraphInstantiate(&P.exec, g, 0);
+    cudaGraphDestroy(g);
+    SAG_CUDA(e);
+    std::memcpy(P.gkey, key, sizeof(key));
+    SAG_CUDA(cudaGraphLaunch(P.exec, c.stream));
+  }
+  SAG_CUDA(cudaStreamSynchronize(c.stream));
+  if (trace) {
+    for (size_t i = 1; i < te.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, te[0], te[i]);
+      fprintf(stderr, "step-trace %-10s %8.1f us\n", tn[i].c_str(), 1e3 * ms);
+    }
+    for (auto e : te) cudaEventDestroy(e);
+  }
+  return true;
+}
+
+// vanka_gather_seq_kernel on a few dof ranges in one launch
+__global__ void vanka_gather_ranges_kernel(RowRanges R, const int* __restrict__ dof_ptr,
+                                           const double* __restrict__ out,
+                                           const double* __restrict__ w, double* __restrict__ delta) {
+  constexpr int U = 8;
+  const int total = R.total();
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < total; v += gridDim.x * blockDim.x) {
+    const int d = R.row(v);
+    const int s0 = __ldg(dof_ptr + d), s1 = __ldg(dof_ptr + d + 1);
+    const double wd = w ? __ldg(w + d) : (s1 > s0 ? 1.0 / (double)(s1 - s0) : 0.0);
+    double acc = 0.0;
+    for (int sb = s0; sb < s1; sb += U) {
+      double vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) vv[u] = sb + u < s1 ? __ldcs(out + sb + u) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (sb + u < s1) acc = __dadd_rn(acc, __dmul_rn(wd, vv[u]));
+    }
+    delta[d] = acc;
+  }
+}
+
 void vanka_apply_stationary(Ctx& c, const Vanka& f, const double* r, double* x, double omega) {
   launch_patch_any(c, f, r, nullptr);
   launch_gather(c, f, nullptr, x, omega, nullptr);
@@ -2606,6 +3156,7 @@ int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const 
     const int n = f->f.n;
     SAG_REQUIRE(k->m.nrows == n && k->m.ncols == n, SAG_DIMENSION_MISMATCH,
                 "sag_vanka_spmv: operator and factorization sizes differ");
+    if (vanka_spmv_pipelined(c, f->f, k->m, x, delta, y)) return;
     InVec xi(c, x, n, 0);                 // x crosses the host link once
     OutVec yo(c, y, n, 2, false);
     OutVec d(c, delta, n, 1, false);
@@ -2639,6 +3190,26 @@ int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const 
     }
     SAG_CUDA(cudaStreamSynchronize(cs));
     SAG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sag_vanka_step_plan(const sag_vanka* f, long long* out, int cap) {
+  return guard([&] {
+    SAG_NOTNULL(f);
+    SAG_NOTNULL(out);
+    long long v[6] = {0, 0, 0, 0, 0, 0};
+    if (f->f.step_plan) {
+      const StepPlan& P = *f->f.step_plan;
+      v[0] = P.S;
+      v[1] = P.ranges;
+      for (int q = 0; q < P.S; ++q) {
+        v[2] += (long long)P.in[q].size();
+        v[3] += (long long)P.rows[q].size();
+        v[4] += (long long)P.gat[q].size();
+        v[5] += (long long)P.pat[q].size();
+      }
+    }
+    for (int i = 0; i < cap && i < 6; ++i) out[i] = v[i];
   });
 }
 

@@ -114,12 +114,14 @@ def test_apply_vanka_parity(S, n):
 def test_vanka_spmv_step(S, monkeypatch, mode, sv, stages):
     """sag_vanka_spmv equals spmv + apply_vanka of the reference with device
     buffers (x read once), pageable host buffers (staged, y copied back under
-    the sweep) and pinned host buffers -- the pipelined step: copy-in, patch
-    solves and host writes in stages -- bitwise the unpipelined results, for
-    any stage count, one-class (TH) and multi-class (SV: sub-warp) levels."""
+    the sweep) and pinned host buffers -- the pipelined step: x arrives in
+    stages, row ranges of y, patch windows and dof ranges of delta run and
+    leave as their inputs arrive -- bitwise the unpipelined results, for any
+    stage count, one-class (TH) and multi-class (SV: fixed-shape + sub-warp +
+    32-lane) levels."""
     import torch
     if stages:
-        monkeypatch.setenv("SAG_STREAMED_STAGES", str(stages))
+        monkeypatch.setenv("SAG_STEP_STAGES", str(stages))
     if sv:
         c = O.RefCase.build("cavity", True, "structured", 64)  # sub-warp classes
         k0 = c.k0().csr()
@@ -141,8 +143,17 @@ def test_vanka_spmv_step(S, monkeypatch, mode, sv, stages):
         xh = torch.from_numpy(x).pin_memory().numpy()
         dh = torch.empty(k0.nrows, dtype=torch.float64).pin_memory().numpy()
         yh = torch.empty(k0.nrows, dtype=torch.float64).pin_memory().numpy()
+        dh[:] = np.nan
+        yh[:] = np.nan
         dl, y = S.vanka_spmv_step(f, K, xh, dh, yh)
         assert dl is dh and y is yh
+        plan = S.vanka_step_plan(f)
+        want = stages if stages else 8
+        assert plan["stages"] == (want if want >= 2 else 0), plan
+        if want >= 2:  # a strip-ordered numbering: a handful of ranges per stage
+            assert 0 < plan["ranges"] <= 64 * want and plan["patch_windows"] >= 1, plan
+            dl2, y2 = S.vanka_spmv_step(f, K, xh, dh, yh)  # the cached plan again
+            assert np.array_equal(dl2, dl) and np.array_equal(y2, y)
     assert rel_inf(y, O.RefMat.from_csr(k0).spmv(x)) <= TOL
     assert rel_inf(dl, rv.apply(x)) <= TOL
     assert np.array_equal(dl, S.apply_vanka(f, x)) and np.array_equal(y, S.spmv(K, x))
