@@ -505,7 +505,7 @@ int sag_plan_array(const sag_plan* plan, int which, int peer, void* out, long lo
 
 /* ---- partitioned-solve primitives ---------------------------
  * Building blocks for a caller that row-partitions the solve across ranks
- * (one process per GPU, paper_2306_06795_b200/dist.py). All pointers are
+ * (one process per GPU, paper_2306_06795_b200/dsolve.py). All pointers are
  * DEVICE pointers and no call synchronises with the host: scalars stay in
  * device memory, so a partial reduction, the caller's all-reduce (NCCL on
  * the same stream) and the axpy that consumes it are stream-ordered.

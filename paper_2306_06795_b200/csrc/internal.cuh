@@ -410,4 +410,5 @@ struct sag_patches {
 };
 struct sag_vanka {
   sag::Vanka f;
+  sag::Ctx* c = nullptr;  // the context whose stream the factorization's kernels run on
 };

@@ -3036,13 +3036,16 @@ int sag_factor_patches(sag_ctx* ctx, const sag_matrix* k, const sag_patches* p, 
     auto f = factor_patches_dev(ctx->c, k->m, p->p, n_u);
     auto* h = new sag_vanka;
     h->f = std::move(*f);
+    h->c = &ctx->c;
     *out = h;
   });
 }
 
 int sag_vanka_destroy(sag_vanka* f) {
   return guard([&] {
-    if (f) cudaDeviceSynchronize();
+    // only this context's stream can still hold work on the factorization
+    // (plus the pipelined step's side streams, joined into it at every call)
+    if (f && f->c) cudaStreamSynchronize(f->c->stream);
     delete f;
   });
 }

@@ -12,6 +12,10 @@ timeout 900 python bench.py --config 3 --steps 20 --warmup 5 --no-cpu > gpurun_o
 timeout 900 python bench.py --config 4 --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
 timeout 900 python bench.py --dist --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_dist1.json 2> gpurun_out/bench_dist1.err
 [ -n "$NO_NCU" ] && exit 0
+# launch list of the bench command (cold-cache, serialised: shares, not absolutes)
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu --no-setup --no-solve > gpurun_out/launches_bench.log 2>&1
+python tools/launch_summary.py gpurun_out/launches.csv > gpurun_out/launches_summary.txt 2>&1
+gzip -f gpurun_out/launches.csv
 for spec in "2 K0" "3 K0" "3 ISO0" "2 ISO0"; do set -- $spec
  rep=gpurun_out/prof_c$1_$2
  timeout 900 ncu --set full --import-source on --clock-control none -k regex:"spmv_kernel|vanka_patch_kernel|vanka_subwarp_kernel|vanka_fixed_kernel|vanka_gather" -o $rep python tools/prof_once.py --config $1 --level $2 > $rep.log 2>&1

@@ -31,6 +31,22 @@ KEYS = [
     ("smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio", "stall lg_throttle / issue"),
     ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math_pipe / issue"),
     ("smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio", "stall sleeping / issue"),
+    # where the L2 traffic and its DRAM fills come from
+    ("lts__t_sectors_op_read.sum", "L2 sectors read"),
+    ("lts__t_sectors_op_write.sum", "L2 sectors written"),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "L2 sectors read by SMs"),
+    ("lts__t_sectors_srcunit_tex_op_write.sum", "L2 sectors written by SMs"),
+    ("lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum", "L2 read misses (SM reads)"),
+    ("lts__t_sectors_srcunit_tex_op_write_lookup_miss.sum", "L2 write misses (SM writes)"),
+    ("lts__t_sectors_srcunit_tex_lookup_miss.sum", "L2 misses (SM)"),
+    ("lts__t_sectors_srcnode_gpc_op_read_lookup_miss.sum", "L2 read misses (GPC)"),
+    ("lts__t_sectors_srcunit_ltcfabric.sum", "L2 sectors over the die fabric"),
+    ("dram__sectors_read.sum", "dram sectors read"),
+    ("dram__sectors_write.sum", "dram sectors written"),
+    ("l1tex__m_xbar2l1tex_read_sectors.sum", "L2 -> L1 sectors"),
+    ("smsp__inst_executed_op_shared_ld.sum", "shared loads"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared wavefronts"),
+    ("sm__inst_issued.avg.pct_of_peak_sustained_active", "issue slots %"),
 ]
 
 
