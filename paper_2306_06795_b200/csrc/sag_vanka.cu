@@ -1394,7 +1394,11 @@ __global__ void __launch_bounds__(256, MINB) vanka_fixed_kernel(
     const int* gate) {
   if (gate && *gate) return;
   constexpr int L = M + NP, P = 32 / L, NV2 = 2 * M;
-  constexpr int NBS = (2 * M + NP + 1) & ~1;  // per-patch b stride (16-byte aligned)
+  // per-patch b stride: 16-byte aligned, and two doubles past a multiple of
+  // 128 bytes so the patches of a group (which read the same entry of their own
+  // b in one instruction) sit on different shared-memory banks: 111.7 -> 100.9 us
+  // on the config-3 K0 sweep
+  constexpr int NBS = (((2 * M + NP + 1) & ~1) + 15) / 16 * 16 + 2;
   constexpr int A2 = M * (M + 1) / 2;          // A pairs
   constexpr int W2 = M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : 16;  // reduction width
   static_assert(W2 <= L, "the w_e tree must stay inside the patch's lanes");
@@ -1766,7 +1770,7 @@ template <int M, int NP>
 static void launch_fixed(Ctx& c, const Vanka& f, const Vanka::RClass& cl, const double* r,
                          const int* gate) {
   static thread_local int configured[2] = {0, 0};
-  constexpr int L = M + NP, P = 32 / L, NB = ((2 * M + NP) + 1) & ~1;
+  constexpr int L = M + NP, P = 32 / L, NB = ((((2 * M + NP) + 1) & ~1) + 15) / 16 * 16 + 2;
   const int npatch = cl.k1 - cl.k0;
   const int bytes = (int)cl.slot_bytes;  // the largest blob of the class
   const int nstage = std::max(2, env_int("SAG_VANKA_STAGES", 2));
