@@ -161,9 +161,11 @@ int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const 
 /* Diagnostic (no reference counterpart): the plan of the last pipelined
  * host-buffer step of f (sag_vanka_spmv with pinned host x, delta, y: x
  * arrives in stages and every output range leaves as soon as its inputs
- * arrived). out = [stages (0: not pipelined), ranges, host->device ranges,
- * SpMV row ranges, gather ranges, patch windows]. SAG_STEP_STAGES sets the
- * stage count (default 8; 1 disables the pipeline). */
+ * arrived). out = [stages (0: no plan), ranges, host->device ranges, SpMV row
+ * ranges, gather ranges, patch windows, choice (1 pipelined, -1 plain, 0 not
+ * yet timed), ns per plain step, ns per pipelined step]. By default the first
+ * call on a plan times both forms of the step and keeps the faster one;
+ * SAG_STEP_STAGES=S forces the pipeline with S stages (1: never). */
 int sag_vanka_step_plan(const sag_vanka* f, long long* out, int cap);
 
 /* One stage of sag_apply_vanka, for per-kernel timing (device pointers):

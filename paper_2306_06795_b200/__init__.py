@@ -670,10 +670,12 @@ def apply_vanka(f: VankaFactorization, r, out=None):
 
 def vanka_step_plan(f: VankaFactorization):
     """Plan of the last pipelined host-buffer step of f (sag_vanka_step_plan)."""
-    v = np.zeros(6, dtype=np.int64)
-    _check(lib().sag_vanka_step_plan(f.h, v.ctypes.data_as(i64p), 6))
+    v = np.zeros(9, dtype=np.int64)
+    _check(lib().sag_vanka_step_plan(f.h, v.ctypes.data_as(i64p), 9))
     return dict(stages=int(v[0]), ranges=int(v[1]), in_ranges=int(v[2]), row_ranges=int(v[3]),
-                gather_ranges=int(v[4]), patch_windows=int(v[5]))
+                gather_ranges=int(v[4]), patch_windows=int(v[5]),
+                choice={1: "pipelined", -1: "plain", 0: "untimed"}[int(v[6])],
+                plain_ms=v[7] * 1e-6, pipelined_ms=v[8] * 1e-6)
 
 
 def vanka_spmv_step(f: VankaFactorization, k: SparseMatrix, x, delta=None, y=None):

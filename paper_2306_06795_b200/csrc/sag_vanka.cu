@@ -7,6 +7,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -1911,6 +1912,8 @@ struct StepRange {
 struct StepPlan {
   const Matrix* k = nullptr;
   int S = 0, want_S = 0, growth = 0;
+  int choice = 0;                 // 0 untimed, 1 pipelined, -1 plain (sag_vanka_spmv)
+  double t_plain = 0.0, t_pipe = 0.0;  // seconds per step measured at the first call
   std::vector<std::vector<StepRange>> in, rows, gat;  // per stage
   std::vector<std::vector<Vanka::RClass>> pat;         // per stage: class windows
   std::vector<cudaEvent_t> ev;                         // 3 S events
@@ -2221,17 +2224,26 @@ static bool is_pinned_host(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-// the pipelined step; false when it does not apply (caller takes the plain path)
-static bool vanka_spmv_pipelined(Ctx& c, const Vanka& f, const Matrix& K, const double* x,
-                                 double* delta, double* y) {
+// the plan of the pipelined step for these buffers; null when it does not
+// apply (pageable or device buffers, one stage, a fragmented numbering).
+// choice: 0 = not yet timed against the plain step, 1 = pipelined, -1 = plain
+// (an explicit SAG_STEP_STAGES forces the pipeline whatever the choice).
+static StepPlan* vanka_step_prepare(Ctx& c, const Vanka& f, const Matrix& K, const double* x,
+                                    double* delta, double* y) {
   const int S = env_int("SAG_STEP_STAGES", 8);
-  if (S < 2 || S > 64 || f.n == 0 || !f.seq) return false;
-  if (!is_pinned_host(x) || !is_pinned_host(delta) || !is_pinned_host(y)) return false;
+  if (S < 2 || S > 64 || f.n == 0 || !f.seq) return nullptr;
+  if (!is_pinned_host(x) || !is_pinned_host(delta) || !is_pinned_host(y)) return nullptr;
   if (!f.step_plan || f.step_plan->k != &K || f.step_plan->want_S != S ||
       f.step_plan->growth != env_int("SAG_STEP_GROWTH", 100))
     f.step_plan = step_plan_build(c, f, K, S);
   StepPlan& P = *f.step_plan;
-  if (P.S == 0) return false;
+  if (P.S == 0) return nullptr;
+  return &P;
+}
+
+static void vanka_spmv_pipelined(Ctx& c, const Vanka& f, const Matrix& K, StepPlan& P,
+                                 const double* x, double* delta, double* y) {
+  const int S = P.S;
   const int n = f.n;
   double* dx = c.stage_buf(0, n);
   double* dd = c.stage_buf(1, n);
@@ -2286,7 +2298,7 @@ static bool vanka_spmv_pipelined(Ctx& c, const Vanka& f, const Matrix& K, const 
     c.launches += P.graph_launches;
     SAG_CUDA(cudaStreamSynchronize(c.stream));
     ktrace_print();
-    return true;
+    return;
   }
   // an error while capturing must not leave the stream in capture mode
   struct CaptureGuard {
@@ -2404,7 +2416,7 @@ static bool vanka_spmv_pipelined(Ctx& c, const Vanka& f, const Matrix& K, const 
     }
     for (auto e : te) cudaEventDestroy(e);
   }
-  return true;
+  return;
 }
 
 // vanka_gather_seq_kernel on a few dof ranges in one launch
@@ -3153,17 +3165,14 @@ int sag_apply_vanka_add_push(sag_ctx* ctx, const sag_vanka* f, const double* r, 
   });
 }
 
-int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const double* x,
-                   double* delta, double* y) {
-  return guard([&] {
-    SAG_NOTNULL(ctx);
-    SAG_NOTNULL(f);
-    SAG_NOTNULL(k);
-    auto& c = ctx->c;
-    const int n = f->f.n;
-    SAG_REQUIRE(k->m.nrows == n && k->m.ncols == n, SAG_DIMENSION_MISMATCH,
-                "sag_vanka_spmv: operator and factorization sizes differ");
-    if (vanka_spmv_pipelined(c, f->f, k->m, x, delta, y)) return;
+}  // extern "C"
+
+// the step with x copied in first: device buffers in place; host outputs leave
+// in chunks as they are computed
+static void vanka_spmv_plain(Ctx& c, const sag_vanka* f, const sag_matrix* k, const double* x,
+                             double* delta, double* y) {
+  const int n = f->f.n;
+  {
     InVec xi(c, x, n, 0);                 // x crosses the host link once
     OutVec yo(c, y, n, 2, false);
     OutVec d(c, delta, n, 1, false);
@@ -3197,6 +3206,52 @@ int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const 
     }
     SAG_CUDA(cudaStreamSynchronize(cs));
     SAG_CUDA(cudaStreamSynchronize(c.stream));
+  }
+}
+
+extern "C" {
+
+int sag_vanka_spmv(sag_ctx* ctx, const sag_vanka* f, const sag_matrix* k, const double* x,
+                   double* delta, double* y) {
+  return guard([&] {
+    SAG_NOTNULL(ctx);
+    SAG_NOTNULL(f);
+    SAG_NOTNULL(k);
+    auto& c = ctx->c;
+    const int n = f->f.n;
+    SAG_REQUIRE(k->m.nrows == n && k->m.ncols == n, SAG_DIMENSION_MISMATCH,
+                "sag_vanka_spmv: operator and factorization sizes differ");
+    // pinned host buffers: the staged pipeline when it applies. Unless
+    // SAG_STEP_STAGES forces it, the first call on a plan times both forms
+    // (each run is the whole step: same results) and keeps the faster one --
+    // the gain depends on the operator and on the host link of the machine.
+    StepPlan* P = vanka_step_prepare(c, f->f, k->m, x, delta, y);
+    const char* forced = getenv("SAG_STEP_STAGES");
+    if (P && forced && *forced) {
+      vanka_spmv_pipelined(c, f->f, k->m, *P, x, delta, y);
+      return;
+    }
+    if (P && P->choice == 0) {
+      auto timed = [&](auto&& run) {
+        double best = 1e30;
+        for (int r = 0; r < 3; ++r) {
+          const auto t0 = std::chrono::steady_clock::now();
+          run();
+          const double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          if (r > 0) best = std::min(best, t);  // the first run warms up (graph capture)
+        }
+        return best;
+      };
+      P->t_plain = timed([&] { vanka_spmv_plain(c, f, k, x, delta, y); });
+      P->t_pipe = timed([&] { vanka_spmv_pipelined(c, f->f, k->m, *P, x, delta, y); });
+      P->choice = P->t_pipe < 0.98 * P->t_plain ? 1 : -1;
+      return;
+    }
+    if (P && P->choice > 0) {
+      vanka_spmv_pipelined(c, f->f, k->m, *P, x, delta, y);
+      return;
+    }
+    vanka_spmv_plain(c, f, k, x, delta, y);
   });
 }
 
@@ -3204,11 +3259,14 @@ int sag_vanka_step_plan(const sag_vanka* f, long long* out, int cap) {
   return guard([&] {
     SAG_NOTNULL(f);
     SAG_NOTNULL(out);
-    long long v[6] = {0, 0, 0, 0, 0, 0};
+    long long v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     if (f->f.step_plan) {
       const StepPlan& P = *f->f.step_plan;
       v[0] = P.S;
       v[1] = P.ranges;
+      v[6] = P.choice;
+      v[7] = (long long)(1e9 * P.t_plain);
+      v[8] = (long long)(1e9 * P.t_pipe);
       for (int q = 0; q < P.S; ++q) {
         v[2] += (long long)P.in[q].size();
         v[3] += (long long)P.rows[q].size();
@@ -3216,7 +3274,7 @@ int sag_vanka_step_plan(const sag_vanka* f, long long* out, int cap) {
         v[5] += (long long)P.pat[q].size();
       }
     }
-    for (int i = 0; i < cap && i < 6; ++i) out[i] = v[i];
+    for (int i = 0; i < cap && i < 9; ++i) out[i] = v[i];
   });
 }
 
