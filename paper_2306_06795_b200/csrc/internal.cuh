@@ -2,6 +2,7 @@
 // the Krylov solvers, and the host-side launchers shared by the .cu files.
 #pragma once
 
+#include <atomic>
 #include <memory>
 
 #include "common.cuh"
@@ -12,8 +13,17 @@ struct sag_ctx {
 
 namespace sag {
 
+// process-wide serial number of a device matrix: plans cached against an
+// operator (the pipelined step) compare it, not the address, so a matrix
+// created later at the same address is never mistaken for the planned one
+inline unsigned long long next_matrix_uid() {
+  static std::atomic<unsigned long long> n{0};
+  return ++n;
+}
+
 // CSR on device (sparse.hpp:11-28). `group` = lanes per row used by SpMV.
 struct Matrix {
+  unsigned long long uid = next_matrix_uid();
   Ctx* ctx = nullptr;
   int nrows = 0, ncols = 0;
   long long nnz = 0;

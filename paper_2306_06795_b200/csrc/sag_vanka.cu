@@ -1911,6 +1911,7 @@ struct StepRange {
 };
 struct StepPlan {
   const Matrix* k = nullptr;
+  unsigned long long k_uid = 0;
   int S = 0, want_S = 0, growth = 0;
   int choice = 0;                 // 0 untimed, 1 pipelined, -1 plain (sag_vanka_spmv)
   double t_plain = 0.0, t_pipe = 0.0;  // seconds per step measured at the first call
@@ -2077,6 +2078,7 @@ static double* host_mapped(const double* p) {
 static std::shared_ptr<StepPlan> step_plan_build(Ctx& c, const Vanka& f, const Matrix& K, int S) {
   auto P = std::make_shared<StepPlan>();
   P->k = &K;
+  P->k_uid = K.uid;
   P->S = S;
   P->want_S = S;
   P->growth = env_int("SAG_STEP_GROWTH", 100);
@@ -2233,7 +2235,8 @@ static StepPlan* vanka_step_prepare(Ctx& c, const Vanka& f, const Matrix& K, con
   const int S = env_int("SAG_STEP_STAGES", 8);
   if (S < 2 || S > 64 || f.n == 0 || !f.seq) return nullptr;
   if (!is_pinned_host(x) || !is_pinned_host(delta) || !is_pinned_host(y)) return nullptr;
-  if (!f.step_plan || f.step_plan->k != &K || f.step_plan->want_S != S ||
+  if (!f.step_plan || f.step_plan->k != &K || f.step_plan->k_uid != K.uid ||
+      f.step_plan->want_S != S ||
       f.step_plan->growth != env_int("SAG_STEP_GROWTH", 100))
     f.step_plan = step_plan_build(c, f, K, S);
   StepPlan& P = *f.step_plan;
